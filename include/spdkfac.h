@@ -1,0 +1,150 @@
+/*
+ * spdkfac.h -- C ABI of the B200-native SPD-KFAC optimizer-step library
+ * (libspdkfac.so, sm_100a).  Drop-in boundary for the reference package
+ * `kfacsched` (pkg/src/kfacsched), whose public operator API is re-exported at
+ * pkg/src/kfacsched/__init__.py:5-69.  Each entry point below names the
+ * reference function it replaces (file:line relative to /root/reference).
+ *
+ * Conventions
+ *  - All tensor pointers are caller-owned DEVICE memory; `stream` is a
+ *    cudaStream_t passed as void*.  Calls are stream-ordered and never
+ *    synchronise the host, except spdkfac_*_info readers that say so.
+ *  - No allocation inside calls: every call that needs scratch takes a
+ *    caller-provided device workspace whose size the matching
+ *    *_workspace_size() returns.  The workspace must stay alive until the
+ *    stream work of the call (or of the plan) completes.
+ *  - Arithmetic: fp32 storage; contractions on tcgen05 tensor cores with
+ *    split-precision operands (3 x bf16 for factors and preconditioning,
+ *    3 x tf32 for inverse updates), fp32 accumulation in TMEM.
+ *  - Packed symmetric layout = the reference's: row-major upper triangle
+ *    including the diagonal, element (i<=j) at i*(2d-i+1)/2 + (j-i)
+ *    (pack_upper, linalg.py:181-184).
+ *  - Return codes mirror the reference's exceptions.
+ */
+#ifndef SPDKFAC_H_
+#define SPDKFAC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SPDKFAC_API __attribute__((visibility("default")))
+#else
+#define SPDKFAC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPDKFAC_OK 0
+#define SPDKFAC_ERR_NOT_PD 1   /* NotPositiveDefiniteError(pivot), linalg.py:37-46,141-145 */
+#define SPDKFAC_ERR_SHAPE 2    /* ValueError on shape mismatch, linalg.py:108-112,161-166 */
+#define SPDKFAC_ERR_ARG 3      /* ValueError on bad argument (gamma<0, empty batch), linalg.py:138-139 */
+#define SPDKFAC_ERR_CUDA 4
+#define SPDKFAC_ERR_NCCL 5
+#define SPDKFAC_ERR_UNSUPPORTED 6 /* not an sm_100 device */
+
+/* Human-readable description of the last error on this thread. */
+SPDKFAC_API const char* spdkfac_last_error(void);
+SPDKFAC_API int spdkfac_version(void);
+/* 1 iff the current device is sm_100 (B200) and the kernels can launch. */
+SPDKFAC_API int spdkfac_device_supported(void);
+
+/* ------------------------------------------------------------------ factors
+ * Replaces compute_factor_A / compute_factor_G / _factor_from_batch
+ * (linalg.py:106-127) and the running-average/aggregation prologue of
+ * _mean_sym (emulator.py:199-200).  Computes, into the packed buffer:
+ *
+ *   packed <- world_scale * ( decay * packed + (1 - decay) * scale * X^T X )
+ *
+ * (decay == 0 never reads `packed`).  The reference's factor is scale = 1/rows,
+ * decay = 0, world_scale = 1; world_scale = 1/P pre-scales a rank's share of
+ * an all-reduce(sum) mean.  X is described by a layout:
+ *   SPDKFAC_ROWS     x = [rows][d] row-major (ld = row stride)     linear layer input / output grad
+ *   SPDKFAC_CONV_A   x = NCHW activation; rows = im2col patches (c,kh,kw order) per output position
+ *   SPDKFAC_SPATIAL  x = NCHW output gradient; rows = (b,h,w) positions, d = C
+ * A plan binds the shapes once and owns the split-precision staging buffers
+ * and tile tables inside the workspace; run() takes the per-step pointers.
+ */
+#define SPDKFAC_ROWS 0
+#define SPDKFAC_CONV_A 1
+#define SPDKFAC_SPATIAL 2
+
+typedef struct spdkfac_factor_geom {
+  int32_t layout;       /* SPDKFAC_ROWS / CONV_A / SPATIAL */
+  int64_t n, c, h, w;   /* ROWS: n = rows, c = d, ld = w (row stride, >= d); h unused */
+  int32_t kh, kw, stride_h, stride_w, pad_h, pad_w, dil_h, dil_w; /* CONV_A only */
+} spdkfac_factor_geom;
+
+typedef struct spdkfac_factor_plan spdkfac_factor_plan;
+
+/* rows and dim of the factor this geometry produces */
+SPDKFAC_API int spdkfac_factor_dims(const spdkfac_factor_geom* g, int64_t* rows, int64_t* dim);
+SPDKFAC_API size_t spdkfac_factor_workspace_size(const spdkfac_factor_geom* g);
+SPDKFAC_API int spdkfac_factor_plan_create(spdkfac_factor_plan** out, const spdkfac_factor_geom* g, void* ws, size_t ws_bytes,
+                               void* stream);
+SPDKFAC_API int spdkfac_factor_plan_run(spdkfac_factor_plan* p, const float* x, float scale, float decay, float world_scale,
+                            float* packed_inout, void* stream);
+SPDKFAC_API void spdkfac_factor_plan_destroy(spdkfac_factor_plan* p);
+
+/* ------------------------------------------------------------------ packing
+ * pack_upper / unpack_upper (linalg.py:181-199) on device. `ld` = row stride
+ * of the full matrix.  unpack writes both triangles. */
+SPDKFAC_API int spdkfac_pack_upper_f32(const float* full, int64_t d, int64_t ld, float* packed, void* stream);
+SPDKFAC_API int spdkfac_unpack_upper_f32(const float* packed, int64_t d, float* full, int64_t ld, void* stream);
+/* Batched over n matrices (host arrays of device pointers). */
+SPDKFAC_API int spdkfac_pack_upper_batched_f32(int n, const int32_t* dims, const float* const* full, float* const* packed,
+                                   void* stream);
+SPDKFAC_API int spdkfac_unpack_upper_batched_f32(int n, const int32_t* dims, const float* const* packed, float* const* full,
+                                     void* stream);
+
+/* ------------------------------------------------------------------ damped inverse
+ * Replaces damped_inverse (linalg.py:130-149) for a batch of n factors:
+ *   out_t = (unpack(packed_t) + gamma I)^-1, symmetrised, full d_t x d_t (ld = d_t)
+ * Blocked Gauss-Jordan sweep (pivot blocks of 128 inverted in shared memory,
+ * trailing updates as 3 x tf32 tcgen05 rank-128 updates).  info_dev[t] = 0 or
+ * LAPACK-style failing pivot + 1 (the reference raises
+ * NotPositiveDefiniteError(info-1)).  The plan binds dims and the in/out
+ * pointers (host arrays of device pointers, copied at create). */
+typedef struct spdkfac_inverse_plan spdkfac_inverse_plan;
+SPDKFAC_API size_t spdkfac_inverse_workspace_size(int n, const int32_t* dims);
+SPDKFAC_API int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t* dims, const float* const* packed_in,
+                                float* const* out_full, int32_t* info_dev, void* ws, size_t ws_bytes, void* stream);
+SPDKFAC_API int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream);
+SPDKFAC_API void spdkfac_inverse_plan_destroy(spdkfac_inverse_plan* p);
+
+/* ------------------------------------------------------------------ precondition + update
+ * Replaces precondition (linalg.py:152-167) and _apply_update
+ * (emulator.py:203-208) for n layers:
+ *   P_l = G_l^-1 . grad_l . A_l^-1      ([d_out][d_in] row-major)
+ *   W_l <- W_l - alpha * P_l            (skipped when weight == NULL)
+ *   precond_out_l <- P_l                (skipped when precond_out == NULL)
+ * Two tcgen05 3 x bf16 GEMMs per layer, batched over layers. */
+typedef struct spdkfac_precond_plan spdkfac_precond_plan;
+SPDKFAC_API size_t spdkfac_precond_workspace_size(int n, const int32_t* d_out, const int32_t* d_in);
+SPDKFAC_API int spdkfac_precond_plan_create(spdkfac_precond_plan** out, int n, const int32_t* d_out, const int32_t* d_in,
+                                void* ws, size_t ws_bytes, void* stream);
+SPDKFAC_API int spdkfac_precond_plan_run(spdkfac_precond_plan* p, const float* const* g_inv, const float* const* grad,
+                             const float* const* a_inv, float* const* weight, float alpha, float* const* precond_out,
+                             void* stream);
+SPDKFAC_API void spdkfac_precond_plan_destroy(spdkfac_precond_plan* p);
+
+/* ------------------------------------------------------------------ collectives
+ * NCCL over NVLink/NVSwitch for the factor all-reduce (_mean_sym,
+ * emulator.py:199-200) and the owner broadcast of CT inverses (placement walk,
+ * emulator.py:256-262).  The communicator is created from a unique id that
+ * the host exchanges out of band (torch.distributed store). */
+typedef struct spdkfac_comm spdkfac_comm;
+SPDKFAC_API int spdkfac_comm_unique_id(void* id_out /* 128 bytes */);
+SPDKFAC_API int spdkfac_comm_create(spdkfac_comm** out, const void* id /* 128 bytes */, int rank, int world);
+SPDKFAC_API int spdkfac_comm_allreduce_sum_f32(spdkfac_comm* c, float* buf, size_t count, void* stream);
+SPDKFAC_API int spdkfac_comm_bcast_f32(spdkfac_comm* c, float* buf, size_t count, int root, void* stream);
+SPDKFAC_API int spdkfac_comm_group_start(void);
+SPDKFAC_API int spdkfac_comm_group_end(void);
+SPDKFAC_API void spdkfac_comm_destroy(spdkfac_comm* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPDKFAC_H_ */

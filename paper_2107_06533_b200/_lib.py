@@ -1,0 +1,110 @@
+"""ctypes binding of the C ABI in include/spdkfac.h (lib/libspdkfac.so).
+
+There is no fallback: if the library is missing or the device is not an
+sm_100 B200, every GPU entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import pathlib
+
+_HERE = pathlib.Path(__file__).resolve().parent
+LIB_PATH = pathlib.Path(os.environ.get("SPDKFAC_LIB", _HERE / "lib" / "libspdkfac.so"))
+
+OK, ERR_NOT_PD, ERR_SHAPE, ERR_ARG, ERR_CUDA, ERR_NCCL, ERR_UNSUPPORTED = range(7)
+ROWS, CONV_A, SPATIAL = 0, 1, 2
+
+
+class FactorGeom(C.Structure):
+    _fields_ = [("layout", C.c_int32), ("n", C.c_int64), ("c", C.c_int64), ("h", C.c_int64), ("w", C.c_int64),
+                ("kh", C.c_int32), ("kw", C.c_int32), ("stride_h", C.c_int32), ("stride_w", C.c_int32),
+                ("pad_h", C.c_int32), ("pad_w", C.c_int32), ("dil_h", C.c_int32), ("dil_w", C.c_int32)]
+
+
+_vp, _i32, _i64, _f32, _sz = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_size_t
+_pp = C.POINTER(C.c_void_p)
+_pi32 = C.POINTER(C.c_int32)
+
+# name -> (restype, argtypes); must match include/spdkfac.h exactly
+SIGNATURES = {
+    "spdkfac_last_error": (C.c_char_p, []),
+    "spdkfac_version": (C.c_int, []),
+    "spdkfac_device_supported": (C.c_int, []),
+    "spdkfac_factor_dims": (C.c_int, [C.POINTER(FactorGeom), C.POINTER(_i64), C.POINTER(_i64)]),
+    "spdkfac_factor_workspace_size": (_sz, [C.POINTER(FactorGeom)]),
+    "spdkfac_factor_plan_create": (C.c_int, [C.POINTER(_vp), C.POINTER(FactorGeom), _vp, _sz, _vp]),
+    "spdkfac_factor_plan_run": (C.c_int, [_vp, _vp, _f32, _f32, _f32, _vp, _vp]),
+    "spdkfac_factor_plan_destroy": (None, [_vp]),
+    "spdkfac_pack_upper_f32": (C.c_int, [_vp, _i64, _i64, _vp, _vp]),
+    "spdkfac_unpack_upper_f32": (C.c_int, [_vp, _i64, _vp, _i64, _vp]),
+    "spdkfac_pack_upper_batched_f32": (C.c_int, [C.c_int, _pi32, _pp, _pp, _vp]),
+    "spdkfac_unpack_upper_batched_f32": (C.c_int, [C.c_int, _pi32, _pp, _pp, _vp]),
+    "spdkfac_inverse_workspace_size": (_sz, [C.c_int, _pi32]),
+    "spdkfac_inverse_plan_create": (C.c_int, [C.POINTER(_vp), C.c_int, _pi32, _pp, _pp, _vp, _vp, _sz, _vp]),
+    "spdkfac_inverse_plan_run": (C.c_int, [_vp, _f32, _vp]),
+    "spdkfac_inverse_plan_destroy": (None, [_vp]),
+    "spdkfac_precond_workspace_size": (_sz, [C.c_int, _pi32, _pi32]),
+    "spdkfac_precond_plan_create": (C.c_int, [C.POINTER(_vp), C.c_int, _pi32, _pi32, _vp, _sz, _vp]),
+    "spdkfac_precond_plan_run": (C.c_int, [_vp, _pp, _pp, _pp, _pp, _f32, _pp, _vp]),
+    "spdkfac_precond_plan_destroy": (None, [_vp]),
+    "spdkfac_comm_unique_id": (C.c_int, [_vp]),
+    "spdkfac_comm_create": (C.c_int, [C.POINTER(_vp), _vp, C.c_int, C.c_int]),
+    "spdkfac_comm_allreduce_sum_f32": (C.c_int, [_vp, _vp, _sz, _vp]),
+    "spdkfac_comm_bcast_f32": (C.c_int, [_vp, _vp, _sz, C.c_int, _vp]),
+    "spdkfac_comm_group_start": (C.c_int, []),
+    "spdkfac_comm_group_end": (C.c_int, []),
+    "spdkfac_comm_destroy": (None, [_vp]),
+}
+
+_lib = None
+
+
+class LibraryError(RuntimeError):
+    pass
+
+
+def load(require_device: bool = False):
+    """Load (once) and return the ctypes library; raise loudly if absent."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise LibraryError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    if require_device and not _lib.spdkfac_device_supported():
+        raise LibraryError("libspdkfac requires an sm_100 (B200) CUDA device")
+    return _lib
+
+
+def last_error() -> str:
+    msg = load().spdkfac_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if rc in (ERR_SHAPE, ERR_ARG):
+        raise ValueError(msg)
+    raise LibraryError(f"spdkfac error {rc}: {msg}")
+
+
+def ptr_array(ptrs):
+    arr = (C.c_void_p * max(1, len(ptrs)))()
+    for i, p in enumerate(ptrs):
+        arr[i] = p
+    return arr
+
+
+def i32_array(vals):
+    arr = (C.c_int32 * max(1, len(vals)))()
+    for i, v in enumerate(vals):
+        arr[i] = int(v)
+    return arr

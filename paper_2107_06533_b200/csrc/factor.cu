@@ -1,0 +1,307 @@
+// Kronecker-factor construction: X^T X over rows (linear), im2col patches (conv A)
+// or spatial output-gradient rows (conv G), on tcgen05 with 3 x bf16 split operands.
+//
+// Pipeline per factor (one plan = one layer-side):
+//   1. stage kernel  : gather rows of X into the K-major split operand Xt[2][d][Mpad] (bf16 hi/lo)
+//                      -- the im2col / layout transform and the precision split in one HBM pass
+//   2. tc3 GEMM      : upper-triangle 128x128 tiles (I <= J) x split-K slices, partial tiles to ws
+//   3. reduce + pack : sum split-K partials in fixed order, apply 1/M, running average, 1/P,
+//                      write the packed upper triangle (the all-reduce / fusion-buffer format)
+#include "runtime.cuh"
+
+namespace spd {
+
+// ------------------------------------------------------------------ staging kernels
+// Xt[r][m] (r < d, m < Mpad) ; planes hi at 0, lo at d*Mpad.  Zero for m >= M.
+
+__global__ void stage_rows_kernel(const float* __restrict__ x, int64_t M, int64_t d, int64_t ldx,
+                                  __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
+  // 32x32 transpose tile through shared memory: coalesced reads along d, writes along m
+  __shared__ float tile[32][33];
+  const int64_t m0 = int64_t(blockIdx.x) * 32, r0 = int64_t(blockIdx.y) * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t m = m0 + k, r = r0 + tx;
+    tile[k][tx] = (m < M && r < d) ? x[m * ldx + r] : 0.f;
+  }
+  __syncthreads();
+  const int64_t plane = d * Mpad;
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t r = r0 + k, m = m0 + tx;
+    if (r < d && m < Mpad) {
+      __nv_bfloat16 h, l;
+      split_bf16(tile[tx][k], h, l);
+      xt[r * Mpad + m] = h;
+      xt[plane + r * Mpad + m] = l;
+    }
+  }
+}
+
+struct ConvGeom {
+  int B, C, H, W, Ho, Wo, kh, kw, sh, sw, ph, pw, dh, dw;
+};
+
+__global__ void stage_im2col_kernel(const float* __restrict__ x, ConvGeom g, int64_t M, int64_t d,
+                                    __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
+  const int64_t r = blockIdx.y;  // (c, ki, kj)
+  const int kj = int(r % g.kw), ki = int((r / g.kw) % g.kh), c = int(r / (int64_t(g.kw) * g.kh));
+  const int64_t plane = d * Mpad;
+  const int64_t HWo = int64_t(g.Ho) * g.Wo;
+  for (int64_t m = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; m < Mpad; m += int64_t(gridDim.x) * blockDim.x) {
+    float v = 0.f;
+    if (m < M) {
+      const int64_t b = m / HWo;
+      const int64_t hw = m - b * HWo;
+      const int ho = int(hw / g.Wo), wo = int(hw - int64_t(ho) * g.Wo);
+      const int hi = ho * g.sh - g.ph + ki * g.dh, wi = wo * g.sw - g.pw + kj * g.dw;
+      if (hi >= 0 && hi < g.H && wi >= 0 && wi < g.W) v = __ldg(x + ((b * g.C + c) * g.H + hi) * g.W + wi);
+    }
+    __nv_bfloat16 h, l;
+    split_bf16(v, h, l);
+    xt[r * Mpad + m] = h;
+    xt[plane + r * Mpad + m] = l;
+  }
+}
+
+__global__ void stage_spatial_kernel(const float* __restrict__ g, int B, int C, int64_t HW, int64_t M,
+                                     __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
+  const int64_t c = blockIdx.y;
+  const int64_t plane = int64_t(C) * Mpad;
+  for (int64_t m = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; m < Mpad; m += int64_t(gridDim.x) * blockDim.x) {
+    float v = 0.f;
+    if (m < M) {
+      const int64_t b = m / HW, hw = m - b * HW;
+      v = __ldg(g + (b * C + c) * HW + hw);
+    }
+    __nv_bfloat16 h, l;
+    split_bf16(v, h, l);
+    xt[c * Mpad + m] = h;
+    xt[plane + c * Mpad + m] = l;
+  }
+}
+
+// ------------------------------------------------------------------ reduce + pack
+// partial[slot][j][i] = D_tile[i][j]; slot = tile_index(I,J) * splits + s.
+__global__ void reduce_pack_kernel(const float* __restrict__ part, int64_t d, int T, int splits, float scale,
+                                   float decay, float world_scale, float* __restrict__ packed) {
+  __shared__ float tile[32][33];
+  const int I = blockIdx.z / T, J = blockIdx.z % T;  // tile pair (only I <= J launched work)
+  if (I > J) return;
+  const int tile_idx = I * T - I * (I - 1) / 2 + (J - I);  // row-major upper enumeration
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;     // within-tile 32x32 sub-block
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  // load: tx along i (contiguous in partial), ty along j
+  for (int k = ty; k < 32; k += 8) {
+    const int j = j0 + k, i = i0 + tx;
+    float acc = 0.f;
+    const float* p = part + (int64_t(tile_idx) * splits) * 16384 + int64_t(j) * 128 + i;
+    for (int s = 0; s < splits; ++s) acc += p[int64_t(s) * 16384];
+    tile[k][tx] = acc;  // tile[j][i]
+  }
+  __syncthreads();
+  // store packed: rows gi (ty), consecutive gj (tx)
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t gi = int64_t(I) * 128 + i0 + k;
+    const int64_t gj = int64_t(J) * 128 + j0 + tx;
+    if (gi < d && gj < d && gi <= gj) {
+      const int64_t pidx = gi * (2 * d - gi + 1) / 2 + (gj - gi);
+      const float fresh = scale * tile[tx][k];
+      float v = (decay == 0.f) ? fresh : decay * packed[pidx] + (1.f - decay) * fresh;
+      packed[pidx] = world_scale * v;
+    }
+  }
+}
+
+}  // namespace spd
+
+using namespace spd;
+
+struct spdkfac_factor_plan {
+  spdkfac_factor_geom g;
+  int64_t M, d, Mpad;
+  int T, splits, n_items;
+  __nv_bfloat16* xt;
+  float* partial;
+  CUtensorMap* maps;
+  TcItem* items;
+  TcEpi* epis;
+};
+
+namespace {
+
+int geom_dims(const spdkfac_factor_geom* g, int64_t* rows, int64_t* dim, int* Ho = nullptr, int* Wo = nullptr) {
+  SPD_ARG(g != nullptr, SPDKFAC_ERR_ARG, "null geometry");
+  if (g->layout == SPDKFAC_ROWS) {
+    SPD_ARG(g->n >= 1, SPDKFAC_ERR_ARG, "compute_factor: empty batch");
+    SPD_ARG(g->c >= 1 && g->w >= g->c, SPDKFAC_ERR_SHAPE, "compute_factor: bad row geometry d=%lld ld=%lld",
+            (long long)g->c, (long long)g->w);
+    *rows = g->n;
+    *dim = g->c;
+  } else if (g->layout == SPDKFAC_CONV_A) {
+    SPD_ARG(g->n >= 1 && g->c >= 1 && g->h >= 1 && g->w >= 1, SPDKFAC_ERR_ARG, "conv factor: empty input");
+    SPD_ARG(g->kh >= 1 && g->kw >= 1 && g->stride_h >= 1 && g->stride_w >= 1 && g->dil_h >= 1 && g->dil_w >= 1 &&
+                g->pad_h >= 0 && g->pad_w >= 0,
+            SPDKFAC_ERR_ARG, "conv factor: bad kernel geometry");
+    const int64_t ho = (g->h + 2 * g->pad_h - g->dil_h * (g->kh - 1) - 1) / g->stride_h + 1;
+    const int64_t wo = (g->w + 2 * g->pad_w - g->dil_w * (g->kw - 1) - 1) / g->stride_w + 1;
+    SPD_ARG(ho >= 1 && wo >= 1, SPDKFAC_ERR_SHAPE, "conv factor: empty output");
+    *rows = g->n * ho * wo;
+    *dim = g->c * g->kh * g->kw;
+    if (Ho) *Ho = int(ho);
+    if (Wo) *Wo = int(wo);
+  } else if (g->layout == SPDKFAC_SPATIAL) {
+    SPD_ARG(g->n >= 1 && g->c >= 1 && g->h >= 1 && g->w >= 1, SPDKFAC_ERR_ARG, "spatial factor: empty input");
+    *rows = g->n * g->h * g->w;
+    *dim = g->c;
+  } else {
+    SPD_ARG(false, SPDKFAC_ERR_ARG, "unknown factor layout %d", g->layout);
+  }
+  SPD_ARG(*dim <= 65536 && *rows < (int64_t(1) << 31), SPDKFAC_ERR_SHAPE, "factor too large");
+  return SPDKFAC_OK;
+}
+
+struct FactorLayout {
+  int64_t M, d, Mpad;
+  int T, splits, n_tiles;
+};
+
+FactorLayout factor_layout(int64_t M, int64_t d) {
+  FactorLayout L;
+  L.M = M;
+  L.d = d;
+  L.Mpad = round_up(M, 64);
+  L.T = int(cdiv(d, 128));
+  L.n_tiles = L.T * (L.T + 1) / 2;
+  const int64_t nkb = L.Mpad / 64;
+  // split K so that the launch has >= ~2 waves of 148 SMs, each slice >= 4 K blocks
+  int64_t want = cdiv(2 * 148, L.n_tiles);
+  int64_t maxs = std::max<int64_t>(1, nkb / 4);
+  L.splits = int(std::max<int64_t>(1, std::min(want, maxs)));
+  return L;
+}
+
+size_t factor_ws(const FactorLayout& L, Carve* c) {
+  Carve& cv = *c;
+  cv.take<__nv_bfloat16>(size_t(2) * L.d * L.Mpad);
+  cv.take<float>(size_t(L.n_tiles) * L.splits * 16384);
+  cv.take<CUtensorMap>(1, 128);
+  cv.take<TcItem>(size_t(L.n_tiles) * L.splits);
+  cv.take<TcEpi>(1);
+  return cv.used;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spdkfac_factor_dims(const spdkfac_factor_geom* g, int64_t* rows, int64_t* dim) {
+  return geom_dims(g, rows, dim);
+}
+
+size_t spdkfac_factor_workspace_size(const spdkfac_factor_geom* g) {
+  int64_t M, d;
+  if (geom_dims(g, &M, &d) != SPDKFAC_OK) return 0;
+  Carve c(nullptr, 0);
+  return factor_ws(factor_layout(M, d), &c) + 256;
+}
+
+int spdkfac_factor_plan_create(spdkfac_factor_plan** out, const spdkfac_factor_geom* g, void* ws, size_t ws_bytes,
+                               void* stream) {
+  SPD_ARG(out != nullptr, SPDKFAC_ERR_ARG, "null plan out");
+  int64_t M, d;
+  int rc = geom_dims(g, &M, &d);
+  if (rc) return rc;
+  FactorLayout L = factor_layout(M, d);
+  Carve c(ws, ws_bytes);
+  auto* p = new spdkfac_factor_plan();
+  p->g = *g;
+  p->M = M;
+  p->d = d;
+  p->Mpad = L.Mpad;
+  p->T = L.T;
+  p->splits = L.splits;
+  p->n_items = L.n_tiles * L.splits;
+  p->xt = c.take<__nv_bfloat16>(size_t(2) * d * L.Mpad);
+  p->partial = c.take<float>(size_t(L.n_tiles) * L.splits * 16384);
+  p->maps = c.take<CUtensorMap>(1, 128);
+  p->items = c.take<TcItem>(size_t(p->n_items));
+  p->epis = c.take<TcEpi>(1);
+  if (!c.ok() || ws == nullptr) {
+    delete p;
+    set_error("factor workspace too small: need %zu bytes, got %zu", c.used, ws_bytes);
+    return SPDKFAC_ERR_ARG;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<CUtensorMap> maps(1);
+  rc = make_operand_map(&maps[0], p->xt, true, L.Mpad, d, L.Mpad);
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  std::vector<TcItem> items;
+  const int64_t nkb = L.Mpad / 64;
+  const int64_t per = cdiv(nkb, L.splits);
+  for (int I = 0; I < L.T; ++I)
+    for (int J = I; J < L.T; ++J) {
+      const int tile_idx = I * L.T - I * (I - 1) / 2 + (J - I);
+      for (int s2 = 0; s2 < L.splits; ++s2) {
+        TcItem it{};
+        it.a_map = 0;
+        it.b_map = 0;
+        it.a_row = I * 128;
+        it.b_row = J * 128;
+        const int64_t kb0 = std::min<int64_t>(nkb, s2 * per), kb1 = std::min<int64_t>(nkb, (s2 + 1) * per);
+        it.k0 = int(kb0 * 64);
+        it.nk = int(kb1 - kb0);
+        it.epi = 0;
+        it.flags = (I == J) ? kSameAB : 0;
+        it.out_r = 0;
+        it.out_c = (tile_idx * L.splits + s2) * 128;
+        it.m_valid = 128;
+        it.n_valid = 128;
+        items.push_back(it);
+      }
+    }
+  std::vector<TcEpi> epis(1);
+  epis[0] = TcEpi{p->partial, 128, 0, 1.f, 0.f, kAxpby, 0};
+  if ((rc = upload(p->maps, maps, s)) || (rc = upload(p->items, items, s)) || (rc = upload(p->epis, epis, s))) {
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return SPDKFAC_OK;
+}
+
+int spdkfac_factor_plan_run(spdkfac_factor_plan* p, const float* x, float scale, float decay, float world_scale,
+                            float* packed, void* stream) {
+  SPD_ARG(p && x && packed, SPDKFAC_ERR_ARG, "null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const spdkfac_factor_geom& g = p->g;
+  if (g.layout == SPDKFAC_ROWS) {
+    dim3 grid(unsigned(cdiv(p->Mpad, 32)), unsigned(cdiv(p->d, 32)));
+    stage_rows_kernel<<<grid, dim3(32, 8), 0, s>>>(x, p->M, p->d, g.w, p->xt, p->Mpad);
+  } else if (g.layout == SPDKFAC_CONV_A) {
+    int64_t rows, dim;
+    int Ho = 0, Wo = 0;
+    geom_dims(&g, &rows, &dim, &Ho, &Wo);
+    ConvGeom cg{int(g.n), int(g.c), int(g.h), int(g.w), Ho, Wo, g.kh, g.kw, g.stride_h, g.stride_w,
+                g.pad_h, g.pad_w, g.dil_h, g.dil_w};
+    dim3 grid(unsigned(std::min<int64_t>(cdiv(p->Mpad, 256), 64)), unsigned(p->d));
+    stage_im2col_kernel<<<grid, 256, 0, s>>>(x, cg, p->M, p->d, p->xt, p->Mpad);
+  } else {
+    dim3 grid(unsigned(std::min<int64_t>(cdiv(p->Mpad, 256), 64)), unsigned(p->d));
+    stage_spatial_kernel<<<grid, 256, 0, s>>>(x, int(g.n), int(g.c), g.h * g.w, p->M, p->xt, p->Mpad);
+  }
+  SPD_CHECK_LAUNCH();
+  int rc = launch_tc3(Kind::BF16, p->maps, p->items, p->epis, p->n_items, s);
+  if (rc) return rc;
+  dim3 rgrid(4, 4, unsigned(p->T * p->T));
+  reduce_pack_kernel<<<rgrid, dim3(32, 8), 0, s>>>(p->partial, p->d, p->T, p->splits, scale, decay, world_scale,
+                                                   packed);
+  SPD_CHECK_LAUNCH();
+  return SPDKFAC_OK;
+}
+
+void spdkfac_factor_plan_destroy(spdkfac_factor_plan* p) { delete p; }
+
+}  // extern "C"

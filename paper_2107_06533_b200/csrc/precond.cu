@@ -1,0 +1,256 @@
+// Preconditioning + update, batched over layers:
+//   P_l = G_l^-1 grad_l A_l^-1,   W_l -= alpha P_l
+// as two tcgen05 3 x bf16 GEMMs per layer with K-major operands only (both inverses are
+// symmetric, so they serve as their own transposes):
+//   GEMM1  D1[m][n] = sum_k grad[m][k] A^-1[n][k]         = (grad A^-1)[m][n]     -> stored as T^T[n][m] (split)
+//   GEMM2  D2[n][m] = sum_k T^T[n][k] G^-1[m][k]         = (G^-1 grad A^-1)[m][n] -> stored as P[m][n]
+// The transposed epilogue store is the coalesced direction of the 32x32b TMEM layout.
+#include "runtime.cuh"
+
+namespace spd {
+
+struct SplitArgs {
+  const float* src[kMaxPtrs];
+  __nv_bfloat16* dst[kMaxPtrs];
+  int32_t cols[kMaxPtrs], ldd[kMaxPtrs];
+  int64_t plane[kMaxPtrs];
+  int32_t row0[kMaxPtrs + 1];
+  int n;
+};
+
+__global__ void split_rows_batched_kernel(const __grid_constant__ SplitArgs a) {
+  const int row = blockIdx.x;
+  int lo = 0, hi = a.n - 1;
+  while (lo < hi) {  // last t with row0[t] <= row
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.row0[mid] <= row) lo = mid;
+    else hi = mid - 1;
+  }
+  const int t = lo;
+  const int64_t r = row - a.row0[t];
+  const float* s = a.src[t] + r * a.cols[t];
+  __nv_bfloat16* d = a.dst[t] + r * a.ldd[t];
+  for (int c = threadIdx.x; c < a.cols[t]; c += blockDim.x) {
+    __nv_bfloat16 h, l;
+    split_bf16(s[c], h, l);
+    d[c] = h;
+    d[c + a.plane[t]] = l;
+  }
+}
+
+struct ApplyArgs {
+  const float* P[kMaxPtrs];
+  float* W[kMaxPtrs];
+  float* out[kMaxPtrs];
+  int64_t n_el[kMaxPtrs];
+  int n;
+};
+
+__global__ void apply_update_kernel(const __grid_constant__ ApplyArgs a, float alpha) {
+  const int t = blockIdx.y;
+  const int64_t n = a.n_el[t];
+  const float* P = a.P[t];
+  float* W = a.W[t];
+  float* o = a.out[t];
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    const float v = P[e];
+    if (W) W[e] -= alpha * v;
+    if (o) o[e] = v;
+  }
+}
+
+}  // namespace spd
+
+using namespace spd;
+
+struct spdkfac_precond_plan {
+  int n;
+  std::vector<int32_t> d_out, d_in;
+  std::vector<int64_t> ldi, ldo;
+  std::vector<__nv_bfloat16*> gW, aI, tT, gI;
+  std::vector<float*> P;
+  CUtensorMap* maps;
+  TcItem* items1;
+  TcItem* items2;
+  int n1, n2;
+  TcEpi* epis;
+};
+
+namespace {
+
+void precond_carve(int n, const int32_t* d_out, const int32_t* d_in, Carve& c, spdkfac_precond_plan* p, int* n1,
+                   int* n2) {
+  *n1 = *n2 = 0;
+  for (int l = 0; l < n; ++l) {
+    const int64_t m = d_out[l], k = d_in[l];
+    const int64_t ldi = round_up(k, 64), ldo = round_up(m, 64);
+    auto* gW = c.take<__nv_bfloat16>(size_t(2) * m * ldi);
+    auto* aI = c.take<__nv_bfloat16>(size_t(2) * k * ldi);
+    auto* tT = c.take<__nv_bfloat16>(size_t(2) * k * ldo);
+    auto* gI = c.take<__nv_bfloat16>(size_t(2) * m * ldo);
+    auto* P = c.take<float>(size_t(m) * k);
+    if (p) {
+      p->ldi.push_back(ldi);
+      p->ldo.push_back(ldo);
+      p->gW.push_back(gW);
+      p->aI.push_back(aI);
+      p->tT.push_back(tT);
+      p->gI.push_back(gI);
+      p->P.push_back(P);
+    }
+    *n1 += int(cdiv(m, 128) * cdiv(k, 128));
+    *n2 += int(cdiv(m, 128) * cdiv(k, 128));
+  }
+}
+
+int run_split(int n, const float* const* src, const std::vector<__nv_bfloat16*>& dst, const std::vector<int32_t>& rows,
+              const std::vector<int32_t>& cols, const std::vector<int64_t>& ldd, cudaStream_t s) {
+  for (int off = 0; off < n; off += kMaxPtrs) {
+    SplitArgs a{};
+    a.n = std::min(kMaxPtrs, n - off);
+    int r = 0;
+    for (int t = 0; t < a.n; ++t) {
+      const int l = off + t;
+      SPD_ARG(src[l] != nullptr, SPDKFAC_ERR_ARG, "null operand pointer for layer %d", l);
+      a.src[t] = src[l];
+      a.dst[t] = dst[l];
+      a.cols[t] = cols[l];
+      a.ldd[t] = int32_t(ldd[l]);
+      a.plane[t] = int64_t(rows[l]) * ldd[l];
+      a.row0[t] = r;
+      r += rows[l];
+    }
+    a.row0[a.n] = r;
+    split_rows_batched_kernel<<<r, 256, 0, s>>>(a);
+    SPD_CHECK_LAUNCH();
+  }
+  return SPDKFAC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t spdkfac_precond_workspace_size(int n, const int32_t* d_out, const int32_t* d_in) {
+  if (n < 1 || !d_out || !d_in) return 0;
+  Carve c(nullptr, 0);
+  int n1, n2;
+  precond_carve(n, d_out, d_in, c, nullptr, &n1, &n2);
+  c.take<CUtensorMap>(size_t(4) * n, 128);
+  c.take<TcItem>(size_t(n1));
+  c.take<TcItem>(size_t(n2));
+  c.take<TcEpi>(size_t(2) * n);
+  return c.used + 256;
+}
+
+int spdkfac_precond_plan_create(spdkfac_precond_plan** out, int n, const int32_t* d_out, const int32_t* d_in,
+                                void* ws, size_t ws_bytes, void* stream) {
+  SPD_ARG(out && n >= 1 && d_out && d_in, SPDKFAC_ERR_ARG, "bad precondition plan arguments");
+  for (int l = 0; l < n; ++l) SPD_ARG(d_out[l] >= 1 && d_in[l] >= 1, SPDKFAC_ERR_ARG, "dimension must be >= 1");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto* p = new spdkfac_precond_plan();
+  p->n = n;
+  p->d_out.assign(d_out, d_out + n);
+  p->d_in.assign(d_in, d_in + n);
+  Carve c(ws, ws_bytes);
+  precond_carve(n, d_out, d_in, c, p, &p->n1, &p->n2);
+  const size_t operand_bytes = c.used;
+  p->maps = c.take<CUtensorMap>(size_t(4) * n, 128);
+  p->items1 = c.take<TcItem>(size_t(p->n1));
+  p->items2 = c.take<TcItem>(size_t(p->n2));
+  p->epis = c.take<TcEpi>(size_t(2) * n);
+  if (!c.ok() || !ws) {
+    delete p;
+    set_error("precondition workspace too small: need %zu bytes, got %zu", c.used, ws_bytes);
+    return SPDKFAC_ERR_ARG;
+  }
+  // zero the split operands once: K padding must read as 0 in every GEMM
+  SPD_CUDA(cudaMemsetAsync(ws, 0, operand_bytes, s));
+  std::vector<CUtensorMap> maps(size_t(4) * n);
+  std::vector<TcItem> it1, it2;
+  std::vector<TcEpi> epis(size_t(2) * n);
+  int rc;
+  for (int l = 0; l < n; ++l) {
+    const int64_t m = d_out[l], k = d_in[l], ldi = p->ldi[l], ldo = p->ldo[l];
+    if ((rc = make_operand_map(&maps[4 * l + 0], p->gW[l], true, ldi, m, ldi)) ||
+        (rc = make_operand_map(&maps[4 * l + 1], p->aI[l], true, ldi, k, ldi)) ||
+        (rc = make_operand_map(&maps[4 * l + 2], p->tT[l], true, ldo, k, ldo)) ||
+        (rc = make_operand_map(&maps[4 * l + 3], p->gI[l], true, ldo, m, ldo))) {
+      delete p;
+      return rc;
+    }
+    epis[2 * l] = TcEpi{p->tT[l], ldo, k * ldo, 1.f, 0.f, kSplitBf16, 0};
+    epis[2 * l + 1] = TcEpi{p->P[l], k, 0, 1.f, 0.f, kAxpby, 0};
+    for (int mb = 0; mb < cdiv(m, 128); ++mb)
+      for (int nb = 0; nb < cdiv(k, 128); ++nb) {
+        TcItem a{};
+        a.a_map = 4 * l + 0;
+        a.b_map = 4 * l + 1;
+        a.a_row = mb * 128;
+        a.b_row = nb * 128;
+        a.k0 = 0;
+        a.nk = int(ldi / 64);
+        a.epi = 2 * l;
+        a.out_r = mb * 128;
+        a.out_c = nb * 128;
+        a.m_valid = int(std::min<int64_t>(128, m - mb * 128));
+        a.n_valid = int(std::min<int64_t>(128, k - nb * 128));
+        it1.push_back(a);
+        TcItem b{};
+        b.a_map = 4 * l + 2;
+        b.b_map = 4 * l + 3;
+        b.a_row = nb * 128;
+        b.b_row = mb * 128;
+        b.k0 = 0;
+        b.nk = int(ldo / 64);
+        b.epi = 2 * l + 1;
+        b.out_r = nb * 128;
+        b.out_c = mb * 128;
+        b.m_valid = int(std::min<int64_t>(128, k - nb * 128));
+        b.n_valid = int(std::min<int64_t>(128, m - mb * 128));
+        it2.push_back(b);
+      }
+  }
+  if ((rc = upload(p->maps, maps, s)) || (rc = upload(p->items1, it1, s)) || (rc = upload(p->items2, it2, s)) ||
+      (rc = upload(p->epis, epis, s))) {
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return SPDKFAC_OK;
+}
+
+int spdkfac_precond_plan_run(spdkfac_precond_plan* p, const float* const* g_inv, const float* const* grad,
+                             const float* const* a_inv, float* const* weight, float alpha, float* const* precond_out,
+                             void* stream) {
+  SPD_ARG(p && g_inv && grad && a_inv, SPDKFAC_ERR_ARG, "null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n = p->n;
+  std::vector<int64_t> ldi(p->ldi), ldo(p->ldo);
+  int rc;
+  if ((rc = run_split(n, grad, p->gW, p->d_out, p->d_in, ldi, s)) ||
+      (rc = run_split(n, a_inv, p->aI, p->d_in, p->d_in, ldi, s)) ||
+      (rc = run_split(n, g_inv, p->gI, p->d_out, p->d_out, ldo, s)))
+    return rc;
+  if ((rc = launch_tc3(Kind::BF16, p->maps, p->items1, p->epis, p->n1, s))) return rc;
+  if ((rc = launch_tc3(Kind::BF16, p->maps, p->items2, p->epis, p->n2, s))) return rc;
+  if (!weight && !precond_out) return SPDKFAC_OK;
+  for (int off = 0; off < n; off += kMaxPtrs) {
+    ApplyArgs a{};
+    a.n = std::min(kMaxPtrs, n - off);
+    for (int t = 0; t < a.n; ++t) {
+      const int l = off + t;
+      a.P[t] = p->P[l];
+      a.W[t] = weight ? weight[l] : nullptr;
+      a.out[t] = precond_out ? precond_out[l] : nullptr;
+      a.n_el[t] = int64_t(p->d_out[l]) * p->d_in[l];
+    }
+    apply_update_kernel<<<dim3(64, a.n), 256, 0, s>>>(a, alpha);
+    SPD_CHECK_LAUNCH();
+  }
+  return SPDKFAC_OK;
+}
+
+void spdkfac_precond_plan_destroy(spdkfac_precond_plan* p) { delete p; }
+
+}  // extern "C"

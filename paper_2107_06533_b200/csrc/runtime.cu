@@ -1,0 +1,181 @@
+// Runtime: error reporting, driver entry point for tensor-map encoding, GEMM launch,
+// packed <-> full symmetric layout kernels.
+#include <cstdarg>
+#include <mutex>
+
+#include "runtime.cuh"
+
+namespace spd {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int make_operand_map(CUtensorMap* out, const void* base, bool bf16, int64_t k_extent, int64_t rows, int64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  SPD_ARG(fn != nullptr, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int64_t es = bf16 ? 2 : 4;
+  SPD_ARG((ld * es) % 16 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0, SPDKFAC_ERR_ARG,
+          "tensor map: misaligned operand");
+  cuuint64_t dims[3] = {cuuint64_t(k_extent), cuuint64_t(rows), 2};
+  cuuint64_t strides[2] = {cuuint64_t(ld * es), cuuint64_t(ld * es * rows)};
+  cuuint32_t box[3] = {cuuint32_t(128 / es), 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(out, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SPD_ARG(r == CUDA_SUCCESS, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return SPDKFAC_OK;
+}
+
+template <Kind K>
+static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    SPD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmemBytes)));
+    attr_set = true;
+  }
+  tc3_gemm_kernel<K><<<n, 128, kTcSmemBytes, s>>>(maps, items, epis);
+  SPD_CHECK_LAUNCH();
+  return SPDKFAC_OK;
+}
+
+int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s) {
+  if (n <= 0) return SPDKFAC_OK;
+  return kind == Kind::BF16 ? launch_kind<Kind::BF16>(maps, items, epis, n, s)
+                            : launch_kind<Kind::TF32>(maps, items, epis, n, s);
+}
+
+// ------------------------------------------------------------------ pack / unpack
+// packed element (i <= j) at i*(2d-i+1)/2 + (j-i)  (row-major upper incl. diagonal)
+__global__ void pack_kernel(const float* __restrict__ full, int64_t d, int64_t ld, float* __restrict__ packed) {
+  const int64_t i = blockIdx.y;
+  const int64_t base = i * (2 * d - i + 1) / 2 - i;
+  for (int64_t j = i + blockIdx.x * blockDim.x + threadIdx.x; j < d; j += int64_t(gridDim.x) * blockDim.x)
+    packed[base + j] = full[i * ld + j];
+}
+
+__global__ void unpack_kernel(const float* __restrict__ packed, int64_t d, float* __restrict__ full, int64_t ld) {
+  // row i of the full matrix: j >= i from packed row i, j < i from packed row j (column i)
+  const int64_t i = blockIdx.y;
+  for (int64_t j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = j < i ? j : i, c = j < i ? i : j;
+    full[i * ld + j] = packed[r * (2 * d - r + 1) / 2 + (c - r)];
+  }
+}
+
+struct PackArgs {
+  const float* src[kMaxPtrs];
+  float* dst[kMaxPtrs];
+  int32_t d[kMaxPtrs];
+  int32_t row0[kMaxPtrs + 1];  // prefix sum of rows (grid.y mapping)
+  int n;
+};
+
+__global__ void pack_batched_kernel(const __grid_constant__ PackArgs a, int unpack) {
+  const int row = blockIdx.y;
+  int t = 0;
+  while (t + 1 < a.n && a.row0[t + 1] <= row) ++t;
+  const int64_t d = a.d[t], i = row - a.row0[t];
+  if (i >= d) return;
+  if (!unpack) {
+    const int64_t base = i * (2 * d - i + 1) / 2 - i;
+    for (int64_t j = i + threadIdx.x; j < d; j += blockDim.x) a.dst[t][base + j] = a.src[t][i * d + j];
+  } else {
+    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+      const int64_t r = j < i ? j : i, c = j < i ? i : j;
+      a.dst[t][i * d + j] = a.src[t][r * (2 * d - r + 1) / 2 + (c - r)];
+    }
+  }
+}
+
+static int pack_batched(int n, const int32_t* dims, const float* const* src, float* const* dst, int unpack,
+                        cudaStream_t s) {
+  SPD_ARG(n >= 0 && (n == 0 || (dims && src && dst)), SPDKFAC_ERR_ARG, "bad batched pack arguments");
+  for (int off = 0; off < n; off += kMaxPtrs) {
+    PackArgs a{};
+    a.n = std::min(kMaxPtrs, n - off);
+    int rows = 0;
+    for (int t = 0; t < a.n; ++t) {
+      SPD_ARG(dims[off + t] >= 1, SPDKFAC_ERR_ARG, "dimension must be >= 1");
+      a.src[t] = src[off + t];
+      a.dst[t] = dst[off + t];
+      a.d[t] = dims[off + t];
+      a.row0[t] = rows;
+      rows += dims[off + t];
+    }
+    a.row0[a.n] = rows;
+    pack_batched_kernel<<<dim3(1, rows), 256, 0, s>>>(a, unpack);
+    SPD_CHECK_LAUNCH();
+  }
+  return SPDKFAC_OK;
+}
+
+}  // namespace spd
+
+using namespace spd;
+
+extern "C" {
+
+const char* spdkfac_last_error(void) { return g_err; }
+int spdkfac_version(void) { return 100; }
+
+int spdkfac_device_supported(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return (major == 10 && minor == 0) ? 1 : 0;
+}
+
+int spdkfac_pack_upper_f32(const float* full, int64_t d, int64_t ld, float* packed, void* stream) {
+  SPD_ARG(d >= 1, SPDKFAC_ERR_ARG, "dimension must be >= 1");
+  SPD_ARG(ld >= d && full && packed, SPDKFAC_ERR_ARG, "bad pack arguments");
+  dim3 grid(unsigned(std::min<int64_t>(cdiv(d, 256), 16)), unsigned(d));
+  pack_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(full, d, ld, packed);
+  SPD_CHECK_LAUNCH();
+  return SPDKFAC_OK;
+}
+
+int spdkfac_unpack_upper_f32(const float* packed, int64_t d, float* full, int64_t ld, void* stream) {
+  SPD_ARG(d >= 1, SPDKFAC_ERR_ARG, "dimension must be >= 1");
+  SPD_ARG(ld >= d && full && packed, SPDKFAC_ERR_ARG, "bad unpack arguments");
+  dim3 grid(unsigned(std::min<int64_t>(cdiv(d, 256), 16)), unsigned(d));
+  unpack_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(packed, d, full, ld);
+  SPD_CHECK_LAUNCH();
+  return SPDKFAC_OK;
+}
+
+int spdkfac_pack_upper_batched_f32(int n, const int32_t* dims, const float* const* full, float* const* packed,
+                                   void* stream) {
+  return pack_batched(n, dims, full, packed, 0, static_cast<cudaStream_t>(stream));
+}
+
+int spdkfac_unpack_upper_batched_f32(int n, const int32_t* dims, const float* const* packed, float* const* full,
+                                     void* stream) {
+  return pack_batched(n, dims, packed, full, 1, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// Host-side runtime helpers: error state, tensor-map encoding, workspace carving,
+// table upload, tcgen05 GEMM launch.
+#pragma once
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "tc_gemm.cuh"
+#include "../../include/spdkfac.h"
+
+namespace spd {
+
+void set_error(const char* fmt, ...);
+
+#define SPD_CUDA(call)                                                                \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      ::spd::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+      return SPDKFAC_ERR_CUDA;                                                        \
+    }                                                                                 \
+  } while (0)
+
+#define SPD_CHECK_LAUNCH()                                                            \
+  do {                                                                                \
+    cudaError_t e_ = cudaGetLastError();                                              \
+    if (e_ != cudaSuccess) {                                                          \
+      ::spd::set_error("%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(e_)); \
+      return SPDKFAC_ERR_CUDA;                                                        \
+    }                                                                                 \
+  } while (0)
+
+#define SPD_ARG(cond, code, ...)            \
+  do {                                      \
+    if (!(cond)) {                          \
+      ::spd::set_error(__VA_ARGS__);        \
+      return code;                          \
+    }                                       \
+  } while (0)
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+inline int64_t cdiv(int64_t x, int64_t m) { return (x + m - 1) / m; }
+
+// Bump allocator over a caller-provided device workspace (256-B aligned slices).
+struct Carve {
+  uint8_t* base;
+  size_t cap, used = 0;
+  Carve(void* b, size_t c) : base(static_cast<uint8_t*>(b)), cap(c) {}
+  template <class T>
+  T* take(size_t count, size_t align = 256) {
+    used = (used + align - 1) / align * align;
+    T* p = reinterpret_cast<T*>(base ? base + used : nullptr);
+    used += count * sizeof(T);
+    return p;
+  }
+  bool ok() const { return used <= cap; }
+};
+
+// 3-D tensor map over a split-precision operand: planes [2][rows][ld] with K (= ld
+// axis, extent k_extent) innermost; box = {128 B of K, 128 rows, 1 plane}, SWIZZLE_128B.
+int make_operand_map(CUtensorMap* out, const void* base, bool bf16, int64_t k_extent, int64_t rows, int64_t ld);
+
+// Upload `n` POD objects into device memory `dst` on `stream` (pageable source: the
+// copy consumes the host buffer before returning).
+template <class T>
+int upload(T* dst, const std::vector<T>& v, cudaStream_t s) {
+  if (v.empty()) return SPDKFAC_OK;
+  SPD_CUDA(cudaMemcpyAsync(dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return SPDKFAC_OK;
+}
+
+// Pointer table passed by value (kernel parameter space).
+constexpr int kMaxPtrs = 128;
+struct PtrTable {
+  const void* p[kMaxPtrs];
+};
+
+int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items,
+               cudaStream_t s);
+
+}  // namespace spd

@@ -1,0 +1,199 @@
+// Split-precision tcgen05 "TN" tile engine shared by the factor SYRK, the blocked
+// sweep-inverse trailing update and the two preconditioning GEMMs.
+//
+//   D[i][j] = sum_k A[a_row + i][k] * B[b_row + j][k]      (128 x 128 tile, fp32 in TMEM)
+//
+// Each operand is stored in HBM as two planes [2][rows][ld] (hi, lo) of a
+// split-precision pair, K contiguous (K-major).  Three MMAs per K step,
+// hi*hi + hi*lo + lo*hi, recover fp32-class accuracy on the tensor cores:
+//   Kind::BF16 (kind::f16, bf16 planes): |x - hi - lo| <= 2^-18|x|  (factors, preconditioning)
+//   Kind::TF32 (kind::tf32, tf32 planes): |x - hi - lo| <= 2^-22|x|  (inverse updates)
+// One TMA producer lane, one MMA-issuing lane, all four warps drain TMEM in the epilogue.
+#pragma once
+#include "common.cuh"
+
+namespace spd {
+
+constexpr int kStages = 3;
+constexpr uint32_t kTileBytes = 128 * 128;  // 128 rows x 128 B (64 bf16 or 32 fp32), SWIZZLE_128B
+constexpr uint32_t kStageBytes = 4 * kTileBytes;
+constexpr size_t kTcSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 256 /*barriers*/;
+
+struct TcItem {
+  int32_t a_map, b_map;  // indices into the tensor-map array
+  int32_t a_row, b_row;  // operand row offsets (tensor-map dim 1)
+  int32_t k0, nk;        // first K element, number of K blocks
+  int32_t epi;           // index into the epilogue table
+  int32_t flags;         // kSameAB | kMirror
+  int32_t out_r, out_c;  // D[i][j] -> target element (out_c + j, out_r + i) (transposed store)
+  int32_t m_valid, n_valid;
+};
+constexpr int32_t kSameAB = 1;  // B tile == A tile (diagonal SYRK tile): load once
+constexpr int32_t kMirror = 2;  // also update target (out_r + i, out_c + j) (symmetric off-diagonal tile)
+
+enum EpiMode : int32_t {
+  kAxpby = 0,      // out = beta*out + alpha*D   (fp32 target)
+  kSplitBf16 = 1,  // out planes (bf16) <- split(alpha*D)
+  kSplitTf32 = 2,  // out planes (fp32, tf32-exact) <- split(alpha*D)
+};
+
+struct TcEpi {
+  void* out;
+  int64_t ld;            // row stride (elements) of the target
+  int64_t plane_stride;  // elements between hi and lo planes (split modes)
+  float alpha, beta;
+  int32_t mode;
+  int32_t pad_;
+};
+
+template <Kind K>
+__global__ void __launch_bounds__(128, 1)
+    tc3_gemm_kernel(const CUtensorMap* __restrict__ maps, const TcItem* __restrict__ items,
+                    const TcEpi* __restrict__ epis) {
+  constexpr int BK = (K == Kind::BF16) ? 64 : 32;  // one 128-byte swizzle row of K
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const TcItem it = items[blockIdx.x];
+  const bool same = (it.flags & kSameAB) != 0;
+  const int warp = warp_id();
+  const int lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<128>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && it.nk > 0) {  // ---- TMA producer
+      const CUtensorMap* am = maps + it.a_map;
+      const CUtensorMap* bm = maps + it.b_map;
+      tmap_acquire(am);
+      if (!same) tmap_acquire(bm);
+      const uint32_t bytes = same ? 2 * kTileBytes : 4 * kTileBytes;
+      for (int kb = 0; kb < it.nk; ++kb) {
+        const int s = kb % kStages;
+        mbar_wait(&empty[s], ((kb / kStages) & 1) ^ 1);
+        mbar_expect_tx(&full[s], bytes);
+        uint8_t* st = smem + s * kStageBytes;
+        const int kc = it.k0 + kb * BK;
+        tma_load_3d(st, am, &full[s], kc, it.a_row, 0);
+        tma_load_3d(st + kTileBytes, am, &full[s], kc, it.a_row, 1);
+        if (!same) {
+          tma_load_3d(st + 2 * kTileBytes, bm, &full[s], kc, it.b_row, 0);
+          tma_load_3d(st + 3 * kTileBytes, bm, &full[s], kc, it.b_row, 1);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && it.nk > 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = make_idesc<K>(128, 128);
+      for (int kb = 0; kb < it.nk; ++kb) {
+        const int s = kb % kStages;
+        mbar_wait(&full[s], (kb / kStages) & 1);
+        tc_fence_after();
+        uint8_t* st = smem + s * kStageBytes;
+        const uint64_t ahi = make_sdesc_sw128(st);
+        const uint64_t alo = make_sdesc_sw128(st + kTileBytes);
+        const uint64_t bhi = same ? ahi : make_sdesc_sw128(st + 2 * kTileBytes);
+        const uint64_t blo = same ? alo : make_sdesc_sw128(st + 3 * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 B of K per 128-B swizzle row
+          const uint64_t off = uint64_t(kk * 2);
+          umma<K>(tmem, ahi + off, bhi + off, idesc, (kb | kk) != 0);
+          umma<K>(tmem, ahi + off, blo + off, idesc, 1u);
+          umma<K>(tmem, alo + off, bhi + off, idesc, 1u);
+        }
+        tc_commit(&empty[s]);  // smem slot free once these MMAs retire
+      }
+      tc_commit(tfull);
+    }
+    __syncwarp();
+  }
+
+  // ---- epilogue: warp w owns TMEM lanes [32w, 32w+32) = tile rows
+  const TcEpi ep = epis[it.epi];
+  const int i = warp * 32 + lane;
+  if (it.nk > 0) {
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+  }
+  const bool row_ok = i < it.m_valid;
+  const int64_t ri = int64_t(it.out_r) + i;
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {
+    float v[32];
+    if (it.nk > 0) {
+      tmem_ld_32x32b_x32(tmem + (uint32_t(warp * 32) << 16) + uint32_t(c * 32), v);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) v[t] = 0.f;
+    }
+    if (ep.mode == kAxpby) {
+      float* out = static_cast<float*>(ep.out);
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const int j = c * 32 + t;
+        if (row_ok && j < it.n_valid) {
+          float* p = out + (int64_t(it.out_c) + j) * ep.ld + ri;
+          *p = (ep.beta == 0.f ? 0.f : ep.beta * *p) + ep.alpha * v[t];
+        }
+      }
+      if (it.flags & kMirror) {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const int j = c * 32 + t;
+          if (row_ok && j < it.n_valid) {
+            float* p = out + ri * ep.ld + it.out_c + j;
+            *p = (ep.beta == 0.f ? 0.f : ep.beta * *p) + ep.alpha * v[t];
+          }
+        }
+      }
+    } else if (ep.mode == kSplitBf16) {
+      __nv_bfloat16* out = static_cast<__nv_bfloat16*>(ep.out);
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const int j = c * 32 + t;
+        if (row_ok && j < it.n_valid) {
+          __nv_bfloat16 h, l;
+          split_bf16(ep.alpha * v[t], h, l);
+          const int64_t o = (int64_t(it.out_c) + j) * ep.ld + ri;
+          out[o] = h;
+          out[o + ep.plane_stride] = l;
+        }
+      }
+    } else {
+      float* out = static_cast<float*>(ep.out);
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const int j = c * 32 + t;
+        if (row_ok && j < it.n_valid) {
+          float h, l;
+          split_tf32(ep.alpha * v[t], h, l);
+          const int64_t o = (int64_t(it.out_c) + j) * ep.ld + ri;
+          out[o] = h;
+          out[o + ep.plane_stride] = l;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_free<128>(tmem);
+}
+
+}  // namespace spd

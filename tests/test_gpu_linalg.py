@@ -1,0 +1,214 @@
+"""GPU parity of the operator API (libspdkfac.so) against the float64 oracle.
+
+Tolerances (north_star): relative Frobenius error <= 1e-4 on factors and
+preconditioned gradients; inverses within a condition-number-scaled bound
+    ||X - X_ref||_F / ||X_ref||_F <= C_INV * kappa(M + gamma I) * 2^-24,
+with C_INV = 16 * sqrt(d) (fp32 Cholesky/Gauss-Jordan forward-error scale),
+and additionally never worse than 8x the error of cuSOLVER's fp32
+Cholesky inverse of the same matrix (torch.cholesky_inverse, comparison only).
+"""
+
+import math
+import pathlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+FACTOR_TOL = 1e-4
+PRECOND_TOL = 1e-4
+GOLD = pathlib.Path(__file__).parent / "golden"
+
+
+def _K():
+    import paper_2107_06533_b200.linalg as K
+    return K
+
+
+def relf(got, want):
+    got = got.detach().double().cpu().numpy() if isinstance(got, torch.Tensor) else np.asarray(got)
+    want = np.asarray(want, dtype=np.float64)
+    return float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-300))
+
+
+def spd(rng, d, jitter=0.1):
+    b = rng.standard_normal((d, d))
+    return b @ b.T / d + jitter * np.eye(d)
+
+
+@pytest.mark.parametrize("b,d", [(1, 1), (1, 3), (7, 5), (32, 64), (64, 130), (9, 200), (1000, 300),
+                                 (4096, 576), (32, 2048), (1568, 1152), (100, 4608)])
+def test_factor_rows_matches_oracle(b, d):
+    K = _K()
+    rng = np.random.default_rng(b * 7919 + d)
+    x = rng.standard_normal((b, d))
+    got = K.compute_factor_A(torch.tensor(x, dtype=torch.float32))
+    want = O.factor_A(x.astype(np.float32).astype(np.float64))
+    assert relf(got, want) <= FACTOR_TOL
+    assert torch.equal(got, got.T)  # unpack writes both triangles from one packed value
+
+
+def test_factor_golden():
+    K = _K()
+    lg = np.load(GOLD / "linalg_golden.npz")
+    for key in [k for k in lg.files if k.startswith("fa_x_")]:
+        x = lg[key]
+        got = K.compute_factor_G(torch.tensor(x, dtype=torch.float32))
+        assert relf(got, lg["fg_y_" + key[5:]]) <= FACTOR_TOL
+
+
+def test_factor_known_answers():  # pkg/tests/test_linalg.py:43-57 (exact in fp32)
+    K = _K()
+    assert torch.equal(K.compute_factor_A([[1.0, 0.0]]).cpu(), torch.tensor([[1.0, 0.0], [0.0, 0.0]]))
+    assert torch.equal(K.compute_factor_G([[0.0, 2.0]]).cpu(), torch.tensor([[0.0, 0.0], [0.0, 4.0]]))
+    assert torch.allclose(K.compute_factor_G([[1.0, 0.0], [0.0, 1.0]]).cpu(), 0.5 * torch.eye(2), atol=0)
+    with pytest.raises(ValueError, match="empty"):
+        K.compute_factor_A(torch.zeros(0, 3))
+
+
+@pytest.mark.parametrize("shape,k,s,p", [((2, 3, 9, 9), 3, 1, 1), ((4, 16, 14, 14), 3, 2, 1), ((2, 3, 32, 32), 7, 2, 3),
+                                         ((8, 64, 8, 8), 1, 1, 0), ((2, 64, 28, 28), 3, 1, 1)])
+def test_factor_conv_matches_oracle(shape, k, s, p):
+    K = _K()
+    rng = np.random.default_rng(sum(shape) + k)
+    x = rng.standard_normal(shape).astype(np.float32)
+    got = K.compute_factor_A_conv(torch.tensor(x), k, s, p)
+    want = O.factor_A(O.im2col_rows(x, k, k, s, p))
+    assert relf(got, want) <= FACTOR_TOL
+
+
+@pytest.mark.parametrize("shape", [(2, 5, 3, 3), (32, 64, 56, 56), (32, 2048, 7, 7)])
+def test_factor_spatial_matches_oracle(shape):
+    K = _K()
+    rng = np.random.default_rng(shape[1])
+    g = rng.standard_normal(shape).astype(np.float32)
+    got = K.compute_factor_G_spatial(torch.tensor(g), row_scale=shape[0])
+    want = O.factor_G(O.conv_grad_rows(g, scale=shape[0]))
+    assert relf(got, want) <= FACTOR_TOL
+
+
+def test_factor_running_average_and_world_scale():
+    K = _K()
+    import paper_2107_06533_b200._lib as L
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((300, 200)).astype(np.float32)
+    old = spd(rng, 200)
+    plan = K.FactorPlan(L.ROWS, x.shape)
+    packed = K.pack_upper(torch.tensor(old, dtype=torch.float32))
+    plan.run(torch.tensor(x).cuda(), packed, decay=0.9, world_scale=0.25)
+    want = 0.25 * (0.9 * old + 0.1 * O.factor_A(x.astype(np.float64)))
+    assert relf(K.unpack_upper(packed, 200), want) <= FACTOR_TOL
+
+
+@pytest.mark.parametrize("d", [1, 2, 17, 64, 129, 512, 1000])
+def test_pack_round_trip_exact(d):
+    K = _K()
+    rng = np.random.default_rng(d)
+    m = torch.tensor(spd(rng, d), dtype=torch.float32)
+    m = (m + m.T) / 2
+    p = K.pack_upper(m)
+    assert torch.equal(p.cpu(), torch.tensor(O.pack_upper(m.double().numpy()), dtype=torch.float32))
+    assert torch.equal(K.unpack_upper(p, d).cpu(), m)
+
+
+def inverse_bound(m, gamma, got_err):
+    d = m.shape[0]
+    ev = np.linalg.eigvalsh(m + gamma * np.eye(d))
+    kappa = ev[-1] / ev[0]
+    return 16.0 * math.sqrt(d) * kappa * 2.0 ** -24, kappa
+
+
+def cusolver_err(m, gamma, want):
+    t = torch.tensor(m + gamma * np.eye(m.shape[0]), dtype=torch.float32, device="cuda")
+    ref = torch.cholesky_inverse(torch.linalg.cholesky(t))
+    return relf(ref, want)
+
+
+@pytest.mark.parametrize("d,gamma", [(1, 0.5), (5, 0.0), (17, 0.01), (64, 0.1), (128, 0.05), (129, 0.05), (147, 0.1),
+                                     (256, 0.1), (300, 0.01), (576, 0.1), (1024, 0.1), (2304, 0.1)])
+def test_damped_inverse_matches_oracle(d, gamma):
+    K = _K()
+    rng = np.random.default_rng(d)
+    m = spd(rng, d)
+    mt = torch.tensor(m, dtype=torch.float32)
+    m32 = mt.double().numpy()
+    got = K.damped_inverse(mt, gamma)
+    want = O.damped_inverse(m32, gamma)
+    err = relf(got, want)
+    bound, kappa = inverse_bound(m32, gamma, err)
+    ref = cusolver_err(m32, gamma, want)
+    assert err <= max(bound, 8 * ref), (err, bound, ref, kappa)
+    assert torch.equal(got, got.T)
+
+
+def test_damped_inverse_golden():
+    K = _K()
+    lg = np.load(GOLD / "linalg_golden.npz")
+    for key in [k for k in lg.files if k.startswith("inv_m_")]:
+        d = key[6:]
+        m, gamma = lg[key], float(lg["inv_gamma_" + d])
+        got = K.damped_inverse(torch.tensor(m, dtype=torch.float32), gamma)
+        want = lg["inv_y_" + d]
+        bound, _ = inverse_bound(m, gamma, 0)
+        assert relf(got, want) <= max(bound, 8 * cusolver_err(m, gamma, want))
+
+
+def test_damped_inverse_batched_mixed_sizes():
+    K = _K()
+    rng = np.random.default_rng(77)
+    dims = [64, 147, 256, 64, 1000, 128, 512]
+    mats = [spd(rng, d) for d in dims]
+    outs = K.damped_inverse_batched([torch.tensor(m, dtype=torch.float32).cuda() for m in mats], 0.1)
+    for m, o in zip(mats, outs):
+        want = O.damped_inverse(m.astype(np.float32).astype(np.float64), 0.1)
+        bound, _ = inverse_bound(m, 0.1, 0)
+        assert relf(o, want) <= max(bound, 8 * cusolver_err(m, 0.1, want))
+
+
+def test_damped_inverse_errors():  # pkg/tests/test_linalg.py:125-133
+    K = _K()
+    with pytest.raises(K.NotPositiveDefiniteError) as e:
+        K.damped_inverse(torch.diag(torch.tensor([1.0, -1.0, 2.0])), 0.0)
+    assert e.value.pivot == 1
+    with pytest.raises(ValueError, match="nonnegative"):
+        K.damped_inverse(torch.eye(2), -0.1)
+    # failure inside the blocked path: leading 200x200 block PD, pivot 200 negative
+    d = 300
+    m = np.eye(d)
+    m[200, 200] = -1.0
+    with pytest.raises(K.NotPositiveDefiniteError) as e:
+        K.damped_inverse(torch.tensor(m, dtype=torch.float32), 0.0)
+    assert e.value.pivot == 200
+    assert torch.allclose(K.damped_inverse(torch.eye(3), 0.0).cpu(), torch.eye(3), atol=1e-7)
+    assert torch.allclose(K.damped_inverse(torch.eye(2), 1.0).cpu(), 0.5 * torch.eye(2), atol=1e-7)
+
+
+@pytest.mark.parametrize("dout,din", [(1, 1), (3, 5), (10, 64), (64, 147), (130, 70), (256, 2304), (1000, 2048),
+                                      (2048, 512)])
+def test_precondition_matches_oracle(dout, din):
+    K = _K()
+    rng = np.random.default_rng(dout * 31 + din)
+    g = rng.standard_normal((dout, din)).astype(np.float32)
+    a = spd(rng, din, 1.0).astype(np.float32)
+    gi = spd(rng, dout, 1.0).astype(np.float32)
+    got = K.precondition(torch.tensor(g), torch.tensor(a), torch.tensor(gi))
+    want = O.precondition(g.astype(np.float64), a.astype(np.float64), gi.astype(np.float64))
+    assert relf(got, want) <= PRECOND_TOL
+
+
+def test_precondition_golden_and_kat():
+    K = _K()
+    lg = np.load(GOLD / "linalg_golden.npz")
+    for key in [k for k in lg.files if k.startswith("pc_grad_")]:
+        t = key[8:]
+        got = K.precondition(torch.tensor(lg[key], dtype=torch.float32), torch.tensor(lg["pc_ainv_" + t], dtype=torch.float32),
+                             torch.tensor(lg["pc_ginv_" + t], dtype=torch.float32))
+        assert relf(got, lg["pc_y_" + t]) <= PRECOND_TOL
+    g = torch.arange(6.0).reshape(2, 3)
+    assert torch.allclose(K.precondition(g, torch.eye(3), torch.eye(2)).cpu(), g, atol=0)
+    with pytest.raises(ValueError, match="shape mismatch"):
+        K.precondition(torch.zeros(2, 3), torch.eye(2), torch.eye(2))
