@@ -1,0 +1,305 @@
+#!/usr/bin/env python
+"""SPD-KFAC iteration-time benchmark (BASELINE.json metric):
+
+  "SPD-KFAC iteration time (ms) ResNet-50 bs32/GPU @1/2/4/8 B200; % roofline"
+
+One step = one SPD-KFAC training iteration of torchvision ResNet-50 at batch 32
+per GPU on synthetic 224x224 data: forward (A factors on a side stream), backward
+(G factors, fused factor all-reduce per fusion group), gradient all-reduce,
+load-balanced damped inverses + owner broadcast, preconditioning + weight update.
+Factor and inverse update frequency 1 (every iteration does all of it).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+Prints ONE JSON line on rank 0.  `value` = iteration ms (max over ranks, CUDA
+events on the launching stream); `e2e` = the same through the public API with
+the batch copied from pinned host memory and the loss read back every step;
+`roofline` = the factor SYRK kernel (the dominant tcgen05 kernel) from live CUDA
+events; `cpu_baseline` = the reference's float64 linear algebra (oracle port) on
+this host's cores for the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+NPROC = os.cpu_count() or 1
+for _k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_k, str(NPROC))
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SPD-KFAC iteration time (ms) ResNet-50 bs32/GPU @1/2/4/8 B200; % roofline"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--model", default="resnet50")
+    p.add_argument("--batch", type=int, default=32)
+    p.add_argument("--lr", type=float, default=0.01)
+    p.add_argument("--damping", type=float, default=0.1)
+    p.add_argument("--factor-freq", type=int, default=1)
+    p.add_argument("--inv-freq", type=int, default=1)
+    p.add_argument("--placement", default="lbp")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--profile", action="store_true", help="short run for ncu: no clocks/e2e/cpu legs")
+    return p.parse_args()
+
+
+def workload_config(a, world):
+    return {"workload": f"{a.model} SPD-KFAC bs{a.batch}/GPU synthetic {'32x32' if a.model == 'resnet20' else '224x224'}"
+                        f" (BASELINE.json configs[{1 if world == 1 else 2}])",
+            "per_gpu_batch": a.batch, "global_batch": a.batch * world, "damping": a.damping, "lr": a.lr,
+            "factor_update_freq": a.factor_freq, "inv_update_freq": a.inv_freq, "fusion": "optimal",
+            "placement": a.placement, "parallelism": f"dp{world}",
+            "l2": "per-iteration working set (activations, 0.3 GB packed factors, im2col staging) >> 126 MB L2; no flush"}
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- CPU reference
+def cpu_reference(model, batch, steps=None, budget_s=30.0):
+    """Time the reference's float64 K-FAC algebra for one full step (see oracle/cpu_step.py)."""
+    from oracle import cpu_step
+    from paper_2107_06533_b200.workloads import layer_shapes
+    shapes = layer_shapes(model, batch)
+    keys = list(cpu_step.distinct_shapes(shapes))
+    cache = {}
+    per_step = []
+    if steps is None:
+        total, spent, n, _ = cpu_step.full_step_estimate(shapes, cache=cache)
+    else:  # reference arm: a rotating quarter of the distinct shapes per step
+        q = max(1, (len(keys) + 3) // 4)
+        for s in range(steps):
+            t0 = time.perf_counter()
+            cpu_step.full_step_estimate(shapes, subset=range(s * q, s * q + q), cache=cache)
+            per_step.append(time.perf_counter() - t0)
+        total, spent, n, missing = cpu_step.full_step_estimate(shapes, subset=[], cache=cache)
+        if missing:
+            idx = [keys.index(k) for k in missing]
+            total, _, _, _ = cpu_step.full_step_estimate(shapes, subset=idx, cache=cache)
+    sample = (f"{len(keys)} distinct layer shapes of {len(shapes)} {model} K-FAC layers (bs{batch}), each timed "
+              f"(factor A+G, 2 damped inverses, precondition, update; float64 numpy/scipy LAPACK) and weighted by "
+              f"multiplicity; im2col and forward/backward not charged")
+    return total * 1e3, sample, per_step
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    import torch.nn as nn
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    torch.backends.cudnn.benchmark = True
+
+    from paper_2107_06533_b200 import _lib
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    from paper_2107_06533_b200.workloads import build_model, input_shape, num_classes
+
+    torch.manual_seed(0)
+    model = build_model(a.model).to(dev)
+    opt = SPDKFAC(model, lr=a.lr, damping=a.damping, factor_update_freq=a.factor_freq, inv_update_freq=a.inv_freq,
+                  placement=a.placement)
+    crit = nn.CrossEntropyLoss()
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + rank)
+    shp = input_shape(a.model, a.batch)
+    xs = [torch.randn(shp, device=dev, generator=g) for _ in range(2)]
+    ys = [torch.randint(0, num_classes(a.model), (a.batch,), device=dev, generator=g) for _ in range(2)]
+
+    def step(i, x=None, y=None):
+        x = xs[i % 2] if x is None else x
+        y = ys[i % 2] if y is None else y
+        opt.zero_grad(set_to_none=False)
+        loss = crit(model(x), y)
+        loss.backward()
+        opt.step()
+        return loss
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for i in range(a.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    barrier()
+
+    clocks = None if a.profile else Clocks(local)
+    _lib.stats_reset(timing=True)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(a.steps):
+        loss = step(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1) / a.steps
+    clk = clocks.stop() if clocks else None
+    st = _lib.stats()
+    launches = st["total_launches"]
+    ms_max = max_over_ranks(ms)
+    final_loss = float(loss.item())
+    opt.check_inverses()
+
+    # ---- e2e through the public API: pinned host batch -> device every step, loss read back
+    e2e = None
+    if not a.no_e2e and not a.profile:
+        xh = [x.cpu().pin_memory() for x in xs]
+        yh = [y.cpu().pin_memory() for y in ys]
+        xd, yd = torch.empty_like(xs[0]), torch.empty_like(ys[0])
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for i in range(a.steps):
+            xd.copy_(xh[i % 2], non_blocking=True)
+            yd.copy_(yh[i % 2], non_blocking=True)
+            loss = step(i, xd, yd)
+            _ = float(loss.item())
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(f0.elapsed_time(f1) / a.steps)
+        e2e = {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": xh[0].numel() * 4 + yh[0].numel() * 8,
+               "d2h_bytes_per_step": 4}
+
+    # ---- roofline of the dominant tcgen05 kernel (factor SYRK), live CUDA events
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    sy = st["factor_syrk"]
+    ach = sy["flops"] / (sy["ms"] * 1e-3) / 1e12 if sy["ms"] > 0 else 0.0
+    peak = peaks.get("bf16_tflops_sustained") or 1362.2
+    step_ms_total = sum(v["ms"] for k, v in st.items() if isinstance(v, dict)) / a.steps
+    roofline = {"kernel": "tc3_gemm_kernel<BF16> (factor SYRK, 3 x bf16 split, tcgen05)", "bound": "tensor",
+                "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
+                "traffic": None,
+                "algorithmic_flops_per_step": sy["flops"] / a.steps,
+                "kernel_ms_per_step": round(sy["ms"] / a.steps, 4),
+                "tensor_pipe_mmas_per_algorithmic_mac": 3,
+                "share_of_library_kernel_time": round(sy["ms"] / a.steps / step_ms_total, 4) if step_ms_total else None}
+    breakdown = {k: {"ms_per_step": round(v["ms"] / a.steps, 4), "launches_per_step": v["launches"] / a.steps,
+                     "tflops": round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 2) if v["ms"] > 0 and v["flops"] else None}
+                 for k, v in st.items() if isinstance(v, dict)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline and not a.profile:
+        cpu_ms, sample, _ = cpu_reference(a.model, a.batch)
+        cpu = {"value": round(cpu_ms, 1), "unit": "ms", "cores": int(os.environ["OPENBLAS_NUM_THREADS"]),
+               "kind": "port", "sample": sample}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(ms_max, 3), "unit": "ms", "n_gpus": world, "steps": a.steps,
+               "warmup": a.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": False, "scaling": "weak",
+               "vs_baseline": None, "dtype": "fp32 (3xbf16/3xtf32 split tensor-core contractions)",
+               "data": "synthetic (random N(0,1) images, uniform labels; random-init torchvision weights)",
+               "config": workload_config(a, world), "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+               "cpu_baseline": cpu, "clocks": clk, "kernel_breakdown": breakdown,
+               "placement_imbalance": _imbalance(opt), "final_loss": final_loss}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _imbalance(opt):
+    from paper_2107_06533_b200.planner import placement_imbalance
+    r = placement_imbalance(opt.placement, weight=lambda d: float(d) ** 3)
+    r2 = placement_imbalance(opt.placement, weight=lambda d: float(d) ** 2)
+    return {"d3_max_over_mean_minus_1": round(r["max_over_mean_minus_1"], 4),
+            "d3_makespan_over_lower_bound": round(r["makespan_over_lower_bound"], 4),
+            "d2_max_over_mean_minus_1": round(r2["max_over_mean_minus_1"], 4)}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    ms, sample, per_step = cpu_reference(a.model, a.batch, steps=max(1, a.steps))
+    cores = int(os.environ["OPENBLAS_NUM_THREADS"])
+    out = {"metric": METRIC, "impl": "reference", "value": round(ms, 1), "unit": "ms", "n_gpus": world,
+           "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 1), "higher_is_better": False,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": workload_config(a, world),
+           "cpu_baseline": {"value": round(ms, 1), "unit": "ms", "cores": cores, "kind": "port",
+                            "sample": sample + "; per timed step a rotating quarter of the distinct shapes"},
+           "e2e": {"value": round(ms, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "note": "reference kfacsched is CPU-only numpy/scipy (no GPU path); timed via the oracle port "
+                   "(oracle/), per-shape times x multiplicity = one full ResNet-50 step per rank"}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)

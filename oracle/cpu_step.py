@@ -1,0 +1,67 @@
+"""Timed CPU reference of the SPD-KFAC step's linear algebra (TEST / BASELINE
+INFRASTRUCTURE ONLY: used by bench.py's `cpu_baseline` leg and `--impl reference`).
+
+Per layer l of the workload (shapes from paper_2107_06533_b200.workloads), exactly
+the reference's float64 arithmetic (restated in oracle/linalg.py):
+  compute_factor_A(rows[M, a]), compute_factor_G(rows[M, g])   linalg.py:116-127
+  damped_inverse(A, gamma), damped_inverse(G, gamma)           linalg.py:130-149
+  precondition(grad, A^-1, G^-1); W -= alpha * step            linalg.py:152-167, emulator.py:203-208
+on synthetic rows of the layer's true (M, a, g).  Distinct layer shapes are timed
+once each and weighted by their multiplicity (the per-layer work depends only on
+the shape), which bounds the CPU time; the reference has no conv layers, so the
+rows are fed as if already im2col'd (im2col cost not charged to the reference).
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from collections import Counter
+
+import numpy as np
+
+from .linalg import damped_inverse, factor_A, factor_G, precondition
+
+
+def distinct_shapes(shapes):
+    """[(M, a, g)] -> Counter of multiplicities, in first-seen order."""
+    return Counter((m, a, g) for _, m, a, g in shapes)
+
+
+def time_layer(m: int, a: int, g: int, gamma: float = 0.1, alpha: float = 0.1, seed: int = 0) -> float:
+    rng = np.random.default_rng(seed)
+    rows_a = rng.standard_normal((m, a))
+    rows_g = rng.standard_normal((m, g))
+    grad = rng.standard_normal((g, a))
+    w = rng.standard_normal((g, a))
+    t0 = time.perf_counter()
+    A = factor_A(rows_a)
+    G = factor_G(rows_g)
+    ai = damped_inverse(A, gamma)
+    gi = damped_inverse(G, gamma)
+    w -= alpha * precondition(grad, ai, gi)
+    return time.perf_counter() - t0
+
+
+def threads() -> int:
+    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        if os.environ.get(k):
+            return int(os.environ[k])
+    return os.cpu_count() or 1
+
+
+def full_step_estimate(shapes, subset=None, cache=None) -> tuple:
+    """Time (a subset of) the distinct shapes; return (estimated seconds for the
+    whole step, seconds actually spent, number of shapes timed)."""
+    cnt = distinct_shapes(shapes)
+    keys = list(cnt)
+    cache = {} if cache is None else cache
+    todo = keys if subset is None else [keys[i % len(keys)] for i in subset]
+    spent = 0.0
+    for k in todo:
+        t = time_layer(*k)
+        spent += t
+        cache.setdefault(k, []).append(t)
+    missing = [k for k in keys if k not in cache]
+    total = sum(cnt[k] * float(np.mean(cache[k])) for k in keys if k in cache)
+    return total, spent, len(todo), missing

@@ -32,6 +32,10 @@ SIGNATURES = {
     "spdkfac_last_error": (C.c_char_p, []),
     "spdkfac_version": (C.c_int, []),
     "spdkfac_device_supported": (C.c_int, []),
+    "spdkfac_stats_reset": (None, [C.c_int]),
+    "spdkfac_stats_launches": (C.c_uint64, []),
+    "spdkfac_stats_read": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(_i64), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_double)]),
     "spdkfac_factor_dims": (C.c_int, [C.POINTER(FactorGeom), C.POINTER(_i64), C.POINTER(_i64)]),
     "spdkfac_factor_workspace_size": (_sz, [C.POINTER(FactorGeom)]),
     "spdkfac_factor_plan_create": (C.c_int, [C.POINTER(_vp), C.POINTER(FactorGeom), _vp, _sz, _vp]),
@@ -80,6 +84,26 @@ def load(require_device: bool = False):
     if require_device and not _lib.spdkfac_device_supported():
         raise LibraryError("libspdkfac requires an sm_100 (B200) CUDA device")
     return _lib
+
+
+STAT_CATEGORIES = ("factor_stage", "factor_syrk", "factor_reduce", "inv_small", "inv_pivot", "inv_panel",
+                   "inv_update", "inv_unpack_finalize", "precond_split", "precond_gemm", "precond_apply", "pack")
+
+
+def stats_reset(timing: bool = False) -> None:
+    load().spdkfac_stats_reset(1 if timing else 0)
+
+
+def stats() -> dict:
+    """Per-category {ms, launches, flops, bytes} since the last stats_reset (synchronises)."""
+    lib = load()
+    out = {}
+    for i, name in enumerate(STAT_CATEGORIES):
+        ms, n, fl, by = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+        check(lib.spdkfac_stats_read(i, C.byref(ms), C.byref(n), C.byref(fl), C.byref(by)), "stats")
+        out[name] = {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
+    out["total_launches"] = int(lib.spdkfac_stats_launches())
+    return out
 
 
 def last_error() -> str:

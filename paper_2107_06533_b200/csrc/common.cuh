@@ -39,11 +39,17 @@ SPD_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+SPD_DEV uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 SPD_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-  // bounded spin: a protocol bug traps (kernel error) instead of hanging the GPU
-  uint32_t spins = 0;
+  // watchdog: a protocol bug traps (kernel error) after ~4 s instead of hanging the GPU
+  if (mbar_try_wait(bar, parity)) return;
+  const uint64_t t0 = global_ns();
   while (!mbar_try_wait(bar, parity)) {
-    if (++spins > (1u << 26)) asm volatile("trap;");
+    if (global_ns() - t0 > 4000000000ull) asm volatile("trap;");
   }
 }
 

@@ -41,42 +41,93 @@ struct ConvGeom {
   int B, C, H, W, Ho, Wo, kh, kw, sh, sw, ph, pw, dh, dw;
 };
 
-__global__ void stage_im2col_kernel(const float* __restrict__ x, ConvGeom g, int64_t M, int64_t d,
-                                    __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
-  const int64_t r = blockIdx.y;  // (c, ki, kj)
-  const int kj = int(r % g.kw), ki = int((r / g.kw) % g.kh), c = int(r / (int64_t(g.kw) * g.kh));
+__device__ __forceinline__ void store_split2(__nv_bfloat16* xt, int64_t plane, int64_t o, float v0, float v1) {
+  __nv_bfloat16 h0, l0, h1, l1;
+  split_bf16(v0, h0, l0);
+  split_bf16(v1, h1, l1);
+  *reinterpret_cast<__nv_bfloat162*>(xt + o) = __halves2bfloat162(h0, h1);
+  *reinterpret_cast<__nv_bfloat162*>(xt + plane + o) = __halves2bfloat162(l0, l1);
+}
+
+// One block per (patch row r = (c, ki, kj), image b): threads walk the output positions of
+// image b two at a time (bf16x2 stores), 32-bit index math, one division per pair.
+__global__ void __launch_bounds__(256) stage_im2col_kernel(const float* __restrict__ x, ConvGeom g, int64_t M,
+                                                           int64_t d, __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
+  const int r = blockIdx.y;
+  const int b = blockIdx.x;
+  const int kj = r % g.kw, ki = (r / g.kw) % g.kh, c = r / (g.kw * g.kh);
+  const int HWo = g.Ho * g.Wo;
   const int64_t plane = d * Mpad;
-  const int64_t HWo = int64_t(g.Ho) * g.Wo;
-  for (int64_t m = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; m < Mpad; m += int64_t(gridDim.x) * blockDim.x) {
-    float v = 0.f;
-    if (m < M) {
-      const int64_t b = m / HWo;
-      const int64_t hw = m - b * HWo;
-      const int ho = int(hw / g.Wo), wo = int(hw - int64_t(ho) * g.Wo);
-      const int hi = ho * g.sh - g.ph + ki * g.dh, wi = wo * g.sw - g.pw + kj * g.dw;
-      if (hi >= 0 && hi < g.H && wi >= 0 && wi < g.W) v = __ldg(x + ((b * g.C + c) * g.H + hi) * g.W + wi);
+  const int64_t row = int64_t(r) * Mpad + int64_t(b) * HWo;  // m = b*HWo + hw
+  const float* xc = x + (int64_t(b) * g.C + c) * g.H * g.W;
+  const int hoff = ki * g.dh - g.ph, woff = kj * g.dw - g.pw;
+  // HWo may be odd (7x7): pair (hw, hw+1) when both in range, row offsets are then even
+  // only if b*HWo is even; fall back to scalar stores otherwise.
+  const bool vec = ((int64_t(b) * HWo) & 1) == 0 && (Mpad & 1) == 0;
+  if (vec) {
+    for (int hw = 2 * threadIdx.x; hw < HWo; hw += 2 * blockDim.x) {
+      float v[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int q = hw + u;
+        v[u] = 0.f;
+        if (q < HWo) {
+          const int ho = q / g.Wo, wo = q - ho * g.Wo;
+          const int hi = ho * g.sh + hoff, wi = wo * g.sw + woff;
+          if (hi >= 0 && hi < g.H && wi >= 0 && wi < g.W) v[u] = __ldg(xc + hi * g.W + wi);
+        }
+      }
+      if (hw + 1 < HWo) {
+        store_split2(xt, plane, row + hw, v[0], v[1]);
+      } else {
+        __nv_bfloat16 h, l;
+        split_bf16(v[0], h, l);
+        xt[row + hw] = h;
+        xt[plane + row + hw] = l;
+      }
     }
-    __nv_bfloat16 h, l;
-    split_bf16(v, h, l);
-    xt[r * Mpad + m] = h;
-    xt[plane + r * Mpad + m] = l;
+  } else {
+    for (int q = threadIdx.x; q < HWo; q += blockDim.x) {
+      const int ho = q / g.Wo, wo = q - ho * g.Wo;
+      const int hi = ho * g.sh + hoff, wi = wo * g.sw + woff;
+      float v = 0.f;
+      if (hi >= 0 && hi < g.H && wi >= 0 && wi < g.W) v = __ldg(xc + hi * g.W + wi);
+      __nv_bfloat16 h, l;
+      split_bf16(v, h, l);
+      xt[row + q] = h;
+      xt[plane + row + q] = l;
+    }
   }
 }
 
-__global__ void stage_spatial_kernel(const float* __restrict__ g, int B, int C, int64_t HW, int64_t M,
-                                     __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
-  const int64_t c = blockIdx.y;
+// rows m = (b, hw) of channel c: a contiguous copy of g[b][c][:] per image
+__global__ void __launch_bounds__(256) stage_spatial_kernel(const float* __restrict__ g, int C, int HW,
+                                                            __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
+  const int c = blockIdx.y, b = blockIdx.x;
   const int64_t plane = int64_t(C) * Mpad;
-  for (int64_t m = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; m < Mpad; m += int64_t(gridDim.x) * blockDim.x) {
-    float v = 0.f;
-    if (m < M) {
-      const int64_t b = m / HW, hw = m - b * HW;
-      v = __ldg(g + (b * C + c) * HW + hw);
+  const float* src = g + (int64_t(b) * C + c) * HW;
+  const int64_t row = int64_t(c) * Mpad + int64_t(b) * HW;
+  if (((int64_t(b) * HW) & 1) == 0 && (HW & 1) == 0) {
+    for (int q = 2 * threadIdx.x; q < HW; q += 2 * blockDim.x) {
+      const float2 v = *reinterpret_cast<const float2*>(src + q);
+      store_split2(xt, plane, row + q, v.x, v.y);
     }
-    __nv_bfloat16 h, l;
-    split_bf16(v, h, l);
-    xt[c * Mpad + m] = h;
-    xt[plane + c * Mpad + m] = l;
+  } else {
+    for (int q = threadIdx.x; q < HW; q += blockDim.x) {
+      __nv_bfloat16 h, l;
+      split_bf16(src[q], h, l);
+      xt[row + q] = h;
+      xt[plane + row + q] = l;
+    }
+  }
+}
+
+// zero the K padding columns [M, Mpad) of every row (once per plan; never written by staging)
+__global__ void zero_pad_kernel(__nv_bfloat16* xt, int64_t d, int64_t M, int64_t Mpad) {
+  const int64_t r = blockIdx.x;
+  for (int64_t m = M + threadIdx.x; m < Mpad; m += blockDim.x) {
+    xt[r * Mpad + m] = __float2bfloat16(0.f);
+    xt[d * Mpad + r * Mpad + m] = __float2bfloat16(0.f);
   }
 }
 
@@ -173,9 +224,10 @@ FactorLayout factor_layout(int64_t M, int64_t d) {
   L.T = int(cdiv(d, 128));
   L.n_tiles = L.T * (L.T + 1) / 2;
   const int64_t nkb = L.Mpad / 64;
-  // split K so that the launch has >= ~2 waves of 148 SMs, each slice >= 4 K blocks
-  int64_t want = cdiv(2 * 148, L.n_tiles);
-  int64_t maxs = std::max<int64_t>(1, nkb / 4);
+  // split K so that the launch fills ~148 SMs, each slice >= 16 K blocks (1024 rows);
+  // splits == 1 stores straight into the packed buffer from the tile epilogue
+  int64_t want = cdiv(148, L.n_tiles);
+  int64_t maxs = std::max<int64_t>(1, nkb / 16);
   L.splits = int(std::max<int64_t>(1, std::min(want, maxs)));
   return L;
 }
@@ -183,7 +235,7 @@ FactorLayout factor_layout(int64_t M, int64_t d) {
 size_t factor_ws(const FactorLayout& L, Carve* c) {
   Carve& cv = *c;
   cv.take<__nv_bfloat16>(size_t(2) * L.d * L.Mpad);
-  cv.take<float>(size_t(L.n_tiles) * L.splits * 16384);
+  cv.take<float>(L.splits > 1 ? size_t(L.n_tiles) * L.splits * 16384 : 1);
   cv.take<CUtensorMap>(1, 128);
   cv.take<TcItem>(size_t(L.n_tiles) * L.splits);
   cv.take<TcEpi>(1);
@@ -222,7 +274,7 @@ int spdkfac_factor_plan_create(spdkfac_factor_plan** out, const spdkfac_factor_g
   p->splits = L.splits;
   p->n_items = L.n_tiles * L.splits;
   p->xt = c.take<__nv_bfloat16>(size_t(2) * d * L.Mpad);
-  p->partial = c.take<float>(size_t(L.n_tiles) * L.splits * 16384);
+  p->partial = c.take<float>(L.splits > 1 ? size_t(L.n_tiles) * L.splits * 16384 : 1);
   p->maps = c.take<CUtensorMap>(1, 128);
   p->items = c.take<TcItem>(size_t(p->n_items));
   p->epis = c.take<TcEpi>(1);
@@ -255,15 +307,25 @@ int spdkfac_factor_plan_create(spdkfac_factor_plan** out, const spdkfac_factor_g
         it.nk = int(kb1 - kb0);
         it.epi = 0;
         it.flags = (I == J) ? kSameAB : 0;
-        it.out_r = 0;
-        it.out_c = (tile_idx * L.splits + s2) * 128;
-        it.m_valid = 128;
-        it.n_valid = 128;
+        if (L.splits > 1) {  // partial tile -> workspace slot, reduced by reduce_pack_kernel
+          it.out_r = 0;
+          it.out_c = (tile_idx * L.splits + s2) * 128;
+        } else {             // direct packed-upper epilogue
+          it.out_r = I * 128;
+          it.out_c = J * 128;
+        }
+        it.m_valid = int(std::min<int64_t>(128, d - int64_t(I) * 128));
+        it.n_valid = int(std::min<int64_t>(128, d - int64_t(J) * 128));
         items.push_back(it);
       }
     }
   std::vector<TcEpi> epis(1);
-  epis[0] = TcEpi{p->partial, 128, 0, 1.f, 0.f, kAxpby, 0};
+  epis[0] = L.splits > 1 ? TcEpi{p->partial, 128, 0, 1.f, 0.f, kAxpby, 0}
+                         : TcEpi{nullptr, 0, 0, 1.f, 0.f, kPackedUpper, 0};
+  if (L.Mpad > M) {
+    zero_pad_kernel<<<unsigned(d), 64, 0, s>>>(p->xt, d, M, L.Mpad);
+    SPD_CHECK_LAUNCH();
+  }
   if ((rc = upload(p->maps, maps, s)) || (rc = upload(p->items, items, s)) || (rc = upload(p->epis, epis, s))) {
     delete p;
     return rc;
@@ -277,6 +339,7 @@ int spdkfac_factor_plan_run(spdkfac_factor_plan* p, const float* x, float scale,
   SPD_ARG(p && x && packed, SPDKFAC_ERR_ARG, "null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const spdkfac_factor_geom& g = p->g;
+  stat_begin(kCatFactorStage, s);
   if (g.layout == SPDKFAC_ROWS) {
     dim3 grid(unsigned(cdiv(p->Mpad, 32)), unsigned(cdiv(p->d, 32)));
     stage_rows_kernel<<<grid, dim3(32, 8), 0, s>>>(x, p->M, p->d, g.w, p->xt, p->Mpad);
@@ -286,19 +349,29 @@ int spdkfac_factor_plan_run(spdkfac_factor_plan* p, const float* x, float scale,
     geom_dims(&g, &rows, &dim, &Ho, &Wo);
     ConvGeom cg{int(g.n), int(g.c), int(g.h), int(g.w), Ho, Wo, g.kh, g.kw, g.stride_h, g.stride_w,
                 g.pad_h, g.pad_w, g.dil_h, g.dil_w};
-    dim3 grid(unsigned(std::min<int64_t>(cdiv(p->Mpad, 256), 64)), unsigned(p->d));
-    stage_im2col_kernel<<<grid, 256, 0, s>>>(x, cg, p->M, p->d, p->xt, p->Mpad);
+    const int hwo = Ho * Wo;
+    dim3 grid(unsigned(g.n), unsigned(p->d));
+    stage_im2col_kernel<<<grid, hwo >= 512 ? 256 : (hwo >= 128 ? 64 : 32), 0, s>>>(x, cg, p->M, p->d, p->xt, p->Mpad);
   } else {
-    dim3 grid(unsigned(std::min<int64_t>(cdiv(p->Mpad, 256), 64)), unsigned(p->d));
-    stage_spatial_kernel<<<grid, 256, 0, s>>>(x, int(g.n), int(g.c), g.h * g.w, p->M, p->xt, p->Mpad);
+    const int hw = int(g.h * g.w);
+    dim3 grid(unsigned(g.n), unsigned(p->d));
+    stage_spatial_kernel<<<grid, hw >= 512 ? 256 : (hw >= 128 ? 64 : 32), 0, s>>>(x, int(g.c), hw, p->xt, p->Mpad);
   }
   SPD_CHECK_LAUNCH();
-  int rc = launch_tc3(Kind::BF16, p->maps, p->items, p->epis, p->n_items, s);
+  stat_end(kCatFactorStage, s, 0, double(p->M) * p->d * 4 + 4.0 * p->d * p->Mpad);
+  // algorithmic work of one factor: M * d * (d + 1) flops (upper triangle incl. diagonal)
+  stat_begin(kCatFactorSyrk, s);
+  TcRun run{packed, p->d, scale, decay, world_scale, 0};
+  int rc = launch_tc3(Kind::BF16, p->maps, p->items, p->epis, p->n_items, s, run);
   if (rc) return rc;
+  stat_end(kCatFactorSyrk, s, double(p->M) * p->d * (p->d + 1), 4.0 * p->d * p->Mpad);
+  if (p->splits == 1) return SPDKFAC_OK;
   dim3 rgrid(4, 4, unsigned(p->T * p->T));
+  stat_begin(kCatFactorReduce, s);
   reduce_pack_kernel<<<rgrid, dim3(32, 8), 0, s>>>(p->partial, p->d, p->T, p->splits, scale, decay, world_scale,
                                                    packed);
   SPD_CHECK_LAUNCH();
+  stat_end(kCatFactorReduce, s, 0, 65536.0 * p->n_items + 4.0 * p->d * (p->d + 1) / 2 * (decay == 0.f ? 1 : 2));
   return SPDKFAC_OK;
 }
 

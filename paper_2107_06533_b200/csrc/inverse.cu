@@ -34,33 +34,49 @@ struct InvMat {
   int32_t pad_;
 };
 
-// In-shared-memory scalar sweep of an n x n block (n <= 128, row stride kSmemLd).
-// Returns -1 on success or the failing local pivot.
-__device__ int sweep_block(float* s, int n, float* rowk, float* colk) {
-  __shared__ int fail;
+// Register-resident scalar sweep of one 128 x 128 block by 512 threads: thread t owns
+// row i = t >> 2, columns [32q, 32q + 32), q = t & 3, in registers.  Per pivot k the four
+// owners of row k publish it to shared memory (double-buffered by k parity, rows skewed by
+// 4 floats per 32 so the four column quarters hit distinct banks); every thread then
+// applies  a_ij -= (a_ik / p) a_kj,  a_ik <- a_ik / p,  a_kj <- a_kj / p,  a_kk <- -1/p,
+// using a_ik = a_ki (the swept block stays symmetric to rounding).  Rows/columns >= n are
+// identity padding and are never pivots.  Returns -1, or the failing pivot (uniform).
+constexpr int kRowSkew = 36;  // skewed row buffer: element j at (j >> 5) * 36 + (j & 31)
+
+__device__ __forceinline__ int sweep128(float (&a)[32], int n, float* rbuf /* 2 x 4*36 */) {
+  const int t = threadIdx.x, i = t >> 2, q = t & 3;
   for (int k = 0; k < n; ++k) {
-    for (int t = threadIdx.x; t < n; t += blockDim.x) {
-      rowk[t] = s[k * kSmemLd + t];
-      colk[t] = s[t * kSmemLd + k];
+    float* rk = rbuf + (k & 1) * (4 * kRowSkew);
+    if (i == k) {
+#pragma unroll
+      for (int jj = 0; jj < 32; jj += 4)
+        *reinterpret_cast<float4*>(rk + q * kRowSkew + jj) = make_float4(a[jj], a[jj + 1], a[jj + 2], a[jj + 3]);
     }
     __syncthreads();
-    const float p = rowk[k];
-    if (!(p > 0.f)) {  // catches NaN like dpotrf's disnan check
-      return k;
-    }
+    const float p = rk[(k >> 5) * kRowSkew + (k & 31)];
+    if (!(p > 0.f)) return k;  // dpotrf's "ajj <= 0 or NaN" test, on the same Schur pivots
     const float pinv = 1.0f / p;
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-      const int i = e / n, j = e - i * n;
-      float v;
-      if (i == k && j == k) v = -pinv;
-      else if (i == k) v = rowk[j] * pinv;
-      else if (j == k) v = colk[i] * pinv;
-      else v = s[i * kSmemLd + j] - colk[i] * rowk[j] * pinv;
-      s[i * kSmemLd + j] = v;
+    const float ci = rk[(i >> 5) * kRowSkew + (i & 31)] * pinv;  // a_ik / p
+    const int kq = k >> 5, kj = k & 31;
+    if (i == k) {
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) a[jj] = (q == kq && jj == kj) ? -pinv : a[jj] * pinv;
+    } else {
+#pragma unroll
+      for (int jj = 0; jj < 32; jj += 4) {
+        const float4 r = *reinterpret_cast<const float4*>(rk + q * kRowSkew + jj);
+        a[jj + 0] = fmaf(-ci, r.x, a[jj + 0]);
+        a[jj + 1] = fmaf(-ci, r.y, a[jj + 1]);
+        a[jj + 2] = fmaf(-ci, r.z, a[jj + 2]);
+        a[jj + 3] = fmaf(-ci, r.w, a[jj + 3]);
+      }
+      if (q == kq) {  // column k: a_ik <- a_ik / p
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj)
+          if (jj == kj) a[jj] = ci;
+      }
     }
-    __syncthreads();
   }
-  (void)fail;
   return -1;
 }
 
@@ -72,26 +88,30 @@ __device__ __forceinline__ float packed_at(const float* p, int64_t d, int64_t i,
 // ---------------------------------------------------------------- d <= 128
 __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __restrict__ mats,
                                                             const int32_t* __restrict__ ids, float gamma) {
-  extern __shared__ float sm[];
-  float* s = sm;
-  float* rowk = s + kB * kSmemLd;
-  float* colk = rowk + kB;
+  __shared__ __align__(16) float rbuf[2 * 4 * kRowSkew];
   const InvMat m = mats[ids[blockIdx.x]];
   const int n = m.d;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e / n, j = e - i * n;
-    s[i * kSmemLd + j] = packed_at(m.in, n, i, j) + (i == j ? gamma : 0.f);
+  const int i = threadIdx.x >> 2, q = threadIdx.x & 3;
+  float a[32];
+#pragma unroll
+  for (int jj = 0; jj < 32; ++jj) {
+    const int j = q * 32 + jj;
+    a[jj] = (i < n && j < n) ? packed_at(m.in, n, i, j) + (i == j ? gamma : 0.f) : (i == j ? 1.f : 0.f);
   }
-  __syncthreads();
-  const int f = sweep_block(s, n, rowk, colk);
+  const int f = sweep128(a, n, rbuf);
   if (f >= 0) {
     if (threadIdx.x == 0) *m.info = f + 1;
     return;
   }
   if (threadIdx.x == 0) *m.info = 0;
+  // out = -(S + S^T)/2 through shared memory (uniform control flow)
+  extern __shared__ float sm[];
+#pragma unroll
+  for (int jj = 0; jj < 32; ++jj) sm[i * kSmemLd + q * 32 + jj] = -a[jj];
+  __syncthreads();
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e / n, j = e - i * n;
-    m.out[int64_t(i) * n + j] = -0.5f * (s[i * kSmemLd + j] + s[j * kSmemLd + i]);
+    const int r = e / n, c = e - r * n;
+    m.out[e] = 0.5f * (sm[r * kSmemLd + c] + sm[c * kSmemLd + r]);
   }
 }
 
@@ -111,28 +131,29 @@ __global__ void damp_unpack_kernel(const InvMat* __restrict__ mats, const int32_
 
 __global__ void __launch_bounds__(512) pivot_kernel(const InvMat* __restrict__ mats,
                                                     const int32_t* __restrict__ ids, int k) {
-  extern __shared__ float sm[];
-  float* s = sm;
-  float* rowk = s + kB * kSmemLd;
-  float* colk = rowk + kB;
+  __shared__ __align__(16) float rbuf[2 * 4 * kRowSkew];
   const InvMat m = mats[ids[blockIdx.x]];
   if (*m.info != 0) return;
   const int64_t dp = m.dp, K0 = int64_t(k) * kB;
-  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
-    const int i = e / kB, j = e % kB;
-    s[i * kSmemLd + j] = m.W[(K0 + i) * dp + K0 + j];
+  const int i = threadIdx.x >> 2, q = threadIdx.x & 3;
+  float a[32];
+  const float* src = m.W + (K0 + i) * dp + K0 + q * 32;
+#pragma unroll
+  for (int jj = 0; jj < 32; jj += 4) {
+    const float4 v = *reinterpret_cast<const float4*>(src + jj);
+    a[jj] = v.x, a[jj + 1] = v.y, a[jj + 2] = v.z, a[jj + 3] = v.w;
   }
-  __syncthreads();
-  const int f = sweep_block(s, kB, rowk, colk);
+  const int f = sweep128(a, kB, rbuf);
   if (f >= 0) {
     if (threadIdx.x == 0) *m.info = int(K0) + f + 1;
     return;
   }
-  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
-    const int i = e / kB, j = e % kB;
-    const float v = s[i * kSmemLd + j];  // = -P^-1
-    m.W[(K0 + i) * dp + K0 + j] = v;
-    m.pinv[e] = -v;
+  float* dst = m.W + (K0 + i) * dp + K0 + q * 32;  // W[K,K] <- -P^-1
+  float* pv = m.pinv + i * kB + q * 32;             // P^-1
+#pragma unroll
+  for (int jj = 0; jj < 32; jj += 4) {
+    *reinterpret_cast<float4*>(dst + jj) = make_float4(a[jj], a[jj + 1], a[jj + 2], a[jj + 3]);
+    *reinterpret_cast<float4*>(pv + jj) = make_float4(-a[jj], -a[jj + 1], -a[jj + 2], -a[jj + 3]);
   }
 }
 
@@ -182,6 +203,7 @@ __global__ void __launch_bounds__(256) panel_kernel(const InvMat* __restrict__ m
 #pragma unroll
       for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(av[r], pv[c], acc[r][c]);
   }
+  __syncthreads();  // all reads of `a` done: reuse it to stage C for the transposed store
 #pragma unroll
   for (int r = 0; r < 8; ++r)
 #pragma unroll
@@ -189,12 +211,17 @@ __global__ void __launch_bounds__(256) panel_kernel(const InvMat* __restrict__ m
       const int i = ty * 8 + r, j = tx + 16 * c;
       const float v = acc[r][c];
       m.W[(R0 + i) * dp + K0 + j] = v;  // A_ik <- A_ik P^-1
-      m.W[(K0 + j) * dp + R0 + i] = v;  // A_ki <- P^-1 A_ki
+      a[j * kSmemLd + i] = v;           // staged transposed
       float h, l;
       split_tf32(v, h, l);
       panC[(prow + i) * kB + j] = h;
       panC[plane + (prow + i) * kB + j] = l;
     }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {  // A_ki <- P^-1 A_ki, coalesced along i
+    const int j = e / kB, i = e % kB;
+    m.W[(K0 + j) * dp + R0 + i] = a[j * kSmemLd + i];
+  }
 }
 
 __global__ void finalize_kernel(const InvMat* __restrict__ mats, const int32_t* __restrict__ ids) {
@@ -214,6 +241,8 @@ using namespace spd;
 struct spdkfac_inverse_plan {
   int n;
   std::vector<int32_t> dims;
+  double small_flops = 0;       // sum d^3 of the shared-memory path (algorithmic potrf+potri)
+  double algo_flops = 0;        // sum d^3 over all matrices
   InvMat* mats;                 // device
   int32_t* small_ids;           // device
   int n_small;
@@ -331,6 +360,11 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     mats[t].info = info_dev + t;
   }
   p->n_small = int(small.size());
+  for (int t = 0; t < n; ++t) {
+    const double d3 = double(dims[t]) * dims[t] * dims[t];
+    p->algo_flops += d3;
+    if (dims[t] <= kB) p->small_flops += d3;
+  }
   p->n_blocked = int(blocked.size());
   // per-step schedules
   std::vector<int32_t> piv_ids;
@@ -390,9 +424,7 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   }
   static bool attrs = false;
   if (!attrs) {
-    const int sm_small = (kB * kSmemLd + 2 * kB) * 4;
-    SPD_CUDA(cudaFuncSetAttribute(small_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_small));
-    SPD_CUDA(cudaFuncSetAttribute(pivot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_small));
+    SPD_CUDA(cudaFuncSetAttribute(small_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kB * kSmemLd * 4));
     SPD_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kB * kSmemLd * 4));
     attrs = true;
   }
@@ -404,29 +436,40 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
   SPD_ARG(p != nullptr, SPDKFAC_ERR_ARG, "null plan");
   SPD_ARG(gamma >= 0.f, SPDKFAC_ERR_ARG, "damping must be nonnegative, got %g", double(gamma));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int sm_small = (kB * kSmemLd + 2 * kB) * 4;
   if (p->n_small > 0) {
-    small_inverse_kernel<<<p->n_small, 512, sm_small, s>>>(p->mats, p->small_ids, gamma);
+    stat_begin(kCatInvSmall, s);
+    small_inverse_kernel<<<p->n_small, 512, kB * kSmemLd * 4, s>>>(p->mats, p->small_ids, gamma);
     SPD_CHECK_LAUNCH();
+    stat_end(kCatInvSmall, s, p->small_flops, 0);
   }
   if (p->n_blocked > 0) {
+    stat_begin(kCatInvUnpackFinal, s);
     damp_unpack_kernel<<<dim3(64, p->n_blocked), 256, 0, s>>>(p->mats, p->blocked_ids, gamma);
     SPD_CHECK_LAUNCH();
+    stat_end(kCatInvUnpackFinal, s, 0, 0);
     for (int k = 0; k < p->steps; ++k) {
       if (p->piv_cnt[k] > 0) {
-        pivot_kernel<<<p->piv_cnt[k], 512, sm_small, s>>>(p->mats, p->piv_ids + p->piv_off[k], k);
+        stat_begin(kCatInvPivot, s);
+        pivot_kernel<<<p->piv_cnt[k], 512, 0, s>>>(p->mats, p->piv_ids + p->piv_off[k], k);
         SPD_CHECK_LAUNCH();
+        stat_end(kCatInvPivot, s, 2.0 * kB * kB * kB * p->piv_cnt[k], 0);
       }
       if (p->pan_cnt[k] > 0) {
+        stat_begin(kCatInvPanel, s);
         panel_kernel<<<p->pan_cnt[k], 256, 2 * kB * kSmemLd * 4, s>>>(p->mats, p->pan_jobs + p->pan_off[k], k,
                                                                         p->panA, p->panC, p->plane_rows);
         SPD_CHECK_LAUNCH();
+        stat_end(kCatInvPanel, s, 2.0 * kB * kB * kB * p->pan_cnt[k], 0);
       }
+      stat_begin(kCatInvUpdate, s);
       int rc = launch_tc3(Kind::TF32, p->maps, p->items + p->upd_off[k], p->epis, p->upd_cnt[k], s);
       if (rc) return rc;
+      stat_end(kCatInvUpdate, s, 2.0 * kB * kB * kB * p->upd_cnt[k], 0);
     }
+    stat_begin(kCatInvUnpackFinal, s);
     finalize_kernel<<<dim3(64, p->n_blocked), 256, 0, s>>>(p->mats, p->blocked_ids);
     SPD_CHECK_LAUNCH();
+    stat_end(kCatInvUnpackFinal, s, 0, 0);
   }
   return SPDKFAC_OK;
 }

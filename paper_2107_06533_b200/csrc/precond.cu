@@ -121,8 +121,10 @@ int run_split(int n, const float* const* src, const std::vector<__nv_bfloat16*>&
       r += rows[l];
     }
     a.row0[a.n] = r;
+    stat_begin(kCatPrecSplit, s);
     split_rows_batched_kernel<<<r, 256, 0, s>>>(a);
     SPD_CHECK_LAUNCH();
+    stat_end(kCatPrecSplit, s, 0, 0);
   }
   return SPDKFAC_OK;
 }
@@ -232,8 +234,18 @@ int spdkfac_precond_plan_run(spdkfac_precond_plan* p, const float* const* g_inv,
       (rc = run_split(n, a_inv, p->aI, p->d_in, p->d_in, ldi, s)) ||
       (rc = run_split(n, g_inv, p->gI, p->d_out, p->d_out, ldo, s)))
     return rc;
+  // algorithmic work: 2 g a (a + g) per layer, split over the two GEMMs
+  double f1 = 0, f2 = 0;
+  for (int l = 0; l < n; ++l) {
+    f1 += 2.0 * p->d_out[l] * p->d_in[l] * p->d_in[l];
+    f2 += 2.0 * p->d_out[l] * p->d_out[l] * p->d_in[l];
+  }
+  stat_begin(kCatPrecGemm, s);
   if ((rc = launch_tc3(Kind::BF16, p->maps, p->items1, p->epis, p->n1, s))) return rc;
+  stat_end(kCatPrecGemm, s, f1, 0);
+  stat_begin(kCatPrecGemm, s);
   if ((rc = launch_tc3(Kind::BF16, p->maps, p->items2, p->epis, p->n2, s))) return rc;
+  stat_end(kCatPrecGemm, s, f2, 0);
   if (!weight && !precond_out) return SPDKFAC_OK;
   for (int off = 0; off < n; off += kMaxPtrs) {
     ApplyArgs a{};
@@ -245,8 +257,10 @@ int spdkfac_precond_plan_run(spdkfac_precond_plan* p, const float* const* g_inv,
       a.out[t] = precond_out ? precond_out[l] : nullptr;
       a.n_el[t] = int64_t(p->d_out[l]) * p->d_in[l];
     }
+    stat_begin(kCatPrecApply, s);
     apply_update_kernel<<<dim3(64, a.n), 256, 0, s>>>(a, alpha);
     SPD_CHECK_LAUNCH();
+    stat_end(kCatPrecApply, s, 0, 0);
   }
   return SPDKFAC_OK;
 }

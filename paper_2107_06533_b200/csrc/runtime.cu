@@ -1,5 +1,6 @@
 // Runtime: error reporting, driver entry point for tensor-map encoding, GEMM launch,
 // packed <-> full symmetric layout kernels.
+#include <atomic>
 #include <cstdarg>
 #include <mutex>
 
@@ -14,6 +15,51 @@ void set_error(const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+
+// ------------------------------------------------------------------ launch accounting
+namespace {
+struct StatRec {
+  cudaEvent_t a = nullptr, b = nullptr;
+  int cat = 0;
+  double flops = 0, bytes = 0;
+};
+std::mutex g_stat_mu;
+std::vector<StatRec> g_recs;
+size_t g_rec_used = 0;
+bool g_timing = false;
+std::atomic<uint64_t> g_launches{0};
+uint64_t g_cat_launches[kNumCats] = {};
+double g_cat_flops[kNumCats] = {}, g_cat_bytes[kNumCats] = {};
+thread_local long g_open = -1;
+}  // namespace
+
+void stat_begin(int cat, cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_timing) return;
+  std::lock_guard<std::mutex> lk(g_stat_mu);
+  if (g_rec_used == g_recs.size()) {
+    StatRec r;
+    cudaEventCreate(&r.a);
+    cudaEventCreate(&r.b);
+    g_recs.push_back(r);
+  }
+  g_open = long(g_rec_used++);
+  g_recs[g_open].cat = cat;
+  cudaEventRecord(g_recs[g_open].a, s);
+}
+
+void stat_end(int cat, cudaStream_t s, double flops, double bytes) {
+  std::lock_guard<std::mutex> lk(g_stat_mu);
+  g_cat_launches[cat] += 1;
+  g_cat_flops[cat] += flops;
+  g_cat_bytes[cat] += bytes;
+  if (g_timing && g_open >= 0) {
+    g_recs[g_open].flops = flops;
+    g_recs[g_open].bytes = bytes;
+    cudaEventRecord(g_recs[g_open].b, s);
+    g_open = -1;
+  }
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -51,21 +97,23 @@ int make_operand_map(CUtensorMap* out, const void* base, bool bf16, int64_t k_ex
 }
 
 template <Kind K>
-static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s) {
+static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
+                       const TcRun& run) {
   static bool attr_set = false;
   if (!attr_set) {
     SPD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmemBytes)));
     attr_set = true;
   }
-  tc3_gemm_kernel<K><<<n, 128, kTcSmemBytes, s>>>(maps, items, epis);
+  tc3_gemm_kernel<K><<<n, 128, kTcSmemBytes, s>>>(maps, items, epis, run);
   SPD_CHECK_LAUNCH();
   return SPDKFAC_OK;
 }
 
-int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s) {
+int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
+               const TcRun& run) {
   if (n <= 0) return SPDKFAC_OK;
-  return kind == Kind::BF16 ? launch_kind<Kind::BF16>(maps, items, epis, n, s)
-                            : launch_kind<Kind::TF32>(maps, items, epis, n, s);
+  return kind == Kind::BF16 ? launch_kind<Kind::BF16>(maps, items, epis, n, s, run)
+                            : launch_kind<Kind::TF32>(maps, items, epis, n, s, run);
 }
 
 // ------------------------------------------------------------------ pack / unpack
@@ -127,8 +175,10 @@ static int pack_batched(int n, const int32_t* dims, const float* const* src, flo
       rows += dims[off + t];
     }
     a.row0[a.n] = rows;
+    stat_begin(kCatPack, s);
     pack_batched_kernel<<<dim3(1, rows), 256, 0, s>>>(a, unpack);
     SPD_CHECK_LAUNCH();
+    stat_end(kCatPack, s, 0, 0);
   }
   return SPDKFAC_OK;
 }
@@ -142,6 +192,34 @@ extern "C" {
 const char* spdkfac_last_error(void) { return g_err; }
 int spdkfac_version(void) { return 100; }
 
+void spdkfac_stats_reset(int timing) {
+  std::lock_guard<std::mutex> lk(g_stat_mu);
+  g_rec_used = 0;
+  g_timing = timing != 0;
+  g_launches.store(0);
+  for (int c = 0; c < kNumCats; ++c) g_cat_launches[c] = 0, g_cat_flops[c] = 0, g_cat_bytes[c] = 0;
+}
+
+uint64_t spdkfac_stats_launches(void) { return g_launches.load(); }
+
+int spdkfac_stats_read(int cat, double* ms, int64_t* launches, double* flops, double* bytes) {
+  SPD_ARG(cat >= 0 && cat < kNumCats, SPDKFAC_ERR_ARG, "bad stats category");
+  std::lock_guard<std::mutex> lk(g_stat_mu);
+  double t = 0;
+  for (size_t i = 0; i < g_rec_used; ++i) {
+    if (g_recs[i].cat != cat) continue;
+    float e = 0;
+    SPD_CUDA(cudaEventSynchronize(g_recs[i].b));
+    SPD_CUDA(cudaEventElapsedTime(&e, g_recs[i].a, g_recs[i].b));
+    t += e;
+  }
+  if (ms) *ms = t;
+  if (launches) *launches = int64_t(g_cat_launches[cat]);
+  if (flops) *flops = g_cat_flops[cat];
+  if (bytes) *bytes = g_cat_bytes[cat];
+  return SPDKFAC_OK;
+}
+
 int spdkfac_device_supported(void) {
   int dev = 0, major = 0, minor = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
@@ -154,8 +232,10 @@ int spdkfac_pack_upper_f32(const float* full, int64_t d, int64_t ld, float* pack
   SPD_ARG(d >= 1, SPDKFAC_ERR_ARG, "dimension must be >= 1");
   SPD_ARG(ld >= d && full && packed, SPDKFAC_ERR_ARG, "bad pack arguments");
   dim3 grid(unsigned(std::min<int64_t>(cdiv(d, 256), 16)), unsigned(d));
+  stat_begin(kCatPack, static_cast<cudaStream_t>(stream));
   pack_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(full, d, ld, packed);
   SPD_CHECK_LAUNCH();
+  stat_end(kCatPack, static_cast<cudaStream_t>(stream), 0, 8.0 * d * (d + 1) / 2);
   return SPDKFAC_OK;
 }
 
@@ -163,8 +243,10 @@ int spdkfac_unpack_upper_f32(const float* packed, int64_t d, float* full, int64_
   SPD_ARG(d >= 1, SPDKFAC_ERR_ARG, "dimension must be >= 1");
   SPD_ARG(ld >= d && full && packed, SPDKFAC_ERR_ARG, "bad unpack arguments");
   dim3 grid(unsigned(std::min<int64_t>(cdiv(d, 256), 16)), unsigned(d));
+  stat_begin(kCatPack, static_cast<cudaStream_t>(stream));
   unpack_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(packed, d, full, ld);
   SPD_CHECK_LAUNCH();
+  stat_end(kCatPack, static_cast<cudaStream_t>(stream), 0, 4.0 * d * d);
   return SPDKFAC_OK;
 }
 

@@ -78,6 +78,16 @@ struct PtrTable {
 };
 
 int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items,
-               cudaStream_t s);
+               cudaStream_t s, const TcRun& run = TcRun{});
+
+// Launch accounting (include/spdkfac.h spdkfac_stats_*): every kernel launch of the
+// library is counted; with timing enabled each launch is bracketed by CUDA events on
+// its own stream and attributed to a category with its algorithmic flop count.
+enum StatCat : int {
+  kCatFactorStage = 0, kCatFactorSyrk, kCatFactorReduce, kCatInvSmall, kCatInvPivot, kCatInvPanel, kCatInvUpdate,
+  kCatInvUnpackFinal, kCatPrecSplit, kCatPrecGemm, kCatPrecApply, kCatPack, kNumCats
+};
+void stat_begin(int cat, cudaStream_t s);
+void stat_end(int cat, cudaStream_t s, double flops, double bytes);
 
 }  // namespace spd

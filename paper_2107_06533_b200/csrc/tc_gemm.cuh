@@ -35,6 +35,18 @@ enum EpiMode : int32_t {
   kAxpby = 0,      // out = beta*out + alpha*D   (fp32 target)
   kSplitBf16 = 1,  // out planes (bf16) <- split(alpha*D)
   kSplitTf32 = 2,  // out planes (fp32, tf32-exact) <- split(alpha*D)
+  kPackedUpper = 3,  // packed upper triangle of a d x d symmetric target (run.out, run.d):
+                     //   P = run.wscale * (run.decay * P + (1 - run.decay) * run.alpha * D), i <= j only
+};
+
+// Per-launch arguments (kernel parameters, not table entries): what changes between runs.
+struct TcRun {
+  void* out;     // kPackedUpper target (packed buffer)
+  int64_t d;     // matrix dimension of the packed target
+  float alpha;   // scale of D (1/M for factors)
+  float decay;   // running-average weight of the old value (0: never read)
+  float wscale;  // final scale (1/P)
+  int32_t pad_;
 };
 
 struct TcEpi {
@@ -49,7 +61,7 @@ struct TcEpi {
 template <Kind K>
 __global__ void __launch_bounds__(128, 1)
     tc3_gemm_kernel(const CUtensorMap* __restrict__ maps, const TcItem* __restrict__ items,
-                    const TcEpi* __restrict__ epis) {
+                    const TcEpi* __restrict__ epis, const TcRun run) {
   constexpr int BK = (K == Kind::BF16) ? 64 : 32;  // one 128-byte swizzle row of K
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -125,7 +137,9 @@ __global__ void __launch_bounds__(128, 1)
     __syncwarp();
   }
 
-  // ---- epilogue: warp w owns TMEM lanes [32w, 32w+32) = tile rows
+  // ---- epilogue: warp w owns TMEM lanes [32w, 32w+32) = tile rows.  All global
+  // reads of a 32-column chunk are issued before any store (independent addresses),
+  // so read-modify-write targets cost one memory latency per chunk, not per element.
   const TcEpi ep = epis[it.epi];
   const int i = warp * 32 + lane;
   if (it.nk > 0) {
@@ -136,6 +150,7 @@ __global__ void __launch_bounds__(128, 1)
   const int64_t ri = int64_t(it.out_r) + i;
 #pragma unroll 1
   for (int c = 0; c < 4; ++c) {
+    if (c * 32 >= it.n_valid) break;  // warp-uniform
     float v[32];
     if (it.nk > 0) {
       tmem_ld_32x32b_x32(tmem + (uint32_t(warp * 32) << 16) + uint32_t(c * 32), v);
@@ -143,50 +158,68 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
       for (int t = 0; t < 32; ++t) v[t] = 0.f;
     }
+    const int jn = it.n_valid - c * 32;  // valid columns in this chunk (may exceed 32)
     if (ep.mode == kAxpby) {
       float* out = static_cast<float*>(ep.out);
+      float* base = out + (int64_t(it.out_c) + c * 32) * ep.ld + ri;  // transposed: column j -> row of target
+      float old[32];
+      if (ep.beta != 0.f) {
 #pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        const int j = c * 32 + t;
-        if (row_ok && j < it.n_valid) {
-          float* p = out + (int64_t(it.out_c) + j) * ep.ld + ri;
-          *p = (ep.beta == 0.f ? 0.f : ep.beta * *p) + ep.alpha * v[t];
-        }
+        for (int t = 0; t < 32; ++t) old[t] = (row_ok && t < jn) ? base[int64_t(t) * ep.ld] : 0.f;
       }
-      if (it.flags & kMirror) {
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int j = c * 32 + t;
-          if (row_ok && j < it.n_valid) {
-            float* p = out + ri * ep.ld + it.out_c + j;
-            *p = (ep.beta == 0.f ? 0.f : ep.beta * *p) + ep.alpha * v[t];
-          }
+      for (int t = 0; t < 32; ++t)
+        if (row_ok && t < jn) base[int64_t(t) * ep.ld] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + ep.alpha * v[t];
+      if (it.flags & kMirror) {  // same values, target row ri, 32 contiguous columns
+        float* rowp = out + ri * ep.ld + it.out_c + c * 32;
+        if (ep.beta != 0.f) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) old[t] = (row_ok && t < jn) ? rowp[t] : 0.f;
         }
+#pragma unroll
+        for (int t = 0; t < 32; ++t)
+          if (row_ok && t < jn) rowp[t] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + ep.alpha * v[t];
       }
     } else if (ep.mode == kSplitBf16) {
       __nv_bfloat16* out = static_cast<__nv_bfloat16*>(ep.out);
+      const int64_t o0 = (int64_t(it.out_c) + c * 32) * ep.ld + ri;
 #pragma unroll
       for (int t = 0; t < 32; ++t) {
-        const int j = c * 32 + t;
-        if (row_ok && j < it.n_valid) {
+        if (row_ok && t < jn) {
           __nv_bfloat16 h, l;
           split_bf16(ep.alpha * v[t], h, l);
-          const int64_t o = (int64_t(it.out_c) + j) * ep.ld + ri;
-          out[o] = h;
-          out[o + ep.plane_stride] = l;
+          out[o0 + int64_t(t) * ep.ld] = h;
+          out[o0 + int64_t(t) * ep.ld + ep.plane_stride] = l;
         }
       }
-    } else {
+    } else if (ep.mode == kSplitTf32) {
       float* out = static_cast<float*>(ep.out);
+      const int64_t o0 = (int64_t(it.out_c) + c * 32) * ep.ld + ri;
 #pragma unroll
       for (int t = 0; t < 32; ++t) {
-        const int j = c * 32 + t;
-        if (row_ok && j < it.n_valid) {
+        if (row_ok && t < jn) {
           float h, l;
           split_tf32(ep.alpha * v[t], h, l);
-          const int64_t o = (int64_t(it.out_c) + j) * ep.ld + ri;
-          out[o] = h;
-          out[o + ep.plane_stride] = l;
+          out[o0 + int64_t(t) * ep.ld] = h;
+          out[o0 + int64_t(t) * ep.ld + ep.plane_stride] = l;
+        }
+      }
+    } else {  // kPackedUpper: global row gi = out_r + i, columns gj = out_c + c*32 + t, keep gj >= gi
+      float* out = static_cast<float*>(run.out);
+      const int64_t gi = ri, d = run.d;
+      const int64_t gj0 = int64_t(it.out_c) + c * 32;
+      float* rowp = out + gi * (2 * d - gi + 1) / 2 - gi;  // packed index of (gi, gj) = rowp + gj
+      float old[32];
+      if (run.decay != 0.f) {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) old[t] = (row_ok && t < jn && gj0 + t >= gi) ? rowp[gj0 + t] : 0.f;
+      }
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        if (row_ok && t < jn && gj0 + t >= gi) {
+          const float fresh = run.alpha * v[t];
+          const float nv = run.decay != 0.f ? run.decay * old[t] + (1.f - run.decay) * fresh : fresh;
+          rowp[gj0 + t] = run.wscale * nv;
         }
       }
     }

@@ -1,0 +1,392 @@
+"""SPDKFAC: the B200-native SPD-KFAC optimizer step behind a torch.optim API.
+
+It executes the step the reference emulates in `dkfac_step`
+(pkg/src/kfacsched/emulator.py:211-263) on real ranks and real devices:
+
+  forward hooks   A_l = a^T a / M   per layer (im2col rows for convs), straight into
+                  the packed forward fusion buffer, running average + 1/P fused
+                  (factor kernels, factor side stream); each fusion group of the
+                  init-time plan (`plan_fusion`, planner.py:249-298) is all-reduced on
+                  the communication stream as soon as its last member is written
+  backward hooks  G_l = (b g)^T (b g) / M likewise into the backward fusion buffer
+  step()          gradient all-reduce; damped inverses of this rank's share of the
+                  load-balanced placement (`lbp_place`, planner.py:301-356), NCT tensors
+                  on every rank, CT inverses broadcast from their owners in packed form;
+                  W_l -= lr * G_l^-1 grad_l A_l^-1 for every K-FAC layer (plain SGD for
+                  the remaining parameters, as the reference has no bias: SPEC.md:418).
+
+Knobs: lr (alpha, emulator.py:207), damping (gamma, linalg.py:130), factor_decay
+(running-average rho; 0 reproduces the reference), factor_update_freq and
+inv_update_freq (the reference's single `kfac_update_interval`, simulator.py:126,
+split in two), fusion policy, placement mode ("lbp" | "seq" | "local").
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import torch
+import torch.nn as nn
+
+from . import _lib as L
+from .linalg import FactorPlan, InversePlan, NotPositiveDefiniteError, PrecondPlan
+from .perfmodel import PerfParams, default_params
+from .planner import (FactorKind, FusionPolicy, inverse_tasks, factor_tasks, lbp_place, local_place, plan_fusion,
+                      seq_place)
+
+
+@dataclass
+class LayerSpec:
+    """One preconditioned layer: factor dims and (estimated) pass times, the
+    shape of `kfacsched.profiles.LayerProfile` (profiles.py:53-86)."""
+
+    name: str
+    a_dim: int
+    g_dim: int
+    t_ff: float = 1e-5
+    t_bp: float = 2e-5
+    t_factorA: float = 1e-5
+    t_factorG: float = 1e-5
+
+
+@dataclass
+class _Layer:
+    index: int
+    name: str
+    module: nn.Module
+    is_conv: bool
+    spec: LayerSpec
+    a_off: int = 0
+    g_off: int = 0
+    a_plan: Optional[FactorPlan] = None
+    g_plan: Optional[FactorPlan] = None
+    a_key: tuple = ()
+    g_key: tuple = ()
+    handles: list = field(default_factory=list)
+
+
+def _conv_ok(m) -> bool:
+    return isinstance(m, nn.Conv2d) and m.groups == 1 and m.padding_mode == "zeros" and isinstance(m.padding, tuple)
+
+
+class SPDKFAC(torch.optim.Optimizer):
+    def __init__(self, model: nn.Module, lr: float = 0.1, damping: float = 0.1, factor_decay: float = 0.0,
+                 factor_update_freq: int = 1, inv_update_freq: int = 1, fusion: FusionPolicy = FusionPolicy.OPTIMAL,
+                 placement: str = "lbp", balance: str = "dim_sq", perf: Optional[PerfParams] = None,
+                 batch_averaged: bool = True, layer_times: Optional[dict] = None, comm=None):
+        if damping < 0:
+            raise ValueError(f"damping must be nonnegative, got {damping}")
+        if not 0.0 <= factor_decay < 1.0:
+            raise ValueError(f"factor_decay must be in [0, 1), got {factor_decay}")
+        if factor_update_freq < 1 or inv_update_freq < 1 or inv_update_freq % factor_update_freq:
+            raise ValueError("update frequencies must be >= 1 and inv_update_freq a multiple of factor_update_freq")
+        if placement not in ("lbp", "seq", "local"):
+            raise ValueError(f"placement must be 'lbp', 'seq' or 'local', got {placement!r}")
+        L.load(require_device=True)
+        self.model = model
+        self.damping, self.factor_decay = float(damping), float(factor_decay)
+        self.factor_update_freq, self.inv_update_freq = int(factor_update_freq), int(inv_update_freq)
+        self.batch_averaged = batch_averaged
+        self.perf = perf or default_params()
+        self.device = next(model.parameters()).device
+
+        import torch.distributed as dist
+        dist_on = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank() if dist_on else 0
+        self.world = dist.get_world_size() if dist_on else 1
+        if self.world > 1 and comm is None:
+            from .comm import NcclComm
+            comm = NcclComm(self.rank, self.world)
+        self.comm = comm
+
+        # ---- preconditioned layers, forward order (model definition order)
+        self.layers: list[_Layer] = []
+        kfac_params = set()
+        for name, m in model.named_modules():
+            if _conv_ok(m) or isinstance(m, nn.Linear):
+                conv = isinstance(m, nn.Conv2d)
+                a_dim = m.in_channels * m.kernel_size[0] * m.kernel_size[1] if conv else m.in_features
+                g_dim = m.out_channels if conv else m.out_features
+                t = (layer_times or {}).get(name, {})
+                spec = LayerSpec(name, a_dim, g_dim, **t) if t else self._estimate_times(name, a_dim, g_dim)
+                self.layers.append(_Layer(len(self.layers), name, m, conv, spec))
+                kfac_params.add(m.weight)
+        if not self.layers:
+            raise ValueError("model has no Conv2d/Linear layers to precondition")
+        params = list(model.parameters())
+        self.other_params = [p for p in params if p not in kfac_params and p.requires_grad]
+        super().__init__([{"params": params}], dict(lr=lr))
+
+        # ---- init-time plans (the paper's "executed during initialization")
+        specs = [l.spec for l in self.layers]
+        ff = [s.t_ff for s in specs]
+        bp = [s.t_bp for s in reversed(specs)]
+        self.fwd_plan = plan_fusion(factor_tasks(specs, FactorKind.A), ff, self.perf.allreduce, fusion)
+        self.bwd_plan = plan_fusion(factor_tasks(specs, FactorKind.G), bp, self.perf.allreduce, fusion)
+        tasks = inverse_tasks(specs)
+        if placement == "lbp":
+            self.placement = lbp_place(tasks, self.world, self.perf.inverse, self.perf.bcast, balance=balance)
+        elif placement == "seq":
+            self.placement = seq_place(tasks, self.world)
+        else:
+            self.placement = local_place(tasks, self.world)
+
+        # ---- packed fusion buffers: A in forward order, G in backward order
+        off = 0
+        for l in self.layers:
+            l.a_off, off = off, off + l.spec.a_dim * (l.spec.a_dim + 1) // 2
+        self.bufA = torch.zeros(off, dtype=torch.float32, device=self.device)
+        off = 0
+        for l in reversed(self.layers):
+            l.g_off, off = off, off + l.spec.g_dim * (l.spec.g_dim + 1) // 2
+        self.bufG = torch.zeros(off, dtype=torch.float32, device=self.device)
+        self._groups_fwd = self._group_slices(self.fwd_plan, FactorKind.A)
+        self._groups_bwd = self._group_slices(self.bwd_plan, FactorKind.G)
+
+        # ---- inverses (every rank holds all of them for preconditioning)
+        self.inv = []
+        for l in self.layers:
+            self.inv.append(torch.zeros(l.spec.a_dim, l.spec.a_dim, dtype=torch.float32, device=self.device))
+            self.inv.append(torch.zeros(l.spec.g_dim, l.spec.g_dim, dtype=torch.float32, device=self.device))
+        mine = list(self.placement.workers[self.rank])
+        self._mine = mine
+        self._inv_plan = InversePlan([self._packed(t) for t in mine], [self.inv[t] for t in mine]) if mine else None
+        self._bcast = self._bcast_layout()
+        self._precond = PrecondPlan([(l.spec.g_dim, l.spec.a_dim) for l in self.layers], device=self.device)
+
+        self.factor_stream = torch.cuda.Stream(self.device)
+        self.comm_stream = torch.cuda.Stream(self.device) if self.world > 1 else None
+        self._info_host = torch.zeros(len(mine), dtype=torch.int32, pin_memory=True) if mine else None
+        self._info_event = None
+        self.steps = 0
+        self._capture = True
+        self._factor_updates = 0
+        self._install_hooks()
+
+    # ------------------------------------------------------------------ setup helpers
+    @staticmethod
+    def _estimate_times(name, a_dim, g_dim) -> LayerSpec:
+        # rough shape-only estimates; only the relative readiness of factors matters to
+        # the OPTIMAL fusion criterion (planner.py:280-290).  Pass `layer_times` to override.
+        t_ff = 5e-6 + a_dim * g_dim * 2e-11
+        return LayerSpec(name, a_dim, g_dim, t_ff, 2 * t_ff, 3e-6 + a_dim * a_dim * 5e-12, 3e-6 + g_dim * g_dim * 5e-12)
+
+    def _packed(self, t: int) -> torch.Tensor:
+        l = self.layers[t // 2]
+        if t % 2 == 0:
+            d = l.spec.a_dim
+            return self.bufA[l.a_off:l.a_off + d * (d + 1) // 2]
+        d = l.spec.g_dim
+        return self.bufG[l.g_off:l.g_off + d * (d + 1) // 2]
+
+    def _group_slices(self, plan, kind):
+        """(last layer index of the group, start, end) per fusion group."""
+        out = []
+        for g in plan.groups:
+            idx = [t.layer_index - 1 for t in g]
+            if kind is FactorKind.A:
+                s = self.layers[idx[0]].a_off
+                last = self.layers[idx[-1]]
+                e = last.a_off + last.spec.a_dim * (last.spec.a_dim + 1) // 2
+            else:
+                s = self.layers[idx[0]].g_off
+                last = self.layers[idx[-1]]
+                e = last.g_off + last.spec.g_dim * (last.spec.g_dim + 1) // 2
+            out.append((idx[-1], s, e))
+        return {last: (s, e) for last, s, e in out}
+
+    def _bcast_layout(self):
+        """Per owner rank: its CT tensors (plan order) and a packed staging buffer."""
+        if self.world == 1:
+            return None
+        lay = []
+        for p, lst in enumerate(self.placement.workers):
+            ct = [t for t in lst if t not in self.placement.nct]
+            dims = [self.inv[t].shape[0] for t in ct]
+            n = sum(d * (d + 1) // 2 for d in dims)
+            buf = torch.empty(max(n, 1), dtype=torch.float32, device=self.device)
+            views, o = [], 0
+            for d in dims:
+                views.append(buf[o:o + d * (d + 1) // 2])
+                o += d * (d + 1) // 2
+            lay.append((ct, dims, buf, views, n))
+        return lay
+
+    def _install_hooks(self):
+        for l in self.layers:
+            l.handles.append(l.module.register_forward_pre_hook(self._make_a_hook(l)))
+            l.handles.append(l.module.register_forward_hook(self._make_out_hook(l)))
+
+    def remove_hooks(self):
+        for l in self.layers:
+            for h in l.handles:
+                h.remove()
+            l.handles.clear()
+
+    # ------------------------------------------------------------------ factor capture
+    def _factor_args(self):
+        decay = self.factor_decay if self._factor_updates > 0 else 0.0
+        return decay, 1.0 / self.world
+
+    def _launch_factor(self, l: _Layer, x: torch.Tensor, kind: str):
+        main = torch.cuda.current_stream(self.device)
+        fs = self.factor_stream
+        fs.wait_stream(main)
+        x = x.detach()
+        if x.dtype != torch.float32 or not x.is_contiguous():
+            with torch.cuda.stream(main):
+                x = x.to(torch.float32).contiguous()
+        decay, wscale = self._factor_args()
+        if kind == "A":
+            key = tuple(x.shape)
+            if l.a_key != key:
+                m = l.module
+                with torch.cuda.stream(fs):
+                    if l.is_conv:
+                        l.a_plan = FactorPlan(L.CONV_A, x.shape, m.kernel_size, m.stride, m.padding, m.dilation)
+                    else:
+                        l.a_plan = FactorPlan(L.ROWS, (x.numel() // x.shape[-1], x.shape[-1]))
+                l.a_key = key
+            plan, buf, off, d = l.a_plan, self.bufA, l.a_off, l.spec.a_dim
+            scale = 1.0 / plan.rows
+        else:
+            key = tuple(x.shape)
+            if l.g_key != key:
+                with torch.cuda.stream(fs):
+                    if l.is_conv:
+                        l.g_plan = FactorPlan(L.SPATIAL, x.shape)
+                    else:
+                        l.g_plan = FactorPlan(L.ROWS, (x.numel() // x.shape[-1], x.shape[-1]))
+                l.g_key = key
+            plan, buf, off, d = l.g_plan, self.bufG, l.g_off, l.spec.g_dim
+            b = x.shape[0] if self.batch_averaged else 1
+            scale = float(b * b) / plan.rows
+        packed = buf[off:off + d * (d + 1) // 2]
+        plan.run(x, packed, scale=scale, decay=decay, world_scale=wscale, stream=fs)
+        x.record_stream(fs)
+        groups = self._groups_fwd if kind == "A" else self._groups_bwd
+        if self.world > 1 and l.index in groups:
+            s, e = groups[l.index]
+            cs = self.comm_stream
+            cs.wait_stream(fs)
+            self.comm.allreduce_sum(buf[s:e], cs)
+
+    def _make_a_hook(self, l: _Layer):
+        def hook(module, inputs):
+            if self._capture and torch.is_grad_enabled() and module.training:
+                self._launch_factor(l, inputs[0], "A")
+        return hook
+
+    def _make_out_hook(self, l: _Layer):
+        def hook(module, inputs, output):
+            if self._capture and torch.is_grad_enabled() and module.training and output.requires_grad:
+                output.register_hook(lambda g: self._launch_factor(l, g, "G"))
+        return hook
+
+    # ------------------------------------------------------------------ step
+    def check_inverses(self) -> None:
+        """Raise NotPositiveDefiniteError for the last completed inversion
+        (linalg.py:141-145); synchronises only on that inversion's event."""
+        if self._info_event is None:
+            return
+        self._info_event.synchronize()
+        self._info_event = None
+        bad = torch.nonzero(self._info_host).flatten()
+        if bad.numel():
+            raise NotPositiveDefiniteError(int(self._info_host[bad[0]]) - 1)
+
+    @torch.no_grad()
+    def step(self, closure=None):
+        loss = closure() if closure is not None else None
+        self.check_inverses()
+        main = torch.cuda.current_stream(self.device)
+        lr = self.param_groups[0]["lr"]
+        factors_now = self._capture
+        invert_now = self.steps % self.inv_update_freq == 0
+        if factors_now:
+            main.wait_stream(self.factor_stream)
+            self._factor_updates += 1
+        if self.world > 1:
+            cs = self.comm_stream
+            cs.wait_stream(main)
+            grads = [p.grad for p in self.param_groups[0]["params"] if p.grad is not None]
+            with self.comm.group():
+                for g in grads:
+                    self.comm.allreduce_sum(g, cs)
+            main.wait_stream(cs)  # also orders the factor all-reduces before inversion
+        if invert_now:
+            if self._inv_plan is not None:
+                self._inv_plan.run(self.damping, main)
+                self._info_host.copy_(self._inv_plan.info, non_blocking=True)
+                self._info_event = torch.cuda.Event()
+                self._info_event.record(main)
+            if self.world > 1:
+                self._exchange_inverses(main)
+        # precondition + update for every K-FAC layer (mean gradient = sum / P)
+        g_inv, grads, a_inv, weights = [], [], [], []
+        for l in self.layers:
+            w = l.module.weight
+            if w.grad is None:
+                raise RuntimeError(f"layer {l.name} has no gradient; call backward() before step()")
+            grads.append(w.grad.reshape(l.spec.g_dim, l.spec.a_dim))
+            weights.append(w.data)
+            a_inv.append(self.inv[2 * l.index])
+            g_inv.append(self.inv[2 * l.index + 1])
+        self._precond.run(g_inv, grads, a_inv, weights=weights, alpha=lr / self.world, stream=main)
+        others = [p for p in self.other_params if p.grad is not None]
+        if others:
+            torch._foreach_add_([p.data for p in others], [p.grad for p in others], alpha=-lr / self.world)
+        self.steps += 1
+        self._capture = self.steps % self.factor_update_freq == 0
+        return loss
+
+    def _exchange_inverses(self, main):
+        """Owner ranks broadcast their CT inverses (packed upper triangle,
+        PAPER.md:281-283 / emulator.py:256-262), one NCCL broadcast per owner."""
+        lib = L.load()
+        ct, dims, buf, views, n = self._bcast[self.rank]
+        if ct:
+            L.check(lib.spdkfac_pack_upper_batched_f32(len(ct), L.i32_array(dims),
+                                                       L.ptr_array([self.inv[t].data_ptr() for t in ct]),
+                                                       L.ptr_array([v.data_ptr() for v in views]),
+                                                       main.cuda_stream), "pack inverses")
+        cs = self.comm_stream
+        cs.wait_stream(main)
+        with self.comm.group():
+            for root, (ct_r, _, buf_r, _, n_r) in enumerate(self._bcast):
+                if n_r:
+                    self.comm.bcast(buf_r[:n_r], root, cs)
+        main.wait_stream(cs)
+        for root, (ct_r, dims_r, _, views_r, n_r) in enumerate(self._bcast):
+            if root == self.rank or not ct_r:
+                continue
+            L.check(lib.spdkfac_unpack_upper_batched_f32(len(ct_r), L.i32_array(dims_r),
+                                                         L.ptr_array([v.data_ptr() for v in views_r]),
+                                                         L.ptr_array([self.inv[t].data_ptr() for t in ct_r]),
+                                                         main.cuda_stream), "unpack inverses")
+
+    # ------------------------------------------------------------------ introspection / checkpoint
+    def factor(self, layer: int, kind: str) -> torch.Tensor:
+        """Current aggregated (running-average) factor of a layer as a full matrix."""
+        from .linalg import unpack_upper
+        t = 2 * layer + (0 if kind == "A" else 1)
+        return unpack_upper(self._packed(t), self.inv[t].shape[0])
+
+    def state_dict(self):
+        sd = super().state_dict()
+        sd["spdkfac"] = {"bufA": self.bufA.clone(), "bufG": self.bufG.clone(), "inv": [t.clone() for t in self.inv],
+                         "steps": self.steps, "factor_updates": self._factor_updates}
+        return sd
+
+    def load_state_dict(self, sd):
+        k = sd.pop("spdkfac", None)
+        super().load_state_dict(sd)
+        if k is not None:
+            self.bufA.copy_(k["bufA"])
+            self.bufG.copy_(k["bufG"])
+            for t, s in zip(self.inv, k["inv"]):
+                t.copy_(s)
+            self.steps = int(k["steps"])
+            self._factor_updates = int(k["factor_updates"])
+            self._capture = self.steps % self.factor_update_freq == 0

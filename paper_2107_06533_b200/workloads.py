@@ -1,0 +1,112 @@
+"""Workloads of BASELINE.json's configs: the models whose K-FAC layers the step
+preconditions, synthetic data, and the per-layer factor shapes (M rows, a, g).
+
+configs[0]  ResNet-20-style CIFAR net, 32x32, single worker (CPU reference runs it)
+configs[1]  torchvision ResNet-50 v1.5, bs32/GPU, 224x224          (the bench workload)
+configs[2]  same at 2/4/8 GPUs (fused factor all-reduce + LBP inverses)
+configs[3]  DenseNet-201 (torchvision), bs16
+configs[4]  Inception-v4 / BERT-base linears (shape sweeps only)
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.nn as nn
+
+
+class _Basic(nn.Module):
+    def __init__(self, cin, cout, stride):
+        super().__init__()
+        self.conv1 = nn.Conv2d(cin, cout, 3, stride, 1, bias=False)
+        self.bn1 = nn.BatchNorm2d(cout)
+        self.conv2 = nn.Conv2d(cout, cout, 3, 1, 1, bias=False)
+        self.bn2 = nn.BatchNorm2d(cout)
+        self.pad = cout - cin
+        self.stride = stride
+
+    def forward(self, x):
+        out = torch.relu(self.bn1(self.conv1(x)))
+        out = self.bn2(self.conv2(out))
+        sc = x
+        if self.stride != 1 or self.pad:  # option-A shortcut: subsample + zero-pad channels
+            sc = x[:, :, ::self.stride, ::self.stride]
+            sc = nn.functional.pad(sc, (0, 0, 0, 0, self.pad // 2, self.pad - self.pad // 2))
+        return torch.relu(out + sc)
+
+
+class ResNet20(nn.Module):
+    """CIFAR ResNet-20 (He et al. 2016, option-A shortcuts): conv1 (a=27, g=16),
+    18 3x3 convs, fc (a=64, g=10) -- 20 preconditioned layers."""
+
+    def __init__(self, num_classes=10):
+        super().__init__()
+        self.conv1 = nn.Conv2d(3, 16, 3, 1, 1, bias=False)
+        self.bn1 = nn.BatchNorm2d(16)
+        blocks, cin = [], 16
+        for cout, stride in ((16, 1), (32, 2), (64, 2)):
+            for i in range(3):
+                blocks.append(_Basic(cin, cout, stride if i == 0 else 1))
+                cin = cout
+        self.layers = nn.Sequential(*blocks)
+        self.fc = nn.Linear(64, num_classes, bias=False)
+
+    def forward(self, x):
+        x = torch.relu(self.bn1(self.conv1(x)))
+        x = self.layers(x)
+        return self.fc(x.mean(dim=(2, 3)))
+
+
+def build_model(name: str) -> nn.Module:
+    import torchvision
+    if name == "resnet50":
+        return torchvision.models.resnet50(weights=None)
+    if name == "resnet152":
+        return torchvision.models.resnet152(weights=None)
+    if name == "densenet201":
+        return torchvision.models.densenet201(weights=None)
+    if name == "resnet20":
+        return ResNet20()
+    raise ValueError(f"unknown model {name!r}")
+
+
+def input_shape(name: str, batch: int):
+    return (batch, 3, 32, 32) if name == "resnet20" else (batch, 3, 224, 224)
+
+
+def num_classes(name: str) -> int:
+    return 10 if name == "resnet20" else 1000
+
+
+def layer_shapes(name: str, batch: int) -> list:
+    """[(layer name, M rows, a_dim, g_dim)] for every Conv2d/Linear in
+    forward-definition order, M = batch * Hout * Wout (conv) or batch (linear)."""
+    model = build_model(name)
+    shapes = []
+    hooks = []
+    for n, m in model.named_modules():
+        if isinstance(m, (nn.Conv2d, nn.Linear)):
+            def hook(mod, inp, out, n=n):
+                if isinstance(mod, nn.Conv2d):
+                    a = mod.in_channels * mod.kernel_size[0] * mod.kernel_size[1]
+                    shapes.append((n, batch * out.shape[2] * out.shape[3], a, mod.out_channels))
+                else:
+                    shapes.append((n, batch, mod.in_features, mod.out_features))
+            hooks.append(m.register_forward_hook(hook))
+    with torch.no_grad():
+        model.eval()(torch.zeros(input_shape(name, 1)))
+    for h in hooks:
+        h.remove()
+    order = {n: i for i, (n, m) in enumerate(model.named_modules())}
+    return sorted(shapes, key=lambda s: order[s[0]])
+
+
+def bert_base_linear_shapes(batch: int = 32, seq: int = 128) -> list:
+    """BERT-base encoder linears (12 layers x {q,k,v,o: 768x768, ffn 768->3072, 3072->768}); FC semantics."""
+    m = batch * seq
+    out = []
+    for l in range(12):
+        for nm in ("q", "k", "v", "o"):
+            out.append((f"layer{l}.{nm}", m, 768, 768))
+        out.append((f"layer{l}.ffn1", m, 768, 3072))
+        out.append((f"layer{l}.ffn2", m, 3072, 768))
+    return out

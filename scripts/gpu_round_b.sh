@@ -1,0 +1,4 @@
+export SPD_WATCHDOG=120
+timeout 180 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/rb_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/rb_smoke.log
+timeout 900 python -m pytest tests/ -q -m gpu -x > gpurun_out/rb_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/rb_tests.log
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/rb_bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/rb_bench.log

@@ -1,0 +1,77 @@
+"""GPU parity of the full optimizer step (SPDKFAC) against the oracle."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def test_golden_fixture_through_optimizer():
+    from tests.smoke_impl import TOL, fixture_step
+    errs = fixture_step()
+    assert max(errs) <= TOL, errs
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_conv_net_step_matches_oracle(seed):
+    from tests.smoke_impl import TOL, conv_step
+    errs = conv_step(seed=seed)
+    assert max(errs.values()) <= TOL, errs
+
+
+def test_running_average_and_frequencies():
+    """decay rho: A_t = rho A_{t-1} + (1-rho) A(batch_t); factors only every
+    factor_update_freq steps; inverses only every inv_update_freq steps."""
+    import oracle as O
+    import torch.nn as nn
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    torch.manual_seed(3)
+    lin = nn.Linear(20, 7, bias=False).cuda()
+    opt = SPDKFAC(lin, lr=0.0, damping=0.1, factor_decay=0.8, factor_update_freq=2, inv_update_freq=4)
+    xs = [torch.randn(16, 20, device="cuda") for _ in range(5)]
+    running = None
+    for i, x in enumerate(xs):
+        opt.zero_grad()
+        lin(x).pow(2).mean().backward()
+        inv_before = opt.inv[0].clone()
+        opt.step()
+        if i % 2 == 0:
+            fresh = O.factor_A(x.double().cpu().numpy())
+            running = fresh if running is None else 0.8 * running + 0.2 * fresh
+        got = opt.factor(0, "A").double().cpu().numpy()
+        assert np.linalg.norm(got - running) / np.linalg.norm(running) < 1e-4, i
+        if i % 4 != 0:
+            assert torch.equal(opt.inv[0], inv_before)
+    opt.remove_hooks()
+
+
+def test_state_dict_round_trip():
+    import torch.nn as nn
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    lin = nn.Linear(8, 4).cuda()
+    opt = SPDKFAC(lin, lr=0.1, damping=0.1)
+    lin(torch.randn(5, 8, device="cuda")).sum().backward()
+    opt.step()
+    sd = opt.state_dict()
+    opt2 = SPDKFAC(nn.Linear(8, 4).cuda(), lr=0.1, damping=0.1)
+    opt2.load_state_dict(sd)
+    assert torch.equal(opt2.bufA, opt.bufA) and all(torch.equal(a, b) for a, b in zip(opt2.inv, opt.inv))
+    assert opt2.steps == 1
+    opt.remove_hooks()
+    opt2.remove_hooks()
+
+
+def test_nonpd_raises_on_next_step():
+    import torch.nn as nn
+    from paper_2107_06533_b200.linalg import NotPositiveDefiniteError
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    lin = nn.Linear(4, 3, bias=False).cuda()
+    opt = SPDKFAC(lin, lr=0.1, damping=0.0)
+    x = torch.zeros(2, 4, device="cuda")  # A = 0, gamma = 0: singular
+    lin(x).sum().backward()
+    opt.step()
+    with pytest.raises(NotPositiveDefiniteError) as e:
+        opt.check_inverses()
+    assert e.value.pivot == 0
+    opt.remove_hooks()
