@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--profile", action="store_true", help="short run for ncu: no clocks/e2e/cpu legs")
+    p.add_argument("--optimizer", choices=("spdkfac", "sgd"), default="spdkfac",
+                   help="sgd = diagnostic floor (forward/backward + SGD, no K-FAC); never the headline")
     return p.parse_args()
 
 
@@ -152,8 +154,13 @@ def run_ours(a):
 
     torch.manual_seed(0)
     model = build_model(a.model).to(dev)
-    opt = SPDKFAC(model, lr=a.lr, damping=a.damping, factor_update_freq=a.factor_freq, inv_update_freq=a.inv_freq,
-                  placement=a.placement)
+    if a.optimizer == "sgd":
+        opt = torch.optim.SGD(model.parameters(), lr=a.lr)
+        opt.check_inverses = lambda: None
+        opt.placement = None
+    else:
+        opt = SPDKFAC(model, lr=a.lr, damping=a.damping, factor_update_freq=a.factor_freq,
+                      inv_update_freq=a.inv_freq, placement=a.placement)
     crit = nn.CrossEntropyLoss()
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)
@@ -262,7 +269,13 @@ def run_ours(a):
                "data": "synthetic (random N(0,1) images, uniform labels; random-init torchvision weights)",
                "config": workload_config(a, world), "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
                "cpu_baseline": cpu, "clocks": clk, "kernel_breakdown": breakdown,
-               "placement_imbalance": _imbalance(opt), "final_loss": final_loss}
+               "placement_imbalance": _imbalance(opt) if opt.placement is not None else None,
+               "final_loss": final_loss}
+        if a.optimizer != "spdkfac":
+            out["diagnostic"] = f"optimizer={a.optimizer}: not the SPD-KFAC metric"
+        if world > 1:
+            out["grad_allreduce"] = "NCCL (libspdkfac comm), grouped per step"
+
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()

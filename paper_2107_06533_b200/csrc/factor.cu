@@ -320,8 +320,8 @@ int spdkfac_factor_plan_create(spdkfac_factor_plan** out, const spdkfac_factor_g
       }
     }
   std::vector<TcEpi> epis(1);
-  epis[0] = L.splits > 1 ? TcEpi{p->partial, 128, 0, 1.f, 0.f, kAxpby, 0}
-                         : TcEpi{nullptr, 0, 0, 1.f, 0.f, kPackedUpper, 0};
+  epis[0] = L.splits > 1 ? TcEpi{p->partial, 128, 0, 1.f, 0.f, kAxpby, 0, nullptr, 0, 0}
+                         : TcEpi{nullptr, 0, 0, 1.f, 0.f, kPackedUpper, 0, nullptr, 0, 0};
   if (L.Mpad > M) {
     zero_pad_kernel<<<unsigned(d), 64, 0, s>>>(p->xt, d, M, L.Mpad);
     SPD_CHECK_LAUNCH();

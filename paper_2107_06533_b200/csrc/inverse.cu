@@ -10,9 +10,10 @@
 //   d <= 128 : one CTA per matrix, whole matrix in shared memory, scalar sweep.
 //   d  > 128 : blocked sweep on the matrix padded to a multiple of 128 with an identity
 //              block, one 128-pivot block per step k, batched over all matrices:
-//                pivot  : P = W[K,K] swept in shared memory  -> P^-1, W[K,K] = -P^-1
-//                panel  : C_R = W[R,K] P^-1 (row blocks R != K), W[R,K] = C_R, W[K,R] = C_R^T,
-//                         old panel and C staged as tf32 hi/lo planes
+//                pivot  : P = W[K,K] swept in registers -> W[K,K] = -P^-1, P^-1 as tf32 planes
+//                stage  : old column panel W[:,K] -> tf32 hi/lo planes
+//                panel  : C = Wold[:,K] P^-1 on tcgen05 (3 x tf32); epilogue writes W[R,K] = C_R,
+//                         W[K,R] = C_R^T and C as tf32 planes
 //                update : W[I,J] -= Wold[I,K] C_J^T for I <= J (I,J != K) on tcgen05
 //                         (3 x tf32, rank-128), mirrored to W[J,I]
 //              finalize: out = -(W + W^T)/2 cropped to d x d (the reference's symmetrisation).
@@ -25,17 +26,20 @@ constexpr int kSmemLd = kB + 1;  // padded row stride of the shared-memory block
 
 struct InvMat {
   float* W;          // padded working matrix [dp][dp] (blocked path)
-  float* pinv;       // [128][128] scratch for the current pivot inverse
   const float* in;   // packed upper input
   float* out;        // full d x d output (ld = d)
   int32_t* info;     // 0 or failing pivot + 1
   int32_t d, dp;
   int32_t panel_row0;  // first row of this matrix's panels in the shared panel planes
-  int32_t pad_;
+  int32_t slot;        // index among blocked matrices (row slot*128 of the P^-1 planes)
+};
+
+struct TileJob {  // one 32 x 32 tile (I <= J) of a blocked matrix, for unpack/finalize
+  int32_t mat, ti, tj, pad_;
 };
 
 // Register-resident scalar sweep of one 128 x 128 block by 512 threads: thread t owns
-// row i = t >> 2, columns [32q, 32q + 32), q = t & 3, in registers.  Per pivot k the four
+// row i = t & 127, columns [32q, 32q + 32), q = t >> 7 (warp-uniform), in registers.  Per pivot k the four
 // owners of row k publish it to shared memory (double-buffered by k parity, rows skewed by
 // 4 floats per 32 so the four column quarters hit distinct banks); every thread then
 // applies  a_ij -= (a_ik / p) a_kj,  a_ik <- a_ik / p,  a_kj <- a_kj / p,  a_kk <- -1/p,
@@ -44,7 +48,7 @@ struct InvMat {
 constexpr int kRowSkew = 36;  // skewed row buffer: element j at (j >> 5) * 36 + (j & 31)
 
 __device__ __forceinline__ int sweep128(float (&a)[32], int n, float* rbuf /* 2 x 4*36 */) {
-  const int t = threadIdx.x, i = t >> 2, q = t & 3;
+  const int t = threadIdx.x, i = t & 127, q = t >> 7;
   for (int k = 0; k < n; ++k) {
     float* rk = rbuf + (k & 1) * (4 * kRowSkew);
     if (i == k) {
@@ -55,7 +59,7 @@ __device__ __forceinline__ int sweep128(float (&a)[32], int n, float* rbuf /* 2 
     __syncthreads();
     const float p = rk[(k >> 5) * kRowSkew + (k & 31)];
     if (!(p > 0.f)) return k;  // dpotrf's "ajj <= 0 or NaN" test, on the same Schur pivots
-    const float pinv = 1.0f / p;
+    const float pinv = __frcp_rn(p);
     const float ci = rk[(i >> 5) * kRowSkew + (i & 31)] * pinv;  // a_ik / p
     const int kq = k >> 5, kj = k & 31;
     if (i == k) {
@@ -91,7 +95,7 @@ __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __rest
   __shared__ __align__(16) float rbuf[2 * 4 * kRowSkew];
   const InvMat m = mats[ids[blockIdx.x]];
   const int n = m.d;
-  const int i = threadIdx.x >> 2, q = threadIdx.x & 3;
+  const int i = threadIdx.x & 127, q = threadIdx.x >> 7;
   float a[32];
 #pragma unroll
   for (int jj = 0; jj < 32; ++jj) {
@@ -116,26 +120,45 @@ __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __rest
 }
 
 // ---------------------------------------------------------------- blocked path
-__global__ void damp_unpack_kernel(const InvMat* __restrict__ mats, const int32_t* __restrict__ ids, float gamma) {
-  const InvMat m = mats[ids[blockIdx.y]];
-  const int64_t dp = m.dp, d = m.d;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *m.info = 0;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < dp * dp; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / dp, j = e - i * dp;
+// W = unpack(packed) + gamma I, identity padding; one 32x32 tile pair (I,J),(J,I) per block.
+__global__ void __launch_bounds__(256) damp_unpack_kernel(const InvMat* __restrict__ mats,
+                                                          const TileJob* __restrict__ jobs, float gamma) {
+  __shared__ float tile[32][33];
+  const TileJob jb = jobs[blockIdx.x];
+  const InvMat m = mats[jb.mat];
+  const int64_t d = m.d, dp = m.dp;
+  if (jb.ti == 0 && jb.tj == 0 && threadIdx.x == 0) *m.info = 0;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int64_t i0 = int64_t(jb.ti) * 32, j0 = int64_t(jb.tj) * 32;
+  for (int r = ty; r < 32; r += 8) {  // row i = i0 + r of the upper tile: contiguous in packed row i
+    const int64_t i = i0 + r, j = j0 + tx;
     float v;
-    if (i < d && j < d) v = packed_at(m.in, d, i, j) + (i == j ? gamma : 0.f);
-    else v = (i == j) ? 1.f : 0.f;  // identity padding: never fails, decouples
-    m.W[e] = v;
+    if (i < d && j < d) v = (j >= i) ? m.in[i * (2 * d - i + 1) / 2 + (j - i)] : 0.f;
+    else v = (i == j) ? 1.f : 0.f;
+    if (i == j && i < d) v += gamma;
+    tile[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = i0 + r, j = j0 + tx;
+    if (jb.ti == jb.tj) {  // diagonal tile: mirror the upper part inside the tile
+      const float v = (tx >= r) ? tile[r][tx] : tile[tx][r];
+      m.W[i * dp + j] = v;
+    } else {
+      m.W[i * dp + j] = tile[r][tx];                      // (I, J)
+      m.W[(j0 + r) * dp + i0 + tx] = tile[tx][r];         // (J, I) transposed through smem
+    }
   }
 }
 
 __global__ void __launch_bounds__(512) pivot_kernel(const InvMat* __restrict__ mats,
-                                                    const int32_t* __restrict__ ids, int k) {
+                                                    const int32_t* __restrict__ ids, int k,
+                                                    float* __restrict__ pinv_planes, int64_t pinv_plane) {
   __shared__ __align__(16) float rbuf[2 * 4 * kRowSkew];
   const InvMat m = mats[ids[blockIdx.x]];
   if (*m.info != 0) return;
   const int64_t dp = m.dp, K0 = int64_t(k) * kB;
-  const int i = threadIdx.x >> 2, q = threadIdx.x & 3;
+  const int i = threadIdx.x & 127, q = threadIdx.x >> 7;
   float a[32];
   const float* src = m.W + (K0 + i) * dp + K0 + q * 32;
 #pragma unroll
@@ -148,89 +171,96 @@ __global__ void __launch_bounds__(512) pivot_kernel(const InvMat* __restrict__ m
     if (threadIdx.x == 0) *m.info = int(K0) + f + 1;
     return;
   }
-  float* dst = m.W + (K0 + i) * dp + K0 + q * 32;  // W[K,K] <- -P^-1
-  float* pv = m.pinv + i * kB + q * 32;             // P^-1
+  float* dst = m.W + (K0 + i) * dp + K0 + q * 32;                        // W[K,K] <- -P^-1
+  float* ph = pinv_planes + (int64_t(m.slot) * kB + i) * kB + q * 32;      // P^-1 hi plane
 #pragma unroll
   for (int jj = 0; jj < 32; jj += 4) {
     *reinterpret_cast<float4*>(dst + jj) = make_float4(a[jj], a[jj + 1], a[jj + 2], a[jj + 3]);
-    *reinterpret_cast<float4*>(pv + jj) = make_float4(-a[jj], -a[jj + 1], -a[jj + 2], -a[jj + 3]);
+    float h[4], l[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) split_tf32(-a[jj + u], h[u], l[u]);
+    *reinterpret_cast<float4*>(ph + jj) = make_float4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<float4*>(ph + pinv_plane + jj) = make_float4(l[0], l[1], l[2], l[3]);
   }
 }
 
 struct PanelJob {
-  int32_t mat, rb;  // matrix id, row block R (!= K)
+  int32_t mat, rb;  // matrix, row block R != K
 };
 
-// C_R = W[R,K] P^-1 (fp32 FFMA, 8x8 register tile per thread), stage split planes.
-__global__ void __launch_bounds__(256) panel_kernel(const InvMat* __restrict__ mats,
-                                                    const PanelJob* __restrict__ jobs, int k,
-                                                    float* __restrict__ panA, float* __restrict__ panC,
-                                                    int64_t plane_rows) {
-  extern __shared__ float sm[];
-  float* a = sm;                  // [128][129] old panel W[R,K]
-  float* p = sm + kB * kSmemLd;   // [128][129] P^-1
-  const PanelJob job = jobs[blockIdx.x];
-  const InvMat m = mats[job.mat];
+// Old column panel Wold[R, K] -> tf32 hi/lo planes panA[prow(R) + i][j].  Only the upper
+// block triangle of W is maintained, so blocks below the pivot (R > K) are read as
+// W[K, R]^T through a shared-memory transpose.
+__global__ void __launch_bounds__(256) stage_panel_kernel(const InvMat* __restrict__ mats,
+                                                          const PanelJob* __restrict__ jobs, int k,
+                                                          float* __restrict__ panA, int64_t plane) {
+  __shared__ float tile[32][33];
+  const PanelJob jb = jobs[blockIdx.x];
+  const InvMat m = mats[jb.mat];
   if (*m.info != 0) return;
-  const int64_t dp = m.dp, K0 = int64_t(k) * kB, R0 = int64_t(job.rb) * kB;
-  const int64_t prow = int64_t(m.panel_row0) + R0;  // panel plane row of local row 0
-  const int64_t plane = plane_rows * kB;
-  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {
-    const int i = e / kB, j = e % kB;
-    const float v = m.W[(R0 + i) * dp + K0 + j];
-    a[i * kSmemLd + j] = v;
-    p[i * kSmemLd + j] = m.pinv[e];
-    float h, l;
-    split_tf32(v, h, l);
-    panA[(prow + i) * kB + j] = h;
-    panA[plane + (prow + i) * kB + j] = l;
-  }
-  __syncthreads();
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // rows ty*8.., cols tx + 16*c
-  float acc[8][8];
-#pragma unroll
-  for (int r = 0; r < 8; ++r)
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[r][c] = 0.f;
-  for (int kk = 0; kk < kB; ++kk) {
-    float av[8], pv[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) av[r] = a[(ty * 8 + r) * kSmemLd + kk];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) pv[c] = p[kk * kSmemLd + tx + 16 * c];
-#pragma unroll
-    for (int r = 0; r < 8; ++r)
-#pragma unroll
-      for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(av[r], pv[c], acc[r][c]);
-  }
-  __syncthreads();  // all reads of `a` done: reuse it to stage C for the transposed store
-#pragma unroll
-  for (int r = 0; r < 8; ++r)
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int i = ty * 8 + r, j = tx + 16 * c;
-      const float v = acc[r][c];
-      m.W[(R0 + i) * dp + K0 + j] = v;  // A_ik <- A_ik P^-1
-      a[j * kSmemLd + i] = v;           // staged transposed
-      float h, l;
-      split_tf32(v, h, l);
-      panC[(prow + i) * kB + j] = h;
-      panC[plane + (prow + i) * kB + j] = l;
+  const int64_t dp = m.dp, K0 = int64_t(k) * kB, R0 = int64_t(jb.rb) * kB;
+  float* dst = panA + (int64_t(m.panel_row0) + R0) * kB;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  if (jb.rb < k) {
+    for (int e = threadIdx.x; e < kB * kB / 4; e += blockDim.x) {
+      const int i = e >> 5, c = (e & 31) * 4;
+      const float4 v = *reinterpret_cast<const float4*>(m.W + (R0 + i) * dp + K0 + c);
+      float h[4], l[4];
+      split_tf32(v.x, h[0], l[0]);
+      split_tf32(v.y, h[1], l[1]);
+      split_tf32(v.z, h[2], l[2]);
+      split_tf32(v.w, h[3], l[3]);
+      *reinterpret_cast<float4*>(dst + i * kB + c) = make_float4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<float4*>(dst + plane + i * kB + c) = make_float4(l[0], l[1], l[2], l[3]);
     }
-  __syncthreads();
-  for (int e = threadIdx.x; e < kB * kB; e += blockDim.x) {  // A_ki <- P^-1 A_ki, coalesced along i
-    const int j = e / kB, i = e % kB;
-    m.W[(K0 + j) * dp + R0 + i] = a[j * kSmemLd + i];
+  } else {
+    for (int sub = 0; sub < 16; ++sub) {  // 32 x 32 sub-tiles (si, sj) of the 128 x 128 block
+      const int si = sub >> 2, sj = sub & 3;
+      __syncthreads();
+      for (int r = ty; r < 32; r += 8)  // W[K0 + 32 sj + r][R0 + 32 si + tx]
+        tile[r][tx] = m.W[(K0 + 32 * sj + r) * dp + R0 + 32 * si + tx];
+      __syncthreads();
+      for (int r = ty; r < 32; r += 8) {  // panA row 32 si + r, col 32 sj + tx = W[K0+32sj+tx][R0+32si+r]
+        float h, l;
+        split_tf32(tile[tx][r], h, l);
+        const int64_t o = int64_t(32 * si + r) * kB + 32 * sj + tx;
+        dst[o] = h;
+        dst[plane + o] = l;
+      }
+    }
   }
 }
 
-__global__ void finalize_kernel(const InvMat* __restrict__ mats, const int32_t* __restrict__ ids) {
-  const InvMat m = mats[ids[blockIdx.y]];
+// out = -(W + W^T)/2 cropped to d x d, one 32x32 tile pair (I <= J) per block.  Inside a
+// diagonal 128-block both triangles are valid and are averaged; elsewhere only the upper
+// block triangle is valid and is mirrored.
+__global__ void __launch_bounds__(256) finalize_kernel(const InvMat* __restrict__ mats,
+                                                       const TileJob* __restrict__ jobs) {
+  __shared__ float tile[32][33];
+  __shared__ float outt[32][33];
+  const TileJob jb = jobs[blockIdx.x];
+  const InvMat m = mats[jb.mat];
   if (*m.info != 0) return;
   const int64_t d = m.d, dp = m.dp;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < d * d; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / d, j = e - i * d;
-    m.out[e] = -0.5f * (m.W[i * dp + j] + m.W[j * dp + i]);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t i0 = int64_t(jb.ti) * 32, j0 = int64_t(jb.tj) * 32;
+  const bool same_block = (jb.ti >> 2) == (jb.tj >> 2);
+  if (same_block)
+    for (int r = ty; r < 32; r += 8) tile[r][tx] = m.W[(j0 + r) * dp + i0 + tx];  // W[J, I], coalesced
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = i0 + r, j = j0 + tx;
+    const float w = m.W[i * dp + j];
+    const float v = same_block ? -0.5f * (w + tile[tx][r]) : -w;
+    outt[tx][r] = v;
+    if (i < d && j < d) m.out[i * d + j] = v;
+  }
+  __syncthreads();
+  if (jb.ti != jb.tj) {
+    for (int r = ty; r < 32; r += 8) {  // out[j0 + r][i0 + tx] = v(i0 + tx, j0 + r)
+      const int64_t j = j0 + r, i = i0 + tx;
+      if (i < d && j < d) m.out[j * d + i] = outt[r][tx];
+    }
   }
 }
 
@@ -241,7 +271,7 @@ using namespace spd;
 struct spdkfac_inverse_plan {
   int n;
   std::vector<int32_t> dims;
-  double small_flops = 0;       // sum d^3 of the shared-memory path (algorithmic potrf+potri)
+  double small_flops = 0;       // sum d^3 of the register path (algorithmic potrf+potri)
   double algo_flops = 0;        // sum d^3 over all matrices
   InvMat* mats;                 // device
   int32_t* small_ids;           // device
@@ -249,56 +279,76 @@ struct spdkfac_inverse_plan {
   int32_t* blocked_ids;         // device
   int n_blocked;
   int steps;
-  std::vector<int> piv_off, piv_cnt, pan_off, pan_cnt, upd_off, upd_cnt;
-  int32_t* piv_ids;             // device, concatenated per step
-  PanelJob* pan_jobs;           // device
-  CUtensorMap* maps;            // [0] = panel A planes, [1] = panel C planes
-  TcItem* items;
-  TcEpi* epis;
+  std::vector<int> act_off, act_cnt, pan_off, pan_cnt, upd_off, upd_cnt, pj_off;
+  int32_t* act_ids;             // device, active blocked matrices per step (concatenated)
+  PanelJob* pan_jobs;           // device, (matrix, R != K) per step, same order as the panel items
+  TileJob* tiles;               // device, 32x32 tile pairs of all blocked matrices
+  int n_tiles;
+  CUtensorMap* maps;            // [0] old panel planes, [1] C planes, [2] P^-1 planes
+  TcItem* items;                // per step: panel GEMM items then update items
+  TcEpi* epis;                  // [0, n): update, [n, 2n): panel
   float* panA;
   float* panC;
+  float* pinvS;
   int64_t plane_rows;
+  int max_rows;                 // largest dp (stage grid)
 };
 
 namespace {
 
-struct InvLayout {
-  size_t bytes;
-};
-
-size_t inverse_carve(int n, const int32_t* dims, Carve& c, spdkfac_inverse_plan* p, std::vector<InvMat>* mats,
-                     std::vector<int32_t>* small, std::vector<int32_t>* blocked, int64_t* plane_rows,
-                     int64_t* total_items, int64_t* total_piv, int64_t* total_pan, int* steps) {
-  int64_t rows = 0, items = 0, piv = 0, pan = 0;
-  int st = 0;
+void inverse_sizes(int n, const int32_t* dims, int64_t* rows, int64_t* items, int64_t* act, int64_t* tiles,
+                   int* steps, int* nblk) {
+  *rows = *items = *act = *tiles = 0;
+  *steps = *nblk = 0;
   for (int t = 0; t < n; ++t) {
-    const int d = dims[t];
+    if (dims[t] <= kB) continue;
+    const int64_t dp = round_up(dims[t], kB), T = dp / kB, T32 = dp / 32;
+    *rows += dp;
+    *steps = std::max<int>(*steps, int(T));
+    *act += T;
+    *items += T * (T - 1) + T * ((T - 1) * T / 2);  // panel items + update items over all steps
+    *tiles += T32 * (T32 + 1) / 2;
+    *nblk += 1;
+  }
+}
+
+size_t inverse_carve(int n, const int32_t* dims, Carve& c, spdkfac_inverse_plan* p, std::vector<InvMat>* mats) {
+  int64_t rows, items, act, tiles;
+  int steps, nblk;
+  inverse_sizes(n, dims, &rows, &items, &act, &tiles, &steps, &nblk);
+  int64_t prow = 0;
+  int slot = 0;
+  for (int t = 0; t < n; ++t) {
     InvMat m{};
-    m.d = d;
-    if (d <= kB) {
-      m.dp = d;
-      if (small) small->push_back(t);
+    m.d = dims[t];
+    if (dims[t] <= kB) {
+      m.dp = dims[t];
     } else {
-      const int dp = int(round_up(d, kB));
-      const int T = dp / kB;
-      m.dp = dp;
-      m.W = c.take<float>(size_t(dp) * dp);
-      m.pinv = c.take<float>(size_t(kB) * kB);
-      m.panel_row0 = int(rows);
-      rows += dp;
-      if (blocked) blocked->push_back(t);
-      st = std::max(st, T);
-      piv += T;
-      pan += int64_t(T) * (T - 1);
-      items += int64_t(T) * (int64_t(T - 1) * T / 2);  // per step: (T-1)T/2 upper pairs excluding K
+      m.dp = int(round_up(dims[t], kB));
+      m.W = c.take<float>(size_t(m.dp) * m.dp);
+      m.panel_row0 = int(prow);
+      m.slot = slot++;
+      prow += m.dp;
     }
     if (mats) mats->push_back(m);
   }
-  *plane_rows = rows;
-  *total_items = items;
-  *total_piv = piv;
-  *total_pan = pan;
-  *steps = st;
+  float* panA = c.take<float>(size_t(2) * std::max<int64_t>(rows, 1) * kB);
+  float* panC = c.take<float>(size_t(2) * std::max<int64_t>(rows, 1) * kB);
+  float* pinvS = c.take<float>(size_t(2) * std::max(nblk, 1) * kB * kB);
+  auto* dm = c.take<InvMat>(size_t(n));
+  auto* sid = c.take<int32_t>(size_t(n));
+  auto* bid = c.take<int32_t>(size_t(n));
+  auto* aid = c.take<int32_t>(size_t(std::max<int64_t>(act, 1)));
+  auto* tj = c.take<TileJob>(size_t(std::max<int64_t>(tiles, 1)));
+  auto* pj = c.take<PanelJob>(size_t(std::max<int64_t>(items, 1)));
+  auto* mp = c.take<CUtensorMap>(3, 128);
+  auto* it = c.take<TcItem>(size_t(std::max<int64_t>(items, 1)));
+  auto* ep = c.take<TcEpi>(size_t(2) * n);
+  if (p) {
+    p->panA = panA, p->panC = panC, p->pinvS = pinvS, p->mats = dm, p->small_ids = sid, p->blocked_ids = bid;
+    p->act_ids = aid, p->tiles = tj, p->pan_jobs = pj, p->maps = mp, p->items = it, p->epis = ep;
+    p->plane_rows = rows, p->steps = steps, p->n_tiles = int(tiles);
+  }
   return c.used;
 }
 
@@ -309,20 +359,7 @@ extern "C" {
 size_t spdkfac_inverse_workspace_size(int n, const int32_t* dims) {
   if (n < 0 || (n > 0 && !dims)) return 0;
   Carve c(nullptr, 0);
-  int64_t rows, items, piv, pan;
-  int steps;
-  inverse_carve(n, dims, c, nullptr, nullptr, nullptr, nullptr, &rows, &items, &piv, &pan, &steps);
-  c.take<float>(size_t(2) * rows * kB);  // panA
-  c.take<float>(size_t(2) * rows * kB);  // panC
-  c.take<InvMat>(size_t(n));
-  c.take<int32_t>(size_t(n));
-  c.take<int32_t>(size_t(n));
-  c.take<int32_t>(size_t(piv));
-  c.take<PanelJob>(size_t(pan));
-  c.take<CUtensorMap>(2, 128);
-  c.take<TcItem>(size_t(items));
-  c.take<TcEpi>(size_t(n));
-  return c.used + 256;
+  return inverse_carve(n, dims, c, nullptr, nullptr) + 256;
 }
 
 int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t* dims, const float* const* packed_in,
@@ -335,89 +372,121 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   p->dims.assign(dims, dims + n);
   Carve c(ws, ws_bytes);
   std::vector<InvMat> mats;
-  std::vector<int32_t> small, blocked;
-  int64_t items_total, piv_total, pan_total;
-  inverse_carve(n, dims, c, p, &mats, &small, &blocked, &p->plane_rows, &items_total, &piv_total, &pan_total,
-                &p->steps);
-  p->panA = c.take<float>(size_t(2) * p->plane_rows * kB);
-  p->panC = c.take<float>(size_t(2) * p->plane_rows * kB);
-  p->mats = c.take<InvMat>(size_t(n));
-  p->small_ids = c.take<int32_t>(size_t(n));
-  p->blocked_ids = c.take<int32_t>(size_t(n));
-  p->piv_ids = c.take<int32_t>(size_t(piv_total));
-  p->pan_jobs = c.take<PanelJob>(size_t(pan_total));
-  p->maps = c.take<CUtensorMap>(2, 128);
-  p->items = c.take<TcItem>(size_t(items_total));
-  p->epis = c.take<TcEpi>(size_t(n));
+  inverse_carve(n, dims, c, p, &mats);
   if (!c.ok() || !ws) {
     delete p;
     set_error("inverse workspace too small: need %zu bytes, got %zu", c.used, ws_bytes);
     return SPDKFAC_ERR_ARG;
   }
+  std::vector<int32_t> small, blocked;
+  p->max_rows = 0;
   for (int t = 0; t < n; ++t) {
     mats[t].in = packed_in[t];
     mats[t].out = out_full[t];
     mats[t].info = info_dev + t;
-  }
-  p->n_small = int(small.size());
-  for (int t = 0; t < n; ++t) {
     const double d3 = double(dims[t]) * dims[t] * dims[t];
     p->algo_flops += d3;
-    if (dims[t] <= kB) p->small_flops += d3;
+    if (dims[t] <= kB) {
+      small.push_back(t);
+      p->small_flops += d3;
+    } else {
+      blocked.push_back(t);
+      p->max_rows = std::max(p->max_rows, mats[t].dp);
+    }
   }
+  p->n_small = int(small.size());
   p->n_blocked = int(blocked.size());
-  // per-step schedules
-  std::vector<int32_t> piv_ids;
-  std::vector<PanelJob> pan;
+  const int64_t plane = p->plane_rows * kB;
+  std::vector<TcEpi> epis(size_t(2) * n);
+  for (int t = 0; t < n; ++t) {
+    epis[t] = TcEpi{mats[t].W, mats[t].dp, 0, -1.f, 1.f, kAxpby, 0, nullptr, 0, 0};            // update
+    epis[n + t] = TcEpi{mats[t].W, mats[t].dp, 0, 1.f, 0.f, kAxpby, 0, p->panC, kB, plane};    // panel
+  }
+  std::vector<TileJob> tiles;
+  for (int t : blocked) {
+    const int T32 = mats[t].dp / 32;
+    for (int I = 0; I < T32; ++I)
+      for (int J = I; J < T32; ++J) tiles.push_back(TileJob{t, I, J, 0});
+  }
+  std::vector<int32_t> act;
   std::vector<TcItem> items;
-  std::vector<TcEpi> epis(n);
-  for (int t = 0; t < n; ++t)
-    epis[t] = TcEpi{mats[t].W, mats[t].dp, 0, -1.f, 1.f, kAxpby, 0};
+  std::vector<PanelJob> pan;
   for (int k = 0; k < p->steps; ++k) {
-    p->piv_off.push_back(int(piv_ids.size()));
-    p->pan_off.push_back(int(pan.size()));
-    p->upd_off.push_back(int(items.size()));
-    for (int t : blocked) {
+    p->act_off.push_back(int(act.size()));
+    for (int t : blocked)
+      if (k < mats[t].dp / kB) act.push_back(t);
+    p->act_cnt.push_back(int(act.size()) - p->act_off.back());
+    p->pan_off.push_back(int(items.size()));
+    p->pj_off.push_back(int(pan.size()));
+    for (int t : blocked) {  // panel GEMM: C_R = Wold[R,K] P^-1, stored into the upper block triangle
       const int T = mats[t].dp / kB;
       if (k >= T) continue;
-      piv_ids.push_back(t);
-      for (int r = 0; r < T; ++r)
-        if (r != k) pan.push_back(PanelJob{t, r});
+      for (int R = 0; R < T; ++R) {
+        if (R == k) continue;
+        pan.push_back(PanelJob{t, R});
+        const int prow = mats[t].panel_row0 + R * kB;
+        TcItem it{};
+        it.k0 = 0;
+        it.nk = kB / 32;
+        it.epi = n + t;
+        it.m_valid = kB;
+        it.n_valid = kB;
+        it.o2_row = prow;
+        if (R < k) {  // D'[j][i] = (P^-1 Wold[R,K]^T)[j][i] = C_R[i][j] -> W[R0 + i][K0 + j], panC coalesced
+          it.a_map = 2, it.a_row = mats[t].slot * kB;
+          it.b_map = 0, it.b_row = prow;
+          it.out_r = k * kB, it.out_c = R * kB;
+          it.flags = 0;
+        } else {      // D[i][j] = C_R[i][j] -> W[K0 + j][R0 + i] (row panel), panC row-style
+          it.a_map = 0, it.a_row = prow;
+          it.b_map = 2, it.b_row = mats[t].slot * kB;
+          it.out_r = R * kB, it.out_c = k * kB;
+          it.flags = kOut2Rows;
+        }
+        items.push_back(it);
+      }
+    }
+    p->pan_cnt.push_back(int(items.size()) - p->pan_off.back());
+    p->upd_off.push_back(int(items.size()));
+    for (int t : blocked) {  // trailing update: W[I,J] -= Wold[I,K] C_J^T
+      const int T = mats[t].dp / kB;
+      if (k >= T) continue;
       for (int I = 0; I < T; ++I)
         for (int J = I; J < T; ++J) {
           if (I == k || J == k) continue;
+          // D'[y][x] = sum_k Wold[J0+y][k] C[I0+x][k] = U[I0+x][J0+y] (U symmetric):
+          // the coalesced transposed store lands on the upper block W[I, J]
           TcItem it{};
           it.a_map = 0;
           it.b_map = 1;
-          it.a_row = mats[t].panel_row0 + I * kB;
-          it.b_row = mats[t].panel_row0 + J * kB;
+          it.a_row = mats[t].panel_row0 + J * kB;
+          it.b_row = mats[t].panel_row0 + I * kB;
           it.k0 = 0;
           it.nk = kB / 32;
           it.epi = t;
-          it.flags = (I == J) ? 0 : kMirror;
-          it.out_r = I * kB;
-          it.out_c = J * kB;
+          it.flags = 0;
+          it.out_r = J * kB;
+          it.out_c = I * kB;
           it.m_valid = kB;
           it.n_valid = kB;
           items.push_back(it);
         }
     }
-    p->piv_cnt.push_back(int(piv_ids.size()) - p->piv_off.back());
-    p->pan_cnt.push_back(int(pan.size()) - p->pan_off.back());
     p->upd_cnt.push_back(int(items.size()) - p->upd_off.back());
   }
-  std::vector<CUtensorMap> maps(2);
+  std::vector<CUtensorMap> maps(3);
   int rc = SPDKFAC_OK;
-  if (p->plane_rows > 0) {
+  if (p->n_blocked > 0) {
     if ((rc = make_operand_map(&maps[0], p->panA, false, kB, p->plane_rows, kB)) ||
-        (rc = make_operand_map(&maps[1], p->panC, false, kB, p->plane_rows, kB))) {
+        (rc = make_operand_map(&maps[1], p->panC, false, kB, p->plane_rows, kB)) ||
+        (rc = make_operand_map(&maps[2], p->pinvS, false, kB, int64_t(p->n_blocked) * kB, kB))) {
       delete p;
       return rc;
     }
   }
   if ((rc = upload(p->mats, mats, s)) || (rc = upload(p->small_ids, small, s)) ||
-      (rc = upload(p->blocked_ids, blocked, s)) || (rc = upload(p->piv_ids, piv_ids, s)) ||
-      (rc = upload(p->pan_jobs, pan, s)) || (p->plane_rows > 0 && (rc = upload(p->maps, maps, s))) ||
+      (rc = upload(p->blocked_ids, blocked, s)) || (rc = upload(p->act_ids, act, s)) ||
+      (rc = upload(p->tiles, tiles, s)) || (rc = upload(p->pan_jobs, pan, s)) || (p->n_blocked > 0 && (rc = upload(p->maps, maps, s))) ||
       (rc = upload(p->items, items, s)) || (rc = upload(p->epis, epis, s))) {
     delete p;
     return rc;
@@ -425,7 +494,6 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   static bool attrs = false;
   if (!attrs) {
     SPD_CUDA(cudaFuncSetAttribute(small_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kB * kSmemLd * 4));
-    SPD_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kB * kSmemLd * 4));
     attrs = true;
   }
   *out = p;
@@ -443,31 +511,31 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
     stat_end(kCatInvSmall, s, p->small_flops, 0);
   }
   if (p->n_blocked > 0) {
+    const int64_t plane = p->plane_rows * kB;
     stat_begin(kCatInvUnpackFinal, s);
-    damp_unpack_kernel<<<dim3(64, p->n_blocked), 256, 0, s>>>(p->mats, p->blocked_ids, gamma);
+    damp_unpack_kernel<<<p->n_tiles, 256, 0, s>>>(p->mats, p->tiles, gamma);
     SPD_CHECK_LAUNCH();
     stat_end(kCatInvUnpackFinal, s, 0, 0);
     for (int k = 0; k < p->steps; ++k) {
-      if (p->piv_cnt[k] > 0) {
-        stat_begin(kCatInvPivot, s);
-        pivot_kernel<<<p->piv_cnt[k], 512, 0, s>>>(p->mats, p->piv_ids + p->piv_off[k], k);
-        SPD_CHECK_LAUNCH();
-        stat_end(kCatInvPivot, s, 2.0 * kB * kB * kB * p->piv_cnt[k], 0);
-      }
-      if (p->pan_cnt[k] > 0) {
-        stat_begin(kCatInvPanel, s);
-        panel_kernel<<<p->pan_cnt[k], 256, 2 * kB * kSmemLd * 4, s>>>(p->mats, p->pan_jobs + p->pan_off[k], k,
-                                                                        p->panA, p->panC, p->plane_rows);
-        SPD_CHECK_LAUNCH();
-        stat_end(kCatInvPanel, s, 2.0 * kB * kB * kB * p->pan_cnt[k], 0);
-      }
+      const int na = p->act_cnt[k];
+      stat_begin(kCatInvPivot, s);
+      pivot_kernel<<<na, 512, 0, s>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
+                                      int64_t(p->n_blocked) * kB * kB);
+      SPD_CHECK_LAUNCH();
+      stat_end(kCatInvPivot, s, 2.0 * kB * kB * kB * na, 0);
+      stat_begin(kCatInvPanel, s);
+      stage_panel_kernel<<<p->pan_cnt[k], 256, 0, s>>>(p->mats, p->pan_jobs + p->pj_off[k], k, p->panA, plane);
+      SPD_CHECK_LAUNCH();
+      int rc = launch_tc3(Kind::TF32, p->maps, p->items + p->pan_off[k], p->epis, p->pan_cnt[k], s);
+      if (rc) return rc;
+      stat_end(kCatInvPanel, s, 2.0 * kB * kB * kB * p->pan_cnt[k], 0);
       stat_begin(kCatInvUpdate, s);
-      int rc = launch_tc3(Kind::TF32, p->maps, p->items + p->upd_off[k], p->epis, p->upd_cnt[k], s);
+      rc = launch_tc3(Kind::TF32, p->maps, p->items + p->upd_off[k], p->epis, p->upd_cnt[k], s);
       if (rc) return rc;
       stat_end(kCatInvUpdate, s, 2.0 * kB * kB * kB * p->upd_cnt[k], 0);
     }
     stat_begin(kCatInvUnpackFinal, s);
-    finalize_kernel<<<dim3(64, p->n_blocked), 256, 0, s>>>(p->mats, p->blocked_ids);
+    finalize_kernel<<<p->n_tiles, 256, 0, s>>>(p->mats, p->tiles);
     SPD_CHECK_LAUNCH();
     stat_end(kCatInvUnpackFinal, s, 0, 0);
   }

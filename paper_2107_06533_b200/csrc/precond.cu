@@ -181,8 +181,8 @@ int spdkfac_precond_plan_create(spdkfac_precond_plan** out, int n, const int32_t
       delete p;
       return rc;
     }
-    epis[2 * l] = TcEpi{p->tT[l], ldo, k * ldo, 1.f, 0.f, kSplitBf16, 0};
-    epis[2 * l + 1] = TcEpi{p->P[l], k, 0, 1.f, 0.f, kAxpby, 0};
+    epis[2 * l] = TcEpi{p->tT[l], ldo, k * ldo, 1.f, 0.f, kSplitBf16, 0, nullptr, 0, 0};
+    epis[2 * l + 1] = TcEpi{p->P[l], k, 0, 1.f, 0.f, kAxpby, 0, nullptr, 0, 0};
     for (int mb = 0; mb < cdiv(m, 128); ++mb)
       for (int nb = 0; nb < cdiv(k, 128); ++nb) {
         TcItem a{};

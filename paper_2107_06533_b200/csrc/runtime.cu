@@ -104,7 +104,14 @@ static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi
     SPD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmemBytes)));
     attr_set = true;
   }
-  tc3_gemm_kernel<K><<<n, 128, kTcSmemBytes, s>>>(maps, items, epis, run);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    SPD_CUDA(cudaGetDevice(&dev));
+    SPD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int grid = n < sms ? n : sms;
+  tc3_gemm_kernel<K><<<grid, 192, kTcSmemBytes, s>>>(maps, items, epis, run, n);
   SPD_CHECK_LAUNCH();
   return SPDKFAC_OK;
 }

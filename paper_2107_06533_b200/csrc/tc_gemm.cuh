@@ -27,9 +27,13 @@ struct TcItem {
   int32_t flags;         // kSameAB | kMirror
   int32_t out_r, out_c;  // D[i][j] -> target element (out_c + j, out_r + i) (transposed store)
   int32_t m_valid, n_valid;
+  int32_t o2_row;  // row offset of the optional second target (TcEpi::out2)
+  int32_t pad_;
 };
 constexpr int32_t kSameAB = 1;  // B tile == A tile (diagonal SYRK tile): load once
 constexpr int32_t kMirror = 2;  // also update target (out_r + i, out_c + j) (symmetric off-diagonal tile)
+constexpr int32_t kOut2Rows = 4;  // out2 row-style: out2[(o2_row + i) * ld2 + j]; else transposed:
+                                  // out2[(o2_row + j) * ld2 + i] (coalesced along the TMEM lanes)
 
 enum EpiMode : int32_t {
   kAxpby = 0,      // out = beta*out + alpha*D   (fp32 target)
@@ -56,177 +60,239 @@ struct TcEpi {
   float alpha, beta;
   int32_t mode;
   int32_t pad_;
+  // optional second target (kAxpby only): tf32 split planes, row (a_row + i), column j:
+  // out2[(a_row + i) * ld2 + j] = hi(alpha*D), out2[... + plane2] = lo(alpha*D)
+  float* out2;
+  int64_t ld2, plane2;
 };
 
+// Epilogue of one 32-column chunk of the accumulator tile: thread row i (TMEM lane),
+// values v[t] = D[i][c*32 + t].  All global reads of a chunk are issued before any
+// store (independent addresses), so read-modify-write targets pay one memory latency
+// per chunk, not per element.
+__device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep, const TcRun& run, int i, int c,
+                                               const float (&v)[32]) {
+  const bool row_ok = i < it.m_valid;
+  const int64_t ri = int64_t(it.out_r) + i;
+  const int jn = it.n_valid - c * 32;  // valid columns in this chunk (may exceed 32)
+  if (ep.mode == kAxpby) {
+    float* out = static_cast<float*>(ep.out);
+    float* base = out + (int64_t(it.out_c) + c * 32) * ep.ld + ri;  // transposed: column j -> row of target
+    float old[32];
+    if (ep.beta != 0.f) {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) old[t] = (row_ok && t < jn) ? base[int64_t(t) * ep.ld] : 0.f;
+    }
+#pragma unroll
+    for (int t = 0; t < 32; ++t)
+      if (row_ok && t < jn) base[int64_t(t) * ep.ld] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + ep.alpha * v[t];
+    if (it.flags & kMirror) {  // same values, target row ri, 32 contiguous columns
+      float* rowp = out + ri * ep.ld + it.out_c + c * 32;
+      if (ep.beta != 0.f) {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) old[t] = (row_ok && t < jn) ? rowp[t] : 0.f;
+      }
+#pragma unroll
+      for (int t = 0; t < 32; ++t)
+        if (row_ok && t < jn) rowp[t] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + ep.alpha * v[t];
+    }
+    if (ep.out2 != nullptr && row_ok) {
+      if (it.flags & kOut2Rows) {
+        float* o2 = ep.out2 + (int64_t(it.o2_row) + i) * ep.ld2 + c * 32;
+#pragma unroll
+        for (int t = 0; t < 32; t += 4) {
+          float h[4], l[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) split_tf32(ep.alpha * v[t + u], h[u], l[u]);
+          *reinterpret_cast<float4*>(o2 + t) = make_float4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<float4*>(o2 + ep.plane2 + t) = make_float4(l[0], l[1], l[2], l[3]);
+        }
+      } else {
+        float* o2 = ep.out2 + (int64_t(it.o2_row) + c * 32) * ep.ld2 + i;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          if (t < jn) {
+            float h, l;
+            split_tf32(ep.alpha * v[t], h, l);
+            o2[int64_t(t) * ep.ld2] = h;
+            o2[int64_t(t) * ep.ld2 + ep.plane2] = l;
+          }
+        }
+      }
+    }
+  } else if (ep.mode == kSplitBf16) {
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(ep.out);
+    const int64_t o0 = (int64_t(it.out_c) + c * 32) * ep.ld + ri;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      if (row_ok && t < jn) {
+        __nv_bfloat16 h, l;
+        split_bf16(ep.alpha * v[t], h, l);
+        out[o0 + int64_t(t) * ep.ld] = h;
+        out[o0 + int64_t(t) * ep.ld + ep.plane_stride] = l;
+      }
+    }
+  } else if (ep.mode == kSplitTf32) {
+    float* out = static_cast<float*>(ep.out);
+    const int64_t o0 = (int64_t(it.out_c) + c * 32) * ep.ld + ri;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      if (row_ok && t < jn) {
+        float h, l;
+        split_tf32(ep.alpha * v[t], h, l);
+        out[o0 + int64_t(t) * ep.ld] = h;
+        out[o0 + int64_t(t) * ep.ld + ep.plane_stride] = l;
+      }
+    }
+  } else {  // kPackedUpper: global row gi = out_r + i, columns gj = out_c + c*32 + t, keep gj >= gi
+    float* out = static_cast<float*>(run.out);
+    const int64_t gi = ri, d = run.d;
+    const int64_t gj0 = int64_t(it.out_c) + c * 32;
+    float* rowp = out + gi * (2 * d - gi + 1) / 2 - gi;  // packed index of (gi, gj) = rowp + gj
+    float old[32];
+    if (run.decay != 0.f) {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) old[t] = (row_ok && t < jn && gj0 + t >= gi) ? rowp[gj0 + t] : 0.f;
+    }
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      if (row_ok && t < jn && gj0 + t >= gi) {
+        const float fresh = run.alpha * v[t];
+        const float nv = run.decay != 0.f ? run.decay * old[t] + (1.f - run.decay) * fresh : fresh;
+        rowp[gj0 + t] = run.wscale * nv;
+      }
+    }
+  }
+}
+
+// Persistent, warp-specialised tile engine: grid <= #SMs, CTA b processes items b, b+grid, ...
+//   warp 0      TMA producer (one lane), kStages-deep smem ring
+//   warp 1      MMA issuer (one lane) + TMEM owner; two 128-column accumulators so the
+//               next tile's MMAs run while the epilogue drains the previous one
+//   warps 2..5  epilogue (warp w drains TMEM lanes [32 (w % 4), +32))
 template <Kind K>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(192, 1)
     tc3_gemm_kernel(const CUtensorMap* __restrict__ maps, const TcItem* __restrict__ items,
-                    const TcEpi* __restrict__ epis, const TcRun run) {
+                    const TcEpi* __restrict__ epis, const TcRun run, int n_items) {
   constexpr int BK = (K == Kind::BF16) ? 64 : 32;  // one 128-byte swizzle row of K
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = empty + kStages;  // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const TcItem it = items[blockIdx.x];
-  const bool same = (it.flags & kSameAB) != 0;
   const int warp = warp_id();
   const int lane = lane_id();
-
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<128>(tmem_slot);
+  if (warp == 1) tmem_alloc<256>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0 && it.nk > 0) {  // ---- TMA producer
-      const CUtensorMap* am = maps + it.a_map;
-      const CUtensorMap* bm = maps + it.b_map;
-      tmap_acquire(am);
-      if (!same) tmap_acquire(bm);
-      const uint32_t bytes = same ? 2 * kTileBytes : 4 * kTileBytes;
-      for (int kb = 0; kb < it.nk; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&empty[s], ((kb / kStages) & 1) ^ 1);
-        mbar_expect_tx(&full[s], bytes);
-        uint8_t* st = smem + s * kStageBytes;
-        const int kc = it.k0 + kb * BK;
-        tma_load_3d(st, am, &full[s], kc, it.a_row, 0);
-        tma_load_3d(st + kTileBytes, am, &full[s], kc, it.a_row, 1);
-        if (!same) {
-          tma_load_3d(st + 2 * kTileBytes, bm, &full[s], kc, it.b_row, 0);
-          tma_load_3d(st + 3 * kTileBytes, bm, &full[s], kc, it.b_row, 1);
+    if (lane == 0) {  // ---- TMA producer
+      uint32_t g = 0;
+      int last_a = -1, last_b = -1;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const TcItem it = items[item];
+        const bool same = (it.flags & kSameAB) != 0;
+        const CUtensorMap* am = maps + it.a_map;
+        const CUtensorMap* bm = maps + it.b_map;
+        if (it.a_map != last_a) tmap_acquire(am), last_a = it.a_map;
+        if (!same && it.b_map != last_b) tmap_acquire(bm), last_b = it.b_map;
+        const uint32_t bytes = same ? 2 * kTileBytes : 4 * kTileBytes;
+        for (int kb = 0; kb < it.nk; ++kb, ++g) {
+          const uint32_t s = g % kStages;
+          mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
+          mbar_expect_tx(&full[s], bytes);
+          uint8_t* st = smem + s * kStageBytes;
+          const int kc = it.k0 + kb * BK;
+          tma_load_3d(st, am, &full[s], kc, it.a_row, 0);
+          tma_load_3d(st + kTileBytes, am, &full[s], kc, it.a_row, 1);
+          if (!same) {
+            tma_load_3d(st + 2 * kTileBytes, bm, &full[s], kc, it.b_row, 0);
+            tma_load_3d(st + 3 * kTileBytes, bm, &full[s], kc, it.b_row, 1);
+          }
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0 && it.nk > 0) {  // ---- MMA issuer
+    if (lane == 0) {  // ---- MMA issuer
       constexpr uint32_t idesc = make_idesc<K>(128, 128);
-      for (int kb = 0; kb < it.nk; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&full[s], (kb / kStages) & 1);
+      uint32_t g = 0, t = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
+        const TcItem it = items[item];
+        const bool same = (it.flags & kSameAB) != 0;
+        const uint32_t buf = t & 1, use = t >> 1;
+        mbar_wait(&tempty[buf], (use & 1) ^ 1);  // epilogue has drained this accumulator
         tc_fence_after();
-        uint8_t* st = smem + s * kStageBytes;
-        const uint64_t ahi = make_sdesc_sw128(st);
-        const uint64_t alo = make_sdesc_sw128(st + kTileBytes);
-        const uint64_t bhi = same ? ahi : make_sdesc_sw128(st + 2 * kTileBytes);
-        const uint64_t blo = same ? alo : make_sdesc_sw128(st + 3 * kTileBytes);
+        const uint32_t acc = tmem + buf * 128;
+        for (int kb = 0; kb < it.nk; ++kb, ++g) {
+          const uint32_t s = g % kStages;
+          mbar_wait(&full[s], (g / kStages) & 1);
+          tc_fence_after();
+          uint8_t* st = smem + s * kStageBytes;
+          const uint64_t ahi = make_sdesc_sw128(st);
+          const uint64_t alo = make_sdesc_sw128(st + kTileBytes);
+          const uint64_t bhi = same ? ahi : make_sdesc_sw128(st + 2 * kTileBytes);
+          const uint64_t blo = same ? alo : make_sdesc_sw128(st + 3 * kTileBytes);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 B of K per 128-B swizzle row
-          const uint64_t off = uint64_t(kk * 2);
-          umma<K>(tmem, ahi + off, bhi + off, idesc, (kb | kk) != 0);
-          umma<K>(tmem, ahi + off, blo + off, idesc, 1u);
-          umma<K>(tmem, alo + off, bhi + off, idesc, 1u);
+          for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 B of K per 128-B swizzle row
+            const uint64_t off = uint64_t(kk * 2);
+            umma<K>(acc, ahi + off, bhi + off, idesc, (kb | kk) != 0);
+            umma<K>(acc, ahi + off, blo + off, idesc, 1u);
+            umma<K>(acc, alo + off, bhi + off, idesc, 1u);
+          }
+          tc_commit(&empty[s]);  // smem slot free once these MMAs retire
         }
-        tc_commit(&empty[s]);  // smem slot free once these MMAs retire
+        tc_commit(&tfull[buf]);
       }
-      tc_commit(tfull);
     }
     __syncwarp();
-  }
-
-  // ---- epilogue: warp w owns TMEM lanes [32w, 32w+32) = tile rows.  All global
-  // reads of a 32-column chunk are issued before any store (independent addresses),
-  // so read-modify-write targets cost one memory latency per chunk, not per element.
-  const TcEpi ep = epis[it.epi];
-  const int i = warp * 32 + lane;
-  if (it.nk > 0) {
-    mbar_wait(tfull, 0);
-    tc_fence_after();
-  }
-  const bool row_ok = i < it.m_valid;
-  const int64_t ri = int64_t(it.out_r) + i;
+  } else {  // ---- epilogue warps 2..5
+    const int quad = warp & 3;
+    const int i = quad * 32 + lane;
+    uint32_t t = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
+      const TcItem it = items[item];
+      const TcEpi ep = epis[it.epi];
+      const uint32_t buf = t & 1, use = t >> 1;
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
 #pragma unroll 1
-  for (int c = 0; c < 4; ++c) {
-    if (c * 32 >= it.n_valid) break;  // warp-uniform
-    float v[32];
-    if (it.nk > 0) {
-      tmem_ld_32x32b_x32(tmem + (uint32_t(warp * 32) << 16) + uint32_t(c * 32), v);
-    } else {
+      for (int c = 0; c < 4; ++c) {
+        if (c * 32 >= it.n_valid) break;  // uniform
+        float v[32];
+        if (it.nk > 0) {
+          tmem_ld_32x32b_x32(tmem + buf * 128 + (uint32_t(quad * 32) << 16) + uint32_t(c * 32), v);
+        } else {
 #pragma unroll
-      for (int t = 0; t < 32; ++t) v[t] = 0.f;
-    }
-    const int jn = it.n_valid - c * 32;  // valid columns in this chunk (may exceed 32)
-    if (ep.mode == kAxpby) {
-      float* out = static_cast<float*>(ep.out);
-      float* base = out + (int64_t(it.out_c) + c * 32) * ep.ld + ri;  // transposed: column j -> row of target
-      float old[32];
-      if (ep.beta != 0.f) {
-#pragma unroll
-        for (int t = 0; t < 32; ++t) old[t] = (row_ok && t < jn) ? base[int64_t(t) * ep.ld] : 0.f;
-      }
-#pragma unroll
-      for (int t = 0; t < 32; ++t)
-        if (row_ok && t < jn) base[int64_t(t) * ep.ld] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + ep.alpha * v[t];
-      if (it.flags & kMirror) {  // same values, target row ri, 32 contiguous columns
-        float* rowp = out + ri * ep.ld + it.out_c + c * 32;
-        if (ep.beta != 0.f) {
-#pragma unroll
-          for (int t = 0; t < 32; ++t) old[t] = (row_ok && t < jn) ? rowp[t] : 0.f;
+          for (int u = 0; u < 32; ++u) v[u] = 0.f;
         }
-#pragma unroll
-        for (int t = 0; t < 32; ++t)
-          if (row_ok && t < jn) rowp[t] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + ep.alpha * v[t];
+        epilogue_chunk(it, ep, run, i, c, v);
       }
-    } else if (ep.mode == kSplitBf16) {
-      __nv_bfloat16* out = static_cast<__nv_bfloat16*>(ep.out);
-      const int64_t o0 = (int64_t(it.out_c) + c * 32) * ep.ld + ri;
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        if (row_ok && t < jn) {
-          __nv_bfloat16 h, l;
-          split_bf16(ep.alpha * v[t], h, l);
-          out[o0 + int64_t(t) * ep.ld] = h;
-          out[o0 + int64_t(t) * ep.ld + ep.plane_stride] = l;
-        }
-      }
-    } else if (ep.mode == kSplitTf32) {
-      float* out = static_cast<float*>(ep.out);
-      const int64_t o0 = (int64_t(it.out_c) + c * 32) * ep.ld + ri;
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        if (row_ok && t < jn) {
-          float h, l;
-          split_tf32(ep.alpha * v[t], h, l);
-          out[o0 + int64_t(t) * ep.ld] = h;
-          out[o0 + int64_t(t) * ep.ld + ep.plane_stride] = l;
-        }
-      }
-    } else {  // kPackedUpper: global row gi = out_r + i, columns gj = out_c + c*32 + t, keep gj >= gi
-      float* out = static_cast<float*>(run.out);
-      const int64_t gi = ri, d = run.d;
-      const int64_t gj0 = int64_t(it.out_c) + c * 32;
-      float* rowp = out + gi * (2 * d - gi + 1) / 2 - gi;  // packed index of (gi, gj) = rowp + gj
-      float old[32];
-      if (run.decay != 0.f) {
-#pragma unroll
-        for (int t = 0; t < 32; ++t) old[t] = (row_ok && t < jn && gj0 + t >= gi) ? rowp[gj0 + t] : 0.f;
-      }
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        if (row_ok && t < jn && gj0 + t >= gi) {
-          const float fresh = run.alpha * v[t];
-          const float nv = run.decay != 0.f ? run.decay * old[t] + (1.f - run.decay) * fresh : fresh;
-          rowp[gj0 + t] = run.wscale * nv;
-        }
-      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_free<128>(tmem);
+  if (warp == 1) tmem_free<256>(tmem);
 }
 
 }  // namespace spd
