@@ -51,15 +51,18 @@ SPDKFAC_API int spdkfac_version(void);
 /* 1 iff the current device is sm_100 (B200) and the kernels can launch. */
 SPDKFAC_API int spdkfac_device_supported(void);
 
-/* Launch accounting for benchmarks: every kernel launch is counted; with
- * timing != 0 each launch is bracketed by CUDA events on its own stream.
+/* Launch accounting for benchmarks: every kernel launch is counted; launches
+ * of the categories in `timing_mask` (bit c = category c, -1 = all) are
+ * bracketed by CUDA events on their own stream (events pre-created with
+ * spdkfac_stats_reserve so that timing adds no driver allocation).
  * Categories: 0 factor stage (im2col/transpose + split), 1 factor SYRK
  * (tcgen05), 2 factor reduce+pack, 3 small inverse, 4 pivot inverse,
  * 5 panel, 6 inverse update (tcgen05), 7 inverse unpack/finalize,
  * 8 precondition split, 9 precondition GEMMs (tcgen05), 10 update apply,
  * 11 pack/unpack.  flops = algorithmic flops; stats_read
  * synchronises on the recorded events. */
-SPDKFAC_API void spdkfac_stats_reset(int timing);
+SPDKFAC_API void spdkfac_stats_reset(int timing_mask);
+SPDKFAC_API int spdkfac_stats_reserve(int n_launches);
 SPDKFAC_API uint64_t spdkfac_stats_launches(void);
 SPDKFAC_API int spdkfac_stats_read(int category, double* ms, int64_t* launches, double* flops, double* bytes);
 

@@ -34,6 +34,7 @@ SIGNATURES = {
     "spdkfac_device_supported": (C.c_int, []),
     "spdkfac_stats_reset": (None, [C.c_int]),
     "spdkfac_stats_launches": (C.c_uint64, []),
+    "spdkfac_stats_reserve": (C.c_int, [C.c_int]),
     "spdkfac_stats_read": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(_i64), C.POINTER(C.c_double),
                                      C.POINTER(C.c_double)]),
     "spdkfac_factor_dims": (C.c_int, [C.POINTER(FactorGeom), C.POINTER(_i64), C.POINTER(_i64)]),
@@ -90,8 +91,20 @@ STAT_CATEGORIES = ("factor_stage", "factor_syrk", "factor_reduce", "inv_small", 
                    "inv_update", "inv_unpack_finalize", "precond_split", "precond_gemm", "precond_apply", "pack")
 
 
-def stats_reset(timing: bool = False) -> None:
-    load().spdkfac_stats_reset(1 if timing else 0)
+def stats_reset(timing=False, reserve: int = 0) -> None:
+    """timing: False / True (all categories) / iterable of category names."""
+    if timing is True:
+        mask = -1
+    elif not timing:
+        mask = 0
+    else:
+        mask = 0
+        for name in timing:
+            mask |= 1 << STAT_CATEGORIES.index(name)
+    lib = load()
+    if reserve:
+        check(lib.spdkfac_stats_reserve(int(reserve)), "stats reserve")
+    lib.spdkfac_stats_reset(mask)
 
 
 def stats() -> dict:

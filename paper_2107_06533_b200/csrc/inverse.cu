@@ -38,46 +38,89 @@ struct TileJob {  // one 32 x 32 tile (I <= J) of a blocked matrix, for unpack/f
   int32_t mat, ti, tj, pad_;
 };
 
-// Register-resident scalar sweep of one 128 x 128 block by 512 threads: thread t owns
-// row i = t & 127, columns [32q, 32q + 32), q = t >> 7 (warp-uniform), in registers.  Per pivot k the four
-// owners of row k publish it to shared memory (double-buffered by k parity, rows skewed by
-// 4 floats per 32 so the four column quarters hit distinct banks); every thread then
-// applies  a_ij -= (a_ik / p) a_kj,  a_ik <- a_ik / p,  a_kj <- a_kj / p,  a_kk <- -1/p,
-// using a_ik = a_ki (the swept block stays symmetric to rounding).  Rows/columns >= n are
-// identity padding and are never pivots.  Returns -1, or the failing pivot (uniform).
-constexpr int kRowSkew = 36;  // skewed row buffer: element j at (j >> 5) * 36 + (j & 31)
-
-__device__ __forceinline__ int sweep128(float (&a)[32], int n, float* rbuf /* 2 x 4*36 */) {
+// Register-resident sweep of one 128 x 128 block by 512 threads: thread t owns row
+// i = t & 127, columns [32q, 32q + 32), q = t >> 7 (warp-uniform), in registers.
+// Blocked form used by the kernels: pivots are swept four at a time.  The owners of the four
+// pivot rows publish them column-interleaved (R[j] = (a_K0j, a_K0+1,j, a_K0+2,j, a_K0+3,j));
+// every thread sweeps the 4x4 pivot block S = -P4^-1 in registers (its four scalar pivots are
+// the same Schur pivots as the scalar sweep, so the failing index is exact) and applies the
+// rank-4 update  a_ij <- alpha_i a_ij - sum_t w_i[t] R[j].t  with
+//   i not in K: alpha = 1, w_i = A[i,K] P4^-1           (A[i,K] = R[i] by symmetry)
+//   i in K    : alpha = 0, w_i = S[i - K0, :]            (new pivot rows P4^-1 A[K,j])
+// followed by the column fix-up A[i,K] <- w_i (i not in K), A[K,K] <- S.
+// n <= 128; rows/columns >= n are identity padding.  Returns -1 or the failing pivot.
+__device__ __forceinline__ int sweep128_b4(float (&a)[32], int n, float4* rbuf /* 2 x 128 */) {
   const int t = threadIdx.x, i = t & 127, q = t >> 7;
-  for (int k = 0; k < n; ++k) {
-    float* rk = rbuf + (k & 1) * (4 * kRowSkew);
-    if (i == k) {
+  const int nb = (n + 3) >> 2;
+  for (int kb = 0; kb < nb; ++kb) {
+    float4* R = rbuf + (kb & 1) * 128;
+    const int K0 = kb * 4;
+    const int s0 = i - K0;  // pivot-row index of this thread's row, if 0..3
+    if (s0 >= 0 && s0 < 4) {
+      float* Rf = reinterpret_cast<float*>(R);
 #pragma unroll
-      for (int jj = 0; jj < 32; jj += 4)
-        *reinterpret_cast<float4*>(rk + q * kRowSkew + jj) = make_float4(a[jj], a[jj + 1], a[jj + 2], a[jj + 3]);
+      for (int jj = 0; jj < 32; ++jj) Rf[(q * 32 + jj) * 4 + s0] = a[jj];
     }
     __syncthreads();
-    const float p = rk[(k >> 5) * kRowSkew + (k & 31)];
-    if (!(p > 0.f)) return k;  // dpotrf's "ajj <= 0 or NaN" test, on the same Schur pivots
-    const float pinv = __frcp_rn(p);
-    const float ci = rk[(i >> 5) * kRowSkew + (i & 31)] * pinv;  // a_ik / p
-    const int kq = k >> 5, kj = k & 31;
-    if (i == k) {
+    // 4x4 pivot block, swept in registers (identical in every thread)
+    float S[4][4];
 #pragma unroll
-      for (int jj = 0; jj < 32; ++jj) a[jj] = (q == kq && jj == kj) ? -pinv : a[jj] * pinv;
-    } else {
+    for (int c = 0; c < 4; ++c) {
+      const float4 v = R[K0 + c];
+      S[0][c] = v.x, S[1][c] = v.y, S[2][c] = v.z, S[3][c] = v.w;
+    }
 #pragma unroll
-      for (int jj = 0; jj < 32; jj += 4) {
-        const float4 r = *reinterpret_cast<const float4*>(rk + q * kRowSkew + jj);
-        a[jj + 0] = fmaf(-ci, r.x, a[jj + 0]);
-        a[jj + 1] = fmaf(-ci, r.y, a[jj + 1]);
-        a[jj + 2] = fmaf(-ci, r.z, a[jj + 2]);
-        a[jj + 3] = fmaf(-ci, r.w, a[jj + 3]);
-      }
-      if (q == kq) {  // column k: a_ik <- a_ik / p
+    for (int p = 0; p < 4; ++p) {
+      const float piv = S[p][p];
+      if (!(piv > 0.f)) return K0 + p;  // dpotrf's test on the same Schur pivot (uniform)
+      const float pinv = __frcp_rn(piv);
+      float rowp[4], colp[4];
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj)
-          if (jj == kj) a[jj] = ci;
+      for (int c = 0; c < 4; ++c) rowp[c] = S[p][c], colp[c] = S[c][p];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (r == p && c == p) S[r][c] = -pinv;
+          else if (r == p) S[r][c] = rowp[c] * pinv;
+          else if (c == p) S[r][c] = colp[r] * pinv;
+          else S[r][c] = fmaf(-colp[r] * pinv, rowp[c], S[r][c]);
+        }
+    }
+    // weights of this thread's row
+    const bool in_k = (s0 >= 0 && s0 < 4);
+    float w[4];
+    const float4 ri = R[i];
+    const float rv[4] = {ri.x, ri.y, ri.z, ri.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      // ci[c] = sum_s A[i][K0+s] P4^-1[s][c] = -sum_s rv[s] S[s][c]
+      float ci = -(rv[0] * S[0][c] + rv[1] * S[1][c] + rv[2] * S[2][c] + rv[3] * S[3][c]);
+      float sr = S[0][c];
+      if (s0 == 1) sr = S[1][c];
+      if (s0 == 2) sr = S[2][c];
+      if (s0 == 3) sr = S[3][c];
+      w[c] = in_k ? sr : ci;
+    }
+    const float alpha = in_k ? 0.f : 1.f;
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+      const float4 rj = R[q * 32 + jj];
+      float v = alpha * a[jj];
+      v = fmaf(-w[0], rj.x, v);
+      v = fmaf(-w[1], rj.y, v);
+      v = fmaf(-w[2], rj.z, v);
+      v = fmaf(-w[3], rj.w, v);
+      a[jj] = v;
+    }
+    if (q == (K0 >> 5)) {  // warp-uniform: fix the four pivot columns of this quarter
+      switch ((K0 & 31) >> 2) {
+#define SPD_FIX(C)                                       \
+  case C:                                                \
+    a[4 * C + 0] = w[0], a[4 * C + 1] = w[1], a[4 * C + 2] = w[2], a[4 * C + 3] = w[3]; \
+    break;
+        SPD_FIX(0) SPD_FIX(1) SPD_FIX(2) SPD_FIX(3) SPD_FIX(4) SPD_FIX(5) SPD_FIX(6) SPD_FIX(7)
+#undef SPD_FIX
       }
     }
   }
@@ -92,7 +135,7 @@ __device__ __forceinline__ float packed_at(const float* p, int64_t d, int64_t i,
 // ---------------------------------------------------------------- d <= 128
 __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __restrict__ mats,
                                                             const int32_t* __restrict__ ids, float gamma) {
-  __shared__ __align__(16) float rbuf[2 * 4 * kRowSkew];
+  __shared__ float4 rbuf[2 * 128];
   const InvMat m = mats[ids[blockIdx.x]];
   const int n = m.d;
   const int i = threadIdx.x & 127, q = threadIdx.x >> 7;
@@ -102,7 +145,7 @@ __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __rest
     const int j = q * 32 + jj;
     a[jj] = (i < n && j < n) ? packed_at(m.in, n, i, j) + (i == j ? gamma : 0.f) : (i == j ? 1.f : 0.f);
   }
-  const int f = sweep128(a, n, rbuf);
+  const int f = sweep128_b4(a, n, rbuf);
   if (f >= 0) {
     if (threadIdx.x == 0) *m.info = f + 1;
     return;
@@ -154,7 +197,7 @@ __global__ void __launch_bounds__(256) damp_unpack_kernel(const InvMat* __restri
 __global__ void __launch_bounds__(512) pivot_kernel(const InvMat* __restrict__ mats,
                                                     const int32_t* __restrict__ ids, int k,
                                                     float* __restrict__ pinv_planes, int64_t pinv_plane) {
-  __shared__ __align__(16) float rbuf[2 * 4 * kRowSkew];
+  __shared__ float4 rbuf[2 * 128];
   const InvMat m = mats[ids[blockIdx.x]];
   if (*m.info != 0) return;
   const int64_t dp = m.dp, K0 = int64_t(k) * kB;
@@ -166,7 +209,7 @@ __global__ void __launch_bounds__(512) pivot_kernel(const InvMat* __restrict__ m
     const float4 v = *reinterpret_cast<const float4*>(src + jj);
     a[jj] = v.x, a[jj + 1] = v.y, a[jj + 2] = v.z, a[jj + 3] = v.w;
   }
-  const int f = sweep128(a, kB, rbuf);
+  const int f = sweep128_b4(a, kB, rbuf);
   if (f >= 0) {
     if (threadIdx.x == 0) *m.info = int(K0) + f + 1;
     return;

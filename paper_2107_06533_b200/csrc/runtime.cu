@@ -27,7 +27,7 @@ struct StatRec {
 std::mutex g_stat_mu;
 std::vector<StatRec> g_recs;
 size_t g_rec_used = 0;
-bool g_timing = false;
+uint32_t g_timing = 0;  // bitmask of timed categories
 std::atomic<uint64_t> g_launches{0};
 uint64_t g_cat_launches[kNumCats] = {};
 double g_cat_flops[kNumCats] = {}, g_cat_bytes[kNumCats] = {};
@@ -36,7 +36,7 @@ thread_local long g_open = -1;
 
 void stat_begin(int cat, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (!g_timing) return;
+  if (!(g_timing & (1u << cat))) return;
   std::lock_guard<std::mutex> lk(g_stat_mu);
   if (g_rec_used == g_recs.size()) {
     StatRec r;
@@ -54,7 +54,7 @@ void stat_end(int cat, cudaStream_t s, double flops, double bytes) {
   g_cat_launches[cat] += 1;
   g_cat_flops[cat] += flops;
   g_cat_bytes[cat] += bytes;
-  if (g_timing && g_open >= 0) {
+  if ((g_timing & (1u << cat)) && g_open >= 0) {
     g_recs[g_open].flops = flops;
     g_recs[g_open].bytes = bytes;
     cudaEventRecord(g_recs[g_open].b, s);
@@ -199,15 +199,26 @@ extern "C" {
 const char* spdkfac_last_error(void) { return g_err; }
 int spdkfac_version(void) { return 100; }
 
-void spdkfac_stats_reset(int timing) {
+void spdkfac_stats_reset(int timing_mask) {
   std::lock_guard<std::mutex> lk(g_stat_mu);
   g_rec_used = 0;
-  g_timing = timing != 0;
+  g_timing = uint32_t(timing_mask);
   g_launches.store(0);
   for (int c = 0; c < kNumCats; ++c) g_cat_launches[c] = 0, g_cat_flops[c] = 0, g_cat_bytes[c] = 0;
 }
 
 uint64_t spdkfac_stats_launches(void) { return g_launches.load(); }
+
+int spdkfac_stats_reserve(int n) {
+  std::lock_guard<std::mutex> lk(g_stat_mu);
+  while (int(g_recs.size()) < n) {
+    StatRec r;
+    SPD_CUDA(cudaEventCreate(&r.a));
+    SPD_CUDA(cudaEventCreate(&r.b));
+    g_recs.push_back(r);
+  }
+  return SPDKFAC_OK;
+}
 
 int spdkfac_stats_read(int cat, double* ms, int64_t* launches, double* flops, double* bytes) {
   SPD_ARG(cat >= 0 && cat < kNumCats, SPDKFAC_ERR_ARG, "bad stats category");

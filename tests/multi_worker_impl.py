@@ -1,0 +1,76 @@
+"""Rank program for the multi-GPU parity test (launched by torchrun, one rank per GPU).
+
+The reference's frozen fixture (aggregated_step_w4.json: 4 workers x 6 samples) is split
+over the ranks (4 / P workers' samples per rank); the P-rank SPD-KFAC step (factor
+all-reduce in fusion groups, LBP placement with owner broadcast of CT inverses, gradient
+all-reduce) must reproduce the fixture's centralized-oracle weights, exactly as
+dkfac_step does (emulator.py:211-263, worker-count invariance test_emulator.py:115-158).
+Rank 0 prints one JSON line with the per-layer errors.
+"""
+import json
+import os
+import pathlib
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.nn as nn
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    from paper_2107_06533_b200.perfmodel import PerfParams, AllReduceParams, BcastParams, InverseParams
+    fx = json.loads((ROOT / "tests/golden/aggregated_step_w4.json").read_text())
+    mods = []
+    for w, act in zip(fx["weights"], fx["activations"]):
+        w = np.array(w)
+        lin = nn.Linear(w.shape[1], w.shape[0], bias=False)
+        lin.weight.data = torch.tensor(w, dtype=torch.float32)
+        mods.append(lin)
+        if act == "relu":
+            mods.append(nn.ReLU())
+    model = nn.Sequential(*mods).to(dev)
+    per = 4 // world
+    xs = np.concatenate(fx["worker_inputs"][rank * per:(rank + 1) * per])
+    ts = np.concatenate(fx["worker_targets"][rank * per:(rank + 1) * per])
+    x = torch.tensor(xs, dtype=torch.float32, device=dev)
+    t = torch.tensor(ts, dtype=torch.float32, device=dev)
+    mode = os.environ.get("SPD_PLACEMENT", "lbp")
+    # all-CT calibration: every inverse has one owner and is broadcast (exercises the bcast path)
+    perf = PerfParams(AllReduceParams(1e-5, 1e-9), BcastParams(1e-9, 1e-12), InverseParams(1.0, 1e-6), world)
+    opt = SPDKFAC(model, lr=fx["alpha"], damping=fx["gamma"], placement=mode, perf=perf)
+    loss = ((model(x) - t) ** 2).mean()
+    loss.backward()
+    opt.step()
+    torch.cuda.synchronize()
+    errs = []
+    for lin, w0, want in zip([m for m in model if isinstance(m, nn.Linear)], fx["weights"], fx["expected_weights"]):
+        got = lin.weight.detach().double().cpu().numpy()
+        d = np.array(want) - np.array(w0)
+        errs.append(float(np.linalg.norm(got - np.array(w0) - d) / np.linalg.norm(d)))
+    # weights must be identical on every rank
+    w_all = torch.cat([p.detach().flatten() for p in model.parameters()])
+    ref = w_all.clone()
+    dist.broadcast(ref, 0)
+    same = bool(torch.equal(ref, w_all))
+    ok = torch.tensor([1 if same else 0], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(json.dumps({"errors": errs, "identical_on_all_ranks": bool(ok.item()), "world": world,
+                          "placement": mode, "nct": sorted(opt.placement.nct),
+                          "workers": [list(w) for w in opt.placement.workers]}), flush=True)
+    opt.comm.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
