@@ -57,6 +57,12 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--profile", action="store_true", help="short run for ncu: no clocks/e2e/cpu legs")
+    p.add_argument("--gc", choices=("freeze", "default"), default="freeze",
+                   help="freeze: gc.freeze() after setup+warmup so generation-2 collections do not walk the "
+                        "model/optimizer object graph mid-step")
+    p.add_argument("--mode", choices=("graph", "eager"), default="graph",
+                   help="graph: the whole step (fwd, bwd, K-FAC step) replayed as one CUDA graph")
+    p.add_argument("--clocks", choices=("nvml", "smi", "off"), default="nvml")
     p.add_argument("--stats-off", action="store_true", help="no per-launch CUDA events in the timed region (diagnostic)")
     p.add_argument("--optimizer", choices=("spdkfac", "sgd"), default="spdkfac",
                    help="sgd = diagnostic floor (forward/backward + SGD, no K-FAC); never the headline")
@@ -68,11 +74,50 @@ def workload_config(a, world):
                         f" (BASELINE.json configs[{1 if world == 1 else 2}])",
             "per_gpu_batch": a.batch, "global_batch": a.batch * world, "damping": a.damping, "lr": a.lr,
             "factor_update_freq": a.factor_freq, "inv_update_freq": a.inv_freq, "fusion": "optimal",
-            "placement": a.placement, "parallelism": f"dp{world}",
+            "placement": a.placement, "parallelism": f"dp{world}", "python_gc": a.gc,
+            "execution": "one CUDA graph per iteration (fwd+bwd+K-FAC step)" if a.mode == "graph" else "eager",
             "l2": "per-iteration working set (activations, 0.3 GB packed factors, im2col staging) >> 126 MB L2; no flush"}
 
 
 # ---------------------------------------------------------------- clocks
+class NvmlClocks:
+    """Clock / throttle-reason sampler on a background thread via NVML (light queries only;
+    an `nvidia-smi -lms` loop with power/reason fields stalled the GPU ~50-100 ms per sample)."""
+
+    def __init__(self, index: int, period_s: float = 0.1):
+        import threading
+        import pynvml as N
+        self.N = N
+        N.nvmlInit()
+        self.h = N.nvmlDeviceGetHandleByIndex(index)
+        self.max = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        self.samples = []
+        self.stop_ev = threading.Event()
+        self.period = period_s
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        N = self.N
+        while not self.stop_ev.is_set():
+            self.samples.append((N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
+                                 N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            self.stop_ev.wait(self.period)
+
+    def stop(self):
+        self.stop_ev.set()
+        self.t.join()
+        N = self.N
+        bits = {"hw_slowdown": getattr(N, "nvmlClocksEventReasonHwSlowdown", 0x8),
+                "hw_thermal_slowdown": getattr(N, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                "sw_thermal_slowdown": getattr(N, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": getattr(N, "nvmlClocksEventReasonSwPowerCap", 0x4)}
+        reasons = sorted({k for _, r in self.samples for k, b in bits.items() if r & b})
+        sm = [c for c, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max, "reasons": reasons,
+                "samples": len(sm), "source": "nvml"}
+
+
 class Clocks:
     def __init__(self, index: int):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
@@ -169,13 +214,20 @@ def run_ours(a):
     xs = [torch.randn(shp, device=dev, generator=g) for _ in range(2)]
     ys = [torch.randint(0, num_classes(a.model), (a.batch,), device=dev, generator=g) for _ in range(2)]
 
+    host_phases = []
+
     def step(i, x=None, y=None):
         x = xs[i % 2] if x is None else x
         y = ys[i % 2] if y is None else y
+        t0 = time.perf_counter()
         opt.zero_grad(set_to_none=False)
         loss = crit(model(x), y)
+        t1 = time.perf_counter()
         loss.backward()
+        t2 = time.perf_counter()
         opt.step()
+        t3 = time.perf_counter()
+        host_phases.append((round((t1 - t0) * 1e3, 2), round((t2 - t1) * 1e3, 2), round((t3 - t2) * 1e3, 2)))
         return loss
 
     def barrier():
@@ -189,36 +241,75 @@ def run_ours(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for i in range(a.warmup):
-        step(i)
+    graphed = a.mode == "graph" and a.optimizer == "spdkfac"
+    if graphed:
+        from paper_2107_06533_b200.graph import GraphedStep
+        gs = GraphedStep(model, crit, opt, [xs[0]], [ys[0]], warmup=a.warmup,
+                         before_capture=lambda: _lib.stats_reset(
+                             timing=() if a.stats_off else ("factor_syrk",), reserve=400))
+        eager_step = step
+
+        def step(i, x=None, y=None):
+            x = xs[i % 2] if x is None else x
+            y = ys[i % 2] if y is None else y
+            return gs([x], [y])
+        step(0)
+    else:
+        for i in range(a.warmup):
+            step(i)
     torch.cuda.synchronize()
     barrier()
+    if a.gc == "freeze":
+        import gc
+        gc.collect()
+        gc.freeze()
 
-    clocks = None if a.profile else Clocks(local)
-    # live roofline timing of the dominant kernel only (events pre-created, outside the region)
-    _lib.stats_reset(timing=() if a.stats_off else ("factor_syrk",), reserve=200 * a.steps)
+    clocks = None
+    if not a.profile and a.clocks == "nvml":
+        try:
+            clocks = NvmlClocks(local)
+        except Exception:
+            clocks = Clocks(local)
+    elif not a.profile and a.clocks == "smi":
+        clocks = Clocks(local)
+    # live roofline timing of the dominant kernel only (events pre-created, outside the region);
+    # in graph mode the event nodes were captured into the graph (stats reset before capture)
+    if not graphed:
+        _lib.stats_reset(timing=() if a.stats_off else ("factor_syrk",), reserve=200 * a.steps)
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
+    ms0 = torch.cuda.memory_stats()
     w0 = time.perf_counter()
     e0.record(stream)
+    evs = []
     for i in range(a.steps):
         loss = step(i)
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        evs.append(ev)
     e1.record(stream)
     torch.cuda.synchronize()
     wall_ms = (time.perf_counter() - w0) * 1e3 / a.steps
     wall_ms = max_over_ranks(wall_ms)
+    ms1 = torch.cuda.memory_stats()
+    alloc_diag = {k: ms1.get(k, 0) - ms0.get(k, 0) for k in ("num_device_alloc", "num_device_free", "num_alloc_retries",
+                                                              "num_sync_all_streams")}
     barrier()
     ms = e0.elapsed_time(e1) / a.steps
+    per_step = [round(e0.elapsed_time(evs[0]), 2)] + [round(evs[i - 1].elapsed_time(evs[i]), 2) for i in range(1, len(evs))]
     clk = clocks.stop() if clocks else None
     st = _lib.stats()
-    launches = st["total_launches"]
-    # per-category breakdown: a separate 2-step pass with every launch bracketed by events
+    # graph mode: launch counts / flops were accounted once at capture (= per replay) and the
+    # captured event nodes hold the last replay's timestamps
+    per = 1 if graphed else a.steps
+    launches = st["total_launches"] * (a.steps if graphed else 1)
+    # per-category breakdown: a separate 2-step eager pass with every launch bracketed by events
     nb = 2
     _lib.stats_reset(timing=True, reserve=600 * nb)
     for i in range(nb):
-        step(i)
+        (eager_step if graphed else step)(i)
     torch.cuda.synchronize()
     bst = _lib.stats()
     ms_max = max_over_ranks(ms)
@@ -237,9 +328,12 @@ def run_ours(a):
         w1 = time.perf_counter()
         f0.record(stream)
         for i in range(a.steps):
-            xd.copy_(xh[i % 2], non_blocking=True)
-            yd.copy_(yh[i % 2], non_blocking=True)
-            loss = step(i, xd, yd)
+            if graphed:  # pinned host batch straight into the graph's static input buffers
+                loss = gs([xh[i % 2]], [yh[i % 2]])
+            else:
+                xd.copy_(xh[i % 2], non_blocking=True)
+                yd.copy_(yh[i % 2], non_blocking=True)
+                loss = step(i, xd, yd)
             _ = float(loss.item())
         f1.record(stream)
         torch.cuda.synchronize()
@@ -255,15 +349,16 @@ def run_ours(a):
     except Exception:
         pass
     sy = st["factor_syrk"]
-    ach = sy["flops"] / (sy["ms"] * 1e-3) / 1e12 if sy["ms"] > 0 else 0.0
+    ach = sy["flops"] / (sy["ms"] * 1e-3) / 1e12 if sy["ms"] > 0 else 0.0  # same ratio per step or total
     peak = peaks.get("bf16_tflops_sustained") or 1362.2
     step_ms_total = sum(v["ms"] for k, v in bst.items() if isinstance(v, dict)) / nb
     roofline = {"kernel": "tc3_gemm_kernel<BF16> (factor SYRK, 3 x bf16 split, tcgen05)", "bound": "tensor",
                 "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
                 "traffic": None,
-                "algorithmic_flops_per_step": sy["flops"] / a.steps,
-                "kernel_ms_per_step": round(sy["ms"] / a.steps, 4),
+                "algorithmic_flops_per_step": sy["flops"] / per,
+                "kernel_ms_per_step": round(sy["ms"] / per, 4),
+                "launches_per_step": sy["launches"] / per,
                 "tensor_pipe_mmas_per_algorithmic_mac": 3,
                 "share_of_library_kernel_time": round(bst["factor_syrk"]["ms"] / nb / step_ms_total, 4)
                 if step_ms_total else None}
@@ -286,7 +381,8 @@ def run_ours(a):
                "config": workload_config(a, world), "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
                "cpu_baseline": cpu, "clocks": clk, "kernel_breakdown": breakdown,
                "placement_imbalance": _imbalance(opt) if opt.placement is not None else None,
-               "host_wall_ms_per_step": round(wall_ms, 3),
+               "host_wall_ms_per_step": round(wall_ms, 3), "per_step_ms": per_step, "allocator_in_region": alloc_diag,
+               "host_phase_ms_fwd_bwd_step": host_phases[a.warmup:a.warmup + a.steps] if a.profile is False else None,
                "final_loss": final_loss}
         if a.optimizer != "spdkfac":
             out["diagnostic"] = f"optimizer={a.optimizer}: not the SPD-KFAC metric"

@@ -101,6 +101,13 @@ SPDKFAC_API int spdkfac_factor_plan_create(spdkfac_factor_plan** out, const spdk
                                void* stream);
 SPDKFAC_API int spdkfac_factor_plan_run(spdkfac_factor_plan* p, const float* x, float scale, float decay, float world_scale,
                             float* packed_inout, void* stream);
+/* run() in two halves: stage() reads x (im2col / transpose + precision split into the
+ * plan's staging buffer) on the stream that owns x; compute() (tensor-core SYRK +
+ * packed epilogue) reads only plan memory, so it may run on a side stream ordered
+ * after stage() without extending the lifetime of x. */
+SPDKFAC_API int spdkfac_factor_plan_stage(spdkfac_factor_plan* p, const float* x, void* stream);
+SPDKFAC_API int spdkfac_factor_plan_compute(spdkfac_factor_plan* p, float scale, float decay, float world_scale,
+                                            float* packed_inout, void* stream);
 SPDKFAC_API void spdkfac_factor_plan_destroy(spdkfac_factor_plan* p);
 
 /* ------------------------------------------------------------------ packing

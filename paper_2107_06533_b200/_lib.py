@@ -41,6 +41,8 @@ SIGNATURES = {
     "spdkfac_factor_workspace_size": (_sz, [C.POINTER(FactorGeom)]),
     "spdkfac_factor_plan_create": (C.c_int, [C.POINTER(_vp), C.POINTER(FactorGeom), _vp, _sz, _vp]),
     "spdkfac_factor_plan_run": (C.c_int, [_vp, _vp, _f32, _f32, _f32, _vp, _vp]),
+    "spdkfac_factor_plan_stage": (C.c_int, [_vp, _vp, _vp]),
+    "spdkfac_factor_plan_compute": (C.c_int, [_vp, _f32, _f32, _f32, _vp, _vp]),
     "spdkfac_factor_plan_destroy": (None, [_vp]),
     "spdkfac_pack_upper_f32": (C.c_int, [_vp, _i64, _i64, _vp, _vp]),
     "spdkfac_unpack_upper_f32": (C.c_int, [_vp, _i64, _vp, _i64, _vp]),

@@ -334,9 +334,8 @@ int spdkfac_factor_plan_create(spdkfac_factor_plan** out, const spdkfac_factor_g
   return SPDKFAC_OK;
 }
 
-int spdkfac_factor_plan_run(spdkfac_factor_plan* p, const float* x, float scale, float decay, float world_scale,
-                            float* packed, void* stream) {
-  SPD_ARG(p && x && packed, SPDKFAC_ERR_ARG, "null argument");
+int spdkfac_factor_plan_stage(spdkfac_factor_plan* p, const float* x, void* stream) {
+  SPD_ARG(p && x, SPDKFAC_ERR_ARG, "null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const spdkfac_factor_geom& g = p->g;
   stat_begin(kCatFactorStage, s);
@@ -359,6 +358,13 @@ int spdkfac_factor_plan_run(spdkfac_factor_plan* p, const float* x, float scale,
   }
   SPD_CHECK_LAUNCH();
   stat_end(kCatFactorStage, s, 0, double(p->M) * p->d * 4 + 4.0 * p->d * p->Mpad);
+  return SPDKFAC_OK;
+}
+
+int spdkfac_factor_plan_compute(spdkfac_factor_plan* p, float scale, float decay, float world_scale, float* packed,
+                                void* stream) {
+  SPD_ARG(p && packed, SPDKFAC_ERR_ARG, "null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
   // algorithmic work of one factor: M * d * (d + 1) flops (upper triangle incl. diagonal)
   stat_begin(kCatFactorSyrk, s);
   TcRun run{packed, p->d, scale, decay, world_scale, 0};
@@ -373,6 +379,13 @@ int spdkfac_factor_plan_run(spdkfac_factor_plan* p, const float* x, float scale,
   SPD_CHECK_LAUNCH();
   stat_end(kCatFactorReduce, s, 0, 65536.0 * p->n_items + 4.0 * p->d * (p->d + 1) / 2 * (decay == 0.f ? 1 : 2));
   return SPDKFAC_OK;
+}
+
+int spdkfac_factor_plan_run(spdkfac_factor_plan* p, const float* x, float scale, float decay, float world_scale,
+                            float* packed, void* stream) {
+  int rc = spdkfac_factor_plan_stage(p, x, stream);
+  if (rc) return rc;
+  return spdkfac_factor_plan_compute(p, scale, decay, world_scale, packed, stream);
 }
 
 void spdkfac_factor_plan_destroy(spdkfac_factor_plan* p) { delete p; }

@@ -32,6 +32,15 @@ std::atomic<uint64_t> g_launches{0};
 uint64_t g_cat_launches[kNumCats] = {};
 double g_cat_flops[kNumCats] = {}, g_cat_bytes[kNumCats] = {};
 thread_local long g_open = -1;
+
+// inside stream capture, record as an external event node so the timestamps of every
+// graph replay are readable (and timeable) from the host
+void record_stat_event(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &st);
+  if (st == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else cudaEventRecord(e, s);
+}
 }  // namespace
 
 void stat_begin(int cat, cudaStream_t s) {
@@ -46,7 +55,7 @@ void stat_begin(int cat, cudaStream_t s) {
   }
   g_open = long(g_rec_used++);
   g_recs[g_open].cat = cat;
-  cudaEventRecord(g_recs[g_open].a, s);
+  record_stat_event(g_recs[g_open].a, s);
 }
 
 void stat_end(int cat, cudaStream_t s, double flops, double bytes) {
@@ -57,7 +66,7 @@ void stat_end(int cat, cudaStream_t s, double flops, double bytes) {
   if ((g_timing & (1u << cat)) && g_open >= 0) {
     g_recs[g_open].flops = flops;
     g_recs[g_open].bytes = bytes;
-    cudaEventRecord(g_recs[g_open].b, s);
+    record_stat_event(g_recs[g_open].b, s);
     g_open = -1;
   }
 }

@@ -87,6 +87,16 @@ class FactorPlan:
         L.check(self._lib.spdkfac_factor_plan_run(self._h, x.data_ptr(), s, float(decay), float(world_scale),
                                                   packed.data_ptr(), _stream(stream)), "factor run")
 
+    def stage(self, x: torch.Tensor, stream=None) -> None:
+        """First half of run(): consume x into the plan's split-precision staging buffer."""
+        L.check(self._lib.spdkfac_factor_plan_stage(self._h, x.data_ptr(), _stream(stream)), "factor stage")
+
+    def compute(self, packed: torch.Tensor, scale: float, decay: float = 0.0, world_scale: float = 1.0,
+                stream=None) -> None:
+        """Second half of run(): tensor-core SYRK from the staging buffer into `packed`."""
+        L.check(self._lib.spdkfac_factor_plan_compute(self._h, float(scale), float(decay), float(world_scale),
+                                                      packed.data_ptr(), _stream(stream)), "factor compute")
+
     def __del__(self):
         if getattr(self, "_h", None):
             self._lib.spdkfac_factor_plan_destroy(self._h)
@@ -261,6 +271,19 @@ class PrecondPlan:
                                                 _stream(stream)), "precondition plan")
         self._h = h
         self._lib = lib
+
+    def bind(self, g_inv, grads, a_inv, weights=None, out=None):
+        """Pre-build the pointer tables for tensors whose storage stays fixed across steps."""
+        self._bound = (L.ptr_array([t.data_ptr() for t in g_inv]), L.ptr_array([t.data_ptr() for t in grads]),
+                       L.ptr_array([t.data_ptr() for t in a_inv]),
+                       L.ptr_array([w.data_ptr() for w in weights]) if weights is not None else None,
+                       L.ptr_array([o.data_ptr() for o in out]) if out is not None else None)
+        self._bound_key = tuple(t.data_ptr() for t in grads)
+
+    def run_bound(self, alpha: float, stream=None) -> None:
+        gi, gr, ai, pw, po = self._bound
+        L.check(self._lib.spdkfac_precond_plan_run(self._h, gi, gr, ai, pw, float(alpha), po, _stream(stream)),
+                "precondition run")
 
     def run(self, g_inv, grads, a_inv, weights=None, alpha: float = 0.0, out=None, stream=None) -> None:
         n = self.n

@@ -64,6 +64,8 @@ class _Layer:
     a_key: tuple = ()
     g_key: tuple = ()
     handles: list = field(default_factory=list)
+    events: dict = field(default_factory=dict)   # kind -> (compute done, staged)
+    pending: dict = field(default_factory=lambda: {"A": False, "G": False})
 
 
 def _conv_ok(m) -> bool:
@@ -159,6 +161,7 @@ class SPDKFAC(torch.optim.Optimizer):
         self.comm_stream = torch.cuda.Stream(self.device) if self.world > 1 else None
         self._info_host = torch.zeros(len(mine), dtype=torch.int32, pin_memory=True) if mine else None
         self._info_event = None
+        self._precond_key = None
         self.steps = 0
         self._capture = True
         self._factor_updates = 0
@@ -215,6 +218,7 @@ class SPDKFAC(torch.optim.Optimizer):
 
     def _install_hooks(self):
         for l in self.layers:
+            l.events = {k: (torch.cuda.Event(), torch.cuda.Event()) for k in ("A", "G")}
             l.handles.append(l.module.register_forward_pre_hook(self._make_a_hook(l)))
             l.handles.append(l.module.register_forward_hook(self._make_out_hook(l)))
 
@@ -229,42 +233,51 @@ class SPDKFAC(torch.optim.Optimizer):
         decay = self.factor_decay if self._factor_updates > 0 else 0.0
         return decay, 1.0 / self.world
 
+    def _plan_for(self, l: _Layer, x: torch.Tensor, kind: str) -> FactorPlan:
+        key = tuple(x.shape)
+        m = l.module
+        if kind == "A":
+            if l.a_key != key:
+                if l.is_conv:
+                    l.a_plan = FactorPlan(L.CONV_A, x.shape, m.kernel_size, m.stride, m.padding, m.dilation)
+                else:
+                    l.a_plan = FactorPlan(L.ROWS, (x.numel() // x.shape[-1], x.shape[-1]))
+                l.a_key = key
+            return l.a_plan
+        if l.g_key != key:
+            if l.is_conv:
+                l.g_plan = FactorPlan(L.SPATIAL, x.shape)
+            else:
+                l.g_plan = FactorPlan(L.ROWS, (x.numel() // x.shape[-1], x.shape[-1]))
+            l.g_key = key
+        return l.g_plan
+
     def _launch_factor(self, l: _Layer, x: torch.Tensor, kind: str):
+        """Stage x on the stream that owns it (im2col/transpose + precision split into the
+        plan's buffer), then run the tensor-core SYRK on the factor stream.  The SYRK reads
+        only plan memory, so x's lifetime is not extended across streams."""
         main = torch.cuda.current_stream(self.device)
         fs = self.factor_stream
-        fs.wait_stream(main)
         x = x.detach()
         if x.dtype != torch.float32 or not x.is_contiguous():
-            with torch.cuda.stream(main):
-                x = x.to(torch.float32).contiguous()
-        decay, wscale = self._factor_args()
+            x = x.to(torch.float32).contiguous()
+        plan = self._plan_for(l, x, kind)
+        ev_done, ev_staged = l.events[kind]
+        capturing = torch.cuda.is_current_stream_capturing()
+        if not capturing and l.pending[kind]:
+            main.wait_event(ev_done)  # previous iteration's SYRK has consumed the staging buffer
+        plan.stage(x, main)
+        ev_staged.record(main)
+        fs.wait_event(ev_staged)
+        decay = self.factor_decay if self._factor_updates > 0 else 0.0
         if kind == "A":
-            key = tuple(x.shape)
-            if l.a_key != key:
-                m = l.module
-                with torch.cuda.stream(fs):
-                    if l.is_conv:
-                        l.a_plan = FactorPlan(L.CONV_A, x.shape, m.kernel_size, m.stride, m.padding, m.dilation)
-                    else:
-                        l.a_plan = FactorPlan(L.ROWS, (x.numel() // x.shape[-1], x.shape[-1]))
-                l.a_key = key
-            plan, buf, off, d = l.a_plan, self.bufA, l.a_off, l.spec.a_dim
-            scale = 1.0 / plan.rows
+            buf, off, d, scale = self.bufA, l.a_off, l.spec.a_dim, 1.0 / plan.rows
         else:
-            key = tuple(x.shape)
-            if l.g_key != key:
-                with torch.cuda.stream(fs):
-                    if l.is_conv:
-                        l.g_plan = FactorPlan(L.SPATIAL, x.shape)
-                    else:
-                        l.g_plan = FactorPlan(L.ROWS, (x.numel() // x.shape[-1], x.shape[-1]))
-                l.g_key = key
-            plan, buf, off, d = l.g_plan, self.bufG, l.g_off, l.spec.g_dim
             b = x.shape[0] if self.batch_averaged else 1
-            scale = float(b * b) / plan.rows
-        packed = buf[off:off + d * (d + 1) // 2]
-        plan.run(x, packed, scale=scale, decay=decay, world_scale=wscale, stream=fs)
-        x.record_stream(fs)
+            buf, off, d, scale = self.bufG, l.g_off, l.spec.g_dim, float(b * b) / plan.rows
+        plan.compute(buf[off:off + d * (d + 1) // 2], scale, decay, 1.0 / self.world, fs)
+        ev_done.record(fs)
+        l.pending[kind] = not capturing
         groups = self._groups_fwd if kind == "A" else self._groups_bwd
         if self.world > 1 and l.index in groups:
             s, e = groups[l.index]
@@ -299,7 +312,9 @@ class SPDKFAC(torch.optim.Optimizer):
     @torch.no_grad()
     def step(self, closure=None):
         loss = closure() if closure is not None else None
-        self.check_inverses()
+        capturing = torch.cuda.is_current_stream_capturing()
+        if not capturing:
+            self.check_inverses()
         main = torch.cuda.current_stream(self.device)
         lr = self.param_groups[0]["lr"]
         factors_now = self._capture
@@ -319,27 +334,39 @@ class SPDKFAC(torch.optim.Optimizer):
             if self._inv_plan is not None:
                 self._inv_plan.run(self.damping, main)
                 self._info_host.copy_(self._inv_plan.info, non_blocking=True)
-                self._info_event = torch.cuda.Event()
-                self._info_event.record(main)
+                if not capturing:  # graph replays record this event after the replay (GraphedStep)
+                    self._info_event = torch.cuda.Event()
+                    self._info_event.record(main)
             if self.world > 1:
                 self._exchange_inverses(main)
-        # precondition + update for every K-FAC layer (mean gradient = sum / P)
-        g_inv, grads, a_inv, weights = [], [], [], []
-        for l in self.layers:
-            w = l.module.weight
-            if w.grad is None:
-                raise RuntimeError(f"layer {l.name} has no gradient; call backward() before step()")
-            grads.append(w.grad.reshape(l.spec.g_dim, l.spec.a_dim))
-            weights.append(w.data)
-            a_inv.append(self.inv[2 * l.index])
-            g_inv.append(self.inv[2 * l.index + 1])
-        self._precond.run(g_inv, grads, a_inv, weights=weights, alpha=lr / self.world, stream=main)
+        # precondition + update for every K-FAC layer (mean gradient = sum / P); the pointer
+        # tables are rebuilt only when a gradient's storage changes (zero_grad(set_to_none=True))
+        key = tuple(l.module.weight.grad.data_ptr() if l.module.weight.grad is not None else 0 for l in self.layers)
+        if key != self._precond_key:
+            if 0 in key:
+                missing = [l.name for l in self.layers if l.module.weight.grad is None]
+                raise RuntimeError(f"layers {missing[:3]} have no gradient; call backward() before step()")
+            self._precond.bind([self.inv[2 * l.index + 1] for l in self.layers],
+                               [l.module.weight.grad.reshape(l.spec.g_dim, l.spec.a_dim) for l in self.layers],
+                               [self.inv[2 * l.index] for l in self.layers],
+                               weights=[l.module.weight.data for l in self.layers])
+            self._precond_key = key
+        self._precond.run_bound(lr / self.world, stream=main)
         others = [p for p in self.other_params if p.grad is not None]
         if others:
             torch._foreach_add_([p.data for p in others], [p.grad for p in others], alpha=-lr / self.world)
-        self.steps += 1
-        self._capture = self.steps % self.factor_update_freq == 0
+        if not capturing:  # a captured step is counted per replay (_after_replay)
+            self.steps += 1
+            self._capture = self.steps % self.factor_update_freq == 0
         return loss
+
+    def _after_replay(self, stream) -> None:
+        """Bookkeeping for one replay of a captured step (GraphedStep): the Python side
+        effects of step() ran once at capture time."""
+        self.steps += 1
+        if self._inv_plan is not None:
+            self._info_event = torch.cuda.Event()
+            self._info_event.record(stream)
 
     def _exchange_inverses(self, main):
         """Owner ranks broadcast their CT inverses (packed upper triangle,

@@ -75,3 +75,36 @@ def test_nonpd_raises_on_next_step():
         opt.check_inverses()
     assert e.value.pivot == 0
     opt.remove_hooks()
+
+
+def test_graphed_step_matches_eager():
+    """One CUDA-graph replay per iteration gives the same weights as the eager step."""
+    import torch.nn as nn
+    from paper_2107_06533_b200.graph import GraphedStep
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    from tests.smoke_impl import SmallNet
+    torch.backends.cudnn.deterministic = True
+    torch.backends.cudnn.benchmark = False
+    torch.manual_seed(7)
+    m1 = SmallNet().cuda()
+    m2 = SmallNet().cuda()
+    m2.load_state_dict(m1.state_dict())
+    crit = nn.CrossEntropyLoss()
+    xs = [torch.randn(16, 3, 8, 8, device="cuda") for _ in range(5)]
+    ys = [torch.randint(0, 10, (16,), device="cuda") for _ in range(5)]
+    o1 = SPDKFAC(m1, lr=0.05, damping=0.1)
+    for x, y in zip(xs, ys):
+        o1.zero_grad(set_to_none=False)
+        crit(m1(x), y).backward()
+        o1.step()
+    o2 = SPDKFAC(m2, lr=0.05, damping=0.1)
+    gs = GraphedStep(m2, crit, o2, [xs[0]], [ys[0]], warmup=1)  # warmup = eager step 1 on xs[0]
+    for x, y in zip(xs[1:], ys[1:]):
+        gs([x], [y])
+    torch.cuda.synchronize()
+    o2.check_inverses()
+    for p1, p2 in zip(m1.parameters(), m2.parameters()):
+        assert torch.allclose(p1, p2, rtol=1e-5, atol=1e-6), (p1 - p2).abs().max()
+    assert o2.steps == 5
+    o1.remove_hooks()
+    o2.remove_hooks()
