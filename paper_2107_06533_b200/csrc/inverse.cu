@@ -327,7 +327,7 @@ struct spdkfac_inverse_plan {
   PanelJob* pan_jobs;           // device, (matrix, R != K) per step, same order as the panel items
   TileJob* tiles;               // device, 32x32 tile pairs of all blocked matrices
   int n_tiles;
-  CUtensorMap* maps;            // [0] old panel planes, [1] C planes, [2] P^-1 planes
+  CUtensorMap* maps;            // [0] old panel planes, [1] C planes, [2] P^-1 planes, [3 + slot] W_slot tiles
   TcItem* items;                // per step: panel GEMM items then update items
   TcEpi* epis;                  // [0, n): update, [n, 2n): panel
   float* panA;
@@ -384,7 +384,7 @@ size_t inverse_carve(int n, const int32_t* dims, Carve& c, spdkfac_inverse_plan*
   auto* aid = c.take<int32_t>(size_t(std::max<int64_t>(act, 1)));
   auto* tj = c.take<TileJob>(size_t(std::max<int64_t>(tiles, 1)));
   auto* pj = c.take<PanelJob>(size_t(std::max<int64_t>(items, 1)));
-  auto* mp = c.take<CUtensorMap>(3, 128);
+  auto* mp = c.take<CUtensorMap>(size_t(3 + nblk), 128);
   auto* it = c.take<TcItem>(size_t(std::max<int64_t>(items, 1)));
   auto* ep = c.take<TcEpi>(size_t(2) * n);
   if (p) {
@@ -442,7 +442,8 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   const int64_t plane = p->plane_rows * kB;
   std::vector<TcEpi> epis(size_t(2) * n);
   for (int t = 0; t < n; ++t) {
-    epis[t] = TcEpi{mats[t].W, mats[t].dp, 0, -1.f, 1.f, kAxpby, 0, nullptr, 0, 0};            // update
+    epis[t] = TcEpi{mats[t].W, mats[t].dp, 0, -1.f, 1.f, kAxpby, 0, nullptr, 0, 0,
+                    dims[t] > kB ? 3 + mats[t].slot : 0};                                        // update
     epis[n + t] = TcEpi{mats[t].W, mats[t].dp, 0, 1.f, 0.f, kAxpby, 0, p->panC, kB, plane};    // panel
   }
   std::vector<TileJob> tiles;
@@ -517,7 +518,7 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     }
     p->upd_cnt.push_back(int(items.size()) - p->upd_off.back());
   }
-  std::vector<CUtensorMap> maps(3);
+  std::vector<CUtensorMap> maps(size_t(3 + p->n_blocked));
   int rc = SPDKFAC_OK;
   if (p->n_blocked > 0) {
     if ((rc = make_operand_map(&maps[0], p->panA, false, kB, p->plane_rows, kB)) ||
@@ -526,6 +527,11 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
       delete p;
       return rc;
     }
+    for (int t : blocked)
+      if ((rc = make_ctile_map(&maps[3 + mats[t].slot], mats[t].W, mats[t].dp, mats[t].dp, mats[t].dp))) {
+        delete p;
+        return rc;
+      }
   }
   if ((rc = upload(p->mats, mats, s)) || (rc = upload(p->small_ids, small, s)) ||
       (rc = upload(p->blocked_ids, blocked, s)) || (rc = upload(p->act_ids, act, s)) ||
@@ -573,7 +579,7 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       if (rc) return rc;
       stat_end(kCatInvPanel, s, 2.0 * kB * kB * kB * p->pan_cnt[k], 0);
       stat_begin(kCatInvUpdate, s);
-      rc = launch_tc3(Kind::TF32, p->maps, p->items + p->upd_off[k], p->epis, p->upd_cnt[k], s);
+      rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k], p->epis, p->upd_cnt[k], s);
       if (rc) return rc;
       stat_end(kCatInvUpdate, s, 2.0 * kB * kB * kB * p->upd_cnt[k], 0);
     }

@@ -105,12 +105,14 @@ int make_operand_map(CUtensorMap* out, const void* base, bool bf16, int64_t k_ex
   return SPDKFAC_OK;
 }
 
-template <Kind K>
+template <Kind K, int kSt, bool kCTile>
 static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
                        const TcRun& run) {
+  constexpr size_t smem = tc_smem_bytes<kSt>(kCTile);
   static bool attr_set = false;
   if (!attr_set) {
-    SPD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTcSmemBytes)));
+    SPD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<K, kSt, kCTile>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem)));
     attr_set = true;
   }
   static int sms = 0;
@@ -120,7 +122,7 @@ static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi
     SPD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   const int grid = n < sms ? n : sms;
-  tc3_gemm_kernel<K><<<grid, 192, kTcSmemBytes, s>>>(maps, items, epis, run, n);
+  tc3_gemm_kernel<K, kSt, kCTile><<<grid, 192, smem, s>>>(maps, items, epis, run, n);
   SPD_CHECK_LAUNCH();
   return SPDKFAC_OK;
 }
@@ -128,8 +130,29 @@ static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi
 int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
                const TcRun& run) {
   if (n <= 0) return SPDKFAC_OK;
-  return kind == Kind::BF16 ? launch_kind<Kind::BF16>(maps, items, epis, n, s, run)
-                            : launch_kind<Kind::TF32>(maps, items, epis, n, s, run);
+  return kind == Kind::BF16 ? launch_kind<Kind::BF16, kStages, false>(maps, items, epis, n, s, run)
+                            : launch_kind<Kind::TF32, kStages, false>(maps, items, epis, n, s, run);
+}
+
+int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s) {
+  if (n <= 0) return SPDKFAC_OK;
+  return launch_kind<Kind::TF32, 2, true>(maps, items, epis, n, s, TcRun{});
+}
+
+int make_ctile_map(CUtensorMap* out, const float* base, int64_t rows, int64_t cols, int64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  SPD_ARG(fn != nullptr, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  SPD_ARG((ld * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0, SPDKFAC_ERR_ARG,
+          "tensor map: misaligned target");
+  cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(ld * 4)};
+  cuuint32_t box[2] = {128, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SPD_ARG(r == CUDA_SUCCESS, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled (C tile) failed (%d)", int(r));
+  return SPDKFAC_OK;
 }
 
 // ------------------------------------------------------------------ pack / unpack

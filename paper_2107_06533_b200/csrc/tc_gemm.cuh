@@ -64,6 +64,8 @@ struct TcEpi {
   // out2[(a_row + i) * ld2 + j] = hi(alpha*D), out2[... + plane2] = lo(alpha*D)
   float* out2;
   int64_t ld2, plane2;
+  int32_t c_map;  // kCTile kernels: 2-D tensor map of the fp32 target (box 128 x 128)
+  int32_t pad2_;
 };
 
 // Epilogue of one 32-column chunk of the accumulator tile: thread row i (TMEM lane),
@@ -170,23 +172,37 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
 //   warp 1      MMA issuer (one lane) + TMEM owner; two 128-column accumulators so the
 //               next tile's MMAs run while the epilogue drains the previous one
 //   warps 2..5  epilogue (warp w drains TMEM lanes [32 (w % 4), +32))
-template <Kind K>
+// kCTile (template): the epilogue target is a fp32 matrix reached through a 2-D tensor
+// map (TcEpi::c_map): the producer TMA-loads the 128x128 target tile into shared memory
+// while the tile's MMAs run, the epilogue applies out = beta*out + alpha*D^T there
+// (lanes walk contiguous smem -> conflict-free) and one thread TMA-stores it back.  Used
+// for the read-modify-write inverse updates, where per-thread loads left the kernel
+// latency-bound at ~2 TB/s.
+template <int kSt>
+constexpr size_t tc_smem_bytes(bool ctile) {
+  return size_t(kSt) * kStageBytes + (ctile ? 65536 : 0) + 1024 + 256;
+}
+
+template <Kind K, int kSt, bool kCTile>
 __global__ void __launch_bounds__(192, 1)
     tc3_gemm_kernel(const CUtensorMap* __restrict__ maps, const TcItem* __restrict__ items,
                     const TcEpi* __restrict__ epis, const TcRun run, int n_items) {
   constexpr int BK = (K == Kind::BF16) ? 64 : 32;  // one 128-byte swizzle row of K
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;  // [2]
-  uint64_t* tempty = tfull + 2;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* ctile = reinterpret_cast<float*>(smem + kSt * kStageBytes);  // [128][128] (kCTile)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageBytes + (kCTile ? 65536 : 0));
+  uint64_t* empty = full + kSt;
+  uint64_t* tfull = empty + kSt;  // [2]
+  uint64_t* tempty = tfull + 2;   // [2]
+  uint64_t* cfull = tempty + 2;   // C tile landed
+  uint64_t* cfree = cfull + 1;    // C tile stored back (smem reusable)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfree + 1);
 
   const int warp = warp_id();
   const int lane = lane_id();
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kSt; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -194,6 +210,8 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4);
     }
+    mbar_init(cfull, 1);
+    mbar_init(cfree, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<256>(tmem_slot);
@@ -204,9 +222,9 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
-      uint32_t g = 0;
-      int last_a = -1, last_b = -1;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      uint32_t g = 0, t = 0;
+      int last_a = -1, last_b = -1, last_c = -1;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
         const TcItem it = items[item];
         const bool same = (it.flags & kSameAB) != 0;
         const CUtensorMap* am = maps + it.a_map;
@@ -215,8 +233,8 @@ __global__ void __launch_bounds__(192, 1)
         if (!same && it.b_map != last_b) tmap_acquire(bm), last_b = it.b_map;
         const uint32_t bytes = same ? 2 * kTileBytes : 4 * kTileBytes;
         for (int kb = 0; kb < it.nk; ++kb, ++g) {
-          const uint32_t s = g % kStages;
-          mbar_wait(&empty[s], ((g / kStages) & 1) ^ 1);
+          const uint32_t s = g % kSt;
+          mbar_wait(&empty[s], ((g / kSt) & 1) ^ 1);
           mbar_expect_tx(&full[s], bytes);
           uint8_t* st = smem + s * kStageBytes;
           const int kc = it.k0 + kb * BK;
@@ -226,6 +244,14 @@ __global__ void __launch_bounds__(192, 1)
             tma_load_3d(st + 2 * kTileBytes, bm, &full[s], kc, it.b_row, 0);
             tma_load_3d(st + 3 * kTileBytes, bm, &full[s], kc, it.b_row, 1);
           }
+        }
+        if constexpr (kCTile) {  // target tile of this item, after the previous tile was stored
+          const TcEpi ep = epis[it.epi];
+          const CUtensorMap* cm = maps + ep.c_map;
+          if (ep.c_map != last_c) tmap_acquire(cm), last_c = ep.c_map;
+          mbar_wait(cfree, (t & 1) ^ 1);
+          mbar_expect_tx(cfull, 65536);
+          tma_load_2d(ctile, cm, cfull, it.out_r, it.out_c);  // rows out_c.., cols out_r..
         }
       }
     }
@@ -242,8 +268,8 @@ __global__ void __launch_bounds__(192, 1)
         tc_fence_after();
         const uint32_t acc = tmem + buf * 128;
         for (int kb = 0; kb < it.nk; ++kb, ++g) {
-          const uint32_t s = g % kStages;
-          mbar_wait(&full[s], (g / kStages) & 1);
+          const uint32_t s = g % kSt;
+          mbar_wait(&full[s], (g / kSt) & 1);
           tc_fence_after();
           uint8_t* st = smem + s * kStageBytes;
           const uint64_t ahi = make_sdesc_sw128(st);
@@ -273,6 +299,7 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t buf = t & 1, use = t >> 1;
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
+      if constexpr (kCTile) mbar_wait(cfull, t & 1);
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         if (c * 32 >= it.n_valid) break;  // uniform
@@ -283,11 +310,26 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int u = 0; u < 32; ++u) v[u] = 0.f;
         }
-        epilogue_chunk(it, ep, run, i, c, v);
+        if constexpr (kCTile) {  // ctile[j][i] = beta * ctile[j][i] + alpha * D[i][j]
+          float* col = ctile + (c * 32) * 128 + i;
+#pragma unroll
+          for (int u = 0; u < 32; ++u) col[u * 128] = ep.beta * col[u * 128] + ep.alpha * v[u];
+        } else {
+          epilogue_chunk(it, ep, run, i, c, v);
+        }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM drained: MMA may reuse this accumulator
+      if constexpr (kCTile) {
+        fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the TMA store
+        named_bar_sync(1, 128);
+        if (warp == 2 && lane == 0) {
+          tma_store_2d(maps + ep.c_map, ctile, it.out_r, it.out_c);
+          tma_store_commit_and_wait_read();
+          mbar_arrive(cfree);
+        }
+      }
     }
   }
   tc_fence_before();
