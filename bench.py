@@ -60,6 +60,8 @@ def parse():
     p.add_argument("--gc", choices=("freeze", "default"), default="freeze",
                    help="freeze: gc.freeze() after setup+warmup so generation-2 collections do not walk the "
                         "model/optimizer object graph mid-step")
+    p.add_argument("--memory-format", choices=("channels_last", "nchw"), default="channels_last",
+                   help="activation/weight memory format of the model (cuDNN runs NHWC natively on B200)")
     p.add_argument("--mode", choices=("graph", "eager"), default="graph",
                    help="graph: the whole step (fwd, bwd, K-FAC step) replayed as one CUDA graph")
     p.add_argument("--clocks", choices=("nvml", "smi", "off"), default="nvml")
@@ -76,6 +78,7 @@ def workload_config(a, world):
             "factor_update_freq": a.factor_freq, "inv_update_freq": a.inv_freq, "fusion": "optimal",
             "placement": a.placement, "parallelism": f"dp{world}", "python_gc": a.gc,
             "execution": "one CUDA graph per iteration (fwd+bwd+K-FAC step)" if a.mode == "graph" else "eager",
+            "memory_format": a.memory_format,
             "l2": "per-iteration working set (activations, 0.3 GB packed factors, im2col staging) >> 126 MB L2; no flush"}
 
 
@@ -173,10 +176,11 @@ def cpu_reference(model, batch, steps=None, budget_s=30.0):
         if missing:
             idx = [keys.index(k) for k in missing]
             total, _, _, _ = cpu_step.full_step_estimate(shapes, subset=idx, cache=cache)
+    kind = cpu_step.implementation()[4]
     sample = (f"{len(keys)} distinct layer shapes of {len(shapes)} {model} K-FAC layers (bs{batch}), each timed "
               f"(factor A+G, 2 damped inverses, precondition, update; float64 numpy/scipy LAPACK) and weighted by "
               f"multiplicity; im2col and forward/backward not charged")
-    return total * 1e3, sample, per_step
+    return total * 1e3, sample, per_step, kind
 
 
 # ---------------------------------------------------------------- our arm
@@ -200,6 +204,9 @@ def run_ours(a):
 
     torch.manual_seed(0)
     model = build_model(a.model).to(dev)
+    cl = a.memory_format == "channels_last"
+    if cl:
+        model = model.to(memory_format=torch.channels_last)
     if a.optimizer == "sgd":
         opt = torch.optim.SGD(model.parameters(), lr=a.lr)
         opt.check_inverses = lambda: None
@@ -212,6 +219,8 @@ def run_ours(a):
     g.manual_seed(1000 + rank)
     shp = input_shape(a.model, a.batch)
     xs = [torch.randn(shp, device=dev, generator=g) for _ in range(2)]
+    if cl:
+        xs = [x.contiguous(memory_format=torch.channels_last) for x in xs]
     ys = [torch.randint(0, num_classes(a.model), (a.batch,), device=dev, generator=g) for _ in range(2)]
 
     host_phases = []
@@ -319,7 +328,7 @@ def run_ours(a):
     # ---- e2e through the public API: pinned host batch -> device every step, loss read back
     e2e = None
     if not a.no_e2e and not a.profile:
-        xh = [x.cpu().pin_memory() for x in xs]
+        xh = [x.cpu().pin_memory() for x in xs]  # keeps the channels-last strides
         yh = [y.cpu().pin_memory() for y in ys]
         xd, yd = torch.empty_like(xs[0]), torch.empty_like(ys[0])
         barrier()
@@ -369,9 +378,9 @@ def run_ours(a):
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline and not a.profile:
-        cpu_ms, sample, _ = cpu_reference(a.model, a.batch)
+        cpu_ms, sample, _, kind = cpu_reference(a.model, a.batch)
         cpu = {"value": round(cpu_ms, 1), "unit": "ms", "cores": int(os.environ["OPENBLAS_NUM_THREADS"]),
-               "kind": "port", "sample": sample}
+               "kind": kind, "sample": sample}
 
     if rank == 0:
         out = {"metric": METRIC, "value": round(ms_max, 3), "unit": "ms", "n_gpus": world, "steps": a.steps,
@@ -409,17 +418,18 @@ def run_reference(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    ms, sample, per_step = cpu_reference(a.model, a.batch, steps=max(1, a.steps))
+    ms, sample, per_step, kind = cpu_reference(a.model, a.batch, steps=max(1, a.steps))
     cores = int(os.environ["OPENBLAS_NUM_THREADS"])
     out = {"metric": METRIC, "impl": "reference", "value": round(ms, 1), "unit": "ms", "n_gpus": world,
            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 1), "higher_is_better": False,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": workload_config(a, world),
-           "cpu_baseline": {"value": round(ms, 1), "unit": "ms", "cores": cores, "kind": "port",
+           "cpu_baseline": {"value": round(ms, 1), "unit": "ms", "cores": cores, "kind": kind,
                             "sample": sample + "; per timed step a rotating quarter of the distinct shapes"},
            "e2e": {"value": round(ms, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-           "note": "reference kfacsched is CPU-only numpy/scipy (no GPU path); timed via the oracle port "
-                   "(oracle/), per-shape times x multiplicity = one full ResNet-50 step per rank"}
+           "note": "reference kfacsched is CPU-only numpy/scipy (no GPU path); its own functions from "
+                   "baseline/_ref (kind=reference) or the oracle port (kind=port), per-shape times x "
+                   "multiplicity = one full ResNet-50 step per rank"}
     print(json.dumps(out), flush=True)
 
 

@@ -79,12 +79,17 @@ SPDKFAC_API int spdkfac_stats_read(int category, double* ms, int64_t* launches, 
  *   SPDKFAC_ROWS     x = [rows][d] row-major (ld = row stride)     linear layer input / output grad
  *   SPDKFAC_CONV_A   x = NCHW activation; rows = im2col patches (c,kh,kw order) per output position
  *   SPDKFAC_SPATIAL  x = NCHW output gradient; rows = (b,h,w) positions, d = C
+ *   SPDKFAC_CONV_A_NHWC   x = channels-last activation; patch rows ordered (kh,kw,c), the column
+ *                         order of a channels-last conv weight viewed as [cout][kh*kw*cin]
+ *   SPDKFAC_SPATIAL_NHWC  x = channels-last output gradient (rows [b*h*w][C])
  * A plan binds the shapes once and owns the split-precision staging buffers
  * and tile tables inside the workspace; run() takes the per-step pointers.
  */
 #define SPDKFAC_ROWS 0
 #define SPDKFAC_CONV_A 1
 #define SPDKFAC_SPATIAL 2
+#define SPDKFAC_CONV_A_NHWC 3
+#define SPDKFAC_SPATIAL_NHWC 4
 
 typedef struct spdkfac_factor_geom {
   int32_t layout;       /* SPDKFAC_ROWS / CONV_A / SPATIAL */

@@ -22,6 +22,24 @@ import numpy as np
 
 from .linalg import damped_inverse, factor_A, factor_G, precondition
 
+_REF_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+
+
+def implementation():
+    """The reference's own functions when its unmodified package is installed under
+    baseline/_ref (pip install --no-deps --target baseline/_ref <reference pkg>), else the
+    oracle port.  Returns (factor_A, factor_G, damped_inverse, precondition, kind)."""
+    import sys
+    if os.path.isdir(os.path.join(_REF_DIR, "kfacsched")):
+        if _REF_DIR not in sys.path:
+            sys.path.insert(0, _REF_DIR)
+        try:
+            import kfacsched as K
+            return K.compute_factor_A, K.compute_factor_G, K.damped_inverse, K.precondition, "reference"
+        except Exception:  # pragma: no cover - broken install: fall back to the port
+            pass
+    return factor_A, factor_G, damped_inverse, precondition, "port"
+
 
 def distinct_shapes(shapes):
     """[(M, a, g)] -> Counter of multiplicities, in first-seen order."""
@@ -29,17 +47,18 @@ def distinct_shapes(shapes):
 
 
 def time_layer(m: int, a: int, g: int, gamma: float = 0.1, alpha: float = 0.1, seed: int = 0) -> float:
+    fa, fg, dinv, pre, _ = implementation()
     rng = np.random.default_rng(seed)
     rows_a = rng.standard_normal((m, a))
     rows_g = rng.standard_normal((m, g))
     grad = rng.standard_normal((g, a))
     w = rng.standard_normal((g, a))
     t0 = time.perf_counter()
-    A = factor_A(rows_a)
-    G = factor_G(rows_g)
-    ai = damped_inverse(A, gamma)
-    gi = damped_inverse(G, gamma)
-    w -= alpha * precondition(grad, ai, gi)
+    A = fa(rows_a)
+    G = fg(rows_g)
+    ai = dinv(A, gamma)
+    gi = dinv(G, gamma)
+    w -= alpha * pre(grad, ai, gi)
     return time.perf_counter() - t0
 
 

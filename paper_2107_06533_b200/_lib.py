@@ -14,7 +14,7 @@ _HERE = pathlib.Path(__file__).resolve().parent
 LIB_PATH = pathlib.Path(os.environ.get("SPDKFAC_LIB", _HERE / "lib" / "libspdkfac.so"))
 
 OK, ERR_NOT_PD, ERR_SHAPE, ERR_ARG, ERR_CUDA, ERR_NCCL, ERR_UNSUPPORTED = range(7)
-ROWS, CONV_A, SPATIAL = 0, 1, 2
+ROWS, CONV_A, SPATIAL, CONV_A_NHWC, SPATIAL_NHWC = 0, 1, 2, 3, 4
 
 
 class FactorGeom(C.Structure):

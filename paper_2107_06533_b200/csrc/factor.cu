@@ -14,26 +14,26 @@ namespace spd {
 // ------------------------------------------------------------------ staging kernels
 // Xt[r][m] (r < d, m < Mpad) ; planes hi at 0, lo at d*Mpad.  Zero for m >= M.
 
-__global__ void stage_rows_kernel(const float* __restrict__ x, int64_t M, int64_t d, int64_t ldx,
-                                  __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
-  // 32x32 transpose tile through shared memory: coalesced reads along d, writes along m
-  __shared__ float tile[32][33];
-  const int64_t m0 = int64_t(blockIdx.x) * 32, r0 = int64_t(blockIdx.y) * 32;
-  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-  for (int k = ty; k < 32; k += 8) {
+__device__ __forceinline__ void store_split2(__nv_bfloat16* xt, int64_t plane, int64_t o, float v0, float v1);
+
+// [M][d] rows (row stride ldx) -> K-major split planes Xt[2][d][Mpad].  64(m) x 32(r) tiles
+// through shared memory: 128-B reads along r, bf16x2 (128-B per warp) writes along m.
+__global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict__ x, int64_t M, int64_t d,
+                                                         int64_t ldx, __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
+  __shared__ float tile[64][33];
+  const int64_t m0 = int64_t(blockIdx.x) * 64, r0 = int64_t(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+  for (int k = ty; k < 64; k += 8) {
     const int64_t m = m0 + k, r = r0 + tx;
-    tile[k][tx] = (m < M && r < d) ? x[m * ldx + r] : 0.f;
+    tile[k][tx] = (m < M && r < d) ? __ldg(x + m * ldx + r) : 0.f;
   }
   __syncthreads();
   const int64_t plane = d * Mpad;
+#pragma unroll
   for (int k = ty; k < 32; k += 8) {
-    const int64_t r = r0 + k, m = m0 + tx;
-    if (r < d && m < Mpad) {
-      __nv_bfloat16 h, l;
-      split_bf16(tile[tx][k], h, l);
-      xt[r * Mpad + m] = h;
-      xt[plane + r * Mpad + m] = l;
-    }
+    const int64_t r = r0 + k, m = m0 + 2 * tx;
+    if (r < d && m < Mpad) store_split2(xt, plane, r * Mpad + m, tile[2 * tx][k], tile[2 * tx + 1][k]);
   }
 }
 
@@ -97,6 +97,48 @@ __global__ void __launch_bounds__(256) stage_im2col_kernel(const float* __restri
       xt[row + q] = h;
       xt[plane + row + q] = l;
     }
+  }
+}
+
+// channels-last input x[b][h][w][c]; patch rows ordered (ki, kj, c) -- the column order of a
+// channels-last conv weight viewed as [cout][kh*kw*cin].  32(m) x 32(c) tiles through shared
+// memory: reads coalesced along c, bf16x2 hi/lo writes coalesced along m.
+__global__ void __launch_bounds__(256) stage_im2col_nhwc_kernel(const float* __restrict__ x, ConvGeom g, int64_t M,
+                                                                int64_t d, __nv_bfloat16* __restrict__ xt,
+                                                                int64_t Mpad) {
+  __shared__ float tile[64][33];
+  __shared__ int rowoff[64];  // element offset of (b, hi, wi, 0) for the block's 64 rows, -1 = padding
+  const int kk = blockIdx.z, ki = kk / g.kw, kj = kk - ki * g.kw;
+  const uint32_t m0 = blockIdx.x * 64u;
+  const int c0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  if (threadIdx.x < 64) {
+    const uint32_t m = m0 + threadIdx.x;
+    int off = -1;
+    if (m < uint32_t(M)) {
+      const uint32_t HWo = uint32_t(g.Ho) * g.Wo;
+      const uint32_t b = m / HWo, q = m - b * HWo;
+      const uint32_t ho = q / uint32_t(g.Wo), wo = q - ho * g.Wo;
+      const int hi = int(ho) * g.sh - g.ph + ki * g.dh, wi = int(wo) * g.sw - g.pw + kj * g.dw;
+      if (hi >= 0 && hi < g.H && wi >= 0 && wi < g.W) off = ((int(b) * g.H + hi) * g.W + wi) * g.C;
+    }
+    rowoff[threadIdx.x] = off;
+  }
+  __syncthreads();
+  const int c = c0 + tx;
+#pragma unroll
+  for (int r = ty; r < 64; r += 8) {
+    const int off = rowoff[r];
+    tile[r][tx] = (off >= 0 && c < g.C) ? __ldg(x + off + c) : 0.f;
+  }
+  __syncthreads();
+  const int64_t plane = d * Mpad;
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int cc = c0 + r;
+    const int64_t m = int64_t(m0) + 2 * tx;
+    if (cc < g.C && m < Mpad)
+      store_split2(xt, plane, (int64_t(kk) * g.C + cc) * Mpad + m, tile[2 * tx][r], tile[2 * tx + 1][r]);
   }
 }
 
@@ -188,7 +230,7 @@ int geom_dims(const spdkfac_factor_geom* g, int64_t* rows, int64_t* dim, int* Ho
             (long long)g->c, (long long)g->w);
     *rows = g->n;
     *dim = g->c;
-  } else if (g->layout == SPDKFAC_CONV_A) {
+  } else if (g->layout == SPDKFAC_CONV_A || g->layout == SPDKFAC_CONV_A_NHWC) {
     SPD_ARG(g->n >= 1 && g->c >= 1 && g->h >= 1 && g->w >= 1, SPDKFAC_ERR_ARG, "conv factor: empty input");
     SPD_ARG(g->kh >= 1 && g->kw >= 1 && g->stride_h >= 1 && g->stride_w >= 1 && g->dil_h >= 1 && g->dil_w >= 1 &&
                 g->pad_h >= 0 && g->pad_w >= 0,
@@ -196,11 +238,12 @@ int geom_dims(const spdkfac_factor_geom* g, int64_t* rows, int64_t* dim, int* Ho
     const int64_t ho = (g->h + 2 * g->pad_h - g->dil_h * (g->kh - 1) - 1) / g->stride_h + 1;
     const int64_t wo = (g->w + 2 * g->pad_w - g->dil_w * (g->kw - 1) - 1) / g->stride_w + 1;
     SPD_ARG(ho >= 1 && wo >= 1, SPDKFAC_ERR_SHAPE, "conv factor: empty output");
+    SPD_ARG(g->n * g->c * g->h * g->w < (int64_t(1) << 31), SPDKFAC_ERR_SHAPE, "conv factor: input too large");
     *rows = g->n * ho * wo;
     *dim = g->c * g->kh * g->kw;
     if (Ho) *Ho = int(ho);
     if (Wo) *Wo = int(wo);
-  } else if (g->layout == SPDKFAC_SPATIAL) {
+  } else if (g->layout == SPDKFAC_SPATIAL || g->layout == SPDKFAC_SPATIAL_NHWC) {
     SPD_ARG(g->n >= 1 && g->c >= 1 && g->h >= 1 && g->w >= 1, SPDKFAC_ERR_ARG, "spatial factor: empty input");
     *rows = g->n * g->h * g->w;
     *dim = g->c;
@@ -339,9 +382,19 @@ int spdkfac_factor_plan_stage(spdkfac_factor_plan* p, const float* x, void* stre
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const spdkfac_factor_geom& g = p->g;
   stat_begin(kCatFactorStage, s);
-  if (g.layout == SPDKFAC_ROWS) {
-    dim3 grid(unsigned(cdiv(p->Mpad, 32)), unsigned(cdiv(p->d, 32)));
-    stage_rows_kernel<<<grid, dim3(32, 8), 0, s>>>(x, p->M, p->d, g.w, p->xt, p->Mpad);
+  if (g.layout == SPDKFAC_ROWS || g.layout == SPDKFAC_SPATIAL_NHWC) {
+    // channels-last output gradients are rows [b*h*w][C]: the same transpose
+    const int64_t ld = g.layout == SPDKFAC_ROWS ? g.w : g.c;
+    dim3 grid(unsigned(cdiv(p->Mpad, 64)), unsigned(cdiv(p->d, 32)));
+    stage_rows_kernel<<<grid, 256, 0, s>>>(x, p->M, p->d, ld, p->xt, p->Mpad);
+  } else if (g.layout == SPDKFAC_CONV_A_NHWC) {
+    int64_t rows, dim;
+    int Ho = 0, Wo = 0;
+    geom_dims(&g, &rows, &dim, &Ho, &Wo);
+    ConvGeom cg{int(g.n), int(g.c), int(g.h), int(g.w), Ho, Wo, g.kh, g.kw, g.stride_h, g.stride_w,
+                g.pad_h, g.pad_w, g.dil_h, g.dil_w};
+    dim3 grid(unsigned(cdiv(p->Mpad, 64)), unsigned(cdiv(g.c, 32)), unsigned(g.kh * g.kw));
+    stage_im2col_nhwc_kernel<<<grid, 256, 0, s>>>(x, cg, p->M, p->d, p->xt, p->Mpad);
   } else if (g.layout == SPDKFAC_CONV_A) {
     int64_t rows, dim;
     int Ho = 0, Wo = 0;

@@ -82,7 +82,9 @@ class FactorPlan:
     def run(self, x: torch.Tensor, packed: torch.Tensor, scale: float | None = None, decay: float = 0.0,
             world_scale: float = 1.0, stream=None) -> None:
         """packed <- world_scale*(decay*packed + (1-decay)*scale*X^T X); scale defaults to 1/rows."""
-        assert x.is_contiguous() and x.dtype == torch.float32 and packed.dtype == torch.float32
+        fmt = torch.channels_last if self.geom.layout in (L.CONV_A_NHWC, L.SPATIAL_NHWC) else torch.contiguous_format
+        if not (x.is_contiguous(memory_format=fmt) and x.dtype == torch.float32 and packed.dtype == torch.float32):
+            raise ValueError("factor input must be float32 in the plan's memory format; packed float32")
         s = 1.0 / self.rows if scale is None else float(scale)
         L.check(self._lib.spdkfac_factor_plan_run(self._h, x.data_ptr(), s, float(decay), float(world_scale),
                                                   packed.data_ptr(), _stream(stream)), "factor run")

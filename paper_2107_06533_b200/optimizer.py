@@ -63,6 +63,7 @@ class _Layer:
     g_plan: Optional[FactorPlan] = None
     a_key: tuple = ()
     g_key: tuple = ()
+    w_cl: bool = False  # conv weight stored channels-last: A rows ordered (kh, kw, c)
     handles: list = field(default_factory=list)
     events: dict = field(default_factory=dict)   # kind -> (compute done, staged)
     pending: dict = field(default_factory=lambda: {"A": False, "G": False})
@@ -151,16 +152,24 @@ class SPDKFAC(torch.optim.Optimizer):
         for l in self.layers:
             self.inv.append(torch.zeros(l.spec.a_dim, l.spec.a_dim, dtype=torch.float32, device=self.device))
             self.inv.append(torch.zeros(l.spec.g_dim, l.spec.g_dim, dtype=torch.float32, device=self.device))
+        # this rank's inversions, split by side: A inverses only need the forward pass's
+        # factors, so they run on their own stream concurrently with the backward pass
         mine = list(self.placement.workers[self.rank])
         self._mine = mine
-        self._inv_plan = InversePlan([self._packed(t) for t in mine], [self.inv[t] for t in mine]) if mine else None
-        self._bcast = self._bcast_layout()
+        self._inv_plans, self._info_host = {}, {}
+        for side, par in (("A", 0), ("G", 1)):
+            ts = [t for t in mine if t % 2 == par]
+            self._inv_plans[side] = InversePlan([self._packed(t) for t in ts], [self.inv[t] for t in ts]) if ts else None
+            self._info_host[side] = torch.zeros(len(ts), dtype=torch.int32, pin_memory=True) if ts else None
+        self._bcast = {side: self._bcast_layout(par) for side, par in (("A", 0), ("G", 1))}
         self._precond = PrecondPlan([(l.spec.g_dim, l.spec.a_dim) for l in self.layers], device=self.device)
 
         self.factor_stream = torch.cuda.Stream(self.device)
+        self.inv_stream = torch.cuda.Stream(self.device)
         self.comm_stream = torch.cuda.Stream(self.device) if self.world > 1 else None
-        self._info_host = torch.zeros(len(mine), dtype=torch.int32, pin_memory=True) if mine else None
-        self._info_event = None
+        self._info_events = []
+        self._a_count = 0
+        self._a_inverted = False
         self._precond_key = None
         self.steps = 0
         self._capture = True
@@ -199,13 +208,13 @@ class SPDKFAC(torch.optim.Optimizer):
             out.append((idx[-1], s, e))
         return {last: (s, e) for last, s, e in out}
 
-    def _bcast_layout(self):
-        """Per owner rank: its CT tensors (plan order) and a packed staging buffer."""
+    def _bcast_layout(self, parity: int):
+        """Per owner rank: its CT tensors of one side (plan order) and a packed staging buffer."""
         if self.world == 1:
             return None
         lay = []
         for p, lst in enumerate(self.placement.workers):
-            ct = [t for t in lst if t not in self.placement.nct]
+            ct = [t for t in lst if t not in self.placement.nct and t % 2 == parity]
             dims = [self.inv[t].shape[0] for t in ct]
             n = sum(d * (d + 1) // 2 for d in dims)
             buf = torch.empty(max(n, 1), dtype=torch.float32, device=self.device)
@@ -216,8 +225,20 @@ class SPDKFAC(torch.optim.Optimizer):
             lay.append((ct, dims, buf, views, n))
         return lay
 
+    def _weight_matrix(self, l: _Layer, t: torch.Tensor) -> torch.Tensor:
+        """[d_out][d_in] view of a weight (or its gradient) in the A-factor column order."""
+        if l.is_conv and l.w_cl:
+            v = t.permute(0, 2, 3, 1).reshape(l.spec.g_dim, l.spec.a_dim)
+        else:
+            v = t.reshape(l.spec.g_dim, l.spec.a_dim)
+        if v.data_ptr() != t.data_ptr() or not v.is_contiguous():
+            raise RuntimeError(f"layer {l.name}: weight/gradient is not a dense [d_out, d_in] view")
+        return v
+
     def _install_hooks(self):
         for l in self.layers:
+            if l.is_conv:
+                l.w_cl = self._weight_channels_last(l.module)
             l.events = {k: (torch.cuda.Event(), torch.cuda.Event()) for k in ("A", "G")}
             l.handles.append(l.module.register_forward_pre_hook(self._make_a_hook(l)))
             l.handles.append(l.module.register_forward_hook(self._make_out_hook(l)))
@@ -233,22 +254,42 @@ class SPDKFAC(torch.optim.Optimizer):
         decay = self.factor_decay if self._factor_updates > 0 else 0.0
         return decay, 1.0 / self.world
 
-    def _plan_for(self, l: _Layer, x: torch.Tensor, kind: str) -> FactorPlan:
-        key = tuple(x.shape)
+    @staticmethod
+    def _weight_channels_last(m) -> bool:
+        w = m.weight
+        return w.dim() == 4 and not w.is_contiguous() and w.is_contiguous(memory_format=torch.channels_last)
+
+    def _prepare(self, l: _Layer, x: torch.Tensor, kind: str):
+        """Pick the staging layout that matches the tensor's memory format (no copy in the
+        common cases).  A-factor rows follow the weight's column order: (c, kh, kw) for a
+        contiguous conv weight, (kh, kw, c) for a channels-last one."""
+        if x.dtype != torch.float32:
+            x = x.to(torch.float32)
+        if not l.is_conv:
+            x = x.contiguous()
+            return L.ROWS, x.reshape(-1, x.shape[-1])
+        cl = torch.channels_last
+        if kind == "A":
+            if l.w_cl:
+                return L.CONV_A_NHWC, x.contiguous(memory_format=cl)
+            return L.CONV_A, x.contiguous()
+        if x.is_contiguous():
+            return L.SPATIAL, x
+        return L.SPATIAL_NHWC, x.contiguous(memory_format=cl)
+
+    def _plan_for(self, l: _Layer, layout: int, x: torch.Tensor, kind: str) -> FactorPlan:
+        key = (layout,) + tuple(x.shape)
         m = l.module
         if kind == "A":
             if l.a_key != key:
                 if l.is_conv:
-                    l.a_plan = FactorPlan(L.CONV_A, x.shape, m.kernel_size, m.stride, m.padding, m.dilation)
+                    l.a_plan = FactorPlan(layout, x.shape, m.kernel_size, m.stride, m.padding, m.dilation)
                 else:
-                    l.a_plan = FactorPlan(L.ROWS, (x.numel() // x.shape[-1], x.shape[-1]))
+                    l.a_plan = FactorPlan(L.ROWS, x.shape)
                 l.a_key = key
             return l.a_plan
         if l.g_key != key:
-            if l.is_conv:
-                l.g_plan = FactorPlan(L.SPATIAL, x.shape)
-            else:
-                l.g_plan = FactorPlan(L.ROWS, (x.numel() // x.shape[-1], x.shape[-1]))
+            l.g_plan = FactorPlan(layout, x.shape) if l.is_conv else FactorPlan(L.ROWS, x.shape)
             l.g_key = key
         return l.g_plan
 
@@ -258,10 +299,10 @@ class SPDKFAC(torch.optim.Optimizer):
         only plan memory, so x's lifetime is not extended across streams."""
         main = torch.cuda.current_stream(self.device)
         fs = self.factor_stream
-        x = x.detach()
-        if x.dtype != torch.float32 or not x.is_contiguous():
-            x = x.to(torch.float32).contiguous()
-        plan = self._plan_for(l, x, kind)
+        # samples of a batch-mean loss: the image batch for convs, the rows for linears
+        nb = x.shape[0] if l.is_conv else x.numel() // x.shape[-1]
+        layout, x = self._prepare(l, x.detach(), kind)
+        plan = self._plan_for(l, layout, x, kind)
         ev_done, ev_staged = l.events[kind]
         capturing = torch.cuda.is_current_stream_capturing()
         if not capturing and l.pending[kind]:
@@ -273,7 +314,7 @@ class SPDKFAC(torch.optim.Optimizer):
         if kind == "A":
             buf, off, d, scale = self.bufA, l.a_off, l.spec.a_dim, 1.0 / plan.rows
         else:
-            b = x.shape[0] if self.batch_averaged else 1
+            b = nb if self.batch_averaged else 1
             buf, off, d, scale = self.bufG, l.g_off, l.spec.g_dim, float(b * b) / plan.rows
         plan.compute(buf[off:off + d * (d + 1) // 2], scale, decay, 1.0 / self.world, fs)
         ev_done.record(fs)
@@ -284,6 +325,38 @@ class SPDKFAC(torch.optim.Optimizer):
             cs = self.comm_stream
             cs.wait_stream(fs)
             self.comm.allreduce_sum(buf[s:e], cs)
+        if kind == "A":
+            self._a_count += 1
+            if self._a_count == len(self.layers):
+                self._launch_inverse_A()
+
+    def _inverting(self) -> bool:
+        return self.steps % self.inv_update_freq == 0
+
+    def _launch_inverse_A(self):
+        """All A factors of this iteration are enqueued (and, for P > 1, their fusion-group
+        all-reduces): invert this rank's A tensors on the inverse stream, overlapping the
+        rest of the forward pass and the backward pass, and broadcast the CT ones."""
+        if self._a_inverted or not self._inverting():
+            return
+        s = self.inv_stream
+        s.wait_stream(self.factor_stream)
+        if self.world > 1:
+            s.wait_stream(self.comm_stream)
+        self._run_inverse("A", s)
+        self._a_inverted = True
+
+    def _run_inverse(self, side: str, stream) -> None:
+        plan = self._inv_plans[side]
+        if plan is not None:
+            plan.run(self.damping, stream)
+            self._info_host[side].copy_(plan.info, non_blocking=True)
+            if not torch.cuda.is_current_stream_capturing():
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                self._info_events.append((ev, side, self.steps))
+        if self.world > 1:
+            self._exchange_inverses(side, stream)
 
     def _make_a_hook(self, l: _Layer):
         def hook(module, inputs):
@@ -298,23 +371,28 @@ class SPDKFAC(torch.optim.Optimizer):
         return hook
 
     # ------------------------------------------------------------------ step
-    def check_inverses(self) -> None:
-        """Raise NotPositiveDefiniteError for the last completed inversion
-        (linalg.py:141-145); synchronises only on that inversion's event."""
-        if self._info_event is None:
-            return
-        self._info_event.synchronize()
-        self._info_event = None
-        bad = torch.nonzero(self._info_host).flatten()
-        if bad.numel():
-            raise NotPositiveDefiniteError(int(self._info_host[bad[0]]) - 1)
+    def check_inverses(self, previous_steps_only: bool = False) -> None:
+        """Raise NotPositiveDefiniteError for completed inversions (linalg.py:141-145);
+        synchronises only on those inversions' events.  step() checks the previous steps'
+        inversions only, so it never waits for the current iteration's A inverses."""
+        if previous_steps_only:
+            events = [e for e in self._info_events if e[2] < self.steps]
+            self._info_events = [e for e in self._info_events if e[2] >= self.steps]
+        else:
+            events, self._info_events = self._info_events, []
+        for ev, side, _ in events:
+            ev.synchronize()
+            info = self._info_host[side]
+            bad = torch.nonzero(info).flatten()
+            if bad.numel():
+                raise NotPositiveDefiniteError(int(info[bad[0]]) - 1)
 
     @torch.no_grad()
     def step(self, closure=None):
         loss = closure() if closure is not None else None
         capturing = torch.cuda.is_current_stream_capturing()
         if not capturing:
-            self.check_inverses()
+            self.check_inverses(previous_steps_only=True)
         main = torch.cuda.current_stream(self.device)
         lr = self.param_groups[0]["lr"]
         factors_now = self._capture
@@ -331,14 +409,10 @@ class SPDKFAC(torch.optim.Optimizer):
                     self.comm.allreduce_sum(g, cs)
             main.wait_stream(cs)  # also orders the factor all-reduces before inversion
         if invert_now:
-            if self._inv_plan is not None:
-                self._inv_plan.run(self.damping, main)
-                self._info_host.copy_(self._inv_plan.info, non_blocking=True)
-                if not capturing:  # graph replays record this event after the replay (GraphedStep)
-                    self._info_event = torch.cuda.Event()
-                    self._info_event.record(main)
-            if self.world > 1:
-                self._exchange_inverses(main)
+            if not self._a_inverted:  # hooks did not see a full forward (e.g. factors reused)
+                self._launch_inverse_A()
+            self._run_inverse("G", main)
+            main.wait_stream(self.inv_stream)  # A inverses (and their broadcasts) landed
         # precondition + update for every K-FAC layer (mean gradient = sum / P); the pointer
         # tables are rebuilt only when a gradient's storage changes (zero_grad(set_to_none=True))
         key = tuple(l.module.weight.grad.data_ptr() if l.module.weight.grad is not None else 0 for l in self.layers)
@@ -346,15 +420,20 @@ class SPDKFAC(torch.optim.Optimizer):
             if 0 in key:
                 missing = [l.name for l in self.layers if l.module.weight.grad is None]
                 raise RuntimeError(f"layers {missing[:3]} have no gradient; call backward() before step()")
+            for l in self.layers:  # memory format may change (model.to(channels_last) after construction)
+                if l.is_conv:
+                    l.w_cl = self._weight_channels_last(l.module)
             self._precond.bind([self.inv[2 * l.index + 1] for l in self.layers],
-                               [l.module.weight.grad.reshape(l.spec.g_dim, l.spec.a_dim) for l in self.layers],
+                               [self._weight_matrix(l, l.module.weight.grad) for l in self.layers],
                                [self.inv[2 * l.index] for l in self.layers],
-                               weights=[l.module.weight.data for l in self.layers])
+                               weights=[self._weight_matrix(l, l.module.weight.data) for l in self.layers])
             self._precond_key = key
         self._precond.run_bound(lr / self.world, stream=main)
         others = [p for p in self.other_params if p.grad is not None]
         if others:
             torch._foreach_add_([p.data for p in others], [p.grad for p in others], alpha=-lr / self.world)
+        self._a_count = 0
+        self._a_inverted = False
         if not capturing:  # a captured step is counted per replay (_after_replay)
             self.steps += 1
             self._capture = self.steps % self.factor_update_freq == 0
@@ -364,15 +443,18 @@ class SPDKFAC(torch.optim.Optimizer):
         """Bookkeeping for one replay of a captured step (GraphedStep): the Python side
         effects of step() ran once at capture time."""
         self.steps += 1
-        if self._inv_plan is not None:
-            self._info_event = torch.cuda.Event()
-            self._info_event.record(stream)
+        for side in ("A", "G"):
+            if self._inv_plans[side] is not None:
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                self._info_events.append((ev, side, self.steps - 1))
 
-    def _exchange_inverses(self, main):
-        """Owner ranks broadcast their CT inverses (packed upper triangle,
+    def _exchange_inverses(self, side, main):
+        """Owner ranks broadcast their CT inverses of one side (packed upper triangle,
         PAPER.md:281-283 / emulator.py:256-262), one NCCL broadcast per owner."""
         lib = L.load()
-        ct, dims, buf, views, n = self._bcast[self.rank]
+        lay = self._bcast[side]
+        ct, dims, buf, views, n = lay[self.rank]
         if ct:
             L.check(lib.spdkfac_pack_upper_batched_f32(len(ct), L.i32_array(dims),
                                                        L.ptr_array([self.inv[t].data_ptr() for t in ct]),
@@ -381,11 +463,11 @@ class SPDKFAC(torch.optim.Optimizer):
         cs = self.comm_stream
         cs.wait_stream(main)
         with self.comm.group():
-            for root, (ct_r, _, buf_r, _, n_r) in enumerate(self._bcast):
+            for root, (ct_r, _, buf_r, _, n_r) in enumerate(lay):
                 if n_r:
                     self.comm.bcast(buf_r[:n_r], root, cs)
         main.wait_stream(cs)
-        for root, (ct_r, dims_r, _, views_r, n_r) in enumerate(self._bcast):
+        for root, (ct_r, dims_r, _, views_r, n_r) in enumerate(lay):
             if root == self.rank or not ct_r:
                 continue
             L.check(lib.spdkfac_unpack_upper_batched_f32(len(ct_r), L.i32_array(dims_r),

@@ -73,10 +73,12 @@ class SmallNet(nn.Module):
         return self.fc(x.flatten(1))
 
 
-def conv_step(device="cuda:0", seed=0, gamma=0.1, lr=0.1):
+def conv_step(device="cuda:0", seed=0, gamma=0.1, lr=0.1, channels_last=False):
     from paper_2107_06533_b200.optimizer import SPDKFAC
     torch.manual_seed(seed)
     model = SmallNet().to(device)
+    if channels_last:
+        model = model.to(memory_format=torch.channels_last)
     w0 = {n: m.weight.detach().double().cpu().numpy().copy() for n, m in model.named_children()}
     cap = {}
 
@@ -96,6 +98,8 @@ def conv_step(device="cuda:0", seed=0, gamma=0.1, lr=0.1):
     opt = SPDKFAC(model, lr=lr, damping=gamma)
     b = 16
     x = torch.randn(b, 3, 8, 8, device=device)
+    if channels_last:
+        x = x.contiguous(memory_format=torch.channels_last)
     y = torch.randint(0, 10, (b,), device=device)
     loss = nn.functional.cross_entropy(model(x), y)
     loss.backward()
@@ -133,6 +137,9 @@ def run_smoke():
     assert max(errs) <= TOL, errs
     cerrs = conv_step()
     print("conv net: per-layer relative update error", {k: "%.2e" % v for k, v in cerrs.items()})
+    assert max(cerrs.values()) <= TOL, cerrs
+    cerrs = conv_step(channels_last=True)
+    print("conv net (channels-last): per-layer relative update error", {k: "%.2e" % v for k, v in cerrs.items()})
     assert max(cerrs.values()) <= TOL, cerrs
     print("smoke OK")
 

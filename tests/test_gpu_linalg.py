@@ -81,6 +81,39 @@ def test_factor_conv_matches_oracle(shape, k, s, p):
     assert relf(got, want) <= FACTOR_TOL
 
 
+@pytest.mark.parametrize("shape,k,s,p", [((2, 3, 9, 9), 3, 1, 1), ((4, 16, 14, 14), 3, 2, 1), ((2, 3, 32, 32), 7, 2, 3),
+                                         ((8, 64, 8, 8), 1, 1, 0), ((2, 40, 28, 28), 3, 1, 1)])
+def test_factor_conv_channels_last(shape, k, s, p):
+    """NHWC staging: rows ordered (kh, kw, c) = the oracle's (c, kh, kw) factor permuted."""
+    K = _K()
+    import paper_2107_06533_b200._lib as L
+    rng = np.random.default_rng(sum(shape) + 7 * k)
+    x = rng.standard_normal(shape).astype(np.float32)
+    xt = torch.tensor(x).cuda().contiguous(memory_format=torch.channels_last)
+    plan = K.FactorPlan(L.CONV_A_NHWC, x.shape, (k, k), (s, s), (p, p))
+    packed = torch.empty(plan.packed_size, device="cuda")
+    plan.run(xt, packed)
+    got = K.unpack_upper(packed, plan.dim)
+    c = shape[1]
+    perm = [ci * k * k + ki * k + kj for ki in range(k) for kj in range(k) for ci in range(c)]
+    want = O.factor_A(O.im2col_rows(x, k, k, s, p))[np.ix_(perm, perm)]
+    assert relf(got, want) <= FACTOR_TOL
+
+
+@pytest.mark.parametrize("shape", [(2, 5, 3, 3), (32, 64, 56, 56), (32, 2048, 7, 7)])
+def test_factor_spatial_channels_last(shape):
+    K = _K()
+    import paper_2107_06533_b200._lib as L
+    rng = np.random.default_rng(shape[1] + 1)
+    g = rng.standard_normal(shape).astype(np.float32)
+    gt = torch.tensor(g).cuda().contiguous(memory_format=torch.channels_last)
+    plan = K.FactorPlan(L.SPATIAL_NHWC, g.shape)
+    packed = torch.empty(plan.packed_size, device="cuda")
+    plan.run(gt, packed)
+    want = O.factor_G(O.conv_grad_rows(g))
+    assert relf(K.unpack_upper(packed, plan.dim), want) <= FACTOR_TOL
+
+
 @pytest.mark.parametrize("shape", [(2, 5, 3, 3), (32, 64, 56, 56), (32, 2048, 7, 7)])
 def test_factor_spatial_matches_oracle(shape):
     K = _K()

@@ -13,10 +13,10 @@ def test_golden_fixture_through_optimizer():
     assert max(errs) <= TOL, errs
 
 
-@pytest.mark.parametrize("seed", [0, 1])
-def test_conv_net_step_matches_oracle(seed):
+@pytest.mark.parametrize("seed,cl", [(0, False), (1, False), (0, True), (2, True)])
+def test_conv_net_step_matches_oracle(seed, cl):
     from tests.smoke_impl import TOL, conv_step
-    errs = conv_step(seed=seed)
+    errs = conv_step(seed=seed, channels_last=cl)
     assert max(errs.values()) <= TOL, errs
 
 
