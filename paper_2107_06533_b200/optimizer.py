@@ -30,6 +30,7 @@ import torch
 import torch.nn as nn
 
 from . import _lib as L
+from . import schedule as S
 from .linalg import FactorPlan, InversePlan, NotPositiveDefiniteError, PrecondPlan
 from .perfmodel import PerfParams, default_params
 from .planner import (FactorKind, FusionPolicy, inverse_tasks, factor_tasks, lbp_place, local_place, plan_fusion,
@@ -135,17 +136,18 @@ class SPDKFAC(torch.optim.Optimizer):
         else:
             self.placement = local_place(tasks, self.world)
 
-        # ---- packed fusion buffers: A in forward order, G in backward order
-        off = 0
+        # ---- packed fusion buffers: A in forward order, G in backward order (schedule.py)
+        a_dims = [l.spec.a_dim for l in self.layers]
+        g_dims = [l.spec.g_dim for l in self.layers]
+        a_off, g_off, size_a, size_g = S.packed_layout(a_dims, g_dims)
         for l in self.layers:
-            l.a_off, off = off, off + l.spec.a_dim * (l.spec.a_dim + 1) // 2
-        self.bufA = torch.zeros(off, dtype=torch.float32, device=self.device)
-        off = 0
-        for l in reversed(self.layers):
-            l.g_off, off = off, off + l.spec.g_dim * (l.spec.g_dim + 1) // 2
-        self.bufG = torch.zeros(off, dtype=torch.float32, device=self.device)
-        self._groups_fwd = self._group_slices(self.fwd_plan, FactorKind.A)
-        self._groups_bwd = self._group_slices(self.bwd_plan, FactorKind.G)
+            l.a_off, l.g_off = a_off[l.index], g_off[l.index]
+        self.bufA = torch.zeros(size_a, dtype=torch.float32, device=self.device)
+        self.bufG = torch.zeros(size_g, dtype=torch.float32, device=self.device)
+        self._groups_fwd = S.fusion_slices(self.fwd_plan, a_off, a_dims)
+        self._groups_bwd = S.fusion_slices(self.bwd_plan, g_off, g_dims)
+        S.check_fusion_cover(self._groups_fwd, size_a)
+        S.check_fusion_cover(self._groups_bwd, size_g)
 
         # ---- inverses (every rank holds all of them for preconditioning)
         self.inv = []
@@ -192,36 +194,14 @@ class SPDKFAC(torch.optim.Optimizer):
         d = l.spec.g_dim
         return self.bufG[l.g_off:l.g_off + d * (d + 1) // 2]
 
-    def _group_slices(self, plan, kind):
-        """(last layer index of the group, start, end) per fusion group."""
-        out = []
-        for g in plan.groups:
-            idx = [t.layer_index - 1 for t in g]
-            if kind is FactorKind.A:
-                s = self.layers[idx[0]].a_off
-                last = self.layers[idx[-1]]
-                e = last.a_off + last.spec.a_dim * (last.spec.a_dim + 1) // 2
-            else:
-                s = self.layers[idx[0]].g_off
-                last = self.layers[idx[-1]]
-                e = last.g_off + last.spec.g_dim * (last.spec.g_dim + 1) // 2
-            out.append((idx[-1], s, e))
-        return {last: (s, e) for last, s, e in out}
-
     def _bcast_layout(self, parity: int):
-        """Per owner rank: its CT tensors of one side (plan order) and a packed staging buffer."""
+        """Per owner rank: its CT tensors of one side (placement order) and packed staging views."""
         if self.world == 1:
             return None
         lay = []
-        for p, lst in enumerate(self.placement.workers):
-            ct = [t for t in lst if t not in self.placement.nct and t % 2 == parity]
-            dims = [self.inv[t].shape[0] for t in ct]
-            n = sum(d * (d + 1) // 2 for d in dims)
+        for ct, dims, offs, n in S.bcast_layout(self.placement, [t.shape[0] for t in self.inv], parity):
             buf = torch.empty(max(n, 1), dtype=torch.float32, device=self.device)
-            views, o = [], 0
-            for d in dims:
-                views.append(buf[o:o + d * (d + 1) // 2])
-                o += d * (d + 1) // 2
+            views = [buf[o:o + S.packed_size(d)] for o, d in zip(offs, dims)]
             lay.append((ct, dims, buf, views, n))
         return lay
 

@@ -1,0 +1,78 @@
+"""Communication schedule of the SPD-KFAC step (host logic, no device code).
+
+Pure functions shared by `SPDKFAC` (GPU, NCCL) and the CPU/gloo tests that check the
+multi-rank logic without a GPU:
+
+  packed_layout   offsets of each layer's packed factor in the two fusion buffers
+                  (A in forward order, G in backward order: a fusion group, planner.py:94-121,
+                  is then one contiguous slice = one all-reduce)
+  fusion_slices   {layer index that completes the group: (start, end)} per pass
+  bcast_layout    per owner rank, the CT tensors it broadcasts (placement order) and the
+                  packed offsets inside that owner's staging buffer (planner.py:141-207 and
+                  the owner-compute-then-share walk of emulator.py:256-262)
+"""
+
+from __future__ import annotations
+
+from typing import Sequence
+
+from .planner import FactorKind, FusionPlan, PlacementPlan
+
+
+def packed_size(d: int) -> int:
+    return d * (d + 1) // 2
+
+
+def packed_layout(a_dims: Sequence[int], g_dims: Sequence[int]):
+    """Returns (a_off, g_off, size_a, size_g): a_off[l] in forward order, g_off[l] in backward order."""
+    a_off, off = [], 0
+    for d in a_dims:
+        a_off.append(off)
+        off += packed_size(d)
+    size_a = off
+    g_off = [0] * len(g_dims)
+    off = 0
+    for l in reversed(range(len(g_dims))):
+        g_off[l] = off
+        off += packed_size(g_dims[l])
+    return a_off, g_off, size_a, off
+
+
+def fusion_slices(plan: FusionPlan, offsets: Sequence[int], dims: Sequence[int]) -> dict:
+    """{0-based layer index of the group's last member: (start, end)} for one pass."""
+    out = {}
+    for group in plan.groups:
+        idx = [t.layer_index - 1 for t in group]
+        first, last = idx[0], idx[-1]
+        out[last] = (offsets[first], offsets[last] + packed_size(dims[last]))
+    return out
+
+
+def check_fusion_cover(slices: dict, total: int) -> None:
+    """The groups of one pass tile its fusion buffer exactly once (no gap, no overlap)."""
+    spans = sorted(slices.values())
+    pos = 0
+    for s, e in spans:
+        if s != pos or e <= s:
+            raise ValueError(f"fusion slices do not tile the buffer at {pos}: {spans}")
+        pos = e
+    if pos != total:
+        raise ValueError(f"fusion slices cover {pos} of {total} elements")
+
+
+def bcast_layout(placement: PlacementPlan, dims: Sequence[int], parity: int | None = None) -> list:
+    """Per owner rank p: (ct tensor indices in p's placement order, their dims, offsets, total).
+    `parity` 0/1 restricts to A/G tensors (tensor_index = 2l / 2l+1, simulator.py:276-282)."""
+    out = []
+    for lst in placement.workers:
+        ct = [t for t in lst if t not in placement.nct and (parity is None or t % 2 == parity)]
+        offs, o = [], 0
+        for t in ct:
+            offs.append(o)
+            o += packed_size(dims[t])
+        out.append((ct, [dims[t] for t in ct], offs, o))
+    return out
+
+
+def kind_of(tensor_index: int) -> FactorKind:
+    return FactorKind.A if tensor_index % 2 == 0 else FactorKind.G
