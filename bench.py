@@ -65,6 +65,7 @@ def parse():
     p.add_argument("--mode", choices=("graph", "eager"), default="graph",
                    help="graph: the whole step (fwd, bwd, K-FAC step) replayed as one CUDA graph")
     p.add_argument("--clocks", choices=("nvml", "smi", "off"), default="nvml")
+    p.add_argument("--timeline", action="store_true", help="diagnostic: per-phase CUDA-event timeline of one eager step")
     p.add_argument("--stats-off", action="store_true", help="no per-launch CUDA events in the timed region (diagnostic)")
     p.add_argument("--optimizer", choices=("spdkfac", "sgd"), default="spdkfac",
                    help="sgd = diagnostic floor (forward/backward + SGD, no K-FAC); never the headline")
@@ -376,6 +377,14 @@ def run_ours(a):
                  for k, v in bst.items() if isinstance(v, dict)}
     breakdown["note"] = "separate 2-step pass with CUDA events around every library launch (not the timed region)"
 
+    timeline = None
+    if a.timeline and a.optimizer == "spdkfac":
+        opt.timeline = {}
+        (eager_step if graphed else step)(0)
+        torch.cuda.synchronize()
+        timeline = opt.timeline_ms()
+        opt.timeline = None
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline and not a.profile:
         cpu_ms, sample, _, kind = cpu_reference(a.model, a.batch)
@@ -392,7 +401,7 @@ def run_ours(a):
                "placement_imbalance": _imbalance(opt) if opt.placement is not None else None,
                "host_wall_ms_per_step": round(wall_ms, 3), "per_step_ms": per_step, "allocator_in_region": alloc_diag,
                "host_phase_ms_fwd_bwd_step": host_phases[a.warmup:a.warmup + a.steps] if a.profile is False else None,
-               "final_loss": final_loss}
+               "final_loss": final_loss, "timeline_ms": timeline}
         if a.optimizer != "spdkfac":
             out["diagnostic"] = f"optimizer={a.optimizer}: not the SPD-KFAC metric"
         if world > 1:

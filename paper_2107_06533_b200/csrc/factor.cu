@@ -142,6 +142,47 @@ __global__ void __launch_bounds__(256) stage_im2col_nhwc_kernel(const float* __r
   }
 }
 
+// channels-last im2col for few input channels (the stem conv: C = 3): one thread per pair of
+// output positions walks all (ki, kj, c) patch rows; bf16x2 stores stay coalesced along m and
+// the overlapping patch reads are served by L1.
+__global__ void __launch_bounds__(256) stage_im2col_nhwc_smallc_kernel(const float* __restrict__ x, ConvGeom g,
+                                                                       int64_t M, int64_t d,
+                                                                       __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
+  const int64_t m = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 2;
+  if (m >= Mpad) return;
+  const uint32_t HWo = uint32_t(g.Ho) * g.Wo;
+  int hb[2], wb[2], bo[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const uint32_t mm = uint32_t(m) + u;
+    if (mm < uint32_t(M)) {
+      const uint32_t b = mm / HWo, q = mm - b * HWo;
+      const uint32_t ho = q / uint32_t(g.Wo), wo = q - ho * g.Wo;
+      bo[u] = int(b) * g.H;
+      hb[u] = int(ho) * g.sh - g.ph;
+      wb[u] = int(wo) * g.sw - g.pw;
+    } else {
+      bo[u] = -1, hb[u] = 0, wb[u] = 0;
+    }
+  }
+  const int64_t plane = d * Mpad;
+  for (int ki = 0; ki < g.kh; ++ki)
+    for (int kj = 0; kj < g.kw; ++kj) {
+      int off[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int hi = hb[u] + ki * g.dh, wi = wb[u] + kj * g.dw;
+        off[u] = (bo[u] >= 0 && hi >= 0 && hi < g.H && wi >= 0 && wi < g.W) ? ((bo[u] + hi) * g.W + wi) * g.C : -1;
+      }
+      const int64_t row0 = int64_t(ki * g.kw + kj) * g.C;
+      for (int c = 0; c < g.C; ++c) {
+        const float v0 = off[0] >= 0 ? __ldg(x + off[0] + c) : 0.f;
+        const float v1 = off[1] >= 0 ? __ldg(x + off[1] + c) : 0.f;
+        store_split2(xt, plane, (row0 + c) * Mpad + m, v0, v1);
+      }
+    }
+}
+
 // rows m = (b, hw) of channel c: a contiguous copy of g[b][c][:] per image
 __global__ void __launch_bounds__(256) stage_spatial_kernel(const float* __restrict__ g, int C, int HW,
                                                             __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
@@ -175,31 +216,69 @@ __global__ void zero_pad_kernel(__nv_bfloat16* xt, int64_t d, int64_t M, int64_t
 
 // ------------------------------------------------------------------ reduce + pack
 // partial[slot][j][i] = D_tile[i][j]; slot = tile_index(I,J) * splits + s.
-__global__ void reduce_pack_kernel(const float* __restrict__ part, int64_t d, int T, int splits, float scale,
-                                   float decay, float world_scale, float* __restrict__ packed) {
+// Split-K reduction, one launch, deterministic: block (sub-block sb, upper tile, chunk c) sums
+// the 8 split-K partial tiles of its chunk (32 independent loads per thread), stores the chunk
+// sum, and the last chunk block to arrive (per tile/sub-block counter) adds the chunk sums in
+// fixed order, applies scale / running average / 1/P and writes the packed upper triangle.
+constexpr int kChunk = 8;
+
+__global__ void __launch_bounds__(256) reduce_pack_kernel(const float* __restrict__ part, int64_t d, int T, int splits,
+                                                          float scale, float decay, float world_scale,
+                                                          float* __restrict__ packed, float* __restrict__ chunks,
+                                                          int* __restrict__ counters) {
   __shared__ float tile[32][33];
-  const int I = blockIdx.z / T, J = blockIdx.z % T;  // tile pair (only I <= J launched work)
-  if (I > J) return;
-  const int tile_idx = I * T - I * (I - 1) / 2 + (J - I);  // row-major upper enumeration
-  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;     // within-tile 32x32 sub-block
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  // load: tx along i (contiguous in partial), ty along j
-  for (int k = ty; k < 32; k += 8) {
-    const int j = j0 + k, i = i0 + tx;
-    float acc = 0.f;
-    const float* p = part + (int64_t(tile_idx) * splits) * 16384 + int64_t(j) * 128 + i;
-    for (int s = 0; s < splits; ++s) acc += p[int64_t(s) * 16384];
-    tile[k][tx] = acc;  // tile[j][i]
+  __shared__ int last;
+  int I = 0, rem = blockIdx.y;
+  while (rem >= T - I) rem -= T - I, ++I;
+  const int J = I + rem;
+  const int tile_idx = blockIdx.y;
+  const int sb = blockIdx.x, i0 = (sb >> 2) * 32, j0 = (sb & 3) * 32;
+  if (int64_t(I) * 128 + i0 >= d || int64_t(J) * 128 + j0 >= d) return;
+  const int nch = (splits + kChunk - 1) / kChunk, ch = blockIdx.z;
+  const int s0 = ch * kChunk, s1 = min(splits, s0 + kChunk);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const float* base = part + (int64_t(tile_idx) * splits) * 16384 + i0 + tx;
+  float acc[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const float* p = base + int64_t(j0 + ty + 8 * r) * 128;
+    float a = 0.f;
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u)
+      if (s0 + u < s1) a += __ldg(p + int64_t(s0 + u) * 16384);
+    acc[r] = a;
   }
+  const int slot = tile_idx * 16 + sb;
+  if (nch > 1) {
+    float* mine = chunks + (int64_t(slot) * nch + ch) * 1024;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) mine[(ty + 8 * r) * 32 + tx] = acc[r];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(counters + slot, 1) == nch - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      float a = 0.f;
+      for (int c = 0; c < nch; ++c) a += __ldcg(chunks + (int64_t(slot) * nch + c) * 1024 + (ty + 8 * r) * 32 + tx);
+      acc[r] = a;
+    }
+    if (threadIdx.x == 0) counters[slot] = 0;  // ready for the next run
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) tile[ty + 8 * r][tx] = acc[r];  // tile[j][i]
   __syncthreads();
-  // store packed: rows gi (ty), consecutive gj (tx)
-  for (int k = ty; k < 32; k += 8) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int k = ty + 8 * r;
     const int64_t gi = int64_t(I) * 128 + i0 + k;
     const int64_t gj = int64_t(J) * 128 + j0 + tx;
     if (gi < d && gj < d && gi <= gj) {
       const int64_t pidx = gi * (2 * d - gi + 1) / 2 + (gj - gi);
       const float fresh = scale * tile[tx][k];
-      float v = (decay == 0.f) ? fresh : decay * packed[pidx] + (1.f - decay) * fresh;
+      const float v = (decay == 0.f) ? fresh : decay * packed[pidx] + (1.f - decay) * fresh;
       packed[pidx] = world_scale * v;
     }
   }
@@ -215,6 +294,8 @@ struct spdkfac_factor_plan {
   int T, splits, n_items;
   __nv_bfloat16* xt;
   float* partial;
+  float* chunks;
+  int* counters;
   CUtensorMap* maps;
   TcItem* items;
   TcEpi* epis;
@@ -279,6 +360,8 @@ size_t factor_ws(const FactorLayout& L, Carve* c) {
   Carve& cv = *c;
   cv.take<__nv_bfloat16>(size_t(2) * L.d * L.Mpad);
   cv.take<float>(L.splits > 1 ? size_t(L.n_tiles) * L.splits * 16384 : 1);
+  cv.take<float>(L.splits > 1 ? size_t(L.n_tiles) * 16 * cdiv(L.splits, kChunk) * 1024 : 1);
+  cv.take<int>(size_t(L.n_tiles) * 16);
   cv.take<CUtensorMap>(1, 128);
   cv.take<TcItem>(size_t(L.n_tiles) * L.splits);
   cv.take<TcEpi>(1);
@@ -318,6 +401,8 @@ int spdkfac_factor_plan_create(spdkfac_factor_plan** out, const spdkfac_factor_g
   p->n_items = L.n_tiles * L.splits;
   p->xt = c.take<__nv_bfloat16>(size_t(2) * d * L.Mpad);
   p->partial = c.take<float>(L.splits > 1 ? size_t(L.n_tiles) * L.splits * 16384 : 1);
+  p->chunks = c.take<float>(L.splits > 1 ? size_t(L.n_tiles) * 16 * cdiv(L.splits, kChunk) * 1024 : 1);
+  p->counters = c.take<int>(size_t(L.n_tiles) * 16);
   p->maps = c.take<CUtensorMap>(1, 128);
   p->items = c.take<TcItem>(size_t(p->n_items));
   p->epis = c.take<TcEpi>(1);
@@ -369,6 +454,7 @@ int spdkfac_factor_plan_create(spdkfac_factor_plan** out, const spdkfac_factor_g
     zero_pad_kernel<<<unsigned(d), 64, 0, s>>>(p->xt, d, M, L.Mpad);
     SPD_CHECK_LAUNCH();
   }
+  SPD_CUDA(cudaMemsetAsync(p->counters, 0, sizeof(int) * size_t(L.n_tiles) * 16, s));
   if ((rc = upload(p->maps, maps, s)) || (rc = upload(p->items, items, s)) || (rc = upload(p->epis, epis, s))) {
     delete p;
     return rc;
@@ -393,8 +479,13 @@ int spdkfac_factor_plan_stage(spdkfac_factor_plan* p, const float* x, void* stre
     geom_dims(&g, &rows, &dim, &Ho, &Wo);
     ConvGeom cg{int(g.n), int(g.c), int(g.h), int(g.w), Ho, Wo, g.kh, g.kw, g.stride_h, g.stride_w,
                 g.pad_h, g.pad_w, g.dil_h, g.dil_w};
-    dim3 grid(unsigned(cdiv(p->Mpad, 64)), unsigned(cdiv(g.c, 32)), unsigned(g.kh * g.kw));
-    stage_im2col_nhwc_kernel<<<grid, 256, 0, s>>>(x, cg, p->M, p->d, p->xt, p->Mpad);
+    if (g.c < 16) {
+      stage_im2col_nhwc_smallc_kernel<<<unsigned(cdiv(p->Mpad, 512)), 256, 0, s>>>(x, cg, p->M, p->d, p->xt,
+                                                                                   p->Mpad);
+    } else {
+      dim3 grid(unsigned(cdiv(p->Mpad, 64)), unsigned(cdiv(g.c, 32)), unsigned(g.kh * g.kw));
+      stage_im2col_nhwc_kernel<<<grid, 256, 0, s>>>(x, cg, p->M, p->d, p->xt, p->Mpad);
+    }
   } else if (g.layout == SPDKFAC_CONV_A) {
     int64_t rows, dim;
     int Ho = 0, Wo = 0;
@@ -425,10 +516,10 @@ int spdkfac_factor_plan_compute(spdkfac_factor_plan* p, float scale, float decay
   if (rc) return rc;
   stat_end(kCatFactorSyrk, s, double(p->M) * p->d * (p->d + 1), 4.0 * p->d * p->Mpad);
   if (p->splits == 1) return SPDKFAC_OK;
-  dim3 rgrid(4, 4, unsigned(p->T * p->T));
+  dim3 rgrid(16, unsigned(p->T * (p->T + 1) / 2), unsigned(cdiv(p->splits, kChunk)));
   stat_begin(kCatFactorReduce, s);
-  reduce_pack_kernel<<<rgrid, dim3(32, 8), 0, s>>>(p->partial, p->d, p->T, p->splits, scale, decay, world_scale,
-                                                   packed);
+  reduce_pack_kernel<<<rgrid, 256, 0, s>>>(p->partial, p->d, p->T, p->splits, scale, decay, world_scale,
+                                           packed, p->chunks, p->counters);
   SPD_CHECK_LAUNCH();
   stat_end(kCatFactorReduce, s, 0, 65536.0 * p->n_items + 4.0 * p->d * (p->d + 1) / 2 * (decay == 0.f ? 1 : 2));
   return SPDKFAC_OK;

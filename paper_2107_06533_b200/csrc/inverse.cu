@@ -322,15 +322,17 @@ struct spdkfac_inverse_plan {
   int32_t* blocked_ids;         // device
   int n_blocked;
   int steps;
-  std::vector<int> act_off, act_cnt, pan_off, pan_cnt, upd_off, upd_cnt, pj_off;
+  std::vector<int> act_off, act_cnt, pan_off, pan_cnt, upd_off, upd_cnt, pj_off, u1_cnt;
+  cudaStream_t side = nullptr;  // look-ahead stream: pivot/stage/panel of step k+1
+  cudaEvent_t ev_u1 = nullptr, ev_panel = nullptr;
   int32_t* act_ids;             // device, active blocked matrices per step (concatenated)
   PanelJob* pan_jobs;           // device, (matrix, R != K) per step, same order as the panel items
   TileJob* tiles;               // device, 32x32 tile pairs of all blocked matrices
   int n_tiles;
-  CUtensorMap* maps;            // [0] old panel planes, [1] C planes, [2] P^-1 planes, [3 + slot] W_slot tiles
+  CUtensorMap* maps;            // [0] panA0, [1] panC0, [2] P^-1, [3] panA1, [4] panC1, [5 + slot] W_slot tiles
   TcItem* items;                // per step: panel GEMM items then update items
-  TcEpi* epis;                  // [0, n): update, [n, 2n): panel
-  float* panA;
+  TcEpi* epis;                  // [0, n): update, [n, 2n) / [2n, 3n): panel writing panC parity 0 / 1
+  float* panA;                  // [2 parity][2 planes][rows][128]
   float* panC;
   float* pinvS;
   int64_t plane_rows;
@@ -375,8 +377,8 @@ size_t inverse_carve(int n, const int32_t* dims, Carve& c, spdkfac_inverse_plan*
     }
     if (mats) mats->push_back(m);
   }
-  float* panA = c.take<float>(size_t(2) * std::max<int64_t>(rows, 1) * kB);
-  float* panC = c.take<float>(size_t(2) * std::max<int64_t>(rows, 1) * kB);
+  float* panA = c.take<float>(size_t(4) * std::max<int64_t>(rows, 1) * kB);
+  float* panC = c.take<float>(size_t(4) * std::max<int64_t>(rows, 1) * kB);
   float* pinvS = c.take<float>(size_t(2) * std::max(nblk, 1) * kB * kB);
   auto* dm = c.take<InvMat>(size_t(n));
   auto* sid = c.take<int32_t>(size_t(n));
@@ -384,9 +386,9 @@ size_t inverse_carve(int n, const int32_t* dims, Carve& c, spdkfac_inverse_plan*
   auto* aid = c.take<int32_t>(size_t(std::max<int64_t>(act, 1)));
   auto* tj = c.take<TileJob>(size_t(std::max<int64_t>(tiles, 1)));
   auto* pj = c.take<PanelJob>(size_t(std::max<int64_t>(items, 1)));
-  auto* mp = c.take<CUtensorMap>(size_t(3 + nblk), 128);
+  auto* mp = c.take<CUtensorMap>(size_t(5 + nblk), 128);
   auto* it = c.take<TcItem>(size_t(std::max<int64_t>(items, 1)));
-  auto* ep = c.take<TcEpi>(size_t(2) * n);
+  auto* ep = c.take<TcEpi>(size_t(3) * n);
   if (p) {
     p->panA = panA, p->panC = panC, p->pinvS = pinvS, p->mats = dm, p->small_ids = sid, p->blocked_ids = bid;
     p->act_ids = aid, p->tiles = tj, p->pan_jobs = pj, p->maps = mp, p->items = it, p->epis = ep;
@@ -440,11 +442,13 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   p->n_small = int(small.size());
   p->n_blocked = int(blocked.size());
   const int64_t plane = p->plane_rows * kB;
-  std::vector<TcEpi> epis(size_t(2) * n);
+  const int64_t pbuf = 2 * plane;  // elements per parity buffer (2 planes)
+  std::vector<TcEpi> epis(size_t(3) * n);
   for (int t = 0; t < n; ++t) {
     epis[t] = TcEpi{mats[t].W, mats[t].dp, 0, -1.f, 1.f, kAxpby, 0, nullptr, 0, 0,
-                    dims[t] > kB ? 3 + mats[t].slot : 0};                                        // update
-    epis[n + t] = TcEpi{mats[t].W, mats[t].dp, 0, 1.f, 0.f, kAxpby, 0, p->panC, kB, plane};    // panel
+                    dims[t] > kB ? 5 + mats[t].slot : 0};                                               // update
+    epis[n + t] = TcEpi{mats[t].W, mats[t].dp, 0, 1.f, 0.f, kAxpby, 0, p->panC, kB, plane};           // panel, parity 0
+    epis[2 * n + t] = TcEpi{mats[t].W, mats[t].dp, 0, 1.f, 0.f, kAxpby, 0, p->panC + pbuf, kB, plane};  // parity 1
   }
   std::vector<TileJob> tiles;
   for (int t : blocked) {
@@ -469,20 +473,21 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
         if (R == k) continue;
         pan.push_back(PanelJob{t, R});
         const int prow = mats[t].panel_row0 + R * kB;
+        const int pa = (k & 1) ? 3 : 0;  // panA parity map
         TcItem it{};
         it.k0 = 0;
         it.nk = kB / 32;
-        it.epi = n + t;
+        it.epi = (k & 1 ? 2 * n : n) + t;
         it.m_valid = kB;
         it.n_valid = kB;
         it.o2_row = prow;
         if (R < k) {  // D'[j][i] = (P^-1 Wold[R,K]^T)[j][i] = C_R[i][j] -> W[R0 + i][K0 + j], panC coalesced
           it.a_map = 2, it.a_row = mats[t].slot * kB;
-          it.b_map = 0, it.b_row = prow;
+          it.b_map = pa, it.b_row = prow;
           it.out_r = k * kB, it.out_c = R * kB;
           it.flags = 0;
         } else {      // D[i][j] = C_R[i][j] -> W[K0 + j][R0 + i] (row panel), panC row-style
-          it.a_map = 0, it.a_row = prow;
+          it.a_map = pa, it.a_row = prow;
           it.b_map = 2, it.b_row = mats[t].slot * kB;
           it.out_r = R * kB, it.out_c = k * kB;
           it.flags = kOut2Rows;
@@ -492,43 +497,53 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     }
     p->pan_cnt.push_back(int(items.size()) - p->pan_off.back());
     p->upd_off.push_back(int(items.size()));
-    for (int t : blocked) {  // trailing update: W[I,J] -= Wold[I,K] C_J^T
-      const int T = mats[t].dp / kB;
-      if (k >= T) continue;
-      for (int I = 0; I < T; ++I)
-        for (int J = I; J < T; ++J) {
-          if (I == k || J == k) continue;
-          // D'[y][x] = sum_k Wold[J0+y][k] C[I0+x][k] = U[I0+x][J0+y] (U symmetric):
-          // the coalesced transposed store lands on the upper block W[I, J]
-          TcItem it{};
-          it.a_map = 0;
-          it.b_map = 1;
-          it.a_row = mats[t].panel_row0 + J * kB;
-          it.b_row = mats[t].panel_row0 + I * kB;
-          it.k0 = 0;
-          it.nk = kB / 32;
-          it.epi = t;
-          it.flags = 0;
-          it.out_r = J * kB;
-          it.out_c = I * kB;
-          it.m_valid = kB;
-          it.n_valid = kB;
-          items.push_back(it);
-        }
+    // U1: tiles in block row/column k+1 (what step k+1's pivot/panel read) first, then U2
+    int u1 = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int t : blocked) {  // trailing update: W[I,J] -= Wold[I,K] C_J^T
+        const int T = mats[t].dp / kB;
+        if (k >= T) continue;
+        for (int I = 0; I < T; ++I)
+          for (int J = I; J < T; ++J) {
+            if (I == k || J == k) continue;
+            const bool in_u1 = (I == k + 1 || J == k + 1);
+            if (in_u1 != (pass == 0)) continue;
+            // D'[y][x] = sum_k Wold[J0+y][k] C[I0+x][k] = U[I0+x][J0+y] (U symmetric):
+            // the coalesced transposed store lands on the upper block W[I, J]
+            TcItem it{};
+            it.a_map = (k & 1) ? 3 : 0;
+            it.b_map = (k & 1) ? 4 : 1;
+            it.a_row = mats[t].panel_row0 + J * kB;
+            it.b_row = mats[t].panel_row0 + I * kB;
+            it.k0 = 0;
+            it.nk = kB / 32;
+            it.epi = t;
+            it.flags = 0;
+            it.out_r = J * kB;
+            it.out_c = I * kB;
+            it.m_valid = kB;
+            it.n_valid = kB;
+            items.push_back(it);
+            if (pass == 0) ++u1;
+          }
+      }
     }
+    p->u1_cnt.push_back(u1);
     p->upd_cnt.push_back(int(items.size()) - p->upd_off.back());
   }
-  std::vector<CUtensorMap> maps(size_t(3 + p->n_blocked));
+  std::vector<CUtensorMap> maps(size_t(5 + p->n_blocked));
   int rc = SPDKFAC_OK;
   if (p->n_blocked > 0) {
     if ((rc = make_operand_map(&maps[0], p->panA, false, kB, p->plane_rows, kB)) ||
         (rc = make_operand_map(&maps[1], p->panC, false, kB, p->plane_rows, kB)) ||
-        (rc = make_operand_map(&maps[2], p->pinvS, false, kB, int64_t(p->n_blocked) * kB, kB))) {
+        (rc = make_operand_map(&maps[2], p->pinvS, false, kB, int64_t(p->n_blocked) * kB, kB)) ||
+        (rc = make_operand_map(&maps[3], p->panA + pbuf, false, kB, p->plane_rows, kB)) ||
+        (rc = make_operand_map(&maps[4], p->panC + pbuf, false, kB, p->plane_rows, kB))) {
       delete p;
       return rc;
     }
     for (int t : blocked)
-      if ((rc = make_ctile_map(&maps[3 + mats[t].slot], mats[t].W, mats[t].dp, mats[t].dp, mats[t].dp))) {
+      if ((rc = make_ctile_map(&maps[5 + mats[t].slot], mats[t].W, mats[t].dp, mats[t].dp, mats[t].dp))) {
         delete p;
         return rc;
       }
@@ -539,6 +554,11 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
       (rc = upload(p->items, items, s)) || (rc = upload(p->epis, epis, s))) {
     delete p;
     return rc;
+  }
+  if (p->n_blocked > 0) {
+    SPD_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    SPD_CUDA(cudaEventCreateWithFlags(&p->ev_u1, cudaEventDisableTiming));
+    SPD_CUDA(cudaEventCreateWithFlags(&p->ev_panel, cudaEventDisableTiming));
   }
   static bool attrs = false;
   if (!attrs) {
@@ -565,23 +585,45 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
     damp_unpack_kernel<<<p->n_tiles, 256, 0, s>>>(p->mats, p->tiles, gamma);
     SPD_CHECK_LAUNCH();
     stat_end(kCatInvUnpackFinal, s, 0, 0);
-    for (int k = 0; k < p->steps; ++k) {
+    // step k's pivot -> stage -> panel GEMM on stream q (the critical chain)
+    auto front = [&](int k, cudaStream_t q) -> int {
       const int na = p->act_cnt[k];
-      stat_begin(kCatInvPivot, s);
-      pivot_kernel<<<na, 512, 0, s>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
+      float* pa = p->panA + (k & 1) * 2 * plane;
+      stat_begin(kCatInvPivot, q);
+      pivot_kernel<<<na, 512, 0, q>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
                                       int64_t(p->n_blocked) * kB * kB);
       SPD_CHECK_LAUNCH();
-      stat_end(kCatInvPivot, s, 2.0 * kB * kB * kB * na, 0);
-      stat_begin(kCatInvPanel, s);
-      stage_panel_kernel<<<p->pan_cnt[k], 256, 0, s>>>(p->mats, p->pan_jobs + p->pj_off[k], k, p->panA, plane);
+      stat_end(kCatInvPivot, q, 2.0 * kB * kB * kB * na, 0);
+      stat_begin(kCatInvPanel, q);
+      stage_panel_kernel<<<p->pan_cnt[k], 256, 0, q>>>(p->mats, p->pan_jobs + p->pj_off[k], k, pa, plane);
       SPD_CHECK_LAUNCH();
-      int rc = launch_tc3(Kind::TF32, p->maps, p->items + p->pan_off[k], p->epis, p->pan_cnt[k], s);
+      int rc = launch_tc3(Kind::TF32, p->maps, p->items + p->pan_off[k], p->epis, p->pan_cnt[k], q);
       if (rc) return rc;
-      stat_end(kCatInvPanel, s, 2.0 * kB * kB * kB * p->pan_cnt[k], 0);
+      stat_end(kCatInvPanel, q, 2.0 * kB * kB * kB * p->pan_cnt[k], 0);
+      return SPDKFAC_OK;
+    };
+    int rc = front(0, s);
+    if (rc) return rc;
+    for (int k = 0; k < p->steps; ++k) {
+      // U1(k): the tiles step k+1 reads; then step k+1's front runs on the side stream
+      // while U2(k) (the rest of the trailing update) runs here (look-ahead)
+      const int u1 = p->u1_cnt[k], u2 = p->upd_cnt[k] - u1;
       stat_begin(kCatInvUpdate, s);
-      rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k], p->epis, p->upd_cnt[k], s);
+      rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k], p->epis, u1, s);
       if (rc) return rc;
-      stat_end(kCatInvUpdate, s, 2.0 * kB * kB * kB * p->upd_cnt[k], 0);
+      stat_end(kCatInvUpdate, s, 2.0 * kB * kB * kB * u1, 0);
+      const bool ahead = k + 1 < p->steps;
+      if (ahead) {
+        SPD_CUDA(cudaEventRecord(p->ev_u1, s));
+        SPD_CUDA(cudaStreamWaitEvent(p->side, p->ev_u1, 0));
+        if ((rc = front(k + 1, p->side))) return rc;
+        SPD_CUDA(cudaEventRecord(p->ev_panel, p->side));
+      }
+      stat_begin(kCatInvUpdate, s);
+      rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k] + u1, p->epis, u2, s);
+      if (rc) return rc;
+      stat_end(kCatInvUpdate, s, 2.0 * kB * kB * kB * u2, 0);
+      if (ahead) SPD_CUDA(cudaStreamWaitEvent(s, p->ev_panel, 0));
     }
     stat_begin(kCatInvUnpackFinal, s);
     finalize_kernel<<<p->n_tiles, 256, 0, s>>>(p->mats, p->tiles);
@@ -591,6 +633,12 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
   return SPDKFAC_OK;
 }
 
-void spdkfac_inverse_plan_destroy(spdkfac_inverse_plan* p) { delete p; }
+void spdkfac_inverse_plan_destroy(spdkfac_inverse_plan* p) {
+  if (!p) return;
+  if (p->ev_u1) cudaEventDestroy(p->ev_u1);
+  if (p->ev_panel) cudaEventDestroy(p->ev_panel);
+  if (p->side) cudaStreamDestroy(p->side);
+  delete p;
+}
 
 }  // extern "C"

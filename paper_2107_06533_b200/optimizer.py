@@ -172,6 +172,7 @@ class SPDKFAC(torch.optim.Optimizer):
         self._info_events = []
         self._a_count = 0
         self._a_inverted = False
+        self.timeline = None  # set to {} to record per-phase CUDA events (eager diagnostics)
         self._precond_key = None
         self.steps = 0
         self._capture = True
@@ -281,6 +282,8 @@ class SPDKFAC(torch.optim.Optimizer):
         fs = self.factor_stream
         # samples of a batch-mean loss: the image batch for convs, the rows for linears
         nb = x.shape[0] if l.is_conv else x.numel() // x.shape[-1]
+        if kind == "A" and self._a_count == 0:
+            self._tl("fwd_start", torch.cuda.current_stream(self.device))
         layout, x = self._prepare(l, x.detach(), kind)
         plan = self._plan_for(l, layout, x, kind)
         ev_done, ev_staged = l.events[kind]
@@ -310,6 +313,22 @@ class SPDKFAC(torch.optim.Optimizer):
             if self._a_count == len(self.layers):
                 self._launch_inverse_A()
 
+    def _tl(self, name: str, stream) -> None:
+        if self.timeline is not None and not torch.cuda.is_current_stream_capturing():
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+            self.timeline[name] = ev
+
+    def timeline_ms(self) -> dict:
+        """Milliseconds of each recorded phase event relative to 'fwd_start' (synchronises)."""
+        tl = self.timeline or {}
+        if "fwd_start" not in tl:
+            return {}
+        tl["fwd_start"].synchronize()
+        for ev in tl.values():
+            ev.synchronize()
+        return {k: round(tl["fwd_start"].elapsed_time(v), 3) for k, v in tl.items()}
+
     def _inverting(self) -> bool:
         return self.steps % self.inv_update_freq == 0
 
@@ -323,7 +342,9 @@ class SPDKFAC(torch.optim.Optimizer):
         s.wait_stream(self.factor_stream)
         if self.world > 1:
             s.wait_stream(self.comm_stream)
+        self._tl("a_factors_done", s)
         self._run_inverse("A", s)
+        self._tl("a_inverse_done", s)
         self._a_inverted = True
 
     def _run_inverse(self, side: str, stream) -> None:
@@ -377,9 +398,11 @@ class SPDKFAC(torch.optim.Optimizer):
         lr = self.param_groups[0]["lr"]
         factors_now = self._capture
         invert_now = self.steps % self.inv_update_freq == 0
+        self._tl("backward_done", main)
         if factors_now:
             main.wait_stream(self.factor_stream)
             self._factor_updates += 1
+            self._tl("g_factors_done", main)
         if self.world > 1:
             cs = self.comm_stream
             cs.wait_stream(main)
@@ -392,7 +415,9 @@ class SPDKFAC(torch.optim.Optimizer):
             if not self._a_inverted:  # hooks did not see a full forward (e.g. factors reused)
                 self._launch_inverse_A()
             self._run_inverse("G", main)
+            self._tl("g_inverse_done", main)
             main.wait_stream(self.inv_stream)  # A inverses (and their broadcasts) landed
+            self._tl("inverses_joined", main)
         # precondition + update for every K-FAC layer (mean gradient = sum / P); the pointer
         # tables are rebuilt only when a gradient's storage changes (zero_grad(set_to_none=True))
         key = tuple(l.module.weight.grad.data_ptr() if l.module.weight.grad is not None else 0 for l in self.layers)
@@ -409,6 +434,7 @@ class SPDKFAC(torch.optim.Optimizer):
                                weights=[self._weight_matrix(l, l.module.weight.data) for l in self.layers])
             self._precond_key = key
         self._precond.run_bound(lr / self.world, stream=main)
+        self._tl("precond_done", main)
         others = [p for p in self.other_params if p.grad is not None]
         if others:
             torch._foreach_add_([p.data for p in others], [p.grad for p in others], alpha=-lr / self.world)

@@ -70,3 +70,57 @@ if what in ("factor", "all"):
         packed = torch.empty(plan.packed_size, device=dev)
         timed(lambda: plan.run(x, packed), "factor " + label)
     report(4 * (reps + 1))
+
+if what == "stage":
+    # per-layer staging + SYRK time for every distinct ResNet-50 conv/fc shape (channels-last)
+    import torch.nn as nn
+    from paper_2107_06533_b200.workloads import build_model
+    model = build_model("resnet50").to(dev).to(memory_format=torch.channels_last)
+    geo = []
+
+    def hook(m, inp, out):
+        geo.append((m, tuple(inp[0].shape), tuple(out.shape)))
+    hs = [m.register_forward_hook(hook) for m in model.modules() if isinstance(m, (nn.Conv2d, nn.Linear))]
+    with torch.no_grad():
+        model(torch.randn(32, 3, 224, 224, device=dev).contiguous(memory_format=torch.channels_last))
+    for h in hs:
+        h.remove()
+    seen = {}
+    tot = {"A_stage": 0.0, "A_syrk": 0.0, "G_stage": 0.0, "G_syrk": 0.0}
+    for m, ishape, oshape in geo:
+        for side in ("A", "G"):
+            if isinstance(m, nn.Linear):
+                key = (side, "fc")
+                shp = ishape if side == "A" else oshape
+                plan = FactorPlan(L.ROWS, shp)
+                x = torch.randn(shp, device=dev)
+            elif side == "A":
+                key = ("A",) + ishape + tuple(m.kernel_size) + tuple(m.stride)
+                plan = FactorPlan(L.CONV_A_NHWC, ishape, m.kernel_size, m.stride, m.padding, m.dilation)
+                x = torch.randn(ishape, device=dev).contiguous(memory_format=torch.channels_last)
+            else:
+                key = ("G",) + oshape
+                plan = FactorPlan(L.SPATIAL_NHWC, oshape)
+                x = torch.randn(oshape, device=dev).contiguous(memory_format=torch.channels_last)
+            if key not in seen:
+                packed = torch.empty(plan.packed_size, device=dev)
+                for _ in range(2):
+                    plan.run(x, packed)
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                e[0].record()
+                for _ in range(5):
+                    plan.stage(x)
+                e[1].record()
+                for _ in range(5):
+                    plan.compute(packed, 1.0 / plan.rows)
+                e[2].record()
+                torch.cuda.synchronize()
+                seen[key] = (e[0].elapsed_time(e[1]) / 5, e[1].elapsed_time(e[2]) / 5, plan.rows, plan.dim)
+            st, sy, rows, dim = seen[key]
+            tot[side + "_stage"] += st
+            tot[side + "_syrk"] += sy
+    for key, (st, sy, rows, dim) in seen.items():
+        gbs = rows * dim * 4 / (st * 1e-3) / 1e9
+        tf = rows * dim * (dim + 1) / (sy * 1e-3) / 1e12
+        print(f"{str(key):60s} M={rows:7d} d={dim:5d} stage {st*1e3:8.1f} us ({gbs:6.0f} GB/s written)  syrk {sy*1e3:8.1f} us ({tf:6.1f} TF/s)")
+    print({k: round(v, 3) for k, v in tot.items()}, "ms per step (sum over layers)")
