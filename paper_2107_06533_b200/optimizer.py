@@ -103,6 +103,13 @@ class SPDKFAC(torch.optim.Optimizer):
             from .comm import NcclComm
             comm = NcclComm(self.rank, self.world)
         self.comm = comm
+        # inverse broadcasts get their own communicator and stream: NCCL orders collectives per
+        # communicator, so all-reduces of later fusion groups never queue behind a broadcast that
+        # is waiting for an inversion (and the per-communicator order is identical on all ranks)
+        self.comm_bc = None
+        if self.world > 1:
+            from .comm import NcclComm
+            self.comm_bc = NcclComm(self.rank, self.world) if isinstance(comm, NcclComm) else comm
 
         # ---- preconditioned layers, forward order (model definition order)
         self.layers: list[_Layer] = []
@@ -148,27 +155,41 @@ class SPDKFAC(torch.optim.Optimizer):
         self._groups_bwd = S.fusion_slices(self.bwd_plan, g_off, g_dims)
         S.check_fusion_cover(self._groups_fwd, size_a)
         S.check_fusion_cover(self._groups_bwd, size_g)
+        # group id per layer and member counts; slices keyed by group id
+        self._gid = {"A": S.fusion_members(self.fwd_plan)[0], "G": S.fusion_members(self.bwd_plan)[0]}
+        self._gsize = {"A": S.fusion_members(self.fwd_plan)[1], "G": S.fusion_members(self.bwd_plan)[1]}
+        self._gslice = {"A": [self._groups_fwd[g[-1].layer_index - 1] for g in self.fwd_plan.groups],
+                        "G": [self._groups_bwd[g[-1].layer_index - 1] for g in self.bwd_plan.groups]}
+        self._gseen = {"A": [0] * len(self.fwd_plan.groups), "G": [0] * len(self.bwd_plan.groups)}
 
         # ---- inverses (every rank holds all of them for preconditioning)
         self.inv = []
         for l in self.layers:
             self.inv.append(torch.zeros(l.spec.a_dim, l.spec.a_dim, dtype=torch.float32, device=self.device))
             self.inv.append(torch.zeros(l.spec.g_dim, l.spec.g_dim, dtype=torch.float32, device=self.device))
-        # this rank's inversions, split by side: A inverses only need the forward pass's
-        # factors, so they run on their own stream concurrently with the backward pass
+        # this rank's inversions in three groups, each launched as soon as its factors exist
+        # (schedule.inversion_groups): A after the forward pass (own stream, overlaps the
+        # backward pass), G1 (the layers backward reaches first, most of the G work) mid-backward
+        # on a second stream, G2 in step()
         mine = list(self.placement.workers[self.rank])
         self._mine = mine
-        self._inv_plans, self._info_host = {}, {}
-        for side, par in (("A", 0), ("G", 1)):
-            ts = [t for t in mine if t % 2 == par]
+        grp = S.inversion_groups([l.spec.a_dim for l in self.layers], [l.spec.g_dim for l in self.layers])
+        self._n_g1 = grp["n_g1"]
+        self._inv_plans, self._info_host, self._bcast = {}, {}, {}
+        for side in ("A", "G1", "G2"):
+            ts = [t for t in mine if t in grp[side]]
             self._inv_plans[side] = InversePlan([self._packed(t) for t in ts], [self.inv[t] for t in ts]) if ts else None
             self._info_host[side] = torch.zeros(len(ts), dtype=torch.int32, pin_memory=True) if ts else None
-        self._bcast = {side: self._bcast_layout(par) for side, par in (("A", 0), ("G", 1))}
+            self._bcast[side] = self._bcast_layout(grp[side])
         self._precond = PrecondPlan([(l.spec.g_dim, l.spec.a_dim) for l in self.layers], device=self.device)
 
         self.factor_stream = torch.cuda.Stream(self.device)
         self.inv_stream = torch.cuda.Stream(self.device)
+        self.inv_stream2 = torch.cuda.Stream(self.device)
+        self._g_count = 0
+        self._g1_inverted = False
         self.comm_stream = torch.cuda.Stream(self.device) if self.world > 1 else None
+        self.bcast_stream = torch.cuda.Stream(self.device) if self.world > 1 else None
         self._info_events = []
         self._a_count = 0
         self._a_inverted = False
@@ -195,12 +216,12 @@ class SPDKFAC(torch.optim.Optimizer):
         d = l.spec.g_dim
         return self.bufG[l.g_off:l.g_off + d * (d + 1) // 2]
 
-    def _bcast_layout(self, parity: int):
-        """Per owner rank: its CT tensors of one side (placement order) and packed staging views."""
+    def _bcast_layout(self, members):
+        """Per owner rank: its CT tensors of one group (placement order) and packed staging views."""
         if self.world == 1:
             return None
         lay = []
-        for ct, dims, offs, n in S.bcast_layout(self.placement, [t.shape[0] for t in self.inv], parity):
+        for ct, dims, offs, n in S.bcast_layout(self.placement, [t.shape[0] for t in self.inv], members=members):
             buf = torch.empty(max(n, 1), dtype=torch.float32, device=self.device)
             views = [buf[o:o + S.packed_size(d)] for o, d in zip(offs, dims)]
             lay.append((ct, dims, buf, views, n))
@@ -302,16 +323,22 @@ class SPDKFAC(torch.optim.Optimizer):
         plan.compute(buf[off:off + d * (d + 1) // 2], scale, decay, 1.0 / self.world, fs)
         ev_done.record(fs)
         l.pending[kind] = not capturing
-        groups = self._groups_fwd if kind == "A" else self._groups_bwd
-        if self.world > 1 and l.index in groups:
-            s, e = groups[l.index]
-            cs = self.comm_stream
-            cs.wait_stream(fs)
-            self.comm.allreduce_sum(buf[s:e], cs)
+        if self.world > 1:
+            gid = self._gid[kind][l.index]
+            self._gseen[kind][gid] += 1
+            if self._gseen[kind][gid] == self._gsize[kind][gid]:  # every member of the group written
+                s, e = self._gslice[kind][gid]
+                cs = self.comm_stream
+                cs.wait_stream(fs)
+                self.comm.allreduce_sum(buf[s:e], cs)
         if kind == "A":
             self._a_count += 1
             if self._a_count == len(self.layers):
                 self._launch_inverse_A()
+        elif l.index >= len(self.layers) - self._n_g1:  # a G1 member
+            self._g_count += 1
+            if self._g_count == self._n_g1:
+                self._launch_inverse_G1()
 
     def _tl(self, name: str, stream) -> None:
         if self.timeline is not None and not torch.cuda.is_current_stream_capturing():
@@ -346,6 +373,19 @@ class SPDKFAC(torch.optim.Optimizer):
         self._run_inverse("A", s)
         self._tl("a_inverse_done", s)
         self._a_inverted = True
+
+    def _launch_inverse_G1(self):
+        """The G factors of the layers backward reached first are enqueued: invert them on the
+        second inverse stream while the rest of the backward pass runs."""
+        if self._g1_inverted or not self._inverting():
+            return
+        s = self.inv_stream2
+        s.wait_stream(self.factor_stream)
+        if self.world > 1:
+            s.wait_stream(self.comm_stream)
+        self._run_inverse("G1", s)
+        self._tl("g1_inverse_done", s)
+        self._g1_inverted = True
 
     def _run_inverse(self, side: str, stream) -> None:
         plan = self._inv_plans[side]
@@ -414,9 +454,12 @@ class SPDKFAC(torch.optim.Optimizer):
         if invert_now:
             if not self._a_inverted:  # hooks did not see a full forward (e.g. factors reused)
                 self._launch_inverse_A()
-            self._run_inverse("G", main)
+            if not self._g1_inverted:
+                self._launch_inverse_G1()
+            self._run_inverse("G2", main)
             self._tl("g_inverse_done", main)
-            main.wait_stream(self.inv_stream)  # A inverses (and their broadcasts) landed
+            main.wait_stream(self.inv_stream)   # A inverses (and their broadcasts) landed
+            main.wait_stream(self.inv_stream2)  # G1 likewise
             self._tl("inverses_joined", main)
         # precondition + update for every K-FAC layer (mean gradient = sum / P); the pointer
         # tables are rebuilt only when a gradient's storage changes (zero_grad(set_to_none=True))
@@ -440,6 +483,11 @@ class SPDKFAC(torch.optim.Optimizer):
             torch._foreach_add_([p.data for p in others], [p.grad for p in others], alpha=-lr / self.world)
         self._a_count = 0
         self._a_inverted = False
+        self._g_count = 0
+        self._g1_inverted = False
+        if self.world > 1:
+            for k in ("A", "G"):
+                self._gseen[k] = [0] * len(self._gseen[k])
         if not capturing:  # a captured step is counted per replay (_after_replay)
             self.steps += 1
             self._capture = self.steps % self.factor_update_freq == 0
@@ -449,7 +497,7 @@ class SPDKFAC(torch.optim.Optimizer):
         """Bookkeeping for one replay of a captured step (GraphedStep): the Python side
         effects of step() ran once at capture time."""
         self.steps += 1
-        for side in ("A", "G"):
+        for side in ("A", "G1", "G2"):
             if self._inv_plans[side] is not None:
                 ev = torch.cuda.Event()
                 ev.record(stream)
@@ -466,13 +514,13 @@ class SPDKFAC(torch.optim.Optimizer):
                                                        L.ptr_array([self.inv[t].data_ptr() for t in ct]),
                                                        L.ptr_array([v.data_ptr() for v in views]),
                                                        main.cuda_stream), "pack inverses")
-        cs = self.comm_stream
-        cs.wait_stream(main)
-        with self.comm.group():
+        bs = self.bcast_stream
+        bs.wait_stream(main)
+        with self.comm_bc.group():
             for root, (ct_r, _, buf_r, _, n_r) in enumerate(lay):
                 if n_r:
-                    self.comm.bcast(buf_r[:n_r], root, cs)
-        main.wait_stream(cs)
+                    self.comm_bc.bcast(buf_r[:n_r], root, bs)
+        main.wait_stream(bs)
         for root, (ct_r, dims_r, _, views_r, n_r) in enumerate(lay):
             if root == self.rank or not ct_r:
                 continue

@@ -48,6 +48,17 @@ def fusion_slices(plan: FusionPlan, offsets: Sequence[int], dims: Sequence[int])
     return out
 
 
+def fusion_members(plan: FusionPlan) -> tuple:
+    """(group id of every 0-based layer, member count of every group) for one pass: a group's
+    all-reduce is issued once all its members are written, whatever order the hooks fire in."""
+    gid, sizes = {}, []
+    for k, group in enumerate(plan.groups):
+        for t in group:
+            gid[t.layer_index - 1] = k
+        sizes.append(len(group))
+    return gid, sizes
+
+
 def check_fusion_cover(slices: dict, total: int) -> None:
     """The groups of one pass tile its fusion buffer exactly once (no gap, no overlap)."""
     spans = sorted(slices.values())
@@ -60,18 +71,40 @@ def check_fusion_cover(slices: dict, total: int) -> None:
         raise ValueError(f"fusion slices cover {pos} of {total} elements")
 
 
-def bcast_layout(placement: PlacementPlan, dims: Sequence[int], parity: int | None = None) -> list:
+def bcast_layout(placement: PlacementPlan, dims: Sequence[int], parity: int | None = None,
+                 members=None) -> list:
     """Per owner rank p: (ct tensor indices in p's placement order, their dims, offsets, total).
-    `parity` 0/1 restricts to A/G tensors (tensor_index = 2l / 2l+1, simulator.py:276-282)."""
+    `parity` 0/1 restricts to A/G tensors (tensor_index = 2l / 2l+1, simulator.py:276-282);
+    `members` (a set) restricts to one inversion group."""
     out = []
     for lst in placement.workers:
-        ct = [t for t in lst if t not in placement.nct and (parity is None or t % 2 == parity)]
+        ct = [t for t in lst if t not in placement.nct and (parity is None or t % 2 == parity)
+              and (members is None or t in members)]
         offs, o = [], 0
         for t in ct:
             offs.append(o)
             o += packed_size(dims[t])
         out.append((ct, [dims[t] for t in ct], offs, o))
     return out
+
+
+def inversion_groups(a_dims: Sequence[int], g_dims: Sequence[int], early_fraction: float = 0.85) -> dict:
+    """Tensor sets inverted as soon as their factors exist:
+      "A"  every input-side factor (complete after the forward pass)
+      "G1" output-side factors of the layers the backward pass reaches first, up to
+           `early_fraction` of the output-side inversion work (sum d^3)
+      "G2" the remaining output-side factors (inverted in step()).
+    Returns {"A": set, "G1": set, "G2": set, "n_g1": number of layers in G1}."""
+    nl = len(g_dims)
+    total = sum(float(d) ** 3 for d in g_dims)
+    acc, n_g1 = 0.0, 0
+    for l in reversed(range(nl)):
+        if n_g1 >= nl - 1 or (total and acc >= early_fraction * total):
+            break
+        acc += float(g_dims[l]) ** 3
+        n_g1 += 1
+    g1 = {2 * l + 1 for l in range(nl - n_g1, nl)}
+    return {"A": {2 * l for l in range(nl)}, "G1": g1, "G2": {2 * l + 1 for l in range(nl)} - g1, "n_g1": n_g1}
 
 
 def kind_of(tensor_index: int) -> FactorKind:

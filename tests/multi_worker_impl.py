@@ -69,6 +69,8 @@ def main():
                           "placement": mode, "nct": sorted(opt.placement.nct),
                           "workers": [list(w) for w in opt.placement.workers]}), flush=True)
     opt.comm.close()
+    if opt.comm_bc is not None and opt.comm_bc is not opt.comm:
+        opt.comm_bc.close()
     dist.destroy_process_group()
 
 
