@@ -40,87 +40,127 @@ struct TileJob {  // one 32 x 32 tile (I <= J) of a blocked matrix, for unpack/f
 
 // Register-resident sweep of one 128 x 128 block by 512 threads: thread t owns row
 // i = t & 127, columns [32q, 32q + 32), q = t >> 7 (warp-uniform), in registers.
-// Blocked form used by the kernels: pivots are swept four at a time.  The owners of the four
-// pivot rows publish them column-interleaved (R[j] = (a_K0j, a_K0+1,j, a_K0+2,j, a_K0+3,j));
-// every thread sweeps the 4x4 pivot block S = -P4^-1 in registers (its four scalar pivots are
-// the same Schur pivots as the scalar sweep, so the failing index is exact) and applies the
-// rank-4 update  a_ij <- alpha_i a_ij - sum_t w_i[t] R[j].t  with
-//   i not in K: alpha = 1, w_i = A[i,K] P4^-1           (A[i,K] = R[i] by symmetry)
-//   i in K    : alpha = 0, w_i = S[i - K0, :]            (new pivot rows P4^-1 A[K,j])
-// followed by the column fix-up A[i,K] <- w_i (i not in K), A[K,K] <- S.
-// n <= 128; rows/columns >= n are identity padding.  Returns -1 or the failing pivot.
-__device__ __forceinline__ int sweep128_b4(float (&a)[32], int n, float4* rbuf /* 2 x 128 */) {
-  const int t = threadIdx.x, i = t & 127, q = t >> 7;
-  const int nb = (n + 3) >> 2;
+// 8-pivot block sweep used by the kernels: thread t owns rows 2r, 2r+1
+// (r = t & 63) x columns [16q, 16q + 16) (q = t >> 6, warp-uniform), so every pivot-row
+// vector R[j] read from shared memory serves two rows.  Warp 0 sweeps the 8x8 pivot block
+// (shuffles) once; warps 0-3 then form the row weights w_i once per row (not once per column
+// quarter) and publish them, so the update costs 2 x LDS.128 + 8 FFMA per element pair.
+struct B8v2Shared {
+  float4 R[2][128][2];  // pivot rows K0..K0+7 of column j (double-buffered)
+  float4 W[2][128][2];  // row weights w_i
+  float S[8][8];
+  int fail[2];
+};
+
+__device__ __forceinline__ int sweep128_b8v2(float (&a)[2][16], int n, B8v2Shared& sh) {
+  const int t = threadIdx.x, r = t & 63, q = t >> 6;
+  const int lane = t & 31, warp = t >> 5;
+  const int nb = (n + 7) >> 3;
   for (int kb = 0; kb < nb; ++kb) {
-    float4* R = rbuf + (kb & 1) * 128;
-    const int K0 = kb * 4;
-    const int s0 = i - K0;  // pivot-row index of this thread's row, if 0..3
-    if (s0 >= 0 && s0 < 4) {
-      float* Rf = reinterpret_cast<float*>(R);
+    const int buf = kb & 1;
+    float* Rf = reinterpret_cast<float*>(sh.R[buf]);
+    const int K0 = kb * 8;
 #pragma unroll
-      for (int jj = 0; jj < 32; ++jj) Rf[(q * 32 + jj) * 4 + s0] = a[jj];
+    for (int u = 0; u < 2; ++u) {
+      const int s0 = 2 * r + u - K0;
+      if (s0 >= 0 && s0 < 8) {
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) Rf[(q * 16 + jj) * 8 + s0] = a[u][jj];
+      }
     }
     __syncthreads();
-    // 4x4 pivot block, swept in registers (identical in every thread)
-    float S[4][4];
+    if (warp < 4) {
+      if (warp == 0) {  // lane holds S[rr][c] and S[rr][c + 4]
+        const int rr = lane >> 2, c = lane & 3;
+        float v0 = Rf[(K0 + c) * 8 + rr], v1 = Rf[(K0 + c + 4) * 8 + rr];
+        int fail = -1;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const float4 v = R[K0 + c];
-      S[0][c] = v.x, S[1][c] = v.y, S[2][c] = v.z, S[3][c] = v.w;
-    }
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const float piv = S[p][p];
-      if (!(piv > 0.f)) return K0 + p;  // dpotrf's test on the same Schur pivot (uniform)
-      const float pinv = __frcp_rn(piv);
-      float rowp[4], colp[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) rowp[c] = S[p][c], colp[c] = S[c][p];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (r == p && c == p) S[r][c] = -pinv;
-          else if (r == p) S[r][c] = rowp[c] * pinv;
-          else if (c == p) S[r][c] = colp[r] * pinv;
-          else S[r][c] = fmaf(-colp[r] * pinv, rowp[c], S[r][c]);
+        for (int p = 0; p < 8; ++p) {
+          const float pv = __shfl_sync(0xffffffffu, (p < 4) ? v0 : v1, (p << 2) | (p & 3));
+          if (!(pv > 0.f)) {
+            fail = p;
+            break;
+          }
+          const float pinv = __frcp_rn(pv);
+          const float rp0 = __shfl_sync(0xffffffffu, v0, (p << 2) | c);
+          const float rp1 = __shfl_sync(0xffffffffu, v1, (p << 2) | c);
+          const float cp = __shfl_sync(0xffffffffu, (p < 4) ? v0 : v1, (rr << 2) | (p & 3));
+          float n0, n1;
+          if (rr == p) {
+            n0 = (c == p) ? -pinv : rp0 * pinv;
+            n1 = (c + 4 == p) ? -pinv : rp1 * pinv;
+          } else {
+            n0 = (c == p) ? cp * pinv : fmaf(-cp * pinv, rp0, v0);
+            n1 = (c + 4 == p) ? cp * pinv : fmaf(-cp * pinv, rp1, v1);
+          }
+          v0 = n0, v1 = n1;
         }
-    }
-    // weights of this thread's row
-    const bool in_k = (s0 >= 0 && s0 < 4);
-    float w[4];
-    const float4 ri = R[i];
-    const float rv[4] = {ri.x, ri.y, ri.z, ri.w};
+        sh.S[rr][c] = v0;
+        sh.S[rr][c + 4] = v1;
+        if (lane == 0) sh.fail[buf] = fail;
+      }
+      named_bar_sync(1, 128);
+      const int i = t;  // row weights for row i = t (128 threads)
+      const int s0 = i - K0;
+      float w[8];
+      if (s0 >= 0 && s0 < 8) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      // ci[c] = sum_s A[i][K0+s] P4^-1[s][c] = -sum_s rv[s] S[s][c]
-      float ci = -(rv[0] * S[0][c] + rv[1] * S[1][c] + rv[2] * S[2][c] + rv[3] * S[3][c]);
-      float sr = S[0][c];
-      if (s0 == 1) sr = S[1][c];
-      if (s0 == 2) sr = S[2][c];
-      if (s0 == 3) sr = S[3][c];
-      w[c] = in_k ? sr : ci;
-    }
-    const float alpha = in_k ? 0.f : 1.f;
+        for (int cc = 0; cc < 8; ++cc) w[cc] = sh.S[s0][cc];
+      } else {
+        const float4 ra = sh.R[buf][i][0], rb = sh.R[buf][i][1];
+        const float rv[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
 #pragma unroll
-    for (int jj = 0; jj < 32; ++jj) {
-      const float4 rj = R[q * 32 + jj];
-      float v = alpha * a[jj];
-      v = fmaf(-w[0], rj.x, v);
-      v = fmaf(-w[1], rj.y, v);
-      v = fmaf(-w[2], rj.z, v);
-      v = fmaf(-w[3], rj.w, v);
-      a[jj] = v;
+        for (int cc = 0; cc < 8; ++cc) {
+          float acc = 0.f;
+#pragma unroll
+          for (int ss = 0; ss < 8; ++ss) acc = fmaf(rv[ss], sh.S[ss][cc], acc);
+          w[cc] = -acc;
+        }
+      }
+      sh.W[buf][i][0] = make_float4(w[0], w[1], w[2], w[3]);
+      sh.W[buf][i][1] = make_float4(w[4], w[5], w[6], w[7]);
     }
-    if (q == (K0 >> 5)) {  // warp-uniform: fix the four pivot columns of this quarter
-      switch ((K0 & 31) >> 2) {
-#define SPD_FIX(C)                                       \
-  case C:                                                \
-    a[4 * C + 0] = w[0], a[4 * C + 1] = w[1], a[4 * C + 2] = w[2], a[4 * C + 3] = w[3]; \
-    break;
-        SPD_FIX(0) SPD_FIX(1) SPD_FIX(2) SPD_FIX(3) SPD_FIX(4) SPD_FIX(5) SPD_FIX(6) SPD_FIX(7)
-#undef SPD_FIX
+    __syncthreads();
+    const int f = sh.fail[buf];
+    if (f >= 0) return K0 + f;
+    float w[2][8];
+    bool pk[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = 2 * r + u;
+      const float4 wa = sh.W[buf][i][0], wb = sh.W[buf][i][1];
+      w[u][0] = wa.x, w[u][1] = wa.y, w[u][2] = wa.z, w[u][3] = wa.w;
+      w[u][4] = wb.x, w[u][5] = wb.y, w[u][6] = wb.z, w[u][7] = wb.w;
+      pk[u] = (i >= K0 && i < K0 + 8);
+    }
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      const float4 ra = sh.R[buf][q * 16 + jj][0], rb = sh.R[buf][q * 16 + jj][1];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        float v = pk[u] ? 0.f : a[u][jj];
+        v = fmaf(-w[u][0], ra.x, v);
+        v = fmaf(-w[u][1], ra.y, v);
+        v = fmaf(-w[u][2], ra.z, v);
+        v = fmaf(-w[u][3], ra.w, v);
+        v = fmaf(-w[u][4], rb.x, v);
+        v = fmaf(-w[u][5], rb.y, v);
+        v = fmaf(-w[u][6], rb.z, v);
+        v = fmaf(-w[u][7], rb.w, v);
+        a[u][jj] = v;
+      }
+    }
+    if (q == (K0 >> 4)) {  // warp-uniform: the eight pivot columns of this column group
+      if ((K0 & 15) == 0) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) a[u][cc] = w[u][cc];
+      } else {
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) a[u][8 + cc] = w[u][cc];
       }
     }
   }
@@ -135,17 +175,21 @@ __device__ __forceinline__ float packed_at(const float* p, int64_t d, int64_t i,
 // ---------------------------------------------------------------- d <= 128
 __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __restrict__ mats,
                                                             const int32_t* __restrict__ ids, float gamma) {
-  __shared__ float4 rbuf[2 * 128];
+  __shared__ B8v2Shared sh;
   const InvMat m = mats[ids[blockIdx.x]];
   const int n = m.d;
-  const int i = threadIdx.x & 127, q = threadIdx.x >> 7;
-  float a[32];
+  const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
+  float a[2][16];
 #pragma unroll
-  for (int jj = 0; jj < 32; ++jj) {
-    const int j = q * 32 + jj;
-    a[jj] = (i < n && j < n) ? packed_at(m.in, n, i, j) + (i == j ? gamma : 0.f) : (i == j ? 1.f : 0.f);
+  for (int u = 0; u < 2; ++u) {
+    const int i = 2 * r + u;
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      const int j = q * 16 + jj;
+      a[u][jj] = (i < n && j < n) ? packed_at(m.in, n, i, j) + (i == j ? gamma : 0.f) : (i == j ? 1.f : 0.f);
+    }
   }
-  const int f = sweep128_b4(a, n, rbuf);
+  const int f = sweep128_b8v2(a, n, sh);
   if (f >= 0) {
     if (threadIdx.x == 0) *m.info = f + 1;
     return;
@@ -154,11 +198,13 @@ __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __rest
   // out = -(S + S^T)/2 through shared memory (uniform control flow)
   extern __shared__ float sm[];
 #pragma unroll
-  for (int jj = 0; jj < 32; ++jj) sm[i * kSmemLd + q * 32 + jj] = -a[jj];
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) sm[(2 * r + u) * kSmemLd + q * 16 + jj] = -a[u][jj];
   __syncthreads();
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int r = e / n, c = e - r * n;
-    m.out[e] = 0.5f * (sm[r * kSmemLd + c] + sm[c * kSmemLd + r]);
+    const int rr = e / n, c = e - rr * n;
+    m.out[e] = 0.5f * (sm[rr * kSmemLd + c] + sm[c * kSmemLd + rr]);
   }
 }
 
@@ -197,33 +243,40 @@ __global__ void __launch_bounds__(256) damp_unpack_kernel(const InvMat* __restri
 __global__ void __launch_bounds__(512) pivot_kernel(const InvMat* __restrict__ mats,
                                                     const int32_t* __restrict__ ids, int k,
                                                     float* __restrict__ pinv_planes, int64_t pinv_plane) {
-  __shared__ float4 rbuf[2 * 128];
+  __shared__ B8v2Shared sh;
   const InvMat m = mats[ids[blockIdx.x]];
   if (*m.info != 0) return;
   const int64_t dp = m.dp, K0 = int64_t(k) * kB;
-  const int i = threadIdx.x & 127, q = threadIdx.x >> 7;
-  float a[32];
-  const float* src = m.W + (K0 + i) * dp + K0 + q * 32;
+  const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
+  float a[2][16];
 #pragma unroll
-  for (int jj = 0; jj < 32; jj += 4) {
-    const float4 v = *reinterpret_cast<const float4*>(src + jj);
-    a[jj] = v.x, a[jj + 1] = v.y, a[jj + 2] = v.z, a[jj + 3] = v.w;
+  for (int u = 0; u < 2; ++u) {
+    const float* src = m.W + (K0 + 2 * r + u) * dp + K0 + q * 16;
+#pragma unroll
+    for (int jj = 0; jj < 16; jj += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(src + jj);
+      a[u][jj] = v.x, a[u][jj + 1] = v.y, a[u][jj + 2] = v.z, a[u][jj + 3] = v.w;
+    }
   }
-  const int f = sweep128_b4(a, kB, rbuf);
+  const int f = sweep128_b8v2(a, kB, sh);
   if (f >= 0) {
     if (threadIdx.x == 0) *m.info = int(K0) + f + 1;
     return;
   }
-  float* dst = m.W + (K0 + i) * dp + K0 + q * 32;                        // W[K,K] <- -P^-1
-  float* ph = pinv_planes + (int64_t(m.slot) * kB + i) * kB + q * 32;      // P^-1 hi plane
 #pragma unroll
-  for (int jj = 0; jj < 32; jj += 4) {
-    *reinterpret_cast<float4*>(dst + jj) = make_float4(a[jj], a[jj + 1], a[jj + 2], a[jj + 3]);
-    float h[4], l[4];
+  for (int u = 0; u < 2; ++u) {
+    const int i = 2 * r + u;
+    float* dst = m.W + (K0 + i) * dp + K0 + q * 16;                           // W[K,K] <- -P^-1
+    float* ph = pinv_planes + (int64_t(m.slot) * kB + i) * kB + q * 16;        // P^-1 hi plane
 #pragma unroll
-    for (int u = 0; u < 4; ++u) split_tf32(-a[jj + u], h[u], l[u]);
-    *reinterpret_cast<float4*>(ph + jj) = make_float4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<float4*>(ph + pinv_plane + jj) = make_float4(l[0], l[1], l[2], l[3]);
+    for (int jj = 0; jj < 16; jj += 4) {
+      *reinterpret_cast<float4*>(dst + jj) = make_float4(a[u][jj], a[u][jj + 1], a[u][jj + 2], a[u][jj + 3]);
+      float h[4], l[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) split_tf32(-a[u][jj + v], h[v], l[v]);
+      *reinterpret_cast<float4*>(ph + jj) = make_float4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<float4*>(ph + pinv_plane + jj) = make_float4(l[0], l[1], l[2], l[3]);
+    }
   }
 }
 
@@ -324,6 +377,7 @@ struct spdkfac_inverse_plan {
   int steps;
   std::vector<int> act_off, act_cnt, pan_off, pan_cnt, upd_off, upd_cnt, pj_off, u1_cnt;
   cudaStream_t side = nullptr;  // look-ahead stream: pivot/stage/panel of step k+1
+  bool lookahead = true;        // SPDKFAC_NO_LOOKAHEAD=1 serialises (diagnostics)
   cudaEvent_t ev_u1 = nullptr, ev_panel = nullptr;
   int32_t* act_ids;             // device, active blocked matrices per step (concatenated)
   PanelJob* pan_jobs;           // device, (matrix, R != K) per step, same order as the panel items
@@ -555,6 +609,10 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     delete p;
     return rc;
   }
+  {
+    const char* e = getenv("SPDKFAC_NO_LOOKAHEAD");
+    p->lookahead = !(e && e[0] == '1');
+  }
   if (p->n_blocked > 0) {
     SPD_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
     SPD_CUDA(cudaEventCreateWithFlags(&p->ev_u1, cudaEventDisableTiming));
@@ -613,6 +671,14 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       if (rc) return rc;
       stat_end(kCatInvUpdate, s, 2.0 * kB * kB * kB * u1, 0);
       const bool ahead = k + 1 < p->steps;
+      if (ahead && !p->lookahead) {  // serial order: rest of the update, then the next front
+        stat_begin(kCatInvUpdate, s);
+        rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k] + u1, p->epis, u2, s);
+        if (rc) return rc;
+        stat_end(kCatInvUpdate, s, 2.0 * kB * kB * kB * u2, 0);
+        if ((rc = front(k + 1, s))) return rc;
+        continue;
+      }
       if (ahead) {
         SPD_CUDA(cudaEventRecord(p->ev_u1, s));
         SPD_CUDA(cudaStreamWaitEvent(p->side, p->ev_u1, 0));

@@ -55,6 +55,17 @@ if what in ("inverse", "all"):
     report(reps + 1)
     plan.check()
 
+if what == "inverse_single":
+    for d in (4608, 2304, 1024):
+        g = torch.Generator(device=dev).manual_seed(d)
+        b = torch.randn(d, d, device=dev, generator=g)
+        m = b @ b.T / d + 0.1 * torch.eye(d, device=dev)
+        r, c = torch.triu_indices(d, d, device=dev)
+        plan = InversePlan([m[r, c].contiguous()], [torch.empty(d, d, device=dev)])
+        L.stats_reset(timing=True)
+        timed(lambda: plan.run(0.1), f"single inverse d={d}")
+        report(reps + 1)
+
 if what in ("factor", "all"):
     L.stats_reset(timing=True)
     for label, shp, layout, k in [("A layer4 conv2 (M=1568, d=4608)", (32, 512, 7, 7), L.CONV_A, 3),
