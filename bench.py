@@ -443,6 +443,9 @@ def run_reference(a):
 
 
 if __name__ == "__main__":
+    if os.environ.get("SPD_WATCHDOG"):
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["SPD_WATCHDOG"]), exit=True)
     args = parse()
     if args.impl == "reference":
         run_reference(args)

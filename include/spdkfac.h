@@ -115,6 +115,20 @@ SPDKFAC_API int spdkfac_factor_plan_compute(spdkfac_factor_plan* p, float scale,
                                             float* packed_inout, void* stream);
 SPDKFAC_API void spdkfac_factor_plan_destroy(spdkfac_factor_plan* p);
 
+/* A factor group: n layer-sides staged independently (stage(member, x) on the stream that
+ * owns x) and reduced by ONE persistent tensor-core launch over all members' tiles
+ * (compute()).  Each member writes packed_out[k] <- world_scale*(decay*old + (1-decay)*
+ * scales[k]*X_k^T X_k).  The optimizer builds one group per fusion group of the plan
+ * (planner.py:94-121), so a group's all-reduce follows its single compute launch. */
+typedef struct spdkfac_factor_group spdkfac_factor_group;
+SPDKFAC_API size_t spdkfac_factor_group_workspace_size(int n, const spdkfac_factor_geom* geoms);
+SPDKFAC_API int spdkfac_factor_group_create(spdkfac_factor_group** out, int n, const spdkfac_factor_geom* geoms,
+                                            float* const* packed_out, const float* scales, void* ws,
+                                            size_t ws_bytes, void* stream);
+SPDKFAC_API int spdkfac_factor_group_stage(spdkfac_factor_group* g, int member, const float* x, void* stream);
+SPDKFAC_API int spdkfac_factor_group_compute(spdkfac_factor_group* g, float decay, float world_scale, void* stream);
+SPDKFAC_API void spdkfac_factor_group_destroy(spdkfac_factor_group* g);
+
 /* ------------------------------------------------------------------ packing
  * pack_upper / unpack_upper (linalg.py:181-199) on device. `ld` = row stride
  * of the full matrix.  unpack writes both triangles. */

@@ -44,6 +44,12 @@ SIGNATURES = {
     "spdkfac_factor_plan_stage": (C.c_int, [_vp, _vp, _vp]),
     "spdkfac_factor_plan_compute": (C.c_int, [_vp, _f32, _f32, _f32, _vp, _vp]),
     "spdkfac_factor_plan_destroy": (None, [_vp]),
+    "spdkfac_factor_group_workspace_size": (_sz, [C.c_int, C.POINTER(FactorGeom)]),
+    "spdkfac_factor_group_create": (C.c_int, [C.POINTER(_vp), C.c_int, C.POINTER(FactorGeom), _pp,
+                                              C.POINTER(C.c_float), _vp, _sz, _vp]),
+    "spdkfac_factor_group_stage": (C.c_int, [_vp, C.c_int, _vp, _vp]),
+    "spdkfac_factor_group_compute": (C.c_int, [_vp, _f32, _f32, _vp]),
+    "spdkfac_factor_group_destroy": (None, [_vp]),
     "spdkfac_pack_upper_f32": (C.c_int, [_vp, _i64, _i64, _vp, _vp]),
     "spdkfac_unpack_upper_f32": (C.c_int, [_vp, _i64, _vp, _i64, _vp]),
     "spdkfac_pack_upper_batched_f32": (C.c_int, [C.c_int, _pi32, _pp, _pp, _vp]),

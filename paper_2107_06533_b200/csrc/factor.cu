@@ -7,6 +7,8 @@
 //   2. tc3 GEMM      : upper-triangle 128x128 tiles (I <= J) x split-K slices, partial tiles to ws
 //   3. reduce + pack : sum split-K partials in fixed order, apply 1/M, running average, 1/P,
 //                      write the packed upper triangle (the all-reduce / fusion-buffer format)
+#include <algorithm>
+
 #include "runtime.cuh"
 
 namespace spd {
@@ -216,28 +218,44 @@ __global__ void zero_pad_kernel(__nv_bfloat16* xt, int64_t d, int64_t M, int64_t
 
 // ------------------------------------------------------------------ reduce + pack
 // partial[slot][j][i] = D_tile[i][j]; slot = tile_index(I,J) * splits + s.
-// Split-K reduction, one launch, deterministic: block (sub-block sb, upper tile, chunk c) sums
-// the 8 split-K partial tiles of its chunk (32 independent loads per thread), stores the chunk
-// sum, and the last chunk block to arrive (per tile/sub-block counter) adds the chunk sums in
-// fixed order, applies scale / running average / 1/P and writes the packed upper triangle.
+// Split-K reduction, one launch per group, deterministic: block (sub-block sb, job, chunk c)
+// sums the 8 split-K partial tiles of its chunk (32 independent loads per thread), stores the
+// chunk sum, and the last chunk block to arrive (per tile/sub-block counter) adds the chunk
+// sums in fixed order, applies scale / running average / 1/P and writes the packed upper
+// triangle.  A job is one upper tile of one group member with split K.
 constexpr int kChunk = 8;
 
-__global__ void __launch_bounds__(256) reduce_pack_kernel(const float* __restrict__ part, int64_t d, int T, int splits,
-                                                          float scale, float decay, float world_scale,
-                                                          float* __restrict__ packed, float* __restrict__ chunks,
-                                                          int* __restrict__ counters) {
+struct RedMember {
+  const float* part;
+  float* chunks;
+  int* counters;
+  float* packed;
+  int64_t d;
+  int T, splits;
+  float scale;
+  int pad_;
+};
+struct RedJob {
+  int32_t member, tile, I, J;
+};
+
+__global__ void __launch_bounds__(256) reduce_pack_kernel(const RedJob* __restrict__ jobs,
+                                                          const RedMember* __restrict__ mems, float decay,
+                                                          float world_scale, float* packed_override,
+                                                          float scale_override) {
   __shared__ float tile[32][33];
   __shared__ int last;
-  int I = 0, rem = blockIdx.y;
-  while (rem >= T - I) rem -= T - I, ++I;
-  const int J = I + rem;
-  const int tile_idx = blockIdx.y;
+  const RedJob jb = jobs[blockIdx.y];
+  const RedMember mb = mems[jb.member];
+  const int64_t d = mb.d;
+  const int I = jb.I, J = jb.J, splits = mb.splits;
   const int sb = blockIdx.x, i0 = (sb >> 2) * 32, j0 = (sb & 3) * 32;
-  if (int64_t(I) * 128 + i0 >= d || int64_t(J) * 128 + j0 >= d) return;
   const int nch = (splits + kChunk - 1) / kChunk, ch = blockIdx.z;
+  if (ch >= nch) return;
+  if (int64_t(I) * 128 + i0 >= d || int64_t(J) * 128 + j0 >= d) return;
   const int s0 = ch * kChunk, s1 = min(splits, s0 + kChunk);
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const float* base = part + (int64_t(tile_idx) * splits) * 16384 + i0 + tx;
+  const float* base = mb.part + (int64_t(jb.tile) * splits) * 16384 + i0 + tx;
   float acc[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -248,28 +266,30 @@ __global__ void __launch_bounds__(256) reduce_pack_kernel(const float* __restric
       if (s0 + u < s1) a += __ldg(p + int64_t(s0 + u) * 16384);
     acc[r] = a;
   }
-  const int slot = tile_idx * 16 + sb;
+  const int slot = jb.tile * 16 + sb;
   if (nch > 1) {
-    float* mine = chunks + (int64_t(slot) * nch + ch) * 1024;
+    float* mine = mb.chunks + (int64_t(slot) * nch + ch) * 1024;
 #pragma unroll
     for (int r = 0; r < 4; ++r) mine[(ty + 8 * r) * 32 + tx] = acc[r];
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = (atomicAdd(counters + slot, 1) == nch - 1);
+    if (threadIdx.x == 0) last = (atomicAdd(mb.counters + slot, 1) == nch - 1);
     __syncthreads();
     if (!last) return;
     __threadfence();
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       float a = 0.f;
-      for (int c = 0; c < nch; ++c) a += __ldcg(chunks + (int64_t(slot) * nch + c) * 1024 + (ty + 8 * r) * 32 + tx);
+      for (int c = 0; c < nch; ++c) a += __ldcg(mb.chunks + (int64_t(slot) * nch + c) * 1024 + (ty + 8 * r) * 32 + tx);
       acc[r] = a;
     }
-    if (threadIdx.x == 0) counters[slot] = 0;  // ready for the next run
+    if (threadIdx.x == 0) mb.counters[slot] = 0;  // ready for the next run
   }
 #pragma unroll
   for (int r = 0; r < 4; ++r) tile[ty + 8 * r][tx] = acc[r];  // tile[j][i]
   __syncthreads();
+  float* packed = packed_override ? packed_override : mb.packed;
+  const float scale = scale_override >= 0.f ? scale_override : mb.scale;
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     const int k = ty + 8 * r;
@@ -288,18 +308,33 @@ __global__ void __launch_bounds__(256) reduce_pack_kernel(const float* __restric
 
 using namespace spd;
 
-struct spdkfac_factor_plan {
+// A factor group: n layer-sides staged independently (per-member staging buffers and tensor
+// maps) and reduced by ONE persistent tcgen05 launch over all members' tiles (largest K
+// first) plus one grouped split-K reduce.  The single-factor plan is a group of one whose
+// packed target and scale are supplied per run.
+struct Member {
   spdkfac_factor_geom g;
   int64_t M, d, Mpad;
-  int T, splits, n_items;
+  int T, splits, n_tiles;
+  int Ho, Wo;
   __nv_bfloat16* xt;
   float* partial;
   float* chunks;
   int* counters;
-  CUtensorMap* maps;
-  TcItem* items;
-  TcEpi* epis;
 };
+
+struct spdkfac_factor_group {
+  std::vector<Member> m;
+  CUtensorMap* maps = nullptr;
+  TcItem* items = nullptr;
+  TcEpi* epis = nullptr;
+  RedJob* jobs = nullptr;
+  RedMember* rmem = nullptr;
+  int n_items = 0, n_jobs = 0, max_chunks = 0;
+  double flops = 0;
+  bool per_run_target = false;  // single-factor plan: packed pointer / scale given to run()
+};
+struct spdkfac_factor_plan : spdkfac_factor_group {};
 
 namespace {
 
@@ -335,37 +370,178 @@ int geom_dims(const spdkfac_factor_geom* g, int64_t* rows, int64_t* dim, int* Ho
   return SPDKFAC_OK;
 }
 
-struct FactorLayout {
-  int64_t M, d, Mpad;
-  int T, splits, n_tiles;
-};
-
-FactorLayout factor_layout(int64_t M, int64_t d) {
-  FactorLayout L;
-  L.M = M;
-  L.d = d;
-  L.Mpad = round_up(M, 64);
-  L.T = int(cdiv(d, 128));
-  L.n_tiles = L.T * (L.T + 1) / 2;
-  const int64_t nkb = L.Mpad / 64;
-  // split K so that the launch fills ~148 SMs, each slice >= 16 K blocks (1024 rows);
-  // splits == 1 stores straight into the packed buffer from the tile epilogue
-  int64_t want = cdiv(148, L.n_tiles);
-  int64_t maxs = std::max<int64_t>(1, nkb / 16);
-  L.splits = int(std::max<int64_t>(1, std::min(want, maxs)));
-  return L;
+// splits: fill ~148 SMs per factor (the group launch then has >= that many items), each
+// K slice >= 16 blocks (1024 rows); splits == 1 stores straight into the packed buffer
+int choose_splits(int64_t Mpad, int n_tiles) {
+  const int64_t nkb = Mpad / 64;
+  const int64_t want = cdiv(148, n_tiles);
+  const int64_t maxs = std::max<int64_t>(1, nkb / 16);
+  return int(std::max<int64_t>(1, std::min(want, maxs)));
 }
 
-size_t factor_ws(const FactorLayout& L, Carve* c) {
-  Carve& cv = *c;
-  cv.take<__nv_bfloat16>(size_t(2) * L.d * L.Mpad);
-  cv.take<float>(L.splits > 1 ? size_t(L.n_tiles) * L.splits * 16384 : 1);
-  cv.take<float>(L.splits > 1 ? size_t(L.n_tiles) * 16 * cdiv(L.splits, kChunk) * 1024 : 1);
-  cv.take<int>(size_t(L.n_tiles) * 16);
-  cv.take<CUtensorMap>(1, 128);
-  cv.take<TcItem>(size_t(L.n_tiles) * L.splits);
-  cv.take<TcEpi>(1);
-  return cv.used;
+int member_init(Member* mb, const spdkfac_factor_geom* g) {
+  int64_t M, d;
+  int Ho = 0, Wo = 0;
+  int rc = geom_dims(g, &M, &d, &Ho, &Wo);
+  if (rc) return rc;
+  mb->g = *g;
+  mb->M = M;
+  mb->d = d;
+  mb->Ho = Ho;
+  mb->Wo = Wo;
+  mb->Mpad = round_up(M, 64);
+  mb->T = int(cdiv(d, 128));
+  mb->n_tiles = mb->T * (mb->T + 1) / 2;
+  mb->splits = choose_splits(mb->Mpad, mb->n_tiles);
+  return SPDKFAC_OK;
+}
+
+// carve one group's workspace (c.base == nullptr: size only)
+void group_carve(spdkfac_factor_group* G, Carve& c) {
+  int items = 0, jobs = 0;
+  for (Member& mb : G->m) {
+    mb.xt = c.take<__nv_bfloat16>(size_t(2) * mb.d * mb.Mpad);
+    if (mb.splits > 1) {
+      mb.partial = c.take<float>(size_t(mb.n_tiles) * mb.splits * 16384);
+      mb.chunks = c.take<float>(size_t(mb.n_tiles) * 16 * cdiv(mb.splits, kChunk) * 1024);
+      mb.counters = c.take<int>(size_t(mb.n_tiles) * 16);
+      jobs += mb.n_tiles;
+    } else {
+      mb.partial = nullptr, mb.chunks = nullptr, mb.counters = nullptr;
+    }
+    items += mb.n_tiles * mb.splits;
+  }
+  const size_t n = G->m.size();
+  G->maps = c.take<CUtensorMap>(n, 128);
+  G->items = c.take<TcItem>(size_t(std::max(items, 1)));
+  G->epis = c.take<TcEpi>(n);
+  G->jobs = c.take<RedJob>(size_t(std::max(jobs, 1)));
+  G->rmem = c.take<RedMember>(n);
+  G->n_items = items;
+  G->n_jobs = jobs;
+}
+
+int group_build(spdkfac_factor_group* G, float* const* packed, const float* scales, cudaStream_t s) {
+  const int n = int(G->m.size());
+  std::vector<CUtensorMap> maps(n);
+  std::vector<TcItem> items;
+  std::vector<TcEpi> epis(n);
+  std::vector<RedJob> jobs;
+  std::vector<RedMember> rmem(n);
+  G->max_chunks = 1;
+  G->flops = 0;
+  for (int k = 0; k < n; ++k) {
+    Member& mb = G->m[k];
+    int rc = make_operand_map(&maps[k], mb.xt, true, mb.Mpad, mb.d, mb.Mpad);
+    if (rc) return rc;
+    G->flops += double(mb.M) * mb.d * (mb.d + 1);
+    const int64_t nkb = mb.Mpad / 64, per = cdiv(nkb, mb.splits);
+    for (int I = 0; I < mb.T; ++I)
+      for (int J = I; J < mb.T; ++J) {
+        const int tile_idx = I * mb.T - I * (I - 1) / 2 + (J - I);
+        if (mb.splits > 1) jobs.push_back(RedJob{k, tile_idx, I, J});
+        for (int s2 = 0; s2 < mb.splits; ++s2) {
+          TcItem it{};
+          it.a_map = k;
+          it.b_map = k;
+          it.a_row = I * 128;
+          it.b_row = J * 128;
+          const int64_t kb0 = std::min<int64_t>(nkb, s2 * per), kb1 = std::min<int64_t>(nkb, (s2 + 1) * per);
+          it.k0 = int(kb0 * 64);
+          it.nk = int(kb1 - kb0);
+          it.epi = k;
+          it.flags = (I == J) ? kSameAB : 0;
+          if (mb.splits > 1) {  // partial tile -> member workspace slot, reduced by reduce_pack_kernel
+            it.out_r = 0;
+            it.out_c = (tile_idx * mb.splits + s2) * 128;
+          } else {              // direct packed-upper epilogue
+            it.out_r = I * 128;
+            it.out_c = J * 128;
+          }
+          it.m_valid = int(std::min<int64_t>(128, mb.d - int64_t(I) * 128));
+          it.n_valid = int(std::min<int64_t>(128, mb.d - int64_t(J) * 128));
+          if (it.nk > 0) items.push_back(it);
+        }
+      }
+    if (mb.splits > 1) {
+      epis[k] = TcEpi{mb.partial, 128, 0, 1.f, 0.f, kAxpby, 0, nullptr, 0, 0};
+      G->max_chunks = std::max<int>(G->max_chunks, int(cdiv(mb.splits, kChunk)));
+    } else {  // packed target: from the epilogue table (group) or the run arguments (single plan)
+      epis[k] = TcEpi{packed ? packed[k] : nullptr, mb.d, 0, scales ? scales[k] : 1.f, 0.f, kPackedUpper, 0,
+                      nullptr, 0, 0};
+    }
+    rmem[k] = RedMember{mb.partial, mb.chunks, mb.counters, packed ? packed[k] : nullptr, mb.d, mb.T, mb.splits,
+                        scales ? scales[k] : 1.f, 0};
+    if (mb.Mpad > mb.M) {
+      zero_pad_kernel<<<unsigned(mb.d), 64, 0, s>>>(mb.xt, mb.d, mb.M, mb.Mpad);
+      SPD_CHECK_LAUNCH();
+    }
+    if (mb.counters) SPD_CUDA(cudaMemsetAsync(mb.counters, 0, sizeof(int) * size_t(mb.n_tiles) * 16, s));
+  }
+  // persistent CTAs take items round-robin: longest K first balances the group
+  std::stable_sort(items.begin(), items.end(), [](const TcItem& a, const TcItem& b) { return a.nk > b.nk; });
+  G->n_items = int(items.size());
+  int rc;
+  if ((rc = upload(G->maps, maps, s)) || (rc = upload(G->items, items, s)) || (rc = upload(G->epis, epis, s)) ||
+      (rc = upload(G->jobs, jobs, s)) || (rc = upload(G->rmem, rmem, s)))
+    return rc;
+  return SPDKFAC_OK;
+}
+
+int member_stage(const Member& mb, const float* x, cudaStream_t s) {
+  const spdkfac_factor_geom& g = mb.g;
+  stat_begin(kCatFactorStage, s);
+  if (g.layout == SPDKFAC_ROWS || g.layout == SPDKFAC_SPATIAL_NHWC) {
+    // channels-last output gradients are rows [b*h*w][C]: the same transpose
+    const int64_t ld = g.layout == SPDKFAC_ROWS ? g.w : g.c;
+    dim3 grid(unsigned(cdiv(mb.Mpad, 64)), unsigned(cdiv(mb.d, 32)));
+    stage_rows_kernel<<<grid, 256, 0, s>>>(x, mb.M, mb.d, ld, mb.xt, mb.Mpad);
+  } else if (g.layout == SPDKFAC_CONV_A_NHWC || g.layout == SPDKFAC_CONV_A) {
+    ConvGeom cg{int(g.n), int(g.c), int(g.h), int(g.w), mb.Ho, mb.Wo, g.kh, g.kw, g.stride_h, g.stride_w,
+                g.pad_h, g.pad_w, g.dil_h, g.dil_w};
+    if (g.layout == SPDKFAC_CONV_A_NHWC) {
+      if (g.c < 16) {
+        stage_im2col_nhwc_smallc_kernel<<<unsigned(cdiv(mb.Mpad, 512)), 256, 0, s>>>(x, cg, mb.M, mb.d, mb.xt,
+                                                                                     mb.Mpad);
+      } else {
+        dim3 grid(unsigned(cdiv(mb.Mpad, 64)), unsigned(cdiv(g.c, 32)), unsigned(g.kh * g.kw));
+        stage_im2col_nhwc_kernel<<<grid, 256, 0, s>>>(x, cg, mb.M, mb.d, mb.xt, mb.Mpad);
+      }
+    } else {
+      const int hwo = mb.Ho * mb.Wo;
+      dim3 grid(unsigned(g.n), unsigned(mb.d));
+      stage_im2col_kernel<<<grid, hwo >= 512 ? 256 : (hwo >= 128 ? 64 : 32), 0, s>>>(x, cg, mb.M, mb.d, mb.xt,
+                                                                                      mb.Mpad);
+    }
+  } else {
+    const int hw = int(g.h * g.w);
+    dim3 grid(unsigned(g.n), unsigned(mb.d));
+    stage_spatial_kernel<<<grid, hw >= 512 ? 256 : (hw >= 128 ? 64 : 32), 0, s>>>(x, int(g.c), hw, mb.xt, mb.Mpad);
+  }
+  SPD_CHECK_LAUNCH();
+  stat_end(kCatFactorStage, s, 0, double(mb.M) * mb.d * 4 + 4.0 * mb.d * mb.Mpad);
+  return SPDKFAC_OK;
+}
+
+int group_compute(spdkfac_factor_group* G, float scale, float decay, float world_scale, float* packed,
+                  cudaStream_t s) {
+  // algorithmic work: sum over members of M * d * (d + 1) flops
+  stat_begin(kCatFactorSyrk, s);
+  TcRun run{packed, G->m.empty() ? 0 : G->m[0].d, scale, decay, world_scale, 0};
+  int rc = launch_tc3(Kind::BF16, G->maps, G->items, G->epis, G->n_items, s, run);
+  if (rc) return rc;
+  double bytes = 0;
+  for (const Member& mb : G->m) bytes += 4.0 * mb.d * mb.Mpad;
+  stat_end(kCatFactorSyrk, s, G->flops, bytes);
+  if (G->n_jobs == 0) return SPDKFAC_OK;
+  dim3 rgrid(16, unsigned(G->n_jobs), unsigned(G->max_chunks));
+  stat_begin(kCatFactorReduce, s);
+  reduce_pack_kernel<<<rgrid, 256, 0, s>>>(G->jobs, G->rmem, decay, world_scale,
+                                           G->per_run_target ? packed : nullptr,
+                                           G->per_run_target ? scale : -1.f);
+  SPD_CHECK_LAUNCH();
+  stat_end(kCatFactorReduce, s, 0, 0);
+  return SPDKFAC_OK;
 }
 
 }  // namespace
@@ -377,85 +553,33 @@ int spdkfac_factor_dims(const spdkfac_factor_geom* g, int64_t* rows, int64_t* di
 }
 
 size_t spdkfac_factor_workspace_size(const spdkfac_factor_geom* g) {
-  int64_t M, d;
-  if (geom_dims(g, &M, &d) != SPDKFAC_OK) return 0;
+  spdkfac_factor_group G;
+  G.m.resize(1);
+  if (member_init(&G.m[0], g) != SPDKFAC_OK) return 0;
   Carve c(nullptr, 0);
-  return factor_ws(factor_layout(M, d), &c) + 256;
+  group_carve(&G, c);
+  return c.used + 256;
 }
 
 int spdkfac_factor_plan_create(spdkfac_factor_plan** out, const spdkfac_factor_geom* g, void* ws, size_t ws_bytes,
                                void* stream) {
   SPD_ARG(out != nullptr, SPDKFAC_ERR_ARG, "null plan out");
-  int64_t M, d;
-  int rc = geom_dims(g, &M, &d);
-  if (rc) return rc;
-  FactorLayout L = factor_layout(M, d);
-  Carve c(ws, ws_bytes);
   auto* p = new spdkfac_factor_plan();
-  p->g = *g;
-  p->M = M;
-  p->d = d;
-  p->Mpad = L.Mpad;
-  p->T = L.T;
-  p->splits = L.splits;
-  p->n_items = L.n_tiles * L.splits;
-  p->xt = c.take<__nv_bfloat16>(size_t(2) * d * L.Mpad);
-  p->partial = c.take<float>(L.splits > 1 ? size_t(L.n_tiles) * L.splits * 16384 : 1);
-  p->chunks = c.take<float>(L.splits > 1 ? size_t(L.n_tiles) * 16 * cdiv(L.splits, kChunk) * 1024 : 1);
-  p->counters = c.take<int>(size_t(L.n_tiles) * 16);
-  p->maps = c.take<CUtensorMap>(1, 128);
-  p->items = c.take<TcItem>(size_t(p->n_items));
-  p->epis = c.take<TcEpi>(1);
+  p->m.resize(1);
+  int rc = member_init(&p->m[0], g);
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  Carve c(ws, ws_bytes);
+  group_carve(p, c);
   if (!c.ok() || ws == nullptr) {
     delete p;
     set_error("factor workspace too small: need %zu bytes, got %zu", c.used, ws_bytes);
     return SPDKFAC_ERR_ARG;
   }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  std::vector<CUtensorMap> maps(1);
-  rc = make_operand_map(&maps[0], p->xt, true, L.Mpad, d, L.Mpad);
-  if (rc) {
-    delete p;
-    return rc;
-  }
-  std::vector<TcItem> items;
-  const int64_t nkb = L.Mpad / 64;
-  const int64_t per = cdiv(nkb, L.splits);
-  for (int I = 0; I < L.T; ++I)
-    for (int J = I; J < L.T; ++J) {
-      const int tile_idx = I * L.T - I * (I - 1) / 2 + (J - I);
-      for (int s2 = 0; s2 < L.splits; ++s2) {
-        TcItem it{};
-        it.a_map = 0;
-        it.b_map = 0;
-        it.a_row = I * 128;
-        it.b_row = J * 128;
-        const int64_t kb0 = std::min<int64_t>(nkb, s2 * per), kb1 = std::min<int64_t>(nkb, (s2 + 1) * per);
-        it.k0 = int(kb0 * 64);
-        it.nk = int(kb1 - kb0);
-        it.epi = 0;
-        it.flags = (I == J) ? kSameAB : 0;
-        if (L.splits > 1) {  // partial tile -> workspace slot, reduced by reduce_pack_kernel
-          it.out_r = 0;
-          it.out_c = (tile_idx * L.splits + s2) * 128;
-        } else {             // direct packed-upper epilogue
-          it.out_r = I * 128;
-          it.out_c = J * 128;
-        }
-        it.m_valid = int(std::min<int64_t>(128, d - int64_t(I) * 128));
-        it.n_valid = int(std::min<int64_t>(128, d - int64_t(J) * 128));
-        items.push_back(it);
-      }
-    }
-  std::vector<TcEpi> epis(1);
-  epis[0] = L.splits > 1 ? TcEpi{p->partial, 128, 0, 1.f, 0.f, kAxpby, 0, nullptr, 0, 0}
-                         : TcEpi{nullptr, 0, 0, 1.f, 0.f, kPackedUpper, 0, nullptr, 0, 0};
-  if (L.Mpad > M) {
-    zero_pad_kernel<<<unsigned(d), 64, 0, s>>>(p->xt, d, M, L.Mpad);
-    SPD_CHECK_LAUNCH();
-  }
-  SPD_CUDA(cudaMemsetAsync(p->counters, 0, sizeof(int) * size_t(L.n_tiles) * 16, s));
-  if ((rc = upload(p->maps, maps, s)) || (rc = upload(p->items, items, s)) || (rc = upload(p->epis, epis, s))) {
+  p->per_run_target = true;
+  if ((rc = group_build(p, nullptr, nullptr, static_cast<cudaStream_t>(stream)))) {
     delete p;
     return rc;
   }
@@ -465,64 +589,13 @@ int spdkfac_factor_plan_create(spdkfac_factor_plan** out, const spdkfac_factor_g
 
 int spdkfac_factor_plan_stage(spdkfac_factor_plan* p, const float* x, void* stream) {
   SPD_ARG(p && x, SPDKFAC_ERR_ARG, "null argument");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const spdkfac_factor_geom& g = p->g;
-  stat_begin(kCatFactorStage, s);
-  if (g.layout == SPDKFAC_ROWS || g.layout == SPDKFAC_SPATIAL_NHWC) {
-    // channels-last output gradients are rows [b*h*w][C]: the same transpose
-    const int64_t ld = g.layout == SPDKFAC_ROWS ? g.w : g.c;
-    dim3 grid(unsigned(cdiv(p->Mpad, 64)), unsigned(cdiv(p->d, 32)));
-    stage_rows_kernel<<<grid, 256, 0, s>>>(x, p->M, p->d, ld, p->xt, p->Mpad);
-  } else if (g.layout == SPDKFAC_CONV_A_NHWC) {
-    int64_t rows, dim;
-    int Ho = 0, Wo = 0;
-    geom_dims(&g, &rows, &dim, &Ho, &Wo);
-    ConvGeom cg{int(g.n), int(g.c), int(g.h), int(g.w), Ho, Wo, g.kh, g.kw, g.stride_h, g.stride_w,
-                g.pad_h, g.pad_w, g.dil_h, g.dil_w};
-    if (g.c < 16) {
-      stage_im2col_nhwc_smallc_kernel<<<unsigned(cdiv(p->Mpad, 512)), 256, 0, s>>>(x, cg, p->M, p->d, p->xt,
-                                                                                   p->Mpad);
-    } else {
-      dim3 grid(unsigned(cdiv(p->Mpad, 64)), unsigned(cdiv(g.c, 32)), unsigned(g.kh * g.kw));
-      stage_im2col_nhwc_kernel<<<grid, 256, 0, s>>>(x, cg, p->M, p->d, p->xt, p->Mpad);
-    }
-  } else if (g.layout == SPDKFAC_CONV_A) {
-    int64_t rows, dim;
-    int Ho = 0, Wo = 0;
-    geom_dims(&g, &rows, &dim, &Ho, &Wo);
-    ConvGeom cg{int(g.n), int(g.c), int(g.h), int(g.w), Ho, Wo, g.kh, g.kw, g.stride_h, g.stride_w,
-                g.pad_h, g.pad_w, g.dil_h, g.dil_w};
-    const int hwo = Ho * Wo;
-    dim3 grid(unsigned(g.n), unsigned(p->d));
-    stage_im2col_kernel<<<grid, hwo >= 512 ? 256 : (hwo >= 128 ? 64 : 32), 0, s>>>(x, cg, p->M, p->d, p->xt, p->Mpad);
-  } else {
-    const int hw = int(g.h * g.w);
-    dim3 grid(unsigned(g.n), unsigned(p->d));
-    stage_spatial_kernel<<<grid, hw >= 512 ? 256 : (hw >= 128 ? 64 : 32), 0, s>>>(x, int(g.c), hw, p->xt, p->Mpad);
-  }
-  SPD_CHECK_LAUNCH();
-  stat_end(kCatFactorStage, s, 0, double(p->M) * p->d * 4 + 4.0 * p->d * p->Mpad);
-  return SPDKFAC_OK;
+  return member_stage(p->m[0], x, static_cast<cudaStream_t>(stream));
 }
 
 int spdkfac_factor_plan_compute(spdkfac_factor_plan* p, float scale, float decay, float world_scale, float* packed,
                                 void* stream) {
   SPD_ARG(p && packed, SPDKFAC_ERR_ARG, "null argument");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // algorithmic work of one factor: M * d * (d + 1) flops (upper triangle incl. diagonal)
-  stat_begin(kCatFactorSyrk, s);
-  TcRun run{packed, p->d, scale, decay, world_scale, 0};
-  int rc = launch_tc3(Kind::BF16, p->maps, p->items, p->epis, p->n_items, s, run);
-  if (rc) return rc;
-  stat_end(kCatFactorSyrk, s, double(p->M) * p->d * (p->d + 1), 4.0 * p->d * p->Mpad);
-  if (p->splits == 1) return SPDKFAC_OK;
-  dim3 rgrid(16, unsigned(p->T * (p->T + 1) / 2), unsigned(cdiv(p->splits, kChunk)));
-  stat_begin(kCatFactorReduce, s);
-  reduce_pack_kernel<<<rgrid, 256, 0, s>>>(p->partial, p->d, p->T, p->splits, scale, decay, world_scale,
-                                           packed, p->chunks, p->counters);
-  SPD_CHECK_LAUNCH();
-  stat_end(kCatFactorReduce, s, 0, 65536.0 * p->n_items + 4.0 * p->d * (p->d + 1) / 2 * (decay == 0.f ? 1 : 2));
-  return SPDKFAC_OK;
+  return group_compute(p, scale, decay, world_scale, packed, static_cast<cudaStream_t>(stream));
 }
 
 int spdkfac_factor_plan_run(spdkfac_factor_plan* p, const float* x, float scale, float decay, float world_scale,
@@ -533,5 +606,55 @@ int spdkfac_factor_plan_run(spdkfac_factor_plan* p, const float* x, float scale,
 }
 
 void spdkfac_factor_plan_destroy(spdkfac_factor_plan* p) { delete p; }
+
+size_t spdkfac_factor_group_workspace_size(int n, const spdkfac_factor_geom* geoms) {
+  if (n < 1 || !geoms) return 0;
+  spdkfac_factor_group G;
+  G.m.resize(n);
+  for (int k = 0; k < n; ++k)
+    if (member_init(&G.m[k], &geoms[k]) != SPDKFAC_OK) return 0;
+  Carve c(nullptr, 0);
+  group_carve(&G, c);
+  return c.used + 256;
+}
+
+int spdkfac_factor_group_create(spdkfac_factor_group** out, int n, const spdkfac_factor_geom* geoms,
+                                float* const* packed_out, const float* scales, void* ws, size_t ws_bytes,
+                                void* stream) {
+  SPD_ARG(out && n >= 1 && geoms && packed_out && scales, SPDKFAC_ERR_ARG, "bad factor group arguments");
+  auto* G = new spdkfac_factor_group();
+  G->m.resize(n);
+  int rc;
+  for (int k = 0; k < n; ++k)
+    if ((rc = member_init(&G->m[k], &geoms[k]))) {
+      delete G;
+      return rc;
+    }
+  Carve c(ws, ws_bytes);
+  group_carve(G, c);
+  if (!c.ok() || ws == nullptr) {
+    delete G;
+    set_error("factor group workspace too small: need %zu bytes, got %zu", c.used, ws_bytes);
+    return SPDKFAC_ERR_ARG;
+  }
+  if ((rc = group_build(G, packed_out, scales, static_cast<cudaStream_t>(stream)))) {
+    delete G;
+    return rc;
+  }
+  *out = G;
+  return SPDKFAC_OK;
+}
+
+int spdkfac_factor_group_stage(spdkfac_factor_group* G, int member, const float* x, void* stream) {
+  SPD_ARG(G && x && member >= 0 && member < int(G->m.size()), SPDKFAC_ERR_ARG, "bad factor group stage arguments");
+  return member_stage(G->m[member], x, static_cast<cudaStream_t>(stream));
+}
+
+int spdkfac_factor_group_compute(spdkfac_factor_group* G, float decay, float world_scale, void* stream) {
+  SPD_ARG(G != nullptr, SPDKFAC_ERR_ARG, "null factor group");
+  return group_compute(G, 1.f, decay, world_scale, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+void spdkfac_factor_group_destroy(spdkfac_factor_group* G) { delete G; }
 
 }  // extern "C"

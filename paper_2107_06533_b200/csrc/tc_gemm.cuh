@@ -147,8 +147,10 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
       }
     }
   } else {  // kPackedUpper: global row gi = out_r + i, columns gj = out_c + c*32 + t, keep gj >= gi
-    float* out = static_cast<float*>(run.out);
-    const int64_t gi = ri, d = run.d;
+    // target / dim / scale from the epilogue table (factor groups) or the run arguments (single plan)
+    float* out = static_cast<float*>(ep.out ? ep.out : run.out);
+    const int64_t gi = ri, d = ep.out ? ep.ld : run.d;
+    const float alpha = ep.out ? ep.alpha : run.alpha;
     const int64_t gj0 = int64_t(it.out_c) + c * 32;
     float* rowp = out + gi * (2 * d - gi + 1) / 2 - gi;  // packed index of (gi, gj) = rowp + gj
     float old[32];
@@ -159,7 +161,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
 #pragma unroll
     for (int t = 0; t < 32; ++t) {
       if (row_ok && t < jn && gj0 + t >= gi) {
-        const float fresh = run.alpha * v[t];
+        const float fresh = alpha * v[t];
         const float nv = run.decay != 0.f ? run.decay * old[t] + (1.f - run.decay) * fresh : fresh;
         rowp[gj0 + t] = run.wscale * nv;
       }

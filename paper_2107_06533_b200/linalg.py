@@ -105,6 +105,52 @@ class FactorPlan:
             self._h = None
 
 
+class FactorGroup:
+    """Several factor sides staged one by one and computed by ONE tensor-core launch
+    (include/spdkfac.h factor group).  `members`: list of (layout, shape, kernel, stride,
+    padding, dilation); `packed`: per member, the fusion-buffer slice it writes; `scales`:
+    per member, the factor normalisation (1/M, or b^2/M for output gradients)."""
+
+    def __init__(self, members, packed, scales, stream=None):
+        lib = L.load(require_device=True)
+        n = len(members)
+        geoms = (L.FactorGeom * n)()
+        for k, (layout, shape, kernel, stride, padding, dilation) in enumerate(members):
+            g = geoms[k]
+            g.layout = layout
+            if layout == L.ROWS:
+                g.n, g.c, g.h, g.w = int(shape[0]), int(shape[1]), 1, int(shape[1])
+            else:
+                g.n, g.c, g.h, g.w = (int(v) for v in shape)
+            g.kh, g.kw = (int(v) for v in kernel)
+            g.stride_h, g.stride_w = (int(v) for v in stride)
+            g.pad_h, g.pad_w = (int(v) for v in padding)
+            g.dil_h, g.dil_w = (int(v) for v in dilation)
+        self.n = n
+        self.device = packed[0].device
+        self._keep = list(packed)
+        self._ws = _workspace(lib.spdkfac_factor_group_workspace_size(n, geoms), self.device)
+        sc = (C.c_float * n)(*[float(x) for x in scales])
+        h = C.c_void_p()
+        L.check(lib.spdkfac_factor_group_create(C.byref(h), n, geoms, L.ptr_array([p.data_ptr() for p in packed]),
+                                                sc, self._ws.data_ptr(), self._ws.numel(), _stream(stream)),
+                "factor group")
+        self._h, self._lib = h, lib
+
+    def stage(self, member: int, x: torch.Tensor, stream=None) -> None:
+        L.check(self._lib.spdkfac_factor_group_stage(self._h, int(member), x.data_ptr(), _stream(stream)),
+                "factor group stage")
+
+    def compute(self, decay: float = 0.0, world_scale: float = 1.0, stream=None) -> None:
+        L.check(self._lib.spdkfac_factor_group_compute(self._h, float(decay), float(world_scale), _stream(stream)),
+                "factor group compute")
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            self._lib.spdkfac_factor_group_destroy(self._h)
+            self._h = None
+
+
 def _rows_batch(batch, what: str) -> torch.Tensor:
     x = _f32(batch, what)
     if x.dim() != 2:

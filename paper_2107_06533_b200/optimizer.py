@@ -31,7 +31,7 @@ import torch.nn as nn
 
 from . import _lib as L
 from . import schedule as S
-from .linalg import FactorPlan, InversePlan, NotPositiveDefiniteError, PrecondPlan
+from .linalg import FactorGroup, FactorPlan, InversePlan, NotPositiveDefiniteError, PrecondPlan
 from .perfmodel import PerfParams, default_params
 from .planner import (FactorKind, FusionPolicy, inverse_tasks, factor_tasks, lbp_place, local_place, plan_fusion,
                       seq_place)
@@ -103,13 +103,11 @@ class SPDKFAC(torch.optim.Optimizer):
             from .comm import NcclComm
             comm = NcclComm(self.rank, self.world)
         self.comm = comm
-        # inverse broadcasts get their own communicator and stream: NCCL orders collectives per
-        # communicator, so all-reduces of later fusion groups never queue behind a broadcast that
-        # is waiting for an inversion (and the per-communicator order is identical on all ranks)
-        self.comm_bc = None
-        if self.world > 1:
-            from .comm import NcclComm
-            self.comm_bc = NcclComm(self.rank, self.world) if isinstance(comm, NcclComm) else comm
+        # one communicator, one comm stream: every rank issues the same collective sequence
+        # (factor all-reduces as fusion groups complete, then in step(): gradient all-reduce and
+        # the owners' inverse broadcasts), so no all-reduce ever queues behind a broadcast that
+        # waits for an inversion, and no two communicators' kernels can wait on each other
+        self.comm_bc = comm
 
         # ---- preconditioned layers, forward order (model definition order)
         self.layers: list[_Layer] = []
@@ -161,6 +159,8 @@ class SPDKFAC(torch.optim.Optimizer):
         self._gslice = {"A": [self._groups_fwd[g[-1].layer_index - 1] for g in self.fwd_plan.groups],
                         "G": [self._groups_bwd[g[-1].layer_index - 1] for g in self.bwd_plan.groups]}
         self._gseen = {"A": [0] * len(self.fwd_plan.groups), "G": [0] * len(self.bwd_plan.groups)}
+        self._fgroups = None  # per fusion group FactorGroup objects, built after the first iteration
+        self._rec = {"A": [None] * len(self.layers), "G": [None] * len(self.layers)}
 
         # ---- inverses (every rank holds all of them for preconditioning)
         self.inv = []
@@ -175,6 +175,10 @@ class SPDKFAC(torch.optim.Optimizer):
         self._mine = mine
         grp = S.inversion_groups([l.spec.a_dim for l in self.layers], [l.spec.g_dim for l in self.layers])
         self._n_g1 = grp["n_g1"]
+        # G1 may start once every backward fusion group holding a G1 member is computed; the
+        # factors a G1 inverse reads must be complete (members of a group run together)
+        self._g1_groups = {self._gid["G"][li] for li in range(len(self.layers) - self._n_g1, len(self.layers))}
+        self._g1_left = len(self._g1_groups)
         self._inv_plans, self._info_host, self._bcast = {}, {}, {}
         for side in ("A", "G1", "G2"):
             ts = [t for t in mine if t in grp[side]]
@@ -189,7 +193,6 @@ class SPDKFAC(torch.optim.Optimizer):
         self._g_count = 0
         self._g1_inverted = False
         self.comm_stream = torch.cuda.Stream(self.device) if self.world > 1 else None
-        self.bcast_stream = torch.cuda.Stream(self.device) if self.world > 1 else None
         self._info_events = []
         self._a_count = 0
         self._a_inverted = False
@@ -296,49 +299,112 @@ class SPDKFAC(torch.optim.Optimizer):
         return l.g_plan
 
     def _launch_factor(self, l: _Layer, x: torch.Tensor, kind: str):
-        """Stage x on the stream that owns it (im2col/transpose + precision split into the
-        plan's buffer), then run the tensor-core SYRK on the factor stream.  The SYRK reads
-        only plan memory, so x's lifetime is not extended across streams."""
+        """Stage x on the stream that owns it (im2col/transpose + precision split into a
+        staging buffer), then run the tensor-core SYRK on the factor stream.  The SYRK reads
+        only staging memory, so x's lifetime is not extended across streams.
+
+        Steady state: one FactorGroup per fusion group (planner.py:94-121); members are staged
+        as their hooks fire and the group's single tensor-core launch (and, for P > 1, its
+        all-reduce) follows its last member.  The first iteration (and any shape change) runs
+        per-layer plans and records the shapes the groups are built from (in step())."""
         main = torch.cuda.current_stream(self.device)
         fs = self.factor_stream
         # samples of a batch-mean loss: the image batch for convs, the rows for linears
         nb = x.shape[0] if l.is_conv else x.numel() // x.shape[-1]
         if kind == "A" and self._a_count == 0:
-            self._tl("fwd_start", torch.cuda.current_stream(self.device))
+            self._tl("fwd_start", main)
         layout, x = self._prepare(l, x.detach(), kind)
-        plan = self._plan_for(l, layout, x, kind)
-        ev_done, ev_staged = l.events[kind]
+        key = (layout,) + tuple(x.shape)
         capturing = torch.cuda.is_current_stream_capturing()
-        if not capturing and l.pending[kind]:
-            main.wait_event(ev_done)  # previous iteration's SYRK has consumed the staging buffer
-        plan.stage(x, main)
-        ev_staged.record(main)
-        fs.wait_event(ev_staged)
         decay = self.factor_decay if self._factor_updates > 0 else 0.0
-        if kind == "A":
-            buf, off, d, scale = self.bufA, l.a_off, l.spec.a_dim, 1.0 / plan.rows
+        gid = self._gid[kind][l.index]
+        fg = self._fgroups[kind][gid] if self._fgroups is not None else None
+        if fg is not None and fg["keys"][l.index] == key:
+            if fg["seen"] == 0 and not capturing and fg["pending"]:
+                main.wait_event(fg["done"])  # previous iteration's SYRK has consumed the staging buffers
+            fg["obj"].stage(fg["member"][l.index], x, main)
+            fg["seen"] += 1
         else:
-            b = nb if self.batch_averaged else 1
-            buf, off, d, scale = self.bufG, l.g_off, l.spec.g_dim, float(b * b) / plan.rows
-        plan.compute(buf[off:off + d * (d + 1) // 2], scale, decay, 1.0 / self.world, fs)
-        ev_done.record(fs)
-        l.pending[kind] = not capturing
-        if self.world > 1:
-            gid = self._gid[kind][l.index]
-            self._gseen[kind][gid] += 1
-            if self._gseen[kind][gid] == self._gsize[kind][gid]:  # every member of the group written
-                s, e = self._gslice[kind][gid]
-                cs = self.comm_stream
-                cs.wait_stream(fs)
-                self.comm.allreduce_sum(buf[s:e], cs)
+            if fg is not None:  # shape changed: per-layer plans this iteration, rebuild groups after
+                self._fgroups = None
+            plan = self._plan_for(l, layout, x, kind)
+            ev_done, ev_staged = l.events[kind]
+            if not capturing and l.pending[kind]:
+                main.wait_event(ev_done)
+            plan.stage(x, main)
+            ev_staged.record(main)
+            fs.wait_event(ev_staged)
+            if kind == "A":
+                buf, off, d, scale = self.bufA, l.a_off, l.spec.a_dim, 1.0 / plan.rows
+            else:
+                b = nb if self.batch_averaged else 1
+                buf, off, d, scale = self.bufG, l.g_off, l.spec.g_dim, float(b * b) / plan.rows
+            plan.compute(buf[off:off + d * (d + 1) // 2], scale, decay, 1.0 / self.world, fs)
+            ev_done.record(fs)
+            l.pending[kind] = not capturing
+            m = l.module
+            geo = (layout, tuple(x.shape), tuple(m.kernel_size), tuple(m.stride), tuple(m.padding),
+                   tuple(m.dilation)) if (l.is_conv and kind == "A") else (layout, tuple(x.shape), (1, 1), (1, 1),
+                                                                           (0, 0), (1, 1))
+            self._rec[kind][l.index] = (key, geo, scale)
+        self._gseen[kind][gid] += 1
+        if self._gseen[kind][gid] == self._gsize[kind][gid]:  # every member of the fusion group staged
+            self._group_complete(kind, gid, decay, capturing)
         if kind == "A":
             self._a_count += 1
             if self._a_count == len(self.layers):
                 self._launch_inverse_A()
-        elif l.index >= len(self.layers) - self._n_g1:  # a G1 member
-            self._g_count += 1
-            if self._g_count == self._n_g1:
+
+    def _group_complete(self, kind: str, gid: int, decay: float, capturing: bool) -> None:
+        main = torch.cuda.current_stream(self.device)
+        fs = self.factor_stream
+        buf = self.bufA if kind == "A" else self.bufG
+        fg = self._fgroups[kind][gid] if self._fgroups is not None else None
+        if fg is not None and fg["seen"] == self._gsize[kind][gid]:
+            fg["staged"].record(main)
+            fs.wait_event(fg["staged"])
+            fg["obj"].compute(decay, 1.0 / self.world, fs)
+            fg["done"].record(fs)
+            fg["pending"] = not capturing
+            fg["seen"] = 0
+        if self.world > 1:
+            s, e = self._gslice[kind][gid]
+            cs = self.comm_stream
+            cs.wait_stream(fs)
+            self.comm.allreduce_sum(buf[s:e], cs)
+        if kind == "G" and gid in self._g1_groups:
+            self._g1_left -= 1
+            if self._g1_left == 0:
                 self._launch_inverse_G1()
+
+    def _build_factor_groups(self) -> None:
+        """One FactorGroup per fusion group from the shapes recorded by the per-layer path."""
+        if any(r is None for k in ("A", "G") for r in self._rec[k]):
+            return
+        groups = {}
+        for kind, plan in (("A", self.fwd_plan), ("G", self.bwd_plan)):
+            buf = self.bufA if kind == "A" else self.bufG
+            out = []
+            for g in plan.groups:
+                idx = [t.layer_index - 1 for t in g]
+                members, packed, scales, keys, member = [], [], [], {}, {}
+                for k, li in enumerate(idx):
+                    key, geo, scale = self._rec[kind][li]
+                    l = self.layers[li]
+                    off, d = (l.a_off, l.spec.a_dim) if kind == "A" else (l.g_off, l.spec.g_dim)
+                    members.append(geo)
+                    packed.append(buf[off:off + d * (d + 1) // 2])
+                    scales.append(scale)
+                    keys[li] = key
+                    member[li] = k
+                out.append({"obj": FactorGroup(members, packed, scales), "keys": keys, "member": member, "seen": 0,
+                            "pending": False, "staged": torch.cuda.Event(), "done": torch.cuda.Event()})
+            groups[kind] = out
+        torch.cuda.current_stream(self.device).synchronize()
+        self._fgroups = groups
+        for l in self.layers:  # the per-layer staging buffers are no longer needed
+            l.a_plan = l.g_plan = None
+            l.a_key = l.g_key = ()
 
     def _tl(self, name: str, stream) -> None:
         if self.timeline is not None and not torch.cuda.is_current_stream_capturing():
@@ -370,7 +436,7 @@ class SPDKFAC(torch.optim.Optimizer):
         if self.world > 1:
             s.wait_stream(self.comm_stream)
         self._tl("a_factors_done", s)
-        self._run_inverse("A", s)
+        self._run_inverse("A", s, exchange=False)  # broadcast in step(), after the all-reduces
         self._tl("a_inverse_done", s)
         self._a_inverted = True
 
@@ -383,11 +449,11 @@ class SPDKFAC(torch.optim.Optimizer):
         s.wait_stream(self.factor_stream)
         if self.world > 1:
             s.wait_stream(self.comm_stream)
-        self._run_inverse("G1", s)
+        self._run_inverse("G1", s, exchange=False)
         self._tl("g1_inverse_done", s)
         self._g1_inverted = True
 
-    def _run_inverse(self, side: str, stream) -> None:
+    def _run_inverse(self, side: str, stream, exchange: bool = True) -> None:
         plan = self._inv_plans[side]
         if plan is not None:
             plan.run(self.damping, stream)
@@ -396,7 +462,7 @@ class SPDKFAC(torch.optim.Optimizer):
                 ev = torch.cuda.Event()
                 ev.record(stream)
                 self._info_events.append((ev, side, self.steps))
-        if self.world > 1:
+        if self.world > 1 and exchange:
             self._exchange_inverses(side, stream)
 
     def _make_a_hook(self, l: _Layer):
@@ -456,10 +522,13 @@ class SPDKFAC(torch.optim.Optimizer):
                 self._launch_inverse_A()
             if not self._g1_inverted:
                 self._launch_inverse_G1()
-            self._run_inverse("G2", main)
+            self._run_inverse("G2", main, exchange=False)
             self._tl("g_inverse_done", main)
-            main.wait_stream(self.inv_stream)   # A inverses (and their broadcasts) landed
+            main.wait_stream(self.inv_stream)   # A inverses landed
             main.wait_stream(self.inv_stream2)  # G1 likewise
+            if self.world > 1:
+                for side in ("A", "G1", "G2"):
+                    self._exchange_inverses(side, main)
             self._tl("inverses_joined", main)
         # precondition + update for every K-FAC layer (mean gradient = sum / P); the pointer
         # tables are rebuilt only when a gradient's storage changes (zero_grad(set_to_none=True))
@@ -485,9 +554,11 @@ class SPDKFAC(torch.optim.Optimizer):
         self._a_inverted = False
         self._g_count = 0
         self._g1_inverted = False
-        if self.world > 1:
-            for k in ("A", "G"):
-                self._gseen[k] = [0] * len(self._gseen[k])
+        self._g1_left = len(self._g1_groups)
+        for k in ("A", "G"):
+            self._gseen[k] = [0] * len(self._gseen[k])
+        if self._fgroups is None and not capturing and factors_now:
+            self._build_factor_groups()
         if not capturing:  # a captured step is counted per replay (_after_replay)
             self.steps += 1
             self._capture = self.steps % self.factor_update_freq == 0
@@ -514,13 +585,13 @@ class SPDKFAC(torch.optim.Optimizer):
                                                        L.ptr_array([self.inv[t].data_ptr() for t in ct]),
                                                        L.ptr_array([v.data_ptr() for v in views]),
                                                        main.cuda_stream), "pack inverses")
-        bs = self.bcast_stream
-        bs.wait_stream(main)
-        with self.comm_bc.group():
+        cs = self.comm_stream
+        cs.wait_stream(main)
+        with self.comm.group():
             for root, (ct_r, _, buf_r, _, n_r) in enumerate(lay):
                 if n_r:
-                    self.comm_bc.bcast(buf_r[:n_r], root, bs)
-        main.wait_stream(bs)
+                    self.comm.bcast(buf_r[:n_r], root, cs)
+        main.wait_stream(cs)
         for root, (ct_r, dims_r, _, views_r, n_r) in enumerate(lay):
             if root == self.rank or not ct_r:
                 continue
