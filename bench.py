@@ -64,6 +64,8 @@ def parse():
                    help="activation/weight memory format of the model (cuDNN runs NHWC natively on B200)")
     p.add_argument("--mode", choices=("graph", "eager"), default="graph",
                    help="graph: the whole step (fwd, bwd, K-FAC step) replayed as one CUDA graph")
+    p.add_argument("--main-priority", type=int, default=0,
+                   help="CUDA priority of the forward/backward stream (negative = higher than the K-FAC side streams)")
     p.add_argument("--clocks", choices=("nvml", "smi", "off"), default="nvml")
     p.add_argument("--timeline", action="store_true", help="diagnostic: per-phase CUDA-event timeline of one eager step")
     p.add_argument("--stats-off", action="store_true", help="no per-launch CUDA events in the timed region (diagnostic)")
@@ -256,7 +258,8 @@ def run_ours(a):
         from paper_2107_06533_b200.graph import GraphedStep
         gs = GraphedStep(model, crit, opt, [xs[0]], [ys[0]], warmup=a.warmup,
                          before_capture=lambda: _lib.stats_reset(
-                             timing=() if a.stats_off else ("factor_syrk",), reserve=400))
+                             timing=() if a.stats_off else ("factor_syrk",), reserve=400),
+                         priority=a.main_priority)
         eager_step = step
 
         def step(i, x=None, y=None):

@@ -120,6 +120,11 @@ static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi
     int dev = 0;
     SPD_CUDA(cudaGetDevice(&dev));
     SPD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // optional cap on the persistent grid (leaves SMs to concurrent streams); diagnostics
+    if (const char* e = getenv("SPDKFAC_MAX_CTAS")) {
+      const int cap = atoi(e);
+      if (cap > 0 && cap < sms) sms = cap;
+    }
   }
   const int grid = n < sms ? n : sms;
   tc3_gemm_kernel<K, kSt, kCTile><<<grid, 192, smem, s>>>(maps, items, epis, run, n);

@@ -21,7 +21,8 @@ import torch
 
 class GraphedStep:
     def __init__(self, model: torch.nn.Module, loss_fn: Callable, optimizer, inputs: Sequence[torch.Tensor],
-                 targets: Sequence[torch.Tensor], warmup: int = 3, before_capture: Callable | None = None):
+                 targets: Sequence[torch.Tensor], warmup: int = 3, before_capture: Callable | None = None,
+                 priority: int = 0):
         from .optimizer import SPDKFAC
         if isinstance(optimizer, SPDKFAC) and (optimizer.factor_update_freq != 1 or optimizer.inv_update_freq != 1):
             raise ValueError("GraphedStep captures one step type: factor_update_freq and inv_update_freq must be 1")
@@ -29,7 +30,8 @@ class GraphedStep:
         self.static_in = [t.detach().clone() for t in inputs]
         self.static_tg = [t.detach().clone() for t in targets]
         cur = torch.cuda.current_stream()
-        side = torch.cuda.Stream()
+        side = torch.cuda.Stream(priority=priority)
+        self.stream = side
         side.wait_stream(cur)
         with torch.cuda.stream(side):
             for _ in range(max(1, warmup)):
@@ -39,7 +41,7 @@ class GraphedStep:
         if before_capture is not None:
             before_capture()
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
+        with torch.cuda.graph(self.graph, stream=side if priority else None):
             self.static_loss = self._body()
         torch.cuda.synchronize()
 
