@@ -134,6 +134,19 @@ SPD_DEV uint64_t make_sdesc_sw128(const void* smem_tile) {
   return desc;
 }
 
+// MN-major operand (the MN index contiguous), SWIZZLE_128B: 64 MN elements (128 B) x 8 K rows
+// per 1024-B atom; atoms along K every 1024 B (SBO), the second 64-wide MN half at +LBO.
+// A 128 (MN) x 64 (K) bf16 tile is two TMA boxes of 64 x 64 (8 KB each): LBO = 8192.
+SPD_DEV uint64_t make_sdesc_sw128_mn(const void* smem_tile) {
+  uint64_t addr = (smem_u32(smem_tile) & 0x3FFFFu) >> 4;
+  uint64_t desc = addr;
+  desc |= uint64_t(8192 >> 4) << 16;     // LBO: MN atom stride
+  desc |= uint64_t(1024 >> 4) << 32;     // SBO: 8-row K group stride
+  desc |= uint64_t(1) << 46;             // version
+  desc |= uint64_t(2) << 61;             // SWIZZLE_128B
+  return desc;
+}
+
 template <Kind K>
 SPD_DEV void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
   if constexpr (K == Kind::BF16) {

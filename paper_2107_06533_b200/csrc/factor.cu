@@ -2,8 +2,8 @@
 // or spatial output-gradient rows (conv G), on tcgen05 with 3 x bf16 split operands.
 //
 // Pipeline per factor (one plan = one layer-side):
-//   1. stage kernel  : gather rows of X into the K-major split operand Xt[2][d][Mpad] (bf16 hi/lo)
-//                      -- the im2col / layout transform and the precision split in one HBM pass
+//   1. stage kernel  : rows of X (im2col patches for conv A) split into bf16 hi/lo planes
+//                      Xs[2][M][ld] in their natural row order -- one streaming HBM pass
 //   2. tc3 GEMM      : upper-triangle 128x128 tiles (I <= J) x split-K slices, partial tiles to ws
 //   3. reduce + pack : sum split-K partials in fixed order, apply 1/M, running average, 1/P,
 //                      write the packed upper triangle (the all-reduce / fusion-buffer format)
@@ -14,205 +14,224 @@
 namespace spd {
 
 // ------------------------------------------------------------------ staging kernels
-// Xt[r][m] (r < d, m < Mpad) ; planes hi at 0, lo at d*Mpad.  Zero for m >= M.
-
-__device__ __forceinline__ void store_split2(__nv_bfloat16* xt, int64_t plane, int64_t o, float v0, float v1);
-
-// [M][d] rows (row stride ldx) -> K-major split planes Xt[2][d][Mpad].  64(m) x 32(r) tiles
-// through shared memory: 128-B reads along r, bf16x2 (128-B per warp) writes along m.
-__global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict__ x, int64_t M, int64_t d,
-                                                         int64_t ldx, __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
-  __shared__ float tile[64][33];
-  const int64_t m0 = int64_t(blockIdx.x) * 64, r0 = int64_t(blockIdx.y) * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-#pragma unroll
-  for (int k = ty; k < 64; k += 8) {
-    const int64_t m = m0 + k, r = r0 + tx;
-    tile[k][tx] = (m < M && r < d) ? __ldg(x + m * ldx + r) : 0.f;
-  }
-  __syncthreads();
-  const int64_t plane = d * Mpad;
-#pragma unroll
-  for (int k = ty; k < 32; k += 8) {
-    const int64_t r = r0 + k, m = m0 + 2 * tx;
-    if (r < d && m < Mpad) store_split2(xt, plane, r * Mpad + m, tile[2 * tx][k], tile[2 * tx + 1][k]);
-  }
-}
+// Xs[p][m][j]: plane p (hi, lo), row m < M (one sample / output position), column j < ld
+// (ld = d rounded up to 8; columns [d, ld) are zero).  Rows are the natural order of the
+// activations, so staging is a streaming split (plus the im2col gather for conv A) with no
+// transpose; the tcgen05 kernel reads the planes as MN-major operands (kMnMajor).
 
 struct ConvGeom {
   int B, C, H, W, Ho, Wo, kh, kw, sh, sw, ph, pw, dh, dw;
 };
 
-__device__ __forceinline__ void store_split2(__nv_bfloat16* xt, int64_t plane, int64_t o, float v0, float v1) {
+__device__ __forceinline__ uint32_t pack_bf16x2(__nv_bfloat16 a, __nv_bfloat16 b) {
+  __nv_bfloat162 v = __halves2bfloat162(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void store_split4(__nv_bfloat16* xs, int64_t plane, int64_t o, float4 v) {
+  __nv_bfloat16 h[4], l[4];
+  split_bf16(v.x, h[0], l[0]);
+  split_bf16(v.y, h[1], l[1]);
+  split_bf16(v.z, h[2], l[2]);
+  split_bf16(v.w, h[3], l[3]);
+  uint2 hv, lv;
+  hv.x = pack_bf16x2(h[0], h[1]), hv.y = pack_bf16x2(h[2], h[3]);
+  lv.x = pack_bf16x2(l[0], l[1]), lv.y = pack_bf16x2(l[2], l[3]);
+  *reinterpret_cast<uint2*>(xs + o) = hv;
+  *reinterpret_cast<uint2*>(xs + plane + o) = lv;
+}
+
+__device__ __forceinline__ void store_split2(__nv_bfloat16* xs, int64_t plane, int64_t o, float v0, float v1) {
   __nv_bfloat16 h0, l0, h1, l1;
   split_bf16(v0, h0, l0);
   split_bf16(v1, h1, l1);
-  *reinterpret_cast<__nv_bfloat162*>(xt + o) = __halves2bfloat162(h0, h1);
-  *reinterpret_cast<__nv_bfloat162*>(xt + plane + o) = __halves2bfloat162(l0, l1);
+  *reinterpret_cast<__nv_bfloat162*>(xs + o) = __halves2bfloat162(h0, h1);
+  *reinterpret_cast<__nv_bfloat162*>(xs + plane + o) = __halves2bfloat162(l0, l1);
 }
 
-// One block per (patch row r = (c, ki, kj), image b): threads walk the output positions of
-// image b two at a time (bf16x2 stores), 32-bit index math, one division per pair.
-__global__ void __launch_bounds__(256) stage_im2col_kernel(const float* __restrict__ x, ConvGeom g, int64_t M,
-                                                           int64_t d, __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
-  const int r = blockIdx.y;
-  const int b = blockIdx.x;
-  const int kj = r % g.kw, ki = (r / g.kw) % g.kh, c = r / (g.kw * g.kh);
-  const int HWo = g.Ho * g.Wo;
-  const int64_t plane = d * Mpad;
-  const int64_t row = int64_t(r) * Mpad + int64_t(b) * HWo;  // m = b*HWo + hw
-  const float* xc = x + (int64_t(b) * g.C + c) * g.H * g.W;
-  const int hoff = ki * g.dh - g.ph, woff = kj * g.dw - g.pw;
-  // HWo may be odd (7x7): pair (hw, hw+1) when both in range, row offsets are then even
-  // only if b*HWo is even; fall back to scalar stores otherwise.
-  const bool vec = ((int64_t(b) * HWo) & 1) == 0 && (Mpad & 1) == 0;
-  if (vec) {
-    for (int hw = 2 * threadIdx.x; hw < HWo; hw += 2 * blockDim.x) {
-      float v[2];
+// rows x[m][0..d) (row stride ldx) -> Xs.  Block = kStageRows rows; thread (row lane, column
+// slot) as in the im2col kernel below (no per-element index division).  kVec: ldx % 4 == 0,
+// d % 4 == 0, x 16-B aligned -> float4 loads, 2 x 8-B stores.
+constexpr int kStageRows = 32;
+
+template <bool kVec>
+__global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict__ x, int64_t M, int64_t d,
+                                                         int64_t ldx, __nv_bfloat16* __restrict__ xs, int64_t ld,
+                                                         int tpr, int cps) {
+  const int64_t plane = M * ld;
+  constexpr int kW = kVec ? 4 : 2;
+  const int64_t m0 = int64_t(blockIdx.x) * kStageRows;
+  const int ncol = int(ld / kW), rpar = int(blockDim.x) / tpr;
+  const int cs0 = int(threadIdx.x) % tpr, r0 = int(threadIdx.x) / tpr;
+  const int rows = int(M - m0 < kStageRows ? M - m0 : int64_t(kStageRows));
+  const int cs_end = min(ncol, int(blockIdx.y + 1) * cps);
+  for (int cs = int(blockIdx.y) * cps + cs0; cs < cs_end; cs += tpr) {
+    const int j = cs * kW;
+    for (int rb = r0; rb < rows; rb += 4 * rpar) {  // 4 rows per pass: loads first, then stores
+      float4 val[4];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int q = hw + u;
-        v[u] = 0.f;
-        if (q < HWo) {
-          const int ho = q / g.Wo, wo = q - ho * g.Wo;
-          const int hi = ho * g.sh + hoff, wi = wo * g.sw + woff;
-          if (hi >= 0 && hi < g.H && wi >= 0 && wi < g.W) v[u] = __ldg(xc + hi * g.W + wi);
+      for (int u = 0; u < 4; ++u) {
+        const int r = rb + u * rpar;
+        const float* src = x + (m0 + r) * ldx + j;
+        val[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < rows) {
+          if constexpr (kVec) {
+            if (j < d) val[u] = __ldg(reinterpret_cast<const float4*>(src));
+          } else {
+            if (j < d) val[u].x = __ldg(src);
+            if (j + 1 < d) val[u].y = __ldg(src + 1);
+          }
         }
       }
-      if (hw + 1 < HWo) {
-        store_split2(xt, plane, row + hw, v[0], v[1]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = rb + u * rpar;
+        if (r < rows) {
+          if constexpr (kVec)
+            store_split4(xs, plane, (m0 + r) * ld + j, val[u]);
+          else
+            store_split2(xs, plane, (m0 + r) * ld + j, val[u].x, val[u].y);
+        }
+      }
+    }
+  }
+}
+
+// launch shape for M rows of ncol column slots, `rows` rows per block: enough blocks for the
+// 148 SMs (column ranges of cps slots split over blockIdx.y when M is small), tpr threads
+// per row (a multiple of 32 balancing the passes over the range), as many row lanes as fit
+// in 256 threads.
+struct RowShape {
+  dim3 grid;
+  int tpr, threads, cps;
+};
+inline RowShape row_shape(int64_t M, int64_t ncol, int rows) {
+  const int64_t row_blocks = cdiv(M, rows);
+  int64_t ysplit = 1;
+  if (row_blocks < 600) ysplit = std::max<int64_t>(1, std::min(cdiv(600, row_blocks), ncol / 32));
+  const int cps = int(cdiv(ncol, ysplit));
+  ysplit = cdiv(ncol, cps);
+  int tpr = cps;
+  if (cps > 32) {
+    const int passes = int(cdiv(cps, 256));
+    tpr = int(std::min<int64_t>(256, round_up(cdiv(cps, passes), 32)));
+  }
+  const int lanes = std::max(1, std::min(rows, 256 / tpr));
+  return RowShape{dim3(unsigned(row_blocks), unsigned(ysplit)), tpr, tpr * lanes, cps};
+}
+
+// im2col: block = kIm2colRows consecutive output positions.  The per-row source geometry is
+// computed once into shared memory; thread (row lane r0, column slot cs) keeps its column
+// decomposition across the rows it walks (tpr threads per row, 256/tpr rows in parallel).
+// Column order: channels-last (ki, kj, c) -- the column order of a channels-last conv weight
+// [cout][kh*kw*cin] -- or NCHW (c, ki, kj), the reference's unfold order.  kVec
+// (channels-last, C % 4 == 0): float4 loads of 4 channels, 2 x 8-B stores; otherwise column
+// pairs (bf16x2).
+constexpr int kIm2colRows = 32;
+
+template <bool kNhwc, bool kVec>
+__global__ void __launch_bounds__(256) stage_im2col_kernel(const float* __restrict__ x, ConvGeom g, int64_t M,
+                                                           int64_t d, __nv_bfloat16* __restrict__ xs, int64_t ld,
+                                                           int tpr, int cps) {
+  __shared__ int s_b[kIm2colRows], s_h[kIm2colRows], s_w[kIm2colRows];
+  const int64_t m0 = int64_t(blockIdx.x) * kIm2colRows;
+  if (threadIdx.x < kIm2colRows) {
+    const int64_t m = m0 + threadIdx.x;
+    int b = -1, h = 0, w = 0;
+    if (m < M) {
+      const int HWo = g.Ho * g.Wo;
+      b = int(m / HWo);
+      const int q = int(m - int64_t(b) * HWo), ho = q / g.Wo, wo = q - ho * g.Wo;
+      h = ho * g.sh - g.ph;
+      w = wo * g.sw - g.pw;
+    }
+    s_b[threadIdx.x] = b, s_h[threadIdx.x] = h, s_w[threadIdx.x] = w;
+  }
+  __syncthreads();
+  const int64_t plane = M * ld;
+  constexpr int kW = kVec ? 4 : 2;
+  const int kk_n = g.kh * g.kw;
+  const int ncol = int(ld / kW), rpar = int(blockDim.x) / tpr;
+  const int cs0 = int(threadIdx.x) % tpr, r0 = int(threadIdx.x) / tpr;
+  const int rows = int(M - m0 < kIm2colRows ? M - m0 : int64_t(kIm2colRows));
+  const int cs_end = min(ncol, int(blockIdx.y + 1) * cps);
+  for (int cs = int(blockIdx.y) * cps + cs0; cs < cs_end; cs += tpr) {
+    const int j = cs * kW;
+    int ki[2], kj[2], c[2];
+    bool valid[2];
+#pragma unroll
+    for (int u = 0; u < (kVec ? 1 : 2); ++u) {
+      const int jj = j + u;
+      valid[u] = jj < d;
+      int kk, cc;
+      if (kNhwc) {
+        kk = jj / g.C;
+        cc = jj - kk * g.C;
       } else {
-        __nv_bfloat16 h, l;
-        split_bf16(v[0], h, l);
-        xt[row + hw] = h;
-        xt[plane + row + hw] = l;
+        cc = jj / kk_n;
+        kk = jj - cc * kk_n;
       }
+      ki[u] = kk / g.kw;
+      kj[u] = kk - ki[u] * g.kw;
+      c[u] = cc;
     }
-  } else {
-    for (int q = threadIdx.x; q < HWo; q += blockDim.x) {
-      const int ho = q / g.Wo, wo = q - ho * g.Wo;
-      const int hi = ho * g.sh + hoff, wi = wo * g.sw + woff;
-      float v = 0.f;
-      if (hi >= 0 && hi < g.H && wi >= 0 && wi < g.W) v = __ldg(xc + hi * g.W + wi);
-      __nv_bfloat16 h, l;
-      split_bf16(v, h, l);
-      xt[row + q] = h;
-      xt[plane + row + q] = l;
+    for (int rb = r0; rb < rows; rb += 4 * rpar) {  // 4 rows per pass: loads first, then stores
+      float4 val[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = rb + u * rpar;
+        val[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r >= rows) continue;
+        const int b = s_b[r];
+        if constexpr (kVec) {
+          const int hi = s_h[r] + ki[0] * g.dh, wi = s_w[r] + kj[0] * g.dw;
+          if (valid[0] && hi >= 0 && hi < g.H && wi >= 0 && wi < g.W)
+            val[u] = __ldg(reinterpret_cast<const float4*>(x + ((int64_t(b) * g.H + hi) * g.W + wi) * g.C + c[0]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int hi = s_h[r] + ki[e] * g.dh, wi = s_w[r] + kj[e] * g.dw;
+            if (valid[e] && hi >= 0 && hi < g.H && wi >= 0 && wi < g.W) {
+              const int64_t off = kNhwc ? ((int64_t(b) * g.H + hi) * g.W + wi) * g.C + c[e]
+                                        : ((int64_t(b) * g.C + c[e]) * g.H + hi) * g.W + wi;
+              (e ? val[u].y : val[u].x) = __ldg(x + off);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = rb + u * rpar;
+        if (r >= rows) continue;
+        const int64_t o = (m0 + r) * ld + j;
+        if constexpr (kVec)
+          store_split4(xs, plane, o, val[u]);
+        else
+          store_split2(xs, plane, o, val[u].x, val[u].y);
+      }
     }
   }
 }
 
-// channels-last input x[b][h][w][c]; patch rows ordered (ki, kj, c) -- the column order of a
-// channels-last conv weight viewed as [cout][kh*kw*cin].  32(m) x 32(c) tiles through shared
-// memory: reads coalesced along c, bf16x2 hi/lo writes coalesced along m.
-__global__ void __launch_bounds__(256) stage_im2col_nhwc_kernel(const float* __restrict__ x, ConvGeom g, int64_t M,
-                                                                int64_t d, __nv_bfloat16* __restrict__ xt,
-                                                                int64_t Mpad) {
-  __shared__ float tile[64][33];
-  __shared__ int rowoff[64];  // element offset of (b, hi, wi, 0) for the block's 64 rows, -1 = padding
-  const int kk = blockIdx.z, ki = kk / g.kw, kj = kk - ki * g.kw;
-  const uint32_t m0 = blockIdx.x * 64u;
-  const int c0 = blockIdx.y * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  if (threadIdx.x < 64) {
-    const uint32_t m = m0 + threadIdx.x;
-    int off = -1;
-    if (m < uint32_t(M)) {
-      const uint32_t HWo = uint32_t(g.Ho) * g.Wo;
-      const uint32_t b = m / HWo, q = m - b * HWo;
-      const uint32_t ho = q / uint32_t(g.Wo), wo = q - ho * g.Wo;
-      const int hi = int(ho) * g.sh - g.ph + ki * g.dh, wi = int(wo) * g.sw - g.pw + kj * g.dw;
-      if (hi >= 0 && hi < g.H && wi >= 0 && wi < g.W) off = ((int(b) * g.H + hi) * g.W + wi) * g.C;
-    }
-    rowoff[threadIdx.x] = off;
-  }
-  __syncthreads();
-  const int c = c0 + tx;
-#pragma unroll
-  for (int r = ty; r < 64; r += 8) {
-    const int off = rowoff[r];
-    tile[r][tx] = (off >= 0 && c < g.C) ? __ldg(x + off + c) : 0.f;
-  }
-  __syncthreads();
-  const int64_t plane = d * Mpad;
-#pragma unroll
-  for (int r = ty; r < 32; r += 8) {
-    const int cc = c0 + r;
-    const int64_t m = int64_t(m0) + 2 * tx;
-    if (cc < g.C && m < Mpad)
-      store_split2(xt, plane, (int64_t(kk) * g.C + cc) * Mpad + m, tile[2 * tx][r], tile[2 * tx + 1][r]);
-  }
-}
-
-// channels-last im2col for few input channels (the stem conv: C = 3): one thread per pair of
-// output positions walks all (ki, kj, c) patch rows; bf16x2 stores stay coalesced along m and
-// the overlapping patch reads are served by L1.
-__global__ void __launch_bounds__(256) stage_im2col_nhwc_smallc_kernel(const float* __restrict__ x, ConvGeom g,
-                                                                       int64_t M, int64_t d,
-                                                                       __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
-  const int64_t m = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 2;
-  if (m >= Mpad) return;
-  const uint32_t HWo = uint32_t(g.Ho) * g.Wo;
-  int hb[2], wb[2], bo[2];
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const uint32_t mm = uint32_t(m) + u;
-    if (mm < uint32_t(M)) {
-      const uint32_t b = mm / HWo, q = mm - b * HWo;
-      const uint32_t ho = q / uint32_t(g.Wo), wo = q - ho * g.Wo;
-      bo[u] = int(b) * g.H;
-      hb[u] = int(ho) * g.sh - g.ph;
-      wb[u] = int(wo) * g.sw - g.pw;
-    } else {
-      bo[u] = -1, hb[u] = 0, wb[u] = 0;
-    }
-  }
-  const int64_t plane = d * Mpad;
-  for (int ki = 0; ki < g.kh; ++ki)
-    for (int kj = 0; kj < g.kw; ++kj) {
-      int off[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int hi = hb[u] + ki * g.dh, wi = wb[u] + kj * g.dw;
-        off[u] = (bo[u] >= 0 && hi >= 0 && hi < g.H && wi >= 0 && wi < g.W) ? ((bo[u] + hi) * g.W + wi) * g.C : -1;
-      }
-      const int64_t row0 = int64_t(ki * g.kw + kj) * g.C;
-      for (int c = 0; c < g.C; ++c) {
-        const float v0 = off[0] >= 0 ? __ldg(x + off[0] + c) : 0.f;
-        const float v1 = off[1] >= 0 ? __ldg(x + off[1] + c) : 0.f;
-        store_split2(xt, plane, (row0 + c) * Mpad + m, v0, v1);
-      }
-    }
-}
-
-// rows m = (b, hw) of channel c: a contiguous copy of g[b][c][:] per image
+// NCHW output gradients g[b][c][p] -> rows m = b*HW + p, columns c: per-image 32 x 32 transpose
 __global__ void __launch_bounds__(256) stage_spatial_kernel(const float* __restrict__ g, int C, int HW,
-                                                            __nv_bfloat16* __restrict__ xt, int64_t Mpad) {
-  const int c = blockIdx.y, b = blockIdx.x;
-  const int64_t plane = int64_t(C) * Mpad;
-  const float* src = g + (int64_t(b) * C + c) * HW;
-  const int64_t row = int64_t(c) * Mpad + int64_t(b) * HW;
-  if (((int64_t(b) * HW) & 1) == 0 && (HW & 1) == 0) {
-    for (int q = 2 * threadIdx.x; q < HW; q += 2 * blockDim.x) {
-      const float2 v = *reinterpret_cast<const float2*>(src + q);
-      store_split2(xt, plane, row + q, v.x, v.y);
-    }
-  } else {
-    for (int q = threadIdx.x; q < HW; q += blockDim.x) {
-      __nv_bfloat16 h, l;
-      split_bf16(src[q], h, l);
-      xt[row + q] = h;
-      xt[plane + row + q] = l;
-    }
+                                                            __nv_bfloat16* __restrict__ xs, int64_t M, int64_t ld) {
+  __shared__ float tile[32][33];
+  const int b = blockIdx.z, p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = ty; k < 32; k += 8) {
+    const int c = c0 + k, p = p0 + tx;
+    tile[k][tx] = (c < C && p < HW) ? __ldg(g + (int64_t(b) * C + c) * HW + p) : 0.f;
   }
-}
-
-// zero the K padding columns [M, Mpad) of every row (once per plan; never written by staging)
-__global__ void zero_pad_kernel(__nv_bfloat16* xt, int64_t d, int64_t M, int64_t Mpad) {
-  const int64_t r = blockIdx.x;
-  for (int64_t m = M + threadIdx.x; m < Mpad; m += blockDim.x) {
-    xt[r * Mpad + m] = __float2bfloat16(0.f);
-    xt[d * Mpad + r * Mpad + m] = __float2bfloat16(0.f);
+  __syncthreads();
+  const int64_t plane = M * ld;
+  // 16 column pairs per row, 16 rows per pass
+  const int pr = threadIdx.x & 15, rr = threadIdx.x >> 4;
+#pragma unroll
+  for (int k = rr; k < 32; k += 16) {
+    const int p = p0 + k, c = c0 + 2 * pr;
+    if (p < HW && c < ld) store_split2(xs, plane, (int64_t(b) * HW + p) * ld + c, tile[2 * pr][k], tile[2 * pr + 1][k]);
   }
 }
 
@@ -314,7 +333,7 @@ using namespace spd;
 // packed target and scale are supplied per run.
 struct Member {
   spdkfac_factor_geom g;
-  int64_t M, d, Mpad;
+  int64_t M, d, Mpad, ld;  // ld: row length of the staged planes (d rounded up to 8)
   int T, splits, n_tiles;
   int Ho, Wo;
   __nv_bfloat16* xt;
@@ -389,7 +408,8 @@ int member_init(Member* mb, const spdkfac_factor_geom* g) {
   mb->d = d;
   mb->Ho = Ho;
   mb->Wo = Wo;
-  mb->Mpad = round_up(M, 64);
+  mb->Mpad = round_up(M, 64);  // K blocks; rows [M, Mpad) are TMA out-of-bounds zeros
+  mb->ld = round_up(d, 8);
   mb->T = int(cdiv(d, 128));
   mb->n_tiles = mb->T * (mb->T + 1) / 2;
   mb->splits = choose_splits(mb->Mpad, mb->n_tiles);
@@ -400,7 +420,7 @@ int member_init(Member* mb, const spdkfac_factor_geom* g) {
 void group_carve(spdkfac_factor_group* G, Carve& c) {
   int items = 0, jobs = 0;
   for (Member& mb : G->m) {
-    mb.xt = c.take<__nv_bfloat16>(size_t(2) * mb.d * mb.Mpad);
+    mb.xt = c.take<__nv_bfloat16>(size_t(2) * mb.M * mb.ld);
     if (mb.splits > 1) {
       mb.partial = c.take<float>(size_t(mb.n_tiles) * mb.splits * 16384);
       mb.chunks = c.take<float>(size_t(mb.n_tiles) * 16 * cdiv(mb.splits, kChunk) * 1024);
@@ -432,7 +452,7 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
   G->flops = 0;
   for (int k = 0; k < n; ++k) {
     Member& mb = G->m[k];
-    int rc = make_operand_map(&maps[k], mb.xt, true, mb.Mpad, mb.d, mb.Mpad);
+    int rc = make_operand_map_mn(&maps[k], mb.xt, mb.ld, mb.M);
     if (rc) return rc;
     G->flops += double(mb.M) * mb.d * (mb.d + 1);
     const int64_t nkb = mb.Mpad / 64, per = cdiv(nkb, mb.splits);
@@ -450,7 +470,7 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
           it.k0 = int(kb0 * 64);
           it.nk = int(kb1 - kb0);
           it.epi = k;
-          it.flags = (I == J) ? kSameAB : 0;
+          it.flags = kMnMajor | ((I == J) ? kSameAB : 0);
           if (mb.splits > 1) {  // partial tile -> member workspace slot, reduced by reduce_pack_kernel
             it.out_r = 0;
             it.out_c = (tile_idx * mb.splits + s2) * 128;
@@ -472,10 +492,6 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
     }
     rmem[k] = RedMember{mb.partial, mb.chunks, mb.counters, packed ? packed[k] : nullptr, mb.d, mb.T, mb.splits,
                         scales ? scales[k] : 1.f, 0};
-    if (mb.Mpad > mb.M) {
-      zero_pad_kernel<<<unsigned(mb.d), 64, 0, s>>>(mb.xt, mb.d, mb.M, mb.Mpad);
-      SPD_CHECK_LAUNCH();
-    }
     if (mb.counters) SPD_CUDA(cudaMemsetAsync(mb.counters, 0, sizeof(int) * size_t(mb.n_tiles) * 16, s));
   }
   // persistent CTAs take items round-robin: longest K first balances the group
@@ -491,35 +507,41 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
 int member_stage(const Member& mb, const float* x, cudaStream_t s) {
   const spdkfac_factor_geom& g = mb.g;
   stat_begin(kCatFactorStage, s);
-  if (g.layout == SPDKFAC_ROWS || g.layout == SPDKFAC_SPATIAL_NHWC) {
-    // channels-last output gradients are rows [b*h*w][C]: the same transpose
-    const int64_t ld = g.layout == SPDKFAC_ROWS ? g.w : g.c;
-    dim3 grid(unsigned(cdiv(mb.Mpad, 64)), unsigned(cdiv(mb.d, 32)));
-    stage_rows_kernel<<<grid, 256, 0, s>>>(x, mb.M, mb.d, ld, mb.xt, mb.Mpad);
+  const bool pointwise = g.layout == SPDKFAC_CONV_A_NHWC && g.kh == 1 && g.kw == 1 && g.stride_h == 1 &&
+                         g.stride_w == 1 && g.pad_h == 0 && g.pad_w == 0;
+  if (g.layout == SPDKFAC_ROWS || g.layout == SPDKFAC_SPATIAL_NHWC || pointwise) {
+    // linear inputs [n][w] (row stride w); channels-last output gradients [b*h*w][C] and the
+    // inputs of channels-last 1x1 stride-1 convs: rows [b*h*w][C]
+    const int64_t ldx = g.layout == SPDKFAC_ROWS ? g.w : g.c;
+    const bool vec = ldx % 4 == 0 && mb.d % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const RowShape rs = row_shape(mb.M, mb.ld / (vec ? 4 : 2), kStageRows);
+    if (vec)
+      stage_rows_kernel<true><<<rs.grid, rs.threads, 0, s>>>(x, mb.M, mb.d, ldx, mb.xt, mb.ld, rs.tpr, rs.cps);
+    else
+      stage_rows_kernel<false><<<rs.grid, rs.threads, 0, s>>>(x, mb.M, mb.d, ldx, mb.xt, mb.ld, rs.tpr, rs.cps);
   } else if (g.layout == SPDKFAC_CONV_A_NHWC || g.layout == SPDKFAC_CONV_A) {
     ConvGeom cg{int(g.n), int(g.c), int(g.h), int(g.w), mb.Ho, mb.Wo, g.kh, g.kw, g.stride_h, g.stride_w,
                 g.pad_h, g.pad_w, g.dil_h, g.dil_w};
+    const bool vec = g.layout == SPDKFAC_CONV_A_NHWC && g.c % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const int64_t ncol = mb.ld / (vec ? 4 : 2);
+    const RowShape rs = row_shape(mb.M, ncol, kIm2colRows);
     if (g.layout == SPDKFAC_CONV_A_NHWC) {
-      if (g.c < 16) {
-        stage_im2col_nhwc_smallc_kernel<<<unsigned(cdiv(mb.Mpad, 512)), 256, 0, s>>>(x, cg, mb.M, mb.d, mb.xt,
-                                                                                     mb.Mpad);
-      } else {
-        dim3 grid(unsigned(cdiv(mb.Mpad, 64)), unsigned(cdiv(g.c, 32)), unsigned(g.kh * g.kw));
-        stage_im2col_nhwc_kernel<<<grid, 256, 0, s>>>(x, cg, mb.M, mb.d, mb.xt, mb.Mpad);
-      }
+      if (vec)
+        stage_im2col_kernel<true, true><<<rs.grid, rs.threads, 0, s>>>(x, cg, mb.M, mb.d, mb.xt, mb.ld, rs.tpr, rs.cps);
+      else
+        stage_im2col_kernel<true, false><<<rs.grid, rs.threads, 0, s>>>(x, cg, mb.M, mb.d, mb.xt, mb.ld, rs.tpr,
+                                                                        rs.cps);
     } else {
-      const int hwo = mb.Ho * mb.Wo;
-      dim3 grid(unsigned(g.n), unsigned(mb.d));
-      stage_im2col_kernel<<<grid, hwo >= 512 ? 256 : (hwo >= 128 ? 64 : 32), 0, s>>>(x, cg, mb.M, mb.d, mb.xt,
-                                                                                      mb.Mpad);
+      stage_im2col_kernel<false, false><<<rs.grid, rs.threads, 0, s>>>(x, cg, mb.M, mb.d, mb.xt, mb.ld, rs.tpr,
+                                                                        rs.cps);
     }
   } else {
     const int hw = int(g.h * g.w);
-    dim3 grid(unsigned(g.n), unsigned(mb.d));
-    stage_spatial_kernel<<<grid, hw >= 512 ? 256 : (hw >= 128 ? 64 : 32), 0, s>>>(x, int(g.c), hw, mb.xt, mb.Mpad);
+    dim3 grid(unsigned(cdiv(hw, 32)), unsigned(cdiv(mb.ld, 32)), unsigned(g.n));
+    stage_spatial_kernel<<<grid, 256, 0, s>>>(x, int(g.c), hw, mb.xt, mb.M, mb.ld);
   }
   SPD_CHECK_LAUNCH();
-  stat_end(kCatFactorStage, s, 0, double(mb.M) * mb.d * 4 + 4.0 * mb.d * mb.Mpad);
+  stat_end(kCatFactorStage, s, 0, double(mb.M) * mb.d * 4 + 4.0 * mb.ld * mb.M);
   return SPDKFAC_OK;
 }
 
@@ -531,7 +553,7 @@ int group_compute(spdkfac_factor_group* G, float scale, float decay, float world
   int rc = launch_tc3(Kind::BF16, G->maps, G->items, G->epis, G->n_items, s, run);
   if (rc) return rc;
   double bytes = 0;
-  for (const Member& mb : G->m) bytes += 4.0 * mb.d * mb.Mpad;
+  for (const Member& mb : G->m) bytes += 4.0 * mb.ld * mb.M;
   stat_end(kCatFactorSyrk, s, G->flops, bytes);
   if (G->n_jobs == 0) return SPDKFAC_OK;
   dim3 rgrid(16, unsigned(G->n_jobs), unsigned(G->max_chunks));

@@ -105,6 +105,22 @@ int make_operand_map(CUtensorMap* out, const void* base, bool bf16, int64_t k_ex
   return SPDKFAC_OK;
 }
 
+int make_operand_map_mn(CUtensorMap* out, const void* base, int64_t ld, int64_t k_rows) {
+  EncodeTiledFn fn = encode_fn();
+  SPD_ARG(fn != nullptr, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  SPD_ARG((ld * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0, SPDKFAC_ERR_ARG,
+          "tensor map: misaligned operand");
+  cuuint64_t dims[3] = {cuuint64_t(ld), cuuint64_t(k_rows), 2};
+  cuuint64_t strides[2] = {cuuint64_t(ld * 2), cuuint64_t(ld * 2 * k_rows)};
+  cuuint32_t box[3] = {64, 64, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SPD_ARG(r == CUDA_SUCCESS, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return SPDKFAC_OK;
+}
+
 template <Kind K, int kSt, bool kCTile>
 static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
                        const TcRun& run) {

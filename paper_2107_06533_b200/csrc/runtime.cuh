@@ -61,6 +61,8 @@ struct Carve {
 // 3-D tensor map over a split-precision operand: planes [2][rows][ld] with K (= ld
 // axis, extent k_extent) innermost; box = {128 B of K, 128 rows, 1 plane}, SWIZZLE_128B.
 int make_operand_map(CUtensorMap* out, const void* base, bool bf16, int64_t k_extent, int64_t rows, int64_t ld);
+// MN-major bf16 split planes [2][k_rows][ld] (box 64 x 64, SWIZZLE_128B; items flagged kMnMajor)
+int make_operand_map_mn(CUtensorMap* out, const void* base, int64_t ld, int64_t k_rows);
 
 // Upload `n` POD objects into device memory `dst` on `stream` (pageable source: the
 // copy consumes the host buffer before returning).

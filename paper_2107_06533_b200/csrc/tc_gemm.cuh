@@ -32,6 +32,8 @@ struct TcItem {
 };
 constexpr int32_t kSameAB = 1;  // B tile == A tile (diagonal SYRK tile): load once
 constexpr int32_t kMirror = 2;  // also update target (out_r + i, out_c + j) (symmetric off-diagonal tile)
+constexpr int32_t kMnMajor = 8;  // operands are MN-major split planes [2][K][ld] (bf16 only): each
+                                 // 16-KB tile is two 64(MN) x 64(K) TMA boxes at (row, k), (row + 64, k)
 constexpr int32_t kOut2Rows = 4;  // out2 row-style: out2[(o2_row + i) * ld2 + j]; else transposed:
                                   // out2[(o2_row + j) * ld2 + i] (coalesced along the TMEM lanes)
 
@@ -240,11 +242,23 @@ __global__ void __launch_bounds__(192, 1)
           mbar_expect_tx(&full[s], bytes);
           uint8_t* st = smem + s * kStageBytes;
           const int kc = it.k0 + kb * BK;
-          tma_load_3d(st, am, &full[s], kc, it.a_row, 0);
-          tma_load_3d(st + kTileBytes, am, &full[s], kc, it.a_row, 1);
-          if (!same) {
-            tma_load_3d(st + 2 * kTileBytes, bm, &full[s], kc, it.b_row, 0);
-            tma_load_3d(st + 3 * kTileBytes, bm, &full[s], kc, it.b_row, 1);
+          if (it.flags & kMnMajor) {
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+              tma_load_3d(st + p * kTileBytes, am, &full[s], it.a_row, kc, p);
+              tma_load_3d(st + p * kTileBytes + kTileBytes / 2, am, &full[s], it.a_row + 64, kc, p);
+              if (!same) {
+                tma_load_3d(st + (2 + p) * kTileBytes, bm, &full[s], it.b_row, kc, p);
+                tma_load_3d(st + (2 + p) * kTileBytes + kTileBytes / 2, bm, &full[s], it.b_row + 64, kc, p);
+              }
+            }
+          } else {
+            tma_load_3d(st, am, &full[s], kc, it.a_row, 0);
+            tma_load_3d(st + kTileBytes, am, &full[s], kc, it.a_row, 1);
+            if (!same) {
+              tma_load_3d(st + 2 * kTileBytes, bm, &full[s], kc, it.b_row, 0);
+              tma_load_3d(st + 3 * kTileBytes, bm, &full[s], kc, it.b_row, 1);
+            }
           }
         }
         if constexpr (kCTile) {  // target tile of this item, after the previous tile was stored
@@ -260,7 +274,8 @@ __global__ void __launch_bounds__(192, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
-      constexpr uint32_t idesc = make_idesc<K>(128, 128);
+      constexpr uint32_t idesc_k = make_idesc<K>(128, 128);
+      constexpr uint32_t idesc_mn = idesc_k | (1u << 15) | (1u << 16);  // transpose A and B
       uint32_t g = 0, t = 0;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
         const TcItem it = items[item];
@@ -274,16 +289,30 @@ __global__ void __launch_bounds__(192, 1)
           mbar_wait(&full[s], (g / kSt) & 1);
           tc_fence_after();
           uint8_t* st = smem + s * kStageBytes;
-          const uint64_t ahi = make_sdesc_sw128(st);
-          const uint64_t alo = make_sdesc_sw128(st + kTileBytes);
-          const uint64_t bhi = same ? ahi : make_sdesc_sw128(st + 2 * kTileBytes);
-          const uint64_t blo = same ? alo : make_sdesc_sw128(st + 3 * kTileBytes);
+          if (K == Kind::BF16 && (it.flags & kMnMajor)) {
+            const uint64_t ahi = make_sdesc_sw128_mn(st);
+            const uint64_t alo = make_sdesc_sw128_mn(st + kTileBytes);
+            const uint64_t bhi = same ? ahi : make_sdesc_sw128_mn(st + 2 * kTileBytes);
+            const uint64_t blo = same ? alo : make_sdesc_sw128_mn(st + 3 * kTileBytes);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 B of K per 128-B swizzle row
-            const uint64_t off = uint64_t(kk * 2);
-            umma<K>(acc, ahi + off, bhi + off, idesc, (kb | kk) != 0);
-            umma<K>(acc, ahi + off, blo + off, idesc, 1u);
-            umma<K>(acc, alo + off, bhi + off, idesc, 1u);
+            for (int kk = 0; kk < 4; ++kk) {  // 16 K rows = two 1024-B atoms per instruction
+              const uint64_t off = uint64_t(kk * (2048 >> 4));
+              umma<K>(acc, ahi + off, bhi + off, idesc_mn, (kb | kk) != 0);
+              umma<K>(acc, ahi + off, blo + off, idesc_mn, 1u);
+              umma<K>(acc, alo + off, bhi + off, idesc_mn, 1u);
+            }
+          } else {
+            const uint64_t ahi = make_sdesc_sw128(st);
+            const uint64_t alo = make_sdesc_sw128(st + kTileBytes);
+            const uint64_t bhi = same ? ahi : make_sdesc_sw128(st + 2 * kTileBytes);
+            const uint64_t blo = same ? alo : make_sdesc_sw128(st + 3 * kTileBytes);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 B of K per 128-B swizzle row
+              const uint64_t off = uint64_t(kk * 2);
+              umma<K>(acc, ahi + off, bhi + off, idesc_k, (kb | kk) != 0);
+              umma<K>(acc, ahi + off, blo + off, idesc_k, 1u);
+              umma<K>(acc, alo + off, bhi + off, idesc_k, 1u);
+            }
           }
           tc_commit(&empty[s]);  // smem slot free once these MMAs retire
         }

@@ -275,7 +275,10 @@ class SPDKFAC(torch.optim.Optimizer):
             return L.ROWS, x.reshape(-1, x.shape[-1])
         cl = torch.channels_last
         if kind == "A":
-            if l.w_cl:
+            pointwise = tuple(l.module.kernel_size) == (1, 1)
+            if l.w_cl or (pointwise and not x.is_contiguous() and x.is_contiguous(memory_format=cl)):
+                # 1x1 kernels: (kh, kw, c) and (c, kh, kw) are the same column order, so a
+                # channels-last input is staged as rows whatever the weight's memory format
                 return L.CONV_A_NHWC, x.contiguous(memory_format=cl)
             return L.CONV_A, x.contiguous()
         if x.is_contiguous():

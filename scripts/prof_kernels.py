@@ -66,6 +66,57 @@ if what == "inverse_single":
         timed(lambda: plan.run(0.1), f"single inverse d={d}")
         report(reps + 1)
 
+if what == "stage":  # every ResNet-50 bs32 layer side, channels-last, staging and SYRK timed apart
+    from paper_2107_06533_b200.workloads import build_model
+    model = build_model("resnet50").to(dev).to(memory_format=torch.channels_last)
+    recs = []
+
+    def hook(m, inp, out):
+        recs.append((m, inp[0].detach(), out.detach()))
+
+    hs = [m.register_forward_hook(hook) for m in model.modules() if isinstance(m, (torch.nn.Conv2d, torch.nn.Linear))]
+    with torch.no_grad():
+        model(torch.randn(32, 3, 224, 224, device=dev).contiguous(memory_format=torch.channels_last))
+    for h in hs:
+        h.remove()
+    tot_stage = tot_syrk = tot_bytes = 0.0
+    for m, x, y in recs:
+        for side in ("A", "G"):
+            if isinstance(m, torch.nn.Conv2d):
+                if side == "A":
+                    t = x.contiguous(memory_format=torch.channels_last)
+                    plan = FactorPlan(L.CONV_A_NHWC, t.shape, m.kernel_size, m.stride, m.padding, m.dilation)
+                else:
+                    t = torch.randn_like(y).contiguous(memory_format=torch.channels_last)
+                    plan = FactorPlan(L.SPATIAL_NHWC, t.shape)
+            else:
+                t = (x if side == "A" else torch.randn_like(y)).contiguous()
+                plan = FactorPlan(L.ROWS, t.shape)
+            packed = torch.zeros(plan.packed_size, device=dev)
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            plan.stage(t)
+            plan.compute(packed, 1.0)
+            torch.cuda.synchronize()
+            e[0].record()
+            for _ in range(reps):
+                plan.stage(t)
+            e[1].record()
+            for _ in range(reps):
+                plan.compute(packed, 1.0)
+            e[2].record()
+            torch.cuda.synchronize()
+            st, sy = e[0].elapsed_time(e[1]) / reps, e[1].elapsed_time(e[2]) / reps
+            ld = (plan.dim + 7) // 8 * 8
+            nbytes = plan.rows * ld * 4 + t.numel() * 4
+            tot_stage += st
+            tot_syrk += sy
+            tot_bytes += nbytes
+            print(f"{side} {tuple(t.shape)} k={getattr(m, 'kernel_size', '-')} M={plan.rows} d={plan.dim}: "
+                  f"stage {st * 1e3:7.1f} us ({nbytes / st / 1e6:6.0f} GB/s)  syrk {sy * 1e3:7.1f} us "
+                  f"({plan.rows * plan.dim * (plan.dim + 1) / sy / 1e9:6.1f} TF/s)", flush=True)
+            del plan
+    print(f"total stage {tot_stage:.3f} ms ({tot_bytes / tot_stage / 1e6:.0f} GB/s), syrk {tot_syrk:.3f} ms")
+
 if what in ("factor", "all"):
     L.stats_reset(timing=True)
     for label, shp, layout, k in [("A layer4 conv2 (M=1568, d=4608)", (32, 512, 7, 7), L.CONV_A, 3),
