@@ -286,43 +286,52 @@ struct PanelJob {
 
 // Old column panel Wold[R, K] -> tf32 hi/lo planes panA[prow(R) + i][j].  Only the upper
 // block triangle of W is maintained, so blocks below the pivot (R > K) are read as
-// W[K, R]^T through a shared-memory transpose.
+// W[K, R]^T through a shared-memory transpose.  Block (job, quarter q) writes panel rows
+// [32q, 32q + 32); every thread issues all of its loads before its first store.
 __global__ void __launch_bounds__(256) stage_panel_kernel(const InvMat* __restrict__ mats,
                                                           const PanelJob* __restrict__ jobs, int k,
                                                           float* __restrict__ panA, int64_t plane) {
-  __shared__ float tile[32][33];
+  __shared__ float tile[128][33];
   const PanelJob jb = jobs[blockIdx.x];
   const InvMat m = mats[jb.mat];
   if (*m.info != 0) return;
+  const int q = blockIdx.y;
   const int64_t dp = m.dp, K0 = int64_t(k) * kB, R0 = int64_t(jb.rb) * kB;
-  float* dst = panA + (int64_t(m.panel_row0) + R0) * kB;
+  float* dst = panA + (int64_t(m.panel_row0) + R0 + 32 * q) * kB;
+  const float* __restrict__ W = m.W;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  if (jb.rb < k) {
-    for (int e = threadIdx.x; e < kB * kB / 4; e += blockDim.x) {
-      const int i = e >> 5, c = (e & 31) * 4;
-      const float4 v = *reinterpret_cast<const float4*>(m.W + (R0 + i) * dp + K0 + c);
+  if (jb.rb < k) {  // rows R0 + 32q + i, columns K0 + c: 32 x 128 floats, 4 float4 per thread
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + 256 * u, i = e >> 5, c = (e & 31) * 4;
+      v[u] = __ldcg(reinterpret_cast<const float4*>(W + (R0 + 32 * q + i) * dp + K0 + c));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + 256 * u, i = e >> 5, c = (e & 31) * 4;
       float h[4], l[4];
-      split_tf32(v.x, h[0], l[0]);
-      split_tf32(v.y, h[1], l[1]);
-      split_tf32(v.z, h[2], l[2]);
-      split_tf32(v.w, h[3], l[3]);
+      split_tf32(v[u].x, h[0], l[0]);
+      split_tf32(v[u].y, h[1], l[1]);
+      split_tf32(v[u].z, h[2], l[2]);
+      split_tf32(v[u].w, h[3], l[3]);
       *reinterpret_cast<float4*>(dst + i * kB + c) = make_float4(h[0], h[1], h[2], h[3]);
       *reinterpret_cast<float4*>(dst + plane + i * kB + c) = make_float4(l[0], l[1], l[2], l[3]);
     }
-  } else {
-    for (int sub = 0; sub < 16; ++sub) {  // 32 x 32 sub-tiles (si, sj) of the 128 x 128 block
-      const int si = sub >> 2, sj = sub & 3;
-      __syncthreads();
-      for (int r = ty; r < 32; r += 8)  // W[K0 + 32 sj + r][R0 + 32 si + tx]
-        tile[r][tx] = m.W[(K0 + 32 * sj + r) * dp + R0 + 32 * si + tx];
-      __syncthreads();
-      for (int r = ty; r < 32; r += 8) {  // panA row 32 si + r, col 32 sj + tx = W[K0+32sj+tx][R0+32si+r]
-        float h, l;
-        split_tf32(tile[tx][r], h, l);
-        const int64_t o = int64_t(32 * si + r) * kB + 32 * sj + tx;
-        dst[o] = h;
-        dst[plane + o] = l;
-      }
+  } else {  // panel row 32q + r, column j = W[K0 + j][R0 + 32q + r]
+    float v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = __ldcg(W + (K0 + ty + 8 * u) * dp + R0 + 32 * q + tx);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) tile[ty + 8 * u][tx] = v[u];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {  // output row r = ty + 8 (u & 3), column j = tx + 32 (u >> 2)
+      const int r = ty + 8 * (u & 3), j = tx + 32 * (u >> 2);
+      float h, l;
+      split_tf32(tile[j][r], h, l);
+      dst[r * kB + j] = h;
+      dst[plane + r * kB + j] = l;
     }
   }
 }
@@ -653,7 +662,7 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       SPD_CHECK_LAUNCH();
       stat_end(kCatInvPivot, q, 2.0 * kB * kB * kB * na, 0);
       stat_begin(kCatInvPanel, q);
-      stage_panel_kernel<<<p->pan_cnt[k], 256, 0, q>>>(p->mats, p->pan_jobs + p->pj_off[k], k, pa, plane);
+      stage_panel_kernel<<<dim3(p->pan_cnt[k], 4), 256, 0, q>>>(p->mats, p->pan_jobs + p->pj_off[k], k, pa, plane);
       SPD_CHECK_LAUNCH();
       int rc = launch_tc3(Kind::TF32, p->maps, p->items + p->pan_off[k], p->epis, p->pan_cnt[k], q);
       if (rc) return rc;
