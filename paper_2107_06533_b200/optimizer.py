@@ -192,6 +192,7 @@ class SPDKFAC(torch.optim.Optimizer):
         self.inv_stream2 = torch.cuda.Stream(self.device)
         self._g_count = 0
         self._g1_inverted = False
+        self._sent = {"A": False, "G1": False, "G2": False}
         self.comm_stream = torch.cuda.Stream(self.device) if self.world > 1 else None
         self._info_events = []
         self._a_count = 0
@@ -452,6 +453,8 @@ class SPDKFAC(torch.optim.Optimizer):
         s.wait_stream(self.factor_stream)
         if self.world > 1:
             s.wait_stream(self.comm_stream)
+            if self._a_inverted:  # A inverses are on their way: share them while backward runs
+                self._exchange_send("A", self.inv_stream)
         self._run_inverse("G1", s, exchange=False)
         self._tl("g1_inverse_done", s)
         self._g1_inverted = True
@@ -466,7 +469,9 @@ class SPDKFAC(torch.optim.Optimizer):
                 ev.record(stream)
                 self._info_events.append((ev, side, self.steps))
         if self.world > 1 and exchange:
-            self._exchange_inverses(side, stream)
+            self._exchange_send(side, stream)
+            stream.wait_stream(self.comm_stream)
+            self._exchange_recv(side, stream)
 
     def _make_a_hook(self, l: _Layer):
         def hook(module, inputs):
@@ -513,6 +518,13 @@ class SPDKFAC(torch.optim.Optimizer):
             self._factor_updates += 1
             self._tl("g_factors_done", main)
         if self.world > 1:
+            if invert_now:
+                if not self._a_inverted:  # hooks did not see a full forward (e.g. factors reused)
+                    self._launch_inverse_A()
+                if not self._g1_inverted:
+                    self._launch_inverse_G1()
+                self._exchange_send("A", self.inv_stream)
+                self._exchange_send("G1", self.inv_stream2)
             cs = self.comm_stream
             cs.wait_stream(main)
             grads = [p.grad for p in self.param_groups[0]["params"] if p.grad is not None]
@@ -530,8 +542,10 @@ class SPDKFAC(torch.optim.Optimizer):
             main.wait_stream(self.inv_stream)   # A inverses landed
             main.wait_stream(self.inv_stream2)  # G1 likewise
             if self.world > 1:
+                self._exchange_send("G2", main)
+                main.wait_stream(self.comm_stream)
                 for side in ("A", "G1", "G2"):
-                    self._exchange_inverses(side, main)
+                    self._exchange_recv(side, main)
             self._tl("inverses_joined", main)
         # precondition + update for every K-FAC layer (mean gradient = sum / P); the pointer
         # tables are rebuilt only when a gradient's storage changes (zero_grad(set_to_none=True))
@@ -557,6 +571,7 @@ class SPDKFAC(torch.optim.Optimizer):
         self._a_inverted = False
         self._g_count = 0
         self._g1_inverted = False
+        self._sent = {"A": False, "G1": False, "G2": False}
         self._g1_left = len(self._g1_groups)
         for k in ("A", "G"):
             self._gseen[k] = [0] * len(self._gseen[k])
@@ -577,9 +592,13 @@ class SPDKFAC(torch.optim.Optimizer):
                 ev.record(stream)
                 self._info_events.append((ev, side, self.steps - 1))
 
-    def _exchange_inverses(self, side, main):
+    def _exchange_send(self, side, src) -> None:
         """Owner ranks broadcast their CT inverses of one side (packed upper triangle,
-        PAPER.md:281-283 / emulator.py:256-262), one NCCL broadcast per owner."""
+        PAPER.md:281-283 / emulator.py:256-262), one NCCL broadcast per owner, on the comm
+        stream once `src` (the stream that inverted them) has packed them.  Every rank issues
+        the sends of an iteration in the same program order (single communicator)."""
+        if self.world == 1 or self._sent[side]:
+            return
         lib = L.load()
         lay = self._bcast[side]
         ct, dims, buf, views, n = lay[self.rank]
@@ -587,15 +606,19 @@ class SPDKFAC(torch.optim.Optimizer):
             L.check(lib.spdkfac_pack_upper_batched_f32(len(ct), L.i32_array(dims),
                                                        L.ptr_array([self.inv[t].data_ptr() for t in ct]),
                                                        L.ptr_array([v.data_ptr() for v in views]),
-                                                       main.cuda_stream), "pack inverses")
+                                                       src.cuda_stream), "pack inverses")
         cs = self.comm_stream
-        cs.wait_stream(main)
+        cs.wait_stream(src)
         with self.comm.group():
             for root, (ct_r, _, buf_r, _, n_r) in enumerate(lay):
                 if n_r:
                     self.comm.bcast(buf_r[:n_r], root, cs)
-        main.wait_stream(cs)
-        for root, (ct_r, dims_r, _, views_r, n_r) in enumerate(lay):
+        self._sent[side] = True
+
+    def _exchange_recv(self, side, main) -> None:
+        """Unpack the inverses received from the other owners (after main joined the comm stream)."""
+        lib = L.load()
+        for root, (ct_r, dims_r, _, views_r, n_r) in enumerate(self._bcast[side]):
             if root == self.rank or not ct_r:
                 continue
             L.check(lib.spdkfac_unpack_upper_batched_f32(len(ct_r), L.i32_array(dims_r),
