@@ -335,6 +335,7 @@ struct Member {
   spdkfac_factor_geom g;
   int64_t M, d, Mpad, ld;  // ld: row length of the staged planes (d rounded up to 8)
   int T, splits, n_tiles;
+  int S;  // 256-wide super blocks (CTA-pair engine) when T >= 2, else 0 (single-CTA engine)
   int Ho, Wo;
   __nv_bfloat16* xt;
   float* partial;
@@ -346,6 +347,9 @@ struct spdkfac_factor_group {
   std::vector<Member> m;
   CUtensorMap* maps = nullptr;
   TcItem* items = nullptr;
+  TcPairItem* pitems = nullptr;
+  int n_pitems = 0;
+  double flops_single = 0, flops_pair = 0;
   TcEpi* epis = nullptr;
   RedJob* jobs = nullptr;
   RedMember* rmem = nullptr;
@@ -389,11 +393,12 @@ int geom_dims(const spdkfac_factor_geom* g, int64_t* rows, int64_t* dim, int* Ho
   return SPDKFAC_OK;
 }
 
-// splits: fill ~148 SMs per factor (the group launch then has >= that many items), each
-// K slice >= 16 blocks (1024 rows); splits == 1 stores straight into the packed buffer
-int choose_splits(int64_t Mpad, int n_tiles) {
+// splits: fill the SMs per factor (148 single-CTA tiles or 74 CTA-pair super tiles; the
+// group launch then has at least that many work items), each K slice >= 16 blocks (1024
+// rows); splits == 1 stores straight into the packed buffer
+int choose_splits(int64_t Mpad, int n_units, int target) {
   const int64_t nkb = Mpad / 64;
-  const int64_t want = cdiv(148, n_tiles);
+  const int64_t want = cdiv(target, n_units);
   const int64_t maxs = std::max<int64_t>(1, nkb / 16);
   return int(std::max<int64_t>(1, std::min(want, maxs)));
 }
@@ -412,13 +417,22 @@ int member_init(Member* mb, const spdkfac_factor_geom* g) {
   mb->ld = round_up(d, 8);
   mb->T = int(cdiv(d, 128));
   mb->n_tiles = mb->T * (mb->T + 1) / 2;
-  mb->splits = choose_splits(mb->Mpad, mb->n_tiles);
+  // CTA-pair super tiles where they pay (measured on B200, ResNet-50 shapes): an even number
+  // of 128-blocks (no padded half super tile) and at least ~48 pair items to fill the GPU,
+  // or a two-block factor over very many rows (the stem conv)
+  mb->S = 0;
+  if (mb->T >= 2) {
+    const int S = mb->T / 2, units = S * (S + 1) / 2;
+    const int sp = choose_splits(mb->Mpad, units, 74);
+    if ((mb->T % 2 == 0 && mb->T >= 4 && units * sp >= 48) || (mb->T == 2 && M >= 200000)) mb->S = S;
+  }
+  mb->splits = mb->S ? choose_splits(mb->Mpad, mb->S * (mb->S + 1) / 2, 74) : choose_splits(mb->Mpad, mb->n_tiles, 148);
   return SPDKFAC_OK;
 }
 
 // carve one group's workspace (c.base == nullptr: size only)
 void group_carve(spdkfac_factor_group* G, Carve& c) {
-  int items = 0, jobs = 0;
+  int items = 0, pitems = 0, jobs = 0;
   for (Member& mb : G->m) {
     mb.xt = c.take<__nv_bfloat16>(size_t(2) * mb.M * mb.ld);
     if (mb.splits > 1) {
@@ -429,15 +443,20 @@ void group_carve(spdkfac_factor_group* G, Carve& c) {
     } else {
       mb.partial = nullptr, mb.chunks = nullptr, mb.counters = nullptr;
     }
-    items += mb.n_tiles * mb.splits;
+    if (mb.S)
+      pitems += mb.S * (mb.S + 1) / 2 * mb.splits;
+    else
+      items += mb.n_tiles * mb.splits;
   }
   const size_t n = G->m.size();
   G->maps = c.take<CUtensorMap>(n, 128);
   G->items = c.take<TcItem>(size_t(std::max(items, 1)));
+  G->pitems = c.take<TcPairItem>(size_t(std::max(pitems, 1)));
   G->epis = c.take<TcEpi>(n);
   G->jobs = c.take<RedJob>(size_t(std::max(jobs, 1)));
   G->rmem = c.take<RedMember>(n);
   G->n_items = items;
+  G->n_pitems = pitems;
   G->n_jobs = jobs;
 }
 
@@ -445,44 +464,82 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
   const int n = int(G->m.size());
   std::vector<CUtensorMap> maps(n);
   std::vector<TcItem> items;
+  std::vector<TcPairItem> pitems;
   std::vector<TcEpi> epis(n);
   std::vector<RedJob> jobs;
   std::vector<RedMember> rmem(n);
   G->max_chunks = 1;
   G->flops = 0;
+  G->flops_single = G->flops_pair = 0;
   for (int k = 0; k < n; ++k) {
     Member& mb = G->m[k];
     int rc = make_operand_map_mn(&maps[k], mb.xt, mb.ld, mb.M);
     if (rc) return rc;
     G->flops += double(mb.M) * mb.d * (mb.d + 1);
+    (mb.S ? G->flops_pair : G->flops_single) += double(mb.M) * mb.d * (mb.d + 1);
     const int64_t nkb = mb.Mpad / 64, per = cdiv(nkb, mb.splits);
+    auto tile_index = [&](int I, int J) { return I * mb.T - I * (I - 1) / 2 + (J - I); };
     for (int I = 0; I < mb.T; ++I)
-      for (int J = I; J < mb.T; ++J) {
-        const int tile_idx = I * mb.T - I * (I - 1) / 2 + (J - I);
-        if (mb.splits > 1) jobs.push_back(RedJob{k, tile_idx, I, J});
-        for (int s2 = 0; s2 < mb.splits; ++s2) {
-          TcItem it{};
-          it.a_map = k;
-          it.b_map = k;
-          it.a_row = I * 128;
-          it.b_row = J * 128;
-          const int64_t kb0 = std::min<int64_t>(nkb, s2 * per), kb1 = std::min<int64_t>(nkb, (s2 + 1) * per);
-          it.k0 = int(kb0 * 64);
-          it.nk = int(kb1 - kb0);
-          it.epi = k;
-          it.flags = kMnMajor | ((I == J) ? kSameAB : 0);
-          if (mb.splits > 1) {  // partial tile -> member workspace slot, reduced by reduce_pack_kernel
-            it.out_r = 0;
-            it.out_c = (tile_idx * mb.splits + s2) * 128;
-          } else {              // direct packed-upper epilogue
-            it.out_r = I * 128;
-            it.out_c = J * 128;
-          }
-          it.m_valid = int(std::min<int64_t>(128, mb.d - int64_t(I) * 128));
-          it.n_valid = int(std::min<int64_t>(128, mb.d - int64_t(J) * 128));
-          if (it.nk > 0) items.push_back(it);
+      for (int J = I; J < mb.T; ++J)
+        if (mb.splits > 1) jobs.push_back(RedJob{k, tile_index(I, J), I, J});
+    for (int s2 = 0; s2 < mb.splits; ++s2) {
+      const int64_t kb0 = std::min<int64_t>(nkb, s2 * per), kb1 = std::min<int64_t>(nkb, (s2 + 1) * per);
+      if (kb1 <= kb0) continue;
+      // target of block tile (I, J): partial slot (split K) or packed-upper position
+      auto out_of = [&](int I, int J, int32_t& out_r, int32_t& out_c) {
+        if (mb.splits > 1) {
+          out_r = 0;
+          out_c = (tile_index(I, J) * mb.splits + s2) * 128;
+        } else {
+          out_r = I * 128;
+          out_c = J * 128;
         }
+      };
+      auto valid = [&](int I) { return int(std::min<int64_t>(128, mb.d - int64_t(I) * 128)); };
+      if (mb.S) {
+        for (int P = 0; P < mb.S; ++P)
+          for (int Q = P; Q < mb.S; ++Q) {
+            TcPairItem it{};
+            it.map = k;
+            it.a_row = 2 * P * 128;
+            it.b_row = 2 * Q * 128;
+            it.k0 = int(kb0 * 64);
+            it.nk = int(kb1 - kb0);
+            it.epi = k;
+            it.flags = (P == Q) ? kSameAB : 0;
+            for (int r = 0; r < 2; ++r) {
+              const int I = 2 * P + r;
+              it.m_valid[r] = I < mb.T ? valid(I) : 0;
+              it.n_valid[r] = (2 * Q + r) < mb.T ? valid(2 * Q + r) : 0;
+              for (int h = 0; h < 2; ++h) {
+                const int J = 2 * Q + h;
+                int32_t orr = 0, occ = -1;
+                if (I < mb.T && J < mb.T && I <= J) out_of(I, J, orr, occ);
+                if (occ >= 0) it.out_r[r] = orr;
+                it.out_c[2 * r + h] = occ;
+              }
+            }
+            pitems.push_back(it);
+          }
+      } else {
+        for (int I = 0; I < mb.T; ++I)
+          for (int J = I; J < mb.T; ++J) {
+            TcItem it{};
+            it.a_map = k;
+            it.b_map = k;
+            it.a_row = I * 128;
+            it.b_row = J * 128;
+            it.k0 = int(kb0 * 64);
+            it.nk = int(kb1 - kb0);
+            it.epi = k;
+            it.flags = kMnMajor | (I == J ? kSameAB : 0);
+            out_of(I, J, it.out_r, it.out_c);
+            it.m_valid = valid(I);
+            it.n_valid = valid(J);
+            items.push_back(it);
+          }
       }
+    }
     if (mb.splits > 1) {
       epis[k] = TcEpi{mb.partial, 128, 0, 1.f, 0.f, kAxpby, 0, nullptr, 0, 0};
       G->max_chunks = std::max<int>(G->max_chunks, int(cdiv(mb.splits, kChunk)));
@@ -496,9 +553,13 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
   }
   // persistent CTAs take items round-robin: longest K first balances the group
   std::stable_sort(items.begin(), items.end(), [](const TcItem& a, const TcItem& b) { return a.nk > b.nk; });
+  std::stable_sort(pitems.begin(), pitems.end(),
+                   [](const TcPairItem& a, const TcPairItem& b) { return a.nk > b.nk; });
   G->n_items = int(items.size());
+  G->n_pitems = int(pitems.size());
   int rc;
-  if ((rc = upload(G->maps, maps, s)) || (rc = upload(G->items, items, s)) || (rc = upload(G->epis, epis, s)) ||
+  if ((rc = upload(G->maps, maps, s)) || (rc = upload(G->items, items, s)) || (rc = upload(G->pitems, pitems, s)) ||
+      (rc = upload(G->epis, epis, s)) ||
       (rc = upload(G->jobs, jobs, s)) || (rc = upload(G->rmem, rmem, s)))
     return rc;
   return SPDKFAC_OK;
@@ -548,13 +609,20 @@ int member_stage(const Member& mb, const float* x, cudaStream_t s) {
 int group_compute(spdkfac_factor_group* G, float scale, float decay, float world_scale, float* packed,
                   cudaStream_t s) {
   // algorithmic work: sum over members of M * d * (d + 1) flops
-  stat_begin(kCatFactorSyrk, s);
   TcRun run{packed, G->m.empty() ? 0 : G->m[0].d, scale, decay, world_scale, 0};
-  int rc = launch_tc3(Kind::BF16, G->maps, G->items, G->epis, G->n_items, s, run);
-  if (rc) return rc;
-  double bytes = 0;
-  for (const Member& mb : G->m) bytes += 4.0 * mb.ld * mb.M;
-  stat_end(kCatFactorSyrk, s, G->flops, bytes);
+  double bytes_single = 0, bytes_pair = 0;
+  for (const Member& mb : G->m) (mb.S ? bytes_pair : bytes_single) += 4.0 * mb.ld * mb.M;
+  int rc;
+  if (G->n_items) {
+    stat_begin(kCatFactorSyrk, s);
+    if ((rc = launch_tc3(Kind::BF16, G->maps, G->items, G->epis, G->n_items, s, run))) return rc;
+    stat_end(kCatFactorSyrk, s, G->flops_single, bytes_single);
+  }
+  if (G->n_pitems) {
+    stat_begin(kCatFactorSyrk, s);
+    if ((rc = launch_tc3_pair(G->maps, G->pitems, G->epis, G->n_pitems, s, run))) return rc;
+    stat_end(kCatFactorSyrk, s, G->flops_pair, bytes_pair);
+  }
   if (G->n_jobs == 0) return SPDKFAC_OK;
   dim3 rgrid(16, unsigned(G->n_jobs), unsigned(G->max_chunks));
   stat_begin(kCatFactorReduce, s);

@@ -160,6 +160,31 @@ int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* 
   return launch_kind<Kind::TF32, 2, true>(maps, items, epis, n, s, TcRun{});
 }
 
+int launch_tc3_pair(const CUtensorMap* maps, const TcPairItem* items, const TcEpi* epis, int n, cudaStream_t s,
+                    const TcRun& run) {
+  if (n <= 0) return SPDKFAC_OK;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SPD_CUDA(cudaFuncSetAttribute(tc3_pair_kernel<kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPairSmemBytes)));
+    attr_set = true;
+  }
+  static int pairs = 0;
+  if (!pairs) {
+    int dev = 0, sms = 0;
+    SPD_CUDA(cudaGetDevice(&dev));
+    SPD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (const char* e = getenv("SPDKFAC_MAX_CTAS")) {
+      const int cap = atoi(e);
+      if (cap > 0 && cap < sms) sms = cap;
+    }
+    pairs = sms / 2;
+  }
+  const int grid = 2 * (n < pairs ? n : pairs);
+  tc3_pair_kernel<kStages><<<grid, 192, kPairSmemBytes, s>>>(maps, items, epis, run, n);
+  SPD_CHECK_LAUNCH();
+  return SPDKFAC_OK;
+}
+
 int make_ctile_map(CUtensorMap* out, const float* base, int64_t rows, int64_t cols, int64_t ld) {
   EncodeTiledFn fn = encode_fn();
   SPD_ARG(fn != nullptr, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -167,7 +192,7 @@ int make_ctile_map(CUtensorMap* out, const float* base, int64_t rows, int64_t co
           "tensor map: misaligned target");
   cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
   cuuint64_t strides[1] = {cuuint64_t(ld * 4)};
-  cuuint32_t box[2] = {128, 128};
+  cuuint32_t box[2] = {128, 64};  // 64-row halves (kCTile ring)
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

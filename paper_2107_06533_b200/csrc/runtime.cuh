@@ -82,6 +82,9 @@ struct PtrTable {
 int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items,
                cudaStream_t s, const TcRun& run = TcRun{});
 // TF32 engine with a TMA-staged fp32 C tile (read-modify-write targets, TcEpi::c_map)
+// CTA-pair SYRK engine (cta_group::2, 256 x 256 super tiles; bf16 MN-major split planes)
+int launch_tc3_pair(const CUtensorMap* maps, const TcPairItem* items, const TcEpi* epis, int n_items, cudaStream_t s,
+                    const TcRun& run);
 int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items, cudaStream_t s);
 // 2-D tensor map over a row-major fp32 matrix [rows][ld], box 128 x 128, no swizzle
 int make_ctile_map(CUtensorMap* out, const float* base, int64_t rows, int64_t cols, int64_t ld);

@@ -182,9 +182,13 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
 // (lanes walk contiguous smem -> conflict-free) and one thread TMA-stores it back.  Used
 // for the read-modify-write inverse updates, where per-thread loads left the kernel
 // latency-bound at ~2 TB/s.
+// kCTile target tiles move as 64-row halves through a ring of three 32-KB slots, so the
+// next tile's first half loads while the current tile's second half is being updated
+constexpr int kCRing = 3;
+constexpr uint32_t kCHalfBytes = 64 * 128 * 4;
 template <int kSt>
 constexpr size_t tc_smem_bytes(bool ctile) {
-  return size_t(kSt) * kStageBytes + (ctile ? 65536 : 0) + 1024 + 256;
+  return size_t(kSt) * kStageBytes + (ctile ? kCRing * kCHalfBytes : 0) + 1024 + 256;
 }
 
 template <Kind K, int kSt, bool kCTile>
@@ -194,14 +198,14 @@ __global__ void __launch_bounds__(192, 1)
   constexpr int BK = (K == Kind::BF16) ? 64 : 32;  // one 128-byte swizzle row of K
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* ctile = reinterpret_cast<float*>(smem + kSt * kStageBytes);  // [128][128] (kCTile)
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageBytes + (kCTile ? 65536 : 0));
+  float* ctile = reinterpret_cast<float*>(smem + kSt * kStageBytes);  // kCRing x [64][128] (kCTile)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageBytes + (kCTile ? kCRing * kCHalfBytes : 0));
   uint64_t* empty = full + kSt;
   uint64_t* tfull = empty + kSt;  // [2]
   uint64_t* tempty = tfull + 2;   // [2]
-  uint64_t* cfull = tempty + 2;   // C tile landed
-  uint64_t* cfree = cfull + 1;    // C tile stored back (smem reusable)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfree + 1);
+  uint64_t* cfull = tempty + 2;     // [kCRing] C half tile landed
+  uint64_t* cfree = cfull + kCRing;  // [kCRing] C half tile stored back (slot reusable)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfree + kCRing);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -214,8 +218,10 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4);
     }
-    mbar_init(cfull, 1);
-    mbar_init(cfree, 1);
+    for (int q = 0; q < kCRing; ++q) {
+      mbar_init(&cfull[q], 1);
+      mbar_init(&cfree[q], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<256>(tmem_slot);
@@ -265,9 +271,13 @@ __global__ void __launch_bounds__(192, 1)
           const TcEpi ep = epis[it.epi];
           const CUtensorMap* cm = maps + ep.c_map;
           if (ep.c_map != last_c) tmap_acquire(cm), last_c = ep.c_map;
-          mbar_wait(cfree, (t & 1) ^ 1);
-          mbar_expect_tx(cfull, 65536);
-          tma_load_2d(ctile, cm, cfull, it.out_r, it.out_c);  // rows out_c.., cols out_r..
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {  // rows out_c + 64 h .., cols out_r ..
+            const uint32_t u = 2 * t + h, q = u % kCRing;
+            mbar_wait(&cfree[q], ((u / kCRing) & 1) ^ 1);
+            mbar_expect_tx(&cfull[q], kCHalfBytes);
+            tma_load_2d(ctile + q * (kCHalfBytes / 4), cm, &cfull[q], it.out_r, it.out_c + 64 * h);
+          }
         }
       }
     }
@@ -330,10 +340,9 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t buf = t & 1, use = t >> 1;
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
-      if constexpr (kCTile) mbar_wait(cfull, t & 1);
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
-        if (c * 32 >= it.n_valid) break;  // uniform
+        if (!kCTile && c * 32 >= it.n_valid) break;  // uniform (kCTile targets are whole 128-tiles)
         float v[32];
         if (it.nk > 0) {
           tmem_ld_32x32b_x32(tmem + buf * 128 + (uint32_t(quad * 32) << 16) + uint32_t(c * 32), v);
@@ -341,10 +350,21 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int u = 0; u < 32; ++u) v[u] = 0.f;
         }
-        if constexpr (kCTile) {  // ctile[j][i] = beta * ctile[j][i] + alpha * D[i][j]
-          float* col = ctile + (c * 32) * 128 + i;
+        if constexpr (kCTile) {  // half h = c / 2: slot[j][i] = beta * slot[j][i] + alpha * D[i][j]
+          const uint32_t u2 = 2 * t + (c >> 1), q = u2 % kCRing;
+          if ((c & 1) == 0) mbar_wait(&cfull[q], (u2 / kCRing) & 1);
+          float* col = ctile + q * (kCHalfBytes / 4) + ((c & 1) * 32) * 128 + i;
 #pragma unroll
           for (int u = 0; u < 32; ++u) col[u * 128] = ep.beta * col[u * 128] + ep.alpha * v[u];
+          if (c & 1) {  // half complete: hand it to the TMA store
+            fence_proxy_async_smem();
+            named_bar_sync(1, 128);
+            if (warp == 2 && lane == 0) {
+              tma_store_2d(maps + ep.c_map, ctile + q * (kCHalfBytes / 4), it.out_r, it.out_c + 64 * (c >> 1));
+              tma_store_commit_and_wait_read();
+              mbar_arrive(&cfree[q]);
+            }
+          }
         } else {
           epilogue_chunk(it, ep, run, i, c, v);
         }
@@ -352,20 +372,177 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM drained: MMA may reuse this accumulator
-      if constexpr (kCTile) {
-        fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the TMA store
-        named_bar_sync(1, 128);
-        if (warp == 2 && lane == 0) {
-          tma_store_2d(maps + ep.c_map, ctile, it.out_r, it.out_c);
-          tma_store_commit_and_wait_read();
-          mbar_arrive(cfree);
-        }
-      }
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_free<256>(tmem);
+}
+
+
+// ------------------------------------------------------------------ CTA-pair engine
+// cta_group::2 variant for the symmetric factor SYRK (bf16 split planes, MN-major): a
+// cluster of two CTAs computes one 256 x 256 super tile = 2 x 2 blocks of 128.  CTA r
+// stages A block (a_row + 128 r) and B block (b_row + 128 r) of every K slab (the same
+// 64-KB stage layout as the single-CTA engine, signalled on the leader's barrier); the
+// leader issues M = 256, N = 256 MMAs that read both CTAs' shared memory, and each CTA's
+// TMEM receives its 128 rows x 256 columns.  Per SM this halves the operand bytes per MMA
+// cycle (the single-CTA SYRK sat at ~40% tensor-pipe activity waiting on TMA).
+struct TcPairItem {
+  int32_t map;           // operand tensor map (A and B both come from it: symmetric factor)
+  int32_t a_row, b_row;  // MN coordinates of CTA 0's A and B blocks (CTA 1: +128)
+  int32_t k0, nk;
+  int32_t epi;
+  int32_t flags;         // kSameAB: diagonal super tile, B blocks == A blocks
+  int32_t out_r[2];      // per CTA rank: target row offset
+  int32_t out_c[4];      // per (rank, half) at [2 r + h]: target column offset, -1 = no store
+  int32_t m_valid[2], n_valid[2];
+  int32_t pad_;
+};
+
+constexpr size_t kPairSmemBytes = size_t(kStages) * kStageBytes + 1024 + 256;
+
+template <int kSt>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    tc3_pair_kernel(const CUtensorMap* __restrict__ maps, const TcPairItem* __restrict__ items,
+                    const TcEpi* __restrict__ epis, const TcRun run, int n_items) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageBytes);
+  uint64_t* empty = full + kSt;
+  uint64_t* tfull = empty + kSt;  // [2]
+  uint64_t* tempty = tfull + 2;   // [2] (leader: 8 arrivals = 4 epilogue warps x 2 CTAs)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t pair = cluster_idx(), npairs = cluster_count();
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kSt; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated in both
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs), completion on the leader's full[s]
+      uint32_t g = 0;
+      int last = -1;
+      for (int item = int(pair); item < n_items; item += int(npairs)) {
+        const TcPairItem it = items[item];
+        const bool same = (it.flags & kSameAB) != 0;
+        const CUtensorMap* m = maps + it.map;
+        if (it.map != last) tmap_acquire(m), last = it.map;
+        const int ar = it.a_row + 128 * int(rank), br = it.b_row + 128 * int(rank);
+        const uint32_t bytes = 2u * (same ? 2 * kTileBytes : 4 * kTileBytes);  // both CTAs
+        for (int kb = 0; kb < it.nk; ++kb, ++g) {
+          const uint32_t s = g % kSt;
+          mbar_wait(&empty[s], ((g / kSt) & 1) ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[s], bytes);
+          const uint32_t fb = mapa_shared(&full[s], 0);
+          uint8_t* st = smem + s * kStageBytes;
+          const int kc = it.k0 + kb * 64;
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            tma_load_3d_pair(st + p * kTileBytes, m, fb, ar, kc, p);
+            tma_load_3d_pair(st + p * kTileBytes + kTileBytes / 2, m, fb, ar + 64, kc, p);
+            if (!same) {
+              tma_load_3d_pair(st + (2 + p) * kTileBytes, m, fb, br, kc, p);
+              tma_load_3d_pair(st + (2 + p) * kTileBytes + kTileBytes / 2, m, fb, br + 64, kc, p);
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ---- MMA issuer (leader only)
+      constexpr uint32_t idesc = make_idesc<Kind::BF16>(256, 256) | (1u << 15) | (1u << 16);
+      uint32_t g = 0, t = 0;
+      for (int item = int(pair); item < n_items; item += int(npairs), ++t) {
+        const TcPairItem it = items[item];
+        const bool same = (it.flags & kSameAB) != 0;
+        const uint32_t buf = t & 1, use = t >> 1;
+        mbar_wait(&tempty[buf], (use & 1) ^ 1);  // both CTAs drained this accumulator
+        tc_fence_after();
+        const uint32_t acc = tmem + buf * 256;
+        for (int kb = 0; kb < it.nk; ++kb, ++g) {
+          const uint32_t s = g % kSt;
+          mbar_wait(&full[s], (g / kSt) & 1);
+          tc_fence_after();
+          uint8_t* st = smem + s * kStageBytes;
+          const uint64_t ahi = make_sdesc_sw128_mn(st);
+          const uint64_t alo = make_sdesc_sw128_mn(st + kTileBytes);
+          const uint64_t bhi = same ? ahi : make_sdesc_sw128_mn(st + 2 * kTileBytes);
+          const uint64_t blo = same ? alo : make_sdesc_sw128_mn(st + 3 * kTileBytes);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t off = uint64_t(kk * (2048 >> 4));
+            umma_pair_bf16(acc, ahi + off, bhi + off, idesc, (kb | kk) != 0);
+            umma_pair_bf16(acc, ahi + off, blo + off, idesc, 1u);
+            umma_pair_bf16(acc, alo + off, bhi + off, idesc, 1u);
+          }
+          tc_commit_pair(&empty[s], 3);  // both CTAs' stage s free once these retire
+        }
+        tc_commit_pair(&tfull[buf], 3);
+      }
+    }
+    __syncwarp();
+  } else {  // ---- epilogue warps 2..5 (both CTAs): rows 128 r + i of the super tile
+    const int quad = warp & 3;
+    const int i = quad * 32 + lane;
+    const uint32_t tempty_leader0 = mapa_shared(&tempty[0], 0);
+    uint32_t t = 0;
+    for (int item = int(pair); item < n_items; item += int(npairs), ++t) {
+      const TcPairItem it = items[item];
+      const TcEpi ep = epis[it.epi];
+      const uint32_t buf = t & 1, use = t >> 1;
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+      const int32_t occ[2] = {rank ? it.out_c[2] : it.out_c[0], rank ? it.out_c[3] : it.out_c[1]};
+      const int32_t orr = rank ? it.out_r[1] : it.out_r[0];
+      const int32_t mv = rank ? it.m_valid[1] : it.m_valid[0];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int oc = occ[h];
+        if (oc < 0) continue;  // uniform: lower-triangle or padding block
+        TcItem ti{};
+        ti.out_r = orr;
+        ti.out_c = oc;
+        ti.m_valid = mv;
+        ti.n_valid = it.n_valid[h];
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          if (c * 32 >= ti.n_valid) break;
+          float v[32];
+          if (it.nk > 0) {
+            tmem_ld_32x32b_x32(tmem + buf * 256 + (uint32_t(quad * 32) << 16) + uint32_t(h * 128 + c * 32), v);
+          } else {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) v[u] = 0.f;
+          }
+          epilogue_chunk(ti, ep, run, i, c, v);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + buf * 8);  // leader's tempty[buf]
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // the peer's TMEM / smem are read by the leader's MMAs until the end
+  if (warp == 1) tmem_free_pair<512>(tmem);
 }
 
 }  // namespace spd
