@@ -66,6 +66,11 @@ def parse():
                    help="graph: the whole step (fwd, bwd, K-FAC step) replayed as one CUDA graph")
     p.add_argument("--main-priority", type=int, default=0,
                    help="CUDA priority of the forward/backward stream (negative = higher than the K-FAC side streams)")
+    p.add_argument("--trace", default=None,
+                   help="diagnostic: torch.profiler (CUPTI) trace of 3 steps after the timed region; writes a "
+                        "kernel-timeline summary JSON to this path")
+    p.add_argument("--g1-fraction", type=float, default=0.85,
+                   help="share of the output-side inversion work (sum g^3) inverted during backward")
     p.add_argument("--clocks", choices=("nvml", "smi", "off"), default="nvml")
     p.add_argument("--timeline", action="store_true", help="diagnostic: per-phase CUDA-event timeline of one eager step")
     p.add_argument("--stats-off", action="store_true", help="no per-launch CUDA events in the timed region (diagnostic)")
@@ -186,6 +191,45 @@ def cpu_reference(model, batch, steps=None, budget_s=30.0):
     return total * 1e3, sample, per_step, kind
 
 
+# ---------------------------------------------------------------- diagnostics
+def trace_summary(step, path, torch, n=3):
+    """CUPTI kernel timeline of n steps: GPU busy union per step, per-stream busy, top kernels."""
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for i in range(n):
+            step(i)
+        torch.cuda.synchronize()
+    evs = [e for e in prof.events() if e.device_type.name == "CUDA" and e.time_range.elapsed_us() > 0]
+    ks = sorted(((e.time_range.start, e.time_range.end, e.name, getattr(e, "device_resource_id", 0)) for e in evs))
+    if not ks:
+        json.dump({"error": "no CUDA events"}, open(path, "w"))
+        return
+    t0, t1 = ks[0][0], max(k[1] for k in ks)
+    busy, cur_s, cur_e = 0.0, None, None
+    for s0, e0, _, _ in ks:
+        if cur_e is None or s0 > cur_e:
+            if cur_e is not None:
+                busy += cur_e - cur_s
+            cur_s, cur_e = s0, e0
+        else:
+            cur_e = max(cur_e, e0)
+    busy += cur_e - cur_s
+    per_name, per_stream = {}, {}
+    for s0, e0, nm, sid in ks:
+        key = nm[:90]
+        c = per_name.setdefault(key, [0.0, 0])
+        c[0] += e0 - s0
+        c[1] += 1
+        per_stream[str(sid)] = per_stream.get(str(sid), 0.0) + (e0 - s0)
+    top = sorted(per_name.items(), key=lambda kv: -kv[1][0])[:40]
+    out = {"steps": n, "span_ms_per_step": (t1 - t0) / 1e3 / n, "gpu_busy_union_ms_per_step": busy / 1e3 / n,
+           "kernel_sum_ms_per_step": sum(v[0] for v in per_name.values()) / 1e3 / n,
+           "per_stream_ms_per_step": {k: v / 1e3 / n for k, v in sorted(per_stream.items(), key=lambda kv: -kv[1])},
+           "top": [{"name": k, "ms_per_step": v[0] / 1e3 / n, "count_per_step": v[1] / n} for k, v in top]}
+    json.dump(out, open(path, "w"), indent=1)
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(a):
     import torch
@@ -216,7 +260,7 @@ def run_ours(a):
         opt.placement = None
     else:
         opt = SPDKFAC(model, lr=a.lr, damping=a.damping, factor_update_freq=a.factor_freq,
-                      inv_update_freq=a.inv_freq, placement=a.placement)
+                      inv_update_freq=a.inv_freq, placement=a.placement, early_g_fraction=a.g1_fraction)
     crit = nn.CrossEntropyLoss()
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)
@@ -318,6 +362,8 @@ def run_ours(a):
     # captured event nodes hold the last replay's timestamps
     per = 1 if graphed else a.steps
     launches = st["total_launches"] * (a.steps if graphed else 1)
+    if a.trace and rank == 0:
+        trace_summary(step, a.trace, torch)
     # per-category breakdown: a separate 2-step eager pass with every launch bracketed by events
     nb = 2
     _lib.stats_reset(timing=True, reserve=600 * nb)

@@ -78,7 +78,8 @@ class SPDKFAC(torch.optim.Optimizer):
     def __init__(self, model: nn.Module, lr: float = 0.1, damping: float = 0.1, factor_decay: float = 0.0,
                  factor_update_freq: int = 1, inv_update_freq: int = 1, fusion: FusionPolicy = FusionPolicy.OPTIMAL,
                  placement: str = "lbp", balance: str = "dim_sq", perf: Optional[PerfParams] = None,
-                 batch_averaged: bool = True, layer_times: Optional[dict] = None, comm=None):
+                 batch_averaged: bool = True, layer_times: Optional[dict] = None, comm=None,
+                 early_g_fraction: float = 0.85):
         if damping < 0:
             raise ValueError(f"damping must be nonnegative, got {damping}")
         if not 0.0 <= factor_decay < 1.0:
@@ -173,7 +174,8 @@ class SPDKFAC(torch.optim.Optimizer):
         # on a second stream, G2 in step()
         mine = list(self.placement.workers[self.rank])
         self._mine = mine
-        grp = S.inversion_groups([l.spec.a_dim for l in self.layers], [l.spec.g_dim for l in self.layers])
+        grp = S.inversion_groups([l.spec.a_dim for l in self.layers], [l.spec.g_dim for l in self.layers],
+                                 early_fraction=early_g_fraction)
         self._n_g1 = grp["n_g1"]
         # G1 may start once every backward fusion group holding a G1 member is computed; the
         # factors a G1 inverse reads must be complete (members of a group run together)
