@@ -17,12 +17,19 @@
 //                update : W[I,J] -= Wold[I,K] C_J^T for I <= J (I,J != K) on tcgen05
 //                         (3 x tf32, rank-128), mirrored to W[J,I]
 //              finalize: out = -(W + W^T)/2 cropped to d x d (the reference's symmetrisation).
+#include <algorithm>
+
 #include "runtime.cuh"
 
 namespace spd {
 
 constexpr int kB = 128;          // pivot block = tile edge
 constexpr int kSmemLd = kB + 1;  // padded row stride of the shared-memory block
+// Panel planes panA / panC: [2 planes][rows][kPanCols]; step k uses the 128 columns of slot
+// k % 4, so the two panels of an even/odd step pair are adjacent columns (one K = 256
+// update reads both) and the look-ahead step never overwrites a slot still being read.
+constexpr int kPanSlots = 4;
+constexpr int kPanCols = kPanSlots * kB;
 
 struct InvMat {
   float* W;          // padded working matrix [dp][dp] (blocked path)
@@ -297,7 +304,7 @@ __global__ void __launch_bounds__(256) stage_panel_kernel(const InvMat* __restri
   if (*m.info != 0) return;
   const int q = blockIdx.y;
   const int64_t dp = m.dp, K0 = int64_t(k) * kB, R0 = int64_t(jb.rb) * kB;
-  float* dst = panA + (int64_t(m.panel_row0) + R0 + 32 * q) * kB;
+  float* dst = panA + (int64_t(m.panel_row0) + R0 + 32 * q) * kPanCols;  // panA: slot base
   const float* __restrict__ W = m.W;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   if (jb.rb < k) {  // rows R0 + 32q + i, columns K0 + c: 32 x 128 floats, 4 float4 per thread
@@ -315,8 +322,8 @@ __global__ void __launch_bounds__(256) stage_panel_kernel(const InvMat* __restri
       split_tf32(v[u].y, h[1], l[1]);
       split_tf32(v[u].z, h[2], l[2]);
       split_tf32(v[u].w, h[3], l[3]);
-      *reinterpret_cast<float4*>(dst + i * kB + c) = make_float4(h[0], h[1], h[2], h[3]);
-      *reinterpret_cast<float4*>(dst + plane + i * kB + c) = make_float4(l[0], l[1], l[2], l[3]);
+      *reinterpret_cast<float4*>(dst + i * kPanCols + c) = make_float4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<float4*>(dst + plane + i * kPanCols + c) = make_float4(l[0], l[1], l[2], l[3]);
     }
   } else {  // panel row 32q + r, column j = W[K0 + j][R0 + 32q + r]
     float v[16];
@@ -330,8 +337,8 @@ __global__ void __launch_bounds__(256) stage_panel_kernel(const InvMat* __restri
       const int r = ty + 8 * (u & 3), j = tx + 32 * (u >> 2);
       float h, l;
       split_tf32(tile[j][r], h, l);
-      dst[r * kB + j] = h;
-      dst[plane + r * kB + j] = l;
+      dst[r * kPanCols + j] = h;
+      dst[plane + r * kPanCols + j] = l;
     }
   }
 }
@@ -385,6 +392,7 @@ struct spdkfac_inverse_plan {
   int n_blocked;
   int steps;
   std::vector<int> act_off, act_cnt, pan_off, pan_cnt, upd_off, upd_cnt, pj_off, u1_cnt;
+  std::vector<double> upd_flops, u2_flops;  // per step: U1 / U2 tensor work (algorithmic, per launch)
   cudaStream_t side = nullptr;  // look-ahead stream: pivot/stage/panel of step k+1
   bool lookahead = true;        // SPDKFAC_NO_LOOKAHEAD=1 serialises (diagnostics)
   cudaEvent_t ev_u1 = nullptr, ev_panel = nullptr;
@@ -392,10 +400,10 @@ struct spdkfac_inverse_plan {
   PanelJob* pan_jobs;           // device, (matrix, R != K) per step, same order as the panel items
   TileJob* tiles;               // device, 32x32 tile pairs of all blocked matrices
   int n_tiles;
-  CUtensorMap* maps;            // [0] panA0, [1] panC0, [2] P^-1, [3] panA1, [4] panC1, [5 + slot] W_slot tiles
+  CUtensorMap* maps;            // [0] panA, [1] panC, [2] P^-1, [3], [4] unused, [5 + slot] W_slot tiles
   TcItem* items;                // per step: panel GEMM items then update items
-  TcEpi* epis;                  // [0, n): update, [n, 2n) / [2n, 3n): panel writing panC parity 0 / 1
-  float* panA;                  // [2 parity][2 planes][rows][128]
+  TcEpi* epis;                  // [0, n): update, [n + q n, n + (q + 1) n): panel writing panC slot q
+  float* panA;                  // [2 planes][rows][kPanCols] (slot q = columns [128 q, 128 q + 128))
   float* panC;
   float* pinvS;
   int64_t plane_rows;
@@ -440,8 +448,8 @@ size_t inverse_carve(int n, const int32_t* dims, Carve& c, spdkfac_inverse_plan*
     }
     if (mats) mats->push_back(m);
   }
-  float* panA = c.take<float>(size_t(4) * std::max<int64_t>(rows, 1) * kB);
-  float* panC = c.take<float>(size_t(4) * std::max<int64_t>(rows, 1) * kB);
+  float* panA = c.take<float>(size_t(2) * std::max<int64_t>(rows, 1) * kPanCols);
+  float* panC = c.take<float>(size_t(2) * std::max<int64_t>(rows, 1) * kPanCols);
   float* pinvS = c.take<float>(size_t(2) * std::max(nblk, 1) * kB * kB);
   auto* dm = c.take<InvMat>(size_t(n));
   auto* sid = c.take<int32_t>(size_t(n));
@@ -451,7 +459,7 @@ size_t inverse_carve(int n, const int32_t* dims, Carve& c, spdkfac_inverse_plan*
   auto* pj = c.take<PanelJob>(size_t(std::max<int64_t>(items, 1)));
   auto* mp = c.take<CUtensorMap>(size_t(5 + nblk), 128);
   auto* it = c.take<TcItem>(size_t(std::max<int64_t>(items, 1)));
-  auto* ep = c.take<TcEpi>(size_t(3) * n);
+  auto* ep = c.take<TcEpi>(size_t(1 + kPanSlots) * n);
   if (p) {
     p->panA = panA, p->panC = panC, p->pinvS = pinvS, p->mats = dm, p->small_ids = sid, p->blocked_ids = bid;
     p->act_ids = aid, p->tiles = tj, p->pan_jobs = pj, p->maps = mp, p->items = it, p->epis = ep;
@@ -504,14 +512,13 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   }
   p->n_small = int(small.size());
   p->n_blocked = int(blocked.size());
-  const int64_t plane = p->plane_rows * kB;
-  const int64_t pbuf = 2 * plane;  // elements per parity buffer (2 planes)
-  std::vector<TcEpi> epis(size_t(3) * n);
+  const int64_t plane = p->plane_rows * kPanCols;
+  std::vector<TcEpi> epis(size_t(1 + kPanSlots) * n);
   for (int t = 0; t < n; ++t) {
     epis[t] = TcEpi{mats[t].W, mats[t].dp, 0, -1.f, 1.f, kAxpby, 0, nullptr, 0, 0,
-                    dims[t] > kB ? 5 + mats[t].slot : 0};                                               // update
-    epis[n + t] = TcEpi{mats[t].W, mats[t].dp, 0, 1.f, 0.f, kAxpby, 0, p->panC, kB, plane};           // panel, parity 0
-    epis[2 * n + t] = TcEpi{mats[t].W, mats[t].dp, 0, 1.f, 0.f, kAxpby, 0, p->panC + pbuf, kB, plane};  // parity 1
+                    dims[t] > kB ? 5 + mats[t].slot : 0};  // update
+    for (int q = 0; q < kPanSlots; ++q)                   // panel GEMM writing panC slot q
+      epis[n + q * n + t] = TcEpi{mats[t].W, mats[t].dp, 0, 1.f, 0.f, kAxpby, 0, p->panC + q * kB, kPanCols, plane};
   }
   std::vector<TileJob> tiles;
   for (int t : blocked) {
@@ -536,22 +543,21 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
         if (R == k) continue;
         pan.push_back(PanelJob{t, R});
         const int prow = mats[t].panel_row0 + R * kB;
-        const int pa = (k & 1) ? 3 : 0;  // panA parity map
+        const int q = k % kPanSlots;  // panel slot of step k
         TcItem it{};
-        it.k0 = 0;
         it.nk = kB / 32;
-        it.epi = (k & 1 ? 2 * n : n) + t;
+        it.epi = n + q * n + t;
         it.m_valid = kB;
         it.n_valid = kB;
         it.o2_row = prow;
         if (R < k) {  // D'[j][i] = (P^-1 Wold[R,K]^T)[j][i] = C_R[i][j] -> W[R0 + i][K0 + j], panC coalesced
-          it.a_map = 2, it.a_row = mats[t].slot * kB;
-          it.b_map = pa, it.b_row = prow;
+          it.a_map = 2, it.a_row = mats[t].slot * kB, it.k0 = 0;
+          it.b_map = 0, it.b_row = prow, it.b_koff = q * kB;
           it.out_r = k * kB, it.out_c = R * kB;
           it.flags = 0;
         } else {      // D[i][j] = C_R[i][j] -> W[K0 + j][R0 + i] (row panel), panC row-style
-          it.a_map = pa, it.a_row = prow;
-          it.b_map = 2, it.b_row = mats[t].slot * kB;
+          it.a_map = 0, it.a_row = prow, it.k0 = q * kB;
+          it.b_map = 2, it.b_row = mats[t].slot * kB, it.b_koff = -q * kB;
           it.out_r = R * kB, it.out_c = k * kB;
           it.flags = kOut2Rows;
         }
@@ -560,51 +566,79 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     }
     p->pan_cnt.push_back(int(items.size()) - p->pan_off.back());
     p->upd_off.push_back(int(items.size()));
-    // U1: tiles in block row/column k+1 (what step k+1's pivot/panel read) first, then U2
+    // Update of step k, split into U1 (issued before step k+1's look-ahead front: it must
+    // see these tiles) and U2 (runs under the front).  Steps are fused in pairs (k even,
+    // k + 1 < T): step k updates only block row/column k+1 (U1) and k+2 (U2); step k+1
+    // updates row/column k+2 (U1) and then every other tile with BOTH steps' panels in one
+    // K = 256 contraction (panel slots k % 4, k % 4 + 1 are adjacent), which halves the
+    // read-modify-write passes over W.  Tiles in row/column k only take step k+1's panel.
     int u1 = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int t : blocked) {  // trailing update: W[I,J] -= Wold[I,K] C_J^T
-        const int T = mats[t].dp / kB;
-        if (k >= T) continue;
-        for (int I = 0; I < T; ++I)
-          for (int J = I; J < T; ++J) {
-            if (I == k || J == k) continue;
-            const bool in_u1 = (I == k + 1 || J == k + 1);
-            if (in_u1 != (pass == 0)) continue;
-            // D'[y][x] = sum_k Wold[J0+y][k] C[I0+x][k] = U[I0+x][J0+y] (U symmetric):
-            // the coalesced transposed store lands on the upper block W[I, J]
-            TcItem it{};
-            it.a_map = (k & 1) ? 3 : 0;
-            it.b_map = (k & 1) ? 4 : 1;
-            it.a_row = mats[t].panel_row0 + J * kB;
-            it.b_row = mats[t].panel_row0 + I * kB;
-            it.k0 = 0;
-            it.nk = kB / 32;
-            it.epi = t;
-            it.flags = 0;
-            it.out_r = J * kB;
-            it.out_c = I * kB;
-            it.m_valid = kB;
-            it.n_valid = kB;
-            items.push_back(it);
-            if (pass == 0) ++u1;
+    std::vector<TcItem> u1v, u2v;
+    for (int t : blocked) {
+      const int T = mats[t].dp / kB;
+      if (k >= T) continue;
+      const bool first = (k % 2 == 0) && k + 1 < T;  // first step of a fused pair
+      const bool second = (k % 2 == 1);               // second step of a pair (k - 1 was the first)
+      const int q = k % kPanSlots;
+      for (int I = 0; I < T; ++I)
+        for (int J = I; J < T; ++J) {
+          if (I == k || J == k) continue;
+          const bool row1 = (I == k + 1 || J == k + 1), row2 = (I == k + 2 || J == k + 2);
+          int k0 = q * kB, nk = kB / 32;
+          bool in_u1;
+          if (first) {
+            if (row1) in_u1 = true;
+            else if (row2) in_u1 = false;
+            else continue;  // deferred to step k+1's fused K = 256 update
+          } else if (second) {
+            in_u1 = row1;
+            const bool row_prev = (I == k - 1 || J == k - 1);
+            if (!row1 && !row_prev) {  // deferred by step k-1: both steps, slots q - 1, q
+              k0 = (q - 1) * kB;
+              nk = 2 * kB / 32;
+            }
+          } else {  // unpaired last step (odd T): classic single-step update
+            in_u1 = row1;
           }
-      }
+          // D'[y][x] = sum_k Wold[J0+y][k] C[I0+x][k] = U[I0+x][J0+y] (U symmetric):
+          // the coalesced transposed store lands on the upper block W[I, J]
+          TcItem it{};
+          it.a_map = 0;
+          it.b_map = 1;
+          it.a_row = mats[t].panel_row0 + J * kB;
+          it.b_row = mats[t].panel_row0 + I * kB;
+          it.k0 = k0;
+          it.nk = nk;
+          it.epi = t;
+          it.flags = 0;
+          it.out_r = J * kB;
+          it.out_c = I * kB;
+          it.m_valid = kB;
+          it.n_valid = kB;
+          (in_u1 ? u1v : u2v).push_back(it);
+        }
     }
+    std::stable_sort(u2v.begin(), u2v.end(), [](const TcItem& a, const TcItem& b) { return a.nk > b.nk; });
+    u1 = int(u1v.size());
+    items.insert(items.end(), u1v.begin(), u1v.end());
+    items.insert(items.end(), u2v.begin(), u2v.end());
+    p->upd_flops.push_back(0.0);
+    for (const TcItem& it : u1v) p->upd_flops.back() += 2.0 * kB * kB * 32 * it.nk;
+    p->u2_flops.push_back(0.0);
+    for (const TcItem& it : u2v) p->u2_flops.back() += 2.0 * kB * kB * 32 * it.nk;
     p->u1_cnt.push_back(u1);
     p->upd_cnt.push_back(int(items.size()) - p->upd_off.back());
   }
   std::vector<CUtensorMap> maps(size_t(5 + p->n_blocked));
   int rc = SPDKFAC_OK;
   if (p->n_blocked > 0) {
-    if ((rc = make_operand_map(&maps[0], p->panA, false, kB, p->plane_rows, kB)) ||
-        (rc = make_operand_map(&maps[1], p->panC, false, kB, p->plane_rows, kB)) ||
-        (rc = make_operand_map(&maps[2], p->pinvS, false, kB, int64_t(p->n_blocked) * kB, kB)) ||
-        (rc = make_operand_map(&maps[3], p->panA + pbuf, false, kB, p->plane_rows, kB)) ||
-        (rc = make_operand_map(&maps[4], p->panC + pbuf, false, kB, p->plane_rows, kB))) {
+    if ((rc = make_operand_map(&maps[0], p->panA, false, kPanCols, p->plane_rows, kPanCols)) ||
+        (rc = make_operand_map(&maps[1], p->panC, false, kPanCols, p->plane_rows, kPanCols)) ||
+        (rc = make_operand_map(&maps[2], p->pinvS, false, kB, int64_t(p->n_blocked) * kB, kB))) {
       delete p;
       return rc;
     }
+    maps[3] = maps[0], maps[4] = maps[1];
     for (int t : blocked)
       if ((rc = make_ctile_map(&maps[5 + mats[t].slot], mats[t].W, mats[t].dp, mats[t].dp, mats[t].dp))) {
         delete p;
@@ -647,7 +681,7 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
     stat_end(kCatInvSmall, s, p->small_flops, 0);
   }
   if (p->n_blocked > 0) {
-    const int64_t plane = p->plane_rows * kB;
+    const int64_t plane = p->plane_rows * kPanCols;
     stat_begin(kCatInvUnpackFinal, s);
     damp_unpack_kernel<<<p->n_tiles, 256, 0, s>>>(p->mats, p->tiles, gamma);
     SPD_CHECK_LAUNCH();
@@ -655,7 +689,7 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
     // step k's pivot -> stage -> panel GEMM on stream q (the critical chain)
     auto front = [&](int k, cudaStream_t q) -> int {
       const int na = p->act_cnt[k];
-      float* pa = p->panA + (k & 1) * 2 * plane;
+      float* pa = p->panA + (k % kPanSlots) * kB;
       stat_begin(kCatInvPivot, q);
       pivot_kernel<<<na, 512, 0, q>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
                                       int64_t(p->n_blocked) * kB * kB);
@@ -678,13 +712,13 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       stat_begin(kCatInvUpdate, s);
       rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k], p->epis, u1, s);
       if (rc) return rc;
-      stat_end(kCatInvUpdate, s, 2.0 * kB * kB * kB * u1, 0);
+      stat_end(kCatInvUpdate, s, p->upd_flops[k], 0);
       const bool ahead = k + 1 < p->steps;
       if (ahead && !p->lookahead) {  // serial order: rest of the update, then the next front
         stat_begin(kCatInvUpdate, s);
         rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k] + u1, p->epis, u2, s);
         if (rc) return rc;
-        stat_end(kCatInvUpdate, s, 2.0 * kB * kB * kB * u2, 0);
+        stat_end(kCatInvUpdate, s, p->u2_flops[k], 0);
         if ((rc = front(k + 1, s))) return rc;
         continue;
       }
@@ -697,7 +731,7 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       stat_begin(kCatInvUpdate, s);
       rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k] + u1, p->epis, u2, s);
       if (rc) return rc;
-      stat_end(kCatInvUpdate, s, 2.0 * kB * kB * kB * u2, 0);
+      stat_end(kCatInvUpdate, s, p->u2_flops[k], 0);
       if (ahead) SPD_CUDA(cudaStreamWaitEvent(s, p->ev_panel, 0));
     }
     stat_begin(kCatInvUnpackFinal, s);

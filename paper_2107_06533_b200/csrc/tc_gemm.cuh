@@ -28,7 +28,7 @@ struct TcItem {
   int32_t out_r, out_c;  // D[i][j] -> target element (out_c + j, out_r + i) (transposed store)
   int32_t m_valid, n_valid;
   int32_t o2_row;  // row offset of the optional second target (TcEpi::out2)
-  int32_t pad_;
+  int32_t b_koff;  // K-major items: B's K coordinate = A's + b_koff (operands in different K columns)
 };
 constexpr int32_t kSameAB = 1;  // B tile == A tile (diagonal SYRK tile): load once
 constexpr int32_t kMirror = 2;  // also update target (out_r + i, out_c + j) (symmetric off-diagonal tile)
@@ -262,8 +262,8 @@ __global__ void __launch_bounds__(192, 1)
             tma_load_3d(st, am, &full[s], kc, it.a_row, 0);
             tma_load_3d(st + kTileBytes, am, &full[s], kc, it.a_row, 1);
             if (!same) {
-              tma_load_3d(st + 2 * kTileBytes, bm, &full[s], kc, it.b_row, 0);
-              tma_load_3d(st + 3 * kTileBytes, bm, &full[s], kc, it.b_row, 1);
+              tma_load_3d(st + 2 * kTileBytes, bm, &full[s], kc + it.b_koff, it.b_row, 0);
+              tma_load_3d(st + 3 * kTileBytes, bm, &full[s], kc + it.b_koff, it.b_row, 1);
             }
           }
         }
