@@ -202,6 +202,8 @@ def trace_summary(step, path, torch, n=3):
         torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type.name == "CUDA" and e.time_range.elapsed_us() > 0]
     ks = sorted(((e.time_range.start, e.time_range.end, e.name, getattr(e, "device_resource_id", 0)) for e in evs))
+    if path is None:
+        return
     if not ks:
         json.dump({"error": "no CUDA events"}, open(path, "w"))
         return
@@ -223,9 +225,32 @@ def trace_summary(step, path, torch, n=3):
         c[1] += 1
         per_stream[str(sid)] = per_stream.get(str(sid), 0.0) + (e0 - s0)
     top = sorted(per_name.items(), key=lambda kv: -kv[1][0])[:40]
+    # phase windows of the LAST traced step (from its first kernel), by kernel family
+    import re
+    fam = {"fwd_bwd (cudnn/cutlass/aten)": r"cudnn|cutlass3x|sm80_xmma|at::native|Memset|max_pool",
+           "factor stage": r"stage_rows|stage_im2col|stage_spatial", "factor syrk": r"tc3_gemm_kernel<\(spd::Kind\)1, 3|tc3_pair",
+           "factor reduce": r"reduce_pack", "inv pivot": r"pivot_kernel", "inv update": r"Kind\)2, 2, true",
+           "inv panel": r"stage_panel|Kind\)2, 3, false", "inv unpack/finalize": r"damp_unpack|finalize_kernel|small_inverse",
+           "precond": r"split_rows_batched|apply_update|tc3_gemm_kernel<\(spd::Kind\)1, 3, false>.*", "nccl": r"nccl",
+           "pack/unpack": r"pack_upper|unpack_upper"}
+    step_len = (t1 - t0) / n
+    last0 = t0 + (n - 1) * step_len
+    phases = {}
+    for s0, e0, nm, _ in ks:
+        if s0 < last0:
+            continue
+        for f, rx in fam.items():
+            if re.search(rx, nm):
+                w = phases.setdefault(f"{f} @stream{sid}", [s0, e0, 0.0])
+                w[0], w[1], w[2] = min(w[0], s0), max(w[1], e0), w[2] + (e0 - s0)
+                break
+    phases = {f: {"first_ms": round((w[0] - last0) / 1e3, 3), "last_ms": round((w[1] - last0) / 1e3, 3),
+                  "busy_ms": round(w[2] / 1e3, 3)} for f, w in sorted(phases.items(), key=lambda kv: kv[1][1])
+              if w[2] > 20.0}
     out = {"steps": n, "span_ms_per_step": (t1 - t0) / 1e3 / n, "gpu_busy_union_ms_per_step": busy / 1e3 / n,
            "kernel_sum_ms_per_step": sum(v[0] for v in per_name.values()) / 1e3 / n,
            "per_stream_ms_per_step": {k: v / 1e3 / n for k, v in sorted(per_stream.items(), key=lambda kv: -kv[1])},
+           "last_step_phases": phases,
            "top": [{"name": k, "ms_per_step": v[0] / 1e3 / n, "count_per_step": v[1] / n} for k, v in top]}
     json.dump(out, open(path, "w"), indent=1)
 
@@ -362,8 +387,8 @@ def run_ours(a):
     # captured event nodes hold the last replay's timestamps
     per = 1 if graphed else a.steps
     launches = st["total_launches"] * (a.steps if graphed else 1)
-    if a.trace and rank == 0:
-        trace_summary(step, a.trace, torch)
+    if a.trace:  # every rank steps (collectives); rank 0 writes
+        trace_summary(step, a.trace if rank == 0 else None, torch)
     # per-category breakdown: a separate 2-step eager pass with every launch bracketed by events
     nb = 2
     _lib.stats_reset(timing=True, reserve=600 * nb)

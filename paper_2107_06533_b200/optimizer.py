@@ -519,26 +519,35 @@ class SPDKFAC(torch.optim.Optimizer):
             main.wait_stream(self.factor_stream)
             self._factor_updates += 1
             self._tl("g_factors_done", main)
+        factors_reduced = None
         if self.world > 1:
+            cs = self.comm_stream
             if invert_now:
                 if not self._a_inverted:  # hooks did not see a full forward (e.g. factors reused)
                     self._launch_inverse_A()
                 if not self._g1_inverted:
                     self._launch_inverse_G1()
+            # every factor all-reduce of this iteration is enqueued: G2's inversion waits for
+            # exactly these, not for the broadcasts and the gradient all-reduce queued behind
+            factors_reduced = torch.cuda.Event()
+            factors_reduced.record(cs)
+            if invert_now:
                 self._exchange_send("A", self.inv_stream)
                 self._exchange_send("G1", self.inv_stream2)
-            cs = self.comm_stream
             cs.wait_stream(main)
             grads = [p.grad for p in self.param_groups[0]["params"] if p.grad is not None]
             with self.comm.group():
                 for g in grads:
                     self.comm.allreduce_sum(g, cs)
-            main.wait_stream(cs)  # also orders the factor all-reduces before inversion
+            if not invert_now:
+                main.wait_stream(cs)
         if invert_now:
             if not self._a_inverted:  # hooks did not see a full forward (e.g. factors reused)
                 self._launch_inverse_A()
             if not self._g1_inverted:
                 self._launch_inverse_G1()
+            if factors_reduced is not None:
+                main.wait_event(factors_reduced)
             self._run_inverse("G2", main, exchange=False)
             self._tl("g_inverse_done", main)
             main.wait_stream(self.inv_stream)   # A inverses landed
