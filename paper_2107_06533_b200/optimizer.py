@@ -195,6 +195,7 @@ class SPDKFAC(torch.optim.Optimizer):
         self._g_count = 0
         self._g1_inverted = False
         self._sent = {"A": False, "G1": False, "G2": False}
+        self._grad_src = {}
         self.comm_stream = torch.cuda.Stream(self.device) if self.world > 1 else None
         self._info_events = []
         self._a_count = 0
@@ -535,10 +536,12 @@ class SPDKFAC(torch.optim.Optimizer):
                 self._exchange_send("A", self.inv_stream)
                 self._exchange_send("G1", self.inv_stream2)
             cs.wait_stream(main)
-            grads = [p.grad for p in self.param_groups[0]["params"] if p.grad is not None]
-            with self.comm.group():
-                for g in grads:
-                    self.comm.allreduce_sum(g, cs)
+            params = [p for p in self.param_groups[0]["params"] if p.grad is not None]
+            flat, views = self._flat_grad_buffer(params)
+            with torch.cuda.stream(cs):  # one contiguous all-reduce instead of one per parameter
+                torch._foreach_copy_(views, [p.grad for p in params])
+            self.comm.allreduce_sum(flat, cs)
+            self._grad_src = {id(p): v for p, v in zip(params, views)}
             if not invert_now:
                 main.wait_stream(cs)
         if invert_now:
@@ -560,7 +563,11 @@ class SPDKFAC(torch.optim.Optimizer):
             self._tl("inverses_joined", main)
         # precondition + update for every K-FAC layer (mean gradient = sum / P); the pointer
         # tables are rebuilt only when a gradient's storage changes (zero_grad(set_to_none=True))
-        key = tuple(l.module.weight.grad.data_ptr() if l.module.weight.grad is not None else 0 for l in self.layers)
+        # P > 1: the all-reduced gradient lives in the flat buffer (same shapes and strides)
+        src = self._grad_src if self.world > 1 else {}
+        grad_of = lambda p: src.get(id(p), p.grad)  # noqa: E731
+        key = tuple(grad_of(l.module.weight).data_ptr() if l.module.weight.grad is not None else 0
+                    for l in self.layers)
         if key != self._precond_key:
             if 0 in key:
                 missing = [l.name for l in self.layers if l.module.weight.grad is None]
@@ -569,7 +576,7 @@ class SPDKFAC(torch.optim.Optimizer):
                 if l.is_conv:
                     l.w_cl = self._weight_channels_last(l.module)
             self._precond.bind([self.inv[2 * l.index + 1] for l in self.layers],
-                               [self._weight_matrix(l, l.module.weight.grad) for l in self.layers],
+                               [self._weight_matrix(l, grad_of(l.module.weight)) for l in self.layers],
                                [self.inv[2 * l.index] for l in self.layers],
                                weights=[self._weight_matrix(l, l.module.weight.data) for l in self.layers])
             self._precond_key = key
@@ -577,7 +584,7 @@ class SPDKFAC(torch.optim.Optimizer):
         self._tl("precond_done", main)
         others = [p for p in self.other_params if p.grad is not None]
         if others:
-            torch._foreach_add_([p.data for p in others], [p.grad for p in others], alpha=-lr / self.world)
+            torch._foreach_add_([p.data for p in others], [grad_of(p) for p in others], alpha=-lr / self.world)
         self._a_count = 0
         self._a_inverted = False
         self._g_count = 0
@@ -592,6 +599,24 @@ class SPDKFAC(torch.optim.Optimizer):
             self.steps += 1
             self._capture = self.steps % self.factor_update_freq == 0
         return loss
+
+    def _flat_grad_buffer(self, params):
+        """One fp32 buffer holding every gradient (views with each gradient's shape and
+        strides, e.g. channels-last conv weights), allocated once per parameter layout."""
+        layout = tuple((tuple(p.grad.shape), tuple(p.grad.stride()), p.grad.dtype) for p in params)
+        if getattr(self, "_flat_layout", None) != layout:
+            dense = lambda g: g.is_contiguous() or (g.dim() == 4 and g.is_contiguous(memory_format=torch.channels_last))  # noqa: E731
+            if any(not dense(p.grad) or p.grad.dtype != torch.float32 for p in params):
+                raise RuntimeError("gradients must be dense float32 tensors")
+            total = sum(p.grad.numel() for p in params)
+            flat = torch.empty(total, dtype=torch.float32, device=self.device)
+            views, off = [], 0
+            for p in params:
+                n = p.grad.numel()
+                views.append(flat[off:off + n].as_strided(p.grad.shape, p.grad.stride()))
+                off += n
+            self._flat, self._flat_views, self._flat_layout = flat, views, layout
+        return self._flat, self._flat_views
 
     def _after_replay(self, stream) -> None:
         """Bookkeeping for one replay of a captured step (GraphedStep): the Python side
