@@ -181,6 +181,11 @@ SPDKFAC_API int spdkfac_comm_unique_id(void* id_out /* 128 bytes */);
 SPDKFAC_API int spdkfac_comm_create(spdkfac_comm** out, const void* id /* 128 bytes */, int rank, int world);
 SPDKFAC_API int spdkfac_comm_allreduce_sum_f32(spdkfac_comm* c, float* buf, size_t count, void* stream);
 SPDKFAC_API int spdkfac_comm_bcast_f32(spdkfac_comm* c, float* buf, size_t count, int root, void* stream);
+/* In-place sum onto `root` only (the other ranks' buffers are left unchanged).  Replaces the
+ * all-reduce of a CT factor, whose aggregate only its inverse's owner reads (factor_decay == 0):
+ * the reference's _mean_sym (emulator.py:199-200) restricted to the placement walk's owner
+ * (emulator.py:247-262). */
+SPDKFAC_API int spdkfac_comm_reduce_sum_f32(spdkfac_comm* c, float* buf, size_t count, int root, void* stream);
 SPDKFAC_API int spdkfac_comm_group_start(void);
 SPDKFAC_API int spdkfac_comm_group_end(void);
 SPDKFAC_API void spdkfac_comm_destroy(spdkfac_comm* c);

@@ -66,6 +66,7 @@ SIGNATURES = {
     "spdkfac_comm_create": (C.c_int, [C.POINTER(_vp), _vp, C.c_int, C.c_int]),
     "spdkfac_comm_allreduce_sum_f32": (C.c_int, [_vp, _vp, _sz, _vp]),
     "spdkfac_comm_bcast_f32": (C.c_int, [_vp, _vp, _sz, C.c_int, _vp]),
+    "spdkfac_comm_reduce_sum_f32": (C.c_int, [_vp, _vp, _sz, C.c_int, _vp]),
     "spdkfac_comm_group_start": (C.c_int, []),
     "spdkfac_comm_group_end": (C.c_int, []),
     "spdkfac_comm_destroy": (None, [_vp]),

@@ -41,6 +41,10 @@ class NcclComm:
         L.check(self._lib.spdkfac_comm_bcast_f32(self._h, buf.data_ptr(), buf.numel(), int(root), stream.cuda_stream),
                 "broadcast")
 
+    def reduce_sum(self, buf: torch.Tensor, root: int, stream) -> None:
+        L.check(self._lib.spdkfac_comm_reduce_sum_f32(self._h, buf.data_ptr(), buf.numel(), int(root),
+                                                     stream.cuda_stream), "reduce")
+
     @contextmanager
     def group(self):
         L.check(self._lib.spdkfac_comm_group_start(), "group start")

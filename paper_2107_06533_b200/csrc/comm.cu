@@ -61,6 +61,13 @@ int spdkfac_comm_bcast_f32(spdkfac_comm* c, float* buf, size_t count, int root, 
   return SPDKFAC_OK;
 }
 
+int spdkfac_comm_reduce_sum_f32(spdkfac_comm* c, float* buf, size_t count, int root, void* stream) {
+  SPD_ARG(c && (buf || count == 0) && root >= 0 && root < c->world, SPDKFAC_ERR_ARG, "bad reduce arguments");
+  if (count == 0) return SPDKFAC_OK;
+  SPD_NCCL(ncclReduce(buf, buf, count, ncclFloat32, ncclSum, root, c->comm, static_cast<cudaStream_t>(stream)));
+  return SPDKFAC_OK;
+}
+
 int spdkfac_comm_group_start(void) {
   SPD_NCCL(ncclGroupStart());
   return SPDKFAC_OK;

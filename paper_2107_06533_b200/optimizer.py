@@ -79,13 +79,18 @@ class SPDKFAC(torch.optim.Optimizer):
                  factor_update_freq: int = 1, inv_update_freq: int = 1, fusion: FusionPolicy = FusionPolicy.OPTIMAL,
                  placement: str = "lbp", balance: str = "dim_sq", perf: Optional[PerfParams] = None,
                  batch_averaged: bool = True, layer_times: Optional[dict] = None, comm=None,
-                 early_g_fraction: float = 0.85):
+                 early_g_fraction: float = 0.85, factor_comm: str = "auto"):
         if damping < 0:
             raise ValueError(f"damping must be nonnegative, got {damping}")
         if not 0.0 <= factor_decay < 1.0:
             raise ValueError(f"factor_decay must be in [0, 1), got {factor_decay}")
         if factor_update_freq < 1 or inv_update_freq < 1 or inv_update_freq % factor_update_freq:
             raise ValueError("update frequencies must be >= 1 and inv_update_freq a multiple of factor_update_freq")
+        if factor_comm not in ("auto", "allreduce", "reduce"):
+            raise ValueError(f"factor_comm must be 'auto', 'allreduce' or 'reduce', got {factor_comm!r}")
+        if factor_comm == "reduce" and factor_decay != 0.0:
+            raise ValueError("factor_comm='reduce' needs factor_decay == 0 (the running average needs the aggregate "
+                             "on every rank)")
         if placement not in ("lbp", "seq", "local"):
             raise ValueError(f"placement must be 'lbp', 'seq' or 'local', got {placement!r}")
         L.load(require_device=True)
@@ -160,6 +165,12 @@ class SPDKFAC(torch.optim.Optimizer):
         self._gslice = {"A": [self._groups_fwd[g[-1].layer_index - 1] for g in self.fwd_plan.groups],
                         "G": [self._groups_bwd[g[-1].layer_index - 1] for g in self.bwd_plan.groups]}
         self._gseen = {"A": [0] * len(self.fwd_plan.groups), "G": [0] * len(self.bwd_plan.groups)}
+        # factor aggregation: all-reduce (every rank holds every aggregate, needed for a running
+        # average) or, with factor_decay == 0, a sum onto the owner of each CT inverse only
+        # (half the traffic; NCT factors are still all-reduced)
+        self.factor_comm = ("reduce" if factor_decay == 0.0 else "allreduce") if factor_comm == "auto" else factor_comm
+        self._gsegs = {"A": S.reduce_segments(self.fwd_plan, a_off, a_dims, self.placement, 0),
+                       "G": S.reduce_segments(self.bwd_plan, g_off, g_dims, self.placement, 1)}
         self._fgroups = None  # per fusion group FactorGroup objects, built after the first iteration
         self._rec = {"A": [None] * len(self.layers), "G": [None] * len(self.layers)}
 
@@ -375,10 +386,18 @@ class SPDKFAC(torch.optim.Optimizer):
             fg["pending"] = not capturing
             fg["seen"] = 0
         if self.world > 1:
-            s, e = self._gslice[kind][gid]
             cs = self.comm_stream
             cs.wait_stream(fs)
-            self.comm.allreduce_sum(buf[s:e], cs)
+            if self.factor_comm == "reduce":
+                with self.comm.group():
+                    for s, e, root in self._gsegs[kind][gid]:
+                        if root is None:
+                            self.comm.allreduce_sum(buf[s:e], cs)
+                        else:
+                            self.comm.reduce_sum(buf[s:e], root, cs)
+            else:
+                s, e = self._gslice[kind][gid]
+                self.comm.allreduce_sum(buf[s:e], cs)
         if kind == "G" and gid in self._g1_groups:
             self._g1_left -= 1
             if self._g1_left == 0:
@@ -664,7 +683,9 @@ class SPDKFAC(torch.optim.Optimizer):
 
     # ------------------------------------------------------------------ introspection / checkpoint
     def factor(self, layer: int, kind: str) -> torch.Tensor:
-        """Current aggregated (running-average) factor of a layer as a full matrix."""
+        """Current aggregated (running-average) factor of a layer as a full matrix.  With
+        factor_comm == "reduce" and P > 1 only the owner of the factor's inverse holds the
+        aggregate (placement.owner(2 layer + side)); other ranks hold their own contribution."""
         from .linalg import unpack_upper
         t = 2 * layer + (0 if kind == "A" else 1)
         return unpack_upper(self._packed(t), self.inv[t].shape[0])

@@ -59,6 +59,28 @@ def fusion_members(plan: FusionPlan) -> tuple:
     return gid, sizes
 
 
+def reduce_segments(plan: FusionPlan, offsets: Sequence[int], dims: Sequence[int], placement: PlacementPlan,
+                    parity: int) -> list:
+    """Per fusion group (plan order): [(start, end, root)] covering the group's slice, where root is
+    the owner rank of a CT factor's inverse (its aggregate is read only there: reduce) or None
+    for an NCT factor (every rank inverts it: all-reduce).  Adjacent factors with the same root
+    share one segment.  parity 0 = A (tensor 2l), 1 = G (tensor 2l+1)."""
+    out = []
+    for group in plan.groups:
+        idx = sorted((t.layer_index - 1 for t in group), key=lambda li: offsets[li])
+        segs = []
+        for li in idx:
+            t = 2 * li + parity
+            root = None if t in placement.nct else placement.owner(t)
+            s, e = offsets[li], offsets[li] + packed_size(dims[li])
+            if segs and segs[-1][2] == root and segs[-1][1] == s:
+                segs[-1] = (segs[-1][0], e, root)
+            else:
+                segs.append((s, e, root))
+        out.append(segs)
+    return out
+
+
 def check_fusion_cover(slices: dict, total: int) -> None:
     """The groups of one pass tile its fusion buffer exactly once (no gap, no overlap)."""
     spans = sorted(slices.values())

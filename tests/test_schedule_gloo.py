@@ -5,7 +5,8 @@ fusion groups and owner broadcasts SPDKFAC uses -- with the float64 oracle stand
 for the CUDA kernels, and the gloo collectives performing the real exchanges:
 
   factors packed into the fusion buffers pre-scaled by 1/P, one all_reduce per fusion group
-  in plan order (forward: A, backward: G); gradient all_reduce; LBP placement; each rank
+  in plan order (forward: A, backward: G) -- or, factor_comm "reduce", each CT factor summed
+  onto its inverse's owner only; gradient all_reduce; LBP placement; each rank
   inverts its own share; CT inverses broadcast in packed form from their owners; update.
 
 The result must equal the reference's centralized step on the union batch (the frozen
@@ -40,7 +41,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank_main(rank, world, port, placement_mode, out_dir):
+def _rank_main(rank, world, port, placement_mode, out_dir, factor_comm="allreduce"):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     fx = json.loads((GOLD / "aggregated_step_w4.json").read_text())
     weights = [np.array(w) for w in fx["weights"]]
@@ -62,22 +63,6 @@ def _rank_main(rank, world, port, placement_mode, out_dir):
     sl_a, sl_g = S.fusion_slices(fwd, a_off, a_dims), S.fusion_slices(bwd, g_off, g_dims)
     S.check_fusion_cover(sl_a, sa)
     S.check_fusion_cover(sl_g, sg)
-    buf_a, buf_g = torch.zeros(sa, dtype=torch.float64), torch.zeros(sg, dtype=torch.float64)
-    for l in range(nl):  # forward pass order
-        d = a_dims[l]
-        buf_a[a_off[l]:a_off[l] + d * (d + 1) // 2] = torch.from_numpy(O.pack_upper(O.factor_A(ins[l])) / world)
-        if l in sl_a:
-            s, e = sl_a[l]
-            dist.all_reduce(buf_a[s:e])
-    for l in reversed(range(nl)):  # backward pass order
-        d = g_dims[l]
-        buf_g[g_off[l]:g_off[l] + d * (d + 1) // 2] = torch.from_numpy(O.pack_upper(O.factor_G(gs[l])) / world)
-        if l in sl_g:
-            s, e = sl_g[l]
-            dist.all_reduce(buf_g[s:e])
-    grads = [torch.from_numpy(np.ascontiguousarray(g)) for g in dws]
-    for g in grads:
-        dist.all_reduce(g)
     dims = [d for l in range(nl) for d in (a_dims[l], g_dims[l])]
     tasks = P.inverse_tasks(specs)
     if placement_mode == "lbp":  # all-CT calibration: every inverse travels from its owner
@@ -86,6 +71,36 @@ def _rank_main(rank, world, port, placement_mode, out_dir):
         plan = P.lbp_place(tasks, world, InverseParams(1e-9, 1e-9), BcastParams(10.0, 1e-9))
     else:
         plan = P.seq_place(tasks, world)
+    # factor_comm "reduce": each group's CT factors are summed onto their inverse's owner only
+    # (schedule.reduce_segments), NCT ones all-reduced -- what SPDKFAC does for factor_decay == 0
+    seg_a = dict(zip([g[-1].layer_index - 1 for g in fwd.groups], S.reduce_segments(fwd, a_off, a_dims, plan, 0)))
+    seg_g = dict(zip([g[-1].layer_index - 1 for g in bwd.groups], S.reduce_segments(bwd, g_off, g_dims, plan, 1)))
+
+    def aggregate(buf, sl, segs):
+        if factor_comm == "allreduce":
+            s, e = sl
+            dist.all_reduce(buf[s:e])
+            return
+        for s, e, root in segs:
+            if root is None:
+                dist.all_reduce(buf[s:e])
+            else:
+                dist.reduce(buf[s:e], dst=root)
+
+    buf_a, buf_g = torch.zeros(sa, dtype=torch.float64), torch.zeros(sg, dtype=torch.float64)
+    for l in range(nl):  # forward pass order
+        d = a_dims[l]
+        buf_a[a_off[l]:a_off[l] + d * (d + 1) // 2] = torch.from_numpy(O.pack_upper(O.factor_A(ins[l])) / world)
+        if l in sl_a:
+            aggregate(buf_a, sl_a[l], seg_a[l])
+    for l in reversed(range(nl)):  # backward pass order
+        d = g_dims[l]
+        buf_g[g_off[l]:g_off[l] + d * (d + 1) // 2] = torch.from_numpy(O.pack_upper(O.factor_G(gs[l])) / world)
+        if l in sl_g:
+            aggregate(buf_g, sl_g[l], seg_g[l])
+    grads = [torch.from_numpy(np.ascontiguousarray(g)) for g in dws]
+    for g in grads:
+        dist.all_reduce(g)
 
     def packed(ti):
         l, side = ti // 2, ti % 2
@@ -117,10 +132,13 @@ def _rank_main(rank, world, port, placement_mode, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,placement", [(2, "lbp"), (2, "lbp_nct"), (2, "seq"), (4, "lbp")])
-def test_multirank_schedule_reproduces_centralized_step(tmp_path, world, placement):
+@pytest.mark.parametrize("world,placement,factor_comm", [(2, "lbp", "allreduce"), (2, "lbp_nct", "allreduce"),
+                                                        (2, "seq", "allreduce"), (4, "lbp", "allreduce"),
+                                                        (2, "seq", "reduce"), (4, "lbp", "reduce"),
+                                                        (2, "lbp_nct", "reduce")])
+def test_multirank_schedule_reproduces_centralized_step(tmp_path, world, placement, factor_comm):
     port = _free_port()
-    mp.spawn(_rank_main, args=(world, port, placement, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_rank_main, args=(world, port, placement, str(tmp_path), factor_comm), nprocs=world, join=True)
     for r in range(world):
         err, same = np.load(tmp_path / f"r{r}.npy")
         assert err < 1e-8, (r, err)
