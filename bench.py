@@ -192,18 +192,34 @@ def cpu_reference(model, batch, steps=None, budget_s=30.0):
 
 
 # ---------------------------------------------------------------- diagnostics
-def trace_summary(step, path, torch, n=3):
-    """CUPTI kernel timeline of n steps: GPU busy union per step, per-stream busy, top kernels."""
+def trace_summary(step, path, torch, n=3, comm_tags=None):
+    """CUPTI kernel timeline of n steps: GPU busy union per step, per-stream busy, top kernels,
+    and the six-category breakdown of the last step (breakdown.py) next to `path`."""
     from torch.profiler import ProfilerActivity, profile
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for i in range(n):
+            torch.cuda._sleep(1000)  # step delimiter kernel (outside the graph)
             step(i)
         torch.cuda.synchronize()
     evs = [e for e in prof.events() if e.device_type.name == "CUDA" and e.time_range.elapsed_us() > 0]
     ks = sorted(((e.time_range.start, e.time_range.end, e.name, getattr(e, "device_resource_id", 0)) for e in evs))
     if path is None:
         return
+    marks = [k for k in ks if "spin_kernel" in k[2] or "sleep" in k[2].lower()]
+    if len(marks) >= n:
+        from paper_2107_06533_b200 import breakdown as BD
+        w0 = marks[-1][1]
+        last = [(s0, e0, nm, sid) for s0, e0, nm, sid in ks if s0 >= w0]
+        if comm_tags is None or sum(BD.is_nccl(k[2]) for k in last) != len(comm_tags):
+            comm_tags = ["inverse" if "broadcast" in k[2].lower() else "factor" for k in last if BD.is_nccl(k[2])]
+        lab = BD.label_events(last, comm_tags)
+        tot = BD.breakdown(lab, start=w0)
+        base = os.path.splitext(path)[0]
+        open(base + "_breakdown.csv", "w").write(BD.breakdown_to_csv({k: v * 1e-6 for k, v in tot.items()}))
+        open(base + "_timeline.csv", "w").write(BD.timeline_to_csv([(s0 * 1e-6, e0 * 1e-6, nm, sid, c)
+                                                                    for s0, e0, nm, sid, c in lab], t0=w0 * 1e-6))
+    ks = [k for k in ks if k not in marks]
     if not ks:
         json.dump({"error": "no CUDA events"}, open(path, "w"))
         return
@@ -236,7 +252,7 @@ def trace_summary(step, path, torch, n=3):
     step_len = (t1 - t0) / n
     last0 = t0 + (n - 1) * step_len
     phases = {}
-    for s0, e0, nm, _ in ks:
+    for s0, e0, nm, sid in ks:
         if s0 < last0:
             continue
         for f, rx in fam.items():
@@ -388,7 +404,13 @@ def run_ours(a):
     per = 1 if graphed else a.steps
     launches = st["total_launches"] * (a.steps if graphed else 1)
     if a.trace:  # every rank steps (collectives); rank 0 writes
-        trace_summary(step, a.trace if rank == 0 else None, torch)
+        tags = None
+        if world > 1:  # program order of this rank's collectives over one (eager) iteration
+            opt.comm.log.clear()
+            eager_step(0)
+            torch.cuda.synchronize()
+            tags = list(opt.comm.log)
+        trace_summary(step, a.trace if rank == 0 else None, torch, comm_tags=tags)
     # per-category breakdown: a separate 2-step eager pass with every launch bracketed by events
     nb = 2
     _lib.stats_reset(timing=True, reserve=600 * nb)

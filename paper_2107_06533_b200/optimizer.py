@@ -559,7 +559,7 @@ class SPDKFAC(torch.optim.Optimizer):
             flat, views = self._flat_grad_buffer(params)
             with torch.cuda.stream(cs):  # one contiguous all-reduce instead of one per parameter
                 torch._foreach_copy_(views, [p.grad for p in params])
-            self.comm.allreduce_sum(flat, cs)
+            self.comm.allreduce_sum(flat, cs, tag="grad")
             self._grad_src = {id(p): v for p, v in zip(params, views)}
             if not invert_now:
                 main.wait_stream(cs)
