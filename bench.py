@@ -69,8 +69,11 @@ def parse():
     p.add_argument("--trace", default=None,
                    help="diagnostic: torch.profiler (CUPTI) trace of 3 steps after the timed region; writes a "
                         "kernel-timeline summary JSON to this path")
-    p.add_argument("--g1-fraction", type=float, default=0.85,
-                   help="share of the output-side inversion work (sum g^3) inverted during backward")
+    p.add_argument("--g-fractions", default="0.85,0.983,0.9985",
+                   help="cumulative shares of the output-side inversion work (sum g^3) at which the early G "
+                        "inversion groups are cut (comma list; the rest is inverted in step())")
+    p.add_argument("--launch-groups", choices=("auto", "fusion", "inversion"), default="auto",
+                   help="factor SYRK launch groups: the fusion plan (P>1 default) or few large groups (P=1 default)")
     p.add_argument("--clocks", choices=("nvml", "smi", "off"), default="nvml")
     p.add_argument("--timeline", action="store_true", help="diagnostic: per-phase CUDA-event timeline of one eager step")
     p.add_argument("--stats-off", action="store_true", help="no per-launch CUDA events in the timed region (diagnostic)")
@@ -83,7 +86,10 @@ def workload_config(a, world):
     return {"workload": f"{a.model} SPD-KFAC bs{a.batch}/GPU synthetic {'32x32' if a.model == 'resnet20' else '224x224'}"
                         f" (BASELINE.json configs[{1 if world == 1 else 2}])",
             "per_gpu_batch": a.batch, "global_batch": a.batch * world, "damping": a.damping, "lr": a.lr,
-            "factor_update_freq": a.factor_freq, "inv_update_freq": a.inv_freq, "fusion": "optimal",
+            "factor_update_freq": a.factor_freq, "inv_update_freq": a.inv_freq,
+            "fusion": "optimal" if world > 1 or a.launch_groups == "fusion" else
+                      "none at P=1 (no factor comm): SYRK launch groups = A in 2 halves, G at the inversion groups",
+            "g_inversion_fractions": a.g_fractions,
             "placement": a.placement, "parallelism": f"dp{world}", "python_gc": a.gc,
             "execution": "one CUDA graph per iteration (fwd+bwd+K-FAC step)" if a.mode == "graph" else "eager",
             "memory_format": a.memory_format,
@@ -301,7 +307,8 @@ def run_ours(a):
         opt.placement = None
     else:
         opt = SPDKFAC(model, lr=a.lr, damping=a.damping, factor_update_freq=a.factor_freq,
-                      inv_update_freq=a.inv_freq, placement=a.placement, early_g_fraction=a.g1_fraction)
+                      inv_update_freq=a.inv_freq, placement=a.placement,
+                      early_g_fraction=tuple(float(f) for f in a.g_fractions.split(",")), launch_groups=a.launch_groups)
     crit = nn.CrossEntropyLoss()
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)

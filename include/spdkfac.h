@@ -161,7 +161,10 @@ SPDKFAC_API void spdkfac_inverse_plan_destroy(spdkfac_inverse_plan* p);
  *   P_l = G_l^-1 . grad_l . A_l^-1      ([d_out][d_in] row-major)
  *   W_l <- W_l - alpha * P_l            (skipped when weight == NULL)
  *   precond_out_l <- P_l                (skipped when precond_out == NULL)
- * Two tcgen05 3 x bf16 GEMMs per layer, batched over layers. */
+ * Two tcgen05 3 x bf16 GEMMs per layer, batched over layers.
+ * a_inv / g_inv == NULL: that side's inverses were already staged into the plan's
+ * split-precision operands by spdkfac_precond_plan_stage_inverses (e.g. on the stream that
+ * inverted them, while the backward pass still runs), so run() only splits the gradients. */
 typedef struct spdkfac_precond_plan spdkfac_precond_plan;
 SPDKFAC_API size_t spdkfac_precond_workspace_size(int n, const int32_t* d_out, const int32_t* d_in);
 SPDKFAC_API int spdkfac_precond_plan_create(spdkfac_precond_plan** out, int n, const int32_t* d_out, const int32_t* d_in,
@@ -169,6 +172,10 @@ SPDKFAC_API int spdkfac_precond_plan_create(spdkfac_precond_plan** out, int n, c
 SPDKFAC_API int spdkfac_precond_plan_run(spdkfac_precond_plan* p, const float* const* g_inv, const float* const* grad,
                              const float* const* a_inv, float* const* weight, float alpha, float* const* precond_out,
                              void* stream);
+/* Stage the inverses of n_sel layers (layers[i] indexes the plan's layers; inv[i] its full
+ * fp32 inverse) into the plan's bf16 hi/lo operand planes: which = 0 for A^-1, 1 for G^-1. */
+SPDKFAC_API int spdkfac_precond_plan_stage_inverses(spdkfac_precond_plan* p, int which, int n_sel, const int32_t* layers,
+                                                    const float* const* inv, void* stream);
 SPDKFAC_API void spdkfac_precond_plan_destroy(spdkfac_precond_plan* p);
 
 /* ------------------------------------------------------------------ collectives

@@ -41,7 +41,7 @@ struct InvMat {
   int32_t slot;        // index among blocked matrices (row slot*128 of the P^-1 planes)
 };
 
-struct TileJob {  // one 32 x 32 tile (I <= J) of a blocked matrix, for unpack/finalize
+struct TileJob {  // one 64 x 64 tile (I <= J) of a blocked matrix, for unpack/finalize
   int32_t mat, ti, tj, pad_;
 };
 
@@ -216,34 +216,41 @@ __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __rest
 }
 
 // ---------------------------------------------------------------- blocked path
-// W = unpack(packed) + gamma I, identity padding; one 32x32 tile pair (I,J),(J,I) per block.
+// W = unpack(packed) + gamma I, identity padding; one 64x64 tile (I <= J) per block, 256
+// threads x 16 elements, every load issued before the first store.  Only the upper block
+// triangle of W is ever read (pivot: diagonal 128-blocks; panel, update, finalize: blocks
+// (I, J) with I <= J), so the mirrored (J, I) tile is written only inside a diagonal
+// 128-block.
+constexpr int kT = 64;  // unpack / finalize tile edge
 __global__ void __launch_bounds__(256) damp_unpack_kernel(const InvMat* __restrict__ mats,
                                                           const TileJob* __restrict__ jobs, float gamma) {
-  __shared__ float tile[32][33];
+  __shared__ float tile[kT][kT + 1];
   const TileJob jb = jobs[blockIdx.x];
   const InvMat m = mats[jb.mat];
   const int64_t d = m.d, dp = m.dp;
   if (jb.ti == 0 && jb.tj == 0 && threadIdx.x == 0) *m.info = 0;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  const int64_t i0 = int64_t(jb.ti) * 32, j0 = int64_t(jb.tj) * 32;
-  for (int r = ty; r < 32; r += 8) {  // row i = i0 + r of the upper tile: contiguous in packed row i
-    const int64_t i = i0 + r, j = j0 + tx;
-    float v;
-    if (i < d && j < d) v = (j >= i) ? m.in[i * (2 * d - i + 1) / 2 + (j - i)] : 0.f;
-    else v = (i == j) ? 1.f : 0.f;
-    if (i == j && i < d) v += gamma;
-    tile[r][tx] = v;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+  const int64_t i0 = int64_t(jb.ti) * kT, j0 = int64_t(jb.tj) * kT;
+  const bool diag = jb.ti == jb.tj;
+  const bool mirror = !diag && (jb.ti >> 1) == (jb.tj >> 1);  // both halves of a diagonal 128-block
+  float v[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int64_t i = i0 + ty + 4 * u, j = j0 + tx;
+    const int64_t r = i < j ? i : j, c = i < j ? j : i;  // diagonal tile: the lower half reads (j, i)
+    v[u] = (c < d) ? __ldcs(m.in + r * (2 * d - r + 1) / 2 + (c - r)) : 0.f;
   }
-  __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    const int64_t i = i0 + r, j = j0 + tx;
-    if (jb.ti == jb.tj) {  // diagonal tile: mirror the upper part inside the tile
-      const float v = (tx >= r) ? tile[r][tx] : tile[tx][r];
-      m.W[i * dp + j] = v;
-    } else {
-      m.W[i * dp + j] = tile[r][tx];                      // (I, J)
-      m.W[(j0 + r) * dp + i0 + tx] = tile[tx][r];         // (J, I) transposed through smem
-    }
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int64_t i = i0 + ty + 4 * u, j = j0 + tx;
+    if (i == j) v[u] = (i < d) ? v[u] + gamma : 1.f;
+    m.W[i * dp + j] = v[u];
+    if (mirror) tile[ty + 4 * u][tx] = v[u];
+  }
+  if (mirror) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) m.W[(j0 + ty + 4 * u) * dp + i0 + tx] = tile[tx][ty + 4 * u];  // (J, I)
   }
 }
 
@@ -343,35 +350,49 @@ __global__ void __launch_bounds__(256) stage_panel_kernel(const InvMat* __restri
   }
 }
 
-// out = -(W + W^T)/2 cropped to d x d, one 32x32 tile pair (I <= J) per block.  Inside a
+// out = -(W + W^T)/2 cropped to d x d, one 64x64 tile pair (I <= J) per block.  Inside a
 // diagonal 128-block both triangles are valid and are averaged; elsewhere only the upper
 // block triangle is valid and is mirrored.
 __global__ void __launch_bounds__(256) finalize_kernel(const InvMat* __restrict__ mats,
                                                        const TileJob* __restrict__ jobs) {
-  __shared__ float tile[32][33];
-  __shared__ float outt[32][33];
+  __shared__ float tile[kT][kT + 1];
   const TileJob jb = jobs[blockIdx.x];
   const InvMat m = mats[jb.mat];
   if (*m.info != 0) return;
   const int64_t d = m.d, dp = m.dp;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t i0 = int64_t(jb.ti) * 32, j0 = int64_t(jb.tj) * 32;
-  const bool same_block = (jb.ti >> 2) == (jb.tj >> 2);
-  if (same_block)
-    for (int r = ty; r < 32; r += 8) tile[r][tx] = m.W[(j0 + r) * dp + i0 + tx];  // W[J, I], coalesced
-  __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    const int64_t i = i0 + r, j = j0 + tx;
-    const float w = m.W[i * dp + j];
-    const float v = same_block ? -0.5f * (w + tile[tx][r]) : -w;
-    outt[tx][r] = v;
-    if (i < d && j < d) m.out[i * d + j] = v;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
+  const int64_t i0 = int64_t(jb.ti) * kT, j0 = int64_t(jb.tj) * kT;
+  if (i0 >= d || j0 >= d) return;
+  const bool same_block = (jb.ti >> 1) == (jb.tj >> 1);
+  float v[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) v[u] = __ldcs(m.W + (i0 + ty + 4 * u) * dp + j0 + tx);
+  if (same_block) {  // W[J, I] rows, coalesced, transposed through shared memory
+    float w[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) w[u] = __ldcs(m.W + (j0 + ty + 4 * u) * dp + i0 + tx);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) tile[ty + 4 * u][tx] = w[u];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = -0.5f * (v[u] + tile[tx][ty + 4 * u]);
+    __syncthreads();
+  } else {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = -v[u];
   }
-  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int64_t i = i0 + ty + 4 * u, j = j0 + tx;
+    if (i < d && j < d) m.out[i * d + j] = v[u];
+    tile[ty + 4 * u][tx] = v[u];
+  }
   if (jb.ti != jb.tj) {
-    for (int r = ty; r < 32; r += 8) {  // out[j0 + r][i0 + tx] = v(i0 + tx, j0 + r)
-      const int64_t j = j0 + r, i = i0 + tx;
-      if (i < d && j < d) m.out[j * d + i] = outt[r][tx];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {  // out[j0 + r][i0 + tx] = v(i0 + tx, j0 + r)
+      const int64_t j = j0 + ty + 4 * u, i = i0 + tx;
+      if (i < d && j < d) m.out[j * d + i] = tile[tx][ty + 4 * u];
     }
   }
 }
@@ -418,12 +439,12 @@ void inverse_sizes(int n, const int32_t* dims, int64_t* rows, int64_t* items, in
   *steps = *nblk = 0;
   for (int t = 0; t < n; ++t) {
     if (dims[t] <= kB) continue;
-    const int64_t dp = round_up(dims[t], kB), T = dp / kB, T32 = dp / 32;
+    const int64_t dp = round_up(dims[t], kB), T = dp / kB;
     *rows += dp;
     *steps = std::max<int>(*steps, int(T));
     *act += T;
     *items += T * (T - 1) + T * ((T - 1) * T / 2);  // panel items + update items over all steps
-    *tiles += T32 * (T32 + 1) / 2;
+    *tiles += (dp / kT) * (dp / kT + 1) / 2;
     *nblk += 1;
   }
 }
@@ -522,9 +543,9 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   }
   std::vector<TileJob> tiles;
   for (int t : blocked) {
-    const int T32 = mats[t].dp / 32;
-    for (int I = 0; I < T32; ++I)
-      for (int J = I; J < T32; ++J) tiles.push_back(TileJob{t, I, J, 0});
+    const int T64 = mats[t].dp / kT;
+    for (int I = 0; I < T64; ++I)
+      for (int J = I; J < T64; ++J) tiles.push_back(TileJob{t, I, J, 0});
   }
   std::vector<int32_t> act;
   std::vector<TcItem> items;

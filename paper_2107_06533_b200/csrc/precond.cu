@@ -18,7 +18,9 @@ struct SplitArgs {
   int n;
 };
 
-__global__ void split_rows_batched_kernel(const __grid_constant__ SplitArgs a) {
+// One block per operand row: row r of matrix t -> bf16 hi/lo planes.  Rows whose length and
+// source/destination alignment allow it move as float4 loads and 8-byte (4 x bf16) stores.
+__global__ void __launch_bounds__(256) split_rows_batched_kernel(const __grid_constant__ SplitArgs a) {
   const int row = blockIdx.x;
   int lo = 0, hi = a.n - 1;
   while (lo < hi) {  // last t with row0[t] <= row
@@ -28,13 +30,36 @@ __global__ void split_rows_batched_kernel(const __grid_constant__ SplitArgs a) {
   }
   const int t = lo;
   const int64_t r = row - a.row0[t];
-  const float* s = a.src[t] + r * a.cols[t];
+  const int cols = a.cols[t];
+  const float* s = a.src[t] + r * cols;
   __nv_bfloat16* d = a.dst[t] + r * a.ldd[t];
-  for (int c = threadIdx.x; c < a.cols[t]; c += blockDim.x) {
+  const int64_t pl = a.plane[t];
+  const bool vec = (cols % 4 == 0) && ((reinterpret_cast<uintptr_t>(s) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(d) & 7) == 0) && (pl % 4 == 0);
+  if (vec) {
+    const int n4 = cols >> 2;
+    for (int c = threadIdx.x; c < n4; c += blockDim.x) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(s) + c);
+      __nv_bfloat16 h[4], l[4];
+      split_bf16(v.x, h[0], l[0]);
+      split_bf16(v.y, h[1], l[1]);
+      split_bf16(v.z, h[2], l[2]);
+      split_bf16(v.w, h[3], l[3]);
+      uint2 hv, lv;
+      hv.x = uint32_t(__bfloat16_as_ushort(h[0])) | (uint32_t(__bfloat16_as_ushort(h[1])) << 16);
+      hv.y = uint32_t(__bfloat16_as_ushort(h[2])) | (uint32_t(__bfloat16_as_ushort(h[3])) << 16);
+      lv.x = uint32_t(__bfloat16_as_ushort(l[0])) | (uint32_t(__bfloat16_as_ushort(l[1])) << 16);
+      lv.y = uint32_t(__bfloat16_as_ushort(l[2])) | (uint32_t(__bfloat16_as_ushort(l[3])) << 16);
+      reinterpret_cast<uint2*>(d)[c] = hv;
+      reinterpret_cast<uint2*>(d + pl)[c] = lv;
+    }
+    return;
+  }
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
     __nv_bfloat16 h, l;
     split_bf16(s[c], h, l);
     d[c] = h;
-    d[c + a.plane[t]] = l;
+    d[c + pl] = l;
   }
 }
 
@@ -103,16 +128,19 @@ void precond_carve(int n, const int32_t* d_out, const int32_t* d_in, Carve& c, s
   }
 }
 
-int run_split(int n, const float* const* src, const std::vector<__nv_bfloat16*>& dst, const std::vector<int32_t>& rows,
-              const std::vector<int32_t>& cols, const std::vector<int64_t>& ldd, cudaStream_t s) {
+// Split operand rows of the selected layers (sel == nullptr: layers 0..n-1; src indexed like sel).
+int run_split(int n, const int32_t* sel, const float* const* src, const std::vector<__nv_bfloat16*>& dst,
+              const std::vector<int32_t>& rows, const std::vector<int32_t>& cols, const std::vector<int64_t>& ldd,
+              cudaStream_t s) {
   for (int off = 0; off < n; off += kMaxPtrs) {
     SplitArgs a{};
     a.n = std::min(kMaxPtrs, n - off);
     int r = 0;
     for (int t = 0; t < a.n; ++t) {
-      const int l = off + t;
-      SPD_ARG(src[l] != nullptr, SPDKFAC_ERR_ARG, "null operand pointer for layer %d", l);
-      a.src[t] = src[l];
+      const int i = off + t, l = sel ? sel[i] : i;
+      SPD_ARG(l >= 0 && l < int(dst.size()), SPDKFAC_ERR_ARG, "layer index %d out of range", l);
+      SPD_ARG(src[i] != nullptr, SPDKFAC_ERR_ARG, "null operand pointer for layer %d", l);
+      a.src[t] = src[i];
       a.dst[t] = dst[l];
       a.cols[t] = cols[l];
       a.ldd[t] = int32_t(ldd[l]);
@@ -225,15 +253,14 @@ int spdkfac_precond_plan_create(spdkfac_precond_plan** out, int n, const int32_t
 int spdkfac_precond_plan_run(spdkfac_precond_plan* p, const float* const* g_inv, const float* const* grad,
                              const float* const* a_inv, float* const* weight, float alpha, float* const* precond_out,
                              void* stream) {
-  SPD_ARG(p && g_inv && grad && a_inv, SPDKFAC_ERR_ARG, "null argument");
+  SPD_ARG(p && grad, SPDKFAC_ERR_ARG, "null argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n = p->n;
   std::vector<int64_t> ldi(p->ldi), ldo(p->ldo);
   int rc;
-  if ((rc = run_split(n, grad, p->gW, p->d_out, p->d_in, ldi, s)) ||
-      (rc = run_split(n, a_inv, p->aI, p->d_in, p->d_in, ldi, s)) ||
-      (rc = run_split(n, g_inv, p->gI, p->d_out, p->d_out, ldo, s)))
-    return rc;
+  if ((rc = run_split(n, nullptr, grad, p->gW, p->d_out, p->d_in, ldi, s))) return rc;
+  if (a_inv && (rc = run_split(n, nullptr, a_inv, p->aI, p->d_in, p->d_in, ldi, s))) return rc;
+  if (g_inv && (rc = run_split(n, nullptr, g_inv, p->gI, p->d_out, p->d_out, ldo, s))) return rc;
   // algorithmic work: 2 g a (a + g) per layer, split over the two GEMMs
   double f1 = 0, f2 = 0;
   for (int l = 0; l < n; ++l) {
@@ -263,6 +290,17 @@ int spdkfac_precond_plan_run(spdkfac_precond_plan* p, const float* const* g_inv,
     stat_end(kCatPrecApply, s, 0, 0);
   }
   return SPDKFAC_OK;
+}
+
+int spdkfac_precond_plan_stage_inverses(spdkfac_precond_plan* p, int which, int n_sel, const int32_t* layers,
+                                        const float* const* inv, void* stream) {
+  SPD_ARG(p && (which == 0 || which == 1) && n_sel >= 0 && (n_sel == 0 || (layers && inv)), SPDKFAC_ERR_ARG,
+          "bad stage_inverses arguments");
+  if (n_sel == 0) return SPDKFAC_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<int64_t> ld(which == 0 ? p->ldi : p->ldo);
+  const auto& dims = which == 0 ? p->d_in : p->d_out;
+  return run_split(n_sel, layers, inv, which == 0 ? p->aI : p->gI, dims, dims, ld, s);
 }
 
 void spdkfac_precond_plan_destroy(spdkfac_precond_plan* p) { delete p; }

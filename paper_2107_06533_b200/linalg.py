@@ -328,10 +328,23 @@ class PrecondPlan:
                        L.ptr_array([o.data_ptr() for o in out]) if out is not None else None)
         self._bound_key = tuple(t.data_ptr() for t in grads)
 
-    def run_bound(self, alpha: float, stream=None) -> None:
+    def run_bound(self, alpha: float, stream=None, inverses_staged: bool = False) -> None:
+        """inverses_staged: every layer's inverses were already staged (stage_inverses) since
+        they last changed, so only the gradients are split here."""
         gi, gr, ai, pw, po = self._bound
+        if inverses_staged:
+            gi = ai = None
         L.check(self._lib.spdkfac_precond_plan_run(self._h, gi, gr, ai, pw, float(alpha), po, _stream(stream)),
                 "precondition run")
+
+    def stage_inverses(self, which: str, layers: Sequence[int], inverses: Sequence[torch.Tensor], stream=None) -> None:
+        """Split the given layers' inverses (which = "A" or "G") into the plan's bf16 hi/lo
+        operands, on `stream` (e.g. right after the stream that inverted them)."""
+        if not layers:
+            return
+        L.check(self._lib.spdkfac_precond_plan_stage_inverses(
+            self._h, 0 if which == "A" else 1, len(layers), L.i32_array(layers),
+            L.ptr_array([t.data_ptr() for t in inverses]), _stream(stream)), "stage inverses")
 
     def run(self, g_inv, grads, a_inv, weights=None, alpha: float = 0.0, out=None, stream=None) -> None:
         n = self.n

@@ -33,8 +33,8 @@ from . import _lib as L
 from . import schedule as S
 from .linalg import FactorGroup, FactorPlan, InversePlan, NotPositiveDefiniteError, PrecondPlan
 from .perfmodel import PerfParams, default_params
-from .planner import (FactorKind, FusionPolicy, inverse_tasks, factor_tasks, lbp_place, local_place, plan_fusion,
-                      seq_place)
+from .planner import (FactorKind, FusionPlan, FusionPolicy, inverse_tasks, factor_tasks, lbp_place, local_place,
+                      plan_fusion, seq_place)
 
 
 @dataclass
@@ -79,7 +79,7 @@ class SPDKFAC(torch.optim.Optimizer):
                  factor_update_freq: int = 1, inv_update_freq: int = 1, fusion: FusionPolicy = FusionPolicy.OPTIMAL,
                  placement: str = "lbp", balance: str = "dim_sq", perf: Optional[PerfParams] = None,
                  batch_averaged: bool = True, layer_times: Optional[dict] = None, comm=None,
-                 early_g_fraction: float = 0.85, factor_comm: str = "auto"):
+                 early_g_fraction=(0.85, 0.983, 0.9985), factor_comm: str = "auto", launch_groups: str = "auto"):
         if damping < 0:
             raise ValueError(f"damping must be nonnegative, got {damping}")
         if not 0.0 <= factor_decay < 1.0:
@@ -139,6 +139,21 @@ class SPDKFAC(torch.optim.Optimizer):
         bp = [s.t_bp for s in reversed(specs)]
         self.fwd_plan = plan_fusion(factor_tasks(specs, FactorKind.A), ff, self.perf.allreduce, fusion)
         self.bwd_plan = plan_fusion(factor_tasks(specs, FactorKind.G), bp, self.perf.allreduce, fusion)
+        if launch_groups not in ("auto", "fusion", "inversion"):
+            raise ValueError(f"launch_groups must be 'auto', 'fusion' or 'inversion', got {launch_groups!r}")
+        self.launch_groups = ("inversion" if self.world == 1 else "fusion") if launch_groups == "auto" else launch_groups
+        if self.launch_groups == "inversion":
+            # no factor communication (P = 1, or by request): a fusion group only batches SYRK
+            # launches, so use few large ones: A in two halves of the forward pass, G cut at the
+            # inversion-group boundaries (each early G inversion waits for exactly one launch)
+            fa = factor_tasks(specs, FactorKind.A)
+            fg = factor_tasks(specs, FactorKind.G)
+            n_g = S.inversion_groups([s.a_dim for s in specs], [s.g_dim for s in specs],
+                                     early_fraction=early_g_fraction)["n_g"]
+            cuts = [sum(n_g[:i]) for i in range(len(n_g) + 1)]
+            h = (len(fa) + 1) // 2
+            self.fwd_plan = FusionPlan(tuple(g for g in (tuple(fa[:h]), tuple(fa[h:])) if g), fusion)
+            self.bwd_plan = FusionPlan(tuple(tuple(fg[a:b]) for a, b in zip(cuts, cuts[1:]) if b > a), fusion)
         tasks = inverse_tasks(specs)
         if placement == "lbp":
             self.placement = lbp_place(tasks, self.world, self.perf.inverse, self.perf.bcast, balance=balance)
@@ -179,22 +194,24 @@ class SPDKFAC(torch.optim.Optimizer):
         for l in self.layers:
             self.inv.append(torch.zeros(l.spec.a_dim, l.spec.a_dim, dtype=torch.float32, device=self.device))
             self.inv.append(torch.zeros(l.spec.g_dim, l.spec.g_dim, dtype=torch.float32, device=self.device))
-        # this rank's inversions in three groups, each launched as soon as its factors exist
+        # this rank's inversions in groups, each launched as soon as its factors exist
         # (schedule.inversion_groups): A after the forward pass (own stream, overlaps the
-        # backward pass), G1 (the layers backward reaches first, most of the G work) mid-backward
-        # on a second stream, G2 in step()
+        # backward pass), the early G groups G1..Gk (the layers backward reaches first, most of
+        # the G work) mid-backward on their own streams, the tail G group in step()
         mine = list(self.placement.workers[self.rank])
         self._mine = mine
         grp = S.inversion_groups([l.spec.a_dim for l in self.layers], [l.spec.g_dim for l in self.layers],
                                  early_fraction=early_g_fraction)
-        self._n_g1 = grp["n_g1"]
-        # G1 may start once every backward fusion group holding a G1 member is computed; the
-        # factors a G1 inverse reads must be complete (members of a group run together)
-        self._g1_groups = {self._gid["G"][li] for li in range(len(self.layers) - self._n_g1, len(self.layers))}
-        self._g1_left = len(self._g1_groups)
-        self._inv_plans, self._info_host, self._bcast = {}, {}, {}
-        for side in ("A", "G1", "G2"):
+        self._early, self._tail = list(grp["early"]), grp["tail"]
+        self._sides = ["A"] + self._early + [self._tail]
+        # an early G group may start once every backward fusion group holding one of its members
+        # is computed; the factors its inverses read must be complete (members of a group run together)
+        self._early_groups = {side: {self._gid["G"][t // 2] for t in grp[side]} for side in self._early}
+        self._early_left = {side: len(g) for side, g in self._early_groups.items()}
+        self._inv_plans, self._info_host, self._bcast, self._inv_ts = {}, {}, {}, {}
+        for side in self._sides:
             ts = [t for t in mine if t in grp[side]]
+            self._inv_ts[side] = ts
             self._inv_plans[side] = InversePlan([self._packed(t) for t in ts], [self.inv[t] for t in ts]) if ts else None
             self._info_host[side] = torch.zeros(len(ts), dtype=torch.int32, pin_memory=True) if ts else None
             self._bcast[side] = self._bcast_layout(grp[side])
@@ -202,10 +219,10 @@ class SPDKFAC(torch.optim.Optimizer):
 
         self.factor_stream = torch.cuda.Stream(self.device)
         self.inv_stream = torch.cuda.Stream(self.device)
-        self.inv_stream2 = torch.cuda.Stream(self.device)
+        self._g_streams = {side: torch.cuda.Stream(self.device) for side in self._early}
         self._g_count = 0
-        self._g1_inverted = False
-        self._sent = {"A": False, "G1": False, "G2": False}
+        self._g_inverted = {side: False for side in self._early}
+        self._sent = {side: False for side in self._sides}
         self._grad_src = {}
         self.comm_stream = torch.cuda.Stream(self.device) if self.world > 1 else None
         self._info_events = []
@@ -213,6 +230,9 @@ class SPDKFAC(torch.optim.Optimizer):
         self._a_inverted = False
         self.timeline = None  # set to {} to record per-phase CUDA events (eager diagnostics)
         self._precond_key = None
+        # the preconditioner's split operands of the inverses are staged by the stream that
+        # produced them (inversion or unpack); stale until the first inversion / after a load
+        self._planes_stale = True
         self.steps = 0
         self._capture = True
         self._factor_updates = 0
@@ -398,10 +418,12 @@ class SPDKFAC(torch.optim.Optimizer):
             else:
                 s, e = self._gslice[kind][gid]
                 self.comm.allreduce_sum(buf[s:e], cs)
-        if kind == "G" and gid in self._g1_groups:
-            self._g1_left -= 1
-            if self._g1_left == 0:
-                self._launch_inverse_G1()
+        if kind == "G":
+            for side in self._early:
+                if gid in self._early_groups[side]:
+                    self._early_left[side] -= 1
+                    if self._early_left[side] == 0:
+                        self._launch_inverse_G(side)
 
     def _build_factor_groups(self) -> None:
         """One FactorGroup per fusion group from the shapes recorded by the per-layer path."""
@@ -466,25 +488,28 @@ class SPDKFAC(torch.optim.Optimizer):
         self._tl("a_inverse_done", s)
         self._a_inverted = True
 
-    def _launch_inverse_G1(self):
-        """The G factors of the layers backward reached first are enqueued: invert them on the
-        second inverse stream while the rest of the backward pass runs."""
-        if self._g1_inverted or not self._inverting():
+    def _launch_inverse_G(self, side: str):
+        """The G factors of one early group (layers the backward reached first) are enqueued:
+        invert them on the group's own stream while the rest of the backward pass runs."""
+        if self._g_inverted[side] or not self._inverting():
             return
-        s = self.inv_stream2
+        for prev in self._early[:self._early.index(side)]:  # keep the program order of the sends
+            self._launch_inverse_G(prev)
+        s = self._g_streams[side]
         s.wait_stream(self.factor_stream)
         if self.world > 1:
             s.wait_stream(self.comm_stream)
             if self._a_inverted:  # A inverses are on their way: share them while backward runs
                 self._exchange_send("A", self.inv_stream)
-        self._run_inverse("G1", s, exchange=False)
-        self._tl("g1_inverse_done", s)
-        self._g1_inverted = True
+        self._run_inverse(side, s, exchange=False)
+        self._tl(f"{side.lower()}_inverse_done", s)
+        self._g_inverted[side] = True
 
     def _run_inverse(self, side: str, stream, exchange: bool = True) -> None:
         plan = self._inv_plans[side]
         if plan is not None:
             plan.run(self.damping, stream)
+            self._stage_planes(self._inv_ts[side], stream)
             self._info_host[side].copy_(plan.info, non_blocking=True)
             if not torch.cuda.is_current_stream_capturing():
                 ev = torch.cuda.Event()
@@ -545,15 +570,16 @@ class SPDKFAC(torch.optim.Optimizer):
             if invert_now:
                 if not self._a_inverted:  # hooks did not see a full forward (e.g. factors reused)
                     self._launch_inverse_A()
-                if not self._g1_inverted:
-                    self._launch_inverse_G1()
-            # every factor all-reduce of this iteration is enqueued: G2's inversion waits for
+                for side in self._early:
+                    self._launch_inverse_G(side)
+            # every factor all-reduce of this iteration is enqueued: the tail G group's inversion waits for
             # exactly these, not for the broadcasts and the gradient all-reduce queued behind
             factors_reduced = torch.cuda.Event()
             factors_reduced.record(cs)
             if invert_now:
                 self._exchange_send("A", self.inv_stream)
-                self._exchange_send("G1", self.inv_stream2)
+                for side in self._early:
+                    self._exchange_send(side, self._g_streams[side])
             cs.wait_stream(main)
             params = [p for p in self.param_groups[0]["params"] if p.grad is not None]
             flat, views = self._flat_grad_buffer(params)
@@ -566,18 +592,19 @@ class SPDKFAC(torch.optim.Optimizer):
         if invert_now:
             if not self._a_inverted:  # hooks did not see a full forward (e.g. factors reused)
                 self._launch_inverse_A()
-            if not self._g1_inverted:
-                self._launch_inverse_G1()
+            for side in self._early:
+                self._launch_inverse_G(side)
             if factors_reduced is not None:
                 main.wait_event(factors_reduced)
-            self._run_inverse("G2", main, exchange=False)
+            self._run_inverse(self._tail, main, exchange=False)
             self._tl("g_inverse_done", main)
             main.wait_stream(self.inv_stream)   # A inverses landed
-            main.wait_stream(self.inv_stream2)  # G1 likewise
+            for side in self._early:  # early G groups likewise
+                main.wait_stream(self._g_streams[side])
             if self.world > 1:
-                self._exchange_send("G2", main)
+                self._exchange_send(self._tail, main)
                 main.wait_stream(self.comm_stream)
-                for side in ("A", "G1", "G2"):
+                for side in self._sides:
                     self._exchange_recv(side, main)
             self._tl("inverses_joined", main)
         # precondition + update for every K-FAC layer (mean gradient = sum / P); the pointer
@@ -599,7 +626,10 @@ class SPDKFAC(torch.optim.Optimizer):
                                [self.inv[2 * l.index] for l in self.layers],
                                weights=[self._weight_matrix(l, l.module.weight.data) for l in self.layers])
             self._precond_key = key
-        self._precond.run_bound(lr / self.world, stream=main)
+        # every inverse is staged by the stream that produced it once an inversion round has run
+        self._precond.run_bound(lr / self.world, stream=main, inverses_staged=not self._planes_stale)
+        if invert_now:
+            self._planes_stale = False
         self._tl("precond_done", main)
         others = [p for p in self.other_params if p.grad is not None]
         if others:
@@ -607,9 +637,9 @@ class SPDKFAC(torch.optim.Optimizer):
         self._a_count = 0
         self._a_inverted = False
         self._g_count = 0
-        self._g1_inverted = False
-        self._sent = {"A": False, "G1": False, "G2": False}
-        self._g1_left = len(self._g1_groups)
+        self._g_inverted = {side: False for side in self._early}
+        self._sent = {side: False for side in self._sides}
+        self._early_left = {side: len(g) for side, g in self._early_groups.items()}
         for k in ("A", "G"):
             self._gseen[k] = [0] * len(self._gseen[k])
         if self._fgroups is None and not capturing and factors_now:
@@ -641,7 +671,7 @@ class SPDKFAC(torch.optim.Optimizer):
         """Bookkeeping for one replay of a captured step (GraphedStep): the Python side
         effects of step() ran once at capture time."""
         self.steps += 1
-        for side in ("A", "G1", "G2"):
+        for side in self._sides:
             if self._inv_plans[side] is not None:
                 ev = torch.cuda.Event()
                 ev.record(stream)
@@ -680,6 +710,13 @@ class SPDKFAC(torch.optim.Optimizer):
                                                          L.ptr_array([v.data_ptr() for v in views_r]),
                                                          L.ptr_array([self.inv[t].data_ptr() for t in ct_r]),
                                                          main.cuda_stream), "unpack inverses")
+            self._stage_planes(ct_r, main)
+
+    def _stage_planes(self, tensors, stream) -> None:
+        """Stage freshly produced inverses (tensor indices 2l / 2l+1) into the preconditioner."""
+        for which, par in (("A", 0), ("G", 1)):
+            ts = [t for t in tensors if t % 2 == par]
+            self._precond.stage_inverses(which, [t // 2 for t in ts], [self.inv[t] for t in ts], stream)
 
     # ------------------------------------------------------------------ introspection / checkpoint
     def factor(self, layer: int, kind: str) -> torch.Tensor:
@@ -704,6 +741,7 @@ class SPDKFAC(torch.optim.Optimizer):
             self.bufG.copy_(k["bufG"])
             for t, s in zip(self.inv, k["inv"]):
                 t.copy_(s)
+            self._planes_stale = True
             self.steps = int(k["steps"])
             self._factor_updates = int(k["factor_updates"])
             self._capture = self.steps % self.factor_update_freq == 0

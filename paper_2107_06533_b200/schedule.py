@@ -110,23 +110,38 @@ def bcast_layout(placement: PlacementPlan, dims: Sequence[int], parity: int | No
     return out
 
 
-def inversion_groups(a_dims: Sequence[int], g_dims: Sequence[int], early_fraction: float = 0.85) -> dict:
+def inversion_groups(a_dims: Sequence[int], g_dims: Sequence[int], early_fraction=0.85) -> dict:
     """Tensor sets inverted as soon as their factors exist:
-      "A"  every input-side factor (complete after the forward pass)
-      "G1" output-side factors of the layers the backward pass reaches first, up to
-           `early_fraction` of the output-side inversion work (sum d^3)
-      "G2" the remaining output-side factors (inverted in step()).
-    Returns {"A": set, "G1": set, "G2": set, "n_g1": number of layers in G1}."""
+      "A"       every input-side factor (complete after the forward pass)
+      "G1".."Gk" output-side factors of the layers the backward pass reaches first, cut where
+                the cumulative output-side inversion work (sum d^3, from the last layer) first
+                reaches each of the increasing fractions in `early_fraction` (a float or a
+                sequence); each is inverted mid-backward as soon as its factors are complete
+      "G{k+1}"  the remaining output-side factors (the tail, inverted in step()).
+    Returns the sets plus "early" (names G1..Gk), "tail" (G{k+1}) and "n_g" (layers per G set,
+    in backward order)."""
+    fracs = [float(early_fraction)] if isinstance(early_fraction, (int, float)) else [float(f) for f in early_fraction]
+    if any(not 0.0 < f <= 1.0 for f in fracs) or any(b <= a for a, b in zip(fracs, fracs[1:])):
+        raise ValueError(f"early fractions must increase within (0, 1], got {fracs}")
     nl = len(g_dims)
     total = sum(float(d) ** 3 for d in g_dims)
-    acc, n_g1 = 0.0, 0
-    for l in reversed(range(nl)):
-        if n_g1 >= nl - 1 or (total and acc >= early_fraction * total):
-            break
-        acc += float(g_dims[l]) ** 3
-        n_g1 += 1
-    g1 = {2 * l + 1 for l in range(nl - n_g1, nl)}
-    return {"A": {2 * l for l in range(nl)}, "G1": g1, "G2": {2 * l + 1 for l in range(nl)} - g1, "n_g1": n_g1}
+    out = {"A": {2 * l for l in range(nl)}}
+    acc, l, names, counts = 0.0, nl - 1, [], []
+    for f in fracs:
+        members = set()
+        while l >= 1 and not (total and members and acc >= f * total):  # the tail keeps layer 0
+            acc += float(g_dims[l]) ** 3
+            members.add(2 * l + 1)
+            l -= 1
+        if members:
+            names.append(f"G{len(names) + 1}")
+            out[names[-1]] = members
+            counts.append(len(members))
+    tail = f"G{len(names) + 1}"
+    out[tail] = {2 * i + 1 for i in range(l + 1)}
+    counts.append(l + 1)
+    out.update(early=names, tail=tail, n_g=counts)
+    return out
 
 
 def kind_of(tensor_index: int) -> FactorKind:

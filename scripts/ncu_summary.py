@@ -1,7 +1,7 @@
 """Summarise an `ncu --set full` report into profiles/: per-kernel launch count, mean duration,
 DRAM bytes per launch (read + write, the bench `roofline.traffic` figure) and tensor-pipe /
 DRAM utilisation.  Usage:
-  python scripts/ncu_summary.py REPORT.ncu-rep OUT.json [kernel-regex]
+  python scripts/ncu_summary.py REPORT.ncu-rep|RAW.csv OUT.json [kernel-regex]
 """
 import csv
 import io
@@ -19,8 +19,12 @@ SCALE = {"ns": 1e-3, "us": 1.0, "ms": 1e3, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1
 
 
 def main(rep, out, rx=None):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
-                         capture_output=True, text=True, check=True).stdout
+    if rep.endswith(".csv"):  # `ncu -i X.ncu-rep --page raw --csv` export
+        txt = open(rep).read()
+        txt = txt[txt.index('"ID"'):]
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
+                             capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     col = {h: i for i, h in enumerate(hdr)}

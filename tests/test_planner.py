@@ -196,3 +196,26 @@ def test_imbalance_report_resnet50_p8():
     rep = P.placement_imbalance(plan, weight=lambda d: float(d) ** 2)
     assert rep["max_over_mean_minus_1"] == pytest.approx(0.104, abs=2e-3)
     assert rep["makespan_over_lower_bound"] == pytest.approx(1.0, abs=1e-9)
+
+
+def test_inversion_groups_partition_and_order():
+    """schedule.inversion_groups: A + early G groups (backward order, cut at the cumulative
+    sum-g^3 fractions) + the tail G group partition the 2L tensors."""
+    from paper_2107_06533_b200.schedule import inversion_groups
+    from paper_2107_06533_b200.workloads import layer_shapes
+    sh = layer_shapes("resnet50", 32)
+    a, g = [s[2] for s in sh], [s[3] for s in sh]
+    r = inversion_groups(a, g, (0.85, 0.983, 0.9985))
+    assert r["early"] == ["G1", "G2", "G3"] and r["tail"] == "G4" and r["n_g"] == [15, 15, 14, 10]
+    sets = [r["A"]] + [r[k] for k in r["early"] + [r["tail"]]]
+    assert sum(len(x) for x in sets) == 2 * len(sh) and set().union(*sets) == set(range(2 * len(sh)))
+    # backward order: every member of an earlier group belongs to a later layer
+    for e, f in zip(r["early"], r["early"][1:] + [r["tail"]]):
+        assert min(r[e]) > max(r[f])
+    # the tail holds only layer1 / conv1 output factors (g <= 256): a short inversion chain after backward
+    assert max(g[t // 2] for t in r[r["tail"]]) == 256
+    # single fraction == the two-group split
+    r1 = inversion_groups(a, g, 0.85)
+    assert r1["early"] == ["G1"] and r1["G1"] == r["G1"] and r1["n_g"] == [15, 39]
+    with pytest.raises(ValueError):
+        inversion_groups(a, g, (0.9, 0.8))
