@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--factor-freq", type=int, default=1)
     p.add_argument("--inv-freq", type=int, default=1)
     p.add_argument("--placement", default="lbp")
+    p.add_argument("--balance", choices=("dim_sq", "dim", "dim_cube"), default="dim_cube",
+                   help="LBP bucket weight: d^2 / d (the reference's options) or d^3 (inversion arithmetic)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--profile", action="store_true", help="short run for ncu: no clocks/e2e/cpu legs")
@@ -74,6 +76,8 @@ def parse():
                         "inversion groups are cut (comma list; the rest is inverted in step())")
     p.add_argument("--launch-groups", choices=("auto", "fusion", "inversion"), default="auto",
                    help="factor SYRK launch groups: the fusion plan (P>1 default) or few large groups (P=1 default)")
+    p.add_argument("--update-in-backward", choices=("auto", "on", "off"), default="auto",
+                   help="precondition + update the early G groups' layers during backward (auto: on at P=1)")
     p.add_argument("--clocks", choices=("nvml", "smi", "off"), default="nvml")
     p.add_argument("--timeline", action="store_true", help="diagnostic: per-phase CUDA-event timeline of one eager step")
     p.add_argument("--stats-off", action="store_true", help="no per-launch CUDA events in the timed region (diagnostic)")
@@ -90,7 +94,8 @@ def workload_config(a, world):
             "fusion": "optimal" if world > 1 or a.launch_groups == "fusion" else
                       "none at P=1 (no factor comm): SYRK launch groups = A in 2 halves, G at the inversion groups",
             "g_inversion_fractions": a.g_fractions,
-            "placement": a.placement, "parallelism": f"dp{world}", "python_gc": a.gc,
+            "update_in_backward": a.update_in_backward == "on" or (a.update_in_backward == "auto" and world == 1),
+            "placement": a.placement, "lbp_balance": a.balance, "parallelism": f"dp{world}", "python_gc": a.gc,
             "execution": "one CUDA graph per iteration (fwd+bwd+K-FAC step)" if a.mode == "graph" else "eager",
             "memory_format": a.memory_format,
             "l2": "per-iteration working set (activations, 0.3 GB packed factors, im2col staging) >> 126 MB L2; no flush"}
@@ -307,8 +312,9 @@ def run_ours(a):
         opt.placement = None
     else:
         opt = SPDKFAC(model, lr=a.lr, damping=a.damping, factor_update_freq=a.factor_freq,
-                      inv_update_freq=a.inv_freq, placement=a.placement,
-                      early_g_fraction=tuple(float(f) for f in a.g_fractions.split(",")), launch_groups=a.launch_groups)
+                      inv_update_freq=a.inv_freq, placement=a.placement, balance=a.balance,
+                      early_g_fraction=tuple(float(f) for f in a.g_fractions.split(",")), launch_groups=a.launch_groups,
+                      update_in_backward=a.update_in_backward == "on" or (a.update_in_backward == "auto" and world == 1))
     crit = nn.CrossEntropyLoss()
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)

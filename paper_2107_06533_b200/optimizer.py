@@ -79,7 +79,8 @@ class SPDKFAC(torch.optim.Optimizer):
                  factor_update_freq: int = 1, inv_update_freq: int = 1, fusion: FusionPolicy = FusionPolicy.OPTIMAL,
                  placement: str = "lbp", balance: str = "dim_sq", perf: Optional[PerfParams] = None,
                  batch_averaged: bool = True, layer_times: Optional[dict] = None, comm=None,
-                 early_g_fraction=(0.85, 0.983, 0.9985), factor_comm: str = "auto", launch_groups: str = "auto"):
+                 early_g_fraction=(0.85, 0.983, 0.9985), factor_comm: str = "auto", launch_groups: str = "auto",
+                 update_in_backward: bool = False):
         if damping < 0:
             raise ValueError(f"damping must be nonnegative, got {damping}")
         if not 0.0 <= factor_decay < 1.0:
@@ -215,7 +216,24 @@ class SPDKFAC(torch.optim.Optimizer):
             self._inv_plans[side] = InversePlan([self._packed(t) for t in ts], [self.inv[t] for t in ts]) if ts else None
             self._info_host[side] = torch.zeros(len(ts), dtype=torch.int32, pin_memory=True) if ts else None
             self._bcast[side] = self._bcast_layout(grp[side])
-        self._precond = PrecondPlan([(l.spec.g_dim, l.spec.a_dim) for l in self.layers], device=self.device)
+        # preconditioning + update in groups that follow the G inversion groups (layer sets in
+        # backward order): with update_in_backward, an early group's layers are preconditioned
+        # and updated on that group's stream as soon as their gradients are accumulated and
+        # their inverses exist, while the rest of the backward pass runs; step() handles the
+        # tail group (and every group otherwise)
+        self._pc_sides = self._early + [self._tail]
+        self._pc_side = {t // 2: side for side in self._pc_sides for t in grp[side]}
+        self._pc_layers = {side: sorted(li for li, sd in self._pc_side.items() if sd == side) for side in self._pc_sides}
+        self._pc_local = {li: k for side in self._pc_sides for k, li in enumerate(self._pc_layers[side])}
+        self._precond = {side: PrecondPlan([(self.layers[li].spec.g_dim, self.layers[li].spec.a_dim)
+                                            for li in self._pc_layers[side]], device=self.device)
+                         for side in self._pc_sides if self._pc_layers[side]}
+        self._precond_key = {side: None for side in self._precond}
+        self._pc_done = {side: False for side in self._precond}
+        self._grad_left = {side: len(self._pc_layers[side]) for side in self._precond}
+        if update_in_backward and self.world > 1:
+            raise ValueError("update_in_backward needs P == 1 (the gradient mean is formed in step())")
+        self.update_in_backward = bool(update_in_backward)
 
         self.factor_stream = torch.cuda.Stream(self.device)
         self.inv_stream = torch.cuda.Stream(self.device)
@@ -229,7 +247,6 @@ class SPDKFAC(torch.optim.Optimizer):
         self._a_count = 0
         self._a_inverted = False
         self.timeline = None  # set to {} to record per-phase CUDA events (eager diagnostics)
-        self._precond_key = None
         # the preconditioner's split operands of the inverses are staged by the stream that
         # produced them (inversion or unpack); stale until the first inversion / after a load
         self._planes_stale = True
@@ -282,6 +299,7 @@ class SPDKFAC(torch.optim.Optimizer):
             l.events = {k: (torch.cuda.Event(), torch.cuda.Event()) for k in ("A", "G")}
             l.handles.append(l.module.register_forward_pre_hook(self._make_a_hook(l)))
             l.handles.append(l.module.register_forward_hook(self._make_out_hook(l)))
+            l.handles.append(l.module.weight.register_post_accumulate_grad_hook(self._make_grad_hook(l)))
 
     def remove_hooks(self):
         for l in self.layers:
@@ -607,39 +625,29 @@ class SPDKFAC(torch.optim.Optimizer):
                 for side in self._sides:
                     self._exchange_recv(side, main)
             self._tl("inverses_joined", main)
-        # precondition + update for every K-FAC layer (mean gradient = sum / P); the pointer
-        # tables are rebuilt only when a gradient's storage changes (zero_grad(set_to_none=True))
-        # P > 1: the all-reduced gradient lives in the flat buffer (same shapes and strides)
-        src = self._grad_src if self.world > 1 else {}
-        grad_of = lambda p: src.get(id(p), p.grad)  # noqa: E731
-        key = tuple(grad_of(l.module.weight).data_ptr() if l.module.weight.grad is not None else 0
-                    for l in self.layers)
-        if key != self._precond_key:
-            if 0 in key:
-                missing = [l.name for l in self.layers if l.module.weight.grad is None]
-                raise RuntimeError(f"layers {missing[:3]} have no gradient; call backward() before step()")
-            for l in self.layers:  # memory format may change (model.to(channels_last) after construction)
-                if l.is_conv:
-                    l.w_cl = self._weight_channels_last(l.module)
-            self._precond.bind([self.inv[2 * l.index + 1] for l in self.layers],
-                               [self._weight_matrix(l, grad_of(l.module.weight)) for l in self.layers],
-                               [self.inv[2 * l.index] for l in self.layers],
-                               weights=[self._weight_matrix(l, l.module.weight.data) for l in self.layers])
-            self._precond_key = key
-        # every inverse is staged by the stream that produced it once an inversion round has run
-        self._precond.run_bound(lr / self.world, stream=main, inverses_staged=not self._planes_stale)
+        # precondition + update for every K-FAC layer not yet done during backward (mean gradient
+        # = sum / P); P > 1: the all-reduced gradient lives in the flat buffer (same shapes and strides)
+        for side in self._precond:
+            if self._pc_done[side]:
+                main.wait_stream(self._g_streams[side])
+            else:
+                self._run_precond(side, main, lr)
         if invert_now:
             self._planes_stale = False
         self._tl("precond_done", main)
         others = [p for p in self.other_params if p.grad is not None]
         if others:
-            torch._foreach_add_([p.data for p in others], [grad_of(p) for p in others], alpha=-lr / self.world)
+            src = self._grad_src if self.world > 1 else {}
+            torch._foreach_add_([p.data for p in others], [src.get(id(p), p.grad) for p in others],
+                                alpha=-lr / self.world)
         self._a_count = 0
         self._a_inverted = False
         self._g_count = 0
         self._g_inverted = {side: False for side in self._early}
         self._sent = {side: False for side in self._sides}
         self._early_left = {side: len(g) for side, g in self._early_groups.items()}
+        self._pc_done = {side: False for side in self._precond}
+        self._grad_left = {side: len(self._pc_layers[side]) for side in self._precond}
         for k in ("A", "G"):
             self._gseen[k] = [0] * len(self._gseen[k])
         if self._fgroups is None and not capturing and factors_now:
@@ -713,10 +721,59 @@ class SPDKFAC(torch.optim.Optimizer):
             self._stage_planes(ct_r, main)
 
     def _stage_planes(self, tensors, stream) -> None:
-        """Stage freshly produced inverses (tensor indices 2l / 2l+1) into the preconditioner."""
-        for which, par in (("A", 0), ("G", 1)):
-            ts = [t for t in tensors if t % 2 == par]
-            self._precond.stage_inverses(which, [t // 2 for t in ts], [self.inv[t] for t in ts], stream)
+        """Stage freshly produced inverses (tensor indices 2l / 2l+1) into the preconditioner
+        group that owns their layer."""
+        for side, plan in self._precond.items():
+            for which, par in (("A", 0), ("G", 1)):
+                ts = [t for t in tensors if t % 2 == par and self._pc_side[t // 2] == side]
+                plan.stage_inverses(which, [self._pc_local[t // 2] for t in ts], [self.inv[t] for t in ts], stream)
+
+    def _run_precond(self, side: str, stream, lr: float) -> None:
+        """P = G^-1 grad A^-1 and W -= lr/P_world * P for the layers of one group, on `stream`;
+        the pointer tables are rebuilt only when a gradient's storage changes."""
+        layers = [self.layers[li] for li in self._pc_layers[side]]
+        src = self._grad_src if self.world > 1 else {}
+        grad_of = lambda p: src.get(id(p), p.grad)  # noqa: E731
+        key = tuple(grad_of(l.module.weight).data_ptr() if l.module.weight.grad is not None else 0 for l in layers)
+        plan = self._precond[side]
+        if key != self._precond_key[side]:
+            if 0 in key:
+                missing = [l.name for l in layers if l.module.weight.grad is None]
+                raise RuntimeError(f"layers {missing[:3]} have no gradient; call backward() before step()")
+            for l in layers:  # memory format may change (model.to(channels_last) after construction)
+                if l.is_conv:
+                    l.w_cl = self._weight_channels_last(l.module)
+            plan.bind([self.inv[2 * l.index + 1] for l in layers],
+                      [self._weight_matrix(l, grad_of(l.module.weight)) for l in layers],
+                      [self.inv[2 * l.index] for l in layers],
+                      weights=[self._weight_matrix(l, l.module.weight.data) for l in layers])
+            self._precond_key[side] = key
+        # every inverse is staged by the stream that produced it once an inversion round has run
+        plan.run_bound(lr / self.world, stream=stream, inverses_staged=not self._planes_stale)
+
+    def _make_grad_hook(self, l: _Layer):
+        def hook(param):
+            if not self.update_in_backward or not l.module.training:
+                return
+            side = self._pc_side[l.index]
+            self._grad_left[side] -= 1
+            if self._grad_left[side] == 0 and side != self._tail:
+                self._launch_precond(side)
+        return hook
+
+    def _launch_precond(self, side: str) -> None:
+        """Every gradient of an early group's layers is accumulated (post-accumulate-grad hooks
+        run after the layer's backward kernels were enqueued on the current stream): precondition
+        and update those layers on the group's stream once its inverses exist."""
+        if self._inverting() and not self._g_inverted[side]:
+            return  # inverses not launched yet (factors reused / incomplete): step() handles it
+        main = torch.cuda.current_stream(self.device)
+        s = self._g_streams[side]
+        s.wait_stream(main)
+        if self._inverting():
+            s.wait_stream(self.inv_stream)  # A inverses (the group's G inverses are on s already)
+        self._run_precond(side, s, self.param_groups[0]["lr"])
+        self._pc_done[side] = True
 
     # ------------------------------------------------------------------ introspection / checkpoint
     def factor(self, layer: int, kind: str) -> torch.Tensor:

@@ -108,3 +108,46 @@ def test_graphed_step_matches_eager():
     assert o2.steps == 5
     o1.remove_hooks()
     o2.remove_hooks()
+
+
+@pytest.mark.parametrize("graphed", [False, True])
+def test_update_in_backward_matches_step(graphed):
+    """update_in_backward: early G groups precondition + update during the backward pass (on
+    their own streams); the weights equal those of the plain step() path."""
+    import torch.nn as nn
+    from paper_2107_06533_b200.graph import GraphedStep
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    from paper_2107_06533_b200.workloads import build_model
+    torch.backends.cudnn.deterministic = True
+    torch.backends.cudnn.benchmark = False
+    torch.manual_seed(11)
+    m1 = build_model("resnet20").cuda()
+    m2 = build_model("resnet20").cuda()
+    m2.load_state_dict(m1.state_dict())
+    crit = nn.CrossEntropyLoss()
+    xs = [torch.randn(8, 3, 32, 32, device="cuda") for _ in range(4)]
+    ys = [torch.randint(0, 10, (8,), device="cuda") for _ in range(4)]
+    freq = 1 if graphed else 2  # GraphedStep captures one step type
+    o1 = SPDKFAC(m1, lr=0.05, damping=0.1, inv_update_freq=freq)
+    o2 = SPDKFAC(m2, lr=0.05, damping=0.1, inv_update_freq=freq, update_in_backward=True,
+                 early_g_fraction=(0.5, 0.9))
+    assert len(o2._early) == 2
+    for x, y in zip(xs, ys):
+        o1.zero_grad(set_to_none=False)
+        crit(m1(x), y).backward()
+        o1.step()
+    if graphed:
+        gs = GraphedStep(m2, crit, o2, [xs[0]], [ys[0]], warmup=1)
+        for x, y in zip(xs[1:], ys[1:]):
+            gs([x], [y])
+    else:
+        for x, y in zip(xs, ys):
+            o2.zero_grad(set_to_none=False)
+            crit(m2(x), y).backward()
+            assert any(o2._pc_done.values())  # early groups ran during backward
+            o2.step()
+    torch.cuda.synchronize()
+    for p1, p2 in zip(m1.parameters(), m2.parameters()):
+        assert torch.allclose(p1, p2, rtol=1e-5, atol=1e-6), (p1 - p2).abs().max()
+    o1.remove_hooks()
+    o2.remove_hooks()

@@ -219,3 +219,24 @@ def test_inversion_groups_partition_and_order():
     assert r1["early"] == ["G1"] and r1["G1"] == r["G1"] and r1["n_g"] == [15, 39]
     with pytest.raises(ValueError):
         inversion_groups(a, g, (0.9, 0.8))
+
+
+def test_lbp_dim_cube_balances_inversion_work():
+    """balance="dim_cube" (extension): Algorithm 1 with d^3 bucket weights; on ResNet-50 it
+    balances the inversion arithmetic exactly at P = 2, 4 and reaches the indivisible-task
+    lower bound (one d = 4608 inverse per rank) at P = 8; d^2 stays the reference default."""
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    from paper_2107_06533_b200.perfmodel import default_params
+    from paper_2107_06533_b200.workloads import layer_shapes
+    specs = [SPDKFAC._estimate_times(n, a, g) for n, m, a, g in layer_shapes("resnet50", 32)]
+    tasks = P.inverse_tasks(specs)
+    perf = default_params()
+    for w, tol in ((2, 0.01), (4, 0.01)):
+        r = P.placement_imbalance(P.lbp_place(tasks, w, perf.inverse, perf.bcast, balance="dim_cube"))
+        assert r["max_over_mean_minus_1"] <= tol
+        r2 = P.placement_imbalance(P.lbp_place(tasks, w, perf.inverse, perf.bcast, balance="dim_sq"))
+        assert r2["max_over_mean_minus_1"] > 0.1  # the d^2 weights leave > 10 % on the table here
+    r = P.placement_imbalance(P.lbp_place(tasks, 8, perf.inverse, perf.bcast, balance="dim_cube"))
+    assert abs(r["makespan_over_lower_bound"] - 1.0) < 1e-9
+    with pytest.raises(ValueError):
+        P.lbp_place(tasks, 2, perf.inverse, perf.bcast, balance="dim_4")
