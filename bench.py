@@ -78,6 +78,8 @@ def parse():
                    help="factor SYRK launch groups: the fusion plan (P>1 default) or few large groups (P=1 default)")
     p.add_argument("--update-in-backward", choices=("auto", "on", "off"), default="auto",
                    help="precondition + update the early G groups' layers during backward (auto: on at P=1)")
+    p.add_argument("--ncu-range", action="store_true",
+                   help="wrap the last timed step in cudaProfilerStart/Stop (ncu --profile-from-start off)")
     p.add_argument("--clocks", choices=("nvml", "smi", "off"), default="nvml")
     p.add_argument("--timeline", action="store_true", help="diagnostic: per-phase CUDA-event timeline of one eager step")
     p.add_argument("--stats-off", action="store_true", help="no per-launch CUDA events in the timed region (diagnostic)")
@@ -396,7 +398,11 @@ def run_ours(a):
     e0.record(stream)
     evs = []
     for i in range(a.steps):
+        if a.ncu_range and i == a.steps - 1:  # ncu --profile-from-start off: the last timed step only
+            torch.cuda.cudart().cudaProfilerStart()
         loss = step(i)
+        if a.ncu_range and i == a.steps - 1:
+            torch.cuda.cudart().cudaProfilerStop()
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream)
         evs.append(ev)
@@ -468,13 +474,25 @@ def run_ours(a):
     except Exception:
         pass
     sy = st["factor_syrk"]
+    # DRAM bytes of the same kernels from one `ncu --set full` capture of a whole step's SYRK
+    # launches (scripts/ncu_summary.py --step, committed under profiles/), if it matches
+    traffic = None
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "syrk_traffic_n1.json")))
+        if world == 1 and t.get("launches_per_step") == sy["launches"] / per and t.get("model") == a.model:
+            traffic = t
+    except Exception:
+        pass
     ach = sy["flops"] / (sy["ms"] * 1e-3) / 1e12 if sy["ms"] > 0 else 0.0  # same ratio per step or total
     peak = peaks.get("bf16_tflops_sustained") or 1362.2
     step_ms_total = sum(v["ms"] for k, v in bst.items() if isinstance(v, dict)) / nb
     roofline = {"kernel": "tc3_gemm_kernel<BF16> (factor SYRK, 3 x bf16 split, tcgen05)", "bound": "tensor",
                 "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
-                "traffic": None,
+                "traffic": (round(traffic["dram_bytes_per_step"] / (sy["launches"] / per)) if traffic else None),
+                "traffic_source": traffic.get("source") if traffic else "no ncu capture for this launch configuration",
+                "traffic_per_step": traffic.get("dram_bytes_per_step") if traffic else None,
+                "algorithmic_bytes_per_step": sy["bytes"] / per,
                 "algorithmic_flops_per_step": sy["flops"] / per,
                 "kernel_ms_per_step": round(sy["ms"] / per, 4),
                 "launches_per_step": sy["launches"] / per,

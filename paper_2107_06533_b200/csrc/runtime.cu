@@ -244,6 +244,47 @@ __global__ void pack_batched_kernel(const __grid_constant__ PackArgs a, int unpa
   }
 }
 
+// packed upper -> full symmetric, one 64 x 64 upper tile (I <= J) per block: rows of the
+// upper tile are contiguous in the packed rows, the mirrored (J, I) tile goes through shared
+// memory (a per-row gather of the lower triangle reads one 32-B sector per element).
+// PackArgs::row0 holds the tile prefix of each matrix.
+__global__ void __launch_bounds__(256) unpack_tiles_kernel(const __grid_constant__ PackArgs a) {
+  __shared__ float tile[64][65];
+  const int blk = blockIdx.x;
+  int t = 0;
+  while (t + 1 < a.n && a.row0[t + 1] <= blk) ++t;
+  const int64_t d = a.d[t];
+  const int T = int((d + 63) / 64);
+  int k = blk - a.row0[t], I = 0;
+  while (k >= T - I) k -= T - I, ++I;
+  const int J = I + k;
+  const int64_t i0 = int64_t(I) * 64, j0 = int64_t(J) * 64;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  const float* src = a.src[t];
+  float* dst = a.dst[t];
+  float v[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int64_t i = i0 + ty + 4 * u, j = j0 + tx;
+    const int64_t r = i < j ? i : j, c = i < j ? j : i;
+    v[u] = (i < d && j < d) ? src[r * (2 * d - r + 1) / 2 + (c - r)] : 0.f;
+  }
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int64_t i = i0 + ty + 4 * u, j = j0 + tx;
+    if (i < d && j < d) dst[i * d + j] = v[u];
+    tile[ty + 4 * u][tx] = v[u];
+  }
+  if (I != J) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int64_t j = j0 + ty + 4 * u, i = i0 + tx;
+      if (i < d && j < d) dst[j * d + i] = tile[tx][ty + 4 * u];
+    }
+  }
+}
+
 static int pack_batched(int n, const int32_t* dims, const float* const* src, float* const* dst, int unpack,
                         cudaStream_t s) {
   SPD_ARG(n >= 0 && (n == 0 || (dims && src && dst)), SPDKFAC_ERR_ARG, "bad batched pack arguments");
@@ -257,11 +298,13 @@ static int pack_batched(int n, const int32_t* dims, const float* const* src, flo
       a.dst[t] = dst[off + t];
       a.d[t] = dims[off + t];
       a.row0[t] = rows;
-      rows += dims[off + t];
+      const int T = (dims[off + t] + 63) / 64;
+      rows += unpack ? T * (T + 1) / 2 : dims[off + t];  // unpack: upper 64-tiles; pack: rows
     }
     a.row0[a.n] = rows;
     stat_begin(kCatPack, s);
-    pack_batched_kernel<<<dim3(1, rows), 256, 0, s>>>(a, unpack);
+    if (unpack) unpack_tiles_kernel<<<rows, 256, 0, s>>>(a);
+    else pack_batched_kernel<<<dim3(1, rows), 256, 0, s>>>(a, 0);
     SPD_CHECK_LAUNCH();
     stat_end(kCatPack, s, 0, 0);
   }

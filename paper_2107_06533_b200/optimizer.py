@@ -221,8 +221,15 @@ class SPDKFAC(torch.optim.Optimizer):
         # and updated on that group's stream as soon as their gradients are accumulated and
         # their inverses exist, while the rest of the backward pass runs; step() handles the
         # tail group (and every group otherwise)
-        self._pc_sides = self._early + [self._tail]
-        self._pc_side = {t // 2: side for side in self._pc_sides for t in grp[side]}
+        if update_in_backward and self.world > 1:
+            raise ValueError("update_in_backward needs P == 1 (the gradient mean is formed in step())")
+        self.update_in_backward = bool(update_in_backward)
+        # without it, one plan over every layer runs in step() (fewest launches)
+        self._pc_sides = self._early + [self._tail] if self.update_in_backward else ["ALL"]
+        if self.update_in_backward:
+            self._pc_side = {t // 2: side for side in self._pc_sides for t in grp[side]}
+        else:
+            self._pc_side = {li: "ALL" for li in range(len(self.layers))}
         self._pc_layers = {side: sorted(li for li, sd in self._pc_side.items() if sd == side) for side in self._pc_sides}
         self._pc_local = {li: k for side in self._pc_sides for k, li in enumerate(self._pc_layers[side])}
         self._precond = {side: PrecondPlan([(self.layers[li].spec.g_dim, self.layers[li].spec.a_dim)
@@ -231,11 +238,12 @@ class SPDKFAC(torch.optim.Optimizer):
         self._precond_key = {side: None for side in self._precond}
         self._pc_done = {side: False for side in self._precond}
         self._grad_left = {side: len(self._pc_layers[side]) for side in self._precond}
-        if update_in_backward and self.world > 1:
-            raise ValueError("update_in_backward needs P == 1 (the gradient mean is formed in step())")
-        self.update_in_backward = bool(update_in_backward)
 
         self.factor_stream = torch.cuda.Stream(self.device)
+        # steady-state staging (im2col / precision split, HBM-bound) runs beside the
+        # tensor-core convolutions instead of on the forward/backward stream
+        self.stage_stream = torch.cuda.Stream(self.device)
+        self._stage_refs = []  # inputs staged on stage_stream, kept alive until step() joins it
         self.inv_stream = torch.cuda.Stream(self.device)
         self._g_streams = {side: torch.cuda.Stream(self.device) for side in self._early}
         self._g_count = 0
@@ -376,9 +384,15 @@ class SPDKFAC(torch.optim.Optimizer):
         gid = self._gid[kind][l.index]
         fg = self._fgroups[kind][gid] if self._fgroups is not None else None
         if fg is not None and fg["keys"][l.index] == key:
+            ss = self.stage_stream
+            ss.wait_stream(main)  # x is complete
             if fg["seen"] == 0 and not capturing and fg["pending"]:
-                main.wait_event(fg["done"])  # previous iteration's SYRK has consumed the staging buffers
-            fg["obj"].stage(fg["member"][l.index], x, main)
+                ss.wait_event(fg["done"])  # previous iteration's SYRK has consumed the staging buffers
+            fg["obj"].stage(fg["member"][l.index], x, ss)
+            # an output gradient may be freed once its layer's backward ran (and _prepare may
+            # return a temporary): hold x until step() joins stage_stream (A inputs are saved
+            # for backward anyway, so they are never modified in place)
+            self._stage_refs.append(x)
             fg["seen"] += 1
         else:
             if fg is not None:  # shape changed: per-layer plans this iteration, rebuild groups after
@@ -417,7 +431,7 @@ class SPDKFAC(torch.optim.Optimizer):
         buf = self.bufA if kind == "A" else self.bufG
         fg = self._fgroups[kind][gid] if self._fgroups is not None else None
         if fg is not None and fg["seen"] == self._gsize[kind][gid]:
-            fg["staged"].record(main)
+            fg["staged"].record(self.stage_stream)
             fs.wait_event(fg["staged"])
             fg["obj"].compute(decay, 1.0 / self.world, fs)
             fg["done"].record(fs)
@@ -517,7 +531,12 @@ class SPDKFAC(torch.optim.Optimizer):
         s.wait_stream(self.factor_stream)
         if self.world > 1:
             s.wait_stream(self.comm_stream)
-            if self._a_inverted:  # A inverses are on their way: share them while backward runs
+            # A inverses are on their way: share them while backward runs.  The broadcast waits
+            # for this rank's A inversions and every later collective on the single comm stream
+            # queues behind it, so it is issued only after the last early G group's factor
+            # reductions (earlier, it would hold those groups' inversions back until the A side
+            # finished)
+            if self._a_inverted and side == self._early[-1]:
                 self._exchange_send("A", self.inv_stream)
         self._run_inverse(side, s, exchange=False)
         self._tl(f"{side.lower()}_inverse_done", s)
@@ -578,6 +597,8 @@ class SPDKFAC(torch.optim.Optimizer):
         factors_now = self._capture
         invert_now = self.steps % self.inv_update_freq == 0
         self._tl("backward_done", main)
+        main.wait_stream(self.stage_stream)  # every staged input / output gradient is consumed
+        self._stage_refs.clear()
         if factors_now:
             main.wait_stream(self.factor_stream)
             self._factor_updates += 1

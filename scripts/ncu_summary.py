@@ -59,5 +59,36 @@ def main(rep, out, rx=None):
     print(json.dumps(res, indent=1))
 
 
+
+
+def step_traffic(raw_csv, out, launches_per_step, model="resnet50", note=""):
+    """profiles/syrk_traffic_n1.json for bench.py's roofline.traffic: DRAM bytes of the LAST
+    `launches_per_step` factor-SYRK launches (one whole step) of an ncu --set full capture of
+    eager steps; the factor stream is the one the CTA-pair engine launches on (the
+    preconditioning GEMMs share the single-CTA kernel but run on the main stream)."""
+    txt = open(raw_csv).read()
+    txt = txt[txt.index('"ID"'):]
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    col = {h: i for i, h in enumerate(hdr)}
+    pair_streams = [r[col["Stream"]] for r in data if "tc3_pair" in r[col["Kernel Name"]]]
+    fs = max(set(pair_streams), key=pair_streams.count)
+    syrk = [r for r in data if r[col["Stream"]] == fs][-int(launches_per_step):]
+
+    def val(r, m):
+        return float(r[col[m]].replace(",", "")) * SCALE.get(units[col[m]], 1.0)
+    b = sum(val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum") for r in syrk)
+    us = sum(val(r, "gpu__time_duration.sum") for r in syrk)
+    res = {"model": model, "launches_per_step": len(syrk), "dram_bytes_per_step": round(b),
+           "ncu_us_per_step": round(us, 1),
+           "source": f"ncu --set full --clock-control none, last {len(syrk)} factor-SYRK launches (one eager step) "
+                     f"of {raw_csv.split('/')[-1]}" + (f"; {note}" if note else "")}
+    json.dump(res, open(out, "w"), indent=1)
+    print(res)
+
+
 if __name__ == "__main__":
-    main(*sys.argv[1:])
+    if sys.argv[1] == "--step":
+        step_traffic(sys.argv[2], sys.argv[3], int(sys.argv[4]))
+    else:
+        main(*sys.argv[1:])

@@ -148,6 +148,31 @@ def test_pack_round_trip_exact(d):
     assert torch.equal(K.unpack_upper(p, d).cpu(), m)
 
 
+def test_pack_unpack_batched_exact():
+    """spdkfac_(un)pack_upper_batched_f32 (the inverse broadcast path): tiled unpack of mixed
+    sizes, including partial 64-tiles, is bit-exact against the oracle's unpack_upper."""
+    import ctypes as C
+    from paper_2107_06533_b200 import _lib as L
+    lib = L.load(require_device=True)
+    dims = [1, 5, 63, 64, 65, 130, 300, 700]
+    rng = np.random.default_rng(5)
+    fulls = []
+    for d in dims:
+        m = torch.tensor(spd(rng, d), dtype=torch.float32)
+        fulls.append(((m + m.T) / 2).cuda())
+    packed = [torch.empty(d * (d + 1) // 2, device="cuda") for d in dims]
+    back = [torch.full((d, d), float("nan"), device="cuda") for d in dims]
+    s = torch.cuda.current_stream().cuda_stream
+    L.check(lib.spdkfac_pack_upper_batched_f32(len(dims), L.i32_array(dims), L.ptr_array([f.data_ptr() for f in fulls]),
+                                               L.ptr_array([p.data_ptr() for p in packed]), s), "pack")
+    L.check(lib.spdkfac_unpack_upper_batched_f32(len(dims), L.i32_array(dims), L.ptr_array([p.data_ptr() for p in packed]),
+                                                 L.ptr_array([b.data_ptr() for b in back]), s), "unpack")
+    torch.cuda.synchronize()
+    for d, f, p, b in zip(dims, fulls, packed, back):
+        assert torch.equal(p.cpu(), torch.tensor(O.pack_upper(f.double().cpu().numpy()), dtype=torch.float32)), d
+        assert torch.equal(b, f), d
+
+
 def inverse_bound(m, gamma, got_err):
     d = m.shape[0]
     ev = np.linalg.eigvalsh(m + gamma * np.eye(d))
