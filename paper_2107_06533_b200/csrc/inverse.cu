@@ -26,9 +26,10 @@ namespace spd {
 constexpr int kB = 128;          // pivot block = tile edge
 constexpr int kSmemLd = kB + 1;  // padded row stride of the shared-memory block
 // Panel planes panA / panC: [2 planes][rows][kPanCols]; step k uses the 128 columns of slot
-// k % 4, so the two panels of an even/odd step pair are adjacent columns (one K = 256
-// update reads both) and the look-ahead step never overwrites a slot still being read.
-constexpr int kPanSlots = 4;
+// k % kPanSlots, so the panels of a fused step group are adjacent columns (one K = 128 x steps
+// update reads them all) and the look-ahead step never overwrites a slot still being read.
+constexpr int kFuse = 4;                // trailing-update steps fused per W pass (see the update plan)
+constexpr int kPanSlots = 2 * kFuse;    // a group's slots + the next group's look-ahead never alias
 constexpr int kPanCols = kPanSlots * kB;
 
 struct InvMat {
@@ -588,39 +589,42 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     p->pan_cnt.push_back(int(items.size()) - p->pan_off.back());
     p->upd_off.push_back(int(items.size()));
     // Update of step k, split into U1 (issued before step k+1's look-ahead front: it must
-    // see these tiles) and U2 (runs under the front).  Steps are fused in pairs (k even,
-    // k + 1 < T): step k updates only block row/column k+1 (U1) and k+2 (U2); step k+1
-    // updates row/column k+2 (U1) and then every other tile with BOTH steps' panels in one
-    // K = 256 contraction (panel slots k % 4, k % 4 + 1 are adjacent), which halves the
-    // read-modify-write passes over W.  Tiles in row/column k only take step k+1's panel.
+    // see these tiles) and U2 (runs under the front).  Steps are fused in groups of kFuse
+    // (k0 = multiple of kFuse, last = min(k0 + kFuse - 1, T - 1)): a non-last step s updates
+    // only the block rows/columns s+1 (U1) and s+2 .. last+1 (U2), which the group's later
+    // pivots and panels read; the last step updates every other tile with all of its pending
+    // steps' panels in ONE contraction of K = (pending steps) x 128 (their panel slots are
+    // adjacent), so W is read-modify-written once per group instead of once per step.  A tile's
+    // pending steps are those after the last group step that updated it eagerly or had it in
+    // its pivot row/column (the panel epilogue writes those).
     int u1 = 0;
     std::vector<TcItem> u1v, u2v;
     for (int t : blocked) {
       const int T = mats[t].dp / kB;
       if (k >= T) continue;
-      const bool first = (k % 2 == 0) && k + 1 < T;  // first step of a fused pair
-      const bool second = (k % 2 == 1);               // second step of a pair (k - 1 was the first)
-      const int q = k % kPanSlots;
+      const int k0 = k - k % kFuse, last = std::min(k0 + kFuse - 1, T - 1);
+      const bool bulk = (k == last);
+      auto touched = [&](int s, int I, int J) {  // group step s < k updated or owned tile (I, J)
+        if (I == s || J == s) return true;  // pivot row/column: written by the panel epilogue
+        return (I >= s + 1 && I <= last + 1) || (J >= s + 1 && J <= last + 1);  // eager rows of step s
+      };
       for (int I = 0; I < T; ++I)
         for (int J = I; J < T; ++J) {
           if (I == k || J == k) continue;
-          const bool row1 = (I == k + 1 || J == k + 1), row2 = (I == k + 2 || J == k + 2);
-          int k0 = q * kB, nk = kB / 32;
-          bool in_u1;
-          if (first) {
-            if (row1) in_u1 = true;
-            else if (row2) in_u1 = false;
-            else continue;  // deferred to step k+1's fused K = 256 update
-          } else if (second) {
-            in_u1 = row1;
-            const bool row_prev = (I == k - 1 || J == k - 1);
-            if (!row1 && !row_prev) {  // deferred by step k-1: both steps, slots q - 1, q
-              k0 = (q - 1) * kB;
-              nk = 2 * kB / 32;
-            }
-          } else {  // unpaired last step (odd T): classic single-step update
-            in_u1 = row1;
+          const bool row1 = (I == k + 1 || J == k + 1);
+          const bool eager = (I >= k + 1 && I <= last + 1) || (J >= k + 1 && J <= last + 1);
+          int first = k;  // first pending step of this tile
+          if (bulk) {
+            first = k0;
+            for (int s2 = k - 1; s2 >= k0; --s2)
+              if (touched(s2, I, J)) {
+                first = s2 + 1;
+                break;
+              }
+          } else if (!eager) {
+            continue;  // deferred to the group's last step
           }
+          const bool in_u1 = row1;
           // D'[y][x] = sum_k Wold[J0+y][k] C[I0+x][k] = U[I0+x][J0+y] (U symmetric):
           // the coalesced transposed store lands on the upper block W[I, J]
           TcItem it{};
@@ -628,8 +632,8 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
           it.b_map = 1;
           it.a_row = mats[t].panel_row0 + J * kB;
           it.b_row = mats[t].panel_row0 + I * kB;
-          it.k0 = k0;
-          it.nk = nk;
+          it.k0 = (first % kPanSlots) * kB;
+          it.nk = (k - first + 1) * (kB / 32);
           it.epi = t;
           it.flags = 0;
           it.out_r = J * kB;

@@ -4,6 +4,8 @@
 #include <cstdarg>
 #include <mutex>
 
+#include <string>
+
 #include "runtime.cuh"
 
 namespace spd {
@@ -121,6 +123,19 @@ int make_operand_map_mn(CUtensorMap* out, const void* base, int64_t ld, int64_t 
   return SPDKFAC_OK;
 }
 
+// Grid policy of the tile engines: persistent (<= one CTA per SM, static round robin over the
+// work items) or one CTA per work item (SPDKFAC_GRID=tiles): CTAs then retire tile by tile,
+// so kernels of concurrent streams (the forward/backward convolutions) get SMs as soon as a
+// tile finishes instead of after the whole launch.
+static bool tile_grid() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("SPDKFAC_GRID");
+    mode = (e && std::string(e) == "tiles") ? 1 : 0;
+  }
+  return mode == 1;
+}
+
 template <Kind K, int kSt, bool kCTile>
 static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
                        const TcRun& run) {
@@ -142,7 +157,7 @@ static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi
       if (cap > 0 && cap < sms) sms = cap;
     }
   }
-  const int grid = n < sms ? n : sms;
+  const int grid = (tile_grid() || n < sms) ? n : sms;
   tc3_gemm_kernel<K, kSt, kCTile><<<grid, 192, smem, s>>>(maps, items, epis, run, n);
   SPD_CHECK_LAUNCH();
   return SPDKFAC_OK;
@@ -179,7 +194,7 @@ int launch_tc3_pair(const CUtensorMap* maps, const TcPairItem* items, const TcEp
     }
     pairs = sms / 2;
   }
-  const int grid = 2 * (n < pairs ? n : pairs);
+  const int grid = 2 * ((tile_grid() || n < pairs) ? n : pairs);
   tc3_pair_kernel<kStages><<<grid, 192, kPairSmemBytes, s>>>(maps, items, epis, run, n);
   SPD_CHECK_LAUNCH();
   return SPDKFAC_OK;
