@@ -497,6 +497,8 @@ def run_ours(a):
                 "kernel_ms_per_step": round(sy["ms"] / per, 4),
                 "launches_per_step": sy["launches"] / per,
                 "tensor_pipe_mmas_per_algorithmic_mac": 3,
+                # 3 split-precision MMAs per algorithmic MAC: the pipe executes 3 x the algorithmic rate
+                "tensor_pipe_equivalent_frac": round(3 * ach / peak, 4),
                 "share_of_library_kernel_time": round(bst["factor_syrk"]["ms"] / nb / step_ms_total, 4)
                 if step_ms_total else None}
     breakdown = {k: {"ms_per_step": round(v["ms"] / nb, 4), "launches_per_step": v["launches"] / nb,

@@ -417,6 +417,7 @@ struct spdkfac_inverse_plan {
   std::vector<double> upd_flops, u2_flops;  // per step: U1 / U2 tensor work (algorithmic, per launch)
   cudaStream_t side = nullptr;  // look-ahead stream: pivot/stage/panel of step k+1
   bool lookahead = true;        // SPDKFAC_NO_LOOKAHEAD=1 serialises (diagnostics)
+  int panel_ctas = 32;          // grid cap of the panel GEMM (SPDKFAC_PANEL_CTAS overrides; 0 = all SMs)
   cudaEvent_t ev_u1 = nullptr, ev_panel = nullptr;
   int32_t* act_ids;             // device, active blocked matrices per step (concatenated)
   PanelJob* pan_jobs;           // device, (matrix, R != K) per step, same order as the panel items
@@ -678,6 +679,7 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     return rc;
   }
   {
+    if (const char* pc = getenv("SPDKFAC_PANEL_CTAS")) p->panel_ctas = atoi(pc);
     const char* e = getenv("SPDKFAC_NO_LOOKAHEAD");
     p->lookahead = !(e && e[0] == '1');
   }
@@ -723,7 +725,11 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       stat_begin(kCatInvPanel, q);
       stage_panel_kernel<<<dim3(p->pan_cnt[k], 4), 256, 0, q>>>(p->mats, p->pan_jobs + p->pj_off[k], k, pa, plane);
       SPD_CHECK_LAUNCH();
-      int rc = launch_tc3(Kind::TF32, p->maps, p->items + p->pan_off[k], p->epis, p->pan_cnt[k], q);
+      // the panel GEMM has few K blocks per tile: a full persistent grid would hold every SM for
+      // ~20 us per step while doing little work; a capped grid leaves the SMs to the
+      // concurrent convolutions at almost the same chain latency
+      int rc = launch_tc3(Kind::TF32, p->maps, p->items + p->pan_off[k], p->epis, p->pan_cnt[k], q, TcRun{},
+                          p->panel_ctas);
       if (rc) return rc;
       stat_end(kCatInvPanel, q, 2.0 * kB * kB * kB * p->pan_cnt[k], 0);
       return SPDKFAC_OK;

@@ -138,7 +138,7 @@ static bool tile_grid() {
 
 template <Kind K, int kSt, bool kCTile>
 static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
-                       const TcRun& run) {
+                       const TcRun& run, int max_ctas = 0) {
   constexpr size_t smem = tc_smem_bytes<kSt>(kCTile);
   static bool attr_set = false;
   if (!attr_set) {
@@ -157,17 +157,19 @@ static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi
       if (cap > 0 && cap < sms) sms = cap;
     }
   }
-  const int grid = (tile_grid() || n < sms) ? n : sms;
+  int cap = sms;
+  if (max_ctas > 0 && max_ctas < cap) cap = max_ctas;
+  const int grid = (tile_grid() || n < cap) ? n : cap;
   tc3_gemm_kernel<K, kSt, kCTile><<<grid, 192, smem, s>>>(maps, items, epis, run, n);
   SPD_CHECK_LAUNCH();
   return SPDKFAC_OK;
 }
 
 int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
-               const TcRun& run) {
+               const TcRun& run, int max_ctas) {
   if (n <= 0) return SPDKFAC_OK;
-  return kind == Kind::BF16 ? launch_kind<Kind::BF16, kStages, false>(maps, items, epis, n, s, run)
-                            : launch_kind<Kind::TF32, kStages, false>(maps, items, epis, n, s, run);
+  return kind == Kind::BF16 ? launch_kind<Kind::BF16, kStages, false>(maps, items, epis, n, s, run, max_ctas)
+                            : launch_kind<Kind::TF32, kStages, false>(maps, items, epis, n, s, run, max_ctas);
 }
 
 int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s) {

@@ -80,7 +80,7 @@ struct PtrTable {
 };
 
 int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items,
-               cudaStream_t s, const TcRun& run = TcRun{});
+               cudaStream_t s, const TcRun& run = TcRun{}, int max_ctas = 0);
 // TF32 engine with a TMA-staged fp32 C tile (read-modify-write targets, TcEpi::c_map)
 // CTA-pair SYRK engine (cta_group::2, 256 x 256 super tiles; bf16 MN-major split planes)
 int launch_tc3_pair(const CUtensorMap* maps, const TcPairItem* items, const TcEpi* epis, int n_items, cudaStream_t s,
