@@ -417,7 +417,7 @@ struct spdkfac_inverse_plan {
   std::vector<double> upd_flops, u2_flops;  // per step: U1 / U2 tensor work (algorithmic, per launch)
   cudaStream_t side = nullptr;  // look-ahead stream: pivot/stage/panel of step k+1
   bool lookahead = true;        // SPDKFAC_NO_LOOKAHEAD=1 serialises (diagnostics)
-  int panel_ctas = 32;          // grid cap of the panel GEMM (SPDKFAC_PANEL_CTAS overrides; 0 = all SMs)
+  int panel_ctas = 0;           // grid cap of the panel GEMM (SPDKFAC_PANEL_CTAS; 0 = all SMs: the chain latency wins)
   cudaEvent_t ev_u1 = nullptr, ev_panel = nullptr;
   int32_t* act_ids;             // device, active blocked matrices per step (concatenated)
   PanelJob* pan_jobs;           // device, (matrix, R != K) per step, same order as the panel items

@@ -174,7 +174,7 @@ int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const Tc
 
 int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s) {
   if (n <= 0) return SPDKFAC_OK;
-  return launch_kind<Kind::TF32, 2, true>(maps, items, epis, n, s, TcRun{});
+  return launch_kind<Kind::TF32, 3, true>(maps, items, epis, n, s, TcRun{});
 }
 
 int launch_tc3_pair(const CUtensorMap* maps, const TcPairItem* items, const TcEpi* epis, int n, cudaStream_t s,
@@ -209,7 +209,7 @@ int make_ctile_map(CUtensorMap* out, const float* base, int64_t rows, int64_t co
           "tensor map: misaligned target");
   cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
   cuuint64_t strides[1] = {cuuint64_t(ld * 4)};
-  cuuint32_t box[2] = {128, 64};  // 64-row halves (kCTile ring)
+  cuuint32_t box[2] = {128, kCSliceRows};  // 32-row slices (kCTile ring)
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -182,13 +182,18 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
 // (lanes walk contiguous smem -> conflict-free) and one thread TMA-stores it back.  Used
 // for the read-modify-write inverse updates, where per-thread loads left the kernel
 // latency-bound at ~2 TB/s.
-// kCTile target tiles move as 64-row halves through a ring of three 32-KB slots, so the
-// next tile's first half loads while the current tile's second half is being updated
-constexpr int kCRing = 3;
-constexpr uint32_t kCHalfBytes = 64 * 128 * 4;
+// kCTile target tiles move as 32-row slices through a ring of two 16-KB slots, loaded and
+// stored by one epilogue thread: after slice u is stored it loads slice u + 2 (of this tile,
+// or the first slices of the CTA's next tile, which then land during that tile's mainloop).
+// The TMA producer only streams operands, and the small ring leaves room for 3 operand
+// stages (2 x 64 KB in flight while one is consumed).
+constexpr int kCSliceRows = 32;
+constexpr int kCSlices = 128 / kCSliceRows;
+constexpr int kCRing = 2;
+constexpr uint32_t kCSliceBytes = kCSliceRows * 128 * 4;
 template <int kSt>
 constexpr size_t tc_smem_bytes(bool ctile) {
-  return size_t(kSt) * kStageBytes + (ctile ? kCRing * kCHalfBytes : 0) + 1024 + 256;
+  return size_t(kSt) * kStageBytes + (ctile ? kCRing * kCSliceBytes : 0) + 1024 + 256;
 }
 
 template <Kind K, int kSt, bool kCTile>
@@ -198,14 +203,13 @@ __global__ void __launch_bounds__(192, 1)
   constexpr int BK = (K == Kind::BF16) ? 64 : 32;  // one 128-byte swizzle row of K
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* ctile = reinterpret_cast<float*>(smem + kSt * kStageBytes);  // kCRing x [64][128] (kCTile)
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageBytes + (kCTile ? kCRing * kCHalfBytes : 0));
+  float* ctile = reinterpret_cast<float*>(smem + kSt * kStageBytes);  // kCRing x [32][128] (kCTile)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageBytes + (kCTile ? kCRing * kCSliceBytes : 0));
   uint64_t* empty = full + kSt;
   uint64_t* tfull = empty + kSt;  // [2]
   uint64_t* tempty = tfull + 2;   // [2]
-  uint64_t* cfull = tempty + 2;     // [kCRing] C half tile landed
-  uint64_t* cfree = cfull + kCRing;  // [kCRing] C half tile stored back (slot reusable)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfree + kCRing);
+  uint64_t* cfull = tempty + 2;     // [kCRing] C slice landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + kCRing);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -218,10 +222,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4);
     }
-    for (int q = 0; q < kCRing; ++q) {
-      mbar_init(&cfull[q], 1);
-      mbar_init(&cfree[q], 1);
-    }
+    for (int q = 0; q < kCRing; ++q) mbar_init(&cfull[q], 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<256>(tmem_slot);
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
       uint32_t g = 0, t = 0;
-      int last_a = -1, last_b = -1, last_c = -1;
+      int last_a = -1, last_b = -1;
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
         const TcItem it = items[item];
         const bool same = (it.flags & kSameAB) != 0;
@@ -265,18 +266,6 @@ __global__ void __launch_bounds__(192, 1)
               tma_load_3d(st + 2 * kTileBytes, bm, &full[s], kc + it.b_koff, it.b_row, 0);
               tma_load_3d(st + 3 * kTileBytes, bm, &full[s], kc + it.b_koff, it.b_row, 1);
             }
-          }
-        }
-        if constexpr (kCTile) {  // target tile of this item, after the previous tile was stored
-          const TcEpi ep = epis[it.epi];
-          const CUtensorMap* cm = maps + ep.c_map;
-          if (ep.c_map != last_c) tmap_acquire(cm), last_c = ep.c_map;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {  // rows out_c + 64 h .., cols out_r ..
-            const uint32_t u = 2 * t + h, q = u % kCRing;
-            mbar_wait(&cfree[q], ((u / kCRing) & 1) ^ 1);
-            mbar_expect_tx(&cfull[q], kCHalfBytes);
-            tma_load_2d(ctile + q * (kCHalfBytes / 4), cm, &cfull[q], it.out_r, it.out_c + 64 * h);
           }
         }
       }
@@ -333,6 +322,24 @@ __global__ void __launch_bounds__(192, 1)
   } else {  // ---- epilogue warps 2..5
     const int quad = warp & 3;
     const int i = quad * 32 + lane;
+    const bool cio = kCTile && warp == 2 && lane == 0;  // the C-slice loader / storer
+    // slice u of this CTA = slice u % kCSlices of its (u / kCSlices)-th item: rows
+    // out_c + kCSliceRows * h of the target, columns out_r ..
+    auto load_slice = [&](uint32_t u) {
+      const int item = int(blockIdx.x + (u / kCSlices) * gridDim.x);
+      if (item >= n_items) return;
+      const TcItem it2 = items[item];
+      const CUtensorMap* cm = maps + epis[it2.epi].c_map;
+      tmap_acquire(cm);
+      const uint32_t q = u % kCRing;
+      mbar_expect_tx(&cfull[q], kCSliceBytes);
+      tma_load_2d(ctile + q * (kCSliceBytes / 4), cm, &cfull[q], it2.out_r,
+                  it2.out_c + kCSliceRows * int(u % kCSlices));
+    };
+    if constexpr (kCTile) {
+      if (cio)
+        for (uint32_t u = 0; u < kCRing; ++u) load_slice(u);
+    }
     uint32_t t = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
       const TcItem it = items[item];
@@ -350,19 +357,21 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int u = 0; u < 32; ++u) v[u] = 0.f;
         }
-        if constexpr (kCTile) {  // half h = c / 2: slot[j][i] = beta * slot[j][i] + alpha * D[i][j]
-          const uint32_t u2 = 2 * t + (c >> 1), q = u2 % kCRing;
-          if ((c & 1) == 0) mbar_wait(&cfull[q], (u2 / kCRing) & 1);
-          float* col = ctile + q * (kCHalfBytes / 4) + ((c & 1) * 32) * 128 + i;
+        if constexpr (kCTile) {  // slice h: slot[j][i] = beta * slot[j][i] + alpha * D[i][j]
+          static_assert(kCSliceRows % 32 == 0, "a TMEM chunk of 32 columns lies in one C slice");
+          const int h = (c * 32) / kCSliceRows, r0 = (c * 32) % kCSliceRows;
+          const uint32_t u2 = kCSlices * t + h, q = u2 % kCRing;
+          if (r0 == 0) mbar_wait(&cfull[q], (u2 / kCRing) & 1);
+          float* col = ctile + q * (kCSliceBytes / 4) + r0 * 128 + i;
 #pragma unroll
           for (int u = 0; u < 32; ++u) col[u * 128] = ep.beta * col[u * 128] + ep.alpha * v[u];
-          if (c & 1) {  // half complete: hand it to the TMA store
+          if (r0 + 32 == kCSliceRows) {  // slice complete: store it, then reuse the slot
             fence_proxy_async_smem();
             named_bar_sync(1, 128);
-            if (warp == 2 && lane == 0) {
-              tma_store_2d(maps + ep.c_map, ctile + q * (kCHalfBytes / 4), it.out_r, it.out_c + 64 * (c >> 1));
+            if (cio) {
+              tma_store_2d(maps + ep.c_map, ctile + q * (kCSliceBytes / 4), it.out_r, it.out_c + kCSliceRows * h);
               tma_store_commit_and_wait_read();
-              mbar_arrive(&cfree[q]);
+              load_slice(u2 + kCRing);
             }
           }
         } else {
