@@ -39,6 +39,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "SPD-KFAC iteration time (ms) ResNet-50 bs32/GPU @1/2/4/8 B200; % roofline"
+# scheme -> (fusion policy, placement) (simulator.py:145-193 SchemeConfig factories / ablation)
+SCHEMES = {"spdkfac": ("optimal", "lbp"), "mpdkfac": ("naive", "seq"), "dkfac": ("naive", "local"),
+           "spdkfac-nopipe": ("naive", "lbp"), "spdkfac-nolbp": ("optimal", "seq")}
 
 
 def parse():
@@ -74,6 +77,11 @@ def parse():
     p.add_argument("--g-fractions", default="0.85,0.983,0.9985",
                    help="cumulative shares of the output-side inversion work (sum g^3) at which the early G "
                         "inversion groups are cut (comma list; the rest is inverted in step())")
+    p.add_argument("--scheme", default="spdkfac",
+                   choices=("spdkfac", "mpdkfac", "dkfac", "spdkfac-nopipe", "spdkfac-nolbp"),
+                   help="measured baselines of simulator.py:145-193: dkfac = naive fusion + every worker inverts "
+                        "everything; mpdkfac = naive fusion + round-robin placement; the ablations toggle the "
+                        "pipelined (optimal) fusion and LBP separately")
     p.add_argument("--launch-groups", choices=("auto", "fusion", "inversion"), default="auto",
                    help="factor SYRK launch groups: the fusion plan (P>1 default) or few large groups (P=1 default)")
     p.add_argument("--update-in-backward", choices=("auto", "on", "off"), default="auto",
@@ -93,11 +101,12 @@ def workload_config(a, world):
                         f" (BASELINE.json configs[{1 if world == 1 else 2}])",
             "per_gpu_batch": a.batch, "global_batch": a.batch * world, "damping": a.damping, "lr": a.lr,
             "factor_update_freq": a.factor_freq, "inv_update_freq": a.inv_freq,
-            "fusion": "optimal" if world > 1 or a.launch_groups == "fusion" else
+            "scheme": a.scheme,
+            "fusion": SCHEMES[a.scheme][0] if world > 1 or a.launch_groups == "fusion" else
                       "none at P=1 (no factor comm): SYRK launch groups = A in 2 halves, G at the inversion groups",
             "g_inversion_fractions": a.g_fractions,
             "update_in_backward": a.update_in_backward == "on" or (a.update_in_backward == "auto" and world == 1),
-            "placement": a.placement, "lbp_balance": a.balance, "parallelism": f"dp{world}", "python_gc": a.gc,
+            "placement": SCHEMES[a.scheme][1] if a.scheme != "spdkfac" else a.placement, "lbp_balance": a.balance, "parallelism": f"dp{world}", "python_gc": a.gc,
             "execution": "one CUDA graph per iteration (fwd+bwd+K-FAC step)" if a.mode == "graph" else "eager",
             "memory_format": a.memory_format,
             "l2": "per-iteration working set (activations, 0.3 GB packed factors, im2col staging) >> 126 MB L2; no flush"}
@@ -313,8 +322,13 @@ def run_ours(a):
         opt.check_inverses = lambda: None
         opt.placement = None
     else:
+        from paper_2107_06533_b200.planner import FusionPolicy
+        fusion, placement = SCHEMES[a.scheme]
+        if a.scheme == "spdkfac":
+            placement = a.placement
         opt = SPDKFAC(model, lr=a.lr, damping=a.damping, factor_update_freq=a.factor_freq,
-                      inv_update_freq=a.inv_freq, placement=a.placement, balance=a.balance,
+                      inv_update_freq=a.inv_freq, placement=placement, balance=a.balance,
+                      fusion=FusionPolicy(fusion),
                       early_g_fraction=tuple(float(f) for f in a.g_fractions.split(",")), launch_groups=a.launch_groups,
                       update_in_backward=a.update_in_backward == "on" or (a.update_in_backward == "auto" and world == 1))
     crit = nn.CrossEntropyLoss()
