@@ -246,6 +246,9 @@ class SPDKFAC(torch.optim.Optimizer):
         self._stage_refs = []  # inputs staged on stage_stream, kept alive until step() joins it
         self.inv_stream = torch.cuda.Stream(self.device)
         self._g_streams = {side: torch.cuda.Stream(self.device) for side in self._early}
+        # index of the early G group whose launch issues the A-inverse broadcast (default: the last)
+        import os
+        self._a_bcast_after = int(os.environ.get("SPDKFAC_A_BCAST_AFTER", len(self._early) - 1))
         self._g_count = 0
         self._g_inverted = {side: False for side in self._early}
         self._sent = {side: False for side in self._sides}
@@ -536,7 +539,7 @@ class SPDKFAC(torch.optim.Optimizer):
             # queues behind it, so it is issued only after the last early G group's factor
             # reductions (earlier, it would hold those groups' inversions back until the A side
             # finished)
-            if self._a_inverted and side == self._early[-1]:
+            if self._a_inverted and side == self._early[min(self._a_bcast_after, len(self._early) - 1)]:
                 self._exchange_send("A", self.inv_stream)
         self._run_inverse(side, s, exchange=False)
         self._tl(f"{side.lower()}_inverse_done", s)
