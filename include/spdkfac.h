@@ -176,6 +176,10 @@ SPDKFAC_API int spdkfac_precond_plan_run(spdkfac_precond_plan* p, const float* c
  * fp32 inverse) into the plan's bf16 hi/lo operand planes: which = 0 for A^-1, 1 for G^-1. */
 SPDKFAC_API int spdkfac_precond_plan_stage_inverses(spdkfac_precond_plan* p, int which, int n_sel, const int32_t* layers,
                                                     const float* const* inv, void* stream);
+/* Same from packed upper inverses (the owner broadcast, emulator.py:256-262): one pass writes the
+ * full fp32 inverse (full_out[i], may be NULL) and the operand planes. */
+SPDKFAC_API int spdkfac_precond_plan_stage_packed(spdkfac_precond_plan* p, int which, int n_sel, const int32_t* layers,
+                                                  const float* const* packed, float* const* full_out, void* stream);
 SPDKFAC_API void spdkfac_precond_plan_destroy(spdkfac_precond_plan* p);
 
 /* ------------------------------------------------------------------ collectives

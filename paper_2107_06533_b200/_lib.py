@@ -62,6 +62,7 @@ SIGNATURES = {
     "spdkfac_precond_plan_create": (C.c_int, [C.POINTER(_vp), C.c_int, _pi32, _pi32, _vp, _sz, _vp]),
     "spdkfac_precond_plan_run": (C.c_int, [_vp, _pp, _pp, _pp, _pp, _f32, _pp, _vp]),
     "spdkfac_precond_plan_stage_inverses": (C.c_int, [_vp, C.c_int, C.c_int, _pi32, _pp, _vp]),
+    "spdkfac_precond_plan_stage_packed": (C.c_int, [_vp, C.c_int, C.c_int, _pi32, _pp, _pp, _vp]),
     "spdkfac_precond_plan_destroy": (None, [_vp]),
     "spdkfac_comm_unique_id": (C.c_int, [_vp]),
     "spdkfac_comm_create": (C.c_int, [C.POINTER(_vp), _vp, C.c_int, C.c_int]),

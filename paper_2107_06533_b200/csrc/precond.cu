@@ -63,6 +63,61 @@ __global__ void __launch_bounds__(256) split_rows_batched_kernel(const __grid_co
   }
 }
 
+// Received packed inverse -> full fp32 matrix (optional) AND the preconditioner's bf16 hi/lo
+// operand planes, one 64 x 64 upper tile (I <= J) per block, the mirrored tile through shared
+// memory (the broadcast path: one pass instead of unpack + a re-read to split).
+struct StagePackedArgs {
+  const float* src[kMaxPtrs];     // packed upper, d(d+1)/2
+  float* full[kMaxPtrs];          // d x d or nullptr
+  __nv_bfloat16* dst[kMaxPtrs];   // planes [2][d][ld]
+  int32_t d[kMaxPtrs], ld[kMaxPtrs];
+  int64_t plane[kMaxPtrs];
+  int32_t tile0[kMaxPtrs + 1];
+  int n;
+};
+
+__global__ void __launch_bounds__(256) stage_packed_kernel(const __grid_constant__ StagePackedArgs a) {
+  __shared__ float tile[64][65];
+  const int blk = blockIdx.x;
+  int t = 0;
+  while (t + 1 < a.n && a.tile0[t + 1] <= blk) ++t;
+  const int64_t d = a.d[t], ld = a.ld[t], pl = a.plane[t];
+  const int T = int((d + 63) / 64);
+  int k = blk - a.tile0[t], I = 0;
+  while (k >= T - I) k -= T - I, ++I;
+  const int J = I + k;
+  const int64_t i0 = int64_t(I) * 64, j0 = int64_t(J) * 64;
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  const float* src = a.src[t];
+  float* full = a.full[t];
+  __nv_bfloat16* dst = a.dst[t];
+  float v[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int64_t i = i0 + ty + 4 * u, j = j0 + tx;
+    const int64_t r = i < j ? i : j, c = i < j ? j : i;
+    v[u] = (i < d && j < d) ? src[r * (2 * d - r + 1) / 2 + (c - r)] : 0.f;
+  }
+  auto put = [&](int64_t i, int64_t j, float x) {
+    if (i >= d || j >= d) return;
+    if (full) full[i * d + j] = x;
+    __nv_bfloat16 h, l;
+    split_bf16(x, h, l);
+    dst[i * ld + j] = h;
+    dst[pl + i * ld + j] = l;
+  };
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    put(i0 + ty + 4 * u, j0 + tx, v[u]);
+    tile[ty + 4 * u][tx] = v[u];
+  }
+  if (I != J) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) put(j0 + ty + 4 * u, i0 + tx, tile[tx][ty + 4 * u]);
+  }
+}
+
 struct ApplyArgs {
   const float* P[kMaxPtrs];
   float* W[kMaxPtrs];
@@ -301,6 +356,41 @@ int spdkfac_precond_plan_stage_inverses(spdkfac_precond_plan* p, int which, int 
   std::vector<int64_t> ld(which == 0 ? p->ldi : p->ldo);
   const auto& dims = which == 0 ? p->d_in : p->d_out;
   return run_split(n_sel, layers, inv, which == 0 ? p->aI : p->gI, dims, dims, ld, s);
+}
+
+int spdkfac_precond_plan_stage_packed(spdkfac_precond_plan* p, int which, int n_sel, const int32_t* layers,
+                                      const float* const* packed, float* const* full_out, void* stream) {
+  SPD_ARG(p && (which == 0 || which == 1) && n_sel >= 0 && (n_sel == 0 || (layers && packed)), SPDKFAC_ERR_ARG,
+          "bad stage_packed arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const auto& dims = which == 0 ? p->d_in : p->d_out;
+  const auto& lds = which == 0 ? p->ldi : p->ldo;
+  const auto& planes = which == 0 ? p->aI : p->gI;
+  for (int off = 0; off < n_sel; off += kMaxPtrs) {
+    StagePackedArgs a{};
+    a.n = std::min(kMaxPtrs, n_sel - off);
+    int tiles = 0;
+    for (int t = 0; t < a.n; ++t) {
+      const int i = off + t, l = layers[i];
+      SPD_ARG(l >= 0 && l < p->n, SPDKFAC_ERR_ARG, "layer index %d out of range", l);
+      SPD_ARG(packed[i] != nullptr, SPDKFAC_ERR_ARG, "null packed inverse for layer %d", l);
+      a.src[t] = packed[i];
+      a.full[t] = full_out ? full_out[i] : nullptr;
+      a.dst[t] = planes[l];
+      a.d[t] = dims[l];
+      a.ld[t] = int32_t(lds[l]);
+      a.plane[t] = int64_t(dims[l]) * lds[l];
+      a.tile0[t] = tiles;
+      const int T = (dims[l] + 63) / 64;
+      tiles += T * (T + 1) / 2;
+    }
+    a.tile0[a.n] = tiles;
+    stat_begin(kCatPrecSplit, s);
+    stage_packed_kernel<<<tiles, 256, 0, s>>>(a);
+    SPD_CHECK_LAUNCH();
+    stat_end(kCatPrecSplit, s, 0, 0);
+  }
+  return SPDKFAC_OK;
 }
 
 void spdkfac_precond_plan_destroy(spdkfac_precond_plan* p) { delete p; }

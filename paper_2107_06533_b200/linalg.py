@@ -355,6 +355,17 @@ class PrecondPlan:
             self._h, L.ptr_array([t.data_ptr() for t in g_inv]), L.ptr_array([t.data_ptr() for t in grads]),
             L.ptr_array([t.data_ptr() for t in a_inv]), pw, float(alpha), po, _stream(stream)), "precondition run")
 
+    def stage_packed(self, which: str, layers: Sequence[int], packed: Sequence[torch.Tensor],
+                     full_out: Sequence[torch.Tensor] | None = None, stream=None) -> None:
+        """Packed upper inverses (a broadcast) -> operand planes and, optionally, full matrices."""
+        if not layers:
+            return
+        L.check(self._lib.spdkfac_precond_plan_stage_packed(
+            self._h, 0 if which == "A" else 1, len(layers), L.i32_array(layers),
+            L.ptr_array([t.data_ptr() for t in packed]),
+            L.ptr_array([t.data_ptr() for t in full_out]) if full_out is not None else None,
+            _stream(stream)), "stage packed inverses")
+
     def __del__(self):
         if getattr(self, "_h", None):
             self._lib.spdkfac_precond_plan_destroy(self._h)

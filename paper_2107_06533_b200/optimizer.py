@@ -152,8 +152,10 @@ class SPDKFAC(torch.optim.Optimizer):
             n_g = S.inversion_groups([s.a_dim for s in specs], [s.g_dim for s in specs],
                                      early_fraction=early_g_fraction)["n_g"]
             cuts = [sum(n_g[:i]) for i in range(len(n_g) + 1)]
-            h = (len(fa) + 1) // 2
-            self.fwd_plan = FusionPlan(tuple(g for g in (tuple(fa[:h]), tuple(fa[h:])) if g), fusion)
+            import os
+            na = max(1, int(os.environ.get("SPDKFAC_A_GROUPS", "2")))  # A launch groups (diagnostics)
+            cuts_a = [round(i * len(fa) / na) for i in range(na + 1)]
+            self.fwd_plan = FusionPlan(tuple(tuple(fa[a:b]) for a, b in zip(cuts_a, cuts_a[1:]) if b > a), fusion)
             self.bwd_plan = FusionPlan(tuple(tuple(fg[a:b]) for a, b in zip(cuts, cuts[1:]) if b > a), fusion)
         tasks = inverse_tasks(specs)
         if placement == "lbp":
@@ -733,16 +735,17 @@ class SPDKFAC(torch.optim.Optimizer):
         self._sent[side] = True
 
     def _exchange_recv(self, side, main) -> None:
-        """Unpack the inverses received from the other owners (after main joined the comm stream)."""
-        lib = L.load()
+        """Unpack the inverses received from the other owners (after main joined the comm stream):
+        one pass per preconditioner group writes the full inverses and their operand planes."""
         for root, (ct_r, dims_r, _, views_r, n_r) in enumerate(self._bcast[side]):
             if root == self.rank or not ct_r:
                 continue
-            L.check(lib.spdkfac_unpack_upper_batched_f32(len(ct_r), L.i32_array(dims_r),
-                                                         L.ptr_array([v.data_ptr() for v in views_r]),
-                                                         L.ptr_array([self.inv[t].data_ptr() for t in ct_r]),
-                                                         main.cuda_stream), "unpack inverses")
-            self._stage_planes(ct_r, main)
+            view = dict(zip(ct_r, views_r))
+            for pside, plan in self._precond.items():
+                for which, par in (("A", 0), ("G", 1)):
+                    ts = [t for t in ct_r if t % 2 == par and self._pc_side[t // 2] == pside]
+                    plan.stage_packed(which, [self._pc_local[t // 2] for t in ts], [view[t] for t in ts],
+                                      [self.inv[t] for t in ts], main)
 
     def _stage_planes(self, tensors, stream) -> None:
         """Stage freshly produced inverses (tensor indices 2l / 2l+1) into the preconditioner

@@ -270,3 +270,32 @@ def test_precondition_golden_and_kat():
     assert torch.allclose(K.precondition(g, torch.eye(3), torch.eye(2)).cpu(), g, atol=0)
     with pytest.raises(ValueError, match="shape mismatch"):
         K.precondition(torch.zeros(2, 3), torch.eye(2), torch.eye(2))
+
+
+def test_precond_stage_packed_matches_stage_inverses():
+    """PrecondPlan.stage_packed (the broadcast path: packed inverse -> full + operand planes in one
+    pass) gives bit-identical preconditioned gradients and full inverses to unpack + stage_inverses."""
+    K = _K()
+    rng = np.random.default_rng(9)
+    shapes = [(70, 130), (200, 64)]
+    grads = [torch.tensor(rng.standard_normal(s), dtype=torch.float32, device="cuda") for s in shapes]
+    a_inv = [torch.tensor(spd(rng, s[1]), dtype=torch.float32, device="cuda") for s in shapes]
+    g_inv = [torch.tensor(spd(rng, s[0]), dtype=torch.float32, device="cuda") for s in shapes]
+    a_inv = [(m + m.T) / 2 for m in a_inv]
+    g_inv = [(m + m.T) / 2 for m in g_inv]
+    out1 = [torch.empty(s, device="cuda") for s in shapes]
+    p1 = K.PrecondPlan(shapes)
+    p1.run(g_inv, grads, a_inv, out=out1)
+    p2 = K.PrecondPlan(shapes)
+    full_a = [torch.full_like(m, float("nan")) for m in a_inv]
+    full_g = [torch.full_like(m, float("nan")) for m in g_inv]
+    p2.stage_packed("A", [0, 1], [K.pack_upper(m) for m in a_inv], full_a)
+    p2.stage_packed("G", [0, 1], [K.pack_upper(m) for m in g_inv], full_g)
+    out2 = [torch.empty(s, device="cuda") for s in shapes]
+    p2.bind(g_inv, grads, a_inv, out=out2)
+    p2.run_bound(0.0, inverses_staged=True)
+    torch.cuda.synchronize()
+    for x, y in zip(out1, out2):
+        assert torch.equal(x, y)
+    for f, m in zip(full_a + full_g, a_inv + g_inv):
+        assert torch.equal(f, m)
