@@ -5,6 +5,8 @@
 //   GEMM1  D1[m][n] = sum_k grad[m][k] A^-1[n][k]         = (grad A^-1)[m][n]     -> stored as T^T[n][m] (split)
 //   GEMM2  D2[n][m] = sum_k T^T[n][k] G^-1[m][k]         = (G^-1 grad A^-1)[m][n] -> stored as P[m][n]
 // The transposed epilogue store is the coalesced direction of the 32x32b TMEM layout.
+#include <algorithm>
+
 #include "runtime.cuh"
 
 namespace spd {
@@ -152,8 +154,10 @@ struct spdkfac_precond_plan {
   CUtensorMap* maps;
   TcItem* items1;
   TcItem* items2;
+  TcItem* items2u;  // GEMM2 items whose epilogue updates the weights in place (epis[2n + l])
   int n1, n2;
-  TcEpi* epis;
+  TcEpi* epis;      // [2l] split T^T, [2l+1] P, [2n + l] W += alpha P (weights bound at first run)
+  std::vector<float*> bound_w;
 };
 
 namespace {
@@ -224,7 +228,8 @@ size_t spdkfac_precond_workspace_size(int n, const int32_t* d_out, const int32_t
   c.take<CUtensorMap>(size_t(4) * n, 128);
   c.take<TcItem>(size_t(n1));
   c.take<TcItem>(size_t(n2));
-  c.take<TcEpi>(size_t(2) * n);
+  c.take<TcItem>(size_t(n2));
+  c.take<TcEpi>(size_t(3) * n);
   return c.used + 256;
 }
 
@@ -243,7 +248,8 @@ int spdkfac_precond_plan_create(spdkfac_precond_plan** out, int n, const int32_t
   p->maps = c.take<CUtensorMap>(size_t(4) * n, 128);
   p->items1 = c.take<TcItem>(size_t(p->n1));
   p->items2 = c.take<TcItem>(size_t(p->n2));
-  p->epis = c.take<TcEpi>(size_t(2) * n);
+  p->items2u = c.take<TcItem>(size_t(p->n2));
+  p->epis = c.take<TcEpi>(size_t(3) * n);
   if (!c.ok() || !ws) {
     delete p;
     set_error("precondition workspace too small: need %zu bytes, got %zu", c.used, ws_bytes);
@@ -296,8 +302,10 @@ int spdkfac_precond_plan_create(spdkfac_precond_plan** out, int n, const int32_t
         it2.push_back(b);
       }
   }
+  std::vector<TcItem> it2u(it2);
+  for (TcItem& b : it2u) b.epi = 2 * n + (b.epi - 1) / 2;
   if ((rc = upload(p->maps, maps, s)) || (rc = upload(p->items1, it1, s)) || (rc = upload(p->items2, it2, s)) ||
-      (rc = upload(p->epis, epis, s))) {
+      (rc = upload(p->items2u, it2u, s)) || (rc = upload(p->epis, epis, s))) {
     delete p;
     return rc;
   }
@@ -325,10 +333,30 @@ int spdkfac_precond_plan_run(spdkfac_precond_plan* p, const float* const* g_inv,
   stat_begin(kCatPrecGemm, s);
   if ((rc = launch_tc3(Kind::BF16, p->maps, p->items1, p->epis, p->n1, s))) return rc;
   stat_end(kCatPrecGemm, s, f1, 0);
+  // weight update fused into GEMM2's epilogue (W += (-alpha) P, no P round trip) once the weight
+  // pointers are bound: bound on the first run outside stream capture (weights do not move)
+  bool fused = false;
+  if (weight && !precond_out) {
+    fused = p->bound_w.size() == size_t(n) && std::equal(p->bound_w.begin(), p->bound_w.end(), weight);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    SPD_CUDA(cudaStreamIsCapturing(s, &cs));
+    if (!fused && cs == cudaStreamCaptureStatusNone) {
+      std::vector<TcEpi> ew(static_cast<size_t>(n));
+      for (int l = 0; l < n; ++l) {
+        SPD_ARG(weight[l] != nullptr, SPDKFAC_ERR_ARG, "null weight pointer for layer %d", l);
+        ew[l] = TcEpi{weight[l], p->d_in[l], 0, 0.f, 1.f, kUpdate, 0, nullptr, 0, 0};
+      }
+      SPD_CUDA(cudaMemcpyAsync(p->epis + 2 * n, ew.data(), ew.size() * sizeof(TcEpi), cudaMemcpyHostToDevice, s));
+      p->bound_w.assign(weight, weight + n);
+      fused = true;
+    }
+  }
   stat_begin(kCatPrecGemm, s);
-  if ((rc = launch_tc3(Kind::BF16, p->maps, p->items2, p->epis, p->n2, s))) return rc;
+  if ((rc = launch_tc3(Kind::BF16, p->maps, fused ? p->items2u : p->items2, p->epis, p->n2, s,
+                       TcRun{nullptr, 0, -alpha, 0.f, 1.f, 0})))
+    return rc;
   stat_end(kCatPrecGemm, s, f2, 0);
-  if (!weight && !precond_out) return SPDKFAC_OK;
+  if (fused || (!weight && !precond_out)) return SPDKFAC_OK;
   for (int off = 0; off < n; off += kMaxPtrs) {
     ApplyArgs a{};
     a.n = std::min(kMaxPtrs, n - off);

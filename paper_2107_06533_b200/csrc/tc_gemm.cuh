@@ -43,6 +43,7 @@ enum EpiMode : int32_t {
   kSplitTf32 = 2,  // out planes (fp32, tf32-exact) <- split(alpha*D)
   kPackedUpper = 3,  // packed upper triangle of a d x d symmetric target (run.out, run.d):
                      //   P = run.wscale * (run.decay * P + (1 - run.decay) * run.alpha * D), i <= j only
+  kUpdate = 4,       // out += run.alpha * D (transposed store; the weight update W -= lr * P)
 };
 
 // Per-launch arguments (kernel parameters, not table entries): what changes between runs.
@@ -148,6 +149,15 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
         out[o0 + int64_t(t) * ep.ld + ep.plane_stride] = l;
       }
     }
+  } else if (ep.mode == kUpdate) {
+    float* out = static_cast<float*>(ep.out);
+    float* base = out + (int64_t(it.out_c) + c * 32) * ep.ld + ri;  // transposed: column j -> row of target
+    float old[32];
+#pragma unroll
+    for (int t = 0; t < 32; ++t) old[t] = (row_ok && t < jn) ? base[int64_t(t) * ep.ld] : 0.f;
+#pragma unroll
+    for (int t = 0; t < 32; ++t)
+      if (row_ok && t < jn) base[int64_t(t) * ep.ld] = fmaf(run.alpha, v[t], old[t]);
   } else {  // kPackedUpper: global row gi = out_r + i, columns gj = out_c + c*32 + t, keep gj >= gi
     // target / dim / scale from the epilogue table (factor groups) or the run arguments (single plan)
     float* out = static_cast<float*>(ep.out ? ep.out : run.out);
