@@ -238,6 +238,9 @@ class SPDKFAC(torch.optim.Optimizer):
                                             for li in self._pc_layers[side]], device=self.device)
                          for side in self._pc_sides if self._pc_layers[side]}
         self._precond_key = {side: None for side in self._precond}
+        # gradient buckets (P > 1, see _bucket_hook)
+        self._grad_order, self._order_seen, self._bucket1, self._bucket_params = [], set(), None, []
+        self._b1_sent, self._b1_left, self._b1_count, self._b1_numel, self._b1_ids = False, 0, 0, 0, set()
         self._pc_done = {side: False for side in self._precond}
         self._grad_left = {side: len(self._pc_layers[side]) for side in self._precond}
 
@@ -313,12 +316,62 @@ class SPDKFAC(torch.optim.Optimizer):
             l.handles.append(l.module.register_forward_pre_hook(self._make_a_hook(l)))
             l.handles.append(l.module.register_forward_hook(self._make_out_hook(l)))
             l.handles.append(l.module.weight.register_post_accumulate_grad_hook(self._make_grad_hook(l)))
+        # P > 1: gradient bucket all-reduced during backward (see _bucket_hook)
+        self._param_handles = []
+        if self.world > 1:
+            for p in self.param_groups[0]["params"]:
+                if p.requires_grad:
+                    self._param_handles.append(p.register_post_accumulate_grad_hook(self._bucket_hook))
 
     def remove_hooks(self):
         for l in self.layers:
             for h in l.handles:
                 h.remove()
             l.handles.clear()
+        for h in getattr(self, "_param_handles", []):
+            h.remove()
+        self._param_handles = []
+
+    # ------------------------------------------------------------------ gradient buckets (P > 1)
+    # The gradient all-reduce is split into two buckets in the order gradients are accumulated
+    # (recorded in the first backward): the first ~90 % of the elements (the layers backward
+    # reaches first) is all-reduced on the comm stream as soon as its last gradient lands, under
+    # the rest of the backward pass; step() all-reduces only the remainder.  Hooks fire in the same
+    # order on every rank, so the collective sequence stays identical.  One backward per step()
+    # is assumed (gradient accumulation over several backward passes falls back to step()).
+    def _bucket_hook(self, param) -> None:
+        if self._bucket1 is None:
+            if id(param) not in self._order_seen:
+                self._order_seen.add(id(param))
+                self._grad_order.append(param)
+            return
+        if not self._b1_sent and id(param) in self._b1_ids:
+            self._b1_left -= 1
+            if self._b1_left == 0:
+                main = torch.cuda.current_stream(self.device)
+                cs = self.comm_stream
+                cs.wait_stream(main)
+                b1 = self._bucket_params[:self._b1_count]
+                flat, views = self._flat_grad_buffer(self._bucket_params)
+                with torch.cuda.stream(cs):
+                    torch._foreach_copy_(views[:self._b1_count], [p.grad for p in b1])
+                self.comm.allreduce_sum(flat[:self._b1_numel], cs, tag="grad")
+                self._b1_sent = True
+
+    def _build_buckets(self, params) -> None:
+        order = [p for p in self._grad_order if p.grad is not None]
+        if {id(p) for p in order} != {id(p) for p in params}:
+            self._bucket1 = []  # accumulation order incomplete: no bucketing
+            return
+        total = sum(p.numel() for p in order)
+        n1, acc = 0, 0
+        while n1 < len(order) - 1 and acc + order[n1].numel() <= 0.9 * total:
+            acc += order[n1].numel()
+            n1 += 1
+        self._bucket_params = order
+        self._bucket1, self._b1_count, self._b1_numel = order[:n1], n1, acc
+        self._b1_ids = {id(p) for p in order[:n1]}
+        self._b1_left = n1
 
     # ------------------------------------------------------------------ factor capture
     def _factor_args(self):
@@ -626,11 +679,25 @@ class SPDKFAC(torch.optim.Optimizer):
                     self._exchange_send(side, self._g_streams[side])
             cs.wait_stream(main)
             params = [p for p in self.param_groups[0]["params"] if p.grad is not None]
-            flat, views = self._flat_grad_buffer(params)
-            with torch.cuda.stream(cs):  # one contiguous all-reduce instead of one per parameter
-                torch._foreach_copy_(views, [p.grad for p in params])
-            self.comm.allreduce_sum(flat, cs, tag="grad")
+            if self._bucket1 is None and not capturing:
+                self._build_buckets(params)
+            if self._b1_sent:  # the first bucket was all-reduced during backward: the rest
+                params = self._bucket_params
+                flat, views = self._flat_grad_buffer(params)
+                with torch.cuda.stream(cs):
+                    torch._foreach_copy_(views[self._b1_count:], [p.grad for p in params[self._b1_count:]])
+                self.comm.allreduce_sum(flat[self._b1_numel:], cs, tag="grad")
+            else:
+                if self._bucket1:
+                    params = self._bucket_params if len(params) == len(self._bucket_params) else params
+                flat, views = self._flat_grad_buffer(params)
+                with torch.cuda.stream(cs):  # one contiguous all-reduce instead of one per parameter
+                    torch._foreach_copy_(views, [p.grad for p in params])
+                self.comm.allreduce_sum(flat, cs, tag="grad")
             self._grad_src = {id(p): v for p, v in zip(params, views)}
+            self._b1_sent = False
+            if self._bucket1:
+                self._b1_left = self._b1_count
             if not invert_now:
                 main.wait_stream(cs)
         if invert_now:
@@ -684,19 +751,21 @@ class SPDKFAC(torch.optim.Optimizer):
         return loss
 
     def _flat_grad_buffer(self, params):
-        """One fp32 buffer holding every gradient (views with each gradient's shape and
-        strides, e.g. channels-last conv weights), allocated once per parameter layout."""
-        layout = tuple((tuple(p.grad.shape), tuple(p.grad.stride()), p.grad.dtype) for p in params)
+        """One fp32 buffer holding every gradient (views with each parameter's shape and
+        strides, which its gradient follows by autograd's layout contract, e.g. channels-last
+        conv weights), allocated once per parameter layout.  Built from the parameters, so it
+        also serves while later gradients of the step are still being accumulated."""
+        layout = tuple((tuple(p.shape), tuple(p.stride()), p.dtype) for p in params)
         if getattr(self, "_flat_layout", None) != layout:
             dense = lambda g: g.is_contiguous() or (g.dim() == 4 and g.is_contiguous(memory_format=torch.channels_last))  # noqa: E731
-            if any(not dense(p.grad) or p.grad.dtype != torch.float32 for p in params):
-                raise RuntimeError("gradients must be dense float32 tensors")
-            total = sum(p.grad.numel() for p in params)
+            if any(not dense(p) or p.dtype != torch.float32 for p in params):
+                raise RuntimeError("parameters must be dense float32 tensors")
+            total = sum(p.numel() for p in params)
             flat = torch.empty(total, dtype=torch.float32, device=self.device)
             views, off = [], 0
             for p in params:
-                n = p.grad.numel()
-                views.append(flat[off:off + n].as_strided(p.grad.shape, p.grad.stride()))
+                n = p.numel()
+                views.append(flat[off:off + n].as_strided(p.shape, p.stride()))
                 off += n
             self._flat, self._flat_views, self._flat_layout = flat, views, layout
         return self._flat, self._flat_views

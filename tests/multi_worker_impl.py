@@ -64,8 +64,34 @@ def main():
     same = bool(torch.equal(ref, w_all))
     ok = torch.tensor([1 if same else 0], device=dev)
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    # several steps of a conv net: the gradient bucket all-reduced during backward (P > 1) gives the
+    # same weights as one all-reduce in step()
+    def convnet():
+        torch.manual_seed(5)
+        return nn.Sequential(nn.Conv2d(3, 8, 3, padding=1), nn.BatchNorm2d(8), nn.ReLU(), nn.Conv2d(8, 16, 3, padding=1),
+                             nn.ReLU(), nn.AdaptiveAvgPool2d(1), nn.Flatten(), nn.Linear(16, 10)).to(dev)
+    m_a, m_b = convnet(), convnet()
+    o_a = SPDKFAC(m_a, lr=0.05, damping=0.1, placement=mode, perf=perf)
+    o_b = SPDKFAC(m_b, lr=0.05, damping=0.1, placement=mode, perf=perf)
+    o_b._bucket1 = []  # no bucketing: every gradient all-reduced in step()
+    g = torch.Generator(device=dev).manual_seed(100 + rank)
+    crit = nn.CrossEntropyLoss()
+    for _ in range(3):
+        xb = torch.randn(6, 3, 8, 8, device=dev, generator=g)
+        yb = torch.randint(0, 10, (6,), device=dev, generator=g)
+        for m, o in ((m_a, o_a), (m_b, o_b)):
+            o.zero_grad(set_to_none=True)
+            crit(m(xb), yb).backward()
+            o.step()
+    torch.cuda.synchronize()
+    bucket_err = max(float((pa - pb).abs().max() / (pb.abs().max() + 1e-30))
+                     for pa, pb in zip(m_a.parameters(), m_b.parameters()))
+    bucketed = bool(o_a._bucket1)
+    for o in (o_a, o_b):
+        o.comm.close()
     if rank == 0:
         print(json.dumps({"errors": errs, "identical_on_all_ranks": bool(ok.item()), "world": world,
+                          "bucket_err": bucket_err, "bucketed": bucketed,
                           "placement": mode, "nct": sorted(opt.placement.nct),
                           "workers": [list(w) for w in opt.placement.workers]}), flush=True)
     opt.comm.close()

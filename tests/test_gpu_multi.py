@@ -30,9 +30,11 @@ def test_two_rank_step_matches_centralized(placement):
     r = _run(2, placement)
     assert r["identical_on_all_ranks"]
     assert max(r["errors"]) <= 1e-4, r
+    assert r["bucketed"] and r["bucket_err"] <= 1e-5, r  # gradient bucket during backward == one all-reduce
 
 
 def test_four_rank_step_matches_centralized():
     r = _run(4, "lbp")
     assert r["identical_on_all_ranks"]
     assert max(r["errors"]) <= 1e-4, r
+    assert r["bucketed"] and r["bucket_err"] <= 1e-5, r
