@@ -588,9 +588,12 @@ def run_reference(a):
 
 
 if __name__ == "__main__":
-    if os.environ.get("SPD_WATCHDOG"):
+    # a hung collective should end the run, not hold the GPUs: dump every thread's stack and exit
+    # after SPD_WATCHDOG seconds (default 900; 0 disables, e.g. under ncu)
+    _wd = int(os.environ.get("SPD_WATCHDOG", "900"))
+    if _wd > 0:
         import faulthandler
-        faulthandler.dump_traceback_later(int(os.environ["SPD_WATCHDOG"]), exit=True)
+        faulthandler.dump_traceback_later(_wd, exit=True)
     args = parse()
     if args.impl == "reference":
         run_reference(args)
