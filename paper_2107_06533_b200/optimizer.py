@@ -364,8 +364,10 @@ class SPDKFAC(torch.optim.Optimizer):
             self._bucket1 = []  # accumulation order incomplete: no bucketing
             return
         total = sum(p.numel() for p in order)
+        import os
+        frac = float(os.environ.get("SPDKFAC_GRAD_BUCKET", "0.9"))  # share all-reduced during backward
         n1, acc = 0, 0
-        while n1 < len(order) - 1 and acc + order[n1].numel() <= 0.9 * total:
+        while n1 < len(order) - 1 and acc + order[n1].numel() <= frac * total:
             acc += order[n1].numel()
             n1 += 1
         self._bucket_params = order
