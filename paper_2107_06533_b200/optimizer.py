@@ -9,7 +9,9 @@ It executes the step the reference emulates in `dkfac_step`
                   init-time plan (`plan_fusion`, planner.py:249-298) is all-reduced on
                   the communication stream as soon as its last member is written
   backward hooks  G_l = (b g)^T (b g) / M likewise into the backward fusion buffer
-  step()          gradient all-reduce; damped inverses of this rank's share of the
+                  the early G inversion groups are inverted mid-backward on their own
+                  streams; P > 1: the first gradient bucket is all-reduced mid-backward
+  step()          remaining gradient all-reduce; damped inverses of this rank's share of the
                   load-balanced placement (`lbp_place`, planner.py:301-356), NCT tensors
                   on every rank, CT inverses broadcast from their owners in packed form;
                   W_l -= lr * G_l^-1 grad_l A_l^-1 for every K-FAC layer (plain SGD for
@@ -18,11 +20,15 @@ It executes the step the reference emulates in `dkfac_step`
 Knobs: lr (alpha, emulator.py:207), damping (gamma, linalg.py:130), factor_decay
 (running-average rho; 0 reproduces the reference), factor_update_freq and
 inv_update_freq (the reference's single `kfac_update_interval`, simulator.py:126,
-split in two), fusion policy, placement mode ("lbp" | "seq" | "local").
+split in two), fusion policy, placement mode ("lbp" | "seq" | "local") and LBP
+balance ("dim_sq" | "dim" | "dim_cube"), early_g_fraction (inversion groups),
+launch_groups, update_in_backward (P = 1: precondition + update early groups during
+backward).  See DESIGN.md "Step schedule".
 """
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -152,7 +158,6 @@ class SPDKFAC(torch.optim.Optimizer):
             n_g = S.inversion_groups([s.a_dim for s in specs], [s.g_dim for s in specs],
                                      early_fraction=early_g_fraction)["n_g"]
             cuts = [sum(n_g[:i]) for i in range(len(n_g) + 1)]
-            import os
             na = max(1, int(os.environ.get("SPDKFAC_A_GROUPS", "2")))  # A launch groups (diagnostics)
             cuts_a = [round(i * len(fa) / na) for i in range(na + 1)]
             self.fwd_plan = FusionPlan(tuple(tuple(fa[a:b]) for a, b in zip(cuts_a, cuts_a[1:]) if b > a), fusion)
@@ -252,7 +257,6 @@ class SPDKFAC(torch.optim.Optimizer):
         self.inv_stream = torch.cuda.Stream(self.device)
         self._g_streams = {side: torch.cuda.Stream(self.device) for side in self._early}
         # index of the early G group whose launch issues the A-inverse broadcast (default: the last)
-        import os
         self._a_bcast_after = int(os.environ.get("SPDKFAC_A_BCAST_AFTER", len(self._early) - 1))
         self._g_count = 0
         self._g_inverted = {side: False for side in self._early}
@@ -364,7 +368,6 @@ class SPDKFAC(torch.optim.Optimizer):
             self._bucket1 = []  # accumulation order incomplete: no bucketing
             return
         total = sum(p.numel() for p in order)
-        import os
         frac = float(os.environ.get("SPDKFAC_GRAD_BUCKET", "0.9"))  # share all-reduced during backward
         n1, acc = 0, 0
         while n1 < len(order) - 1 and acc + order[n1].numel() <= frac * total:
