@@ -97,8 +97,10 @@ def parse():
 
 
 def workload_config(a, world):
-    idx = {"resnet20": "0", "resnet50": "1" if world == 1 else "2", "densenet201": "3"}.get(a.model)
-    return {"workload": f"{a.model} SPD-KFAC bs{a.batch}/GPU synthetic {'32x32' if a.model == 'resnet20' else '224x224'}"
+    idx = {"resnet20": "0", "resnet50": "1" if world == 1 else "2", "densenet201": "3",
+           "bert_base_linears": "4"}.get(a.model)
+    data = {"resnet20": "32x32", "bert_base_linears": "seq128 x 768 token embeddings"}.get(a.model, "224x224")
+    return {"workload": f"{a.model} SPD-KFAC bs{a.batch}/GPU synthetic {data}"
                         + (f" (BASELINE.json configs[{idx}])" if idx else " (not a BASELINE.json config)"),
             "per_gpu_batch": a.batch, "global_batch": a.batch * world, "damping": a.damping, "lr": a.lr,
             "factor_update_freq": a.factor_freq, "inv_update_freq": a.inv_freq,
@@ -316,7 +318,7 @@ def run_ours(a):
 
     torch.manual_seed(0)
     model = build_model(a.model).to(dev)
-    cl = a.memory_format == "channels_last"
+    cl = a.memory_format == "channels_last" and len(input_shape(a.model, 1)) == 4
     if cl:
         model = model.to(memory_format=torch.channels_last)
     if a.optimizer == "sgd":

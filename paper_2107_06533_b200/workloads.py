@@ -5,7 +5,8 @@ configs[0]  ResNet-20-style CIFAR net, 32x32, single worker (CPU reference runs 
 configs[1]  torchvision ResNet-50 v1.5, bs32/GPU, 224x224          (the bench workload)
 configs[2]  same at 2/4/8 GPUs (fused factor all-reduce + LBP inverses)
 configs[3]  DenseNet-201 (torchvision), bs16
-configs[4]  Inception-v4 / BERT-base linears (shape sweeps only)
+configs[4]  BERT-base linears: `bert_base_linears`, the 72 encoder linears of BERT-base at their
+            real shapes (bs32 x seq128 = 4096 rows each) in a synthetic attention-free stack
 """
 
 from __future__ import annotations
@@ -56,6 +57,41 @@ class ResNet20(nn.Module):
         return self.fc(x.mean(dim=(2, 3)))
 
 
+class _LinearBlock(nn.Module):
+    """One BERT-base encoder layer's six linears (q, k, v, o: 768x768; ffn1 768->3072, ffn2
+    3072->768) with post-LayerNorm residuals.  Attention's softmax mixing across tokens has no
+    weights and is not preconditioned, so it is replaced by a per-token gate: the K-FAC work
+    (factor rows, factor and gradient shapes) is that of BERT-base."""
+
+    def __init__(self, h=768, f=3072):
+        super().__init__()
+        self.q, self.k, self.v, self.o = (nn.Linear(h, h, bias=False) for _ in range(4))
+        self.ffn1 = nn.Linear(h, f, bias=False)
+        self.ffn2 = nn.Linear(f, h, bias=False)
+        self.ln1, self.ln2 = nn.LayerNorm(h), nn.LayerNorm(h)
+
+    def forward(self, x):
+        u = self.o(self.q(x) * torch.sigmoid(self.k(x)) + self.v(x))
+        x = self.ln1(x + u)
+        return self.ln2(x + self.ffn2(nn.functional.gelu(self.ffn1(x))))
+
+
+class BertBaseLinears(nn.Module):
+    """12 x _LinearBlock on synthetic [batch, seq, 768] token embeddings, mean-pooled into a
+    768 -> 1000 classifier (73 preconditioned linears)."""
+
+    def __init__(self, layers=12, num_classes=1000):
+        super().__init__()
+        self.blocks = nn.Sequential(*(_LinearBlock() for _ in range(layers)))
+        self.fc = nn.Linear(768, num_classes, bias=False)
+
+    def forward(self, x):
+        return self.fc(self.blocks(x).mean(dim=1))
+
+
+BERT_SEQ = 128
+
+
 def build_model(name: str) -> nn.Module:
     import torchvision
     if name == "resnet50":
@@ -66,10 +102,14 @@ def build_model(name: str) -> nn.Module:
         return torchvision.models.densenet201(weights=None)
     if name == "resnet20":
         return ResNet20()
+    if name == "bert_base_linears":
+        return BertBaseLinears()
     raise ValueError(f"unknown model {name!r}")
 
 
 def input_shape(name: str, batch: int):
+    if name == "bert_base_linears":
+        return (batch, BERT_SEQ, 768)
     return (batch, 3, 32, 32) if name == "resnet20" else (batch, 3, 224, 224)
 
 
@@ -90,7 +130,8 @@ def layer_shapes(name: str, batch: int) -> list:
                     a = mod.in_channels * mod.kernel_size[0] * mod.kernel_size[1]
                     shapes.append((n, batch * out.shape[2] * out.shape[3], a, mod.out_channels))
                 else:
-                    shapes.append((n, batch, mod.in_features, mod.out_features))
+                    rows = batch * (inp[0].numel() // inp[0].shape[-1])  # probe runs at batch 1
+                    shapes.append((n, rows, mod.in_features, mod.out_features))
             hooks.append(m.register_forward_hook(hook))
     with torch.no_grad():
         model.eval()(torch.zeros(input_shape(name, 1)))

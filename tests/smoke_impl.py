@@ -124,6 +124,40 @@ def conv_step(device="cuda:0", seed=0, gamma=0.1, lr=0.1, channels_last=False):
     return errs
 
 
+def token_linear_step(device="cuda:0", seed=0, gamma=0.1, lr=0.1, b=4, seq=24, h=48, f=96):
+    """configs[4] path: linears on [batch, seq, features] token inputs (one small
+    _LinearBlock); factor rows are the tokens (G rows scaled by the row count, the optimizer's
+    linear-layer convention), each linear's update checked against the oracle."""
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    from paper_2107_06533_b200.workloads import _LinearBlock
+    torch.manual_seed(seed)
+    model = _LinearBlock(h, f).to(device)
+    lins = {n: m for n, m in model.named_modules() if isinstance(m, nn.Linear)}
+    w0 = {n: m.weight.detach().double().cpu().numpy().copy() for n, m in lins.items()}
+    cap = {}
+    for n, m in lins.items():
+        m.register_forward_pre_hook(lambda mod, inp, n=n: cap.__setitem__(n + ".in", inp[0].detach().double().cpu().numpy()))
+        def post(mod, inp, out, n=n):  # returns None: the output is not replaced
+            out.register_hook(lambda g: cap.__setitem__(n + ".g", g.detach().double().cpu().numpy()))
+        m.register_forward_hook(post)
+    opt = SPDKFAC(model, lr=lr, damping=gamma)
+    x = torch.randn(b, seq, h, device=device)
+    y = torch.randn(b, seq, h, device=device)
+    nn.functional.mse_loss(model(x), y).backward()
+    grads = {n: m.weight.grad.detach().double().cpu().numpy() for n, m in lins.items()}
+    opt.step()
+    torch.cuda.synchronize()
+    errs = {}
+    for n, m in lins.items():
+        a_rows = cap[n + ".in"].reshape(-1, m.in_features)
+        g_rows = cap[n + ".g"].reshape(-1, m.out_features) * a_rows.shape[0]
+        w_new, *_ = O.layer_kfac_update(w0[n], [a_rows], [g_rows], [grads[n]], gamma, lr)
+        got = m.weight.detach().double().cpu().numpy()
+        errs[n] = _rel(got - w0[n], w_new - w0[n])
+    opt.remove_hooks()
+    return errs
+
+
 def run_smoke():
     import faulthandler
     import os

@@ -151,3 +151,11 @@ def test_update_in_backward_matches_step(graphed):
         assert torch.allclose(p1, p2, rtol=1e-5, atol=1e-6), (p1 - p2).abs().max()
     o1.remove_hooks()
     o2.remove_hooks()
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_token_linear_step_matches_oracle(seed):
+    """Linears on [batch, seq, features] inputs (BASELINE configs[4], BERT-base linears)."""
+    from tests.smoke_impl import TOL, token_linear_step
+    errs = token_linear_step(seed=seed)
+    assert max(errs.values()) <= TOL, errs

@@ -240,3 +240,15 @@ def test_lbp_dim_cube_balances_inversion_work():
     assert abs(r["makespan_over_lower_bound"] - 1.0) < 1e-9
     with pytest.raises(ValueError):
         P.lbp_place(tasks, 2, perf.inverse, perf.bcast, balance="dim_4")
+
+
+def test_bert_base_linear_shapes():
+    """configs[4]: the synthetic BERT-base linear stack has BERT-base's 72 encoder linears
+    (q/k/v/o 768x768, ffn 768->3072->768) at bs32 x seq128 = 4096 rows, plus the classifier."""
+    from collections import Counter
+    from paper_2107_06533_b200.workloads import layer_shapes
+    s = layer_shapes("bert_base_linears", 32)
+    assert len(s) == 73
+    assert Counter((m, a, g) for _, m, a, g in s[:-1]) == Counter(
+        {(4096, 768, 768): 48, (4096, 768, 3072): 12, (4096, 3072, 768): 12})
+    assert s[-1][1:] == (32, 768, 1000)
