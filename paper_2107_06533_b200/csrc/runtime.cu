@@ -245,7 +245,7 @@ struct PackArgs {
 };
 
 __global__ void pack_batched_kernel(const __grid_constant__ PackArgs a, int unpack) {
-  const int row = blockIdx.y;
+  const int row = blockIdx.x;  // x: a batch's rows can exceed gridDim.y's 65535
   int t = 0;
   while (t + 1 < a.n && a.row0[t + 1] <= row) ++t;
   const int64_t d = a.d[t], i = row - a.row0[t];
@@ -321,7 +321,7 @@ static int pack_batched(int n, const int32_t* dims, const float* const* src, flo
     a.row0[a.n] = rows;
     stat_begin(kCatPack, s);
     if (unpack) unpack_tiles_kernel<<<rows, 256, 0, s>>>(a);
-    else pack_batched_kernel<<<dim3(1, rows), 256, 0, s>>>(a, 0);
+    else pack_batched_kernel<<<rows, 256, 0, s>>>(a, 0);
     SPD_CHECK_LAUNCH();
     stat_end(kCatPack, s, 0, 0);
   }

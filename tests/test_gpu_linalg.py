@@ -299,3 +299,25 @@ def test_precond_stage_packed_matches_stage_inverses():
         assert torch.equal(x, y)
     for f, m in zip(full_a + full_g, a_inv + g_inv):
         assert torch.equal(f, m)
+
+
+def test_pack_batched_many_rows():
+    """A pack batch whose rows sum past 65535 (BERT-base linears at P=2: 24 x 3072 + 60 x 768
+    owned inverses): bit-exact against the oracle's pack_upper."""
+    from paper_2107_06533_b200 import _lib as L
+    lib = L.load(require_device=True)
+    dims = [3072] * 20 + [768] * 10
+    assert sum(dims) > 65535
+    g = torch.Generator(device="cuda").manual_seed(9)
+    fulls = []
+    for d in dims:
+        m = torch.randn(d, d, device="cuda", generator=g)
+        fulls.append((m + m.T) / 2)
+    packed = [torch.full((d * (d + 1) // 2,), float("nan"), device="cuda") for d in dims]
+    s = torch.cuda.current_stream().cuda_stream
+    L.check(lib.spdkfac_pack_upper_batched_f32(len(dims), L.i32_array(dims), L.ptr_array([f.data_ptr() for f in fulls]),
+                                               L.ptr_array([p.data_ptr() for p in packed]), s), "pack")
+    torch.cuda.synchronize()
+    for d, f, p in zip(dims[::7], fulls[::7], packed[::7]):
+        iu = torch.triu_indices(d, d, device="cuda")
+        assert torch.equal(p, f[iu[0], iu[1]]), d
