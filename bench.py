@@ -15,9 +15,10 @@ Factor and inverse update frequency 1 (every iteration does all of it).
 Prints ONE JSON line on rank 0.  `value` = iteration ms (max over ranks, CUDA
 events on the launching stream); `e2e` = the same through the public API with
 the batch copied from pinned host memory and the loss read back every step;
-`roofline` = the factor SYRK kernel (the dominant tcgen05 kernel) from live CUDA
-events; `cpu_baseline` = the reference's float64 linear algebra (oracle port) on
-this host's cores for the same workload.
+`roofline` = the K-FAC kernel category with the largest live CUDA-event time in
+the timed region (all categories in `roofline_kernels`, the SURVEY 8(d) iteration
+roofline fraction in `iteration_roofline`); `cpu_baseline` = the reference's
+float64 linear algebra on this host's cores for one full step of the same workload.
 """
 
 from __future__ import annotations
@@ -44,7 +45,7 @@ SCHEMES = {"spdkfac": ("optimal", "lbp"), "mpdkfac": ("naive", "seq"), "dkfac": 
            "spdkfac-nopipe": ("naive", "lbp"), "spdkfac-nolbp": ("optimal", "seq")}
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
@@ -93,7 +94,22 @@ def parse():
     p.add_argument("--stats-off", action="store_true", help="no per-launch CUDA events in the timed region (diagnostic)")
     p.add_argument("--optimizer", choices=("spdkfac", "sgd"), default="spdkfac",
                    help="sgd = diagnostic floor (forward/backward + SGD, no K-FAC); never the headline")
-    return p.parse_args()
+    return p.parse_args(argv)
+
+
+def make_optimizer(a, model, world):
+    """The SPDKFAC configuration the bench times (also used by the config-level parity tests,
+    tests/test_gpu_config_parity.py, so the checked step IS the measured step)."""
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    from paper_2107_06533_b200.planner import FusionPolicy
+    fusion, placement = SCHEMES[a.scheme]
+    if a.scheme == "spdkfac":
+        placement = a.placement
+    return SPDKFAC(model, lr=a.lr, damping=a.damping, factor_update_freq=a.factor_freq,
+                   inv_update_freq=a.inv_freq, placement=placement, balance=a.balance,
+                   fusion=FusionPolicy(fusion),
+                   early_g_fraction=tuple(float(f) for f in a.g_fractions.split(",")), launch_groups=a.launch_groups,
+                   update_in_backward=a.update_in_backward == "on" or (a.update_in_backward == "auto" and world == 1))
 
 
 def workload_config(a, world):
@@ -190,31 +206,25 @@ class Clocks:
 
 
 # ---------------------------------------------------------------- CPU reference
-def cpu_reference(model, batch, steps=None, budget_s=30.0):
-    """Time the reference's float64 K-FAC algebra for one full step (see oracle/cpu_step.py)."""
+def cpu_reference(model, batch, steps=1, warmup=0):
+    """Time the reference's float64 K-FAC algebra (oracle/cpu_step.py) for `steps` full steps; each
+    step times every distinct layer shape once, weighted by multiplicity.  Warm-up runs the
+    smallest shape (BLAS thread pool, first-touch pages), not a full step."""
     from oracle import cpu_step
     from paper_2107_06533_b200.workloads import layer_shapes
     shapes = layer_shapes(model, batch)
     keys = list(cpu_step.distinct_shapes(shapes))
+    small = min(keys, key=lambda k: k[0] * (k[1] + k[2]) + k[1] ** 3 + k[2] ** 3)
+    for _ in range(warmup):
+        cpu_step.time_layer(*small)
     cache = {}
-    per_step = []
-    if steps is None:
-        total, spent, n, _ = cpu_step.full_step_estimate(shapes, cache=cache)
-    else:  # reference arm: a rotating quarter of the distinct shapes per step
-        q = max(1, (len(keys) + 3) // 4)
-        for s in range(steps):
-            t0 = time.perf_counter()
-            cpu_step.full_step_estimate(shapes, subset=range(s * q, s * q + q), cache=cache)
-            per_step.append(time.perf_counter() - t0)
-        total, spent, n, missing = cpu_step.full_step_estimate(shapes, subset=[], cache=cache)
-        if missing:
-            idx = [keys.index(k) for k in missing]
-            total, _, _, _ = cpu_step.full_step_estimate(shapes, subset=idx, cache=cache)
+    per_step = [cpu_step.full_step(shapes, cache=cache) for _ in range(max(1, steps))]
     kind = cpu_step.implementation()[4]
-    sample = (f"{len(keys)} distinct layer shapes of {len(shapes)} {model} K-FAC layers (bs{batch}), each timed "
-              f"(factor A+G, 2 damped inverses, precondition, update; float64 numpy/scipy LAPACK) and weighted by "
-              f"multiplicity; im2col and forward/backward not charged")
-    return total * 1e3, sample, per_step, kind
+    sample = (f"full step per timed step: {len(keys)} distinct layer shapes of the {len(shapes)} {model} K-FAC layers "
+              f"(bs{batch}), each timed once (factor A+G, 2 damped inverses, precondition, update; float64 "
+              f"numpy/scipy LAPACK) and weighted by multiplicity; im2col and forward/backward not charged; "
+              f"host CPU {cpu_step.cpu_model()}")
+    return statistics.mean(per_step) * 1e3, sample, per_step, kind
 
 
 # ---------------------------------------------------------------- diagnostics
@@ -271,9 +281,9 @@ def trace_summary(step, path, torch, n=3, comm_tags=None):
     import re
     fam = {"fwd_bwd (cudnn/cutlass/aten)": r"cudnn|cutlass3x|sm80_xmma|at::native|Memset|max_pool",
            "factor stage": r"stage_rows|stage_im2col|stage_spatial", "factor syrk": r"tc3_gemm_kernel<\(spd::Kind\)1, 3|tc3_pair",
-           "factor reduce": r"reduce_pack", "inv pivot": r"pivot_kernel", "inv update": r"Kind\)2, 2, true",
-           "inv panel": r"stage_panel|Kind\)2, 3, false", "inv unpack/finalize": r"damp_unpack|finalize_kernel|small_inverse",
-           "precond": r"split_rows_batched|apply_update|tc3_gemm_kernel<\(spd::Kind\)1, 3, false>.*", "nccl": r"nccl",
+           "factor reduce": r"reduce_pack", "inv pivot": r"pivot_kernel|pivot_tc_kernel<false>", "inv update": r"Kind\)2, 3, true",
+           "precond": r"split_rows_batched|apply_update|Kind\)2, 3, false, 4", "inv panel": r"stage_panel|Kind\)2, 3, false, 0",
+           "inv unpack/finalize": r"damp_unpack|finalize_kernel|small_inverse|pivot_tc_kernel<true>", "nccl": r"nccl",
            "pack/unpack": r"pack_upper|unpack_upper"}
     step_len = (t1 - t0) / n
     last0 = t0 + (n - 1) * step_len
@@ -297,6 +307,134 @@ def trace_summary(step, path, torch, n=3, comm_tags=None):
     json.dump(out, open(path, "w"), indent=1)
 
 
+# ---------------------------------------------------------------- rooflines
+# K-FAC kernel categories timed live in the timed region (libspdkfac stats categories)
+ROOF_CATS = ("factor_stage", "factor_syrk", "inv_pivot", "inv_panel", "inv_update", "precond_gemm")
+# bound and peak of each category: the tensor-core contractions against the measured GEMM peak of
+# the MMA kind they issue (bf16 for the factor SYRK, tf32 for the inverse and the preconditioning),
+# the staging pass against HBM
+_ROOF_SPEC = {"factor_syrk": ("tensor", "bf16_tflops_sustained"), "inv_pivot": ("tensor", "tf32_tflops"),
+              "inv_panel": ("tensor", "tf32_tflops"), "inv_update": ("tensor", "tf32_tflops"),
+              "precond_gemm": ("tensor", "tf32_tflops"), "factor_stage": ("hbm", "hbm_gbs")}
+_KERNEL_NAMES = {"factor_syrk": "tc3_gemm_kernel<BF16> + tc3_pair_kernel (factor SYRK, 3 x bf16, tcgen05)",
+                 "inv_pivot": "pivot_tc_kernel<false> (128-pivot block: warp sweeps + rank-32 tcgen05 updates)",
+                 "inv_panel": "stage_panel_kernel + tc3_gemm_kernel<TF32> (inverse panel C = W[:,K] P^-1)",
+                 "inv_update": "tc3_gemm_kernel<TF32, C-tile> (inverse trailing update, 3 x tf32)",
+                 "precond_gemm": "tc3_gemm_kernel<TF32, chunked accumulation> (G^-1 grad A^-1, W -= lr P)",
+                 "factor_stage": "stage_rows / stage_im2col / stage_spatial (fp32 -> bf16 hi/lo planes)"}
+
+
+def kernel_roofline(cat, rec, per, peaks, world, model):
+    """Roofline of one kernel category from its live CUDA-event time and the algorithmic work the
+    library declares per launch (flops: SURVEY 8(d) per-unit figures x units; bytes: staging)."""
+    bound, peak_key = _ROOF_SPEC[cat]
+    ms = rec["ms"] / per
+    launches = rec["launches"] / per
+    work = rec["flops"] / per if bound == "tensor" else rec["bytes"] / per
+    ach = (work / (ms * 1e-3)) / (1e12 if bound == "tensor" else 1e9) if ms > 0 else 0.0
+    peak = peaks.get(peak_key)
+    out = {"kernel": _KERNEL_NAMES[cat], "category": cat, "bound": bound, "achieved": round(ach, 2),
+           "peak": round(peak, 1) if peak else None, "unit": "TFLOP/s" if bound == "tensor" else "GB/s",
+           "frac": round(ach / peak, 4) if peak and ms > 0 else None, "peak_source": peak_key + (
+               " (MEASURED_PEAKS.json)" if peak_key in ("hbm_gbs", "bf16_tflops_sustained") else " (measured by this run)"),
+           "kernel_ms_per_step": round(ms, 4), "launches_per_step": launches,
+           ("algorithmic_flops_per_step" if bound == "tensor" else "algorithmic_bytes_per_step"): work,
+           "traffic": None}
+    try:  # DRAM bytes per launch from a committed `ncu --set full` capture of the same launches
+        t = json.load(open(os.path.join(ROOT, "profiles", f"traffic_{model}_n{world}.json")))[cat]
+        out["traffic"] = round(t["dram_bytes_per_step"] / max(launches, 1e-9))
+        out["traffic_per_step"] = t["dram_bytes_per_step"]
+        out["traffic_source"] = t.get("source")
+    except Exception:
+        out["traffic_source"] = "no committed ncu capture for this category/config"
+    return out
+
+
+def iteration_roof(bst, nb, peaks, ffbp_flops, ms):
+    """SURVEY 8(d): iteration roofline time = sum over the step's work of max(F / peak, B / BW);
+    fraction = that / measured iteration time.  K-FAC categories from the library's declared
+    algorithmic work (per-launch event pass), forward/backward from torch's FLOP counter at the
+    TF32 GEMM peak (the convolutions run TF32), communication not included (N = 1: none)."""
+    tf32, bf16, hbm = peaks.get("tf32_tflops"), peaks.get("bf16_tflops_sustained"), peaks.get("hbm_gbs")
+    if not (tf32 and bf16 and hbm):
+        return None
+    parts = {}
+    for cat, rec in bst.items():
+        if not isinstance(rec, dict) or not (rec["flops"] or rec["bytes"]):
+            continue
+        pk = bf16 if cat == "factor_syrk" else tf32
+        parts[cat] = max(rec["flops"] / nb / (pk * 1e12), rec["bytes"] / nb / (hbm * 1e9)) * 1e3
+    if ffbp_flops:
+        parts["forward_backward"] = ffbp_flops / (tf32 * 1e12) * 1e3
+    t = sum(parts.values())
+    return {"roofline_ms": round(t, 4), "measured_ms": round(ms, 4), "frac": round(t / ms, 4) if ms else None,
+            "parts_ms": {k: round(v, 4) for k, v in parts.items()}, "ffbp_flops_per_step": ffbp_flops,
+            "peaks": {"tf32_tflops": tf32, "bf16_tflops_sustained": bf16, "hbm_gbs": hbm}}
+
+
+def measure_peaks(torch, dev, world):
+    """FP32 (cuBLAS SGEMM: FFMA) and TF32 (cuBLAS, tensor cores) GEMM peaks on this GPU, the way
+    MEASURED_PEAKS.json measures bf16 (8192^3, best of several, CUDA events); at N > 1 the NCCL
+    all-reduce bus bandwidth of a 256 MiB fp32 buffer (max over ranks)."""
+    out = {}
+    n = 8192
+    a = torch.randn(n, n, device=dev)
+    b = torch.randn(n, n, device=dev)
+    old = torch.backends.cuda.matmul.allow_tf32
+    try:
+        for name, tf32, reps in (("fp32_ffma_tflops", False, 3), ("tf32_tflops", True, 6)):
+            torch.backends.cuda.matmul.allow_tf32 = tf32
+            torch.matmul(a, b)
+            torch.cuda.synchronize()
+            best = float("inf")
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                torch.matmul(a, b)
+                e1.record()
+                torch.cuda.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            out[name] = round(2.0 * n ** 3 / (best * 1e-3) / 1e12, 1)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = old
+    del a, b
+    out["how"] = "cuBLAS fp32 matmul 8192^3 with TF32 off (FFMA) / on (tf32 tensor cores), best of 3 / 6"
+    if world > 1:
+        import torch.distributed as dist
+        buf = torch.ones(64 << 20, device=dev)  # 256 MiB
+        for _ in range(3):
+            dist.all_reduce(buf)
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(5):
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            dist.all_reduce(buf)
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            best = min(best, float(t.item()))
+        nbytes = buf.numel() * 4
+        out["nccl_allreduce_busbw_gbs"] = round(2.0 * (world - 1) / world * nbytes / (best * 1e-3) / 1e9, 1)
+        out["nccl_allreduce_bytes"] = nbytes
+        del buf
+    return out
+
+
+def count_ffbp_flops(torch, model, crit, x, y):
+    """Forward + backward FLOPs of one step (torch.utils.flop_counter; convolutions and matmuls)."""
+    try:
+        from torch.utils.flop_counter import FlopCounterMode
+        with FlopCounterMode(display=False) as fc:
+            crit(model(x), y).backward()
+        model.zero_grad(set_to_none=True)
+        return int(fc.get_total_flops())
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(a):
     import torch
@@ -316,25 +454,25 @@ def run_ours(a):
     from paper_2107_06533_b200.optimizer import SPDKFAC
     from paper_2107_06533_b200.workloads import build_model, input_shape, num_classes
 
+    measured_peaks = measure_peaks(torch, dev, world) if not a.profile else None
     torch.manual_seed(0)
     model = build_model(a.model).to(dev)
     cl = a.memory_format == "channels_last" and len(input_shape(a.model, 1)) == 4
     if cl:
         model = model.to(memory_format=torch.channels_last)
+    ffbp_flops = None
+    if not a.profile:  # before the optimizer exists: its hooks would capture this pass
+        xf = torch.randn(input_shape(a.model, a.batch), device=dev)
+        xf = xf.contiguous(memory_format=torch.channels_last) if cl else xf
+        ffbp_flops = count_ffbp_flops(torch, model, nn.CrossEntropyLoss(), xf,
+                                      torch.zeros(a.batch, dtype=torch.long, device=dev))
+        del xf
     if a.optimizer == "sgd":
         opt = torch.optim.SGD(model.parameters(), lr=a.lr)
         opt.check_inverses = lambda: None
         opt.placement = None
     else:
-        from paper_2107_06533_b200.planner import FusionPolicy
-        fusion, placement = SCHEMES[a.scheme]
-        if a.scheme == "spdkfac":
-            placement = a.placement
-        opt = SPDKFAC(model, lr=a.lr, damping=a.damping, factor_update_freq=a.factor_freq,
-                      inv_update_freq=a.inv_freq, placement=placement, balance=a.balance,
-                      fusion=FusionPolicy(fusion),
-                      early_g_fraction=tuple(float(f) for f in a.g_fractions.split(",")), launch_groups=a.launch_groups,
-                      update_in_backward=a.update_in_backward == "on" or (a.update_in_backward == "auto" and world == 1))
+        opt = make_optimizer(a, model, world)
     crit = nn.CrossEntropyLoss()
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)
@@ -376,7 +514,7 @@ def run_ours(a):
         from paper_2107_06533_b200.graph import GraphedStep
         gs = GraphedStep(model, crit, opt, [xs[0]], [ys[0]], warmup=a.warmup,
                          before_capture=lambda: _lib.stats_reset(
-                             timing=() if a.stats_off else ("factor_syrk",), reserve=400),
+                             timing=() if a.stats_off else ROOF_CATS, reserve=1200),
                          priority=a.main_priority)
         eager_step = step
 
@@ -406,7 +544,7 @@ def run_ours(a):
     # live roofline timing of the dominant kernel only (events pre-created, outside the region);
     # in graph mode the event nodes were captured into the graph (stats reset before capture)
     if not graphed:
-        _lib.stats_reset(timing=() if a.stats_off else ("factor_syrk",), reserve=200 * a.steps)
+        _lib.stats_reset(timing=() if a.stats_off else ROOF_CATS, reserve=700 * a.steps)
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -485,40 +623,24 @@ def run_ours(a):
         e2e = {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": xh[0].numel() * 4 + yh[0].numel() * 8,
                "d2h_bytes_per_step": 4, "host_wall_ms": round(max_over_ranks(e2e_wall), 3)}
 
-    # ---- roofline of the dominant tcgen05 kernel (factor SYRK), live CUDA events
-    peaks = {}
+    # ---- rooflines: every K-FAC kernel category timed live in the timed region (CUDA events on the
+    # launching streams; graph mode: the event nodes of the last replay), the dominant one as the
+    # headline `roofline`, and the iteration roofline fraction of SURVEY 8(d)
+    peaks = dict(measured_peaks) if measured_peaks else {}
     try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peaks.update({k: v for k, v in json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).items()
+                      if k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained")})
     except Exception:
         pass
-    sy = st["factor_syrk"]
-    # DRAM bytes of the same kernels from one `ncu --set full` capture of a whole step's SYRK
-    # launches (scripts/ncu_summary.py --step, committed under profiles/), if it matches
-    traffic = None
-    try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "syrk_traffic_n1.json")))
-        if world == 1 and t.get("launches_per_step") == sy["launches"] / per and t.get("model") == a.model:
-            traffic = t
-    except Exception:
-        pass
-    ach = sy["flops"] / (sy["ms"] * 1e-3) / 1e12 if sy["ms"] > 0 else 0.0  # same ratio per step or total
-    peak = peaks.get("bf16_tflops_sustained") or 1362.2
+    kern = {cat: kernel_roofline(cat, st[cat], per, peaks, world, a.model) for cat in ROOF_CATS if st[cat]["launches"]}
+    timed = {c: r for c, r in kern.items() if r["kernel_ms_per_step"] > 0}
+    dom = max(timed, key=lambda c: timed[c]["kernel_ms_per_step"]) if timed else None
+    roofline = dict(timed[dom]) if dom else None
     step_ms_total = sum(v["ms"] for k, v in bst.items() if isinstance(v, dict)) / nb
-    roofline = {"kernel": "tc3_gemm_kernel<BF16> (factor SYRK, 3 x bf16 split, tcgen05)", "bound": "tensor",
-                "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
-                "traffic": (round(traffic["dram_bytes_per_step"] / (sy["launches"] / per)) if traffic else None),
-                "traffic_source": traffic.get("source") if traffic else "no ncu capture for this launch configuration",
-                "traffic_per_step": traffic.get("dram_bytes_per_step") if traffic else None,
-                "algorithmic_bytes_per_step": sy["bytes"] / per,
-                "algorithmic_flops_per_step": sy["flops"] / per,
-                "kernel_ms_per_step": round(sy["ms"] / per, 4),
-                "launches_per_step": sy["launches"] / per,
-                "tensor_pipe_mmas_per_algorithmic_mac": 3,
-                # 3 split-precision MMAs per algorithmic MAC: the pipe executes 3 x the algorithmic rate
-                "tensor_pipe_equivalent_frac": round(3 * ach / peak, 4),
-                "share_of_library_kernel_time": round(bst["factor_syrk"]["ms"] / nb / step_ms_total, 4)
-                if step_ms_total else None}
+    if roofline is not None:
+        roofline["share_of_library_kernel_time"] = round(bst[dom]["ms"] / nb / step_ms_total, 4) if step_ms_total else None
+        roofline["why_this_kernel"] = "largest live CUDA-event time per step among the K-FAC kernel categories"
+    iteration_roofline = iteration_roof(bst, nb, peaks, ffbp_flops, ms_max)
     breakdown = {k: {"ms_per_step": round(v["ms"] / nb, 4), "launches_per_step": v["launches"] / nb,
                      "tflops": round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 2) if v["ms"] > 0 and v["flops"] else None}
                  for k, v in bst.items() if isinstance(v, dict)}
@@ -534,7 +656,7 @@ def run_ours(a):
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline and not a.profile:
-        cpu_ms, sample, _, kind = cpu_reference(a.model, a.batch)
+        cpu_ms, sample, _, kind = cpu_reference(a.model, a.batch, steps=1, warmup=1)
         cpu = {"value": round(cpu_ms, 1), "unit": "ms", "cores": int(os.environ["OPENBLAS_NUM_THREADS"]),
                "kind": kind, "sample": sample}
 
@@ -546,6 +668,7 @@ def run_ours(a):
                              "forward/backward fp32 with TF32 convolutions (cuDNN default)",
                "data": "synthetic (random N(0,1) images, uniform labels; random-init torchvision weights)",
                "config": workload_config(a, world), "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+               "roofline_kernels": kern, "iteration_roofline": iteration_roofline, "peaks_measured": measured_peaks,
                "cpu_baseline": cpu, "clocks": clk, "kernel_breakdown": breakdown,
                "placement_imbalance": _imbalance(opt) if opt.placement is not None else None,
                "host_wall_ms_per_step": round(wall_ms, 3), "per_step_ms": per_step, "allocator_in_region": alloc_diag,
@@ -576,18 +699,20 @@ def run_reference(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    ms, sample, per_step, kind = cpu_reference(a.model, a.batch, steps=max(1, a.steps))
+    w0 = time.perf_counter()
+    ms, sample, per_step, kind = cpu_reference(a.model, a.batch, steps=max(1, a.steps), warmup=a.warmup)
+    wall = time.perf_counter() - w0
     cores = int(os.environ["OPENBLAS_NUM_THREADS"])
     out = {"metric": METRIC, "impl": "reference", "value": round(ms, 1), "unit": "ms", "n_gpus": world,
            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 1), "higher_is_better": False,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": workload_config(a, world),
-           "cpu_baseline": {"value": round(ms, 1), "unit": "ms", "cores": cores, "kind": kind,
-                            "sample": sample + "; per timed step a rotating quarter of the distinct shapes"},
+           "cpu_baseline": {"value": round(ms, 1), "unit": "ms", "cores": cores, "kind": kind, "sample": sample},
            "e2e": {"value": round(ms, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-           "note": "reference kfacsched is CPU-only numpy/scipy (no GPU path); its own functions from "
-                   "baseline/_ref (kind=reference) or the oracle port (kind=port), per-shape times x "
-                   "multiplicity = one full ResNet-50 step per rank"}
+           "per_step_ms": [round(x * 1e3, 1) for x in per_step], "wall_s": round(wall, 1),
+           "note": "reference kfacsched is CPU-only numpy/scipy (no GPU path): its own functions from "
+                   "baseline/_ref (kind=reference) or the oracle port (kind=port); every timed step is a full "
+                   "step (all distinct layer shapes, weighted by multiplicity) on this rank's host cores"}
     print(json.dumps(out), flush=True)
 
 

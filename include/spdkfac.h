@@ -128,6 +128,10 @@ SPDKFAC_API int spdkfac_factor_group_create(spdkfac_factor_group** out, int n, c
 SPDKFAC_API int spdkfac_factor_group_stage(spdkfac_factor_group* g, int member, const float* x, void* stream);
 SPDKFAC_API int spdkfac_factor_group_compute(spdkfac_factor_group* g, float decay, float world_scale, void* stream);
 SPDKFAC_API void spdkfac_factor_group_destroy(spdkfac_factor_group* g);
+/* Introspection of a group's tile-engine choice for one member (tests and diagnostics):
+ * out[0] = 1 if the member runs on the CTA-pair engine (cta_group::2, 256x256 super tiles)
+ * else 0, out[1] = split-K slices, out[2] = rows M, out[3] = dim d.  No device work. */
+SPDKFAC_API int spdkfac_factor_group_describe(const spdkfac_factor_group* g, int member, int64_t out[4]);
 
 /* ------------------------------------------------------------------ packing
  * pack_upper / unpack_upper (linalg.py:181-199) on device. `ld` = row stride

@@ -46,13 +46,18 @@ def distinct_shapes(shapes):
     return Counter((m, a, g) for _, m, a, g in shapes)
 
 
-def time_layer(m: int, a: int, g: int, gamma: float = 0.1, alpha: float = 0.1, seed: int = 0) -> float:
-    fa, fg, dinv, pre, _ = implementation()
+def layer_inputs(m: int, a: int, g: int, seed: int = 0):
+    """Synthetic float64 inputs of one layer: A rows [m, a], G rows [m, g], gradient and weight [g, a]."""
     rng = np.random.default_rng(seed)
-    rows_a = rng.standard_normal((m, a))
-    rows_g = rng.standard_normal((m, g))
-    grad = rng.standard_normal((g, a))
-    w = rng.standard_normal((g, a))
+    return rng.standard_normal((m, a)), rng.standard_normal((m, g)), rng.standard_normal((g, a)), \
+        rng.standard_normal((g, a))
+
+
+def time_layer(m: int, a: int, g: int, gamma: float = 0.1, alpha: float = 0.1, seed: int = 0, inputs=None) -> float:
+    """Seconds of the reference's per-layer step arithmetic on (m, a, g): factors, both damped
+    inverses, preconditioning and the update (input generation is not timed)."""
+    fa, fg, dinv, pre, _ = implementation()
+    rows_a, rows_g, grad, w = inputs if inputs is not None else layer_inputs(m, a, g, seed)
     t0 = time.perf_counter()
     A = fa(rows_a)
     G = fg(rows_g)
@@ -69,18 +74,26 @@ def threads() -> int:
     return os.cpu_count() or 1
 
 
-def full_step_estimate(shapes, subset=None, cache=None) -> tuple:
-    """Time (a subset of) the distinct shapes; return (estimated seconds for the
-    whole step, seconds actually spent, number of shapes timed)."""
+def full_step(shapes, cache=None) -> float:
+    """One measured step of the whole workload: every distinct layer shape timed once, weighted by
+    its multiplicity (the per-layer arithmetic depends only on the shape).  `cache` keeps each
+    shape's synthetic inputs across steps (generating them costs more than some layers)."""
     cnt = distinct_shapes(shapes)
-    keys = list(cnt)
     cache = {} if cache is None else cache
-    todo = keys if subset is None else [keys[i % len(keys)] for i in subset]
-    spent = 0.0
-    for k in todo:
-        t = time_layer(*k)
-        spent += t
-        cache.setdefault(k, []).append(t)
-    missing = [k for k in keys if k not in cache]
-    total = sum(cnt[k] * float(np.mean(cache[k])) for k in keys if k in cache)
-    return total, spent, len(todo), missing
+    total = 0.0
+    for k, mult in cnt.items():
+        if k not in cache:
+            cache[k] = layer_inputs(*k)
+        total += mult * time_layer(*k, inputs=cache[k])
+    return total
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"

@@ -50,6 +50,7 @@ SIGNATURES = {
     "spdkfac_factor_group_stage": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "spdkfac_factor_group_compute": (C.c_int, [_vp, _f32, _f32, _vp]),
     "spdkfac_factor_group_destroy": (None, [_vp]),
+    "spdkfac_factor_group_describe": (C.c_int, [_vp, C.c_int, C.POINTER(_i64)]),
     "spdkfac_pack_upper_f32": (C.c_int, [_vp, _i64, _i64, _vp, _vp]),
     "spdkfac_unpack_upper_f32": (C.c_int, [_vp, _i64, _vp, _i64, _vp]),
     "spdkfac_pack_upper_batched_f32": (C.c_int, [C.c_int, _pi32, _pp, _pp, _vp]),

@@ -30,14 +30,11 @@ _COMM = {"GradComm", "FactorComm", "InverseComm"}
 
 _K = r"tc3_gemm_kernel<(?:\(spd::Kind\))?"
 _RULES = (
-    ("FactorComp", r"stage_rows|stage_im2col|stage_spatial|reduce_pack|tc3_pair"),
-    ("InverseComp", r"pivot_kernel|stage_panel|small_inverse|damp_unpack|finalize_kernel|unpack_upper|pack_upper|"
-                    + _K + "2,"),
-    ("Precondition", r"split_rows_batched|apply_update"),
+    ("Precondition", r"split_rows_batched|apply_update|" + _K + r"2, \d+, false, [1-9]"),  # TF32, chunked accumulation
+    ("FactorComp", r"stage_rows|stage_im2col|stage_spatial|reduce_pack|tc3_pair|" + _K + "1,"),  # bf16 SYRK
+    ("InverseComp", r"pivot_kernel|pivot_tc_kernel|stage_panel|small_inverse|damp_unpack|finalize_kernel|"
+                    r"unpack_upper|pack_upper|" + _K + "2,"),
 )
-# the factor SYRK and the preconditioning GEMMs are the same kernel instance (bf16 split,
-# 3 stages): the launching stream tells them apart (preconditioning runs on the main stream)
-_BF16_TC = _K + "1,"
 
 
 # comm tags recorded by NcclComm -> category
@@ -47,8 +44,6 @@ COMM_TAGS = {"factor": "FactorComm", "inverse": "InverseComm", "grad": "GradComm
 def classify(name: str, on_main: bool = False) -> str:
     """Category of one non-NCCL kernel; everything that is not ours is forward/backward (FFBP).
     on_main: the kernel ran on the main (forward/backward) stream."""
-    if re.search(_BF16_TC, name):
-        return "Precondition" if on_main else "FactorComp"
     for cat, rx in _RULES:
         if re.search(rx, name):
             return cat

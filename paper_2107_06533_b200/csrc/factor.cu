@@ -427,6 +427,11 @@ int member_init(Member* mb, const spdkfac_factor_geom* g) {
     if ((mb->T % 2 == 0 && mb->T >= 4 && units * sp >= 48) || (mb->T == 2 && M >= 200000)) mb->S = S;
   }
   mb->splits = mb->S ? choose_splits(mb->Mpad, mb->S * (mb->S + 1) / 2, 74) : choose_splits(mb->Mpad, mb->n_tiles, 148);
+  // every K slice must be non-empty: reduce_pack_kernel sums all `splits` partial slots, and
+  // an empty slice would leave its (uninitialised) slot unwritten.  With per = cdiv(nkb, s),
+  // cdiv(nkb, per) slices of `per` blocks cover nkb and the last one holds >= 1 block.
+  const int64_t nkb = mb->Mpad / 64, per = cdiv(nkb, int64_t(mb->splits));
+  mb->splits = int(cdiv(nkb, per));
   return SPDKFAC_OK;
 }
 
@@ -746,5 +751,12 @@ int spdkfac_factor_group_compute(spdkfac_factor_group* G, float decay, float wor
 }
 
 void spdkfac_factor_group_destroy(spdkfac_factor_group* G) { delete G; }
+
+int spdkfac_factor_group_describe(const spdkfac_factor_group* G, int member, int64_t out[4]) {
+  SPD_ARG(G && out && member >= 0 && member < int(G->m.size()), SPDKFAC_ERR_ARG, "bad describe arguments");
+  const Member& mb = G->m[member];
+  out[0] = mb.S ? 1 : 0, out[1] = mb.splits, out[2] = mb.M, out[3] = mb.d;
+  return SPDKFAC_OK;
+}
 
 }  // extern "C"

@@ -180,6 +180,279 @@ __device__ __forceinline__ float packed_at(const float* p, int64_t d, int64_t i,
   return p[r * (2 * d - r + 1) / 2 + (c - r)];
 }
 
+// ---------------------------------------------------------------- 128-pivot block on tcgen05
+// One CTA (256 threads = 8 warps) sweeps one 128 x 128 pivot block P.  Thread (row i, half h)
+// keeps D[i][64 h, 64 h + 64) in registers (warp w: TMEM lanes / rows [32 (w % 4), +32),
+// h = w / 4).  Four 32-pivot steps s (K = columns [32 s, 32 s + 32), held by half s / 2):
+//   1. the K columns of every row go to shared memory (fp32, and as the tf32 hi/lo A operand);
+//      warp s + 4 (s / 2) (rows K) sweeps the 32 x 32 pivot block in registers with warp
+//      shuffles -> S_K = -P_K^-1.  The pivots are the Schur complements in order, so the first
+//      non-positive one is LAPACK dpotrf's failing index;
+//   2. every thread forms C[i][16 h, 16 h + 16) = D[i,K] P_K^-1 (FFMA, P_K^-1 broadcast);
+//   3. one thread issues U = A B^T, A = D[:,K], B = -C (3 x tf32: 12 tcgen05 MMAs, M = N = 128,
+//      K = 8) into a fresh TMEM accumulator; every thread adds its row of U to its registers
+//      (round-to-nearest fp32: TMEM accumulation truncates, so D itself never lives there);
+//   4. fix-up in registers: D[i,K] = C[i] (i not in K), D[K,j] = C[j]^T, D[K,K] = S_K.
+// After the four steps D = -P^-1.  This replaces 16 barrier-separated rank-8 FFMA sweeps of the
+// whole block (the round-1 pivot kernel: 59 us per block under ncu, IPC 0.27) by four short warp
+// sweeps and four rank-32 tensor-core updates.  The sweep loop is kept rolled (8 pivots per
+// unrolled body, the row rotated in registers between bodies) so the kernel's code stays in the
+// instruction cache.
+namespace pvt {
+constexpr int kThreads = 256;
+constexpr int kPvLd = 36;                 // P_K^-1 rows: float4-aligned, conflict-free float4 stores
+constexpr int kLd = 33;                   // fp32 row-major staging (D[:,K], C): conflict-free columns
+constexpr uint32_t kOpBytes = 128 * 128;  // one 128 x 32 fp32 operand plane (128-B rows, SWIZZLE_128B)
+constexpr size_t kSmem = 1024 + 4 * size_t(kOpBytes) + size_t(2 * 128 * kLd + 32 * kPvLd) * 4 + 64;
+static_assert(4 * kOpBytes + 2 * 128 * kLd * 4 >= 128 * 129 * 4, "small-path output staging fits");
+// byte offset of 16-B chunk `chunk` of row i in a K-major 128 x 32 fp32 plane with the 128-B swizzle
+__device__ __forceinline__ uint32_t sw128(int i, int chunk) { return uint32_t(i) * 128u + (uint32_t(chunk ^ (i & 7)) << 4); }
+__device__ __forceinline__ void put_split(uint8_t* plane_hi, uint32_t off, float4 x) {
+  float4 h, l;
+  split_tf32(x.x, h.x, l.x);
+  split_tf32(x.y, h.y, l.y);
+  split_tf32(x.z, h.z, l.z);
+  split_tf32(x.w, h.w, l.w);
+  *reinterpret_cast<float4*>(plane_hi + off) = h;
+  *reinterpret_cast<float4*>(plane_hi + kOpBytes + off) = l;
+}
+__device__ __forceinline__ float rcp_nr(float x) {  // reciprocal: MUFU approximation + one Newton step
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r * fmaf(-x, r, 2.f);
+}
+// Sweep the 32 x 32 block held by one warp (lane r = row r, w[t] = D[r][t]) -> -D^-1; returns the
+// first non-positive pivot (warp-uniform) or -1.  Pivot p = 8 pb + u: the row is kept rotated by
+// 8 pb so that column p sits in register u of the unrolled body.
+__device__ __forceinline__ int sweep32(float (&w)[32], int lane) {
+  int fail = -1;
+#pragma unroll 1
+  for (int pb = 0; pb < 4; ++pb) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int p = 8 * pb + u;
+      const float piv = __shfl_sync(0xffffffffu, w[u], p);
+      if (!(piv > 0.f)) {  // warp-uniform (broadcast value); NaN fails too
+        fail = p;
+        break;
+      }
+      const float rinv = rcp_nr(piv);
+      const bool me = lane == p;
+      const float fct = w[u] * rinv;
+      const float mult = me ? rinv : -fct;
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        if (t == u) continue;
+        const float rp = __shfl_sync(0xffffffffu, w[t], p);
+        w[t] = fmaf(mult, rp, me ? 0.f : w[t]);
+      }
+      w[u] = me ? -rinv : fct;
+    }
+    if (fail >= 0) break;
+    float tmp[8];  // rotate left by 8: the next body's pivot columns move to registers 0..7
+#pragma unroll
+    for (int t = 0; t < 8; ++t) tmp[t] = w[t];
+#pragma unroll
+    for (int t = 0; t < 24; ++t) w[t] = w[t + 8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) w[24 + t] = tmp[t];
+  }
+  return fail;
+}
+}  // namespace pvt
+
+// kSmall: the whole matrix (d <= 128, packed input + gamma I, identity padding) -> out =
+// -(D + D^T)/2 cropped to d x d.  Otherwise: pivot block k of a blocked matrix (W[K,K]) ->
+// W[K,K] = -P^-1 and P^-1 as tf32 hi/lo planes for the panel GEMM.
+template <bool kSmall>
+__global__ void __launch_bounds__(pvt::kThreads, 1)
+    pivot_tc_kernel(const InvMat* __restrict__ mats, const int32_t* __restrict__ ids, int k,
+                    float* __restrict__ pinv_planes, int64_t pinv_plane, float gamma) {
+  using namespace pvt;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* opA = sm;                  // A hi, lo planes
+  uint8_t* opB = sm + 2 * kOpBytes;   // B hi, lo planes
+  float* Ar = reinterpret_cast<float*>(sm + 4 * kOpBytes);  // D[:,K] fp32 [128][kLd]
+  float* Cs = Ar + 128 * kLd;                                // C fp32 [128][kLd]
+  float* Pv = Cs + 128 * kLd;                                // P_K^-1 [32][kPvLd]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Pv + 32 * kPvLd);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  int* sfail = reinterpret_cast<int*>(tslot + 1);
+
+  const InvMat m = mats[ids[blockIdx.x]];
+  if constexpr (!kSmall) {
+    if (*m.info != 0) return;  // an earlier pivot block failed (uniform)
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, h = warp >> 2, i = 32 * q + lane;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<128>(tslot);
+  const int n = kSmall ? m.d : kB;
+  const int64_t dp = m.dp, K0 = int64_t(k) * kB;
+
+  float d[64];  // D[i][64 h + t]
+  if constexpr (kSmall) {
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+      const int j = 64 * h + t;
+      d[t] = (i < n && j < n) ? packed_at(m.in, n, i, j) + (i == j ? gamma : 0.f) : (i == j ? 1.f : 0.f);
+    }
+  } else {
+    const float4* src = reinterpret_cast<const float4*>(m.W + (K0 + i) * dp + K0 + 64 * h);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const float4 x = __ldcg(src + t);
+      d[4 * t] = x.x, d[4 * t + 1] = x.y, d[4 * t + 2] = x.z, d[4 * t + 3] = x.w;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t tU = tbase + (uint32_t(32 * q) << 16) + uint32_t(64 * h);  // this thread's U row half
+
+  constexpr uint32_t idesc = make_idesc<Kind::TF32>(128, 128);
+  const int nsteps = (n + 31) >> 5;
+  int fail = -1;
+#pragma unroll 1
+  for (int s = 0; s < nsteps; ++s) {
+    const int c0 = 32 * s, hs = s >> 1;
+    const bool odd = s & 1;
+    // ---- 1. D[:,K] -> shared memory (fp32 + the A operand planes); the pivot warp sweeps
+    if (h == hs) {
+      float a[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) a[t] = odd ? d[32 + t] : d[t];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) Ar[i * kLd + t] = a[t];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) put_split(opA, sw128(i, t), make_float4(a[4 * t], a[4 * t + 1], a[4 * t + 2], a[4 * t + 3]));
+      if (q == s) {
+        const int f = sweep32(a, lane);
+#pragma unroll
+        for (int t = 0; t < 8; ++t)  // P_K^-1 = -S_K
+          *reinterpret_cast<float4*>(Pv + lane * kPvLd + 4 * t) =
+              make_float4(-a[4 * t], -a[4 * t + 1], -a[4 * t + 2], -a[4 * t + 3]);
+        if (lane == 0) *sfail = f;
+      }
+    }
+    __syncthreads();
+    const int f = *sfail;
+    if (f >= 0) {  // uniform
+      fail = c0 + f;
+      break;
+    }
+    // ---- 2. C[i][16 h + jj] = sum_kk D[i, K0 + kk] P_K^-1[kk][16 h + jj]
+    float c[16];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) c[jj] = 0.f;
+#pragma unroll 4
+    for (int kk = 0; kk < 32; ++kk) {
+      const float x = Ar[i * kLd + kk];
+      const float4* pr = reinterpret_cast<const float4*>(Pv + kk * kPvLd + 16 * h);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float4 p4 = pr[t];
+        c[4 * t] = fmaf(x, p4.x, c[4 * t]);
+        c[4 * t + 1] = fmaf(x, p4.y, c[4 * t + 1]);
+        c[4 * t + 2] = fmaf(x, p4.z, c[4 * t + 2]);
+        c[4 * t + 3] = fmaf(x, p4.w, c[4 * t + 3]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      put_split(opB, sw128(i, 4 * h + t), make_float4(-c[4 * t], -c[4 * t + 1], -c[4 * t + 2], -c[4 * t + 3]));
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) Cs[i * kLd + 16 * h + jj] = c[jj];
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    // ---- 3. U = A B^T on the tensor cores, D += U in registers
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+      const uint64_t ah = make_sdesc_sw128(opA), al = make_sdesc_sw128(opA + kOpBytes);
+      const uint64_t bh = make_sdesc_sw128(opB), bl = make_sdesc_sw128(opB + kOpBytes);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 B of K per 128-B swizzle row
+        const uint64_t off = uint64_t(kk * 2);
+        umma<Kind::TF32>(tbase, ah + off, bh + off, idesc, kk != 0);
+        umma<Kind::TF32>(tbase, ah + off, bl + off, idesc, 1u);
+        umma<Kind::TF32>(tbase, al + off, bh + off, idesc, 1u);
+      }
+      tc_commit(bar);
+    }
+    mbar_wait(bar, uint32_t(s & 1));
+    tc_fence_after();
+    {
+      uint32_t u0[32], u1[32];
+      tmem_ld_32x32b_x32_nowait(tU, u0);
+      tmem_ld_32x32b_x32_nowait(tU + 32, u1);
+      tmem_ld_wait();
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        d[t] += __uint_as_float(u0[t]);
+        d[32 + t] += __uint_as_float(u1[t]);
+      }
+    }
+    // ---- 4. fix-up of row / column block K
+    if (q != s) {
+      if (h == hs) {  // D[i,K] = C[i]
+        if (odd) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) d[32 + t] = Cs[i * kLd + t];
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) d[t] = Cs[i * kLd + t];
+        }
+      }
+    } else {  // rows K: D[K,j] = C[j]^T (j not in K), D[K,K] = S_K = -P_K^-1
+#pragma unroll
+      for (int t = 0; t < 64; ++t) {
+        const int j = 64 * h + t;
+        d[t] = (j >= c0 && j < c0 + 32) ? -Pv[lane * kPvLd + (j - c0)] : Cs[j * kLd + lane];
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // shared staging and the TMEM accumulator are reused by the next step
+    tc_fence_after();
+  }
+
+  if (fail >= 0) {
+    if (threadIdx.x == 0) *m.info = int(kSmall ? 0 : K0) + fail + 1;
+  } else if constexpr (!kSmall) {
+    float4* dst = reinterpret_cast<float4*>(m.W + (K0 + i) * dp + K0 + 64 * h);  // W[K,K] <- -P^-1
+    float* ph = pinv_planes + (int64_t(m.slot) * kB + i) * kB + 64 * h;          // P^-1 hi / lo planes
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      dst[t] = make_float4(d[4 * t], d[4 * t + 1], d[4 * t + 2], d[4 * t + 3]);
+      float4 hi, lo;
+      split_tf32(-d[4 * t], hi.x, lo.x);
+      split_tf32(-d[4 * t + 1], hi.y, lo.y);
+      split_tf32(-d[4 * t + 2], hi.z, lo.z);
+      split_tf32(-d[4 * t + 3], hi.w, lo.w);
+      reinterpret_cast<float4*>(ph)[t] = hi;
+      reinterpret_cast<float4*>(ph + pinv_plane)[t] = lo;
+    }
+  } else {  // out = -(D + D^T)/2 cropped, through shared memory (the staging area is free now)
+    float* F = reinterpret_cast<float*>(sm);
+#pragma unroll
+    for (int t = 0; t < 64; ++t) F[i * 129 + 64 * h + t] = d[t];
+    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int r = e / n, cc = e - r * n;
+      m.out[e] = -0.5f * (F[r * 129 + cc] + F[cc * 129 + r]);
+    }
+    if (threadIdx.x == 0) *m.info = 0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_free<128>(tbase);
+}
+
 // ---------------------------------------------------------------- d <= 128
 __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __restrict__ mats,
                                                             const int32_t* __restrict__ ids, float gamma) {
@@ -417,6 +690,7 @@ struct spdkfac_inverse_plan {
   std::vector<double> upd_flops, u2_flops;  // per step: U1 / U2 tensor work (algorithmic, per launch)
   cudaStream_t side = nullptr;  // look-ahead stream: pivot/stage/panel of step k+1
   bool lookahead = true;        // SPDKFAC_NO_LOOKAHEAD=1 serialises (diagnostics)
+  bool legacy_pivot = false;    // SPDKFAC_PIVOT=ffma: the round-1 FFMA pivot sweep (A/B diagnostics)
   int panel_ctas = 0;           // grid cap of the panel GEMM (SPDKFAC_PANEL_CTAS; 0 = all SMs: the chain latency wins)
   cudaEvent_t ev_u1 = nullptr, ev_panel = nullptr;
   int32_t* act_ids;             // device, active blocked matrices per step (concatenated)
@@ -682,6 +956,8 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     if (const char* pc = getenv("SPDKFAC_PANEL_CTAS")) p->panel_ctas = atoi(pc);
     const char* e = getenv("SPDKFAC_NO_LOOKAHEAD");
     p->lookahead = !(e && e[0] == '1');
+    const char* pv = getenv("SPDKFAC_PIVOT");
+    p->legacy_pivot = pv && std::string(pv) == "ffma";
   }
   if (p->n_blocked > 0) {
     SPD_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
@@ -691,6 +967,8 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   static bool attrs = false;
   if (!attrs) {
     SPD_CUDA(cudaFuncSetAttribute(small_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kB * kSmemLd * 4));
+    SPD_CUDA(cudaFuncSetAttribute(pivot_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pvt::kSmem)));
+    SPD_CUDA(cudaFuncSetAttribute(pivot_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pvt::kSmem)));
     attrs = true;
   }
   *out = p;
@@ -703,7 +981,10 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p->n_small > 0) {
     stat_begin(kCatInvSmall, s);
-    small_inverse_kernel<<<p->n_small, 512, kB * kSmemLd * 4, s>>>(p->mats, p->small_ids, gamma);
+    if (p->legacy_pivot)
+      small_inverse_kernel<<<p->n_small, 512, kB * kSmemLd * 4, s>>>(p->mats, p->small_ids, gamma);
+    else
+      pivot_tc_kernel<true><<<p->n_small, pvt::kThreads, pvt::kSmem, s>>>(p->mats, p->small_ids, 0, nullptr, 0, gamma);
     SPD_CHECK_LAUNCH();
     stat_end(kCatInvSmall, s, p->small_flops, 0);
   }
@@ -718,8 +999,12 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       const int na = p->act_cnt[k];
       float* pa = p->panA + (k % kPanSlots) * kB;
       stat_begin(kCatInvPivot, q);
-      pivot_kernel<<<na, 512, 0, q>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
-                                      int64_t(p->n_blocked) * kB * kB);
+      if (p->legacy_pivot)
+        pivot_kernel<<<na, 512, 0, q>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
+                                        int64_t(p->n_blocked) * kB * kB);
+      else
+        pivot_tc_kernel<false><<<na, pvt::kThreads, pvt::kSmem, q>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
+                                                                     int64_t(p->n_blocked) * kB * kB, 0.f);
       SPD_CHECK_LAUNCH();
       stat_end(kCatInvPivot, q, 2.0 * kB * kB * kB * na, 0);
       stat_begin(kCatInvPanel, q);

@@ -136,13 +136,13 @@ static bool tile_grid() {
   return mode == 1;
 }
 
-template <Kind K, int kSt, bool kCTile>
+template <Kind K, int kSt, bool kCTile, int kAcc = 0>
 static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
                        const TcRun& run, int max_ctas = 0) {
   constexpr size_t smem = tc_smem_bytes<kSt>(kCTile);
   static bool attr_set = false;
   if (!attr_set) {
-    SPD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<K, kSt, kCTile>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SPD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<K, kSt, kCTile, kAcc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem)));
     attr_set = true;
   }
@@ -160,7 +160,7 @@ static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi
   int cap = sms;
   if (max_ctas > 0 && max_ctas < cap) cap = max_ctas;
   const int grid = (tile_grid() || n < cap) ? n : cap;
-  tc3_gemm_kernel<K, kSt, kCTile><<<grid, 192, smem, s>>>(maps, items, epis, run, n);
+  tc3_gemm_kernel<K, kSt, kCTile, kAcc><<<grid, 192, smem, s>>>(maps, items, epis, run, n);
   SPD_CHECK_LAUNCH();
   return SPDKFAC_OK;
 }
@@ -170,6 +170,12 @@ int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const Tc
   if (n <= 0) return SPDKFAC_OK;
   return kind == Kind::BF16 ? launch_kind<Kind::BF16, kStages, false>(maps, items, epis, n, s, run, max_ctas)
                             : launch_kind<Kind::TF32, kStages, false>(maps, items, epis, n, s, run, max_ctas);
+}
+
+int launch_tc3_acc(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
+                   const TcRun& run) {
+  if (n <= 0) return SPDKFAC_OK;
+  return launch_kind<Kind::TF32, kStages, false, kAccChunk>(maps, items, epis, n, s, run);
 }
 
 int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s) {

@@ -86,6 +86,11 @@ int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const Tc
 int launch_tc3_pair(const CUtensorMap* maps, const TcPairItem* items, const TcEpi* epis, int n_items, cudaStream_t s,
                     const TcRun& run);
 int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items, cudaStream_t s);
+// TF32 engine with chunked accumulation (kAccChunk K blocks of 32 per TMEM chunk, chunks summed in
+// fp32 registers): the preconditioning GEMMs (see tc3_gemm_kernel's kAcc)
+constexpr int kAccChunk = 4;
+int launch_tc3_acc(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items, cudaStream_t s,
+                   const TcRun& run = TcRun{});
 // 2-D tensor map over a row-major fp32 matrix [rows][ld], box 128 x 128, no swizzle
 int make_ctile_map(CUtensorMap* out, const float* base, int64_t rows, int64_t cols, int64_t ld);
 

@@ -206,10 +206,18 @@ constexpr size_t tc_smem_bytes(bool ctile) {
   return size_t(kSt) * kStageBytes + (ctile ? kCRing * kCSliceBytes : 0) + 1024 + 256;
 }
 
-template <Kind K, int kSt, bool kCTile>
+// kAcc > 0: chunked accumulation.  tcgen05.mma accumulates into TMEM with truncation (measured on
+// B200: a positive K = 4608 tf32 sum comes out 3.3e-5 low, ~2^-24 per accumulating MMA), which a
+// long K chain turns into a biased relative error; the preconditioning GEMMs (K = d_in <= 4608,
+// heavy cancellation when the gradient lies in a rank-deficient factor's span) need better.  With
+// kAcc, each item's K range is cut into chunks of kAcc K blocks, every chunk is accumulated afresh
+// in a TMEM buffer (the two buffers alternate per chunk) and the epilogue warps add the chunks
+// into a 128-float register accumulator per row with round-to-nearest fp32 adds.
+template <Kind K, int kSt, bool kCTile, int kAcc = 0>
 __global__ void __launch_bounds__(192, 1)
     tc3_gemm_kernel(const CUtensorMap* __restrict__ maps, const TcItem* __restrict__ items,
                     const TcEpi* __restrict__ epis, const TcRun run, int n_items) {
+  static_assert(kAcc == 0 || !kCTile, "chunked accumulation is for register epilogues");
   constexpr int BK = (K == Kind::BF16) ? 64 : 32;  // one 128-byte swizzle row of K
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -235,7 +243,10 @@ __global__ void __launch_bounds__(192, 1)
     for (int q = 0; q < kCRing; ++q) mbar_init(&cfull[q], 1);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (kAcc > 0) tmem_alloc<512>(tmem_slot);  // + the chunk-sum accumulator
+    else tmem_alloc<256>(tmem_slot);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -286,15 +297,19 @@ __global__ void __launch_bounds__(192, 1)
       constexpr uint32_t idesc_k = make_idesc<K>(128, 128);
       constexpr uint32_t idesc_mn = idesc_k | (1u << 15) | (1u << 16);  // transpose A and B
       uint32_t g = 0, t = 0;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         const TcItem it = items[item];
         const bool same = (it.flags & kSameAB) != 0;
+        const int nch = kAcc ? max(1, (it.nk + kAcc - 1) / max(kAcc, 1)) : 1;
+        for (int ch = 0; ch < nch; ++ch, ++t) {
         const uint32_t buf = t & 1, use = t >> 1;
         mbar_wait(&tempty[buf], (use & 1) ^ 1);  // epilogue has drained this accumulator
         tc_fence_after();
         const uint32_t acc = tmem + buf * 128;
-        for (int kb = 0; kb < it.nk; ++kb, ++g) {
+        const int kb0 = kAcc ? ch * kAcc : 0, kb1 = kAcc ? min(it.nk, kb0 + kAcc) : it.nk;
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const uint32_t s = g % kSt;
+          const uint32_t first = uint32_t(kb - kb0);  // 0: this chunk starts a fresh accumulator
           mbar_wait(&full[s], (g / kSt) & 1);
           tc_fence_after();
           uint8_t* st = smem + s * kStageBytes;
@@ -306,7 +321,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {  // 16 K rows = two 1024-B atoms per instruction
               const uint64_t off = uint64_t(kk * (2048 >> 4));
-              umma<K>(acc, ahi + off, bhi + off, idesc_mn, (kb | kk) != 0);
+              umma<K>(acc, ahi + off, bhi + off, idesc_mn, (first | kk) != 0);
               umma<K>(acc, ahi + off, blo + off, idesc_mn, 1u);
               umma<K>(acc, alo + off, bhi + off, idesc_mn, 1u);
             }
@@ -318,7 +333,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 B of K per 128-B swizzle row
               const uint64_t off = uint64_t(kk * 2);
-              umma<K>(acc, ahi + off, bhi + off, idesc_k, (kb | kk) != 0);
+              umma<K>(acc, ahi + off, bhi + off, idesc_k, (first | kk) != 0);
               umma<K>(acc, ahi + off, blo + off, idesc_k, 1u);
               umma<K>(acc, alo + off, bhi + off, idesc_k, 1u);
             }
@@ -326,6 +341,7 @@ __global__ void __launch_bounds__(192, 1)
           tc_commit(&empty[s]);  // smem slot free once these MMAs retire
         }
         tc_commit(&tfull[buf]);
+        }
       }
     }
     __syncwarp();
@@ -354,6 +370,43 @@ __global__ void __launch_bounds__(192, 1)
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
       const TcItem it = items[item];
       const TcEpi ep = epis[it.epi];
+      if constexpr (kAcc > 0) {  // sum the item's chunks in TMEM columns [256, 384), then one epilogue
+        const int nch = max(1, (it.nk + kAcc - 1) / kAcc);
+        const uint32_t lane_off = uint32_t(quad * 32) << 16;
+        for (int ch = 0; ch < nch; ++ch, ++t) {
+          const uint32_t buf = t & 1, use = t >> 1;
+          mbar_wait(&tfull[buf], use & 1);
+          tc_fence_after();
+          const bool last = ch == nch - 1;
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            float v[32];
+            if (it.nk > 0) {
+              tmem_ld_32x32b_x32(tmem + buf * 128 + lane_off + uint32_t(c * 32), v);
+            } else {
+#pragma unroll
+              for (int u = 0; u < 32; ++u) v[u] = 0.f;
+            }
+            if (ch > 0) {  // round-to-nearest fp32 adds of the chunk partial sums
+              float a[32];
+              tmem_ld_32x32b_x32(tmem + 256 + lane_off + uint32_t(c * 32), a);
+#pragma unroll
+              for (int u = 0; u < 32; ++u) v[u] += a[u];
+            }
+            if (!last) {
+              tmem_st_32x32b_x32(tmem + 256 + lane_off + uint32_t(c * 32), v);
+            } else if (c * 32 < it.n_valid) {
+              epilogue_chunk(it, ep, run, i, c, v);
+            }
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[buf]);  // TMEM buffer drained: the next chunk may use it
+        }
+        --t;  // the item loop header advances t past the item's last chunk
+        continue;
+      }
       const uint32_t buf = t & 1, use = t >> 1;
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
@@ -395,7 +448,10 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_free<256>(tmem);
+  if (warp == 1) {
+    if constexpr (kAcc > 0) tmem_free<512>(tmem);
+    else tmem_free<256>(tmem);
+  }
 }
 
 

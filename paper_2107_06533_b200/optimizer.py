@@ -445,6 +445,13 @@ class SPDKFAC(torch.optim.Optimizer):
         capturing = torch.cuda.is_current_stream_capturing()
         decay = self.factor_decay if self._factor_updates > 0 else 0.0
         gid = self._gid[kind][l.index]
+        if self._gseen[kind][gid] >= self._gsize[kind][gid]:
+            # a second train-mode forward/backward before step(): the reference takes its factors from
+            # one batch per step (emulator.py:234-241); a silent second capture would freeze the group's
+            # SYRK (its staging counter never returns to 0) and, at P > 1, re-reduce stale buffers
+            raise RuntimeError(f"SPDKFAC: layer {l.name!r} ({kind} factor) was captured twice before step(); "
+                               "call step() after every backward, or run extra passes under torch.no_grad() "
+                               "or with the module in eval mode")
         fg = self._fgroups[kind][gid] if self._fgroups is not None else None
         if fg is not None and fg["keys"][l.index] == key:
             ss = self.stage_stream
@@ -748,6 +755,8 @@ class SPDKFAC(torch.optim.Optimizer):
         self._grad_left = {side: len(self._pc_layers[side]) for side in self._precond}
         for k in ("A", "G"):
             self._gseen[k] = [0] * len(self._gseen[k])
+            for fg in (self._fgroups or {}).get(k, []):
+                fg["seen"] = 0  # a group whose members were only partly captured this step starts afresh
         if self._fgroups is None and not capturing and factors_now:
             self._build_factor_groups()
         if not capturing:  # a captured step is counted per replay (_after_replay)
@@ -775,10 +784,13 @@ class SPDKFAC(torch.optim.Optimizer):
             self._flat, self._flat_views, self._flat_layout = flat, views, layout
         return self._flat, self._flat_views
 
-    def _after_replay(self, stream) -> None:
+    def _after_replay(self, stream, inverted: bool = True) -> None:
         """Bookkeeping for one replay of a captured step (GraphedStep): the Python side
         effects of step() ran once at capture time."""
         self.steps += 1
+        self._capture = self.steps % self.factor_update_freq == 0
+        if not inverted:
+            return
         for side in self._sides:
             if self._inv_plans[side] is not None:
                 ev = torch.cuda.Event()

@@ -15,7 +15,7 @@ def test_categories_partition_span_and_comm_counts_only_exposed():
           _ev(8, 14, "ncclDevKernel_AllReduce_Sum_f32", 3),        # FactorComm: 10..14 exposed
           _ev(14, 16, "spd::pivot_kernel(x)", 4),                  # InverseComp
           _ev(17, 20, "ncclDevKernel_Broadcast", 3),               # InverseComm (idle 16..17)
-          _ev(20, 22, "void spd::tc3_gemm_kernel<1, 3, 0>(x)", 1)]  # Precondition (main stream)
+          _ev(20, 22, "void spd::tc3_gemm_kernel<(spd::Kind)2, 3, false, 4>(x)", 1)]  # Precondition
     lab = BD.label_events(ks, ["factor", "inverse"])
     cats = [c for *_, c in lab]
     assert cats == ["FFBP", "FactorComp", "FactorComm", "InverseComp", "InverseComm", "Precondition"]
@@ -26,8 +26,10 @@ def test_categories_partition_span_and_comm_counts_only_exposed():
 
 
 def test_factor_syrk_off_main_stream_is_factor_comp():
-    ks = [_ev(0, 5, "cutlass3x_sm100_tensorop_fprop", 7), _ev(1, 3, "void spd::tc3_gemm_kernel<1, 3, 0>(x)", 9),
-          _ev(6, 7, "void spd::tc3_pair_kernel<3>(x)", 9), _ev(7, 9, "void spd::tc3_gemm_kernel<2, 2, 1>(x)", 9)]
+    ks = [_ev(0, 5, "cutlass3x_sm100_tensorop_fprop", 7),
+          _ev(1, 3, "void spd::tc3_gemm_kernel<(spd::Kind)1, 3, false, 0>(x)", 9),
+          _ev(6, 7, "void spd::tc3_pair_kernel<3>(x)", 9),
+          _ev(7, 9, "void spd::tc3_gemm_kernel<(spd::Kind)2, 3, true, 0>(x)", 9)]
     tot = BD.breakdown(BD.label_events(ks, []))
     assert tot["FFBP"] == 5 and tot["FactorComp"] == 1 and tot["InverseComp"] == 2 and tot["Idle"] == 1
 
@@ -48,3 +50,15 @@ def test_csv_formats_match_reference():
     tl = BD.timeline_to_csv([(1.0, 2.0, "k", 5, "FactorComm")], t0=1.0).splitlines()
     assert tl[0] == "event,category,resource,start,end,layer"
     assert tl[1] == "k,FactorComm,comm,0.000000000,1.000000000,stream5"
+
+
+def test_classify_kernel_names():
+    """Kernel-name rules of the current library (precondition = TF32 engine with chunked accumulation)."""
+    from paper_2107_06533_b200.breakdown import classify
+    assert classify("void spd::tc3_gemm_kernel<(spd::Kind)1, 3, false, 0>(...)") == "FactorComp"
+    assert classify("void spd::tc3_pair_kernel<3>(...)") == "FactorComp"
+    assert classify("void spd::tc3_gemm_kernel<(spd::Kind)2, 3, false, 4>(...)") == "Precondition"
+    assert classify("void spd::tc3_gemm_kernel<(spd::Kind)2, 3, true, 0>(...)") == "InverseComp"
+    assert classify("void spd::tc3_gemm_kernel<(spd::Kind)2, 3, false, 0>(...)") == "InverseComp"
+    assert classify("void spd::pivot_tc_kernel<false>(...)") == "InverseComp"
+    assert classify("sm100_xmma_fprop_implicit_gemm") == "FFBP"

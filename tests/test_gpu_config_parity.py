@@ -1,0 +1,31 @@
+"""Config-level parity: BASELINE.json configs[0] (ResNet-20-style, bs32,
+32x32) and configs[1] (torchvision ResNet-50, bs32, 224x224) -- one step in the exact bench
+configuration (CUDA graph, update_in_backward, SYRK launch groups, early G inversion groups, d^3
+LBP) checked per layer against the oracle on the step's own captured tensors.  See
+tests/config_parity_impl.py for the stages and tolerances."""
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _run(name):
+    from tests.config_parity_impl import check, run_config
+    rep = run_config(name, 32)
+    bad = check(rep)
+    worst = {k: max(r[k] for r in rep) for k in ("factor_A", "factor_G", "update", "e2e")}
+    print(name, "worst:", worst, "max kappa:", max(max(r["kappa_A"], r["kappa_G"]) for r in rep))
+    assert not bad, bad
+    return rep
+
+
+def test_config0_resnet20_step_matches_oracle():
+    rep = _run("resnet20")
+    assert len(rep) == 20  # conv1 + 18 3x3 convs + fc
+
+
+def test_config1_resnet50_step_matches_oracle():
+    rep = _run("resnet50")
+    assert len(rep) == 54
+    assert max(r["a"] for r in rep) == 4608

@@ -159,3 +159,92 @@ def test_token_linear_step_matches_oracle(seed):
     from tests.smoke_impl import TOL, token_linear_step
     errs = token_linear_step(seed=seed)
     assert max(errs.values()) <= TOL, errs
+
+
+def test_second_capture_before_step_raises():
+    """A second train-mode forward/backward before step() must not silently freeze a fusion
+    group's SYRK: the optimizer raises, and the next proper step works."""
+    import torch.nn as nn
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    torch.manual_seed(5)
+    lin = nn.Sequential(nn.Linear(12, 9, bias=False), nn.ReLU(), nn.Linear(9, 4, bias=False)).cuda()
+    opt = SPDKFAC(lin, lr=0.01, damping=0.1)
+    for _ in range(2):  # first step: per-layer plans; second: fusion-group objects
+        opt.zero_grad()
+        lin(torch.randn(8, 12, device="cuda")).pow(2).mean().backward()
+        opt.step()
+    opt.zero_grad()
+    lin(torch.randn(8, 12, device="cuda")).pow(2).mean().backward()
+    with pytest.raises(RuntimeError, match="captured twice"):
+        lin(torch.randn(8, 12, device="cuda")).pow(2).mean().backward()
+    opt.step()
+    x = torch.randn(8, 12, device="cuda")
+    opt.zero_grad()
+    lin(x).pow(2).mean().backward()
+    opt.step()
+    torch.cuda.synchronize()
+    import oracle as O
+    want = O.factor_A(x.double().cpu().numpy())
+    got = opt.factor(0, "A").double().cpu().numpy()
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-4
+    opt.remove_hooks()
+
+
+@pytest.mark.parametrize("ff,fi,uib", [(1, 3, False), (2, 4, True)])
+def test_graphed_update_frequencies_match_eager(ff, fi, uib):
+    """GraphedStep with factor_update_freq / inv_update_freq > 1 (one graph per step type:
+    factors + inversion, factors only, reuse) gives the eager step's weights (simulator.py:126,377)."""
+    import torch.nn as nn
+    from paper_2107_06533_b200.graph import GraphedStep
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    from paper_2107_06533_b200.workloads import build_model
+    torch.backends.cudnn.deterministic = True
+    torch.backends.cudnn.benchmark = False
+    torch.manual_seed(13)
+    m1 = build_model("resnet20").cuda()
+    m2 = build_model("resnet20").cuda()
+    m2.load_state_dict(m1.state_dict())
+    crit = nn.CrossEntropyLoss()
+    n = 10
+    xs = [torch.randn(8, 3, 32, 32, device="cuda") for _ in range(n)]
+    ys = [torch.randint(0, 10, (8,), device="cuda") for _ in range(n)]
+    kw = dict(lr=0.05, damping=0.1, factor_decay=0.9, factor_update_freq=ff, inv_update_freq=fi)
+    o1 = SPDKFAC(m1, **kw)
+    o2 = SPDKFAC(m2, update_in_backward=uib, **kw)
+    for x, y in zip(xs, ys):
+        o1.zero_grad(set_to_none=True)
+        crit(m1(x), y).backward()
+        o1.step()
+    gs = GraphedStep(m2, crit, o2, [xs[0]], [ys[0]], warmup=1)
+    assert len(gs.graphs) == len({(s % ff == 0, s % fi == 0) for s in range(fi)})
+    for x, y in zip(xs[1:], ys[1:]):
+        gs([x], [y])
+    torch.cuda.synchronize()
+    o2.check_inverses()
+    assert o2.steps == n
+    for p1, p2 in zip(m1.parameters(), m2.parameters()):
+        assert torch.allclose(p1, p2, rtol=1e-5, atol=1e-6), (p1 - p2).abs().max()
+    assert torch.allclose(o1.bufA, o2.bufA, rtol=1e-5, atol=1e-7)
+    o1.remove_hooks()
+    o2.remove_hooks()
+
+
+def test_graphed_step_rejects_lr_change():
+    import torch.nn as nn
+    from paper_2107_06533_b200.graph import GraphedStep
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    from tests.smoke_impl import SmallNet
+    torch.manual_seed(2)
+    m = SmallNet().cuda()
+    o = SPDKFAC(m, lr=0.05, damping=0.1)
+    crit = nn.CrossEntropyLoss()
+    x, y = torch.randn(16, 3, 8, 8, device="cuda"), torch.randint(0, 10, (16,), device="cuda")
+    gs = GraphedStep(m, crit, o, [x], [y], warmup=1)
+    gs([x], [y])
+    o.param_groups[0]["lr"] = 0.01
+    with pytest.raises(RuntimeError, match="learning rate changed"):
+        gs([x], [y])
+    gs.recapture = True
+    gs([x], [y])  # captures again at the new lr
+    assert gs.lr == 0.01
+    o.remove_hooks()
