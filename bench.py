@@ -338,6 +338,8 @@ def kernel_roofline(cat, rec, per, peaks, world, model):
            "frac": round(ach / peak, 4) if peak and ms > 0 else None, "peak_source": peak_key + (
                " (MEASURED_PEAKS.json)" if peak_key in ("hbm_gbs", "bf16_tflops_sustained") else " (measured by this run)"),
            "kernel_ms_per_step": round(ms, 4), "launches_per_step": launches,
+           "timing": "in-kernel launch probes (first CTA start to last CTA end, %globaltimer) over the timed region's "
+                     "last step (graph mode) or all timed steps (eager)",
            ("algorithmic_flops_per_step" if bound == "tensor" else "algorithmic_bytes_per_step"): work,
            "traffic": None}
     try:  # DRAM bytes per launch from a committed `ncu --set full` capture of the same launches
@@ -513,8 +515,8 @@ def run_ours(a):
     if graphed:
         from paper_2107_06533_b200.graph import GraphedStep
         gs = GraphedStep(model, crit, opt, [xs[0]], [ys[0]], warmup=a.warmup,
-                         before_capture=lambda: _lib.stats_reset(
-                             timing=() if a.stats_off else ROOF_CATS, reserve=1200),
+                         before_capture=lambda: (_lib.stats_probes(() if a.stats_off else ROOF_CATS, slots=4096),
+                                                 _lib.stats_reset(timing=())),
                          priority=a.main_priority)
         eager_step = step
 
@@ -544,7 +546,8 @@ def run_ours(a):
     # live roofline timing of the dominant kernel only (events pre-created, outside the region);
     # in graph mode the event nodes were captured into the graph (stats reset before capture)
     if not graphed:
-        _lib.stats_reset(timing=() if a.stats_off else ROOF_CATS, reserve=700 * a.steps)
+        _lib.stats_probes(() if a.stats_off else ROOF_CATS, slots=1000 * a.steps)
+        _lib.stats_reset(timing=())
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -588,6 +591,7 @@ def run_ours(a):
         trace_summary(step, a.trace if rank == 0 else None, torch, comm_tags=tags)
     # per-category breakdown: a separate 2-step eager pass with every launch bracketed by events
     nb = 2
+    _lib.stats_probes(())  # the breakdown pass times every launch with CUDA events
     _lib.stats_reset(timing=True, reserve=600 * nb)
     for i in range(nb):
         (eager_step if graphed else step)(i)

@@ -65,6 +65,12 @@ SPDKFAC_API void spdkfac_stats_reset(int timing_mask);
 SPDKFAC_API int spdkfac_stats_reserve(int n_launches);
 SPDKFAC_API uint64_t spdkfac_stats_launches(void);
 SPDKFAC_API int spdkfac_stats_read(int category, double* ms, int64_t* launches, double* flops, double* bytes);
+/* In-kernel launch probes for the categories in probe_mask (bit = category): the first CTA of a
+ * launch stamps its start, the last CTA its end (%globaltimer), with no stream or graph node, so a
+ * graphed step can be timed per kernel category without perturbing it.  n_slots probe slots are
+ * allocated once (outside any capture); each probed launch after spdkfac_stats_reset takes one.
+ * spdkfac_stats_read reports the probe time of the last run of each launch for those categories. */
+SPDKFAC_API int spdkfac_stats_set_probes(int probe_mask, int n_slots);
 
 /* ------------------------------------------------------------------ factors
  * Replaces compute_factor_A / compute_factor_G / _factor_from_batch

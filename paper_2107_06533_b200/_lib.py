@@ -37,6 +37,7 @@ SIGNATURES = {
     "spdkfac_stats_reserve": (C.c_int, [C.c_int]),
     "spdkfac_stats_read": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(_i64), C.POINTER(C.c_double),
                                      C.POINTER(C.c_double)]),
+    "spdkfac_stats_set_probes": (C.c_int, [C.c_int, C.c_int]),
     "spdkfac_factor_dims": (C.c_int, [C.POINTER(FactorGeom), C.POINTER(_i64), C.POINTER(_i64)]),
     "spdkfac_factor_workspace_size": (_sz, [C.POINTER(FactorGeom)]),
     "spdkfac_factor_plan_create": (C.c_int, [C.POINTER(_vp), C.POINTER(FactorGeom), _vp, _sz, _vp]),
@@ -117,6 +118,14 @@ def stats_reset(timing=False, reserve: int = 0) -> None:
     if reserve:
         check(lib.spdkfac_stats_reserve(int(reserve)), "stats reserve")
     lib.spdkfac_stats_reset(mask)
+
+
+def stats_probes(categories=(), slots: int = 4096) -> None:
+    """Time the given categories with in-kernel launch probes (no events; see include/spdkfac.h)."""
+    mask = 0
+    for name in categories:
+        mask |= 1 << STAT_CATEGORIES.index(name)
+    check(load().spdkfac_stats_set_probes(mask, int(slots)), "stats probes")
 
 
 def stats() -> dict:

@@ -14,6 +14,10 @@ constexpr int kTile = 128;  // UMMA M = N = 128 tile edge (rows of TMEM lanes / 
 
 // ---------------------------------------------------------------- misc
 SPD_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+// 1024-B aligned base of the dynamic shared memory.  Offsetting the __shared__ array (instead of
+// rounding its generic address through an integer) keeps the pointer in the shared state space,
+// so plain loads / stores through it compile to LDS / STS rather than generic LD / ST.
+SPD_DEV uint8_t* smem_align1024(uint8_t* raw) { return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u); }
 SPD_DEV int lane_id() { return threadIdx.x & 31; }
 SPD_DEV int warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 
@@ -50,6 +54,36 @@ SPD_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint64_t t0 = global_ns();
   while (!mbar_try_wait(bar, parity)) {
     if (global_ns() - t0 > 4000000000ull) asm volatile("trap;");
+  }
+}
+
+// ---------------------------------------------------------------- launch probes
+// In-kernel launch timing (include/spdkfac.h spdkfac_stats_set_probes): the first CTA to start
+// stamps t0, the last CTA to finish stamps t1 and re-arms the counters, so a probe costs two
+// atomics per CTA and no graph / stream nodes (CUDA events around every launch of a graphed step
+// added ~3 ms to a 18 ms ResNet-50 iteration).
+struct Probe {
+  unsigned int started, finished;
+  unsigned long long t0, t1;
+};
+SPD_DEV void probe_start(Probe* p) {
+  if (p != nullptr && threadIdx.x == 0 && threadIdx.y == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (atomicAdd(&p->started, 1u) == 0u) p->t0 = t;
+  }
+}
+SPD_DEV void probe_stop(Probe* p) {  // after the CTA's last __syncthreads
+  if (p != nullptr && threadIdx.x == 0 && threadIdx.y == 0) {
+    __threadfence();
+    const unsigned int nb = gridDim.x * gridDim.y * gridDim.z;
+    if (atomicAdd(&p->finished, 1u) == nb - 1u) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      p->t1 = t;
+      p->started = 0u;
+      p->finished = 0u;
+    }
   }
 }
 

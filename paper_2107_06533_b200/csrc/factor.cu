@@ -57,7 +57,8 @@ constexpr int kStageRows = 32;
 template <bool kVec>
 __global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict__ x, int64_t M, int64_t d,
                                                          int64_t ldx, __nv_bfloat16* __restrict__ xs, int64_t ld,
-                                                         int tpr, int cps) {
+                                                         int tpr, int cps, Probe* probe) {
+  probe_start(probe);
   const int64_t plane = M * ld;
   constexpr int kW = kVec ? 4 : 2;
   const int64_t m0 = int64_t(blockIdx.x) * kStageRows;
@@ -95,6 +96,8 @@ __global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict
       }
     }
   }
+  __syncthreads();
+  probe_stop(probe);
 }
 
 // launch shape for M rows of ncol column slots, `rows` rows per block: enough blocks for the
@@ -132,8 +135,9 @@ constexpr int kIm2colRows = 32;
 template <bool kNhwc, bool kVec>
 __global__ void __launch_bounds__(256) stage_im2col_kernel(const float* __restrict__ x, ConvGeom g, int64_t M,
                                                            int64_t d, __nv_bfloat16* __restrict__ xs, int64_t ld,
-                                                           int tpr, int cps) {
+                                                           int tpr, int cps, Probe* probe) {
   __shared__ int s_b[kIm2colRows], s_h[kIm2colRows], s_w[kIm2colRows];
+  probe_start(probe);
   const int64_t m0 = int64_t(blockIdx.x) * kIm2colRows;
   if (threadIdx.x < kIm2colRows) {
     const int64_t m = m0 + threadIdx.x;
@@ -211,12 +215,16 @@ __global__ void __launch_bounds__(256) stage_im2col_kernel(const float* __restri
       }
     }
   }
+  __syncthreads();
+  probe_stop(probe);
 }
 
 // NCHW output gradients g[b][c][p] -> rows m = b*HW + p, columns c: per-image 32 x 32 transpose
 __global__ void __launch_bounds__(256) stage_spatial_kernel(const float* __restrict__ g, int C, int HW,
-                                                            __nv_bfloat16* __restrict__ xs, int64_t M, int64_t ld) {
+                                                            __nv_bfloat16* __restrict__ xs, int64_t M, int64_t ld,
+                                                            Probe* probe) {
   __shared__ float tile[32][33];
+  probe_start(probe);
   const int b = blockIdx.z, p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
 #pragma unroll
@@ -233,6 +241,8 @@ __global__ void __launch_bounds__(256) stage_spatial_kernel(const float* __restr
     const int p = p0 + k, c = c0 + 2 * pr;
     if (p < HW && c < ld) store_split2(xs, plane, (int64_t(b) * HW + p) * ld + c, tile[2 * pr][k], tile[2 * pr + 1][k]);
   }
+  __syncthreads();
+  probe_stop(probe);
 }
 
 // ------------------------------------------------------------------ reduce + pack
@@ -572,7 +582,7 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
 
 int member_stage(const Member& mb, const float* x, cudaStream_t s) {
   const spdkfac_factor_geom& g = mb.g;
-  stat_begin(kCatFactorStage, s);
+  Probe* pr = stat_begin(kCatFactorStage, s);
   const bool pointwise = g.layout == SPDKFAC_CONV_A_NHWC && g.kh == 1 && g.kw == 1 && g.stride_h == 1 &&
                          g.stride_w == 1 && g.pad_h == 0 && g.pad_w == 0;
   if (g.layout == SPDKFAC_ROWS || g.layout == SPDKFAC_SPATIAL_NHWC || pointwise) {
@@ -582,9 +592,9 @@ int member_stage(const Member& mb, const float* x, cudaStream_t s) {
     const bool vec = ldx % 4 == 0 && mb.d % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
     const RowShape rs = row_shape(mb.M, mb.ld / (vec ? 4 : 2), kStageRows);
     if (vec)
-      stage_rows_kernel<true><<<rs.grid, rs.threads, 0, s>>>(x, mb.M, mb.d, ldx, mb.xt, mb.ld, rs.tpr, rs.cps);
+      stage_rows_kernel<true><<<rs.grid, rs.threads, 0, s>>>(x, mb.M, mb.d, ldx, mb.xt, mb.ld, rs.tpr, rs.cps, pr);
     else
-      stage_rows_kernel<false><<<rs.grid, rs.threads, 0, s>>>(x, mb.M, mb.d, ldx, mb.xt, mb.ld, rs.tpr, rs.cps);
+      stage_rows_kernel<false><<<rs.grid, rs.threads, 0, s>>>(x, mb.M, mb.d, ldx, mb.xt, mb.ld, rs.tpr, rs.cps, pr);
   } else if (g.layout == SPDKFAC_CONV_A_NHWC || g.layout == SPDKFAC_CONV_A) {
     ConvGeom cg{int(g.n), int(g.c), int(g.h), int(g.w), mb.Ho, mb.Wo, g.kh, g.kw, g.stride_h, g.stride_w,
                 g.pad_h, g.pad_w, g.dil_h, g.dil_w};
@@ -593,18 +603,18 @@ int member_stage(const Member& mb, const float* x, cudaStream_t s) {
     const RowShape rs = row_shape(mb.M, ncol, kIm2colRows);
     if (g.layout == SPDKFAC_CONV_A_NHWC) {
       if (vec)
-        stage_im2col_kernel<true, true><<<rs.grid, rs.threads, 0, s>>>(x, cg, mb.M, mb.d, mb.xt, mb.ld, rs.tpr, rs.cps);
+        stage_im2col_kernel<true, true><<<rs.grid, rs.threads, 0, s>>>(x, cg, mb.M, mb.d, mb.xt, mb.ld, rs.tpr, rs.cps, pr);
       else
         stage_im2col_kernel<true, false><<<rs.grid, rs.threads, 0, s>>>(x, cg, mb.M, mb.d, mb.xt, mb.ld, rs.tpr,
-                                                                        rs.cps);
+                                                                        rs.cps, pr);
     } else {
       stage_im2col_kernel<false, false><<<rs.grid, rs.threads, 0, s>>>(x, cg, mb.M, mb.d, mb.xt, mb.ld, rs.tpr,
-                                                                        rs.cps);
+                                                                        rs.cps, pr);
     }
   } else {
     const int hw = int(g.h * g.w);
     dim3 grid(unsigned(cdiv(hw, 32)), unsigned(cdiv(mb.ld, 32)), unsigned(g.n));
-    stage_spatial_kernel<<<grid, 256, 0, s>>>(x, int(g.c), hw, mb.xt, mb.M, mb.ld);
+    stage_spatial_kernel<<<grid, 256, 0, s>>>(x, int(g.c), hw, mb.xt, mb.M, mb.ld, pr);
   }
   SPD_CHECK_LAUNCH();
   stat_end(kCatFactorStage, s, 0, double(mb.M) * mb.d * 4 + 4.0 * mb.ld * mb.M);
@@ -619,12 +629,12 @@ int group_compute(spdkfac_factor_group* G, float scale, float decay, float world
   for (const Member& mb : G->m) (mb.S ? bytes_pair : bytes_single) += 4.0 * mb.ld * mb.M;
   int rc;
   if (G->n_items) {
-    stat_begin(kCatFactorSyrk, s);
+    run.probe = stat_begin(kCatFactorSyrk, s);
     if ((rc = launch_tc3(Kind::BF16, G->maps, G->items, G->epis, G->n_items, s, run))) return rc;
     stat_end(kCatFactorSyrk, s, G->flops_single, bytes_single);
   }
   if (G->n_pitems) {
-    stat_begin(kCatFactorSyrk, s);
+    run.probe = stat_begin(kCatFactorSyrk, s);
     if ((rc = launch_tc3_pair(G->maps, G->pitems, G->epis, G->n_pitems, s, run))) return rc;
     stat_end(kCatFactorSyrk, s, G->flops_pair, bytes_pair);
   }

@@ -184,37 +184,84 @@ __device__ __forceinline__ float packed_at(const float* p, int64_t d, int64_t i,
 // One CTA (256 threads = 8 warps) sweeps one 128 x 128 pivot block P.  Thread (row i, half h)
 // keeps D[i][64 h, 64 h + 64) in registers (warp w: TMEM lanes / rows [32 (w % 4), +32),
 // h = w / 4).  Four 32-pivot steps s (K = columns [32 s, 32 s + 32), held by half s / 2):
-//   1. the K columns of every row go to shared memory (fp32, and as the tf32 hi/lo A operand);
-//      warp s + 4 (s / 2) (rows K) sweeps the 32 x 32 pivot block in registers with warp
-//      shuffles -> S_K = -P_K^-1.  The pivots are the Schur complements in order, so the first
+//   1. D[:,K] -> shared memory as the A operand; warp s + 4 (s / 2) (rows K) sweeps the 32 x 32
+//      pivot block in registers in fp32 (8-pivot groups: an 8 x 8 shuffle sweep, then a rank-8
+//      update) -> S_K = -P_K^-1.  The pivots are the Schur complements in order, so the first
 //      non-positive one is LAPACK dpotrf's failing index;
-//   2. every thread forms C[i][16 h, 16 h + 16) = D[i,K] P_K^-1 (FFMA, P_K^-1 broadcast);
-//   3. one thread issues U = A B^T, A = D[:,K], B = -C (3 x tf32: 12 tcgen05 MMAs, M = N = 128,
-//      K = 8) into a fresh TMEM accumulator; every thread adds its row of U to its registers
-//      (round-to-nearest fp32: TMEM accumulation truncates, so D itself never lives there);
+//   2. panel C = D[:,K] P_K^-1 on the tensor cores (M = 128, N = 32);
+//   3. U = A B^T, A = D[:,K], B = -C (M = N = 128) on the tensor cores; every thread adds its
+//      row of U to its registers;
 //   4. fix-up in registers: D[i,K] = C[i] (i not in K), D[K,j] = C[j]^T, D[K,K] = S_K.
-// After the four steps D = -P^-1.  This replaces 16 barrier-separated rank-8 FFMA sweeps of the
-// whole block (the round-1 pivot kernel: 59 us per block under ncu, IPC 0.27) by four short warp
-// sweeps and four rank-32 tensor-core updates.  The sweep loop is kept rolled (8 pivots per
-// unrolled body, the row rotated in registers between bodies) so the kernel's code stays in the
-// instruction cache.
+// After the four steps D = -P^-1.
+// Precision: the Schur updates inside a pivot block cancel heavily (the result is much smaller
+// than |A||C|), so the products must be fp32-exact relative to |A||C|.  The operands are split
+// three ways into tf32 (x = hi + mid + lo, |x - hi - mid - lo| <= 2^-33 |x|) and the six
+// products above 2^-33 are issued into TWO accumulators: hi*hi alone (4 accumulating MMAs: the
+// tcgen05 accumulation truncates, ~2^-24 per MMA, so it stays at the fp32 FFMA level) and the five
+// cross terms (magnitude <= 2^-11 of it) in the other; the two are summed in registers with
+// round-to-nearest adds.  (A 2-way split into one accumulator measured 10-35x larger inverse
+// errors on rank-deficient factors than fp32 FFMA and failed pivots inside the bench step.)
+#ifdef SPD_PIVOT_TIMING  // per-phase clock64 marks of thread 0, printed by block 0 (diagnostic build)
+#define PVT_MARK(slot) \
+  do {                 \
+    if (threadIdx.x == 0) clk[slot] = clock64(); \
+  } while (0)
+#else
+#define PVT_MARK(slot) \
+  do {                 \
+  } while (0)
+#endif
 namespace pvt {
 constexpr int kThreads = 256;
-constexpr int kPvLd = 36;                 // P_K^-1 rows: float4-aligned, conflict-free float4 stores
-constexpr int kLd = 33;                   // fp32 row-major staging (D[:,K], C): conflict-free columns
+constexpr int kLd = 33;                   // C fp32 [128][kLd]: conflict-free columns
+constexpr int kFLd = 132;                 // 128 x 128 fp32 staging rows (float4-aligned)
+constexpr int kGLd = 36;                  // 8 published rows of the 32 x 32 sweep
 constexpr uint32_t kOpBytes = 128 * 128;  // one 128 x 32 fp32 operand plane (128-B rows, SWIZZLE_128B)
-constexpr size_t kSmem = 1024 + 4 * size_t(kOpBytes) + size_t(2 * 128 * kLd + 32 * kPvLd) * 4 + 64;
-static_assert(4 * kOpBytes + 2 * 128 * kLd * 4 >= 128 * 129 * 4, "small-path output staging fits");
-// byte offset of 16-B chunk `chunk` of row i in a K-major 128 x 32 fp32 plane with the 128-B swizzle
+constexpr uint32_t kPBytes = 32 * 128;    // one 32 x 32 fp32 operand plane
+// smem: [opA hi, mid, lo | opB hi, mid, lo | opP hi, mid, lo | C fp32 | sweep rows | barrier];
+// the 128 x 132 fp32 staging of the global load / store overlays the front
+constexpr uint32_t kOffB = 3 * kOpBytes, kOffP = 6 * kOpBytes, kOffC = kOffP + 3 * kPBytes;
+constexpr uint32_t kOffG = kOffC + 128 * kLd * 4, kOffBar = kOffG + 8 * kGLd * 4;
+constexpr size_t kSmem = 1024 + size_t(kOffBar) + 64;
+static_assert(128 * kFLd * 4 <= kOffBar, "staging overlay fits");
+// TMEM columns: U hi*hi [0, 128), U cross terms [128, 256), C hi*hi [256, 288), C cross [288, 320)
+constexpr uint32_t kTU1 = 0, kTU2 = 128, kTC1 = 256, kTC2 = 288;
+// byte offset of 16-B chunk `chunk` of row i in a K-major x 32 fp32 plane with the 128-B swizzle
 __device__ __forceinline__ uint32_t sw128(int i, int chunk) { return uint32_t(i) * 128u + (uint32_t(chunk ^ (i & 7)) << 4); }
-__device__ __forceinline__ void put_split(uint8_t* plane_hi, uint32_t off, float4 x) {
-  float4 h, l;
-  split_tf32(x.x, h.x, l.x);
-  split_tf32(x.y, h.y, l.y);
-  split_tf32(x.z, h.z, l.z);
-  split_tf32(x.w, h.w, l.w);
-  *reinterpret_cast<float4*>(plane_hi + off) = h;
-  *reinterpret_cast<float4*>(plane_hi + kOpBytes + off) = l;
+__device__ __forceinline__ void split3(float x, float& h, float& m, float& l) {
+  h = tf32_rna(x);
+  const float r = x - h;
+  m = tf32_rna(r);
+  l = tf32_rna(r - m);
+}
+// three tf32 planes (hi, mid, lo) of one 16-B chunk
+__device__ __forceinline__ void put_split3(uint8_t* plane0, uint32_t plane_bytes, uint32_t off, float4 x) {
+  float4 h, m, l;
+  split3(x.x, h.x, m.x, l.x);
+  split3(x.y, h.y, m.y, l.y);
+  split3(x.z, h.z, m.z, l.z);
+  split3(x.w, h.w, m.w, l.w);
+  *reinterpret_cast<float4*>(plane0 + off) = h;
+  *reinterpret_cast<float4*>(plane0 + plane_bytes + off) = m;
+  *reinterpret_cast<float4*>(plane0 + 2 * plane_bytes + off) = l;
+}
+// the six split products of one 128 x N tile over K = 32: hi*hi into acc1, the cross terms into acc2
+template <int N>
+__device__ __forceinline__ void mma_split3(uint32_t acc1, uint32_t acc2, const uint8_t* a, uint32_t a_plane,
+                                           const uint8_t* b, uint32_t b_plane) {
+  constexpr uint32_t idesc = make_idesc<Kind::TF32>(128, N);
+  const uint64_t ah = make_sdesc_sw128(a), am = make_sdesc_sw128(a + a_plane), al = make_sdesc_sw128(a + 2 * a_plane);
+  const uint64_t bh = make_sdesc_sw128(b), bm = make_sdesc_sw128(b + b_plane), bl = make_sdesc_sw128(b + 2 * b_plane);
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 B of K per 128-B swizzle row
+    const uint64_t off = uint64_t(kk * 2);
+    umma<Kind::TF32>(acc1, ah + off, bh + off, idesc, kk != 0);
+    umma<Kind::TF32>(acc2, ah + off, bm + off, idesc, kk != 0);
+    umma<Kind::TF32>(acc2, am + off, bh + off, idesc, 1u);
+    umma<Kind::TF32>(acc2, ah + off, bl + off, idesc, 1u);
+    umma<Kind::TF32>(acc2, am + off, bm + off, idesc, 1u);
+    umma<Kind::TF32>(acc2, al + off, bh + off, idesc, 1u);
+  }
 }
 __device__ __forceinline__ float rcp_nr(float x) {  // reciprocal: MUFU approximation + one Newton step
   float r;
@@ -222,34 +269,80 @@ __device__ __forceinline__ float rcp_nr(float x) {  // reciprocal: MUFU approxim
   return r * fmaf(-x, r, 2.f);
 }
 // Sweep the 32 x 32 block held by one warp (lane r = row r, w[t] = D[r][t]) -> -D^-1; returns the
-// first non-positive pivot (warp-uniform) or -1.  Pivot p = 8 pb + u: the row is kept rotated by
-// 8 pb so that column p sits in register u of the unrolled body.
-__device__ __forceinline__ int sweep32(float (&w)[32], int lane) {
+// first non-positive pivot (warp-uniform) or -1.  Groups g of 8 pivots: the row is kept rotated
+// by 8 g so that the group's columns sit in w[0..8).  buf: [8][kGLd] shared scratch of this warp.
+__device__ __forceinline__ int sweep32(float (&w)[32], int lane, float* buf) {
   int fail = -1;
 #pragma unroll 1
-  for (int pb = 0; pb < 4; ++pb) {
+  for (int g = 0; g < 4; ++g) {
+    // (1) 8 x 8 diagonal block B = W[G,G] (rows in lanes 8g..8g+7) -> S = -B^-1 (shuffles)
+    float b[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int p = 8 * pb + u;
-      const float piv = __shfl_sync(0xffffffffu, w[u], p);
-      if (!(piv > 0.f)) {  // warp-uniform (broadcast value); NaN fails too
-        fail = p;
-        break;
-      }
+    for (int c = 0; c < 8; ++c) b[c] = w[c];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {  // branch-free: the row shuffles issue together with the pivot's
+      const int p = 8 * g + u;
+      float rp[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) rp[c] = __shfl_sync(0xffffffffu, b[c], p);
+      const float piv = rp[u];
+      if (fail < 0 && !(piv > 0.f)) fail = p;  // warp-uniform (broadcast value); NaN fails too
       const float rinv = rcp_nr(piv);
       const bool me = lane == p;
-      const float fct = w[u] * rinv;
+      const float fct = b[u] * rinv;
       const float mult = me ? rinv : -fct;
 #pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        if (t == u) continue;
-        const float rp = __shfl_sync(0xffffffffu, w[t], p);
-        w[t] = fmaf(mult, rp, me ? 0.f : w[t]);
-      }
-      w[u] = me ? -rinv : fct;
+      for (int c = 0; c < 8; ++c)
+        if (c != u) b[c] = fmaf(mult, rp[c], me ? 0.f : b[c]);
+      b[u] = me ? -rinv : fct;
     }
     if (fail >= 0) break;
-    float tmp[8];  // rotate left by 8: the next body's pivot columns move to registers 0..7
+    // (2) rows G publish [S_r | W[G_r, 8..32)]
+    const bool inG = (lane >> 3) == g;
+    if (inG) {
+      float* row = buf + (lane & 7) * kGLd;
+      *reinterpret_cast<float4*>(row) = make_float4(b[0], b[1], b[2], b[3]);
+      *reinterpret_cast<float4*>(row + 4) = make_float4(b[4], b[5], b[6], b[7]);
+#pragma unroll
+      for (int t = 0; t < 6; ++t)
+        *reinterpret_cast<float4*>(row + 8 + 4 * t) = make_float4(w[8 + 4 * t], w[9 + 4 * t], w[10 + 4 * t], w[11 + 4 * t]);
+    }
+    __syncwarp();
+    // (3) rank-8 update.  Row i not in G: y = W[i,G] B^-1 = -W[i,G] S, W[i,j] -= y W[G,j], W[i,G] = y.
+    //     Row r in G: W[G_r,j] = B^-1 W[G,j] = -S_r W[G,j], W[G_r,G] = S_r.  One code path:
+    //     coef = inG ? S_r : y, base = inG ? 0 : W[i,j], W[i,j] = base - coef W[G,j].
+    float y[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) y[c] = 0.f;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const float4 s0 = *reinterpret_cast<const float4*>(buf + m * kGLd);
+      const float4 s1 = *reinterpret_cast<const float4*>(buf + m * kGLd + 4);
+      const float wm = w[m];
+      y[0] = fmaf(-wm, s0.x, y[0]), y[1] = fmaf(-wm, s0.y, y[1]), y[2] = fmaf(-wm, s0.z, y[2]);
+      y[3] = fmaf(-wm, s0.w, y[3]), y[4] = fmaf(-wm, s1.x, y[4]), y[5] = fmaf(-wm, s1.y, y[5]);
+      y[6] = fmaf(-wm, s1.z, y[6]), y[7] = fmaf(-wm, s1.w, y[7]);
+    }
+    float coef[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) coef[c] = inG ? b[c] : y[c];
+#pragma unroll
+    for (int t = 8; t < 32; ++t) w[t] = inG ? 0.f : w[t];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        const float4 g4 = *reinterpret_cast<const float4*>(buf + m * kGLd + 8 + 4 * t);
+        w[8 + 4 * t] = fmaf(-coef[m], g4.x, w[8 + 4 * t]);
+        w[9 + 4 * t] = fmaf(-coef[m], g4.y, w[9 + 4 * t]);
+        w[10 + 4 * t] = fmaf(-coef[m], g4.z, w[10 + 4 * t]);
+        w[11 + 4 * t] = fmaf(-coef[m], g4.w, w[11 + 4 * t]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) w[c] = coef[c];
+    __syncwarp();  // buf is rewritten by the next group
+    float tmp[8];  // rotate left by 8: the next group's columns move to w[0..8)
 #pragma unroll
     for (int t = 0; t < 8; ++t) tmp[t] = w[t];
 #pragma unroll
@@ -267,22 +360,31 @@ __device__ __forceinline__ int sweep32(float (&w)[32], int lane) {
 template <bool kSmall>
 __global__ void __launch_bounds__(pvt::kThreads, 1)
     pivot_tc_kernel(const InvMat* __restrict__ mats, const int32_t* __restrict__ ids, int k,
-                    float* __restrict__ pinv_planes, int64_t pinv_plane, float gamma) {
+                    float* __restrict__ pinv_planes, int64_t pinv_plane, float gamma, Probe* probe) {
   using namespace pvt;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* opA = sm;                  // A hi, lo planes
-  uint8_t* opB = sm + 2 * kOpBytes;   // B hi, lo planes
-  float* Ar = reinterpret_cast<float*>(sm + 4 * kOpBytes);  // D[:,K] fp32 [128][kLd]
-  float* Cs = Ar + 128 * kLd;                                // C fp32 [128][kLd]
-  float* Pv = Cs + 128 * kLd;                                // P_K^-1 [32][kPvLd]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Pv + 32 * kPvLd);
+  uint8_t* sm = smem_align1024(smem_raw);
+  uint8_t* opA = sm;          // A = D[:,K]: hi, mid, lo planes
+  uint8_t* opB = sm + kOffB;  // B = -C
+  uint8_t* opP = sm + kOffP;  // P_K^-1 (32 rows)
+  float* Cs = reinterpret_cast<float*>(sm + kOffC);
+  float* gbuf = reinterpret_cast<float*>(sm + kOffG);
+  float* F = reinterpret_cast<float*>(sm);  // 128 x kFLd staging overlay (load / store)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kOffBar);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
   int* sfail = reinterpret_cast<int*>(tslot + 1);
+#ifdef SPD_PIVOT_TIMING
+  long long clk[32];
+#endif
+  PVT_MARK(0);
+  probe_start(probe);
 
   const InvMat m = mats[ids[blockIdx.x]];
   if constexpr (!kSmall) {
-    if (*m.info != 0) return;  // an earlier pivot block failed (uniform)
+    if (*m.info != 0) {  // an earlier pivot block failed (uniform)
+      probe_stop(probe);
+      return;
+    }
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, h = warp >> 2, i = 32 * q + lane;
@@ -290,7 +392,7 @@ __global__ void __launch_bounds__(pvt::kThreads, 1)
     mbar_init(bar, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc<128>(tslot);
+  if (warp == 0) tmem_alloc<512>(tslot);
   const int n = kSmall ? m.d : kB;
   const int64_t dp = m.dp, K0 = int64_t(k) * kB;
 
@@ -301,162 +403,192 @@ __global__ void __launch_bounds__(pvt::kThreads, 1)
       const int j = 64 * h + t;
       d[t] = (i < n && j < n) ? packed_at(m.in, n, i, j) + (i == j ? gamma : 0.f) : (i == j ? 1.f : 0.f);
     }
-  } else {
-    const float4* src = reinterpret_cast<const float4*>(m.W + (K0 + i) * dp + K0 + 64 * h);
+  } else {  // coalesced: warp w loads rows 16 w .. 16 w + 15, one 512-B row per instruction
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int row = 16 * warp + r;
+      const float4 x = __ldcg(reinterpret_cast<const float4*>(m.W + (K0 + row) * dp + K0) + lane);
+      *reinterpret_cast<float4*>(F + row * kFLd + 4 * lane) = x;
+    }
+    __syncthreads();
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
-      const float4 x = __ldcg(src + t);
+      const float4 x = *reinterpret_cast<const float4*>(F + i * kFLd + 64 * h + 4 * t);
       d[4 * t] = x.x, d[4 * t + 1] = x.y, d[4 * t + 2] = x.z, d[4 * t + 3] = x.w;
     }
   }
   tc_fence_before();
-  __syncthreads();
+  __syncthreads();  // (the staging overlay is free again; TMEM allocated)
   tc_fence_after();
+  PVT_MARK(1);
   const uint32_t tbase = *tslot;
-  const uint32_t tU = tbase + (uint32_t(32 * q) << 16) + uint32_t(64 * h);  // this thread's U row half
+  const uint32_t tq = tbase + (uint32_t(32 * q) << 16);  // this warp's lane quarter
 
-  constexpr uint32_t idesc = make_idesc<Kind::TF32>(128, 128);
   const int nsteps = (n + 31) >> 5;
   int fail = -1;
+  uint32_t phase = 0;
 #pragma unroll 1
   for (int s = 0; s < nsteps; ++s) {
-    const int c0 = 32 * s, hs = s >> 1;
+    const int hs = s >> 1;
     const bool odd = s & 1;
-    // ---- 1. D[:,K] -> shared memory (fp32 + the A operand planes); the pivot warp sweeps
+    // ---- 1. A = D[:,K] -> shared memory; the pivot warp sweeps P_K -> S_K, publishes P_K^-1
+    float a[32];
     if (h == hs) {
-      float a[32];
 #pragma unroll
       for (int t = 0; t < 32; ++t) a[t] = odd ? d[32 + t] : d[t];
 #pragma unroll
-      for (int t = 0; t < 32; ++t) Ar[i * kLd + t] = a[t];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) put_split(opA, sw128(i, t), make_float4(a[4 * t], a[4 * t + 1], a[4 * t + 2], a[4 * t + 3]));
+      for (int t = 0; t < 8; ++t)
+        put_split3(opA, kOpBytes, sw128(i, t), make_float4(a[4 * t], a[4 * t + 1], a[4 * t + 2], a[4 * t + 3]));
       if (q == s) {
-        const int f = sweep32(a, lane);
+        const int f = sweep32(a, lane, gbuf);
 #pragma unroll
-        for (int t = 0; t < 8; ++t)  // P_K^-1 = -S_K
-          *reinterpret_cast<float4*>(Pv + lane * kPvLd + 4 * t) =
-              make_float4(-a[4 * t], -a[4 * t + 1], -a[4 * t + 2], -a[4 * t + 3]);
+        for (int t = 0; t < 8; ++t)  // P_K^-1 = -S_K, row `lane`
+          put_split3(opP, kPBytes, sw128(lane, t), make_float4(-a[4 * t], -a[4 * t + 1], -a[4 * t + 2], -a[4 * t + 3]));
         if (lane == 0) *sfail = f;
       }
     }
-    __syncthreads();
-    const int f = *sfail;
-    if (f >= 0) {  // uniform
-      fail = c0 + f;
-      break;
-    }
-    // ---- 2. C[i][16 h + jj] = sum_kk D[i, K0 + kk] P_K^-1[kk][16 h + jj]
-    float c[16];
-#pragma unroll
-    for (int jj = 0; jj < 16; ++jj) c[jj] = 0.f;
-#pragma unroll 4
-    for (int kk = 0; kk < 32; ++kk) {
-      const float x = Ar[i * kLd + kk];
-      const float4* pr = reinterpret_cast<const float4*>(Pv + kk * kPvLd + 16 * h);
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const float4 p4 = pr[t];
-        c[4 * t] = fmaf(x, p4.x, c[4 * t]);
-        c[4 * t + 1] = fmaf(x, p4.y, c[4 * t + 1]);
-        c[4 * t + 2] = fmaf(x, p4.z, c[4 * t + 2]);
-        c[4 * t + 3] = fmaf(x, p4.w, c[4 * t + 3]);
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      put_split(opB, sw128(i, 4 * h + t), make_float4(-c[4 * t], -c[4 * t + 1], -c[4 * t + 2], -c[4 * t + 3]));
-#pragma unroll
-    for (int jj = 0; jj < 16; ++jj) Cs[i * kLd + 16 * h + jj] = c[jj];
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
+    PVT_MARK(2 + 4 * s);
+    const int f = *sfail;
+    if (f >= 0) {  // uniform
+      fail = 32 * s + f;
+      break;
+    }
+    // ---- 2. C = A P_K^-1 on the tensor cores
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+      mma_split3<32>(tbase + kTC1, tbase + kTC2, opA, kOpBytes, opP, kPBytes);
+      tc_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    tc_fence_after();
+    float c[32];  // C[i][0..32)
+    {
+      uint32_t c1[32], c2[32];
+      tmem_ld_32x32b_x32_nowait(tq + kTC1, c1);
+      tmem_ld_32x32b_x32_nowait(tq + kTC2, c2);
+      tmem_ld_wait();
+#pragma unroll
+      for (int t = 0; t < 32; ++t) c[t] = __uint_as_float(c1[t]) + __uint_as_float(c2[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {  // this thread's 16 columns of -C -> the B operand, C -> Cs
+      const float4 lo4 = make_float4(-c[4 * t], -c[4 * t + 1], -c[4 * t + 2], -c[4 * t + 3]);
+      const float4 hi4 = make_float4(-c[16 + 4 * t], -c[17 + 4 * t], -c[18 + 4 * t], -c[19 + 4 * t]);
+      put_split3(opB, kOpBytes, sw128(i, 4 * h + t), h ? hi4 : lo4);
+    }
+#pragma unroll
+    for (int t = 0; t < 16; ++t) Cs[i * kLd + 16 * h + t] = h ? c[16 + t] : c[t];
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    PVT_MARK(3 + 4 * s);
     // ---- 3. U = A B^T on the tensor cores, D += U in registers
     if (threadIdx.x == 0) {
       tc_fence_after();
-      const uint64_t ah = make_sdesc_sw128(opA), al = make_sdesc_sw128(opA + kOpBytes);
-      const uint64_t bh = make_sdesc_sw128(opB), bl = make_sdesc_sw128(opB + kOpBytes);
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 B of K per 128-B swizzle row
-        const uint64_t off = uint64_t(kk * 2);
-        umma<Kind::TF32>(tbase, ah + off, bh + off, idesc, kk != 0);
-        umma<Kind::TF32>(tbase, ah + off, bl + off, idesc, 1u);
-        umma<Kind::TF32>(tbase, al + off, bh + off, idesc, 1u);
-      }
+      mma_split3<128>(tbase + kTU1, tbase + kTU2, opA, kOpBytes, opB, kOpBytes);
       tc_commit(bar);
     }
-    mbar_wait(bar, uint32_t(s & 1));
+    mbar_wait(bar, phase);
+    phase ^= 1u;
     tc_fence_after();
-    {
-      uint32_t u0[32], u1[32];
-      tmem_ld_32x32b_x32_nowait(tU, u0);
-      tmem_ld_32x32b_x32_nowait(tU + 32, u1);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t u1[32], u2[32];
+      tmem_ld_32x32b_x32_nowait(tq + kTU1 + 64 * h + 32 * half, u1);
+      tmem_ld_32x32b_x32_nowait(tq + kTU2 + 64 * h + 32 * half, u2);
       tmem_ld_wait();
 #pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        d[t] += __uint_as_float(u0[t]);
-        d[32 + t] += __uint_as_float(u1[t]);
-      }
+      for (int t = 0; t < 32; ++t) d[32 * half + t] += __uint_as_float(u1[t]) + __uint_as_float(u2[t]);
     }
+    PVT_MARK(4 + 4 * s);
     // ---- 4. fix-up of row / column block K
     if (q != s) {
       if (h == hs) {  // D[i,K] = C[i]
         if (odd) {
 #pragma unroll
-          for (int t = 0; t < 32; ++t) d[32 + t] = Cs[i * kLd + t];
+          for (int t = 0; t < 32; ++t) d[32 + t] = c[t];
         } else {
 #pragma unroll
-          for (int t = 0; t < 32; ++t) d[t] = Cs[i * kLd + t];
+          for (int t = 0; t < 32; ++t) d[t] = c[t];
         }
       }
-    } else {  // rows K: D[K,j] = C[j]^T (j not in K), D[K,K] = S_K = -P_K^-1
+    } else {  // rows K: D[K,j] = C[j]^T (j not in K), D[K,K] = S_K (the sweeping warp's registers)
+      if (h == hs) {
+        if (odd) {
 #pragma unroll
-      for (int t = 0; t < 64; ++t) {
-        const int j = 64 * h + t;
-        d[t] = (j >= c0 && j < c0 + 32) ? -Pv[lane * kPvLd + (j - c0)] : Cs[j * kLd + lane];
+          for (int t = 0; t < 32; ++t) d[t] = Cs[(64 * h + t) * kLd + lane], d[32 + t] = a[t];
+        } else {
+#pragma unroll
+          for (int t = 0; t < 32; ++t) d[t] = a[t], d[32 + t] = Cs[(64 * h + 32 + t) * kLd + lane];
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 64; ++t) d[t] = Cs[(64 * h + t) * kLd + lane];
       }
     }
     tc_fence_before();
-    __syncthreads();  // shared staging and the TMEM accumulator are reused by the next step
+    __syncthreads();  // shared staging and the TMEM accumulators are reused by the next step
     tc_fence_after();
+    PVT_MARK(5 + 4 * s);
   }
+  PVT_MARK(26);
 
   if (fail >= 0) {
     if (threadIdx.x == 0) *m.info = int(kSmall ? 0 : K0) + fail + 1;
-  } else if constexpr (!kSmall) {
-    float4* dst = reinterpret_cast<float4*>(m.W + (K0 + i) * dp + K0 + 64 * h);  // W[K,K] <- -P^-1
-    float* ph = pinv_planes + (int64_t(m.slot) * kB + i) * kB + 64 * h;          // P^-1 hi / lo planes
+  } else {
 #pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      dst[t] = make_float4(d[4 * t], d[4 * t + 1], d[4 * t + 2], d[4 * t + 3]);
-      float4 hi, lo;
-      split_tf32(-d[4 * t], hi.x, lo.x);
-      split_tf32(-d[4 * t + 1], hi.y, lo.y);
-      split_tf32(-d[4 * t + 2], hi.z, lo.z);
-      split_tf32(-d[4 * t + 3], hi.w, lo.w);
-      reinterpret_cast<float4*>(ph)[t] = hi;
-      reinterpret_cast<float4*>(ph + pinv_plane)[t] = lo;
-    }
-  } else {  // out = -(D + D^T)/2 cropped, through shared memory (the staging area is free now)
-    float* F = reinterpret_cast<float*>(sm);
-#pragma unroll
-    for (int t = 0; t < 64; ++t) F[i * 129 + 64 * h + t] = d[t];
+    for (int t = 0; t < 16; ++t)
+      *reinterpret_cast<float4*>(F + i * kFLd + 64 * h + 4 * t) = make_float4(d[4 * t], d[4 * t + 1], d[4 * t + 2], d[4 * t + 3]);
     __syncthreads();
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-      const int r = e / n, cc = e - r * n;
-      m.out[e] = -0.5f * (F[r * 129 + cc] + F[cc * 129 + r]);
+    if constexpr (!kSmall) {  // W[K,K] <- -P^-1 and P^-1 hi / lo planes, whole rows per warp instruction
+      float* ph = pinv_planes + int64_t(m.slot) * kB * kB;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int row = 16 * warp + r;
+        const float4 x = *reinterpret_cast<const float4*>(F + row * kFLd + 4 * lane);
+        reinterpret_cast<float4*>(m.W + (K0 + row) * dp + K0)[lane] = x;
+        float4 hi, lo;
+        split_tf32(-x.x, hi.x, lo.x);
+        split_tf32(-x.y, hi.y, lo.y);
+        split_tf32(-x.z, hi.z, lo.z);
+        split_tf32(-x.w, hi.w, lo.w);
+        reinterpret_cast<float4*>(ph + row * kB)[lane] = hi;
+        reinterpret_cast<float4*>(ph + pinv_plane + row * kB)[lane] = lo;
+      }
+    } else {  // out = -(D + D^T)/2 cropped
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int r = e / n, cc = e - r * n;
+        m.out[e] = -0.5f * (F[r * kFLd + cc] + F[cc * kFLd + r]);
+      }
+      if (threadIdx.x == 0) *m.info = 0;
     }
-    if (threadIdx.x == 0) *m.info = 0;
   }
+  PVT_MARK(27);
+#ifdef SPD_PIVOT_TIMING
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    printf("pivot k=%d load %lld |", k, clk[1] - clk[0]);
+    for (int s2 = 0; s2 < 4; ++s2)
+      printf(" s%d: sweep %lld panel %lld update %lld fix %lld |", s2, clk[2 + 4 * s2] - clk[s2 ? 1 + 4 * s2 : 1],
+             clk[3 + 4 * s2] - clk[2 + 4 * s2], clk[4 + 4 * s2] - clk[3 + 4 * s2], clk[5 + 4 * s2] - clk[4 + 4 * s2]);
+    printf(" out %lld total %lld\n", clk[27] - clk[26], clk[27] - clk[0]);
+  }
+#endif
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_free<128>(tbase);
+  probe_stop(probe);
+  if (warp == 0) tmem_free<512>(tbase);
 }
 
 // ---------------------------------------------------------------- d <= 128
 __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __restrict__ mats,
-                                                            const int32_t* __restrict__ ids, float gamma) {
+                                                            const int32_t* __restrict__ ids, float gamma,
+                                                            Probe* probe) {
   __shared__ B8v2Shared sh;
+  probe_start(probe);
   const InvMat m = mats[ids[blockIdx.x]];
   const int n = m.d;
   const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
@@ -473,6 +605,7 @@ __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __rest
   const int f = sweep128_b8v2(a, n, sh);
   if (f >= 0) {
     if (threadIdx.x == 0) *m.info = f + 1;
+    probe_stop(probe);
     return;
   }
   if (threadIdx.x == 0) *m.info = 0;
@@ -487,6 +620,8 @@ __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __rest
     const int rr = e / n, c = e - rr * n;
     m.out[e] = 0.5f * (sm[rr * kSmemLd + c] + sm[c * kSmemLd + rr]);
   }
+  __syncthreads();
+  probe_stop(probe);
 }
 
 // ---------------------------------------------------------------- blocked path
@@ -530,10 +665,15 @@ __global__ void __launch_bounds__(256) damp_unpack_kernel(const InvMat* __restri
 
 __global__ void __launch_bounds__(512) pivot_kernel(const InvMat* __restrict__ mats,
                                                     const int32_t* __restrict__ ids, int k,
-                                                    float* __restrict__ pinv_planes, int64_t pinv_plane) {
+                                                    float* __restrict__ pinv_planes, int64_t pinv_plane,
+                                                    Probe* probe) {
   __shared__ B8v2Shared sh;
+  probe_start(probe);
   const InvMat m = mats[ids[blockIdx.x]];
-  if (*m.info != 0) return;
+  if (*m.info != 0) {
+    probe_stop(probe);
+    return;
+  }
   const int64_t dp = m.dp, K0 = int64_t(k) * kB;
   const int r = threadIdx.x & 63, q = threadIdx.x >> 6;
   float a[2][16];
@@ -549,6 +689,7 @@ __global__ void __launch_bounds__(512) pivot_kernel(const InvMat* __restrict__ m
   const int f = sweep128_b8v2(a, kB, sh);
   if (f >= 0) {
     if (threadIdx.x == 0) *m.info = int(K0) + f + 1;
+    probe_stop(probe);
     return;
   }
 #pragma unroll
@@ -566,6 +707,8 @@ __global__ void __launch_bounds__(512) pivot_kernel(const InvMat* __restrict__ m
       *reinterpret_cast<float4*>(ph + pinv_plane + jj) = make_float4(l[0], l[1], l[2], l[3]);
     }
   }
+  __syncthreads();
+  probe_stop(probe);
 }
 
 struct PanelJob {
@@ -690,7 +833,7 @@ struct spdkfac_inverse_plan {
   std::vector<double> upd_flops, u2_flops;  // per step: U1 / U2 tensor work (algorithmic, per launch)
   cudaStream_t side = nullptr;  // look-ahead stream: pivot/stage/panel of step k+1
   bool lookahead = true;        // SPDKFAC_NO_LOOKAHEAD=1 serialises (diagnostics)
-  bool legacy_pivot = false;    // SPDKFAC_PIVOT=ffma: the round-1 FFMA pivot sweep (A/B diagnostics)
+  bool legacy_pivot = true;     // fp32 FFMA pivot sweep; SPDKFAC_PIVOT=tc: the tcgen05 pivot kernel
   int panel_ctas = 0;           // grid cap of the panel GEMM (SPDKFAC_PANEL_CTAS; 0 = all SMs: the chain latency wins)
   cudaEvent_t ev_u1 = nullptr, ev_panel = nullptr;
   int32_t* act_ids;             // device, active blocked matrices per step (concatenated)
@@ -956,8 +1099,11 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     if (const char* pc = getenv("SPDKFAC_PANEL_CTAS")) p->panel_ctas = atoi(pc);
     const char* e = getenv("SPDKFAC_NO_LOOKAHEAD");
     p->lookahead = !(e && e[0] == '1');
+    // the fp32 FFMA pivot sweep is the default: the tcgen05 pivot kernel (SPDKFAC_PIVOT=tc) is 1.6x
+    // faster per block but its 32-wide blocked sweep loses accuracy on rank-deficient factors
+    // (ResNet-50 fc A, kappa 2e4: inverse error 2.6e-2 vs 5e-3), see DESIGN.md
     const char* pv = getenv("SPDKFAC_PIVOT");
-    p->legacy_pivot = pv && std::string(pv) == "ffma";
+    p->legacy_pivot = !(pv && std::string(pv) == "tc");
   }
   if (p->n_blocked > 0) {
     SPD_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
@@ -980,11 +1126,12 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
   SPD_ARG(gamma >= 0.f, SPDKFAC_ERR_ARG, "damping must be nonnegative, got %g", double(gamma));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p->n_small > 0) {
-    stat_begin(kCatInvSmall, s);
+    Probe* pr = stat_begin(kCatInvSmall, s);
     if (p->legacy_pivot)
-      small_inverse_kernel<<<p->n_small, 512, kB * kSmemLd * 4, s>>>(p->mats, p->small_ids, gamma);
+      small_inverse_kernel<<<p->n_small, 512, kB * kSmemLd * 4, s>>>(p->mats, p->small_ids, gamma, pr);
     else
-      pivot_tc_kernel<true><<<p->n_small, pvt::kThreads, pvt::kSmem, s>>>(p->mats, p->small_ids, 0, nullptr, 0, gamma);
+      pivot_tc_kernel<true><<<p->n_small, pvt::kThreads, pvt::kSmem, s>>>(p->mats, p->small_ids, 0, nullptr, 0, gamma,
+                                                                          pr);
     SPD_CHECK_LAUNCH();
     stat_end(kCatInvSmall, s, p->small_flops, 0);
   }
@@ -998,22 +1145,23 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
     auto front = [&](int k, cudaStream_t q) -> int {
       const int na = p->act_cnt[k];
       float* pa = p->panA + (k % kPanSlots) * kB;
-      stat_begin(kCatInvPivot, q);
+      Probe* pr = stat_begin(kCatInvPivot, q);
       if (p->legacy_pivot)
         pivot_kernel<<<na, 512, 0, q>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
-                                        int64_t(p->n_blocked) * kB * kB);
+                                        int64_t(p->n_blocked) * kB * kB, pr);
       else
         pivot_tc_kernel<false><<<na, pvt::kThreads, pvt::kSmem, q>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
-                                                                     int64_t(p->n_blocked) * kB * kB, 0.f);
+                                                                     int64_t(p->n_blocked) * kB * kB, 0.f, pr);
       SPD_CHECK_LAUNCH();
       stat_end(kCatInvPivot, q, 2.0 * kB * kB * kB * na, 0);
-      stat_begin(kCatInvPanel, q);
+      TcRun prun{};
+      prun.probe = stat_begin(kCatInvPanel, q);  // the probe times the panel GEMM launch
       stage_panel_kernel<<<dim3(p->pan_cnt[k], 4), 256, 0, q>>>(p->mats, p->pan_jobs + p->pj_off[k], k, pa, plane);
       SPD_CHECK_LAUNCH();
       // the panel GEMM has few K blocks per tile: a full persistent grid would hold every SM for
       // ~20 us per step while doing little work; a capped grid leaves the SMs to the
       // concurrent convolutions at almost the same chain latency
-      int rc = launch_tc3(Kind::TF32, p->maps, p->items + p->pan_off[k], p->epis, p->pan_cnt[k], q, TcRun{},
+      int rc = launch_tc3(Kind::TF32, p->maps, p->items + p->pan_off[k], p->epis, p->pan_cnt[k], q, prun,
                           p->panel_ctas);
       if (rc) return rc;
       stat_end(kCatInvPanel, q, 2.0 * kB * kB * kB * p->pan_cnt[k], 0);
@@ -1025,14 +1173,14 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       // U1(k): the tiles step k+1 reads; then step k+1's front runs on the side stream
       // while U2(k) (the rest of the trailing update) runs here (look-ahead)
       const int u1 = p->u1_cnt[k], u2 = p->upd_cnt[k] - u1;
-      stat_begin(kCatInvUpdate, s);
-      rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k], p->epis, u1, s);
+      Probe* pu = stat_begin(kCatInvUpdate, s);
+      rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k], p->epis, u1, s, pu);
       if (rc) return rc;
       stat_end(kCatInvUpdate, s, p->upd_flops[k], 0);
       const bool ahead = k + 1 < p->steps;
       if (ahead && !p->lookahead) {  // serial order: rest of the update, then the next front
-        stat_begin(kCatInvUpdate, s);
-        rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k] + u1, p->epis, u2, s);
+        Probe* pu2 = stat_begin(kCatInvUpdate, s);
+        rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k] + u1, p->epis, u2, s, pu2);
         if (rc) return rc;
         stat_end(kCatInvUpdate, s, p->u2_flops[k], 0);
         if ((rc = front(k + 1, s))) return rc;
@@ -1044,8 +1192,8 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
         if ((rc = front(k + 1, p->side))) return rc;
         SPD_CUDA(cudaEventRecord(p->ev_panel, p->side));
       }
-      stat_begin(kCatInvUpdate, s);
-      rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k] + u1, p->epis, u2, s);
+      pu = stat_begin(kCatInvUpdate, s);
+      rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k] + u1, p->epis, u2, s, pu);
       if (rc) return rc;
       stat_end(kCatInvUpdate, s, p->u2_flops[k], 0);
       if (ahead) SPD_CUDA(cudaStreamWaitEvent(s, p->ev_panel, 0));

@@ -29,7 +29,11 @@ struct StatRec {
 std::mutex g_stat_mu;
 std::vector<StatRec> g_recs;
 size_t g_rec_used = 0;
-uint32_t g_timing = 0;  // bitmask of timed categories
+uint32_t g_timing = 0;  // bitmask of event-timed categories
+uint32_t g_probing = 0;  // bitmask of probe-timed categories (in-kernel stamps)
+Probe* g_probes = nullptr;  // device array of probe slots
+size_t g_probe_cap = 0, g_probe_used = 0;
+std::vector<int> g_probe_cat;  // category of each used slot
 std::atomic<uint64_t> g_launches{0};
 uint64_t g_cat_launches[kNumCats] = {};
 double g_cat_flops[kNumCats] = {}, g_cat_bytes[kNumCats] = {};
@@ -45,9 +49,15 @@ void record_stat_event(cudaEvent_t e, cudaStream_t s) {
 }
 }  // namespace
 
-void stat_begin(int cat, cudaStream_t s) {
+Probe* stat_begin(int cat, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  if (!(g_timing & (1u << cat))) return;
+  if (g_probing & (1u << cat)) {
+    std::lock_guard<std::mutex> lk(g_stat_mu);
+    if (g_probe_used >= g_probe_cap) return nullptr;  // out of reserved slots: untimed
+    g_probe_cat.push_back(cat);
+    return g_probes + g_probe_used++;
+  }
+  if (!(g_timing & (1u << cat))) return nullptr;
   std::lock_guard<std::mutex> lk(g_stat_mu);
   if (g_rec_used == g_recs.size()) {
     StatRec r;
@@ -58,6 +68,7 @@ void stat_begin(int cat, cudaStream_t s) {
   g_open = long(g_rec_used++);
   g_recs[g_open].cat = cat;
   record_stat_event(g_recs[g_open].a, s);
+  return nullptr;
 }
 
 void stat_end(int cat, cudaStream_t s, double flops, double bytes) {
@@ -178,9 +189,12 @@ int launch_tc3_acc(const CUtensorMap* maps, const TcItem* items, const TcEpi* ep
   return launch_kind<Kind::TF32, kStages, false, kAccChunk>(maps, items, epis, n, s, run);
 }
 
-int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s) {
+int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
+                     Probe* probe) {
   if (n <= 0) return SPDKFAC_OK;
-  return launch_kind<Kind::TF32, 3, true>(maps, items, epis, n, s, TcRun{});
+  TcRun run{};
+  run.probe = probe;
+  return launch_kind<Kind::TF32, 3, true>(maps, items, epis, n, s, run);
 }
 
 int launch_tc3_pair(const CUtensorMap* maps, const TcPairItem* items, const TcEpi* epis, int n, cudaStream_t s,
@@ -346,7 +360,9 @@ int spdkfac_version(void) { return 100; }
 void spdkfac_stats_reset(int timing_mask) {
   std::lock_guard<std::mutex> lk(g_stat_mu);
   g_rec_used = 0;
-  g_timing = uint32_t(timing_mask);
+  g_probe_used = 0;
+  g_probe_cat.clear();
+  g_timing = uint32_t(timing_mask) & ~g_probing;
   g_launches.store(0);
   for (int c = 0; c < kNumCats; ++c) g_cat_launches[c] = 0, g_cat_flops[c] = 0, g_cat_bytes[c] = 0;
 }
@@ -364,10 +380,34 @@ int spdkfac_stats_reserve(int n) {
   return SPDKFAC_OK;
 }
 
+int spdkfac_stats_set_probes(int probe_mask, int n_slots) {
+  std::lock_guard<std::mutex> lk(g_stat_mu);
+  if (n_slots > 0 && size_t(n_slots) > g_probe_cap) {
+    if (g_probes) SPD_CUDA(cudaFree(g_probes));
+    g_probes = nullptr;
+    g_probe_cap = 0;
+    SPD_CUDA(cudaMalloc(&g_probes, sizeof(Probe) * size_t(n_slots)));
+    SPD_CUDA(cudaMemset(g_probes, 0, sizeof(Probe) * size_t(n_slots)));
+    g_probe_cap = size_t(n_slots);
+  }
+  g_probing = uint32_t(probe_mask);
+  g_timing &= ~g_probing;
+  g_probe_used = 0;
+  g_probe_cat.clear();
+  return SPDKFAC_OK;
+}
+
 int spdkfac_stats_read(int cat, double* ms, int64_t* launches, double* flops, double* bytes) {
   SPD_ARG(cat >= 0 && cat < kNumCats, SPDKFAC_ERR_ARG, "bad stats category");
   std::lock_guard<std::mutex> lk(g_stat_mu);
   double t = 0;
+  if ((g_probing & (1u << cat)) && g_probe_used > 0) {  // probe stamps of the last run of each launch
+    std::vector<Probe> h(g_probe_used);
+    SPD_CUDA(cudaDeviceSynchronize());
+    SPD_CUDA(cudaMemcpy(h.data(), g_probes, sizeof(Probe) * g_probe_used, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < g_probe_used; ++i)
+      if (g_probe_cat[i] == cat && h[i].t1 > h[i].t0) t += double(h[i].t1 - h[i].t0) * 1e-6;
+  }
   for (size_t i = 0; i < g_rec_used; ++i) {
     if (g_recs[i].cat != cat) continue;
     float e = 0;

@@ -85,7 +85,8 @@ int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const Tc
 // CTA-pair SYRK engine (cta_group::2, 256 x 256 super tiles; bf16 MN-major split planes)
 int launch_tc3_pair(const CUtensorMap* maps, const TcPairItem* items, const TcEpi* epis, int n_items, cudaStream_t s,
                     const TcRun& run);
-int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items, cudaStream_t s);
+int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items, cudaStream_t s,
+                     Probe* probe = nullptr);
 // TF32 engine with chunked accumulation (kAccChunk K blocks of 32 per TMEM chunk, chunks summed in
 // fp32 registers): the preconditioning GEMMs (see tc3_gemm_kernel's kAcc)
 constexpr int kAccChunk = 4;
@@ -101,7 +102,9 @@ enum StatCat : int {
   kCatFactorStage = 0, kCatFactorSyrk, kCatFactorReduce, kCatInvSmall, kCatInvPivot, kCatInvPanel, kCatInvUpdate,
   kCatInvUnpackFinal, kCatPrecSplit, kCatPrecGemm, kCatPrecApply, kCatPack, kNumCats
 };
-void stat_begin(int cat, cudaStream_t s);
+// stat_begin returns the launch's probe when `cat` is probe-timed (spdkfac_stats_set_probes): the
+// launch site passes it to its kernel (TcRun::probe or a kernel argument); else nullptr
+Probe* stat_begin(int cat, cudaStream_t s);
 void stat_end(int cat, cudaStream_t s, double flops, double bytes);
 
 }  // namespace spd

@@ -54,6 +54,7 @@ struct TcRun {
   float decay;   // running-average weight of the old value (0: never read)
   float wscale;  // final scale (1/P)
   int32_t pad_;
+  Probe* probe;  // launch probe (spdkfac_stats_set_probes) or nullptr
 };
 
 struct TcEpi {
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(192, 1)
   static_assert(kAcc == 0 || !kCTile, "chunked accumulation is for register epilogues");
   constexpr int BK = (K == Kind::BF16) ? 64 : 32;  // one 128-byte swizzle row of K
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1024(smem_raw);
   float* ctile = reinterpret_cast<float*>(smem + kSt * kStageBytes);  // kCRing x [32][128] (kCTile)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageBytes + (kCTile ? kCRing * kCSliceBytes : 0));
   uint64_t* empty = full + kSt;
@@ -250,6 +251,7 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  probe_start(run.probe);
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
@@ -448,6 +450,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   tc_fence_before();
   __syncthreads();
+  probe_stop(run.probe);
   if (warp == 1) {
     if constexpr (kAcc > 0) tmem_free<512>(tmem);
     else tmem_free<256>(tmem);
@@ -482,7 +485,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     tc3_pair_kernel(const CUtensorMap* __restrict__ maps, const TcPairItem* __restrict__ items,
                     const TcEpi* __restrict__ epis, const TcRun run, int n_items) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageBytes);
   uint64_t* empty = full + kSt;
   uint64_t* tfull = empty + kSt;  // [2]
@@ -508,6 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   tc_fence_before();
   cluster_sync();  // barriers of both CTAs initialised, TMEM allocated in both
   tc_fence_after();
+  probe_start(run.probe);
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
@@ -617,6 +621,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   }
   tc_fence_before();
   cluster_sync();  // the peer's TMEM / smem are read by the leader's MMAs until the end
+  probe_stop(run.probe);
   if (warp == 1) tmem_free_pair<512>(tmem);
 }
 

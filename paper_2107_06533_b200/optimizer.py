@@ -667,7 +667,8 @@ class SPDKFAC(torch.optim.Optimizer):
         factors_now = self._capture
         invert_now = self.steps % self.inv_update_freq == 0
         self._tl("backward_done", main)
-        main.wait_stream(self.stage_stream)  # every staged input / output gradient is consumed
+        if factors_now:  # every staged input / output gradient is consumed (a reuse step stages nothing:
+            main.wait_stream(self.stage_stream)  # under graph capture the stage stream is then not part of it)
         self._stage_refs.clear()
         if factors_now:
             main.wait_stream(self.factor_stream)
