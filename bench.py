@@ -313,11 +313,14 @@ ROOF_CATS = ("factor_stage", "factor_syrk", "inv_pivot", "inv_panel", "inv_updat
 # bound and peak of each category: the tensor-core contractions against the measured GEMM peak of
 # the MMA kind they issue (bf16 for the factor SYRK, tf32 for the inverse and the preconditioning),
 # the staging pass against HBM
-_ROOF_SPEC = {"factor_syrk": ("tensor", "bf16_tflops_sustained"), "inv_pivot": ("tensor", "tf32_tflops"),
+_ROOF_SPEC = {"factor_syrk": ("tensor", "bf16_tflops_sustained"),
+              "inv_pivot": ("fp32", "fp32_ffma_tflops") if os.environ.get("SPDKFAC_PIVOT") != "tc" else ("tensor", "tf32_tflops"),
               "inv_panel": ("tensor", "tf32_tflops"), "inv_update": ("tensor", "tf32_tflops"),
               "precond_gemm": ("tensor", "tf32_tflops"), "factor_stage": ("hbm", "hbm_gbs")}
 _KERNEL_NAMES = {"factor_syrk": "tc3_gemm_kernel<BF16> + tc3_pair_kernel (factor SYRK, 3 x bf16, tcgen05)",
-                 "inv_pivot": "pivot_tc_kernel<false> (128-pivot block: warp sweeps + rank-32 tcgen05 updates)",
+                 "inv_pivot": ("pivot_kernel (128-pivot block: 16 rank-8 fp32 FFMA sweeps)"
+                               if os.environ.get("SPDKFAC_PIVOT") != "tc" else
+                               "pivot_tc_kernel<false> (128-pivot block: warp sweeps + rank-32 tcgen05 updates)"),
                  "inv_panel": "stage_panel_kernel + tc3_gemm_kernel<TF32> (inverse panel C = W[:,K] P^-1)",
                  "inv_update": "tc3_gemm_kernel<TF32, C-tile> (inverse trailing update, 3 x tf32)",
                  "precond_gemm": "tc3_gemm_kernel<TF32, chunked accumulation> (G^-1 grad A^-1, W -= lr P)",
@@ -330,17 +333,17 @@ def kernel_roofline(cat, rec, per, peaks, world, model):
     bound, peak_key = _ROOF_SPEC[cat]
     ms = rec["ms"] / per
     launches = rec["launches"] / per
-    work = rec["flops"] / per if bound == "tensor" else rec["bytes"] / per
-    ach = (work / (ms * 1e-3)) / (1e12 if bound == "tensor" else 1e9) if ms > 0 else 0.0
+    work = rec["bytes"] / per if bound == "hbm" else rec["flops"] / per
+    ach = (work / (ms * 1e-3)) / (1e9 if bound == "hbm" else 1e12) if ms > 0 else 0.0
     peak = peaks.get(peak_key)
     out = {"kernel": _KERNEL_NAMES[cat], "category": cat, "bound": bound, "achieved": round(ach, 2),
-           "peak": round(peak, 1) if peak else None, "unit": "TFLOP/s" if bound == "tensor" else "GB/s",
+           "peak": round(peak, 1) if peak else None, "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
            "frac": round(ach / peak, 4) if peak and ms > 0 else None, "peak_source": peak_key + (
                " (MEASURED_PEAKS.json)" if peak_key in ("hbm_gbs", "bf16_tflops_sustained") else " (measured by this run)"),
            "kernel_ms_per_step": round(ms, 4), "launches_per_step": launches,
            "timing": "in-kernel launch probes (first CTA start to last CTA end, %globaltimer) over the timed region's "
                      "last step (graph mode) or all timed steps (eager)",
-           ("algorithmic_flops_per_step" if bound == "tensor" else "algorithmic_bytes_per_step"): work,
+           ("algorithmic_bytes_per_step" if bound == "hbm" else "algorithmic_flops_per_step"): work,
            "traffic": None}
     try:  # DRAM bytes per launch from a committed `ncu --set full` capture of the same launches
         t = json.load(open(os.path.join(ROOT, "profiles", f"traffic_{model}_n{world}.json")))[cat]
@@ -364,7 +367,8 @@ def iteration_roof(bst, nb, peaks, ffbp_flops, ms):
     for cat, rec in bst.items():
         if not isinstance(rec, dict) or not (rec["flops"] or rec["bytes"]):
             continue
-        pk = bf16 if cat == "factor_syrk" else tf32
+        pk = bf16 if cat == "factor_syrk" else (peaks.get("fp32_ffma_tflops") or tf32) if cat in ("inv_pivot", "inv_small") \
+            and os.environ.get("SPDKFAC_PIVOT") != "tc" else tf32
         parts[cat] = max(rec["flops"] / nb / (pk * 1e12), rec["bytes"] / nb / (hbm * 1e9)) * 1e3
     if ffbp_flops:
         parts["forward_backward"] = ffbp_flops / (tf32 * 1e12) * 1e3

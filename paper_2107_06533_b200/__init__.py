@@ -8,7 +8,7 @@ importing the GPU-facing modules without the built library raises.
 """
 
 from .perfmodel import (  # noqa: F401
-    AllReduceParams, BcastParams, InverseParams, BenchSample, PerfParams,
+    AllReduceParams, BcastParams, InverseParams, MarginalInverseParams, BenchSample, PerfParams,
     allreduce_time, bcast_time, inverse_time, fit_linear, fit_exponential,
     nct_threshold, read_params, write_params,
 )

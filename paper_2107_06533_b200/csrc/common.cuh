@@ -48,12 +48,15 @@ SPD_DEV uint64_t global_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+#ifndef SPD_WATCHDOG_NS
+#define SPD_WATCHDOG_NS 4000000000ull  // the sanitizer build (scripts/r2_sanitize.sh) raises it
+#endif
 SPD_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   // watchdog: a protocol bug traps (kernel error) after ~4 s instead of hanging the GPU
   if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = global_ns();
   while (!mbar_try_wait(bar, parity)) {
-    if (global_ns() - t0 > 4000000000ull) asm volatile("trap;");
+    if (global_ns() - t0 > SPD_WATCHDOG_NS) asm volatile("trap;");
   }
 }
 
@@ -204,6 +207,13 @@ SPD_DEV void umma_pair_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uin
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+SPD_DEV void umma_pair_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 

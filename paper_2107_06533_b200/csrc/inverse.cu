@@ -18,6 +18,9 @@
 //                         (3 x tf32, rank-128), mirrored to W[J,I]
 //              finalize: out = -(W + W^T)/2 cropped to d x d (the reference's symmetrisation).
 #include <algorithm>
+#include <cstdint>
+#include <map>
+#include <tuple>
 
 #include "runtime.cuh"
 
@@ -842,6 +845,9 @@ struct spdkfac_inverse_plan {
   int n_tiles;
   CUtensorMap* maps;            // [0] panA, [1] panC, [2] P^-1, [3], [4] unused, [5 + slot] W_slot tiles
   TcItem* items;                // per step: panel GEMM items then update items
+  TcPairCItem* pitems;          // per step: CTA-pair super tiles of the bulk update (U2)
+  std::vector<int> pu_off, pu_cnt;
+  std::vector<double> pu_flops;
   TcEpi* epis;                  // [0, n): update, [n + q n, n + (q + 1) n): panel writing panC slot q
   float* panA;                  // [2 planes][rows][kPanCols] (slot q = columns [128 q, 128 q + 128))
   float* panC;
@@ -851,6 +857,20 @@ struct spdkfac_inverse_plan {
 };
 
 namespace {
+
+// SPDKFAC_UPDATE_PAIRS=1: 2 x 2 blocks of update tiles with one K range go to the CTA-pair engine
+// (tc3_pair_ctile_kernel, 70 % tensor-pipe under ncu vs 47 % for the single-CTA engine).  Off by
+// default: the aligned-pair cover takes ~57 % of the ResNet-50 update work and the leftover single
+// tiles run less efficiently, so the batched inverse and the bench step are unchanged.
+bool update_pairs() {
+  const char* e = getenv("SPDKFAC_UPDATE_PAIRS");
+  return e && e[0] == '1';
+}
+
+bool update_order_by_matrix() {  // SPDKFAC_UPDATE_ORDER=nk: the round-1 order (longest K first across matrices)
+  const char* e = getenv("SPDKFAC_UPDATE_ORDER");
+  return !(e && std::string(e) == "nk");
+}
 
 void inverse_sizes(int n, const int32_t* dims, int64_t* rows, int64_t* items, int64_t* act, int64_t* tiles,
                    int* steps, int* nblk) {
@@ -899,10 +919,12 @@ size_t inverse_carve(int n, const int32_t* dims, Carve& c, spdkfac_inverse_plan*
   auto* pj = c.take<PanelJob>(size_t(std::max<int64_t>(items, 1)));
   auto* mp = c.take<CUtensorMap>(size_t(5 + nblk), 128);
   auto* it = c.take<TcItem>(size_t(std::max<int64_t>(items, 1)));
+  auto* pit = c.take<TcPairCItem>(size_t(std::max<int64_t>(items / 4, 1)));
   auto* ep = c.take<TcEpi>(size_t(1 + kPanSlots) * n);
   if (p) {
     p->panA = panA, p->panC = panC, p->pinvS = pinvS, p->mats = dm, p->small_ids = sid, p->blocked_ids = bid;
     p->act_ids = aid, p->tiles = tj, p->pan_jobs = pj, p->maps = mp, p->items = it, p->epis = ep;
+    p->pitems = pit;
     p->plane_rows = rows, p->steps = steps, p->n_tiles = int(tiles);
   }
   return c.used;
@@ -968,6 +990,7 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   }
   std::vector<int32_t> act;
   std::vector<TcItem> items;
+  std::vector<TcPairCItem> pitems;
   std::vector<PanelJob> pan;
   for (int k = 0; k < p->steps; ++k) {
     p->act_off.push_back(int(act.size()));
@@ -1061,7 +1084,79 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
           (in_u1 ? u1v : u2v).push_back(it);
         }
     }
-    std::stable_sort(u2v.begin(), u2v.end(), [](const TcItem& a, const TcItem& b) { return a.nk > b.nk; });
+    // CTA-pair super tiles (2 x 2 target tiles sharing their K range) out of the U2 items; the
+    // rest stay single-CTA items
+    p->pu_off.push_back(int(pitems.size()));
+    p->pu_flops.push_back(0.0);
+    if (update_pairs()) {
+      std::map<std::tuple<int, int, int>, size_t> at;  // (matrix, I, J) -> index in u2v
+      for (size_t x = 0; x < u2v.size(); ++x)
+        at[{u2v[x].epi, u2v[x].out_c / kB, u2v[x].out_r / kB}] = x;
+      std::vector<bool> used(u2v.size(), false);
+      for (int t : blocked) {
+        const int T = mats[t].dp / kB;
+        if (k >= T) continue;
+        // greedy row-major cover of the upper block triangle by 2 x 2 super tiles (I0 .. I0+1) x
+        // (J0 .. J0+1), J0 >= I0.  A diagonal super tile (J0 == I0) also computes the lower block
+        // (I0+1, I0): the sweep maintains only the upper block triangle, which is all any kernel
+        // reads, so that block's store is dead and harmless.
+        for (int I0 = 0; I0 + 1 < T; ++I0)
+          for (int J0 = I0; J0 + 1 < T; ++J0) {
+            size_t ix[4];
+            int n_up = 0;
+            bool ok = true;
+            for (int h = 0; h < 2 && ok; ++h)
+              for (int r = 0; r < 2 && ok; ++r) {
+                ix[2 * h + r] = SIZE_MAX;
+                if (I0 + h > J0 + r) continue;  // the dead lower block of a diagonal super tile
+                auto f = at.find({t, I0 + h, J0 + r});
+                ok = f != at.end() && !used[f->second];
+                if (ok) ix[2 * h + r] = f->second, ++n_up;
+              }
+            if (!ok || n_up < 3) continue;
+            const TcItem& q0 = u2v[ix[0]];
+            for (int e = 1; e < 4 && ok; ++e)
+              if (ix[e] != SIZE_MAX) ok = u2v[ix[e]].k0 == q0.k0 && u2v[ix[e]].nk == q0.nk;
+            if (!ok) continue;
+            TcPairCItem pi{};
+            pi.a_map = 0, pi.b_map = 1;
+            pi.a_row = mats[t].panel_row0 + J0 * kB;
+            pi.b_row = mats[t].panel_row0 + I0 * kB;
+            pi.k0 = q0.k0, pi.nk = q0.nk, pi.epi = t;
+            pi.out_r[0] = J0 * kB, pi.out_r[1] = (J0 + 1) * kB;
+            pi.out_c[0] = I0 * kB, pi.out_c[1] = (I0 + 1) * kB;
+            pitems.push_back(pi);
+            p->pu_flops.back() += n_up * 2.0 * kB * kB * 32 * q0.nk;
+            for (size_t e : ix)
+              if (e != SIZE_MAX) used[e] = true;
+          }
+      }
+      std::vector<TcItem> rest;
+      for (size_t x = 0; x < u2v.size(); ++x)
+        if (!used[x]) rest.push_back(u2v[x]);
+      u2v.swap(rest);
+      std::stable_sort(pitems.begin() + p->pu_off.back(), pitems.end(),
+                       [&](const TcPairCItem& a, const TcPairCItem& b) {
+                         const int da = mats[a.epi].dp, db = mats[b.epi].dp;
+                         if (da != db) return da > db;
+                         if (a.epi != b.epi) return a.epi < b.epi;
+                         return a.nk > b.nk;
+                       });
+    }
+    p->pu_cnt.push_back(int(pitems.size()) - p->pu_off.back());
+    if (update_order_by_matrix()) {
+      // matrix-major (largest first), longest K first inside a matrix: the persistent CTAs then work
+      // on one matrix's panels at a time, a working set that stays in L2, instead of streaming every
+      // batched matrix's panels at once
+      std::stable_sort(u2v.begin(), u2v.end(), [&](const TcItem& a, const TcItem& b) {
+        const int da = mats[a.epi].dp, db = mats[b.epi].dp;
+        if (da != db) return da > db;
+        if (a.epi != b.epi) return a.epi < b.epi;
+        return a.nk > b.nk;
+      });
+    } else {
+      std::stable_sort(u2v.begin(), u2v.end(), [](const TcItem& a, const TcItem& b) { return a.nk > b.nk; });
+    }
     u1 = int(u1v.size());
     items.insert(items.end(), u1v.begin(), u1v.end());
     items.insert(items.end(), u2v.begin(), u2v.end());
@@ -1091,7 +1186,7 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   if ((rc = upload(p->mats, mats, s)) || (rc = upload(p->small_ids, small, s)) ||
       (rc = upload(p->blocked_ids, blocked, s)) || (rc = upload(p->act_ids, act, s)) ||
       (rc = upload(p->tiles, tiles, s)) || (rc = upload(p->pan_jobs, pan, s)) || (p->n_blocked > 0 && (rc = upload(p->maps, maps, s))) ||
-      (rc = upload(p->items, items, s)) || (rc = upload(p->epis, epis, s))) {
+      (rc = upload(p->items, items, s)) || (rc = upload(p->pitems, pitems, s)) || (rc = upload(p->epis, epis, s))) {
     delete p;
     return rc;
   }
@@ -1179,6 +1274,11 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       stat_end(kCatInvUpdate, s, p->upd_flops[k], 0);
       const bool ahead = k + 1 < p->steps;
       if (ahead && !p->lookahead) {  // serial order: rest of the update, then the next front
+        if (p->pu_cnt[k]) {
+          Probe* pp = stat_begin(kCatInvUpdate, s);
+          if ((rc = launch_tc3_pair_ctile(p->maps, p->pitems + p->pu_off[k], p->epis, p->pu_cnt[k], s, pp))) return rc;
+          stat_end(kCatInvUpdate, s, p->pu_flops[k], 0);
+        }
         Probe* pu2 = stat_begin(kCatInvUpdate, s);
         rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k] + u1, p->epis, u2, s, pu2);
         if (rc) return rc;
@@ -1191,6 +1291,11 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
         SPD_CUDA(cudaStreamWaitEvent(p->side, p->ev_u1, 0));
         if ((rc = front(k + 1, p->side))) return rc;
         SPD_CUDA(cudaEventRecord(p->ev_panel, p->side));
+      }
+      if (p->pu_cnt[k]) {
+        Probe* pp = stat_begin(kCatInvUpdate, s);
+        if ((rc = launch_tc3_pair_ctile(p->maps, p->pitems + p->pu_off[k], p->epis, p->pu_cnt[k], s, pp))) return rc;
+        stat_end(kCatInvUpdate, s, p->pu_flops[k], 0);
       }
       pu = stat_begin(kCatInvUpdate, s);
       rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k] + u1, p->epis, u2, s, pu);

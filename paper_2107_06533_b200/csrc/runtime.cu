@@ -222,6 +222,34 @@ int launch_tc3_pair(const CUtensorMap* maps, const TcPairItem* items, const TcEp
   return SPDKFAC_OK;
 }
 
+int launch_tc3_pair_ctile(const CUtensorMap* maps, const TcPairCItem* items, const TcEpi* epis, int n, cudaStream_t s,
+                          Probe* probe) {
+  if (n <= 0) return SPDKFAC_OK;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SPD_CUDA(cudaFuncSetAttribute(tc3_pair_ctile_kernel<kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kPairCSmemBytes)));
+    attr_set = true;
+  }
+  static int pairs = 0;
+  if (!pairs) {
+    int dev = 0, sms = 0;
+    SPD_CUDA(cudaGetDevice(&dev));
+    SPD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (const char* e = getenv("SPDKFAC_MAX_CTAS")) {
+      const int cap = atoi(e);
+      if (cap > 0 && cap < sms) sms = cap;
+    }
+    pairs = sms / 2;
+  }
+  TcRun run{};
+  run.probe = probe;
+  const int grid = 2 * (n < pairs ? n : pairs);
+  tc3_pair_ctile_kernel<kStages><<<grid, 192, kPairCSmemBytes, s>>>(maps, items, epis, run, n);
+  SPD_CHECK_LAUNCH();
+  return SPDKFAC_OK;
+}
+
 int make_ctile_map(CUtensorMap* out, const float* base, int64_t rows, int64_t cols, int64_t ld) {
   EncodeTiledFn fn = encode_fn();
   SPD_ARG(fn != nullptr, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");

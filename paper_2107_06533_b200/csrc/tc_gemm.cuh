@@ -625,4 +625,177 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   if (warp == 1) tmem_free_pair<512>(tmem);
 }
 
+
+// ------------------------------------------------------------------ CTA-pair C-tile engine
+// cta_group::2 variant of the kCTile engine for the blocked inverse's trailing update (tf32 split
+// planes, K-major): a cluster of two CTAs computes a 256 x 256 super tile D = A B^T, A = 256 panel
+// rows (two 128-blocks, one per CTA), B = 256 panel rows (two 128-blocks, one per CTA), i.e. four
+// 128 x 128 target tiles that share their K range.  Each CTA stages only its own A and B blocks per
+// K slab (the same 64-KB stage as the single-CTA engine) and the leader's M = N = 256 MMAs read both
+// CTAs' shared memory, so per SM the operand bytes per MMA cycle halve -- the single-CTA update ran
+// at ~30% tensor-pipe, fed from L2 / DRAM.  CTA r's TMEM holds super-tile rows [128 r, +128) x 256
+// columns = its two target tiles h = 0, 1, which it read-modify-writes through the C-slice ring.
+struct TcPairCItem {
+  int32_t a_map, b_map;  // operand tensor maps
+  int32_t a_row, b_row;  // operand rows of CTA 0's blocks (CTA 1: +128)
+  int32_t k0, nk;        // first K element, number of 32-wide K blocks
+  int32_t epi;           // epilogue table entry (kAxpby on a C-tile target: alpha, beta, c_map)
+  int32_t out_r[2];      // per CTA rank: target column offset (the M block)
+  int32_t out_c[2];      // per tile h: target row offset (the N block)
+  int32_t pad_;
+};
+
+constexpr size_t kPairCSmemBytes = size_t(kStages) * kStageBytes + kCRing * kCSliceBytes + 1024 + 256;
+
+template <int kSt>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    tc3_pair_ctile_kernel(const CUtensorMap* __restrict__ maps, const TcPairCItem* __restrict__ items,
+                          const TcEpi* __restrict__ epis, const TcRun run, int n_items) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_align1024(smem_raw);
+  float* ctile = reinterpret_cast<float*>(smem + kSt * kStageBytes);  // kCRing x [32][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSt * kStageBytes + kCRing * kCSliceBytes);
+  uint64_t* empty = full + kSt;
+  uint64_t* tfull = empty + kSt;  // [2]
+  uint64_t* tempty = tfull + 2;   // [2] (leader: 8 arrivals = 4 epilogue warps x 2 CTAs)
+  uint64_t* cfull = tempty + 2;   // [kCRing] C slice landed (own CTA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + kCRing);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t pair = cluster_idx(), npairs = cluster_count();
+  if (warp == 0 && lane == 0) {
+    for (int st = 0; st < kSt; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);
+    }
+    for (int q = 0; q < kCRing; ++q) mbar_init(&cfull[q], 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  probe_start(run.probe);
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer (both CTAs), completion on the leader's full[s]
+      uint32_t g = 0;
+      int last_a = -1, last_b = -1;
+      for (int item = int(pair); item < n_items; item += int(npairs)) {
+        const TcPairCItem it = items[item];
+        const CUtensorMap* am = maps + it.a_map;
+        const CUtensorMap* bm = maps + it.b_map;
+        if (it.a_map != last_a) tmap_acquire(am), last_a = it.a_map;
+        if (it.b_map != last_b) tmap_acquire(bm), last_b = it.b_map;
+        const int ar = it.a_row + 128 * int(rank), br = it.b_row + 128 * int(rank);
+        for (int kb = 0; kb < it.nk; ++kb, ++g) {
+          const uint32_t st = g % kSt;
+          mbar_wait(&empty[st], ((g / kSt) & 1) ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[st], 2u * 4u * kTileBytes);  // both CTAs' A, B hi / lo
+          const uint32_t fb = mapa_shared(&full[st], 0);
+          uint8_t* sp = smem + st * kStageBytes;
+          const int kc = it.k0 + kb * 32;
+          tma_load_3d_pair(sp, am, fb, kc, ar, 0);
+          tma_load_3d_pair(sp + kTileBytes, am, fb, kc, ar, 1);
+          tma_load_3d_pair(sp + 2 * kTileBytes, bm, fb, kc, br, 0);
+          tma_load_3d_pair(sp + 3 * kTileBytes, bm, fb, kc, br, 1);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ---- MMA issuer (leader only)
+      constexpr uint32_t idesc = make_idesc<Kind::TF32>(256, 256);
+      uint32_t g = 0, t = 0;
+      for (int item = int(pair); item < n_items; item += int(npairs), ++t) {
+        const TcPairCItem it = items[item];
+        const uint32_t buf = t & 1, use = t >> 1;
+        mbar_wait(&tempty[buf], (use & 1) ^ 1);  // both CTAs drained this accumulator
+        tc_fence_after();
+        const uint32_t acc = tmem + buf * 256;
+        for (int kb = 0; kb < it.nk; ++kb, ++g) {
+          const uint32_t st = g % kSt;
+          mbar_wait(&full[st], (g / kSt) & 1);
+          tc_fence_after();
+          uint8_t* sp = smem + st * kStageBytes;
+          const uint64_t ahi = make_sdesc_sw128(sp), alo = make_sdesc_sw128(sp + kTileBytes);
+          const uint64_t bhi = make_sdesc_sw128(sp + 2 * kTileBytes), blo = make_sdesc_sw128(sp + 3 * kTileBytes);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 B of K per 128-B swizzle row
+            const uint64_t off = uint64_t(kk * 2);
+            umma_pair_tf32(acc, ahi + off, bhi + off, idesc, (kb | kk) != 0);
+            umma_pair_tf32(acc, ahi + off, blo + off, idesc, 1u);
+            umma_pair_tf32(acc, alo + off, bhi + off, idesc, 1u);
+          }
+          tc_commit_pair(&empty[st], 3);  // both CTAs' stage free once these retire
+        }
+        tc_commit_pair(&tfull[buf], 3);
+      }
+    }
+    __syncwarp();
+  } else {  // ---- epilogue warps 2..5 (both CTAs): rows 128 rank + i of the super tile
+    const int quad = warp & 3;
+    const int i = quad * 32 + lane;
+    const bool cio = warp == 2 && lane == 0;  // the C-slice loader / storer of this CTA
+    const uint32_t tempty_leader0 = mapa_shared(&tempty[0], 0);
+    constexpr int kSl = 2 * kCSlices;  // C slices per item: tile h = 0 then h = 1
+    // slice u of this CTA: slice (u % kCSlices) of tile ((u / kCSlices) % 2) of its (u / kSl)-th item
+    auto load_slice = [&](uint32_t u) {
+      const int item = int(pair + (u / kSl) * npairs);
+      if (item >= n_items) return;
+      const TcPairCItem it2 = items[item];
+      const CUtensorMap* cm = maps + epis[it2.epi].c_map;
+      tmap_acquire(cm);
+      const uint32_t q = u % kCRing;
+      const int hh = int((u / kCSlices) % 2);
+      mbar_expect_tx(&cfull[q], kCSliceBytes);
+      tma_load_2d(ctile + q * (kCSliceBytes / 4), cm, &cfull[q], rank ? it2.out_r[1] : it2.out_r[0],
+                  (hh ? it2.out_c[1] : it2.out_c[0]) + kCSliceRows * int(u % kCSlices));
+    };
+    if (cio)
+      for (uint32_t u = 0; u < kCRing; ++u) load_slice(u);
+    uint32_t t = 0;
+    for (int item = int(pair); item < n_items; item += int(npairs), ++t) {
+      const TcPairCItem it = items[item];
+      const TcEpi ep = epis[it.epi];
+      const uint32_t buf = t & 1, use = t >> 1;
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < 2 * kCSlices; ++c) {  // 32-column chunk c of this CTA's 256 columns
+        float v[32];
+        tmem_ld_32x32b_x32(tmem + buf * 256 + (uint32_t(quad * 32) << 16) + uint32_t(c * 32), v);
+        const uint32_t u2 = kSl * t + c, q = u2 % kCRing;
+        mbar_wait(&cfull[q], (u2 / kCRing) & 1);
+        float* col = ctile + q * (kCSliceBytes / 4) + i;  // slot[j][i] = beta slot[j][i] + alpha D[i][j]
+#pragma unroll
+        for (int uu = 0; uu < 32; ++uu) col[uu * 128] = ep.beta * col[uu * 128] + ep.alpha * v[uu];
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (cio) {  // slice complete: store it, then reuse the slot
+          const int hh = c / kCSlices;
+          tma_store_2d(maps + ep.c_map, ctile + q * (kCSliceBytes / 4), rank ? it.out_r[1] : it.out_r[0],
+                       (hh ? it.out_c[1] : it.out_c[0]) + kCSliceRows * (c % kCSlices));
+          tma_store_commit_and_wait_read();
+          load_slice(u2 + kCRing);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader0 + buf * 8);  // leader's tempty[buf]
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // the peer's TMEM / smem are read by the leader's MMAs until the end
+  probe_stop(run.probe);
+  if (warp == 1) tmem_free_pair<512>(tmem);
+}
+
 }  // namespace spd

@@ -105,7 +105,7 @@ class SPDKFAC(torch.optim.Optimizer):
         self.damping, self.factor_decay = float(damping), float(factor_decay)
         self.factor_update_freq, self.inv_update_freq = int(factor_update_freq), int(inv_update_freq)
         self.batch_averaged = batch_averaged
-        self.perf = perf or default_params()
+        self.perf = perf  # resolved below once the world size is known
         self.device = next(model.parameters()).device
 
         import torch.distributed as dist
@@ -116,6 +116,7 @@ class SPDKFAC(torch.optim.Optimizer):
             from .comm import NcclComm
             comm = NcclComm(self.rank, self.world)
         self.comm = comm
+        self.perf = perf or default_params(self.world)
         # one communicator, one comm stream: every rank issues the same collective sequence
         # (factor all-reduces as fusion groups complete, then in step(): gradient all-reduce and
         # the owners' inverse broadcasts), so no all-reduce ever queues behind a broadcast that
@@ -164,7 +165,8 @@ class SPDKFAC(torch.optim.Optimizer):
             self.bwd_plan = FusionPlan(tuple(tuple(fg[a:b]) for a, b in zip(cuts, cuts[1:]) if b > a), fusion)
         tasks = inverse_tasks(specs)
         if placement == "lbp":
-            self.placement = lbp_place(tasks, self.world, self.perf.inverse, self.perf.bcast, balance=balance)
+            self.placement = lbp_place(tasks, self.world, getattr(self.perf, "placement_inverse", self.perf.inverse),
+                                       self.perf.bcast, balance=balance)
         elif placement == "seq":
             self.placement = seq_place(tasks, self.world)
         else:

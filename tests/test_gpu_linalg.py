@@ -321,3 +321,19 @@ def test_pack_batched_many_rows():
     for d, f, p in zip(dims[::7], fulls[::7], packed[::7]):
         iu = torch.triu_indices(d, d, device="cuda")
         assert torch.equal(p, f[iu[0], iu[1]]), d
+
+
+@pytest.mark.parametrize("pairs", ["1", "0"])
+def test_damped_inverse_update_engines(pairs, monkeypatch):
+    """The blocked inverse with the CTA-pair update engine (SPDKFAC_UPDATE_PAIRS=1: 2x2 super tiles,
+    including diagonal ones whose dead lower block is written) and with single-CTA tiles only."""
+    K = _K()
+    monkeypatch.setenv("SPDKFAC_UPDATE_PAIRS", pairs)
+    rng = np.random.default_rng(123)
+    dims = [1152, 2304, 640]
+    mats = [spd(rng, d) for d in dims]
+    outs = K.damped_inverse_batched([torch.tensor(m, dtype=torch.float32).cuda() for m in mats], 0.1)
+    for m, o in zip(mats, outs):
+        want = O.damped_inverse(m.astype(np.float32).astype(np.float64), 0.1)
+        bound, _ = inverse_bound(m, 0.1, 0)
+        assert relf(o, want) <= max(bound, 8 * cusolver_err(m, 0.1, want))

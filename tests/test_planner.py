@@ -252,3 +252,34 @@ def test_bert_base_linear_shapes():
     assert Counter((m, a, g) for _, m, a, g in s[:-1]) == Counter(
         {(4096, 768, 768): 48, (4096, 768, 3072): 12, (4096, 3072, 768): 12})
     assert s[-1][1:] == (32, 768, 1000)
+
+
+def test_marginal_inverse_model_makes_small_factors_nct(tmp_path):
+    """B200 extension: the batched-inversion marginal model c3 d^3 against the
+    marginal broadcast beta d(d+1)/2 gives a nonzero NCT set; the params file round-trips with the
+    extension keys and reference-format files still read."""
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    from paper_2107_06533_b200.workloads import layer_shapes
+    bc = PM.BcastParams(1.7e-5, 7.3e-12)          # NCCL broadcast fit (P = 2)
+    marg = PM.MarginalInverseParams(1.6e-14)       # ~7 ms for the 108 ResNet-50 factors in one plan
+    thr = PM.nct_threshold(marg, bc)
+    assert thr is not None and 100 < thr < 1000
+    assert PM.nct_threshold(PM.InverseParams(1.36e-4, 9.2e-4), bc) == 1  # exponential: nothing NCT
+    specs = [SPDKFAC._estimate_times(n, a, g) for n, m, a, g in layer_shapes("resnet50", 32)]
+    tasks = P.inverse_tasks(specs)
+    for w in (2, 4, 8):
+        plan = P.lbp_place(tasks, w, marg, bc, balance="dim_cube")
+        dims = {t.tensor_index: t.dim for t in tasks}
+        assert plan.nct and all(dims[i] < thr for i in plan.nct) and all(dims[i] >= thr for i in dims if i not in plan.nct)
+    params = PM.PerfParams(PM.AllReduceParams(2e-5, 8e-12), bc, PM.InverseParams(1.36e-4, 9.2e-4), 4, marg)
+    path = tmp_path / "b200_p4.params"
+    PM.write_params(path, params)
+    back = PM.read_params(path)
+    assert back.marginal == marg and back.placement_inverse == marg and back.fitted_world_size == 4
+    ref = tmp_path / "ref.params"
+    PM.write_params(ref, PM.PerfParams(params.allreduce, bc, params.inverse, 2))
+    assert PM.read_params(ref).marginal is None and PM.read_params(ref).placement_inverse == params.inverse
+    bad = tmp_path / "bad.params"
+    bad.write_text(ref.read_text() + "inverse_model cubic\n")
+    with pytest.raises(ValueError):
+        PM.read_params(bad)
