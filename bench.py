@@ -92,6 +92,8 @@ def parse(argv=None):
     p.add_argument("--clocks", choices=("nvml", "smi", "off"), default="nvml")
     p.add_argument("--timeline", action="store_true", help="diagnostic: per-phase CUDA-event timeline of one eager step")
     p.add_argument("--stats-off", action="store_true", help="no per-launch CUDA events in the timed region (diagnostic)")
+    p.add_argument("--perf-params", default=None,
+                   help="planner cost-model file (perfmodel.read_params); default data/b200_p{N}.params")
     p.add_argument("--optimizer", choices=("spdkfac", "sgd"), default="spdkfac",
                    help="sgd = diagnostic floor (forward/backward + SGD, no K-FAC); never the headline")
     return p.parse_args(argv)
@@ -105,7 +107,11 @@ def make_optimizer(a, model, world):
     fusion, placement = SCHEMES[a.scheme]
     if a.scheme == "spdkfac":
         placement = a.placement
-    return SPDKFAC(model, lr=a.lr, damping=a.damping, factor_update_freq=a.factor_freq,
+    perf = None
+    if getattr(a, "perf_params", None):
+        from paper_2107_06533_b200.perfmodel import read_params
+        perf = read_params(a.perf_params)
+    return SPDKFAC(model, lr=a.lr, damping=a.damping, factor_update_freq=a.factor_freq, perf=perf,
                    inv_update_freq=a.inv_freq, placement=placement, balance=a.balance,
                    fusion=FusionPolicy(fusion),
                    early_g_fraction=tuple(float(f) for f in a.g_fractions.split(",")), launch_groups=a.launch_groups,
@@ -114,8 +120,9 @@ def make_optimizer(a, model, world):
 
 def workload_config(a, world):
     idx = {"resnet20": "0", "resnet50": "1" if world == 1 else "2", "densenet201": "3",
-           "bert_base_linears": "4"}.get(a.model)
-    data = {"resnet20": "32x32", "bert_base_linears": "seq128 x 768 token embeddings"}.get(a.model, "224x224")
+           "bert_base_linears": "4", "inceptionv4": "4"}.get(a.model)
+    data = {"resnet20": "32x32", "bert_base_linears": "seq128 x 768 token embeddings",
+            "inceptionv4": "299x299"}.get(a.model, "224x224")
     return {"workload": f"{a.model} SPD-KFAC bs{a.batch}/GPU synthetic {data}"
                         + (f" (BASELINE.json configs[{idx}])" if idx else " (not a BASELINE.json config)"),
             "per_gpu_batch": a.batch, "global_batch": a.batch * world, "damping": a.damping, "lr": a.lr,
@@ -679,6 +686,9 @@ def run_ours(a):
                "roofline_kernels": kern, "iteration_roofline": iteration_roofline, "peaks_measured": measured_peaks,
                "cpu_baseline": cpu, "clocks": clk, "kernel_breakdown": breakdown,
                "placement_imbalance": _imbalance(opt) if opt.placement is not None else None,
+               "placement_nct_tensors": len(opt.placement.nct) if opt.placement is not None and world > 1 else None,
+               "perf_params": (a.perf_params or "data/b200_p{N}.params (perfmodel.default_params)")
+               if a.optimizer == "spdkfac" else None,
                "host_wall_ms_per_step": round(wall_ms, 3), "per_step_ms": per_step, "allocator_in_region": alloc_diag,
                "host_phase_ms_fwd_bwd_step": host_phases[a.warmup:a.warmup + a.steps] if a.profile is False else None,
                "final_loss": final_loss, "timeline_ms": timeline}

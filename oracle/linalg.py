@@ -125,19 +125,23 @@ def unpack_upper(arr, d: int) -> np.ndarray:
 # the reference and stated in DESIGN.md.
 
 
-def im2col_rows(x, kh: int, kw: int, stride: int = 1, pad: int = 0, dil: int = 1) -> np.ndarray:
-    """[B, C, H, W] -> [B*Ho*Wo, C*kh*kw] patch rows (zero padding)."""
+def im2col_rows(x, kh: int, kw: int, stride=1, pad=0, dil=1) -> np.ndarray:
+    """[B, C, H, W] -> [B*Ho*Wo, C*kh*kw] patch rows (zero padding); stride / pad / dil are ints
+    or (h, w) pairs (Inception's 1x7 / 7x1 kernels pad one axis only)."""
     x = np.asarray(x, dtype=np.float64)
     b, c, h, w = x.shape
-    ho = (h + 2 * pad - dil * (kh - 1) - 1) // stride + 1
-    wo = (w + 2 * pad - dil * (kw - 1) - 1) // stride + 1
-    xp = np.zeros((b, c, h + 2 * pad, w + 2 * pad))
-    xp[:, :, pad:pad + h, pad:pad + w] = x
+    sh, sw = (stride, stride) if np.isscalar(stride) else stride
+    ph, pw = (pad, pad) if np.isscalar(pad) else pad
+    dh, dw = (dil, dil) if np.isscalar(dil) else dil
+    ho = (h + 2 * ph - dh * (kh - 1) - 1) // sh + 1
+    wo = (w + 2 * pw - dw * (kw - 1) - 1) // sw + 1
+    xp = np.zeros((b, c, h + 2 * ph, w + 2 * pw))
+    xp[:, :, ph:ph + h, pw:pw + w] = x
     cols = np.empty((b, c, kh, kw, ho, wo))
     for i in range(kh):
         for j in range(kw):
-            hs, ws = i * dil, j * dil
-            cols[:, :, i, j] = xp[:, :, hs:hs + stride * (ho - 1) + 1:stride, ws:ws + stride * (wo - 1) + 1:stride]
+            hs, ws = i * dh, j * dw
+            cols[:, :, i, j] = xp[:, :, hs:hs + sh * (ho - 1) + 1:sh, ws:ws + sw * (wo - 1) + 1:sw]
     return cols.reshape(b, c * kh * kw, ho * wo).transpose(0, 2, 1).reshape(b * ho * wo, c * kh * kw)
 
 

@@ -5,7 +5,8 @@ configs[0]  ResNet-20-style CIFAR net, 32x32, single worker (CPU reference runs 
 configs[1]  torchvision ResNet-50 v1.5, bs32/GPU, 224x224          (the bench workload)
 configs[2]  same at 2/4/8 GPUs (fused factor all-reduce + LBP inverses)
 configs[3]  DenseNet-201 (torchvision), bs16
-configs[4]  BERT-base linears: `bert_base_linears`, the 72 encoder linears of BERT-base at their
+configs[4]  Inception-v4 (`inceptionv4`, bs16, 299x299: 150 layers, non-square 1x7 / 7x1 kernels) and
+            BERT-base linears: `bert_base_linears`, the 72 encoder linears of BERT-base at their
             real shapes (bs32 x seq128 = 4096 rows each) in a synthetic attention-free stack
 """
 
@@ -92,6 +93,76 @@ class BertBaseLinears(nn.Module):
 BERT_SEQ = 128
 
 
+class _CBR(nn.Sequential):
+    """conv (no bias) + BatchNorm + ReLU, the Inception unit; kernel / padding may be non-square."""
+
+    def __init__(self, cin, cout, k, stride=1, pad=0):
+        kk = k if isinstance(k, tuple) else (k, k)
+        pp = pad if isinstance(pad, tuple) else (pad, pad)
+        super().__init__(nn.Conv2d(cin, cout, kk, stride, pp, bias=False), nn.BatchNorm2d(cout, eps=1e-3),
+                         nn.ReLU(inplace=False))
+
+
+class _Branches(nn.Module):
+    def __init__(self, *branches):
+        super().__init__()
+        self.b = nn.ModuleList(branches)
+
+    def forward(self, x):
+        return torch.cat([b(x) for b in self.b], 1)
+
+
+class _Split(nn.Module):  # x -> cat(a(x), b(x)): the 1x3 / 3x1 pairs of Inception-C
+    def __init__(self, a, b):
+        super().__init__()
+        self.a, self.b = a, b
+
+    def forward(self, x):
+        return torch.cat([self.a(x), self.b(x)], 1)
+
+
+class InceptionV4(nn.Module):
+    """Inception-v4 (Szegedy et al. 2016) on 299x299 inputs: the 149 convolutions + fc whose K-FAC
+    factor dims the reference enumerates (profiles.py:346-405: 300 tensors, d 27..3456), including the
+    non-square 1x7 / 7x1 / 1x3 / 3x1 kernels.  BASELINE.json configs[4]."""
+
+    def __init__(self, num_classes=1000):
+        super().__init__()
+        C = _CBR
+        mx = lambda: nn.MaxPool2d(3, 2)  # noqa: E731
+        av = lambda: nn.AvgPool2d(3, 1, 1, count_include_pad=False)  # noqa: E731
+        self.stem = nn.Sequential(
+            C(3, 32, 3, 2), C(32, 32, 3), C(32, 64, 3, 1, 1),
+            _Branches(mx(), C(64, 96, 3, 2)),                                                   # mixed3a: 160
+            _Branches(nn.Sequential(C(160, 64, 1), C(64, 96, 3)),                                # mixed4a: 192
+                      nn.Sequential(C(160, 64, 1), C(64, 64, (1, 7), 1, (0, 3)), C(64, 64, (7, 1), 1, (3, 0)),
+                                    C(64, 96, 3))),
+            _Branches(C(192, 192, 3, 2), mx()))                                                 # mixed5a: 384
+        a = [_Branches(C(384, 96, 1), nn.Sequential(C(384, 64, 1), C(64, 96, 3, 1, 1)),
+                       nn.Sequential(C(384, 64, 1), C(64, 96, 3, 1, 1), C(96, 96, 3, 1, 1)),
+                       nn.Sequential(av(), C(384, 96, 1))) for _ in range(4)]
+        ra = _Branches(C(384, 384, 3, 2), nn.Sequential(C(384, 192, 1), C(192, 224, 3, 1, 1), C(224, 256, 3, 2)), mx())
+        b = [_Branches(C(1024, 384, 1),
+                       nn.Sequential(C(1024, 192, 1), C(192, 224, (1, 7), 1, (0, 3)), C(224, 256, (7, 1), 1, (3, 0))),
+                       nn.Sequential(C(1024, 192, 1), C(192, 192, (7, 1), 1, (3, 0)), C(192, 224, (1, 7), 1, (0, 3)),
+                                     C(224, 224, (7, 1), 1, (3, 0)), C(224, 256, (1, 7), 1, (0, 3))),
+                       nn.Sequential(av(), C(1024, 128, 1))) for _ in range(7)]
+        rb = _Branches(nn.Sequential(C(1024, 192, 1), C(192, 192, 3, 2)),
+                       nn.Sequential(C(1024, 256, 1), C(256, 256, (1, 7), 1, (0, 3)), C(256, 320, (7, 1), 1, (3, 0)),
+                                     C(320, 320, 3, 2)), mx())
+        c = [_Branches(C(1536, 256, 1),
+                       nn.Sequential(C(1536, 384, 1), _Split(C(384, 256, (1, 3), 1, (0, 1)), C(384, 256, (3, 1), 1, (1, 0)))),
+                       nn.Sequential(C(1536, 384, 1), C(384, 448, (3, 1), 1, (1, 0)), C(448, 512, (1, 3), 1, (0, 1)),
+                                     _Split(C(512, 256, (1, 3), 1, (0, 1)), C(512, 256, (3, 1), 1, (1, 0)))),
+                       nn.Sequential(av(), C(1536, 256, 1))) for _ in range(3)]
+        self.features = nn.Sequential(*a, ra, *b, rb, *c)
+        self.fc = nn.Linear(1536, num_classes, bias=False)
+
+    def forward(self, x):
+        x = self.features(self.stem(x))
+        return self.fc(x.mean(dim=(2, 3)))
+
+
 def build_model(name: str) -> nn.Module:
     import torchvision
     if name == "resnet50":
@@ -104,12 +175,16 @@ def build_model(name: str) -> nn.Module:
         return ResNet20()
     if name == "bert_base_linears":
         return BertBaseLinears()
+    if name == "inceptionv4":
+        return InceptionV4()
     raise ValueError(f"unknown model {name!r}")
 
 
 def input_shape(name: str, batch: int):
     if name == "bert_base_linears":
         return (batch, BERT_SEQ, 768)
+    if name == "inceptionv4":
+        return (batch, 3, 299, 299)
     return (batch, 3, 32, 32) if name == "resnet20" else (batch, 3, 224, 224)
 
 

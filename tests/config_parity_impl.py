@@ -131,7 +131,7 @@ def run_config(model_name: str, batch: int, device="cuda:0", seed: int = 0, warm
         gout = cap.g[l.name].double().cpu().numpy()
         if isinstance(m, nn.Conv2d):
             kh, kw = m.kernel_size
-            a_rows = O.im2col_rows(xin, kh, kw, m.stride[0], m.padding[0], m.dilation[0])
+            a_rows = O.im2col_rows(xin, kh, kw, tuple(m.stride), tuple(m.padding), tuple(m.dilation))
             g_rows = O.conv_grad_rows(gout, scale=batch)
         else:
             a_rows = xin.reshape(-1, m.in_features)

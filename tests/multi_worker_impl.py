@@ -45,8 +45,15 @@ def main():
     x = torch.tensor(xs, dtype=torch.float32, device=dev)
     t = torch.tensor(ts, dtype=torch.float32, device=dev)
     mode = os.environ.get("SPD_PLACEMENT", "lbp")
-    # all-CT calibration: every inverse has one owner and is broadcast (exercises the bcast path)
+    # all-CT calibration: every inverse has one owner and is broadcast (exercises the bcast path);
+    # lbp-nct: the B200 marginal batched-inverse model with a threshold inside the fixture's dims
+    # (d <= 5 replicated on every rank, d = 6 owned + broadcast)
     perf = PerfParams(AllReduceParams(1e-5, 1e-9), BcastParams(1e-9, 1e-12), InverseParams(1.0, 1e-6), world)
+    if mode == "lbp-nct":
+        from paper_2107_06533_b200.perfmodel import MarginalInverseParams
+        perf = PerfParams(perf.allreduce, perf.bcast, perf.inverse, world, MarginalInverseParams(1e-13))
+        mode = "lbp"
+        assert 5 < __import__("paper_2107_06533_b200.perfmodel", fromlist=["x"]).nct_threshold(perf.marginal, perf.bcast) <= 6
     opt = SPDKFAC(model, lr=fx["alpha"], damping=fx["gamma"], placement=mode, perf=perf)
     loss = ((model(x) - t) ** 2).mean()
     loss.backward()
@@ -92,7 +99,7 @@ def main():
     if rank == 0:
         print(json.dumps({"errors": errs, "identical_on_all_ranks": bool(ok.item()), "world": world,
                           "bucket_err": bucket_err, "bucketed": bucketed,
-                          "placement": mode, "nct": sorted(opt.placement.nct),
+                          "placement": os.environ.get("SPD_PLACEMENT", "lbp"), "nct": sorted(opt.placement.nct),
                           "workers": [list(w) for w in opt.placement.workers]}), flush=True)
     opt.comm.close()
     if opt.comm_bc is not None and opt.comm_bc is not opt.comm:

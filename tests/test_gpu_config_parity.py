@@ -29,3 +29,25 @@ def test_config1_resnet50_step_matches_oracle():
     rep = _run("resnet50")
     assert len(rep) == 54
     assert max(r["a"] for r in rep) == 4608
+
+
+def test_config4_inceptionv4_step_matches_oracle():
+    """BASELINE configs[4] Inception-v4 (150 layers, non-square 1x7 / 7x1 / 1x3 / 3x1 kernels) in the
+    bench configuration at batch 4 (the oracle's im2col of bs16 299x299 would take minutes)."""
+    from tests.config_parity_impl import check, run_config
+    rep = run_config("inceptionv4", 4)
+    assert len(rep) == 150
+    bad = check(rep)
+    print("inceptionv4 worst:", {k: max(r[k] for r in rep) for k in ("factor_A", "factor_G", "update", "e2e")})
+    assert not bad, bad
+
+
+def test_config3_densenet201_step_matches_oracle():
+    """BASELINE configs[3] DenseNet-201 (201 layers, 402 factors of d 64..1920: many small factors)
+    in the bench configuration at batch 2."""
+    from tests.config_parity_impl import check, run_config
+    rep = run_config("densenet201", 2)
+    assert len(rep) == 201
+    bad = check(rep)
+    print("densenet201 worst:", {k: max(r[k] for r in rep) for k in ("factor_A", "factor_G", "update", "e2e")})
+    assert not bad, bad

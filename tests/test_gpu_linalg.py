@@ -337,3 +337,29 @@ def test_damped_inverse_update_engines(pairs, monkeypatch):
         want = O.damped_inverse(m.astype(np.float32).astype(np.float64), 0.1)
         bound, _ = inverse_bound(m, 0.1, 0)
         assert relf(o, want) <= max(bound, 8 * cusolver_err(m, 0.1, want))
+
+
+@pytest.mark.parametrize("shape,k,s,p", [((4, 64, 17, 17), (1, 7), (1, 1), (0, 3)), ((4, 64, 17, 17), (7, 1), (1, 1), (3, 0)),
+                                         ((3, 40, 8, 8), (1, 3), (1, 1), (0, 1)), ((3, 40, 8, 8), (3, 1), (1, 1), (1, 0)),
+                                         ((2, 24, 15, 15), (3, 3), (2, 2), (0, 0))])
+@pytest.mark.parametrize("nhwc", [False, True])
+def test_factor_conv_nonsquare_kernels(shape, k, s, p, nhwc):
+    """Inception-v4's non-square kernels with one-axis padding (BASELINE configs[4]), both staging
+    layouts: NCHW (c, kh, kw) column order and channels-last (kh, kw, c)."""
+    K = _K()
+    import paper_2107_06533_b200._lib as L
+    rng = np.random.default_rng(sum(shape) + k[0] * 3 + k[1])
+    x = rng.standard_normal(shape).astype(np.float32)
+    want = O.factor_A(O.im2col_rows(x, k[0], k[1], s, p))
+    if nhwc:
+        xt = torch.tensor(x).cuda().contiguous(memory_format=torch.channels_last)
+        plan = K.FactorPlan(L.CONV_A_NHWC, x.shape, k, s, p)
+        c = shape[1]
+        perm = [ci * k[0] * k[1] + ki * k[1] + kj for ki in range(k[0]) for kj in range(k[1]) for ci in range(c)]
+        want = want[np.ix_(perm, perm)]
+    else:
+        xt = torch.tensor(x).cuda()
+        plan = K.FactorPlan(L.CONV_A, x.shape, k, s, p)
+    packed = torch.empty(plan.packed_size, device="cuda")
+    plan.run(xt, packed)
+    assert relf(K.unpack_upper(packed, plan.dim), want) <= FACTOR_TOL

@@ -25,9 +25,11 @@ def _run(world, placement):
     return json.loads(lines[-1])
 
 
-@pytest.mark.parametrize("placement", ["lbp", "seq", "local"])
+@pytest.mark.parametrize("placement", ["lbp", "seq", "local", "lbp-nct"])
 def test_two_rank_step_matches_centralized(placement):
     r = _run(2, placement)
+    if placement == "lbp-nct":  # replicated (NCT) and owned (CT) inverses in one step
+        assert r["nct"] and len(r["nct"]) < 8, r
     assert r["identical_on_all_ranks"]
     assert max(r["errors"]) <= 1e-4, r
     assert r["bucketed"] and r["bucket_err"] <= 1e-5, r  # gradient bucket during backward == one all-reduce
