@@ -92,7 +92,7 @@ int launch_tc3_pair_ctile(const CUtensorMap* maps, const TcPairCItem* items, con
                           cudaStream_t s, Probe* probe = nullptr);
 // TF32 engine with chunked accumulation (kAccChunk K blocks of 32 per TMEM chunk, chunks summed in
 // fp32 registers): the preconditioning GEMMs (see tc3_gemm_kernel's kAcc)
-constexpr int kAccChunk = 4;
+constexpr int kAccChunk = 2;  // 64 K elements = 24 accumulating MMAs per TMEM chunk
 int launch_tc3_acc(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items, cudaStream_t s,
                    const TcRun& run = TcRun{});
 // 2-D tensor map over a row-major fp32 matrix [rows][ld], box 128 x 128, no swizzle

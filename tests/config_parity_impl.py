@@ -67,10 +67,10 @@ class _Capture:
     def _into(store, name, t):
         t = t.detach()
         buf = store.get(name)
-        if buf is None or buf.shape != t.shape or buf.stride() != t.stride():
+        if buf is None or buf.shape != t.shape:
             assert not torch.cuda.is_current_stream_capturing(), "capture buffers must exist before graph capture"
             buf = store[name] = torch.empty_like(t)
-        buf.copy_(t)
+        buf.copy_(t)  # (autograd may hand over a gradient with other strides under capture: copy_ handles it)
 
     def _pre(self, name):
         def h(m, inp):
