@@ -215,7 +215,7 @@ class Clocks:
 # ---------------------------------------------------------------- CPU reference
 def cpu_reference(model, batch, steps=1, warmup=0):
     """Time the reference's float64 K-FAC algebra (oracle/cpu_step.py) for `steps` full steps; each
-    step times every distinct layer shape once, weighted by multiplicity.  Warm-up runs the
+    step times every layer of the model (each its own call).  Warm-up runs the
     smallest shape (BLAS thread pool, first-touch pages), not a full step."""
     from oracle import cpu_step
     from paper_2107_06533_b200.workloads import layer_shapes
@@ -227,10 +227,9 @@ def cpu_reference(model, batch, steps=1, warmup=0):
     cache = {}
     per_step = [cpu_step.full_step(shapes, cache=cache) for _ in range(max(1, steps))]
     kind = cpu_step.implementation()[4]
-    sample = (f"full step per timed step: {len(keys)} distinct layer shapes of the {len(shapes)} {model} K-FAC layers "
-              f"(bs{batch}), each timed once (factor A+G, 2 damped inverses, precondition, update; float64 "
-              f"numpy/scipy LAPACK) and weighted by multiplicity; im2col and forward/backward not charged; "
-              f"host CPU {cpu_step.cpu_model()}")
+    sample = (f"full step per timed step: all {len(shapes)} {model} K-FAC layers (bs{batch}; {len(keys)} distinct "
+              f"shapes), each layer's factor A+G, 2 damped inverses, precondition and update timed (float64 "
+              f"numpy/scipy LAPACK); im2col and forward/backward not charged; host CPU {cpu_step.cpu_model()}")
     return statistics.mean(per_step) * 1e3, sample, per_step, kind
 
 
@@ -730,7 +729,7 @@ def run_reference(a):
            "per_step_ms": [round(x * 1e3, 1) for x in per_step], "wall_s": round(wall, 1),
            "note": "reference kfacsched is CPU-only numpy/scipy (no GPU path): its own functions from "
                    "baseline/_ref (kind=reference) or the oracle port (kind=port); every timed step is a full "
-                   "step (all distinct layer shapes, weighted by multiplicity) on this rank's host cores"}
+                   "step (every layer of the model) on this rank's host cores"}
     print(json.dumps(out), flush=True)
 
 
