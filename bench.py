@@ -57,6 +57,8 @@ def parse(argv=None):
     p.add_argument("--damping", type=float, default=0.1)
     p.add_argument("--factor-freq", type=int, default=1)
     p.add_argument("--inv-freq", type=int, default=1)
+    p.add_argument("--factor-decay", type=float, default=0.0,
+                   help="running-average weight rho of the factors (0 = the reference's step)")
     p.add_argument("--placement", default="lbp")
     p.add_argument("--balance", choices=("dim_sq", "dim", "dim_cube"), default="dim_cube",
                    help="LBP bucket weight: d^2 / d (the reference's options) or d^3 (inversion arithmetic)")
@@ -112,6 +114,7 @@ def make_optimizer(a, model, world):
         from paper_2107_06533_b200.perfmodel import read_params
         perf = read_params(a.perf_params)
     return SPDKFAC(model, lr=a.lr, damping=a.damping, factor_update_freq=a.factor_freq, perf=perf,
+                   factor_decay=getattr(a, "factor_decay", 0.0),
                    inv_update_freq=a.inv_freq, placement=placement, balance=a.balance,
                    fusion=FusionPolicy(fusion),
                    early_g_fraction=tuple(float(f) for f in a.g_fractions.split(",")), launch_groups=a.launch_groups,
@@ -126,7 +129,7 @@ def workload_config(a, world):
     return {"workload": f"{a.model} SPD-KFAC bs{a.batch}/GPU synthetic {data}"
                         + (f" (BASELINE.json configs[{idx}])" if idx else " (not a BASELINE.json config)"),
             "per_gpu_batch": a.batch, "global_batch": a.batch * world, "damping": a.damping, "lr": a.lr,
-            "factor_update_freq": a.factor_freq, "inv_update_freq": a.inv_freq,
+            "factor_update_freq": a.factor_freq, "inv_update_freq": a.inv_freq, "factor_decay": a.factor_decay,
             "scheme": a.scheme,
             "fusion": SCHEMES[a.scheme][0] if world > 1 or a.launch_groups == "fusion" else
                       "none at P=1 (no factor comm): SYRK launch groups = A in 2 halves, G at the inversion groups",

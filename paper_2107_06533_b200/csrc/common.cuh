@@ -254,6 +254,18 @@ SPD_DEV uint64_t make_sdesc_sw128_mn(const void* smem_tile) {
   return desc;
 }
 
+// the same MN-major layout with an explicit MN-half stride (a 128 x 32 bf16 tile staged by the
+// fp32-rows converters: two 64 x 32 halves of 4 KB)
+SPD_DEV uint64_t make_sdesc_sw128_mn_lbo(const void* smem_tile, uint32_t lbo) {
+  uint64_t addr = (smem_u32(smem_tile) & 0x3FFFFu) >> 4;
+  uint64_t desc = addr;
+  desc |= uint64_t(lbo >> 4) << 16;      // LBO: MN atom stride
+  desc |= uint64_t(1024 >> 4) << 32;     // SBO: 8-row K group stride
+  desc |= uint64_t(1) << 46;             // version
+  desc |= uint64_t(2) << 61;             // SWIZZLE_128B
+  return desc;
+}
+
 template <Kind K>
 SPD_DEV void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
   if constexpr (K == Kind::BF16) {

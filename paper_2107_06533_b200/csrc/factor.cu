@@ -8,6 +8,7 @@
 //   3. reduce + pack : sum split-K partials in fixed order, apply 1/M, running average, 1/P,
 //                      write the packed upper triangle (the all-reduce / fusion-buffer format)
 #include <algorithm>
+#include <cstring>
 
 #include "runtime.cuh"
 
@@ -351,7 +352,25 @@ struct Member {
   float* partial;
   float* chunks;
   int* counters;
+  // fp32-rows members (row layouts: linear inputs, channels-last output gradients, 1x1 stride-1
+  // channels-last conv inputs): the SYRK reads the activation itself (kF32Rows items), no staging
+  bool f32 = false;
+  int f32_slot = -1;        // index in the launch's F32Maps
+  int64_t ldx = 0;          // row stride of x (elements)
+  const float* x = nullptr;  // the activation bound by the last stage()
 };
+
+namespace {
+bool f32_rows_enabled() {  // SPDKFAC_F32_ROWS=0: stage row layouts into bf16 planes as in round 1 (A/B)
+  const char* e = getenv("SPDKFAC_F32_ROWS");
+  return !(e && e[0] == '0');
+}
+bool is_rows_layout(const spdkfac_factor_geom& g) {
+  const bool pointwise = g.layout == SPDKFAC_CONV_A_NHWC && g.kh == 1 && g.kw == 1 && g.stride_h == 1 &&
+                         g.stride_w == 1 && g.pad_h == 0 && g.pad_w == 0;
+  return g.layout == SPDKFAC_ROWS || g.layout == SPDKFAC_SPATIAL_NHWC || pointwise;
+}
+}  // namespace
 
 struct spdkfac_factor_group {
   std::vector<Member> m;
@@ -430,8 +449,10 @@ int member_init(Member* mb, const spdkfac_factor_geom* g) {
   // CTA-pair super tiles where they pay (measured on B200, ResNet-50 shapes): an even number
   // of 128-blocks (no padded half super tile) and at least ~48 pair items to fill the GPU,
   // or a two-block factor over very many rows (the stem conv)
+  mb->ldx = g->layout == SPDKFAC_ROWS ? g->w : g->c;
+  mb->f32 = f32_rows_enabled() && is_rows_layout(*g) && mb->ldx % 4 == 0;
   mb->S = 0;
-  if (mb->T >= 2) {
+  if (mb->T >= 2 && !mb->f32) {  // fp32-rows members run on the single-CTA engine (its converter warps)
     const int S = mb->T / 2, units = S * (S + 1) / 2;
     const int sp = choose_splits(mb->Mpad, units, 74);
     if ((mb->T % 2 == 0 && mb->T >= 4 && units * sp >= 48) || (mb->T == 2 && M >= 200000)) mb->S = S;
@@ -448,8 +469,10 @@ int member_init(Member* mb, const spdkfac_factor_geom* g) {
 // carve one group's workspace (c.base == nullptr: size only)
 void group_carve(spdkfac_factor_group* G, Carve& c) {
   int items = 0, pitems = 0, jobs = 0;
+  int f32 = 0;
   for (Member& mb : G->m) {
-    mb.xt = c.take<__nv_bfloat16>(size_t(2) * mb.M * mb.ld);
+    mb.xt = mb.f32 ? nullptr : c.take<__nv_bfloat16>(size_t(2) * mb.M * mb.ld);
+    mb.f32_slot = mb.f32 ? f32++ : -1;
     if (mb.splits > 1) {
       mb.partial = c.take<float>(size_t(mb.n_tiles) * mb.splits * 16384);
       mb.chunks = c.take<float>(size_t(mb.n_tiles) * 16 * cdiv(mb.splits, kChunk) * 1024);
@@ -488,8 +511,14 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
   G->flops_single = G->flops_pair = 0;
   for (int k = 0; k < n; ++k) {
     Member& mb = G->m[k];
-    int rc = make_operand_map_mn(&maps[k], mb.xt, mb.ld, mb.M);
-    if (rc) return rc;
+    if (!mb.f32) {  // staged bf16 planes (fp32-rows members get their map at compute time)
+      int rc = make_operand_map_mn(&maps[k], mb.xt, mb.ld, mb.M);
+      if (rc) return rc;
+    } else {
+      SPD_ARG(mb.f32_slot < kMaxF32Maps, SPDKFAC_ERR_ARG, "too many fp32-rows members in one factor group (%d)",
+              mb.f32_slot + 1);
+      std::memset(&maps[k], 0, sizeof(CUtensorMap));
+    }
     G->flops += double(mb.M) * mb.d * (mb.d + 1);
     (mb.S ? G->flops_pair : G->flops_single) += double(mb.M) * mb.d * (mb.d + 1);
     const int64_t nkb = mb.Mpad / 64, per = cdiv(nkb, mb.splits);
@@ -540,14 +569,14 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
         for (int I = 0; I < mb.T; ++I)
           for (int J = I; J < mb.T; ++J) {
             TcItem it{};
-            it.a_map = k;
-            it.b_map = k;
+            it.a_map = mb.f32 ? mb.f32_slot : k;
+            it.b_map = mb.f32 ? mb.f32_slot : k;
             it.a_row = I * 128;
             it.b_row = J * 128;
             it.k0 = int(kb0 * 64);
-            it.nk = int(kb1 - kb0);
+            it.nk = int(kb1 - kb0) * (mb.f32 ? 2 : 1);  // fp32-rows stages hold 32 K rows
             it.epi = k;
-            it.flags = kMnMajor | (I == J ? kSameAB : 0);
+            it.flags = (mb.f32 ? kF32Rows : kMnMajor) | (I == J ? kSameAB : 0);
             out_of(I, J, it.out_r, it.out_c);
             it.m_valid = valid(I);
             it.n_valid = valid(J);
@@ -580,8 +609,13 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
   return SPDKFAC_OK;
 }
 
-int member_stage(const Member& mb, const float* x, cudaStream_t s) {
+int member_stage(Member& mb, const float* x, cudaStream_t s) {
   const spdkfac_factor_geom& g = mb.g;
+  if (mb.f32) {  // the SYRK reads x itself: bind it (x must stay valid until compute() has run)
+    SPD_ARG((reinterpret_cast<uintptr_t>(x) & 15) == 0, SPDKFAC_ERR_ARG, "factor input must be 16-byte aligned");
+    mb.x = x;
+    return SPDKFAC_OK;
+  }
   Probe* pr = stat_begin(kCatFactorStage, s);
   const bool pointwise = g.layout == SPDKFAC_CONV_A_NHWC && g.kh == 1 && g.kw == 1 && g.stride_h == 1 &&
                          g.stride_w == 1 && g.pad_h == 0 && g.pad_w == 0;
@@ -626,11 +660,24 @@ int group_compute(spdkfac_factor_group* G, float scale, float decay, float world
   // algorithmic work: sum over members of M * d * (d + 1) flops
   TcRun run{packed, G->m.empty() ? 0 : G->m[0].d, scale, decay, world_scale, 0};
   double bytes_single = 0, bytes_pair = 0;
-  for (const Member& mb : G->m) (mb.S ? bytes_pair : bytes_single) += 4.0 * mb.ld * mb.M;
+  for (const Member& mb : G->m) (mb.S ? bytes_pair : bytes_single) += 4.0 * (mb.f32 ? mb.d : mb.ld) * mb.M;
   int rc;
   if (G->n_items) {
-    run.probe = stat_begin(kCatFactorSyrk, s);
-    if ((rc = launch_tc3(Kind::BF16, G->maps, G->items, G->epis, G->n_items, s, run))) return rc;
+    bool any_f32 = false;
+    for (const Member& mb : G->m) any_f32 |= mb.f32;
+    if (any_f32) {  // fp32 row maps of this run's activations, passed by value with the launch
+      F32Maps fm;  // the launch copies it into the kernel parameters
+      for (const Member& mb : G->m) {
+        if (!mb.f32) continue;
+        SPD_ARG(mb.x != nullptr, SPDKFAC_ERR_ARG, "factor member computed before its input was staged");
+        if ((rc = make_rows_map_f32(&fm.m[mb.f32_slot], mb.x, mb.M, mb.d, mb.ldx))) return rc;
+      }
+      run.probe = stat_begin(kCatFactorSyrk, s);
+      if ((rc = launch_tc3_f32(G->maps, G->items, G->epis, G->n_items, s, run, fm))) return rc;
+    } else {
+      run.probe = stat_begin(kCatFactorSyrk, s);
+      if ((rc = launch_tc3(Kind::BF16, G->maps, G->items, G->epis, G->n_items, s, run))) return rc;
+    }
     stat_end(kCatFactorSyrk, s, G->flops_single, bytes_single);
   }
   if (G->n_pitems) {

@@ -63,10 +63,30 @@ struct B8v2Shared {
   int fail[2];
 };
 
+// reciprocal: MUFU approximation + one Newton step (<= 1 ulp); __frcp_rn's IEEE path measured ~1.2k
+// cycles per call inside the 8x8 pivot sweep, the serial core of every pivot block
+__device__ __forceinline__ float rcp_nr1(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r * fmaf(-x, r, 2.f);
+}
+#ifdef SPD_PIVOT_TIMING
+#define B8_MARK(i) \
+  do {             \
+    if (t == 0) { const long long c_ = clock64(); ph[i] += c_ - last; last = c_; } \
+  } while (0)
+#else
+#define B8_MARK(i) \
+  do {             \
+  } while (0)
+#endif
 __device__ __forceinline__ int sweep128_b8v2(float (&a)[2][16], int n, B8v2Shared& sh) {
   const int t = threadIdx.x, r = t & 63, q = t >> 6;
   const int lane = t & 31, warp = t >> 5;
   const int nb = (n + 7) >> 3;
+#ifdef SPD_PIVOT_TIMING
+  long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, last = clock64();
+#endif
   for (int kb = 0; kb < nb; ++kb) {
     const int buf = kb & 1;
     float* Rf = reinterpret_cast<float*>(sh.R[buf]);
@@ -79,20 +99,20 @@ __device__ __forceinline__ int sweep128_b8v2(float (&a)[2][16], int n, B8v2Share
         for (int jj = 0; jj < 16; ++jj) Rf[(q * 16 + jj) * 8 + s0] = a[u][jj];
       }
     }
+    B8_MARK(0);
     __syncthreads();
+    B8_MARK(1);
     if (warp < 4) {
       if (warp == 0) {  // lane holds S[rr][c] and S[rr][c + 4]
         const int rr = lane >> 2, c = lane & 3;
         float v0 = Rf[(K0 + c) * 8 + rr], v1 = Rf[(K0 + c + 4) * 8 + rr];
         int fail = -1;
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
+        for (int p = 0; p < 8; ++p) {  // branch-free: a `break` here made every shuffle of the sweep
+          // take the compiler's divergent-collective path (WARPSYNC loops), ~9k cycles per 8x8 sweep
           const float pv = __shfl_sync(0xffffffffu, (p < 4) ? v0 : v1, (p << 2) | (p & 3));
-          if (!(pv > 0.f)) {
-            fail = p;
-            break;
-          }
-          const float pinv = __frcp_rn(pv);
+          if (fail < 0 && !(pv > 0.f)) fail = p;  // warp-uniform; later pivots compute garbage, unused
+          const float pinv = rcp_nr1(pv);
           const float rp0 = __shfl_sync(0xffffffffu, v0, (p << 2) | c);
           const float rp1 = __shfl_sync(0xffffffffu, v1, (p << 2) | c);
           const float cp = __shfl_sync(0xffffffffu, (p < 4) ? v0 : v1, (rr << 2) | (p & 3));
@@ -110,7 +130,9 @@ __device__ __forceinline__ int sweep128_b8v2(float (&a)[2][16], int n, B8v2Share
         sh.S[rr][c + 4] = v1;
         if (lane == 0) sh.fail[buf] = fail;
       }
+      B8_MARK(2);
       named_bar_sync(1, 128);
+      B8_MARK(3);
       const int i = t;  // row weights for row i = t (128 threads)
       const int s0 = i - K0;
       float w[8];
@@ -131,7 +153,9 @@ __device__ __forceinline__ int sweep128_b8v2(float (&a)[2][16], int n, B8v2Share
       sh.W[buf][i][0] = make_float4(w[0], w[1], w[2], w[3]);
       sh.W[buf][i][1] = make_float4(w[4], w[5], w[6], w[7]);
     }
+    B8_MARK(4);
     __syncthreads();
+    B8_MARK(5);
     const int f = sh.fail[buf];
     if (f >= 0) return K0 + f;
     float w[2][8];
@@ -174,7 +198,13 @@ __device__ __forceinline__ int sweep128_b8v2(float (&a)[2][16], int n, B8v2Share
           for (int cc = 0; cc < 8; ++cc) a[u][8 + cc] = w[u][cc];
       }
     }
+    B8_MARK(6);
   }
+#ifdef SPD_PIVOT_TIMING
+  if (t == 0 && blockIdx.x == 0)
+    printf("b8 sweep phases (cycles over %d steps): write-R %lld sync1 %lld sweep8x8 %lld nbar %lld weights %lld sync2 %lld update %lld\n",
+           nb, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[6]);
+#endif
   return -1;
 }
 

@@ -134,6 +134,22 @@ int make_operand_map_mn(CUtensorMap* out, const void* base, int64_t ld, int64_t 
   return SPDKFAC_OK;
 }
 
+int make_rows_map_f32(CUtensorMap* out, const float* base, int64_t rows, int64_t cols, int64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  SPD_ARG(fn != nullptr, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  SPD_ARG((ld * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0, SPDKFAC_ERR_ARG,
+          "tensor map: misaligned fp32 rows");
+  cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(ld * 4)};
+  cuuint32_t box[2] = {128, kF32Bk};  // 128 MN columns x 32 K rows, unswizzled (the converters read it)
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SPD_ARG(r == CUDA_SUCCESS, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled (fp32 rows) failed (%d)", int(r));
+  return SPDKFAC_OK;
+}
+
 // Grid policy of the tile engines: persistent (<= one CTA per SM, static round robin over the
 // work items) or one CTA per work item (SPDKFAC_GRID=tiles): CTAs then retire tile by tile,
 // so kernels of concurrent streams (the forward/backward convolutions) get SMs as soon as a
@@ -147,13 +163,13 @@ static bool tile_grid() {
   return mode == 1;
 }
 
-template <Kind K, int kSt, bool kCTile, int kAcc = 0>
+template <Kind K, int kSt, bool kCTile, int kAcc = 0, bool kF32 = false>
 static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
-                       const TcRun& run, int max_ctas = 0) {
+                       const TcRun& run, int max_ctas = 0, const F32Param<kF32>* fm = nullptr) {
   constexpr size_t smem = tc_smem_bytes<kSt>(kCTile);
   static bool attr_set = false;
   if (!attr_set) {
-    SPD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<K, kSt, kCTile, kAcc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SPD_CUDA(cudaFuncSetAttribute(tc3_gemm_kernel<K, kSt, kCTile, kAcc, kF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(smem)));
     attr_set = true;
   }
@@ -171,7 +187,10 @@ static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi
   int cap = sms;
   if (max_ctas > 0 && max_ctas < cap) cap = max_ctas;
   const int grid = (tile_grid() || n < cap) ? n : cap;
-  tc3_gemm_kernel<K, kSt, kCTile, kAcc><<<grid, 192, smem, s>>>(maps, items, epis, run, n);
+  if constexpr (kF32)
+    tc3_gemm_kernel<K, kSt, kCTile, kAcc, true><<<grid, 320, smem, s>>>(maps, items, epis, run, n, *fm);
+  else
+    tc3_gemm_kernel<K, kSt, kCTile, kAcc, false><<<grid, 192, smem, s>>>(maps, items, epis, run, n, NoF32Maps{});
   SPD_CHECK_LAUNCH();
   return SPDKFAC_OK;
 }
@@ -181,6 +200,12 @@ int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const Tc
   if (n <= 0) return SPDKFAC_OK;
   return kind == Kind::BF16 ? launch_kind<Kind::BF16, kStages, false>(maps, items, epis, n, s, run, max_ctas)
                             : launch_kind<Kind::TF32, kStages, false>(maps, items, epis, n, s, run, max_ctas);
+}
+
+int launch_tc3_f32(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
+                   const TcRun& run, const F32Maps& fm) {
+  if (n <= 0) return SPDKFAC_OK;
+  return launch_kind<Kind::BF16, kStages, false, 0, true>(maps, items, epis, n, s, run, 0, &fm);
 }
 
 int launch_tc3_acc(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,

@@ -64,6 +64,9 @@ int make_operand_map(CUtensorMap* out, const void* base, bool bf16, int64_t k_ex
 // MN-major bf16 split planes [2][k_rows][ld] (box 64 x 64, SWIZZLE_128B; items flagged kMnMajor)
 int make_operand_map_mn(CUtensorMap* out, const void* base, int64_t ld, int64_t k_rows);
 
+// 2-D map over fp32 rows [rows][cols] (row stride ld), box 128 columns x kF32Bk rows, no swizzle
+int make_rows_map_f32(CUtensorMap* out, const float* base, int64_t rows, int64_t cols, int64_t ld);
+
 // Upload `n` POD objects into device memory `dst` on `stream` (pageable source: the
 // copy consumes the host buffer before returning).
 template <class T>
@@ -81,6 +84,9 @@ struct PtrTable {
 
 int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items,
                cudaStream_t s, const TcRun& run = TcRun{}, int max_ctas = 0);
+// BF16 SYRK engine whose kF32Rows items read fp32 rows through the tensor maps in `fm` (converter warps)
+int launch_tc3_f32(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items, cudaStream_t s,
+                   const TcRun& run, const F32Maps& fm);
 // TF32 engine with a TMA-staged fp32 C tile (read-modify-write targets, TcEpi::c_map)
 // CTA-pair SYRK engine (cta_group::2, 256 x 256 super tiles; bf16 MN-major split planes)
 int launch_tc3_pair(const CUtensorMap* maps, const TcPairItem* items, const TcEpi* epis, int n_items, cudaStream_t s,

@@ -10,6 +10,8 @@
 //   Kind::TF32 (kind::tf32, tf32 planes): |x - hi - lo| <= 2^-22|x|  (inverse updates)
 // One TMA producer lane, one MMA-issuing lane, all four warps drain TMEM in the epilogue.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace spd {
@@ -34,6 +36,10 @@ constexpr int32_t kSameAB = 1;  // B tile == A tile (diagonal SYRK tile): load o
 constexpr int32_t kMirror = 2;  // also update target (out_r + i, out_c + j) (symmetric off-diagonal tile)
 constexpr int32_t kMnMajor = 8;  // operands are MN-major split planes [2][K][ld] (bf16 only): each
                                  // 16-KB tile is two 64(MN) x 64(K) TMA boxes at (row, k), (row + 64, k)
+constexpr int32_t kF32Rows = 16;  // (kF32 engines) operands are fp32 rows [M][d] read straight from the
+                                 // activations by TMA (tensor maps in the F32Maps kernel parameter, a_map /
+                                 // b_map index it); converter warps split them into the bf16 hi/lo MN-major
+                                 // planes per K block of 32 rows: no staging pass
 constexpr int32_t kOut2Rows = 4;  // out2 row-style: out2[(o2_row + i) * ld2 + j]; else transposed:
                                   // out2[(o2_row + j) * ld2 + i] (coalesced along the TMEM lanes)
 
@@ -45,6 +51,20 @@ enum EpiMode : int32_t {
                      //   P = run.wscale * (run.decay * P + (1 - run.decay) * run.alpha * D), i <= j only
   kUpdate = 4,       // out += run.alpha * D (transposed store; the weight update W -= lr * P)
 };
+
+// fp32-rows operand maps, passed by value (the activation pointers change between runs; a kernel
+// parameter needs no device copy and is captured into CUDA graphs with the launch)
+constexpr int kMaxF32Maps = 40;
+struct F32Maps {
+  CUtensorMap m[kMaxF32Maps];
+};
+struct NoF32Maps {};
+template <bool B>
+using F32Param = typename std::conditional<B, F32Maps, NoF32Maps>::type;
+constexpr uint32_t kF32Bk = 32;                           // K rows per fp32 stage
+constexpr uint32_t kF32Plane = 128 * kF32Bk * 2;          // one bf16 plane of a 128 x 32 tile (8 KB)
+constexpr uint32_t kF32Tile = 128 * kF32Bk * 4;           // one fp32 tile (16 KB)
+static_assert(4 * kF32Plane + 2 * kF32Tile == 4 * 128 * 128, "an fp32-rows stage reuses a bf16 stage's bytes");
 
 // Per-launch arguments (kernel parameters, not table entries): what changes between runs.
 struct TcRun {
@@ -214,11 +234,16 @@ constexpr size_t tc_smem_bytes(bool ctile) {
 // kAcc, each item's K range is cut into chunks of kAcc K blocks, every chunk is accumulated afresh
 // in a TMEM buffer (the two buffers alternate per chunk) and the epilogue warps add the chunks
 // into a 128-float register accumulator per row with round-to-nearest fp32 adds.
-template <Kind K, int kSt, bool kCTile, int kAcc = 0>
-__global__ void __launch_bounds__(192, 1)
+// kF32: four extra warps (6..9) convert kF32Rows items' fp32 tiles to bf16 hi/lo planes in place
+// (the factor SYRK of row-layout members: linear inputs, channels-last output gradients, 1x1 conv
+// inputs); the MMA warp waits on their conv[] barrier instead of the TMA's full[].
+template <Kind K, int kSt, bool kCTile, int kAcc = 0, bool kF32 = false>
+__global__ void __launch_bounds__(kF32 ? 320 : 192, 1)
     tc3_gemm_kernel(const CUtensorMap* __restrict__ maps, const TcItem* __restrict__ items,
-                    const TcEpi* __restrict__ epis, const TcRun run, int n_items) {
+                    const TcEpi* __restrict__ epis, const TcRun run, int n_items,
+                    const __grid_constant__ F32Param<kF32> fm) {
   static_assert(kAcc == 0 || !kCTile, "chunked accumulation is for register epilogues");
+  static_assert(!kF32 || K == Kind::BF16, "fp32-rows operands feed the bf16 SYRK");
   constexpr int BK = (K == Kind::BF16) ? 64 : 32;  // one 128-byte swizzle row of K
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_align1024(smem_raw);
@@ -228,7 +253,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = empty + kSt;  // [2]
   uint64_t* tempty = tfull + 2;   // [2]
   uint64_t* cfull = tempty + 2;     // [kCRing] C slice landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfull + kCRing);
+  uint64_t* conv = cfull + kCRing;  // [kSt] (kF32) converted bf16 planes ready
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(conv + kSt);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -236,6 +262,7 @@ __global__ void __launch_bounds__(192, 1)
     for (int s = 0; s < kSt; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], 4);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -261,6 +288,22 @@ __global__ void __launch_bounds__(192, 1)
       for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
         const TcItem it = items[item];
         const bool same = (it.flags & kSameAB) != 0;
+        if constexpr (kF32) {
+          if (it.flags & kF32Rows) {  // fp32 rows: [32 K rows][128 MN] tiles behind the bf16 planes
+            const CUtensorMap* am = &fm.m[it.a_map];
+            const CUtensorMap* bm = &fm.m[it.b_map];
+            for (int kb = 0; kb < it.nk; ++kb, ++g) {
+              const uint32_t s = g % kSt;
+              mbar_wait(&empty[s], ((g / kSt) & 1) ^ 1);
+              mbar_expect_tx(&full[s], same ? kF32Tile : 2 * kF32Tile);
+              uint8_t* st = smem + s * kStageBytes + 4 * kF32Plane;
+              const int kc = it.k0 + kb * int(kF32Bk);
+              tma_load_2d(st, am, &full[s], it.a_row, kc);
+              if (!same) tma_load_2d(st + kF32Tile, bm, &full[s], it.b_row, kc);
+            }
+            continue;
+          }
+        }
         const CUtensorMap* am = maps + it.a_map;
         const CUtensorMap* bm = maps + it.b_map;
         if (it.a_map != last_a) tmap_acquire(am), last_a = it.a_map;
@@ -312,9 +355,26 @@ __global__ void __launch_bounds__(192, 1)
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
           const uint32_t s = g % kSt;
           const uint32_t first = uint32_t(kb - kb0);  // 0: this chunk starts a fresh accumulator
+          uint8_t* st = smem + s * kStageBytes;
+          if (kF32 && (it.flags & kF32Rows)) {  // bf16 planes converted from fp32 rows, 32 K rows
+            mbar_wait(&conv[s], (g / kSt) & 1);
+            tc_fence_after();
+            const uint64_t ahi = make_sdesc_sw128_mn_lbo(st, kF32Plane / 2);
+            const uint64_t alo = make_sdesc_sw128_mn_lbo(st + kF32Plane, kF32Plane / 2);
+            const uint64_t bhi = same ? ahi : make_sdesc_sw128_mn_lbo(st + 2 * kF32Plane, kF32Plane / 2);
+            const uint64_t blo = same ? alo : make_sdesc_sw128_mn_lbo(st + 3 * kF32Plane, kF32Plane / 2);
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {  // 16 K rows = two 1024-B atoms per instruction
+              const uint64_t off = uint64_t(kk * (2048 >> 4));
+              umma<K>(acc, ahi + off, bhi + off, idesc_mn, (first | kk) != 0);
+              umma<K>(acc, ahi + off, blo + off, idesc_mn, 1u);
+              umma<K>(acc, alo + off, bhi + off, idesc_mn, 1u);
+            }
+            tc_commit(&empty[s]);
+            continue;
+          }
           mbar_wait(&full[s], (g / kSt) & 1);
           tc_fence_after();
-          uint8_t* st = smem + s * kStageBytes;
           if (K == Kind::BF16 && (it.flags & kMnMajor)) {
             const uint64_t ahi = make_sdesc_sw128_mn(st);
             const uint64_t alo = make_sdesc_sw128_mn(st + kTileBytes);
@@ -343,6 +403,59 @@ __global__ void __launch_bounds__(192, 1)
           tc_commit(&empty[s]);  // smem slot free once these MMAs retire
         }
         tc_commit(&tfull[buf]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (kF32 && warp >= 6) {  // ---- fp32 -> bf16 hi/lo converters (warps 6..9)
+    if constexpr (kF32) {
+      const int ct = int(threadIdx.x) - 192;  // 0..127
+      uint32_t g = 0;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const TcItem it = items[item];
+        if (!(it.flags & kF32Rows)) {  // keep conv[s]'s phases in step with the slot's uses: arrive once
+          for (int kb = 0; kb < it.nk; ++kb, ++g) {  // the TMA data landed (never ahead of the MMA)
+            const uint32_t s = g % kSt;
+            mbar_wait(&full[s], (g / kSt) & 1);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&conv[s]);
+          }
+          continue;
+        }
+        const bool same = (it.flags & kSameAB) != 0;
+        for (int kb = 0; kb < it.nk; ++kb, ++g) {
+          const uint32_t s = g % kSt;
+          mbar_wait(&full[s], (g / kSt) & 1);
+          uint8_t* st = smem + s * kStageBytes;
+          const float* src = reinterpret_cast<const float*>(st + 4 * kF32Plane);
+#pragma unroll 1
+          for (int op = 0; op < (same ? 1 : 2); ++op) {
+            uint8_t* hi = st + 2 * op * kF32Plane;  // A: planes 0, 1; B: planes 2, 3
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {  // 1024 float4 of a [32][128] fp32 tile, 8 per thread
+              const int idx = ct + 128 * u, k = idx >> 5, mn = (idx & 31) << 2;
+              const float4 x = *reinterpret_cast<const float4*>(src + op * (kF32Tile / 4) + k * 128 + mn);
+              __nv_bfloat16 h[4], l[4];
+              split_bf16(x.x, h[0], l[0]);
+              split_bf16(x.y, h[1], l[1]);
+              split_bf16(x.z, h[2], l[2]);
+              split_bf16(x.w, h[3], l[3]);
+              // MN-major SWIZZLE_128B: half mn / 64 at +4 KB, row k at k * 128 B, 16-B chunk
+              // ((mn % 64) / 8) ^ (k % 8), element (mn % 8) * 2 B
+              const uint32_t off = uint32_t(mn >> 6) * (kF32Plane / 2) + uint32_t(k) * 128u +
+                                   (uint32_t(((mn & 63) >> 3) ^ (k & 7)) << 4) + uint32_t(mn & 7) * 2u;
+              uint2 hv, lv;
+              hv.x = uint32_t(__bfloat16_as_ushort(h[0])) | (uint32_t(__bfloat16_as_ushort(h[1])) << 16);
+              hv.y = uint32_t(__bfloat16_as_ushort(h[2])) | (uint32_t(__bfloat16_as_ushort(h[3])) << 16);
+              lv.x = uint32_t(__bfloat16_as_ushort(l[0])) | (uint32_t(__bfloat16_as_ushort(l[1])) << 16);
+              lv.y = uint32_t(__bfloat16_as_ushort(l[2])) | (uint32_t(__bfloat16_as_ushort(l[3])) << 16);
+              *reinterpret_cast<uint2*>(hi + off) = hv;
+              *reinterpret_cast<uint2*>(hi + kF32Plane + off) = lv;
+            }
+          }
+          fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core's reads
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv[s]);
         }
       }
     }

@@ -462,8 +462,9 @@ class SPDKFAC(torch.optim.Optimizer):
                 ss.wait_event(fg["done"])  # previous iteration's SYRK has consumed the staging buffers
             fg["obj"].stage(fg["member"][l.index], x, ss)
             # an output gradient may be freed once its layer's backward ran (and _prepare may
-            # return a temporary): hold x until step() joins stage_stream (A inputs are saved
-            # for backward anyway, so they are never modified in place)
+            # return a temporary): hold x until step() joins the stage and factor streams (row
+            # layouts are read by the SYRK directly; A inputs are saved for backward anyway, so
+            # they are never modified in place)
             self._stage_refs.append(x)
             fg["seen"] += 1
         else:
@@ -474,6 +475,7 @@ class SPDKFAC(torch.optim.Optimizer):
             if not capturing and l.pending[kind]:
                 main.wait_event(ev_done)
             plan.stage(x, main)
+            self._stage_refs.append(x)  # row layouts are read by the SYRK itself (factor stream)
             ev_staged.record(main)
             fs.wait_event(ev_staged)
             if kind == "A":
@@ -671,11 +673,12 @@ class SPDKFAC(torch.optim.Optimizer):
         self._tl("backward_done", main)
         if factors_now:  # every staged input / output gradient is consumed (a reuse step stages nothing:
             main.wait_stream(self.stage_stream)  # under graph capture the stage stream is then not part of it)
-        self._stage_refs.clear()
         if factors_now:
             main.wait_stream(self.factor_stream)
             self._factor_updates += 1
             self._tl("g_factors_done", main)
+        # row-layout factor inputs are read by the SYRK on the factor stream: release them only now
+        self._stage_refs.clear()
         factors_reduced = None
         if self.world > 1:
             cs = self.comm_stream
