@@ -135,8 +135,11 @@ SPDKFAC_API int spdkfac_factor_group_stage(spdkfac_factor_group* g, int member, 
 SPDKFAC_API int spdkfac_factor_group_compute(spdkfac_factor_group* g, float decay, float world_scale, void* stream);
 SPDKFAC_API void spdkfac_factor_group_destroy(spdkfac_factor_group* g);
 /* Introspection of a group's tile-engine choice for one member (tests and diagnostics):
- * out[0] = 1 if the member runs on the CTA-pair engine (cta_group::2, 256x256 super tiles)
- * else 0, out[1] = split-K slices, out[2] = rows M, out[3] = dim d.  No device work. */
+ * out[0] = engine: 0 = single-CTA engine on staged bf16 planes, 1 = CTA-pair engine (cta_group::2,
+ * 256x256 super tiles), 2 = single-CTA engine reading the fp32 rows itself (opt-in for row layouts,
+ * environment SPDKFAC_F32_ROWS = max 128-blocks: no staging pass; the input must then be 16-byte
+ * aligned and stay valid until compute; at most 40 such members per group, the rest are staged),
+ * out[1] = split-K slices, out[2] = rows M, out[3] = dim d.  No device work. */
 SPDKFAC_API int spdkfac_factor_group_describe(const spdkfac_factor_group* g, int member, int64_t out[4]);
 
 /* ------------------------------------------------------------------ packing

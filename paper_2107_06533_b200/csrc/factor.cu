@@ -361,9 +361,15 @@ struct Member {
 };
 
 namespace {
-bool f32_rows_enabled() {  // SPDKFAC_F32_ROWS=0: stage row layouts into bf16 planes as in round 1 (A/B)
+// Row layouts whose factor has at most f32_rows_max_blocks() 128-blocks skip the staging pass: the SYRK
+// converts TMA-loaded fp32 tiles itself.  Each row block is converted once per tile it feeds (T
+// times) against once by the staging pass, so it can only pay for small T (measured on
+// ResNet-50: all rows members converted in-kernel cost +2.1 ms of SYRK for -1.25 ms of staging; with
+// d <= 256 only, -0.79 ms of staging for +0.65 ms of SYRK, 18.07 vs 18.05 ms per iteration).  Off by
+// default; SPDKFAC_F32_ROWS=n enables it for members of at most n blocks.
+int f32_rows_max_blocks() {
   const char* e = getenv("SPDKFAC_F32_ROWS");
-  return !(e && e[0] == '0');
+  return e ? atoi(e) : 0;
 }
 bool is_rows_layout(const spdkfac_factor_geom& g) {
   const bool pointwise = g.layout == SPDKFAC_CONV_A_NHWC && g.kh == 1 && g.kw == 1 && g.stride_h == 1 &&
@@ -450,7 +456,7 @@ int member_init(Member* mb, const spdkfac_factor_geom* g) {
   // of 128-blocks (no padded half super tile) and at least ~48 pair items to fill the GPU,
   // or a two-block factor over very many rows (the stem conv)
   mb->ldx = g->layout == SPDKFAC_ROWS ? g->w : g->c;
-  mb->f32 = f32_rows_enabled() && is_rows_layout(*g) && mb->ldx % 4 == 0;
+  mb->f32 = mb->T <= f32_rows_max_blocks() && is_rows_layout(*g) && mb->ldx % 4 == 0;
   mb->S = 0;
   if (mb->T >= 2 && !mb->f32) {  // fp32-rows members run on the single-CTA engine (its converter warps)
     const int S = mb->T / 2, units = S * (S + 1) / 2;
@@ -471,6 +477,7 @@ void group_carve(spdkfac_factor_group* G, Carve& c) {
   int items = 0, pitems = 0, jobs = 0;
   int f32 = 0;
   for (Member& mb : G->m) {
+    if (mb.f32 && f32 == kMaxF32Maps) mb.f32 = false;  // the launch carries at most kMaxF32Maps row maps
     mb.xt = mb.f32 ? nullptr : c.take<__nv_bfloat16>(size_t(2) * mb.M * mb.ld);
     mb.f32_slot = mb.f32 ? f32++ : -1;
     if (mb.splits > 1) {
@@ -812,7 +819,7 @@ void spdkfac_factor_group_destroy(spdkfac_factor_group* G) { delete G; }
 int spdkfac_factor_group_describe(const spdkfac_factor_group* G, int member, int64_t out[4]) {
   SPD_ARG(G && out && member >= 0 && member < int(G->m.size()), SPDKFAC_ERR_ARG, "bad describe arguments");
   const Member& mb = G->m[member];
-  out[0] = mb.S ? 1 : 0, out[1] = mb.splits, out[2] = mb.M, out[3] = mb.d;
+  out[0] = mb.S ? 1 : (mb.f32 ? 2 : 0), out[1] = mb.splits, out[2] = mb.M, out[3] = mb.d;
   return SPDKFAC_OK;
 }
 

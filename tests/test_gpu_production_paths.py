@@ -42,7 +42,7 @@ def _describe(group, member=0):
     from paper_2107_06533_b200 import _lib as L
     out = (C.c_int64 * 4)()
     L.check(L.load().spdkfac_factor_group_describe(group._h, member, out), "describe")
-    return {"pair": bool(out[0]), "splits": int(out[1]), "rows": int(out[2]), "dim": int(out[3])}
+    return {"pair": out[0] == 1, "f32_rows": out[0] == 2, "splits": int(out[1]), "rows": int(out[2]), "dim": int(out[3])}
 
 
 def _group(members, dims, rows):
@@ -128,8 +128,64 @@ def test_syrk_stem_spatial_g():
     assert relf(unpack_upper(packed[0], 64), _factor_rows_oracle(rows)) <= TOL
 
 
-def test_mixed_factor_group_one_launch():
-    """Pair-engine and single-CTA members (split and unsplit) reduced by one group compute."""
+_F32_CASES = [("rows", (1000, 100)), ("rows", (333, 36)), ("rows", (31, 256)), ("rows", (5, 4)), ("rows", (77, 252)),
+              ("rows", (100352, 256)), ("spatial", (32, 64, 56, 56)), ("pointwise", (8, 128, 14, 14))]
+
+
+@pytest.mark.parametrize("kind,shape", _F32_CASES)
+@pytest.mark.parametrize("f32", ["2", "0"])
+def test_syrk_f32_rows_engine(kind, shape, f32, monkeypatch):
+    """Row layouts with d <= 256 (linear inputs, channels-last output gradients, 1x1 conv inputs)
+    skip the staging pass: the SYRK's converter warps split TMA-loaded fp32 tiles (engine 2).
+    SPDKFAC_F32_ROWS=0 stages them as in round 1 (engine 0).  Both against float64: ragged M
+    (< one 32-row K block, not a multiple of 64), d not a multiple of 128, many split-K slices."""
+    from paper_2107_06533_b200 import _lib as L
+    from paper_2107_06533_b200.linalg import unpack_upper
+    monkeypatch.setenv("SPDKFAC_F32_ROWS", f32)
+    g = torch.Generator(device="cuda").manual_seed(sum(shape))
+    if kind == "rows":
+        x = torch.relu(torch.randn(*shape, device="cuda", generator=g) + 0.3)
+        member, rows = _rows_member(*shape), x
+    else:
+        x = torch.randn(*shape, device="cuda", generator=g).contiguous(memory_format=torch.channels_last)
+        layout = L.SPATIAL_NHWC if kind == "spatial" else L.CONV_A_NHWC
+        member = (layout, tuple(x.shape), (1, 1), (1, 1), (0, 0), (1, 1))
+        rows = x.permute(0, 2, 3, 1).reshape(-1, shape[1])
+    m, d = rows.shape
+    grp, packed = _group([member], [d], [m])
+    info = _describe(grp)
+    assert info["f32_rows"] == (f32 != "0") and not info["pair"], info
+    grp.stage(0, x)
+    grp.compute()
+    first = packed[0].clone()
+    grp.stage(0, x)
+    grp.compute()
+    torch.cuda.synchronize()
+    assert torch.equal(first, packed[0])
+    assert relf(unpack_upper(packed[0], d), _factor_rows_oracle(rows)) <= TOL
+
+
+def test_f32_rows_members_beyond_launch_limit_are_staged(monkeypatch):
+    """A factor group launch carries at most 40 fp32 row maps (Inception-v4's groups hold more row
+    members): the members beyond it are staged instead, in the same launch."""
+    from paper_2107_06533_b200.linalg import unpack_upper
+    monkeypatch.setenv("SPDKFAC_F32_ROWS", "2")
+    shapes = [(64 + 7 * k, 32 + 4 * (k % 5)) for k in range(45)]
+    xs = [_correlated_rows(m, d, seed=k) for k, (m, d) in enumerate(shapes)]
+    grp, packed = _group([_rows_member(m, d) for m, d in shapes], [d for _, d in shapes], [m for m, _ in shapes])
+    eng = [_describe(grp, k)["f32_rows"] for k in range(len(shapes))]
+    assert eng == [True] * 40 + [False] * 5, eng
+    for k, x in enumerate(xs):
+        grp.stage(k, x)
+    grp.compute()
+    for k, x in enumerate(xs):
+        assert relf(unpack_upper(packed[k], shapes[k][1]), _factor_rows_oracle(x)) <= TOL, k
+
+
+def test_mixed_factor_group_one_launch(monkeypatch):
+    """Pair-engine, single-CTA staged and single-CTA fp32-rows members (split and unsplit) reduced
+    by one group compute."""
+    monkeypatch.setenv("SPDKFAC_F32_ROWS", "2")
     from paper_2107_06533_b200 import _lib as L
     from paper_2107_06533_b200.linalg import unpack_upper
     shapes = [(6272, 2304), (6272, 256), (1000, 300), (25088, 512), (32, 2048)]
@@ -141,6 +197,7 @@ def test_mixed_factor_group_one_launch():
     grp, packed = _group(members, dims, [m for m, _ in shapes] + [8 * 28 * 28])
     kinds = [_describe(grp, k)["pair"] for k in range(len(members))]
     assert any(kinds) and not all(kinds), kinds
+    assert any(_describe(grp, k)["f32_rows"] for k in range(len(members)))  # (6272, 256): fp32 rows
     for k, x in enumerate(xs + [conv]):
         grp.stage(k, x)
     grp.compute(decay=0.0, world_scale=0.5)
