@@ -320,18 +320,23 @@ def trace_summary(step, path, torch, n=3, comm_tags=None):
 # K-FAC kernel categories timed live in the timed region (libspdkfac stats categories)
 ROOF_CATS = ("factor_stage", "factor_syrk", "inv_pivot", "inv_panel", "inv_update", "precond_gemm")
 # bound and peak of each category: the tensor-core contractions against the measured GEMM peak of
-# the MMA kind they issue (bf16 for the factor SYRK, tf32 for the inverse and the preconditioning),
+# the MMA kind they issue (bf16 for the factor SYRK, f16 for the inverse panel / update, tf32 for the
+# preconditioning),
 # the staging pass against HBM
+_INV_PEAK = "tf32_tflops" if os.environ.get("SPDKFAC_INV_TF32") == "1" else "bf16_tflops_sustained"
+_INV_KIND = "TF32" if os.environ.get("SPDKFAC_INV_TF32") == "1" else "F16"
 _ROOF_SPEC = {"factor_syrk": ("tensor", "bf16_tflops_sustained"),
               "inv_pivot": ("fp32", "fp32_ffma_tflops") if os.environ.get("SPDKFAC_PIVOT") != "tc" else ("tensor", "tf32_tflops"),
-              "inv_panel": ("tensor", "tf32_tflops"), "inv_update": ("tensor", "tf32_tflops"),
+              # the inverse panel / update issue kind::f16 MMAs on scaled fp16 planes (SPDKFAC_INV_TF32=1: tf32)
+              "inv_panel": ("tensor", _INV_PEAK), "inv_update": ("tensor", _INV_PEAK),
               "precond_gemm": ("tensor", "tf32_tflops"), "factor_stage": ("hbm", "hbm_gbs")}
 _KERNEL_NAMES = {"factor_syrk": "tc3_gemm_kernel<BF16> + tc3_pair_kernel (factor SYRK, 3 x bf16, tcgen05)",
                  "inv_pivot": ("pivot_kernel (128-pivot block: 16 rank-8 fp32 FFMA sweeps)"
                                if os.environ.get("SPDKFAC_PIVOT") != "tc" else
                                "pivot_tc_kernel<false> (128-pivot block: warp sweeps + rank-32 tcgen05 updates)"),
-                 "inv_panel": "stage_panel_kernel + tc3_gemm_kernel<TF32> (inverse panel C = W[:,K] P^-1)",
-                 "inv_update": "tc3_gemm_kernel<TF32, C-tile> (inverse trailing update, 3 x tf32)",
+                 "inv_panel": f"stage_panel_kernel + tc3_gemm_kernel<{_INV_KIND}> (inverse panel C = W[:,K] P^-1)",
+                 "inv_update": f"tc3_gemm_kernel<{_INV_KIND}, C-tile> (inverse trailing update, 3 x {_INV_KIND.lower()}"
+                               + (" planes scaled per matrix)" if _INV_KIND == "F16" else ")"),
                  "precond_gemm": "tc3_gemm_kernel<TF32, chunked accumulation> (G^-1 grad A^-1, W -= lr P)",
                  "factor_stage": "stage_rows / stage_im2col / stage_spatial (fp32 -> bf16 hi/lo planes)"}
 

@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #define SPD_DEV __device__ __forceinline__
 
@@ -217,7 +218,9 @@ SPD_DEV void umma_pair_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uin
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-enum class Kind : int { BF16 = 1, TF32 = 2 };
+// the value is the A/B format code of the instruction descriptor
+enum class Kind : int { F16 = 0, BF16 = 1, TF32 = 2 };
+constexpr bool is_16bit(Kind k) { return k == Kind::F16 || k == Kind::BF16; }  // kind::f16, 2-byte elements
 
 // Instruction descriptor (PTX ISA "Instruction descriptor" for .kind::f16/.kind::tf32):
 // [4,6) D fmt (1=f32) | [7,10) A fmt | [10,13) B fmt | [15] A major | [16] B major (0=K)
@@ -268,7 +271,7 @@ SPD_DEV uint64_t make_sdesc_sw128_mn_lbo(const void* smem_tile, uint32_t lbo) {
 
 template <Kind K>
 SPD_DEV void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
-  if constexpr (K == Kind::BF16) {
+  if constexpr (is_16bit(K)) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
@@ -352,6 +355,13 @@ SPD_DEV float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 // x = hi + lo with hi, lo exactly representable in tf32: |x - hi - lo| <= 2^-22 |x|
+// scaled fp16 pair: x * s = hi + lo + r, |r| <= 2^-22 |x s| while |x s| >= 2^-3 (lo normal), else
+// |r| <= 2^-25 (the fp16 subnormal spacing); s is a power of two chosen so that |x s| <= 2^14
+SPD_DEV void split_f16(float x, float s, __half& hi, __half& lo) {
+  const float y = x * s;
+  hi = __float2half_rn(y);
+  lo = __float2half_rn(y - __half2float(hi));
+}
 SPD_DEV void split_tf32(float x, float& hi, float& lo) {
   hi = tf32_rna(x);
   lo = tf32_rna(x - hi);

@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <map>
 #include <tuple>
+#include <type_traits>
 
 #include "runtime.cuh"
 
@@ -34,6 +35,13 @@ constexpr int kSmemLd = kB + 1;  // padded row stride of the shared-memory block
 constexpr int kFuse = 4;                // trailing-update steps fused per W pass (see the update plan)
 constexpr int kPanSlots = 2 * kFuse;    // a group's slots + the next group's look-ahead never alias
 constexpr int kPanCols = kPanSlots * kB;
+// fp16 operand classes of the panel / P^-1 planes (InvMat::scale index; see inv_scale_kernel)
+constexpr int kScInv = 0, kScReg = 1, kScSchur = 2;
+// Accuracy model of the fp16 planes: an entry of class bound B is held to 2^-38 B absolute, so the
+// inverse keeps a normwise error ~ (sigma / gamma) 2^-38 -- fp32-class (<= 2^-22) while max_i (F_ii +
+// gamma) / gamma <= 2^16 (the BASELINE configs: <= 2^10).  Runs with gamma < kF16MinGamma use tf32
+// planes (exponent range of fp32, 2^-22 relative per entry); SPDKFAC_INV_TF32=1 forces them.
+constexpr float kF16MinGamma = 1e-4f;
 
 struct InvMat {
   float* W;          // padded working matrix [dp][dp] (blocked path)
@@ -43,6 +51,7 @@ struct InvMat {
   int32_t d, dp;
   int32_t panel_row0;  // first row of this matrix's panels in the shared panel planes
   int32_t slot;        // index among blocked matrices (row slot*128 of the P^-1 planes)
+  float* scale;        // [4] fp16 operand-class scales (inv_scale_kernel, kScInv / kScReg / kScSchur)
 };
 
 struct TileJob {  // one 64 x 64 tile (I <= J) of a blocked matrix, for unpack/finalize
@@ -73,8 +82,8 @@ __device__ __forceinline__ float rcp_nr1(float x) {
 #ifdef SPD_PIVOT_TIMING
 #define B8_MARK(i) \
   do {             \
-    if (t == 0) { const long long c_ = clock64(); ph[i] += c_ - last; last = c_; } \
-  } while (0)
+    const long long c_ = clock64(); ph[i] += c_ - last; last = c_; \
+  } while (0)  // every thread (no divergence); thread 0 prints
 #else
 #define B8_MARK(i) \
   do {             \
@@ -205,6 +214,167 @@ __device__ __forceinline__ int sweep128_b8v2(float (&a)[2][16], int n, B8v2Share
     printf("b8 sweep phases (cycles over %d steps): write-R %lld sync1 %lld sweep8x8 %lld nbar %lld weights %lld sync2 %lld update %lld\n",
            nb, ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[6]);
 #endif
+  return -1;
+}
+
+// ---- v3: the 8-pivot sweep with the serial part off the bulk update's path.
+// Same arithmetic as sweep128_b8v2 (8x8 block sweep S = -B^-1, row weights w_i = -W[i,K] S,
+// rank-8 update W[i,j] -= w_i W[K,j] with the pivot rows' base zeroed, pivot columns <- w), but
+// R_g is taken from the pivot COLUMNS (W[i, K_g], symmetric) so the two warps that hold group
+// g+1's columns produce everything group g+1 needs while the other 14 warps apply group g's bulk
+// update: they update those 8 columns first, publish them (R_{g+1}), sweep the 8x8 block, form
+// the 128 row weights from their own registers, then finish their other 8 columns.  One block
+// barrier per group instead of three, and the 8x8 sweep (~70 cycles per pivot of shuffle /
+// MUFU latency) overlaps the bulk FFMA work.
+struct B8v3Shared {
+  float4 R[2][128][2];  // R_g[i][s] = W[i][K_g + s]   (buffer g & 1)
+  float4 W[2][128][2];  // row weights of group g
+  float S[8][8];
+  int fail[2];
+};
+
+// 8x8 block B (lane: rr = lane >> 2, c = lane & 3 holds v0 = B[rr][c], v1 = B[rr][c + 4]) -> S =
+// -B^-1 into S; returns the first non-positive pivot (warp-uniform) or -1
+__device__ __forceinline__ int sweep8x8(float v0, float v1, int lane, float (&S)[8][8]) {
+  const int rr = lane >> 2, c = lane & 3;
+  int fail = -1;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {  // branch-free (a `break` makes every shuffle take the divergent path)
+    const float pv = __shfl_sync(0xffffffffu, (p < 4) ? v0 : v1, (p << 2) | (p & 3));
+    if (fail < 0 && !(pv > 0.f)) fail = p;
+    const float pinv = rcp_nr1(pv);
+    const float rp0 = __shfl_sync(0xffffffffu, v0, (p << 2) | c);
+    const float rp1 = __shfl_sync(0xffffffffu, v1, (p << 2) | c);
+    const float cp = __shfl_sync(0xffffffffu, (p < 4) ? v0 : v1, (rr << 2) | (p & 3));
+    float n0, n1;
+    if (rr == p) {
+      n0 = (c == p) ? -pinv : rp0 * pinv;
+      n1 = (c + 4 == p) ? -pinv : rp1 * pinv;
+    } else {
+      n0 = (c == p) ? cp * pinv : fmaf(-cp * pinv, rp0, v0);
+      n1 = (c + 4 == p) ? cp * pinv : fmaf(-cp * pinv, rp1, v1);
+    }
+    v0 = n0, v1 = n1;
+  }
+  S[rr][c] = v0;
+  S[rr][c + 4] = v1;
+  return fail;
+}
+
+// group g's rank-8 update of this thread's columns [8H, 8H + 8) of its 16
+template <int H>
+__device__ __forceinline__ void b8v3_update_half(float (&a)[2][16], const float (&w)[2][8], const bool (&pk)[2],
+                                                 const float4 (*R)[2], int q) {
+#pragma unroll
+  for (int jj = 8 * H; jj < 8 * H + 8; ++jj) {
+    const float4 ra = R[q * 16 + jj][0], rb = R[q * 16 + jj][1];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      float v = pk[u] ? 0.f : a[u][jj];
+      v = fmaf(-w[u][0], ra.x, v);
+      v = fmaf(-w[u][1], ra.y, v);
+      v = fmaf(-w[u][2], ra.z, v);
+      v = fmaf(-w[u][3], ra.w, v);
+      v = fmaf(-w[u][4], rb.x, v);
+      v = fmaf(-w[u][5], rb.y, v);
+      v = fmaf(-w[u][6], rb.z, v);
+      v = fmaf(-w[u][7], rb.w, v);
+      a[u][jj] = v;
+    }
+  }
+}
+
+// group Kn's serial part, run by the two warps holding its columns (half H of their 16):
+// publish R, sweep the 8x8 block (the warp holding rows Kn..Kn+7), form and publish the weights
+template <int H>
+__device__ __forceinline__ void b8v3_pivot_work(const float (&a)[2][16], int Kn, int nb, B8v3Shared& sh, int r,
+                                                int lane, int warp, int qn) {
+  float4(*R)[2] = sh.R[nb];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    R[2 * r + u][0] = make_float4(a[u][8 * H], a[u][8 * H + 1], a[u][8 * H + 2], a[u][8 * H + 3]);
+    R[2 * r + u][1] = make_float4(a[u][8 * H + 4], a[u][8 * H + 5], a[u][8 * H + 6], a[u][8 * H + 7]);
+  }
+  named_bar_sync(1, 64);
+  if (warp == 2 * qn + (Kn >= 64 ? 1 : 0)) {  // rows Kn..Kn+7 live in this warp
+    const float* Rf = reinterpret_cast<const float*>(R);
+    const int rr = lane >> 2, c = lane & 3;
+    const int f = sweep8x8(Rf[(Kn + rr) * 8 + c], Rf[(Kn + rr) * 8 + c + 4], lane, sh.S);
+    if (lane == 0) sh.fail[nb] = f;
+  }
+  named_bar_sync(1, 64);
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int i = 2 * r + u, s0 = i - Kn;
+    float wn[8];
+    if (s0 >= 0 && s0 < 8) {
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) wn[cc] = sh.S[s0][cc];
+    } else {
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        float acc = 0.f;
+#pragma unroll
+        for (int ss = 0; ss < 8; ++ss) acc = fmaf(a[u][8 * H + ss], sh.S[ss][cc], acc);
+        wn[cc] = -acc;
+      }
+    }
+    sh.W[nb][i][0] = make_float4(wn[0], wn[1], wn[2], wn[3]);
+    sh.W[nb][i][1] = make_float4(wn[4], wn[5], wn[6], wn[7]);
+  }
+}
+
+// one group g (P = g & 1); returns the failing pivot of group g+1 or -1
+template <int P>
+__device__ __forceinline__ int b8v3_step(float (&a)[2][16], int g, int ng, B8v3Shared& sh, int r, int q, int lane,
+                                         int warp) {
+  constexpr int H1 = P ^ 1;  // half of the column block holding group g+1
+  const int buf = g & 1, nb = buf ^ 1, K0 = 8 * g, qg = g >> 1, q1 = (g + 1) >> 1;
+  float w[2][8];
+  bool pk[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int i = 2 * r + u;
+    const float4 wa = sh.W[buf][i][0], wb = sh.W[buf][i][1];
+    w[u][0] = wa.x, w[u][1] = wa.y, w[u][2] = wa.z, w[u][3] = wa.w;
+    w[u][4] = wb.x, w[u][5] = wb.y, w[u][6] = wb.z, w[u][7] = wb.w;
+    pk[u] = (i >= K0 && i < K0 + 8);
+  }
+  const float4(*R)[2] = sh.R[buf];
+  b8v3_update_half<H1>(a, w, pk, R, q);
+  const bool next = g + 1 < ng;
+  if (next && q == q1) b8v3_pivot_work<H1>(a, K0 + 8, nb, sh, r, lane, warp, q1);
+  b8v3_update_half<P>(a, w, pk, R, q);
+  if (q == qg) {  // group g's pivot columns (half P of column block qg) <- w
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) a[u][8 * P + cc] = w[u][cc];
+  }
+  __syncthreads();
+  if (next) {
+    const int f = sh.fail[nb];
+    if (f >= 0) return K0 + 8 + f;
+  }
+  return -1;
+}
+
+// -> W[K,K] = -P^-1 in a (the same contract as sweep128_b8v2)
+__device__ __forceinline__ int sweep128_b8v3(float (&a)[2][16], int n, B8v3Shared& sh) {
+  const int t = threadIdx.x, r = t & 63, q = t >> 6, lane = t & 31, warp = t >> 5;
+  const int ng = (n + 7) >> 3;
+  if (q == 0) b8v3_pivot_work<0>(a, 0, 0, sh, r, lane, warp, 0);
+  __syncthreads();
+  if (sh.fail[0] >= 0) return sh.fail[0];
+#pragma unroll 1
+  for (int g = 0; g < ng; g += 2) {
+    int f = b8v3_step<0>(a, g, ng, sh, r, q, lane, warp);
+    if (f >= 0) return f;
+    if (g + 1 < ng) {
+      f = b8v3_step<1>(a, g + 1, ng, sh, r, q, lane, warp);
+      if (f >= 0) return f;
+    }
+  }
   return -1;
 }
 
@@ -393,7 +563,7 @@ __device__ __forceinline__ int sweep32(float (&w)[32], int lane, float* buf) {
 template <bool kSmall>
 __global__ void __launch_bounds__(pvt::kThreads, 1)
     pivot_tc_kernel(const InvMat* __restrict__ mats, const int32_t* __restrict__ ids, int k,
-                    float* __restrict__ pinv_planes, int64_t pinv_plane, float gamma, Probe* probe) {
+                    void* __restrict__ pinv_planes, int64_t pinv_plane, int f16, float gamma, Probe* probe) {
   using namespace pvt;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = smem_align1024(smem_raw);
@@ -578,12 +748,29 @@ __global__ void __launch_bounds__(pvt::kThreads, 1)
       *reinterpret_cast<float4*>(F + i * kFLd + 64 * h + 4 * t) = make_float4(d[4 * t], d[4 * t + 1], d[4 * t + 2], d[4 * t + 3]);
     __syncthreads();
     if constexpr (!kSmall) {  // W[K,K] <- -P^-1 and P^-1 hi / lo planes, whole rows per warp instruction
-      float* ph = pinv_planes + int64_t(m.slot) * kB * kB;
+      const int64_t pbase = int64_t(m.slot) * kB * kB;
+      const float sc = f16 ? m.scale[kScInv] : 1.f;
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         const int row = 16 * warp + r;
         const float4 x = *reinterpret_cast<const float4*>(F + row * kFLd + 4 * lane);
         reinterpret_cast<float4*>(m.W + (K0 + row) * dp + K0)[lane] = x;
+        if (f16) {  // fp16 planes of P^-1 * s
+          __half* ph = static_cast<__half*>(pinv_planes) + pbase + row * kB + 4 * lane;
+          __half h0, l0, h1, l1, h2, l2, h3, l3;
+          split_f16(-x.x, sc, h0, l0);
+          split_f16(-x.y, sc, h1, l1);
+          split_f16(-x.z, sc, h2, l2);
+          split_f16(-x.w, sc, h3, l3);
+          *reinterpret_cast<uint2*>(ph) =
+              make_uint2(uint32_t(__half_as_ushort(h0)) | (uint32_t(__half_as_ushort(h1)) << 16),
+                         uint32_t(__half_as_ushort(h2)) | (uint32_t(__half_as_ushort(h3)) << 16));
+          *reinterpret_cast<uint2*>(ph + pinv_plane) =
+              make_uint2(uint32_t(__half_as_ushort(l0)) | (uint32_t(__half_as_ushort(l1)) << 16),
+                         uint32_t(__half_as_ushort(l2)) | (uint32_t(__half_as_ushort(l3)) << 16));
+          continue;
+        }
+        float* ph = static_cast<float*>(pinv_planes) + pbase;
         float4 hi, lo;
         split_tf32(-x.x, hi.x, lo.x);
         split_tf32(-x.y, hi.y, lo.y);
@@ -617,10 +804,11 @@ __global__ void __launch_bounds__(pvt::kThreads, 1)
 }
 
 // ---------------------------------------------------------------- d <= 128
+template <bool kV3>
 __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __restrict__ mats,
                                                             const int32_t* __restrict__ ids, float gamma,
                                                             Probe* probe) {
-  __shared__ B8v2Shared sh;
+  __shared__ std::conditional_t<kV3, B8v3Shared, B8v2Shared> sh;
   probe_start(probe);
   const InvMat m = mats[ids[blockIdx.x]];
   const int n = m.d;
@@ -635,7 +823,9 @@ __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __rest
       a[u][jj] = (i < n && j < n) ? packed_at(m.in, n, i, j) + (i == j ? gamma : 0.f) : (i == j ? 1.f : 0.f);
     }
   }
-  const int f = sweep128_b8v2(a, n, sh);
+  int f;
+  if constexpr (kV3) f = sweep128_b8v3(a, n, sh);
+  else f = sweep128_b8v2(a, n, sh);
   if (f >= 0) {
     if (threadIdx.x == 0) *m.info = f + 1;
     probe_stop(probe);
@@ -665,7 +855,7 @@ __global__ void __launch_bounds__(512) small_inverse_kernel(const InvMat* __rest
 // 128-block.
 constexpr int kT = 64;  // unpack / finalize tile edge
 __global__ void __launch_bounds__(256) damp_unpack_kernel(const InvMat* __restrict__ mats,
-                                                          const TileJob* __restrict__ jobs, float gamma) {
+                                                          const TileJob* __restrict__ jobs, float gamma, float pad) {
   __shared__ float tile[kT][kT + 1];
   const TileJob jb = jobs[blockIdx.x];
   const InvMat m = mats[jb.mat];
@@ -685,7 +875,7 @@ __global__ void __launch_bounds__(256) damp_unpack_kernel(const InvMat* __restri
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
     const int64_t i = i0 + ty + 4 * u, j = j0 + tx;
-    if (i == j) v[u] = (i < d) ? v[u] + gamma : 1.f;
+    if (i == j) v[u] = (i < d) ? v[u] + gamma : pad;  // padding: decoupled unit (tf32) or gamma (fp16) pivots
     m.W[i * dp + j] = v[u];
     if (mirror) tile[ty + 4 * u][tx] = v[u];
   }
@@ -696,11 +886,48 @@ __global__ void __launch_bounds__(256) damp_unpack_kernel(const InvMat* __restri
   }
 }
 
+// Operand classes of the fp16 planes and their bounds over the whole sweep (F + gamma I with
+// sigma = max(max_i (F_ii + gamma), 1), the 1 covering the identity padding):
+//   kScInv   entries of inverses of principal submatrices (P^-1, panel rows already swept):
+//            |(A_PP^-1)_ij| <= 1 / lambda_min(A_PP) <= 1 / gamma
+//   kScReg   regression blocks A_PP^-1 A_PQ (old panel rows already swept, new panel rows not yet
+//            swept): |.| <= sqrt((A_PP^-1)_ii A_jj) <= sqrt(sigma / gamma)
+//   kScSchur Schur complements (old panel rows not yet swept): |S_ij| <= sqrt(S_ii S_jj) <= sigma
+// Each class gets s = 2^(13 - ceil(log2 bound)), so |x s| <= 2^13 (fp16 max 65504: 8x headroom for
+// rounding) and the split hi + lo keeps every entry to 2^-22 relative or 2^-38 x bound absolute.
+__device__ __forceinline__ float class_scale(float bound) {
+  int e = 0;
+  if (isfinite(bound)) frexpf(bound, &e);  // bound <= 2^e (NaN / inf diagonals: the sweep reports them)
+  e = max(min(e, 76), -100);               // the epilogue's 1 / (s_A s_B) stays finite
+  return ldexpf(1.f, 13 - e);
+}
+__global__ void __launch_bounds__(256) inv_scale_kernel(const InvMat* __restrict__ mats,
+                                                        const int32_t* __restrict__ ids, float gamma) {
+  __shared__ float red[8];
+  const InvMat m = mats[ids[blockIdx.x]];
+  const int64_t d = m.d;
+  float mx = gamma;  // the padding pivots are gamma
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) mx = fmaxf(mx, m.in[i * (2 * d - i + 1) / 2] + gamma);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float sig = red[0];
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) sig = fmaxf(sig, red[w]);
+    m.scale[kScInv] = class_scale(1.f / gamma);
+    m.scale[kScReg] = class_scale(sqrtf(sig / gamma));
+    m.scale[kScSchur] = class_scale(sig);
+    m.scale[3] = sig / gamma;  // the accuracy model's range (diagnostics)
+  }
+}
+
+template <bool kV3>
 __global__ void __launch_bounds__(512) pivot_kernel(const InvMat* __restrict__ mats,
                                                     const int32_t* __restrict__ ids, int k,
-                                                    float* __restrict__ pinv_planes, int64_t pinv_plane,
+                                                    void* __restrict__ pinv_planes, int64_t pinv_plane, int f16,
                                                     Probe* probe) {
-  __shared__ B8v2Shared sh;
+  __shared__ std::conditional_t<kV3, B8v3Shared, B8v2Shared> sh;
   probe_start(probe);
   const InvMat m = mats[ids[blockIdx.x]];
   if (*m.info != 0) {
@@ -719,25 +946,49 @@ __global__ void __launch_bounds__(512) pivot_kernel(const InvMat* __restrict__ m
       a[u][jj] = v.x, a[u][jj + 1] = v.y, a[u][jj + 2] = v.z, a[u][jj + 3] = v.w;
     }
   }
-  const int f = sweep128_b8v2(a, kB, sh);
+  int f;
+  if constexpr (kV3) f = sweep128_b8v3(a, kB, sh);
+  else f = sweep128_b8v2(a, kB, sh);
   if (f >= 0) {
     if (threadIdx.x == 0) *m.info = int(K0) + f + 1;
     probe_stop(probe);
     return;
   }
+  const float sc = f16 ? m.scale[kScInv] : 1.f;
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int i = 2 * r + u;
     float* dst = m.W + (K0 + i) * dp + K0 + q * 16;                           // W[K,K] <- -P^-1
-    float* ph = pinv_planes + (int64_t(m.slot) * kB + i) * kB + q * 16;        // P^-1 hi plane
+    const int64_t po = (int64_t(m.slot) * kB + i) * kB + q * 16;             // P^-1 hi plane
 #pragma unroll
-    for (int jj = 0; jj < 16; jj += 4) {
+    for (int jj = 0; jj < 16; jj += 4)
       *reinterpret_cast<float4*>(dst + jj) = make_float4(a[u][jj], a[u][jj + 1], a[u][jj + 2], a[u][jj + 3]);
-      float h[4], l[4];
+    if (f16) {  // fp16 planes of P^-1 * s (uniform branch)
+      __half* ph = static_cast<__half*>(pinv_planes) + po;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) split_tf32(-a[u][jj + v], h[v], l[v]);
-      *reinterpret_cast<float4*>(ph + jj) = make_float4(h[0], h[1], h[2], h[3]);
-      *reinterpret_cast<float4*>(ph + pinv_plane + jj) = make_float4(l[0], l[1], l[2], l[3]);
+      for (int jj = 0; jj < 16; jj += 8) {
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          __half h0, l0, h1, l1;
+          split_f16(-a[u][jj + 2 * v], sc, h0, l0);
+          split_f16(-a[u][jj + 2 * v + 1], sc, h1, l1);
+          hw[v] = uint32_t(__half_as_ushort(h0)) | (uint32_t(__half_as_ushort(h1)) << 16);
+          lw[v] = uint32_t(__half_as_ushort(l0)) | (uint32_t(__half_as_ushort(l1)) << 16);
+        }
+        *reinterpret_cast<uint4*>(ph + jj) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(ph + pinv_plane + jj) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      }
+    } else {
+      float* ph = static_cast<float*>(pinv_planes) + po;
+#pragma unroll
+      for (int jj = 0; jj < 16; jj += 4) {
+        float h[4], l[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) split_tf32(-a[u][jj + v], h[v], l[v]);
+        *reinterpret_cast<float4*>(ph + jj) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(ph + pinv_plane + jj) = make_float4(l[0], l[1], l[2], l[3]);
+      }
     }
   }
   __syncthreads();
@@ -752,16 +1003,20 @@ struct PanelJob {
 // block triangle of W is maintained, so blocks below the pivot (R > K) are read as
 // W[K, R]^T through a shared-memory transpose.  Block (job, quarter q) writes panel rows
 // [32q, 32q + 32); every thread issues all of its loads before its first store.
+template <bool kF16>  // fp16 planes of x * s (InvMat::scale) instead of tf32 planes
 __global__ void __launch_bounds__(256) stage_panel_kernel(const InvMat* __restrict__ mats,
                                                           const PanelJob* __restrict__ jobs, int k,
-                                                          float* __restrict__ panA, int64_t plane) {
+                                                          void* __restrict__ panA_, int64_t plane) {
+  using PT = std::conditional_t<kF16, __half, float>;
+  PT* panA = static_cast<PT*>(panA_);
   __shared__ float tile[128][33];
   const PanelJob jb = jobs[blockIdx.x];
   const InvMat m = mats[jb.mat];
   if (*m.info != 0) return;
   const int q = blockIdx.y;
   const int64_t dp = m.dp, K0 = int64_t(k) * kB, R0 = int64_t(jb.rb) * kB;
-  float* dst = panA + (int64_t(m.panel_row0) + R0 + 32 * q) * kPanCols;  // panA: slot base
+  PT* dst = panA + (int64_t(m.panel_row0) + R0 + 32 * q) * kPanCols;  // panA: slot base
+  const float sc = kF16 ? m.scale[jb.rb < k ? kScReg : kScSchur] : 1.f;  // swept rows: A_PP^-1 A_PK
   const float* __restrict__ W = m.W;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   if (jb.rb < k) {  // rows R0 + 32q + i, columns K0 + c: 32 x 128 floats, 4 float4 per thread
@@ -774,13 +1029,27 @@ __global__ void __launch_bounds__(256) stage_panel_kernel(const InvMat* __restri
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int e = threadIdx.x + 256 * u, i = e >> 5, c = (e & 31) * 4;
-      float h[4], l[4];
-      split_tf32(v[u].x, h[0], l[0]);
-      split_tf32(v[u].y, h[1], l[1]);
-      split_tf32(v[u].z, h[2], l[2]);
-      split_tf32(v[u].w, h[3], l[3]);
-      *reinterpret_cast<float4*>(dst + i * kPanCols + c) = make_float4(h[0], h[1], h[2], h[3]);
-      *reinterpret_cast<float4*>(dst + plane + i * kPanCols + c) = make_float4(l[0], l[1], l[2], l[3]);
+      if constexpr (kF16) {
+        __half h0, l0, h1, l1, h2, l2, h3, l3;
+        split_f16(v[u].x, sc, h0, l0);
+        split_f16(v[u].y, sc, h1, l1);
+        split_f16(v[u].z, sc, h2, l2);
+        split_f16(v[u].w, sc, h3, l3);
+        *reinterpret_cast<uint2*>(dst + i * kPanCols + c) =
+            make_uint2(uint32_t(__half_as_ushort(h0)) | (uint32_t(__half_as_ushort(h1)) << 16),
+                       uint32_t(__half_as_ushort(h2)) | (uint32_t(__half_as_ushort(h3)) << 16));
+        *reinterpret_cast<uint2*>(dst + plane + i * kPanCols + c) =
+            make_uint2(uint32_t(__half_as_ushort(l0)) | (uint32_t(__half_as_ushort(l1)) << 16),
+                       uint32_t(__half_as_ushort(l2)) | (uint32_t(__half_as_ushort(l3)) << 16));
+      } else {
+        float h[4], l[4];
+        split_tf32(v[u].x, h[0], l[0]);
+        split_tf32(v[u].y, h[1], l[1]);
+        split_tf32(v[u].z, h[2], l[2]);
+        split_tf32(v[u].w, h[3], l[3]);
+        *reinterpret_cast<float4*>(dst + i * kPanCols + c) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(dst + plane + i * kPanCols + c) = make_float4(l[0], l[1], l[2], l[3]);
+      }
     }
   } else {  // panel row 32q + r, column j = W[K0 + j][R0 + 32q + r]
     float v[16];
@@ -792,10 +1061,17 @@ __global__ void __launch_bounds__(256) stage_panel_kernel(const InvMat* __restri
 #pragma unroll
     for (int u = 0; u < 16; ++u) {  // output row r = ty + 8 (u & 3), column j = tx + 32 (u >> 2)
       const int r = ty + 8 * (u & 3), j = tx + 32 * (u >> 2);
-      float h, l;
-      split_tf32(tile[j][r], h, l);
-      dst[r * kPanCols + j] = h;
-      dst[plane + r * kPanCols + j] = l;
+      if constexpr (kF16) {
+        __half h, l;
+        split_f16(tile[j][r], sc, h, l);
+        dst[r * kPanCols + j] = h;
+        dst[plane + r * kPanCols + j] = l;
+      } else {
+        float h, l;
+        split_tf32(tile[j][r], h, l);
+        dst[r * kPanCols + j] = h;
+        dst[plane + r * kPanCols + j] = l;
+      }
     }
   }
 }
@@ -867,6 +1143,10 @@ struct spdkfac_inverse_plan {
   cudaStream_t side = nullptr;  // look-ahead stream: pivot/stage/panel of step k+1
   bool lookahead = true;        // SPDKFAC_NO_LOOKAHEAD=1 serialises (diagnostics)
   bool legacy_pivot = true;     // fp32 FFMA pivot sweep; SPDKFAC_PIVOT=tc: the tcgen05 pivot kernel
+  bool pivot_v3 = true;         // the pipelined 8-pivot sweep; SPDKFAC_PIVOT=b8: round-2 v2 sweep (A/B)
+  // panel / update operands as scaled fp16 planes (kind::f16) for runs with gamma >= kF16MinGamma;
+  // SPDKFAC_INV_TF32=1 (or the CTA-pair update engine) keeps every run on tf32 planes
+  bool f16 = true;
   int panel_ctas = 0;           // grid cap of the panel GEMM (SPDKFAC_PANEL_CTAS; 0 = all SMs: the chain latency wins)
   cudaEvent_t ev_u1 = nullptr, ev_panel = nullptr;
   int32_t* act_ids;             // device, active blocked matrices per step (concatenated)
@@ -875,6 +1155,9 @@ struct spdkfac_inverse_plan {
   int n_tiles;
   CUtensorMap* maps;            // [0] panA, [1] panC, [2] P^-1, [3], [4] unused, [5 + slot] W_slot tiles
   TcItem* items;                // per step: panel GEMM items then update items
+  CUtensorMap* maps16;          // the same over fp16 planes
+  TcItem* items16;              // the same with K blocks of 64 (fp16)
+  TcEpi* epis16;
   TcPairCItem* pitems;          // per step: CTA-pair super tiles of the bulk update (U2)
   std::vector<int> pu_off, pu_cnt;
   std::vector<double> pu_flops;
@@ -941,6 +1224,9 @@ size_t inverse_carve(int n, const int32_t* dims, Carve& c, spdkfac_inverse_plan*
   float* panA = c.take<float>(size_t(2) * std::max<int64_t>(rows, 1) * kPanCols);
   float* panC = c.take<float>(size_t(2) * std::max<int64_t>(rows, 1) * kPanCols);
   float* pinvS = c.take<float>(size_t(2) * std::max(nblk, 1) * kB * kB);
+  float* scales = c.take<float>(size_t(4) * n);
+  if (mats && c.ok())
+    for (int t = 0; t < n; ++t) (*mats)[t].scale = scales + 4 * t;
   auto* dm = c.take<InvMat>(size_t(n));
   auto* sid = c.take<int32_t>(size_t(n));
   auto* bid = c.take<int32_t>(size_t(n));
@@ -948,12 +1234,16 @@ size_t inverse_carve(int n, const int32_t* dims, Carve& c, spdkfac_inverse_plan*
   auto* tj = c.take<TileJob>(size_t(std::max<int64_t>(tiles, 1)));
   auto* pj = c.take<PanelJob>(size_t(std::max<int64_t>(items, 1)));
   auto* mp = c.take<CUtensorMap>(size_t(5 + nblk), 128);
+  auto* mp16 = c.take<CUtensorMap>(size_t(5 + nblk), 128);
   auto* it = c.take<TcItem>(size_t(std::max<int64_t>(items, 1)));
+  auto* it16 = c.take<TcItem>(size_t(std::max<int64_t>(items, 1)));
+  auto* ep16 = c.take<TcEpi>(size_t(1 + kPanSlots) * n);
   auto* pit = c.take<TcPairCItem>(size_t(std::max<int64_t>(items / 4, 1)));
   auto* ep = c.take<TcEpi>(size_t(1 + kPanSlots) * n);
   if (p) {
     p->panA = panA, p->panC = panC, p->pinvS = pinvS, p->mats = dm, p->small_ids = sid, p->blocked_ids = bid;
     p->act_ids = aid, p->tiles = tj, p->pan_jobs = pj, p->maps = mp, p->items = it, p->epis = ep;
+    p->maps16 = mp16, p->items16 = it16, p->epis16 = ep16;
     p->pitems = pit;
     p->plane_rows = rows, p->steps = steps, p->n_tiles = int(tiles);
   }
@@ -978,6 +1268,11 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   auto* p = new spdkfac_inverse_plan();
   p->n = n;
   p->dims.assign(dims, dims + n);
+  {
+    const char* e = getenv("SPDKFAC_INV_TF32");
+    p->f16 = !(e && e[0] == '1') && !update_pairs();
+  }
+  const int bk = 32;  // K elements per 128-byte tf32 operand row (the fp16 item copies hold half as many blocks)
   Carve c(ws, ws_bytes);
   std::vector<InvMat> mats;
   inverse_carve(n, dims, c, p, &mats);
@@ -1005,12 +1300,16 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   p->n_small = int(small.size());
   p->n_blocked = int(blocked.size());
   const int64_t plane = p->plane_rows * kPanCols;
-  std::vector<TcEpi> epis(size_t(1 + kPanSlots) * n);
+  std::vector<TcEpi> epis(size_t(1 + kPanSlots) * n), epis16(epis.size());
   for (int t = 0; t < n; ++t) {
-    epis[t] = TcEpi{mats[t].W, mats[t].dp, 0, -1.f, 1.f, kAxpby, 0, nullptr, 0, 0,
-                    dims[t] > kB ? 5 + mats[t].slot : 0};  // update
-    for (int q = 0; q < kPanSlots; ++q)                   // panel GEMM writing panC slot q
+    const int cm = dims[t] > kB ? 5 + mats[t].slot : 0;
+    epis[t] = TcEpi{mats[t].W, mats[t].dp, 0, -1.f, 1.f, kAxpby, 0, nullptr, 0, 0, cm, 0, nullptr};  // update
+    epis16[t] = TcEpi{mats[t].W, mats[t].dp, 0, -1.f, 1.f, kAxpby, 0, nullptr, 0, 0, cm, 0, mats[t].scale};
+    for (int q = 0; q < kPanSlots; ++q) {  // panel GEMM writing panC slot q
       epis[n + q * n + t] = TcEpi{mats[t].W, mats[t].dp, 0, 1.f, 0.f, kAxpby, 0, p->panC + q * kB, kPanCols, plane};
+      epis16[n + q * n + t] = TcEpi{mats[t].W, mats[t].dp, 0, 1.f, 0.f, kAxpby, 1,
+                                    reinterpret_cast<__half*>(p->panC) + q * kB, kPanCols, plane, 0, 0, mats[t].scale};
+    }
   }
   std::vector<TileJob> tiles;
   for (int t : blocked) {
@@ -1038,7 +1337,7 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
         const int prow = mats[t].panel_row0 + R * kB;
         const int q = k % kPanSlots;  // panel slot of step k
         TcItem it{};
-        it.nk = kB / 32;
+        it.nk = kB / bk;
         it.epi = n + q * n + t;
         it.m_valid = kB;
         it.n_valid = kB;
@@ -1047,12 +1346,12 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
           it.a_map = 2, it.a_row = mats[t].slot * kB, it.k0 = 0;
           it.b_map = 0, it.b_row = prow, it.b_koff = q * kB;
           it.out_r = k * kB, it.out_c = R * kB;
-          it.flags = 0;
+          it.flags = (kScInv << kScaleShiftA) | (kScReg << kScaleShiftB) | (kScInv << kScaleShiftO);
         } else {      // D[i][j] = C_R[i][j] -> W[K0 + j][R0 + i] (row panel), panC row-style
           it.a_map = 0, it.a_row = prow, it.k0 = q * kB;
           it.b_map = 2, it.b_row = mats[t].slot * kB, it.b_koff = -q * kB;
           it.out_r = R * kB, it.out_c = k * kB;
-          it.flags = kOut2Rows;
+          it.flags = kOut2Rows | (kScSchur << kScaleShiftA) | (kScInv << kScaleShiftB) | (kScReg << kScaleShiftO);
         }
         items.push_back(it);
       }
@@ -1104,9 +1403,11 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
           it.a_row = mats[t].panel_row0 + J * kB;
           it.b_row = mats[t].panel_row0 + I * kB;
           it.k0 = (first % kPanSlots) * kB;
-          it.nk = (k - first + 1) * (kB / 32);
+          it.nk = (k - first + 1) * (kB / bk);
           it.epi = t;
-          it.flags = 0;
+          // A = old panel rows J, B = new panel rows I; neither block is a pivot block of steps
+          // first..k (those tiles were written by the panel epilogue), so both keep one class
+          it.flags = ((J < first ? kScReg : kScSchur) << kScaleShiftA) | ((I < first ? kScInv : kScReg) << kScaleShiftB);
           it.out_r = J * kB;
           it.out_c = I * kB;
           it.m_valid = kB;
@@ -1118,7 +1419,7 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     // rest stay single-CTA items
     p->pu_off.push_back(int(pitems.size()));
     p->pu_flops.push_back(0.0);
-    if (update_pairs()) {
+    if (update_pairs()) {  // (tf32 only: the plan then never runs on fp16 planes)
       std::map<std::tuple<int, int, int>, size_t> at;  // (matrix, I, J) -> index in u2v
       for (size_t x = 0; x < u2v.size(); ++x)
         at[{u2v[x].epi, u2v[x].out_c / kB, u2v[x].out_r / kB}] = x;
@@ -1191,31 +1492,40 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     items.insert(items.end(), u1v.begin(), u1v.end());
     items.insert(items.end(), u2v.begin(), u2v.end());
     p->upd_flops.push_back(0.0);
-    for (const TcItem& it : u1v) p->upd_flops.back() += 2.0 * kB * kB * 32 * it.nk;
+    for (const TcItem& it : u1v) p->upd_flops.back() += 2.0 * kB * kB * bk * it.nk;
     p->u2_flops.push_back(0.0);
-    for (const TcItem& it : u2v) p->u2_flops.back() += 2.0 * kB * kB * 32 * it.nk;
+    for (const TcItem& it : u2v) p->u2_flops.back() += 2.0 * kB * kB * bk * it.nk;
     p->u1_cnt.push_back(u1);
     p->upd_cnt.push_back(int(items.size()) - p->upd_off.back());
   }
-  std::vector<CUtensorMap> maps(size_t(5 + p->n_blocked));
+  std::vector<CUtensorMap> maps(size_t(5 + p->n_blocked)), maps16(maps.size());
   int rc = SPDKFAC_OK;
   if (p->n_blocked > 0) {
-    if ((rc = make_operand_map(&maps[0], p->panA, false, kPanCols, p->plane_rows, kPanCols)) ||
+    if ((rc = make_operand_map_f16(&maps16[0], p->panA, kPanCols, p->plane_rows, kPanCols)) ||
+        (rc = make_operand_map_f16(&maps16[1], p->panC, kPanCols, p->plane_rows, kPanCols)) ||
+        (rc = make_operand_map_f16(&maps16[2], p->pinvS, kB, int64_t(p->n_blocked) * kB, kB)) ||
+        (rc = make_operand_map(&maps[0], p->panA, false, kPanCols, p->plane_rows, kPanCols)) ||
         (rc = make_operand_map(&maps[1], p->panC, false, kPanCols, p->plane_rows, kPanCols)) ||
         (rc = make_operand_map(&maps[2], p->pinvS, false, kB, int64_t(p->n_blocked) * kB, kB))) {
       delete p;
       return rc;
     }
     maps[3] = maps[0], maps[4] = maps[1];
+    maps16[3] = maps16[0], maps16[4] = maps16[1];
     for (int t : blocked)
       if ((rc = make_ctile_map(&maps[5 + mats[t].slot], mats[t].W, mats[t].dp, mats[t].dp, mats[t].dp))) {
         delete p;
         return rc;
       }
+    for (int t : blocked) maps16[5 + mats[t].slot] = maps[5 + mats[t].slot];
   }
+  std::vector<TcItem> items16(items);
+  for (TcItem& it : items16) it.nk /= 2;  // K blocks of 64 fp16 elements (tf32: 32)
   if ((rc = upload(p->mats, mats, s)) || (rc = upload(p->small_ids, small, s)) ||
       (rc = upload(p->blocked_ids, blocked, s)) || (rc = upload(p->act_ids, act, s)) ||
       (rc = upload(p->tiles, tiles, s)) || (rc = upload(p->pan_jobs, pan, s)) || (p->n_blocked > 0 && (rc = upload(p->maps, maps, s))) ||
+      (p->n_blocked > 0 && (rc = upload(p->maps16, maps16, s))) || (rc = upload(p->items16, items16, s)) ||
+      (rc = upload(p->epis16, epis16, s)) ||
       (rc = upload(p->items, items, s)) || (rc = upload(p->pitems, pitems, s)) || (rc = upload(p->epis, epis, s))) {
     delete p;
     return rc;
@@ -1229,6 +1539,7 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     // (ResNet-50 fc A, kappa 2e4: inverse error 2.6e-2 vs 5e-3), see DESIGN.md
     const char* pv = getenv("SPDKFAC_PIVOT");
     p->legacy_pivot = !(pv && std::string(pv) == "tc");
+    p->pivot_v3 = !(pv && std::string(pv) == "b8");
   }
   if (p->n_blocked > 0) {
     SPD_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
@@ -1237,7 +1548,8 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   }
   static bool attrs = false;
   if (!attrs) {
-    SPD_CUDA(cudaFuncSetAttribute(small_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kB * kSmemLd * 4));
+    SPD_CUDA(cudaFuncSetAttribute(small_inverse_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kB * kSmemLd * 4));
+    SPD_CUDA(cudaFuncSetAttribute(small_inverse_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kB * kSmemLd * 4));
     SPD_CUDA(cudaFuncSetAttribute(pivot_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pvt::kSmem)));
     SPD_CUDA(cudaFuncSetAttribute(pivot_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pvt::kSmem)));
     attrs = true;
@@ -1252,46 +1564,67 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p->n_small > 0) {
     Probe* pr = stat_begin(kCatInvSmall, s);
-    if (p->legacy_pivot)
-      small_inverse_kernel<<<p->n_small, 512, kB * kSmemLd * 4, s>>>(p->mats, p->small_ids, gamma, pr);
+    if (p->legacy_pivot && p->pivot_v3)
+      small_inverse_kernel<true><<<p->n_small, 512, kB * kSmemLd * 4, s>>>(p->mats, p->small_ids, gamma, pr);
+    else if (p->legacy_pivot)
+      small_inverse_kernel<false><<<p->n_small, 512, kB * kSmemLd * 4, s>>>(p->mats, p->small_ids, gamma, pr);
     else
-      pivot_tc_kernel<true><<<p->n_small, pvt::kThreads, pvt::kSmem, s>>>(p->mats, p->small_ids, 0, nullptr, 0, gamma,
-                                                                          pr);
+      pivot_tc_kernel<true><<<p->n_small, pvt::kThreads, pvt::kSmem, s>>>(p->mats, p->small_ids, 0, nullptr, 0, 0,
+                                                                          gamma, pr);
     SPD_CHECK_LAUNCH();
     stat_end(kCatInvSmall, s, p->small_flops, 0);
   }
   if (p->n_blocked > 0) {
     const int64_t plane = p->plane_rows * kPanCols;
+    // fp16 operand planes when the damping bounds the inverse (gamma >= kF16MinGamma)
+    const bool f16 = p->f16 && gamma >= kF16MinGamma;
+    const CUtensorMap* maps = f16 ? p->maps16 : p->maps;
+    const TcItem* items = f16 ? p->items16 : p->items;
+    const TcEpi* epis = f16 ? p->epis16 : p->epis;
     stat_begin(kCatInvUnpackFinal, s);
-    damp_unpack_kernel<<<p->n_tiles, 256, 0, s>>>(p->mats, p->tiles, gamma);
+    damp_unpack_kernel<<<p->n_tiles, 256, 0, s>>>(p->mats, p->tiles, gamma, f16 ? gamma : 1.f);
     SPD_CHECK_LAUNCH();
+    if (f16) {
+      inv_scale_kernel<<<p->n_blocked, 256, 0, s>>>(p->mats, p->blocked_ids, gamma);
+      SPD_CHECK_LAUNCH();
+    }
     stat_end(kCatInvUnpackFinal, s, 0, 0);
     // step k's pivot -> stage -> panel GEMM on stream q (the critical chain)
     auto front = [&](int k, cudaStream_t q) -> int {
       const int na = p->act_cnt[k];
-      float* pa = p->panA + (k % kPanSlots) * kB;
+      void* pa = f16 ? static_cast<void*>(reinterpret_cast<__half*>(p->panA) + (k % kPanSlots) * kB)
+                     : static_cast<void*>(p->panA + (k % kPanSlots) * kB);
       Probe* pr = stat_begin(kCatInvPivot, q);
-      if (p->legacy_pivot)
-        pivot_kernel<<<na, 512, 0, q>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
-                                        int64_t(p->n_blocked) * kB * kB, pr);
+      if (p->legacy_pivot && p->pivot_v3)
+        pivot_kernel<true><<<na, 512, 0, q>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
+                                              int64_t(p->n_blocked) * kB * kB, int(f16), pr);
+      else if (p->legacy_pivot)
+        pivot_kernel<false><<<na, 512, 0, q>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
+                                               int64_t(p->n_blocked) * kB * kB, int(f16), pr);
       else
         pivot_tc_kernel<false><<<na, pvt::kThreads, pvt::kSmem, q>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
-                                                                     int64_t(p->n_blocked) * kB * kB, 0.f, pr);
+                                                                     int64_t(p->n_blocked) * kB * kB, int(f16), 0.f, pr);
       SPD_CHECK_LAUNCH();
       stat_end(kCatInvPivot, q, 2.0 * kB * kB * kB * na, 0);
       TcRun prun{};
       prun.probe = stat_begin(kCatInvPanel, q);  // the probe times the panel GEMM launch
-      stage_panel_kernel<<<dim3(p->pan_cnt[k], 4), 256, 0, q>>>(p->mats, p->pan_jobs + p->pj_off[k], k, pa, plane);
+      if (f16)
+        stage_panel_kernel<true><<<dim3(p->pan_cnt[k], 4), 256, 0, q>>>(p->mats, p->pan_jobs + p->pj_off[k], k, pa,
+                                                                         plane);
+      else
+        stage_panel_kernel<false><<<dim3(p->pan_cnt[k], 4), 256, 0, q>>>(p->mats, p->pan_jobs + p->pj_off[k], k, pa,
+                                                                          plane);
       SPD_CHECK_LAUNCH();
       // the panel GEMM has few K blocks per tile: a full persistent grid would hold every SM for
       // ~20 us per step while doing little work; a capped grid leaves the SMs to the
       // concurrent convolutions at almost the same chain latency
-      int rc = launch_tc3(Kind::TF32, p->maps, p->items + p->pan_off[k], p->epis, p->pan_cnt[k], q, prun,
+      int rc = launch_tc3(f16 ? Kind::F16 : Kind::TF32, maps, items + p->pan_off[k], epis, p->pan_cnt[k], q, prun,
                           p->panel_ctas);
       if (rc) return rc;
       stat_end(kCatInvPanel, q, 2.0 * kB * kB * kB * p->pan_cnt[k], 0);
       return SPDKFAC_OK;
     };
+    const Kind ukind = f16 ? Kind::F16 : Kind::TF32;
     int rc = front(0, s);
     if (rc) return rc;
     for (int k = 0; k < p->steps; ++k) {
@@ -1299,7 +1632,7 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       // while U2(k) (the rest of the trailing update) runs here (look-ahead)
       const int u1 = p->u1_cnt[k], u2 = p->upd_cnt[k] - u1;
       Probe* pu = stat_begin(kCatInvUpdate, s);
-      rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k], p->epis, u1, s, pu);
+      rc = launch_tc3_ctile(maps, items + p->upd_off[k], epis, u1, s, pu, ukind);
       if (rc) return rc;
       stat_end(kCatInvUpdate, s, p->upd_flops[k], 0);
       const bool ahead = k + 1 < p->steps;
@@ -1310,7 +1643,7 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
           stat_end(kCatInvUpdate, s, p->pu_flops[k], 0);
         }
         Probe* pu2 = stat_begin(kCatInvUpdate, s);
-        rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k] + u1, p->epis, u2, s, pu2);
+        rc = launch_tc3_ctile(maps, items + p->upd_off[k] + u1, epis, u2, s, pu2, ukind);
         if (rc) return rc;
         stat_end(kCatInvUpdate, s, p->u2_flops[k], 0);
         if ((rc = front(k + 1, s))) return rc;
@@ -1328,7 +1661,7 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
         stat_end(kCatInvUpdate, s, p->pu_flops[k], 0);
       }
       pu = stat_begin(kCatInvUpdate, s);
-      rc = launch_tc3_ctile(p->maps, p->items + p->upd_off[k] + u1, p->epis, u2, s, pu);
+      rc = launch_tc3_ctile(maps, items + p->upd_off[k] + u1, epis, u2, s, pu, ukind);
       if (rc) return rc;
       stat_end(kCatInvUpdate, s, p->u2_flops[k], 0);
       if (ahead) SPD_CUDA(cudaStreamWaitEvent(s, p->ev_panel, 0));

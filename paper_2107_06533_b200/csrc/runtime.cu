@@ -118,6 +118,22 @@ int make_operand_map(CUtensorMap* out, const void* base, bool bf16, int64_t k_ex
   return SPDKFAC_OK;
 }
 
+int make_operand_map_f16(CUtensorMap* out, const void* base, int64_t k_extent, int64_t rows, int64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  SPD_ARG(fn != nullptr, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  SPD_ARG((ld * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0, SPDKFAC_ERR_ARG,
+          "tensor map: misaligned operand");
+  cuuint64_t dims[3] = {cuuint64_t(k_extent), cuuint64_t(rows), 2};
+  cuuint64_t strides[2] = {cuuint64_t(ld * 2), cuuint64_t(ld * 2 * rows)};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SPD_ARG(r == CUDA_SUCCESS, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled (fp16) failed (%d)", int(r));
+  return SPDKFAC_OK;
+}
+
 int make_operand_map_mn(CUtensorMap* out, const void* base, int64_t ld, int64_t k_rows) {
   EncodeTiledFn fn = encode_fn();
   SPD_ARG(fn != nullptr, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -198,8 +214,9 @@ static int launch_kind(const CUtensorMap* maps, const TcItem* items, const TcEpi
 int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
                const TcRun& run, int max_ctas) {
   if (n <= 0) return SPDKFAC_OK;
-  return kind == Kind::BF16 ? launch_kind<Kind::BF16, kStages, false>(maps, items, epis, n, s, run, max_ctas)
-                            : launch_kind<Kind::TF32, kStages, false>(maps, items, epis, n, s, run, max_ctas);
+  if (kind == Kind::BF16) return launch_kind<Kind::BF16, kStages, false>(maps, items, epis, n, s, run, max_ctas);
+  if (kind == Kind::F16) return launch_kind<Kind::F16, kStages, false>(maps, items, epis, n, s, run, max_ctas);
+  return launch_kind<Kind::TF32, kStages, false>(maps, items, epis, n, s, run, max_ctas);
 }
 
 int launch_tc3_f32(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
@@ -215,10 +232,11 @@ int launch_tc3_acc(const CUtensorMap* maps, const TcItem* items, const TcEpi* ep
 }
 
 int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
-                     Probe* probe) {
+                     Probe* probe, Kind kind) {
   if (n <= 0) return SPDKFAC_OK;
   TcRun run{};
   run.probe = probe;
+  if (kind == Kind::F16) return launch_kind<Kind::F16, 3, true>(maps, items, epis, n, s, run);
   return launch_kind<Kind::TF32, 3, true>(maps, items, epis, n, s, run);
 }
 

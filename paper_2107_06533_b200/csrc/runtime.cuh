@@ -63,6 +63,8 @@ struct Carve {
 int make_operand_map(CUtensorMap* out, const void* base, bool bf16, int64_t k_extent, int64_t rows, int64_t ld);
 // MN-major bf16 split planes [2][k_rows][ld] (box 64 x 64, SWIZZLE_128B; items flagged kMnMajor)
 int make_operand_map_mn(CUtensorMap* out, const void* base, int64_t ld, int64_t k_rows);
+// fp16 split planes [2][rows][ld], K-major, box 64 (K) x 128 rows, SWIZZLE_128B
+int make_operand_map_f16(CUtensorMap* out, const void* base, int64_t k_extent, int64_t rows, int64_t ld);
 
 // 2-D map over fp32 rows [rows][cols] (row stride ld), box 128 columns x kF32Bk rows, no swizzle
 int make_rows_map_f32(CUtensorMap* out, const float* base, int64_t rows, int64_t cols, int64_t ld);
@@ -87,12 +89,12 @@ int launch_tc3(Kind kind, const CUtensorMap* maps, const TcItem* items, const Tc
 // BF16 SYRK engine whose kF32Rows items read fp32 rows through the tensor maps in `fm` (converter warps)
 int launch_tc3_f32(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items, cudaStream_t s,
                    const TcRun& run, const F32Maps& fm);
-// TF32 engine with a TMA-staged fp32 C tile (read-modify-write targets, TcEpi::c_map)
 // CTA-pair SYRK engine (cta_group::2, 256 x 256 super tiles; bf16 MN-major split planes)
 int launch_tc3_pair(const CUtensorMap* maps, const TcPairItem* items, const TcEpi* epis, int n_items, cudaStream_t s,
                     const TcRun& run);
+// TF32 / F16 engine with a TMA-staged fp32 C tile (read-modify-write targets, TcEpi::c_map)
 int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items, cudaStream_t s,
-                     Probe* probe = nullptr);
+                     Probe* probe = nullptr, Kind kind = Kind::TF32);
 // CTA-pair TF32 engine with the C-slice ring (256 x 256 super tiles of the inverse trailing update)
 int launch_tc3_pair_ctile(const CUtensorMap* maps, const TcPairCItem* items, const TcEpi* epis, int n_items,
                           cudaStream_t s, Probe* probe = nullptr);

@@ -40,6 +40,11 @@ constexpr int32_t kF32Rows = 16;  // (kF32 engines) operands are fp32 rows [M][d
                                  // activations by TMA (tensor maps in the F32Maps kernel parameter, a_map /
                                  // b_map index it); converter warps split them into the bf16 hi/lo MN-major
                                  // planes per K block of 32 rows: no staging pass
+// fp16 operand classes (TcEpi::dscale[c] is the power-of-two scale of class c): flags bits 8-9 the A
+// operand's class, 10-11 the B operand's, 12-13 the out2 planes'.  D carries s_A s_B; the epilogue
+// multiplies alpha by 1 / (s_A s_B) and stores out2 planes of (C * s_out2).
+constexpr int kScaleShiftA = 8, kScaleShiftB = 10, kScaleShiftO = 12;
+SPD_DEV float scale_of(const float* ds, int32_t flags, int shift) { return ds[(flags >> shift) & 3]; }
 constexpr int32_t kOut2Rows = 4;  // out2 row-style: out2[(o2_row + i) * ld2 + j]; else transposed:
                                   // out2[(o2_row + j) * ld2 + i] (coalesced along the TMEM lanes)
 
@@ -83,13 +88,15 @@ struct TcEpi {
   int64_t plane_stride;  // elements between hi and lo planes (split modes)
   float alpha, beta;
   int32_t mode;
-  int32_t pad_;
-  // optional second target (kAxpby only): tf32 split planes, row (a_row + i), column j:
+  int32_t o2_f16;  // out2 planes: 0 = tf32 (fp32 storage), 1 = fp16 scaled by dscale[0]
+  // optional second target (kAxpby only): split planes, row (a_row + i), column j:
   // out2[(a_row + i) * ld2 + j] = hi(alpha*D), out2[... + plane2] = lo(alpha*D)
-  float* out2;
+  void* out2;
   int64_t ld2, plane2;
   int32_t c_map;  // kCTile kernels: 2-D tensor map of the fp32 target (box 128 x 128)
   int32_t pad2_;
+  // optional per-target operand-class scales in device memory (kAxpby / kCTile; see kScaleShiftA)
+  const float* dscale;
 };
 
 // Epilogue of one 32-column chunk of the accumulator tile: thread row i (TMEM lane),
@@ -102,6 +109,9 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
   const int64_t ri = int64_t(it.out_r) + i;
   const int jn = it.n_valid - c * 32;  // valid columns in this chunk (may exceed 32)
   if (ep.mode == kAxpby) {
+    const float alpha =
+        ep.dscale ? ep.alpha / (scale_of(ep.dscale, it.flags, kScaleShiftA) * scale_of(ep.dscale, it.flags, kScaleShiftB))
+                  : ep.alpha;
     float* out = static_cast<float*>(ep.out);
     float* base = out + (int64_t(it.out_c) + c * 32) * ep.ld + ri;  // transposed: column j -> row of target
     float old[32];
@@ -111,7 +121,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
     }
 #pragma unroll
     for (int t = 0; t < 32; ++t)
-      if (row_ok && t < jn) base[int64_t(t) * ep.ld] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + ep.alpha * v[t];
+      if (row_ok && t < jn) base[int64_t(t) * ep.ld] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + alpha * v[t];
     if (it.flags & kMirror) {  // same values, target row ri, 32 contiguous columns
       float* rowp = out + ri * ep.ld + it.out_c + c * 32;
       if (ep.beta != 0.f) {
@@ -120,26 +130,57 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
       }
 #pragma unroll
       for (int t = 0; t < 32; ++t)
-        if (row_ok && t < jn) rowp[t] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + ep.alpha * v[t];
+        if (row_ok && t < jn) rowp[t] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + alpha * v[t];
     }
-    if (ep.out2 != nullptr && row_ok) {
+    if (ep.out2 != nullptr && row_ok && ep.o2_f16) {  // fp16 planes of (C * s)
+      const float sc = scale_of(ep.dscale, it.flags, kScaleShiftO);
+      __half* o2b = static_cast<__half*>(ep.out2);
       if (it.flags & kOut2Rows) {
-        float* o2 = ep.out2 + (int64_t(it.o2_row) + i) * ep.ld2 + c * 32;
+        __half* o2 = o2b + (int64_t(it.o2_row) + i) * ep.ld2 + c * 32;
+#pragma unroll
+        for (int t = 0; t < 32; t += 8) {
+          uint32_t hw[4], lw[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            __half h0, l0, h1, l1;
+            split_f16(alpha * v[t + 2 * u], sc, h0, l0);
+            split_f16(alpha * v[t + 2 * u + 1], sc, h1, l1);
+            hw[u] = uint32_t(__half_as_ushort(h0)) | (uint32_t(__half_as_ushort(h1)) << 16);
+            lw[u] = uint32_t(__half_as_ushort(l0)) | (uint32_t(__half_as_ushort(l1)) << 16);
+          }
+          *reinterpret_cast<uint4*>(o2 + t) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+          *reinterpret_cast<uint4*>(o2 + ep.plane2 + t) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        }
+      } else {
+        __half* o2 = o2b + (int64_t(it.o2_row) + c * 32) * ep.ld2 + i;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          if (t < jn) {
+            __half h, l;
+            split_f16(alpha * v[t], sc, h, l);
+            o2[int64_t(t) * ep.ld2] = h;
+            o2[int64_t(t) * ep.ld2 + ep.plane2] = l;
+          }
+        }
+      }
+    } else if (ep.out2 != nullptr && row_ok) {
+      if (it.flags & kOut2Rows) {
+        float* o2 = static_cast<float*>(ep.out2) + (int64_t(it.o2_row) + i) * ep.ld2 + c * 32;
 #pragma unroll
         for (int t = 0; t < 32; t += 4) {
           float h[4], l[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) split_tf32(ep.alpha * v[t + u], h[u], l[u]);
+          for (int u = 0; u < 4; ++u) split_tf32(alpha * v[t + u], h[u], l[u]);
           *reinterpret_cast<float4*>(o2 + t) = make_float4(h[0], h[1], h[2], h[3]);
           *reinterpret_cast<float4*>(o2 + ep.plane2 + t) = make_float4(l[0], l[1], l[2], l[3]);
         }
       } else {
-        float* o2 = ep.out2 + (int64_t(it.o2_row) + c * 32) * ep.ld2 + i;
+        float* o2 = static_cast<float*>(ep.out2) + (int64_t(it.o2_row) + c * 32) * ep.ld2 + i;
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
           if (t < jn) {
             float h, l;
-            split_tf32(ep.alpha * v[t], h, l);
+            split_tf32(alpha * v[t], h, l);
             o2[int64_t(t) * ep.ld2] = h;
             o2[int64_t(t) * ep.ld2 + ep.plane2] = l;
           }
@@ -244,7 +285,7 @@ __global__ void __launch_bounds__(kF32 ? 320 : 192, 1)
                     const __grid_constant__ F32Param<kF32> fm) {
   static_assert(kAcc == 0 || !kCTile, "chunked accumulation is for register epilogues");
   static_assert(!kF32 || K == Kind::BF16, "fp32-rows operands feed the bf16 SYRK");
-  constexpr int BK = (K == Kind::BF16) ? 64 : 32;  // one 128-byte swizzle row of K
+  constexpr int BK = is_16bit(K) ? 64 : 32;  // one 128-byte swizzle row of K
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_align1024(smem_raw);
   float* ctile = reinterpret_cast<float*>(smem + kSt * kStageBytes);  // kCRing x [32][128] (kCTile)
@@ -523,6 +564,9 @@ __global__ void __launch_bounds__(kF32 ? 320 : 192, 1)
         continue;
       }
       const uint32_t buf = t & 1, use = t >> 1;
+      const float calpha = (kCTile && ep.dscale) ? ep.alpha / (scale_of(ep.dscale, it.flags, kScaleShiftA) *
+                                                                  scale_of(ep.dscale, it.flags, kScaleShiftB))
+                                                 : ep.alpha;
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
 #pragma unroll 1
@@ -542,7 +586,7 @@ __global__ void __launch_bounds__(kF32 ? 320 : 192, 1)
           if (r0 == 0) mbar_wait(&cfull[q], (u2 / kCRing) & 1);
           float* col = ctile + q * (kCSliceBytes / 4) + r0 * 128 + i;
 #pragma unroll
-          for (int u = 0; u < 32; ++u) col[u * 128] = ep.beta * col[u * 128] + ep.alpha * v[u];
+          for (int u = 0; u < 32; ++u) col[u * 128] = ep.beta * col[u * 128] + calpha * v[u];
           if (r0 + 32 == kCSliceRows) {  // slice complete: store it, then reuse the slot
             fence_proxy_async_smem();
             named_bar_sync(1, 128);

@@ -323,6 +323,36 @@ def test_pack_batched_many_rows():
         assert torch.equal(p, f[iu[0], iu[1]]), d
 
 
+@pytest.mark.parametrize("mag,gamma", [(1e-6, 1e-3), (1e-6, 0.1), (1e3, 1e-4), (1.0, 1e-5), (1e8, 0.1), (1e-3, 1e-2)])
+@pytest.mark.parametrize("tf32", ["0", "1"])
+def test_damped_inverse_plane_scaling(mag, gamma, tf32, monkeypatch):
+    """The blocked inverse's panel / update operands are fp16 planes scaled per operand class (1/gamma,
+    sqrt(sigma/gamma), sigma: inv_scale_kernel) or tf32 planes (SPDKFAC_INV_TF32=1, and every run with
+    gamma < 1e-4).  Factors of very small and very large magnitude against small and large damping,
+    full-rank and rank-deficient (rows < d, as the G factors of small batches).  tf32 planes: the
+    kappa-scaled fp32 bound.  fp16 planes: the same bound while sigma / gamma <= 2^16 (sigma = max
+    diagonal of F + gamma I), beyond it the documented normwise model (sigma / gamma) 2^-38."""
+    K = _K()
+    monkeypatch.setenv("SPDKFAC_INV_TF32", tf32)
+    rng = np.random.default_rng(int(abs(math.log10(mag)) * 10 + abs(math.log10(gamma))))
+    for d, rows in [(384, 1000), (640, 96)]:
+        x = rng.standard_normal((rows, d)) * (1.0 + rng.random(d) * 3.0)
+        m = (x.T @ x / rows * mag).astype(np.float32).astype(np.float64)
+        ev = np.linalg.eigvalsh(m + gamma * np.eye(d))
+        if ev[0] <= 0 or ev[-1] / ev[0] > 1e6:  # indefinite after the fp32 rounding of F, or beyond fp32
+            continue                                # (kappa u > 0.06): a failed pivot is then the right answer
+        got = K.damped_inverse(torch.tensor(m, dtype=torch.float32), gamma)
+        want = O.damped_inverse(m, gamma)
+        err = relf(got, want)
+        bound, kappa = inverse_bound(m, gamma, err)
+        ref = cusolver_err(m, gamma, want)
+        assert np.isfinite(got.cpu().numpy()).all()
+        rng_ratio = (np.max(np.diag(m)) + gamma) / gamma
+        f16 = tf32 == "0" and gamma >= 1e-4
+        model = 16 * rng_ratio * 2.0 ** -38 if (f16 and rng_ratio > 2.0 ** 16) else 0.0
+        assert err <= max(bound, 8 * ref, model), (d, err, bound, ref, kappa, rng_ratio)
+
+
 @pytest.mark.parametrize("pairs", ["1", "0"])
 def test_damped_inverse_update_engines(pairs, monkeypatch):
     """The blocked inverse with the CTA-pair update engine (SPDKFAC_UPDATE_PAIRS=1: 2x2 super tiles,
