@@ -1180,6 +1180,11 @@ bool update_pairs() {
   return e && e[0] == '1';
 }
 
+bool eager_rows_schedule() {  // SPDKFAC_EAGER_ROWS=1: the round-2 update schedule (A/B)
+  const char* e = getenv("SPDKFAC_EAGER_ROWS");
+  return e && e[0] == '1';
+}
+
 bool update_order_by_matrix() {  // SPDKFAC_UPDATE_ORDER=nk: the round-1 order (longest K first across matrices)
   const char* e = getenv("SPDKFAC_UPDATE_ORDER");
   return !(e && std::string(e) == "nk");
@@ -1360,15 +1365,17 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     p->upd_off.push_back(int(items.size()));
     // Update of step k, split into U1 (issued before step k+1's look-ahead front: it must
     // see these tiles) and U2 (runs under the front).  Steps are fused in groups of kFuse
-    // (k0 = multiple of kFuse, last = min(k0 + kFuse - 1, T - 1)): a non-last step s updates
-    // only the block rows/columns s+1 (U1) and s+2 .. last+1 (U2), which the group's later
-    // pivots and panels read; the last step updates every other tile with all of its pending
-    // steps' panels in ONE contraction of K = (pending steps) x 128 (their panel slots are
-    // adjacent), so W is read-modify-written once per group instead of once per step.  A tile's
-    // pending steps are those after the last group step that updated it eagerly or had it in
-    // its pivot row/column (the panel epilogue writes those).
+    // (k0 = multiple of kFuse, last = min(k0 + kFuse - 1, T - 1)).  A non-last step s updates
+    // only block row/column s+1 (U1: the next pivot block and panel read it), with all of that
+    // tile's pending group steps in ONE contraction of K = (pending steps) x 128 (their panel
+    // slots are adjacent); the last step also updates every other tile the same way (U2), so
+    // W is read-modify-written about once per group instead of once per step.  A tile's pending
+    // steps are those after the last group step that updated it (its row s+1) or had it in its
+    // pivot row/column (the panel epilogue writes those).  SPDKFAC_EAGER_ROWS=1: the round-2
+    // schedule (step s also updates rows s+2 .. last+1 eagerly, one step per contraction).
     int u1 = 0;
     std::vector<TcItem> u1v, u2v;
+    const bool eager_rows = eager_rows_schedule();
     for (int t : blocked) {
       const int T = mats[t].dp / kB;
       if (k >= T) continue;
@@ -1376,15 +1383,17 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
       const bool bulk = (k == last);
       auto touched = [&](int s, int I, int J) {  // group step s < k updated or owned tile (I, J)
         if (I == s || J == s) return true;  // pivot row/column: written by the panel epilogue
+        if (!eager_rows) return I == s + 1 || J == s + 1;  // the next block row of step s
         return (I >= s + 1 && I <= last + 1) || (J >= s + 1 && J <= last + 1);  // eager rows of step s
       };
       for (int I = 0; I < T; ++I)
         for (int J = I; J < T; ++J) {
           if (I == k || J == k) continue;
           const bool row1 = (I == k + 1 || J == k + 1);
-          const bool eager = (I >= k + 1 && I <= last + 1) || (J >= k + 1 && J <= last + 1);
+          const bool eager = eager_rows ? ((I >= k + 1 && I <= last + 1) || (J >= k + 1 && J <= last + 1)) : row1;
           int first = k;  // first pending step of this tile
-          if (bulk) {
+          if (bulk || !eager_rows) {
+            if (!bulk && !eager) continue;  // deferred to the group's last step
             first = k0;
             for (int s2 = k - 1; s2 >= k0; --s2)
               if (touched(s2, I, J)) {
@@ -1631,10 +1640,13 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       // U1(k): the tiles step k+1 reads; then step k+1's front runs on the side stream
       // while U2(k) (the rest of the trailing update) runs here (look-ahead)
       const int u1 = p->u1_cnt[k], u2 = p->upd_cnt[k] - u1;
-      Probe* pu = stat_begin(kCatInvUpdate, s);
-      rc = launch_tc3_ctile(maps, items + p->upd_off[k], epis, u1, s, pu, ukind);
-      if (rc) return rc;
-      stat_end(kCatInvUpdate, s, p->upd_flops[k], 0);
+      Probe* pu = nullptr;
+      if (u1 > 0) {
+        pu = stat_begin(kCatInvUpdate, s);
+        rc = launch_tc3_ctile(maps, items + p->upd_off[k], epis, u1, s, pu, ukind);
+        if (rc) return rc;
+        stat_end(kCatInvUpdate, s, p->upd_flops[k], 0);
+      }
       const bool ahead = k + 1 < p->steps;
       if (ahead && !p->lookahead) {  // serial order: rest of the update, then the next front
         if (p->pu_cnt[k]) {
@@ -1642,10 +1654,12 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
           if ((rc = launch_tc3_pair_ctile(p->maps, p->pitems + p->pu_off[k], p->epis, p->pu_cnt[k], s, pp))) return rc;
           stat_end(kCatInvUpdate, s, p->pu_flops[k], 0);
         }
-        Probe* pu2 = stat_begin(kCatInvUpdate, s);
-        rc = launch_tc3_ctile(maps, items + p->upd_off[k] + u1, epis, u2, s, pu2, ukind);
-        if (rc) return rc;
-        stat_end(kCatInvUpdate, s, p->u2_flops[k], 0);
+        if (u2 > 0) {  // (non-last steps of a fused group have no U2)
+          Probe* pu2 = stat_begin(kCatInvUpdate, s);
+          rc = launch_tc3_ctile(maps, items + p->upd_off[k] + u1, epis, u2, s, pu2, ukind);
+          if (rc) return rc;
+          stat_end(kCatInvUpdate, s, p->u2_flops[k], 0);
+        }
         if ((rc = front(k + 1, s))) return rc;
         continue;
       }
@@ -1660,10 +1674,12 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
         if ((rc = launch_tc3_pair_ctile(p->maps, p->pitems + p->pu_off[k], p->epis, p->pu_cnt[k], s, pp))) return rc;
         stat_end(kCatInvUpdate, s, p->pu_flops[k], 0);
       }
-      pu = stat_begin(kCatInvUpdate, s);
-      rc = launch_tc3_ctile(maps, items + p->upd_off[k] + u1, epis, u2, s, pu, ukind);
-      if (rc) return rc;
-      stat_end(kCatInvUpdate, s, p->u2_flops[k], 0);
+      if (u2 > 0) {
+        pu = stat_begin(kCatInvUpdate, s);
+        rc = launch_tc3_ctile(maps, items + p->upd_off[k] + u1, epis, u2, s, pu, ukind);
+        if (rc) return rc;
+        stat_end(kCatInvUpdate, s, p->u2_flops[k], 0);
+      }
       if (ahead) SPD_CUDA(cudaStreamWaitEvent(s, p->ev_panel, 0));
     }
     stat_begin(kCatInvUnpackFinal, s);

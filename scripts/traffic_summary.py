@@ -12,12 +12,12 @@ CATS = [  # (category, kernel-name regex) -- first match wins
     ("factor_stage", r"stage_rows|stage_im2col|stage_spatial"),
     ("factor_syrk", r"tc3_gemm_kernel<(\(spd::Kind\))?1,|tc3_pair_kernel"),
     ("factor_reduce", r"reduce_pack"),
-    ("inv_pivot", r"pivot_kernel\(|pivot_tc_kernel<(\(bool\))?(0|false)>"),
+    ("inv_pivot", r"pivot_kernel(<[^>]*>)?\(|pivot_tc_kernel<(\(bool\))?(0|false)>"),
     ("inv_small", r"small_inverse|pivot_tc_kernel<(\(bool\))?(1|true)>"),
-    ("inv_panel", r"stage_panel|tc3_gemm_kernel<(\(spd::Kind\))?[02], (\(int\))?3, (\(bool\))?(0|false), (\(int\))?0>"),
-    ("inv_update", r"tc3_gemm_kernel<(\(spd::Kind\))?[02], (\(int\))?3, (\(bool\))?(1|true)"),
+    ("inv_panel", r"stage_panel|inv_scale|tc3_gemm_kernel<(\(spd::Kind\))?[02], (\(int\))?3, (\(bool\))?(0|false), (\(int\))?0[,>]"),
+    ("inv_update", r"tc3_gemm_kernel<(\(spd::Kind\))?[02], (\(int\))?3, (\(bool\))?(1|true)|tc3_pair_ctile"),
     ("inv_unpack_finalize", r"damp_unpack|finalize_kernel"),
-    ("precond_gemm", r"tc3_gemm_kernel<(\(spd::Kind\))?2, (\(int\))?3, (\(bool\))?(0|false), (\(int\))?4>"),
+    ("precond_gemm", r"tc3_gemm_kernel<(\(spd::Kind\))?2, (\(int\))?3, (\(bool\))?(0|false), (\(int\))?[1-9]"),
     ("precond_split", r"split_rows_batched|stage_packed"),
     ("pack", r"pack_|unpack_"),
 ]
