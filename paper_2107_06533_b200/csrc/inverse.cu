@@ -227,14 +227,15 @@ __device__ __forceinline__ int sweep128_b8v2(float (&a)[2][16], int n, B8v2Share
 // barrier per group instead of three, and the 8x8 sweep (~70 cycles per pivot of shuffle /
 // MUFU latency) overlaps the bulk FFMA work.
 struct B8v3Shared {
-  float4 R[2][128][2];  // R_g[i][s] = W[i][K_g + s]   (buffer g & 1)
+  float Rt[2][8][128];  // R_g^T: Rt[s][i] = W[i][K_g + s]   (buffer g & 1; column pairs feed FFMA2)
   float4 W[2][128][2];  // row weights of group g
   float S[8][8];
   int fail[2];
 };
 
 // 8x8 block B (lane: rr = lane >> 2, c = lane & 3 holds v0 = B[rr][c], v1 = B[rr][c + 4]) -> S =
-// -B^-1 into S; returns the first non-positive pivot (warp-uniform) or -1
+// -B^-1 into S; returns the first non-positive pivot (warp-uniform) or -1.  (A variant in which every
+// lane sweeps its own register copy of B, without shuffles, measured slower: 61 vs 48 us per block.)
 __device__ __forceinline__ int sweep8x8(float v0, float v1, int lane, float (&S)[8][8]) {
   const int rr = lane >> 2, c = lane & 3;
   int fail = -1;
@@ -261,25 +262,33 @@ __device__ __forceinline__ int sweep8x8(float v0, float v1, int lane, float (&S)
   return fail;
 }
 
-// group g's rank-8 update of this thread's columns [8H, 8H + 8) of its 16
+// d = a * b + c on two fp32 lanes (FFMA2: one issue slot for two FMAs, each rounded as fmaf)
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 a, b, c;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%0, %1};\n\t"
+      "fma.rn.f32x2 c, a, b, c;\n\tmov.b64 {%0, %1}, c;\n\t}"
+      : "+f"(d0), "+f"(d1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+// group g's rank-8 update of this thread's columns [8H, 8H + 8) of its 16: W[i,j] = base - sum_c
+// w_i[c] R[j][c] in the order c = 0..7 (base = 0 on the pivot rows), two adjacent columns per FFMA2
 template <int H>
-__device__ __forceinline__ void b8v3_update_half(float (&a)[2][16], const float (&w)[2][8], const bool (&pk)[2],
-                                                 const float4 (*R)[2], int q) {
+__device__ __forceinline__ void b8v3_update_half(float (&a)[2][16], const float (&wn)[2][8], const bool (&pk)[2],
+                                                 const float (*Rt)[128], int q) {
 #pragma unroll
-  for (int jj = 8 * H; jj < 8 * H + 8; ++jj) {
-    const float4 ra = R[q * 16 + jj][0], rb = R[q * 16 + jj][1];
+  for (int u = 0; u < 2; ++u)
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      float v = pk[u] ? 0.f : a[u][jj];
-      v = fmaf(-w[u][0], ra.x, v);
-      v = fmaf(-w[u][1], ra.y, v);
-      v = fmaf(-w[u][2], ra.z, v);
-      v = fmaf(-w[u][3], ra.w, v);
-      v = fmaf(-w[u][4], rb.x, v);
-      v = fmaf(-w[u][5], rb.y, v);
-      v = fmaf(-w[u][6], rb.z, v);
-      v = fmaf(-w[u][7], rb.w, v);
-      a[u][jj] = v;
+    for (int jj = 8 * H; jj < 8 * H + 8; ++jj) a[u][jj] = pk[u] ? 0.f : a[u][jj];
+#pragma unroll
+  for (int jq = 0; jq < 2; ++jq) {  // 4 columns 16 q + 8 H + 4 jq .. + 3
+    const int j0 = 8 * H + 4 * jq;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float4 r = *reinterpret_cast<const float4*>(&Rt[c][q * 16 + j0]);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        ffma2(a[u][j0], a[u][j0 + 1], wn[u][c], wn[u][c], r.x, r.y);
+        ffma2(a[u][j0 + 2], a[u][j0 + 3], wn[u][c], wn[u][c], r.z, r.w);
+      }
     }
   }
 }
@@ -289,17 +298,14 @@ __device__ __forceinline__ void b8v3_update_half(float (&a)[2][16], const float 
 template <int H>
 __device__ __forceinline__ void b8v3_pivot_work(const float (&a)[2][16], int Kn, int nb, B8v3Shared& sh, int r,
                                                 int lane, int warp, int qn) {
-  float4(*R)[2] = sh.R[nb];
+  float(*Rt)[128] = sh.Rt[nb];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    R[2 * r + u][0] = make_float4(a[u][8 * H], a[u][8 * H + 1], a[u][8 * H + 2], a[u][8 * H + 3]);
-    R[2 * r + u][1] = make_float4(a[u][8 * H + 4], a[u][8 * H + 5], a[u][8 * H + 6], a[u][8 * H + 7]);
-  }
+  for (int ss = 0; ss < 8; ++ss)  // rows 2r, 2r + 1 are adjacent columns of R^T
+    *reinterpret_cast<float2*>(&Rt[ss][2 * r]) = make_float2(a[0][8 * H + ss], a[1][8 * H + ss]);
   named_bar_sync(1, 64);
   if (warp == 2 * qn + (Kn >= 64 ? 1 : 0)) {  // rows Kn..Kn+7 live in this warp
-    const float* Rf = reinterpret_cast<const float*>(R);
     const int rr = lane >> 2, c = lane & 3;
-    const int f = sweep8x8(Rf[(Kn + rr) * 8 + c], Rf[(Kn + rr) * 8 + c + 4], lane, sh.S);
+    const int f = sweep8x8(Rt[c][Kn + rr], Rt[c + 4][Kn + rr], lane, sh.S);
     if (lane == 0) sh.fail[nb] = f;
   }
   named_bar_sync(1, 64);
@@ -330,26 +336,26 @@ __device__ __forceinline__ int b8v3_step(float (&a)[2][16], int g, int ng, B8v3S
                                          int warp) {
   constexpr int H1 = P ^ 1;  // half of the column block holding group g+1
   const int buf = g & 1, nb = buf ^ 1, K0 = 8 * g, qg = g >> 1, q1 = (g + 1) >> 1;
-  float w[2][8];
+  float wn[2][8];  // -w (the FFMA2 operand); the pivot columns get w = -wn back exactly
   bool pk[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int i = 2 * r + u;
     const float4 wa = sh.W[buf][i][0], wb = sh.W[buf][i][1];
-    w[u][0] = wa.x, w[u][1] = wa.y, w[u][2] = wa.z, w[u][3] = wa.w;
-    w[u][4] = wb.x, w[u][5] = wb.y, w[u][6] = wb.z, w[u][7] = wb.w;
+    wn[u][0] = -wa.x, wn[u][1] = -wa.y, wn[u][2] = -wa.z, wn[u][3] = -wa.w;
+    wn[u][4] = -wb.x, wn[u][5] = -wb.y, wn[u][6] = -wb.z, wn[u][7] = -wb.w;
     pk[u] = (i >= K0 && i < K0 + 8);
   }
-  const float4(*R)[2] = sh.R[buf];
-  b8v3_update_half<H1>(a, w, pk, R, q);
+  const float(*Rt)[128] = sh.Rt[buf];
+  b8v3_update_half<H1>(a, wn, pk, Rt, q);
   const bool next = g + 1 < ng;
   if (next && q == q1) b8v3_pivot_work<H1>(a, K0 + 8, nb, sh, r, lane, warp, q1);
-  b8v3_update_half<P>(a, w, pk, R, q);
+  b8v3_update_half<P>(a, wn, pk, Rt, q);
   if (q == qg) {  // group g's pivot columns (half P of column block qg) <- w
 #pragma unroll
     for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int cc = 0; cc < 8; ++cc) a[u][8 * P + cc] = w[u][cc];
+      for (int cc = 0; cc < 8; ++cc) a[u][8 * P + cc] = -wn[u][cc];
   }
   __syncthreads();
   if (next) {

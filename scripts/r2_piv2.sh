@@ -1,0 +1,17 @@
+#!/bin/bash
+# FFMA2 pivot sweep: inverse parity, isolated inverse timing (v3 FFMA2 vs v2), bench
+export PYTHONPATH=. SPD_WATCHDOG=900
+timeout 900 python -m pytest tests/test_gpu_linalg.py tests/test_gpu_production_paths.py -m gpu -q -p no:cacheprovider -k "inverse or pivot or damped or small" > gpurun_out/r2_piv2_tests.log 2>&1
+echo "tests rc=$?"; tail -1 gpurun_out/r2_piv2_tests.log; grep -E "^E  |FAILED|d=4608|d=2048" gpurun_out/r2_piv2_tests.log | head
+for v in v3 b8; do
+  SPDKFAC_PIVOT=$v timeout 300 python scripts/bench_inverse.py > gpurun_out/r2_inv_iso_$v.json 2>&1; echo "inv $v rc=$?"
+  python -c "
+import json;d=json.load(open('gpurun_out/r2_inv_iso_$v.json'))
+for k,v in d.items():
+  if isinstance(v,dict): print('$v', k, v['ms_total'], {c:(x['ms'],x['launches'],x['us_per_launch']) for c,x in v['cats'].items()})
+" || tail -5 gpurun_out/r2_inv_iso_$v.json
+done
+timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/r2_piv2_bench.json 2>gpurun_out/r2_piv2_bench.err
+python -c "import json;d=json.loads(open('gpurun_out/r2_piv2_bench.json').read().strip().splitlines()[-1]);print('bench', d['value'], {k:(v['kernel_ms_per_step'], v['frac']) for k,v in d['roofline_kernels'].items()})" || tail -5 gpurun_out/r2_piv2_bench.err
+timeout 900 python -m pytest tests/test_gpu_config_parity.py -m gpu -q -x -s -p no:cacheprovider -k "resnet50 or densenet" > gpurun_out/r2_piv2_cfg.log 2>&1
+echo "cfg rc=$?"; tail -1 gpurun_out/r2_piv2_cfg.log; grep worst gpurun_out/r2_piv2_cfg.log
