@@ -223,7 +223,11 @@ class SPDKFAC(torch.optim.Optimizer):
             ts = [t for t in mine if t in grp[side]]
             self._inv_ts[side] = ts
             self._inv_plans[side] = InversePlan([self._packed(t) for t in ts], [self.inv[t] for t in ts]) if ts else None
-            self._info_host[side] = torch.zeros(len(ts), dtype=torch.int32, pin_memory=True) if ts else None
+            # two pinned slots (eager steps alternate; a captured graph always writes slot 0): step N+1's
+            # A inversion, launched from the forward hooks, cannot overwrite step N's info before
+            # check_inverses reads it
+            self._info_host[side] = ([torch.zeros(len(ts), dtype=torch.int32, pin_memory=True) for _ in range(2)]
+                                     if ts else None)
             self._bcast[side] = self._bcast_layout(grp[side])
         # preconditioning + update in groups that follow the G inversion groups (layer sets in
         # backward order): with update_in_backward, an early group's layers are preconditioned
@@ -621,11 +625,13 @@ class SPDKFAC(torch.optim.Optimizer):
         if plan is not None:
             plan.run(self.damping, stream)
             self._stage_planes(self._inv_ts[side], stream)
-            self._info_host[side].copy_(plan.info, non_blocking=True)
-            if not torch.cuda.is_current_stream_capturing():
+            capturing = torch.cuda.is_current_stream_capturing()
+            slot = 0 if capturing else self.steps % 2
+            self._info_host[side][slot].copy_(plan.info, non_blocking=True)
+            if not capturing:
                 ev = torch.cuda.Event()
                 ev.record(stream)
-                self._info_events.append((ev, side, self.steps))
+                self._info_events.append((ev, side, self.steps, slot))
         if self.world > 1 and exchange:
             self._exchange_send(side, stream)
             stream.wait_stream(self.comm_stream)
@@ -647,15 +653,18 @@ class SPDKFAC(torch.optim.Optimizer):
     def check_inverses(self, previous_steps_only: bool = False) -> None:
         """Raise NotPositiveDefiniteError for completed inversions (linalg.py:141-145);
         synchronises only on those inversions' events.  step() checks the previous steps'
-        inversions only, so it never waits for the current iteration's A inverses."""
+        inversions only, so it never waits for the current iteration's A inverses.  Unlike the
+        reference, which raises before any update, the failing step's weight update has already
+        been applied (with the failed matrix's inverse left unchanged); the error surfaces at the
+        next step() or check_inverses()."""
         if previous_steps_only:
             events = [e for e in self._info_events if e[2] < self.steps]
             self._info_events = [e for e in self._info_events if e[2] >= self.steps]
         else:
             events, self._info_events = self._info_events, []
-        for ev, side, _ in events:
+        for ev, side, _, slot in events:
             ev.synchronize()
-            info = self._info_host[side]
+            info = self._info_host[side][slot]
             bad = torch.nonzero(info).flatten()
             if bad.numel():
                 raise NotPositiveDefiniteError(int(info[bad[0]]) - 1)
@@ -801,7 +810,7 @@ class SPDKFAC(torch.optim.Optimizer):
             if self._inv_plans[side] is not None:
                 ev = torch.cuda.Event()
                 ev.record(stream)
-                self._info_events.append((ev, side, self.steps - 1))
+                self._info_events.append((ev, side, self.steps - 1, 0))
 
     def _exchange_send(self, side, src) -> None:
         """Owner ranks broadcast their CT inverses of one side (packed upper triangle,
