@@ -32,8 +32,8 @@ _K = r"tc3_gemm_kernel<(?:\(spd::Kind\))?"
 _RULES = (
     ("Precondition", r"split_rows_batched|apply_update|" + _K + r"2, \d+, false, [1-9]"),  # TF32, chunked accumulation
     ("FactorComp", r"stage_rows|stage_im2col|stage_spatial|reduce_pack|tc3_pair|" + _K + "1,"),  # bf16 SYRK
-    ("InverseComp", r"pivot_kernel|pivot_tc_kernel|stage_panel|small_inverse|damp_unpack|finalize_kernel|"
-                    r"unpack_upper|pack_upper|" + _K + "2,"),
+    ("InverseComp", r"pivot_kernel|pivot_tc_kernel|stage_panel|small_inverse|damp_unpack|finalize_kernel|inv_scale|"
+                    r"unpack_upper|pack_upper|tc3_pair_ctile|" + _K + "[02],"),  # TF32 / F16 panel + update
 )
 
 

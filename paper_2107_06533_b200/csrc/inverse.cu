@@ -32,7 +32,7 @@ constexpr int kSmemLd = kB + 1;  // padded row stride of the shared-memory block
 // Panel planes panA / panC: [2 planes][rows][kPanCols]; step k uses the 128 columns of slot
 // k % kPanSlots, so the panels of a fused step group are adjacent columns (one K = 128 x steps
 // update reads them all) and the look-ahead step never overwrites a slot still being read.
-constexpr int kFuse = 4;                // trailing-update steps fused per W pass (see the update plan)
+constexpr int kFuse = 8;                // trailing-update steps fused per W pass (see the update plan)
 constexpr int kPanSlots = 2 * kFuse;    // a group's slots + the next group's look-ahead never alias
 constexpr int kPanCols = kPanSlots * kB;
 // fp16 operand classes of the panel / P^-1 planes (InvMat::scale index; see inv_scale_kernel)

@@ -61,4 +61,8 @@ def test_classify_kernel_names():
     assert classify("void spd::tc3_gemm_kernel<(spd::Kind)2, 3, true, 0>(...)") == "InverseComp"
     assert classify("void spd::tc3_gemm_kernel<(spd::Kind)2, 3, false, 0>(...)") == "InverseComp"
     assert classify("void spd::pivot_tc_kernel<false>(...)") == "InverseComp"
+    assert classify("void spd::tc3_gemm_kernel<(spd::Kind)0, 3, true, 0, false>(...)") == "InverseComp"  # fp16 planes
+    assert classify("void spd::tc3_gemm_kernel<(spd::Kind)0, 3, false, 0, false>(...)") == "InverseComp"
+    assert classify("void spd::pivot_kernel<true>(...)") == "InverseComp"
+    assert classify("spd::inv_scale_kernel(...)") == "InverseComp"
     assert classify("sm100_xmma_fprop_implicit_gemm") == "FFBP"
