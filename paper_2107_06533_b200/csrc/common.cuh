@@ -108,6 +108,17 @@ SPD_DEV void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
       : "memory");
 }
 
+// im2col-mode load from an NHWC tensor map: coordinates {c, w, h, n} of the first pixel's base position
+// (its receptive field's top-left corner, padding included), offsets {w, h} of the filter tap
+SPD_DEV void tma_load_im2col_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c, int w, int h, int n,
+                                uint16_t off_w, uint16_t off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(m), "r"(c), "r"(w), "r"(h), "r"(n), "r"(smem_u32(bar)), "h"(off_w), "h"(off_h)
+      : "memory");
+}
+
 SPD_DEV void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"

@@ -358,6 +358,11 @@ struct Member {
   int f32_slot = -1;        // index in the launch's F32Maps
   int64_t ldx = 0;          // row stride of x (elements)
   const float* x = nullptr;  // the activation bound by the last stage()
+  // im2col members (channels-last k x k convs, C % 64 == 0, single-CTA engine): the activation itself
+  // is staged (Mst = N*H*W rows of C), the SYRK reads im2col tiles of it by TMA (kIm2col)
+  bool i2c = false;
+  int64_t Mst = 0;
+  Im2colGeom ig{};
 };
 
 namespace {
@@ -371,6 +376,10 @@ int f32_rows_max_blocks() {
   const char* e = getenv("SPDKFAC_F32_ROWS");
   return e ? atoi(e) : 0;
 }
+bool im2col_enabled() {  // SPDKFAC_IM2COL=0: stage im2col rows as in round 1 (A/B)
+  const char* e = getenv("SPDKFAC_IM2COL");
+  return !(e && e[0] == '0');
+}
 bool is_rows_layout(const spdkfac_factor_geom& g) {
   const bool pointwise = g.layout == SPDKFAC_CONV_A_NHWC && g.kh == 1 && g.kw == 1 && g.stride_h == 1 &&
                          g.stride_w == 1 && g.pad_h == 0 && g.pad_w == 0;
@@ -381,6 +390,7 @@ bool is_rows_layout(const spdkfac_factor_geom& g) {
 struct spdkfac_factor_group {
   std::vector<Member> m;
   CUtensorMap* maps = nullptr;
+  Im2colGeom* i2c = nullptr;  // per map index (kIm2col items)
   TcItem* items = nullptr;
   TcPairItem* pitems = nullptr;
   int n_pitems = 0;
@@ -464,6 +474,19 @@ int member_init(Member* mb, const spdkfac_factor_geom* g) {
     if ((mb->T % 2 == 0 && mb->T >= 4 && units * sp >= 48) || (mb->T == 2 && M >= 200000)) mb->S = S;
   }
   mb->splits = mb->S ? choose_splits(mb->Mpad, mb->S * (mb->S + 1) / 2, 74) : choose_splits(mb->Mpad, mb->n_tiles, 148);
+  // k x k channels-last convs on the single-CTA engine: TMA im2col loads instead of an im2col staging pass
+  const bool pointwise = g->kh == 1 && g->kw == 1 && g->stride_h == 1 && g->stride_w == 1 && g->pad_h == 0 &&
+                         g->pad_w == 0;
+  mb->i2c = false;
+  if (im2col_enabled() && !mb->S && g->layout == SPDKFAC_CONV_A_NHWC && !pointwise && g->c % 64 == 0 &&
+      g->pad_h <= 127 && g->pad_w <= 127 && g->stride_h <= 8 && g->stride_w <= 8 &&
+      g->pad_h - (g->kh - 1) * g->dil_h >= -128 && g->pad_w - (g->kw - 1) * g->dil_w >= -128 &&
+      (g->kw - 1) * g->dil_w < 65536 && (g->kh - 1) * g->dil_h < 65536 && g->n * g->h * g->w < (int64_t(1) << 31)) {
+    mb->i2c = true;
+    mb->Mst = g->n * g->h * g->w;
+    mb->ig = Im2colGeom{int32_t(g->c), g->kw, g->kh * g->kw, Wo, Ho * Wo, int32_t(g->n), g->stride_w, g->stride_h,
+                        g->pad_w, g->pad_h, g->dil_w, g->dil_h};
+  }
   // every K slice must be non-empty: reduce_pack_kernel sums all `splits` partial slots, and
   // an empty slice would leave its (uninitialised) slot unwritten.  With per = cdiv(nkb, s),
   // cdiv(nkb, per) slices of `per` blocks cover nkb and the last one holds >= 1 block.
@@ -478,7 +501,7 @@ void group_carve(spdkfac_factor_group* G, Carve& c) {
   int f32 = 0;
   for (Member& mb : G->m) {
     if (mb.f32 && f32 == kMaxF32Maps) mb.f32 = false;  // the launch carries at most kMaxF32Maps row maps
-    mb.xt = mb.f32 ? nullptr : c.take<__nv_bfloat16>(size_t(2) * mb.M * mb.ld);
+    mb.xt = mb.f32 ? nullptr : c.take<__nv_bfloat16>(size_t(2) * (mb.i2c ? mb.Mst * mb.g.c : mb.M * mb.ld));
     mb.f32_slot = mb.f32 ? f32++ : -1;
     if (mb.splits > 1) {
       mb.partial = c.take<float>(size_t(mb.n_tiles) * mb.splits * 16384);
@@ -494,7 +517,8 @@ void group_carve(spdkfac_factor_group* G, Carve& c) {
       items += mb.n_tiles * mb.splits;
   }
   const size_t n = G->m.size();
-  G->maps = c.take<CUtensorMap>(n, 128);
+  G->maps = c.take<CUtensorMap>(2 * n, 128);  // member k: [2k] (im2col members: [2k] hi, [2k + 1] lo plane)
+  G->i2c = c.take<Im2colGeom>(2 * n);
   G->items = c.take<TcItem>(size_t(std::max(items, 1)));
   G->pitems = c.take<TcPairItem>(size_t(std::max(pitems, 1)));
   G->epis = c.take<TcEpi>(n);
@@ -507,7 +531,8 @@ void group_carve(spdkfac_factor_group* G, Carve& c) {
 
 int group_build(spdkfac_factor_group* G, float* const* packed, const float* scales, cudaStream_t s) {
   const int n = int(G->m.size());
-  std::vector<CUtensorMap> maps(n);
+  std::vector<CUtensorMap> maps(2 * size_t(n));
+  std::vector<Im2colGeom> geo(2 * size_t(n));
   std::vector<TcItem> items;
   std::vector<TcPairItem> pitems;
   std::vector<TcEpi> epis(n);
@@ -518,13 +543,22 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
   G->flops_single = G->flops_pair = 0;
   for (int k = 0; k < n; ++k) {
     Member& mb = G->m[k];
-    if (!mb.f32) {  // staged bf16 planes (fp32-rows members get their map at compute time)
-      int rc = make_operand_map_mn(&maps[k], mb.xt, mb.ld, mb.M);
+    if (mb.i2c) {  // one im2col map per staged activation plane
+      const spdkfac_factor_geom& g = mb.g;
+      for (int p = 0; p < 2; ++p) {
+        int rc = make_im2col_map_bf16(&maps[2 * k + p], mb.xt + size_t(p) * mb.Mst * g.c, int(g.n), int(g.h),
+                                      int(g.w), int(g.c), g.kh, g.kw, g.stride_h, g.stride_w, g.pad_h, g.pad_w,
+                                      g.dil_h, g.dil_w);
+        if (rc) return rc;
+      }
+      geo[2 * k] = mb.ig;
+    } else if (!mb.f32) {  // staged bf16 planes (fp32-rows members get their map at compute time)
+      int rc = make_operand_map_mn(&maps[2 * k], mb.xt, mb.ld, mb.M);
       if (rc) return rc;
     } else {
       SPD_ARG(mb.f32_slot < kMaxF32Maps, SPDKFAC_ERR_ARG, "too many fp32-rows members in one factor group (%d)",
               mb.f32_slot + 1);
-      std::memset(&maps[k], 0, sizeof(CUtensorMap));
+      std::memset(&maps[2 * k], 0, sizeof(CUtensorMap));
     }
     G->flops += double(mb.M) * mb.d * (mb.d + 1);
     (mb.S ? G->flops_pair : G->flops_single) += double(mb.M) * mb.d * (mb.d + 1);
@@ -551,7 +585,7 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
         for (int P = 0; P < mb.S; ++P)
           for (int Q = P; Q < mb.S; ++Q) {
             TcPairItem it{};
-            it.map = k;
+            it.map = 2 * k;
             it.a_row = 2 * P * 128;
             it.b_row = 2 * Q * 128;
             it.k0 = int(kb0 * 64);
@@ -576,14 +610,14 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
         for (int I = 0; I < mb.T; ++I)
           for (int J = I; J < mb.T; ++J) {
             TcItem it{};
-            it.a_map = mb.f32 ? mb.f32_slot : k;
-            it.b_map = mb.f32 ? mb.f32_slot : k;
+            it.a_map = mb.f32 ? mb.f32_slot : 2 * k;
+            it.b_map = mb.f32 ? mb.f32_slot : 2 * k;
             it.a_row = I * 128;
             it.b_row = J * 128;
             it.k0 = int(kb0 * 64);
             it.nk = int(kb1 - kb0) * (mb.f32 ? 2 : 1);  // fp32-rows stages hold 32 K rows
             it.epi = k;
-            it.flags = (mb.f32 ? kF32Rows : kMnMajor) | (I == J ? kSameAB : 0);
+            it.flags = (mb.f32 ? kF32Rows : kMnMajor) | (mb.i2c ? kIm2col : 0) | (I == J ? kSameAB : 0);
             out_of(I, J, it.out_r, it.out_c);
             it.m_valid = valid(I);
             it.n_valid = valid(J);
@@ -609,7 +643,8 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
   G->n_items = int(items.size());
   G->n_pitems = int(pitems.size());
   int rc;
-  if ((rc = upload(G->maps, maps, s)) || (rc = upload(G->items, items, s)) || (rc = upload(G->pitems, pitems, s)) ||
+  if ((rc = upload(G->maps, maps, s)) || (rc = upload(G->i2c, geo, s)) || (rc = upload(G->items, items, s)) ||
+      (rc = upload(G->pitems, pitems, s)) ||
       (rc = upload(G->epis, epis, s)) ||
       (rc = upload(G->jobs, jobs, s)) || (rc = upload(G->rmem, rmem, s)))
     return rc;
@@ -626,7 +661,14 @@ int member_stage(Member& mb, const float* x, cudaStream_t s) {
   Probe* pr = stat_begin(kCatFactorStage, s);
   const bool pointwise = g.layout == SPDKFAC_CONV_A_NHWC && g.kh == 1 && g.kw == 1 && g.stride_h == 1 &&
                          g.stride_w == 1 && g.pad_h == 0 && g.pad_w == 0;
-  if (g.layout == SPDKFAC_ROWS || g.layout == SPDKFAC_SPATIAL_NHWC || pointwise) {
+  if (mb.i2c) {  // the activation itself, [N*H*W][C] -> [2][N*H*W][C]: the SYRK gathers im2col tiles by TMA
+    const bool vec = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const RowShape rs = row_shape(mb.Mst, g.c / (vec ? 4 : 2), kStageRows);
+    if (vec)
+      stage_rows_kernel<true><<<rs.grid, rs.threads, 0, s>>>(x, mb.Mst, g.c, g.c, mb.xt, g.c, rs.tpr, rs.cps, pr);
+    else
+      stage_rows_kernel<false><<<rs.grid, rs.threads, 0, s>>>(x, mb.Mst, g.c, g.c, mb.xt, g.c, rs.tpr, rs.cps, pr);
+  } else if (g.layout == SPDKFAC_ROWS || g.layout == SPDKFAC_SPATIAL_NHWC || pointwise) {
     // linear inputs [n][w] (row stride w); channels-last output gradients [b*h*w][C] and the
     // inputs of channels-last 1x1 stride-1 convs: rows [b*h*w][C]
     const int64_t ldx = g.layout == SPDKFAC_ROWS ? g.w : g.c;
@@ -666,6 +708,7 @@ int group_compute(spdkfac_factor_group* G, float scale, float decay, float world
                   cudaStream_t s) {
   // algorithmic work: sum over members of M * d * (d + 1) flops
   TcRun run{packed, G->m.empty() ? 0 : G->m[0].d, scale, decay, world_scale, 0};
+  run.i2c = G->i2c;
   double bytes_single = 0, bytes_pair = 0;
   for (const Member& mb : G->m) (mb.S ? bytes_pair : bytes_single) += 4.0 * (mb.f32 ? mb.d : mb.ld) * mb.M;
   int rc;
@@ -819,7 +862,7 @@ void spdkfac_factor_group_destroy(spdkfac_factor_group* G) { delete G; }
 int spdkfac_factor_group_describe(const spdkfac_factor_group* G, int member, int64_t out[4]) {
   SPD_ARG(G && out && member >= 0 && member < int(G->m.size()), SPDKFAC_ERR_ARG, "bad describe arguments");
   const Member& mb = G->m[member];
-  out[0] = mb.S ? 1 : (mb.f32 ? 2 : 0), out[1] = mb.splits, out[2] = mb.M, out[3] = mb.d;
+  out[0] = mb.S ? 1 : (mb.f32 ? 2 : (mb.i2c ? 3 : 0)), out[1] = mb.splits, out[2] = mb.M, out[3] = mb.d;
   return SPDKFAC_OK;
 }
 

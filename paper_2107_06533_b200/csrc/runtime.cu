@@ -101,6 +101,43 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+
+static EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(p);
+  });
+  return fn;
+}
+
+int make_im2col_map_bf16(CUtensorMap* out, const void* base, int n, int h, int w, int c, int kh, int kw, int stride_h,
+                         int stride_w, int pad_h, int pad_w, int dil_h, int dil_w) {
+  EncodeIm2colFn fn = encode_im2col_fn();
+  SPD_ARG(fn != nullptr, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable");
+  SPD_ARG(c % 64 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0, SPDKFAC_ERR_ARG, "im2col map: misaligned");
+  cuuint64_t dims[4] = {cuuint64_t(c), cuuint64_t(w), cuuint64_t(h), cuuint64_t(n)};
+  cuuint64_t strides[3] = {cuuint64_t(c) * 2, cuuint64_t(w) * c * 2, cuuint64_t(h) * w * c * 2};
+  // bounding box of the receptive fields' top-left corners, {H, W} order: from (-pad) to
+  // (last index + pad - (k - 1) dil)
+  int lower[2] = {-pad_h, -pad_w};
+  int upper[2] = {pad_h - (kh - 1) * dil_h, pad_w - (kw - 1) * dil_w};
+  cuuint32_t estr[4] = {1, cuuint32_t(stride_w), cuuint32_t(stride_h), 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lower, upper, 64,
+                  64, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SPD_ARG(r == CUDA_SUCCESS, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeIm2col failed (%d)", int(r));
+  return SPDKFAC_OK;
+}
+
 int make_operand_map(CUtensorMap* out, const void* base, bool bf16, int64_t k_extent, int64_t rows, int64_t ld) {
   EncodeTiledFn fn = encode_fn();
   SPD_ARG(fn != nullptr, SPDKFAC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");

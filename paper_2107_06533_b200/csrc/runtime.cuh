@@ -63,6 +63,9 @@ struct Carve {
 int make_operand_map(CUtensorMap* out, const void* base, bool bf16, int64_t k_extent, int64_t rows, int64_t ld);
 // MN-major bf16 split planes [2][k_rows][ld] (box 64 x 64, SWIZZLE_128B; items flagged kMnMajor)
 int make_operand_map_mn(CUtensorMap* out, const void* base, int64_t ld, int64_t k_rows);
+// im2col-mode map of one staged bf16 NHWC activation plane: boxes of 64 output positions x 64 channels
+int make_im2col_map_bf16(CUtensorMap* out, const void* base, int n, int h, int w, int c, int kh, int kw, int stride_h,
+                         int stride_w, int pad_h, int pad_w, int dil_h, int dil_w);
 // fp16 split planes [2][rows][ld], K-major, box 64 (K) x 128 rows, SWIZZLE_128B
 int make_operand_map_f16(CUtensorMap* out, const void* base, int64_t k_extent, int64_t rows, int64_t ld);
 

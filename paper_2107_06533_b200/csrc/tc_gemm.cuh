@@ -45,6 +45,8 @@ constexpr int32_t kF32Rows = 16;  // (kF32 engines) operands are fp32 rows [M][d
 // multiplies alpha by 1 / (s_A s_B) and stores out2 planes of (C * s_out2).
 constexpr int kScaleShiftA = 8, kScaleShiftB = 10, kScaleShiftO = 12;
 SPD_DEV float scale_of(const float* ds, int32_t flags, int shift) { return ds[(flags >> shift) & 3]; }
+constexpr int32_t kIm2col = 32;  // (with kMnMajor) operand tiles come from im2col-mode TMA loads of the staged
+                                 // NHWC activation planes (TcRun::i2c[map] describes the convolution)
 constexpr int32_t kOut2Rows = 4;  // out2 row-style: out2[(o2_row + i) * ld2 + j]; else transposed:
                                   // out2[(o2_row + j) * ld2 + i] (coalesced along the TMEM lanes)
 
@@ -72,6 +74,14 @@ constexpr uint32_t kF32Tile = 128 * kF32Bk * 4;           // one fp32 tile (16 K
 static_assert(4 * kF32Plane + 2 * kF32Tile == 4 * 128 * 128, "an fp32-rows stage reuses a bf16 stage's bytes");
 
 // Per-launch arguments (kernel parameters, not table entries): what changes between runs.
+// One channels-last convolution's im2col operand (kIm2col items): the staged hi / lo activation
+// planes [2][N*H*W][C], one NHWC tensor map per plane (maps[a_map + p]; output positions past the
+// batch are TMA out-of-bounds zeros), column index (tap, channel) = (r * kw + s) * C + c.
+struct Im2colGeom {
+  int32_t C, kw, taps, Wo, HoWo, N;
+  int32_t stride_w, stride_h, pad_w, pad_h, dil_w, dil_h;
+};
+
 struct TcRun {
   void* out;     // kPackedUpper target (packed buffer)
   int64_t d;     // matrix dimension of the packed target
@@ -80,6 +90,7 @@ struct TcRun {
   float wscale;  // final scale (1/P)
   int32_t pad_;
   Probe* probe;  // launch probe (spdkfac_stats_set_probes) or nullptr
+  const Im2colGeom* i2c = nullptr;  // per tensor map (kIm2col items)
 };
 
 struct TcEpi {
@@ -347,8 +358,14 @@ __global__ void __launch_bounds__(kF32 ? 320 : 192, 1)
         }
         const CUtensorMap* am = maps + it.a_map;
         const CUtensorMap* bm = maps + it.b_map;
-        if (it.a_map != last_a) tmap_acquire(am), last_a = it.a_map;
-        if (!same && it.b_map != last_b) tmap_acquire(bm), last_b = it.b_map;
+        if (it.a_map != last_a) {
+          tmap_acquire(am), last_a = it.a_map;
+          if (it.flags & kIm2col) tmap_acquire(am + 1);  // the lo plane's map
+        }
+        if (!same && it.b_map != last_b) {
+          tmap_acquire(bm), last_b = it.b_map;
+          if (it.flags & kIm2col) tmap_acquire(bm + 1);
+        }
         const uint32_t bytes = same ? 2 * kTileBytes : 4 * kTileBytes;
         for (int kb = 0; kb < it.nk; ++kb, ++g) {
           const uint32_t s = g % kSt;
@@ -356,7 +373,27 @@ __global__ void __launch_bounds__(kF32 ? 320 : 192, 1)
           mbar_expect_tx(&full[s], bytes);
           uint8_t* st = smem + s * kStageBytes;
           const int kc = it.k0 + kb * BK;
-          if (it.flags & kMnMajor) {
+          if (it.flags & kIm2col) {  // 64 output positions x 64 (tap, channel) columns per box
+            const Im2colGeom ga = run.i2c[it.a_map];
+            const int n0 = kc / ga.HoWo, rem = kc - n0 * ga.HoWo, ho = rem / ga.Wo, wo = rem - ho * ga.Wo;
+            const int bw = wo * ga.stride_w - ga.pad_w, bh = ho * ga.stride_h - ga.pad_h;
+            auto load_half = [&](uint8_t* dst, const CUtensorMap* mp, int mn, int p) {
+              int tap = mn / ga.C;
+              const int c0 = mn - tap * ga.C;
+              tap = tap < ga.taps ? tap : ga.taps - 1;  // columns past d: any valid box (masked outputs)
+              const int r = tap / ga.kw, q = tap - r * ga.kw;
+              tma_load_im2col_4d(dst, mp + p, &full[s], c0, bw, bh, n0, uint16_t(q * ga.dil_w), uint16_t(r * ga.dil_h));
+            };
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+              load_half(st + p * kTileBytes, am, it.a_row, p);
+              load_half(st + p * kTileBytes + kTileBytes / 2, am, it.a_row + 64, p);
+              if (!same) {
+                load_half(st + (2 + p) * kTileBytes, bm, it.b_row, p);
+                load_half(st + (2 + p) * kTileBytes + kTileBytes / 2, bm, it.b_row + 64, p);
+              }
+            }
+          } else if (it.flags & kMnMajor) {
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
               tma_load_3d(st + p * kTileBytes, am, &full[s], it.a_row, kc, p);

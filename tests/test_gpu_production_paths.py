@@ -42,7 +42,7 @@ def _describe(group, member=0):
     from paper_2107_06533_b200 import _lib as L
     out = (C.c_int64 * 4)()
     L.check(L.load().spdkfac_factor_group_describe(group._h, member, out), "describe")
-    return {"pair": out[0] == 1, "f32_rows": out[0] == 2, "splits": int(out[1]), "rows": int(out[2]), "dim": int(out[3])}
+    return {"pair": out[0] == 1, "f32_rows": out[0] == 2, "im2col": out[0] == 3, "splits": int(out[1]), "rows": int(out[2]), "dim": int(out[3])}
 
 
 def _group(members, dims, rows):
@@ -163,6 +163,44 @@ def test_syrk_f32_rows_engine(kind, shape, f32, monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(first, packed[0])
     assert relf(unpack_upper(packed[0], d), _factor_rows_oracle(rows)) <= TOL
+
+
+_I2C_CASES = [((32, 64, 56, 56), (3, 3), (1, 1), (1, 1), (1, 1)),    # ResNet-50 layer1 conv2
+              ((32, 128, 56, 56), (3, 3), (2, 2), (1, 1), (1, 1)),   # layer2 first conv2 (stride 2)
+              ((3, 64, 7, 9), (3, 3), (1, 1), (1, 1), (1, 1)),       # ragged: M = 189 rows
+              ((4, 192, 17, 17), (1, 7), (1, 1), (0, 3), (1, 1)),    # Inception-v4 1x7
+              ((4, 192, 17, 17), (7, 1), (1, 1), (3, 0), (1, 1)),    # and 7x1
+              ((2, 64, 20, 20), (3, 3), (2, 2), (0, 0), (1, 1)),     # stride 2, no padding
+              ((2, 64, 20, 20), (3, 3), (1, 1), (2, 2), (2, 2)),     # dilation 2
+              ((2, 128, 12, 12), (5, 5), (1, 1), (2, 2), (1, 1))]    # 5x5
+
+
+@pytest.mark.parametrize("shape,k,st,pd,dl", _I2C_CASES)
+@pytest.mark.parametrize("i2c", ["1", "0"])
+def test_syrk_im2col_tma_engine(shape, k, st, pd, dl, i2c, monkeypatch):
+    """Channels-last k x k convolutions with C % 64 == 0 on the single-CTA engine: the staging pass
+    writes the activation's hi / lo planes, and the SYRK gathers its im2col tiles with TMA im2col loads
+    (engine 3: padding as out-of-bounds zeros, stride as the traversal step, taps as im2col offsets).
+    SPDKFAC_IM2COL=0 stages the im2col rows instead (engine 0).  Both against float64."""
+    from paper_2107_06533_b200 import _lib as L
+    from paper_2107_06533_b200.linalg import unpack_upper
+    monkeypatch.setenv("SPDKFAC_IM2COL", i2c)
+    g = torch.Generator(device="cuda").manual_seed(sum(shape) + k[0])
+    x = torch.relu(torch.randn(*shape, device="cuda", generator=g) + 0.2).contiguous(memory_format=torch.channels_last)
+    n, c, h, w = shape
+    ho = (h + 2 * pd[0] - dl[0] * (k[0] - 1) - 1) // st[0] + 1
+    wo = (w + 2 * pd[1] - dl[1] * (k[1] - 1) - 1) // st[1] + 1
+    d, m = c * k[0] * k[1], n * ho * wo
+    grp, packed = _group([(L.CONV_A_NHWC, shape, k, st, pd, dl)], [d], [m])
+    info = _describe(grp)
+    assert info["im2col"] == (i2c == "1") and info["rows"] == m, info
+    for _ in range(2):
+        grp.stage(0, x)
+        grp.compute()
+    rows = O.im2col_rows(x.double().cpu().numpy(), k[0], k[1], st, pd, dl)
+    perm = [ci * k[0] * k[1] + ki * k[1] + kj for ki in range(k[0]) for kj in range(k[1]) for ci in range(c)]
+    want = (rows.T @ rows / rows.shape[0])[np.ix_(perm, perm)]
+    assert relf(unpack_upper(packed[0], d), want) <= TOL
 
 
 def test_f32_rows_members_beyond_launch_limit_are_staged(monkeypatch):
