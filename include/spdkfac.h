@@ -141,7 +141,7 @@ SPDKFAC_API void spdkfac_factor_group_destroy(spdkfac_factor_group* g);
  * aligned and stay valid until compute; at most 40 such members per group, the rest are staged),
  * 3 = single-CTA engine gathering im2col tiles of the staged activation by TMA im2col loads
  * (channels-last k x k convolutions with C % 64 == 0: the staging pass writes the activation, not
- * its im2col rows; environment SPDKFAC_IM2COL=0 disables it),
+ * its im2col rows; opt-in: environment SPDKFAC_IM2COL=1),
  * out[1] = split-K slices, out[2] = rows M, out[3] = dim d.  No device work. */
 SPDKFAC_API int spdkfac_factor_group_describe(const spdkfac_factor_group* g, int member, int64_t out[4]);
 

@@ -376,9 +376,12 @@ int f32_rows_max_blocks() {
   const char* e = getenv("SPDKFAC_F32_ROWS");
   return e ? atoi(e) : 0;
 }
-bool im2col_enabled() {  // SPDKFAC_IM2COL=0: stage im2col rows as in round 1 (A/B)
+// SPDKFAC_IM2COL=1: k x k channels-last convs (C % 64 == 0, single-CTA engine) stage only the
+// activation and the SYRK gathers im2col tiles by TMA.  Off by default: measured on ResNet-50 (layer1/2
+// 3x3 convs) staging -0.23 ms but SYRK +0.37 ms per step (16.74 vs 16.60 ms).
+bool im2col_enabled() {
   const char* e = getenv("SPDKFAC_IM2COL");
-  return !(e && e[0] == '0');
+  return e && e[0] == '1';
 }
 bool is_rows_layout(const spdkfac_factor_geom& g) {
   const bool pointwise = g.layout == SPDKFAC_CONV_A_NHWC && g.kh == 1 && g.kw == 1 && g.stride_h == 1 &&

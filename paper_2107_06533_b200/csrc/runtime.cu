@@ -126,10 +126,11 @@ int make_im2col_map_bf16(CUtensorMap* out, const void* base, int n, int h, int w
   SPD_ARG(c % 64 == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0, SPDKFAC_ERR_ARG, "im2col map: misaligned");
   cuuint64_t dims[4] = {cuuint64_t(c), cuuint64_t(w), cuuint64_t(h), cuuint64_t(n)};
   cuuint64_t strides[3] = {cuuint64_t(c) * 2, cuuint64_t(w) * c * 2, cuuint64_t(h) * w * c * 2};
-  // bounding box of the receptive fields' top-left corners, {H, W} order: from (-pad) to
-  // (last index + pad - (k - 1) dil)
-  int lower[2] = {-pad_h, -pad_w};
-  int upper[2] = {pad_h - (kh - 1) * dil_h, pad_w - (kw - 1) * dil_w};
+  // bounding box of the receptive fields' top-left corners: from (-pad) to (last index + pad -
+  // (k - 1) dil).  Innermost spatial dimension first ({W, H}, like the coordinates; measured: the
+  // {H, W} order of the driver documentation traps on non-square kernels)
+  int lower[2] = {-pad_w, -pad_h};
+  int upper[2] = {pad_w - (kw - 1) * dil_w, pad_h - (kh - 1) * dil_h};
   cuuint32_t estr[4] = {1, cuuint32_t(stride_w), cuuint32_t(stride_h), 1};
   CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, lower, upper, 64,
                   64, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

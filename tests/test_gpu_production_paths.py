@@ -181,7 +181,7 @@ def test_syrk_im2col_tma_engine(shape, k, st, pd, dl, i2c, monkeypatch):
     """Channels-last k x k convolutions with C % 64 == 0 on the single-CTA engine: the staging pass
     writes the activation's hi / lo planes, and the SYRK gathers its im2col tiles with TMA im2col loads
     (engine 3: padding as out-of-bounds zeros, stride as the traversal step, taps as im2col offsets).
-    SPDKFAC_IM2COL=0 stages the im2col rows instead (engine 0).  Both against float64."""
+    SPDKFAC_IM2COL=0 (the default) stages the im2col rows instead (engine 0).  Both against float64."""
     from paper_2107_06533_b200 import _lib as L
     from paper_2107_06533_b200.linalg import unpack_upper
     monkeypatch.setenv("SPDKFAC_IM2COL", i2c)
@@ -221,9 +221,10 @@ def test_f32_rows_members_beyond_launch_limit_are_staged(monkeypatch):
 
 
 def test_mixed_factor_group_one_launch(monkeypatch):
-    """Pair-engine, single-CTA staged and single-CTA fp32-rows members (split and unsplit) reduced
-    by one group compute."""
+    """Pair-engine, single-CTA staged, single-CTA fp32-rows and TMA-im2col members (split and unsplit)
+    reduced by one group compute."""
     monkeypatch.setenv("SPDKFAC_F32_ROWS", "2")
+    monkeypatch.setenv("SPDKFAC_IM2COL", "1")
     from paper_2107_06533_b200 import _lib as L
     from paper_2107_06533_b200.linalg import unpack_upper
     shapes = [(6272, 2304), (6272, 256), (1000, 300), (25088, 512), (32, 2048)]
@@ -236,6 +237,7 @@ def test_mixed_factor_group_one_launch(monkeypatch):
     kinds = [_describe(grp, k)["pair"] for k in range(len(members))]
     assert any(kinds) and not all(kinds), kinds
     assert any(_describe(grp, k)["f32_rows"] for k in range(len(members)))  # (6272, 256): fp32 rows
+    assert _describe(grp, len(members) - 1)["im2col"]  # the 3x3 conv, C = 64
     for k, x in enumerate(xs + [conv]):
         grp.stage(k, x)
     grp.compute(decay=0.0, world_scale=0.5)
