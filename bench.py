@@ -325,11 +325,13 @@ ROOF_CATS = ("factor_stage", "factor_syrk", "inv_pivot", "inv_panel", "inv_updat
 # the staging pass against HBM
 _INV_PEAK = "tf32_tflops" if os.environ.get("SPDKFAC_INV_TF32") == "1" else "bf16_tflops_sustained"
 _INV_KIND = "TF32" if os.environ.get("SPDKFAC_INV_TF32") == "1" else "F16"
+_PREC_PEAK = "bf16_tflops_sustained" if os.environ.get("SPDKFAC_PRECOND_F16") == "1" else "tf32_tflops"
+_PREC_KIND = "F16 row-scaled" if os.environ.get("SPDKFAC_PRECOND_F16") == "1" else "TF32"
 _ROOF_SPEC = {"factor_syrk": ("tensor", "bf16_tflops_sustained"),
               "inv_pivot": ("fp32", "fp32_ffma_tflops") if os.environ.get("SPDKFAC_PIVOT") != "tc" else ("tensor", "tf32_tflops"),
               # the inverse panel / update issue kind::f16 MMAs on scaled fp16 planes (SPDKFAC_INV_TF32=1: tf32)
               "inv_panel": ("tensor", _INV_PEAK), "inv_update": ("tensor", _INV_PEAK),
-              "precond_gemm": ("tensor", "tf32_tflops"), "factor_stage": ("hbm", "hbm_gbs")}
+              "precond_gemm": ("tensor", _PREC_PEAK), "factor_stage": ("hbm", "hbm_gbs")}
 _KERNEL_NAMES = {"factor_syrk": "tc3_gemm_kernel<BF16> + tc3_pair_kernel (factor SYRK, 3 x bf16, tcgen05)",
                  "inv_pivot": ("pivot_kernel (128-pivot block: 16 rank-8 fp32 FFMA sweeps)"
                                if os.environ.get("SPDKFAC_PIVOT") != "tc" else
@@ -337,7 +339,7 @@ _KERNEL_NAMES = {"factor_syrk": "tc3_gemm_kernel<BF16> + tc3_pair_kernel (factor
                  "inv_panel": f"stage_panel_kernel + tc3_gemm_kernel<{_INV_KIND}> (inverse panel C = W[:,K] P^-1)",
                  "inv_update": f"tc3_gemm_kernel<{_INV_KIND}, C-tile> (inverse trailing update, 3 x {_INV_KIND.lower()}"
                                + (" planes scaled per matrix)" if _INV_KIND == "F16" else ")"),
-                 "precond_gemm": "tc3_gemm_kernel<TF32, chunked accumulation> (G^-1 grad A^-1, W -= lr P)",
+                 "precond_gemm": f"tc3_gemm_kernel<{_PREC_KIND}, chunked accumulation> (G^-1 grad A^-1, W -= lr P)",
                  "factor_stage": "stage_rows / stage_im2col / stage_spatial (fp32 -> bf16 hi/lo planes)"}
 
 

@@ -30,7 +30,8 @@ _COMM = {"GradComm", "FactorComm", "InverseComm"}
 
 _K = r"tc3_gemm_kernel<(?:\(spd::Kind\))?"
 _RULES = (
-    ("Precondition", r"split_rows_batched|apply_update|" + _K + r"2, \d+, false, [1-9]"),  # TF32, chunked accumulation
+    ("Precondition", r"split_rows_batched|split_rows_f16|packed_row_bounds|apply_update|" + _K +
+     r"[02], \d+, false, [1-9]"),  # TF32 / F16, chunked accumulation
     ("FactorComp", r"stage_rows|stage_im2col|stage_spatial|reduce_pack|tc3_pair|" + _K + "1,"),  # bf16 SYRK
     ("InverseComp", r"pivot_kernel|pivot_tc_kernel|stage_panel|small_inverse|damp_unpack|finalize_kernel|inv_scale|"
                     r"unpack_upper|pack_upper|tc3_pair_ctile|" + _K + "[02],"),  # TF32 / F16 panel + update

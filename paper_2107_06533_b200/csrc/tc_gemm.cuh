@@ -57,6 +57,8 @@ enum EpiMode : int32_t {
   kPackedUpper = 3,  // packed upper triangle of a d x d symmetric target (run.out, run.d):
                      //   P = run.wscale * (run.decay * P + (1 - run.decay) * run.alpha * D), i <= j only
   kUpdate = 4,       // out += run.alpha * D (transposed store; the weight update W -= lr * P)
+  kSplitF16 = 5,     // out planes (fp16) <- split(alpha * D * s_out[j]), transposed store like kSplitTf32, with
+                     // s_out[j] = scale of bound(gmax * amax_b[b_row + j]) written to rs_out (row scaled planes)
 };
 
 // fp32-rows operand maps, passed by value (the activation pointers change between runs; a kernel
@@ -108,7 +110,23 @@ struct TcEpi {
   int32_t pad2_;
   // optional per-target operand-class scales in device memory (kAxpby / kCTile; see kScaleShiftA)
   const float* dscale;
+  // optional per-row operand scales (fp16 planes of row r hold x * s[r]): D[i][j] carries
+  // rs_a[a_row + i] * rs_b[b_row + j], divided out in kAxpby / kUpdate / kSplitF16
+  const float* rs_a;
+  const float* rs_b;
+  // kSplitF16: the bound of output row j (column j of D) is gmax[0] * amax_b[b_row + j]
+  const float* gmax;
+  const float* amax_b;
+  float* rs_out;
 };
+
+// power-of-two scale s with |x s| <= 2^13 for |x| <= bound (fp16 planes: 8x headroom below 65504)
+__device__ __forceinline__ float f16_scale(float bound) {
+  int e = 0;
+  if (bound > 0.f && isfinite(bound)) frexpf(bound, &e);  // bound <= 2^e
+  e = max(min(e, 100), -100);
+  return ldexpf(1.f, 13 - e);
+}
 
 // Epilogue of one 32-column chunk of the accumulator tile: thread row i (TMEM lane),
 // values v[t] = D[i][c*32 + t].  All global reads of a chunk are issued before any
@@ -120,9 +138,18 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
   const int64_t ri = int64_t(it.out_r) + i;
   const int jn = it.n_valid - c * 32;  // valid columns in this chunk (may exceed 32)
   if (ep.mode == kAxpby) {
-    const float alpha =
+    float alpha =
         ep.dscale ? ep.alpha / (scale_of(ep.dscale, it.flags, kScaleShiftA) * scale_of(ep.dscale, it.flags, kScaleShiftB))
                   : ep.alpha;
+    float v_[32];  // per-row unscaled values (fp16 row-scaled operands)
+    if (ep.rs_a) {
+      alpha /= ep.rs_a[it.a_row + (row_ok ? i : 0)];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) v_[t] = (t < jn) ? v[t] / ep.rs_b[it.b_row + c * 32 + t] : 0.f;
+    } else {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) v_[t] = v[t];
+    }
     float* out = static_cast<float*>(ep.out);
     float* base = out + (int64_t(it.out_c) + c * 32) * ep.ld + ri;  // transposed: column j -> row of target
     float old[32];
@@ -132,7 +159,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
     }
 #pragma unroll
     for (int t = 0; t < 32; ++t)
-      if (row_ok && t < jn) base[int64_t(t) * ep.ld] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + alpha * v[t];
+      if (row_ok && t < jn) base[int64_t(t) * ep.ld] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + alpha * v_[t];
     if (it.flags & kMirror) {  // same values, target row ri, 32 contiguous columns
       float* rowp = out + ri * ep.ld + it.out_c + c * 32;
       if (ep.beta != 0.f) {
@@ -141,7 +168,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
       }
 #pragma unroll
       for (int t = 0; t < 32; ++t)
-        if (row_ok && t < jn) rowp[t] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + alpha * v[t];
+        if (row_ok && t < jn) rowp[t] = (ep.beta != 0.f ? ep.beta * old[t] : 0.f) + alpha * v_[t];
     }
     if (ep.out2 != nullptr && row_ok && ep.o2_f16) {  // fp16 planes of (C * s)
       const float sc = scale_of(ep.dscale, it.flags, kScaleShiftO);
@@ -154,8 +181,8 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             __half h0, l0, h1, l1;
-            split_f16(alpha * v[t + 2 * u], sc, h0, l0);
-            split_f16(alpha * v[t + 2 * u + 1], sc, h1, l1);
+            split_f16(alpha * v_[t + 2 * u], sc, h0, l0);
+            split_f16(alpha * v_[t + 2 * u + 1], sc, h1, l1);
             hw[u] = uint32_t(__half_as_ushort(h0)) | (uint32_t(__half_as_ushort(h1)) << 16);
             lw[u] = uint32_t(__half_as_ushort(l0)) | (uint32_t(__half_as_ushort(l1)) << 16);
           }
@@ -168,7 +195,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
         for (int t = 0; t < 32; ++t) {
           if (t < jn) {
             __half h, l;
-            split_f16(alpha * v[t], sc, h, l);
+            split_f16(alpha * v_[t], sc, h, l);
             o2[int64_t(t) * ep.ld2] = h;
             o2[int64_t(t) * ep.ld2 + ep.plane2] = l;
           }
@@ -181,7 +208,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
         for (int t = 0; t < 32; t += 4) {
           float h[4], l[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) split_tf32(alpha * v[t + u], h[u], l[u]);
+          for (int u = 0; u < 4; ++u) split_tf32(alpha * v_[t + u], h[u], l[u]);
           *reinterpret_cast<float4*>(o2 + t) = make_float4(h[0], h[1], h[2], h[3]);
           *reinterpret_cast<float4*>(o2 + ep.plane2 + t) = make_float4(l[0], l[1], l[2], l[3]);
         }
@@ -191,7 +218,7 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
         for (int t = 0; t < 32; ++t) {
           if (t < jn) {
             float h, l;
-            split_tf32(alpha * v[t], h, l);
+            split_tf32(alpha * v_[t], h, l);
             o2[int64_t(t) * ep.ld2] = h;
             o2[int64_t(t) * ep.ld2 + ep.plane2] = l;
           }
@@ -228,9 +255,30 @@ __device__ __forceinline__ void epilogue_chunk(const TcItem& it, const TcEpi& ep
     float old[32];
 #pragma unroll
     for (int t = 0; t < 32; ++t) old[t] = (row_ok && t < jn) ? base[int64_t(t) * ep.ld] : 0.f;
+    const float ra = ep.rs_a ? 1.f / ep.rs_a[it.a_row + (row_ok ? i : 0)] : 1.f;
 #pragma unroll
     for (int t = 0; t < 32; ++t)
-      if (row_ok && t < jn) base[int64_t(t) * ep.ld] = fmaf(run.alpha, v[t], old[t]);
+      if (row_ok && t < jn) {
+        const float x = ep.rs_a ? v[t] * ra / ep.rs_b[it.b_row + c * 32 + t] : v[t];
+        base[int64_t(t) * ep.ld] = fmaf(run.alpha, x, old[t]);
+      }
+  } else if (ep.mode == kSplitF16) {  // fp16 planes of the output rows j, each with its own scale
+    __half* out = static_cast<__half*>(ep.out);
+    const int64_t o0 = (int64_t(it.out_c) + c * 32) * ep.ld + ri;
+    const float ra = ep.alpha / ep.rs_a[it.a_row + (row_ok ? i : 0)];
+    const float g = ep.gmax[0];
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      if (row_ok && t < jn) {
+        const int jb = it.b_row + c * 32 + t;
+        const float so = f16_scale(g * ep.amax_b[jb]);
+        if (i == 0) ep.rs_out[it.out_c + c * 32 + t] = so;  // the same value from every CTA of this column
+        __half h, l;
+        split_f16(v[t] * ra / ep.rs_b[jb], so, h, l);
+        out[o0 + int64_t(t) * ep.ld] = h;
+        out[o0 + int64_t(t) * ep.ld + ep.plane_stride] = l;
+      }
+    }
   } else {  // kPackedUpper: global row gi = out_r + i, columns gj = out_c + c*32 + t, keep gj >= gi
     // target / dim / scale from the epilogue table (factor groups) or the run arguments (single plan)
     float* out = static_cast<float*>(ep.out ? ep.out : run.out);

@@ -17,8 +17,8 @@ CATS = [  # (category, kernel-name regex) -- first match wins
     ("inv_panel", r"stage_panel|inv_scale|tc3_gemm_kernel<(\(spd::Kind\))?[02], (\(int\))?3, (\(bool\))?(0|false), (\(int\))?0[,>]"),
     ("inv_update", r"tc3_gemm_kernel<(\(spd::Kind\))?[02], (\(int\))?3, (\(bool\))?(1|true)|tc3_pair_ctile"),
     ("inv_unpack_finalize", r"damp_unpack|finalize_kernel"),
-    ("precond_gemm", r"tc3_gemm_kernel<(\(spd::Kind\))?2, (\(int\))?3, (\(bool\))?(0|false), (\(int\))?[1-9]"),
-    ("precond_split", r"split_rows_batched|stage_packed"),
+    ("precond_gemm", r"tc3_gemm_kernel<(\(spd::Kind\))?[02], (\(int\))?3, (\(bool\))?(0|false), (\(int\))?[1-9]"),
+    ("precond_split", r"split_rows_batched|split_rows_f16|packed_row_bounds|stage_packed"),
     ("pack", r"pack_|unpack_"),
 ]
 

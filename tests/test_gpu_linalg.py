@@ -272,9 +272,13 @@ def test_precondition_golden_and_kat():
         K.precondition(torch.zeros(2, 3), torch.eye(2), torch.eye(2))
 
 
-def test_precond_stage_packed_matches_stage_inverses():
+@pytest.mark.parametrize("f16", ["0", "1"])
+def test_precond_stage_packed_matches_stage_inverses(f16, monkeypatch):
     """PrecondPlan.stage_packed (the broadcast path: packed inverse -> full + operand planes in one
-    pass) gives bit-identical preconditioned gradients and full inverses to unpack + stage_inverses."""
+    pass) gives the same preconditioned gradients and bit-identical full inverses as unpack +
+    stage_inverses: bit-identical on tf32 planes; on fp16 planes (opt-in SPDKFAC_PRECOND_F16=1) the two
+    routes scale the inverse rows differently (exact row maxima vs the SPD diagonal bound): equal to 1e-6."""
+    monkeypatch.setenv("SPDKFAC_PRECOND_F16", f16)
     K = _K()
     rng = np.random.default_rng(9)
     shapes = [(70, 130), (200, 64)]
@@ -296,7 +300,7 @@ def test_precond_stage_packed_matches_stage_inverses():
     p2.run_bound(0.0, inverses_staged=True)
     torch.cuda.synchronize()
     for x, y in zip(out1, out2):
-        assert torch.equal(x, y)
+        assert torch.equal(x, y) if f16 == "0" else relf(x, y.double().cpu().numpy()) <= 1e-6
     for f, m in zip(full_a + full_g, a_inv + g_inv):
         assert torch.equal(f, m)
 
