@@ -20,6 +20,12 @@ zero_grad(set_to_none=True): backward then writes each weight gradient straight 
 tensor (no zero-fill and no accumulate-add kernel per parameter), and the replays reuse those
 same addresses.
 
+Input prefetch: `prefetch(inputs, targets)` starts the host->device copy of the NEXT step's batch
+on a copy stream into one of two device staging slots while the current replay runs; the next
+call without inputs waits for that copy and moves the slot into the static buffers with a
+device-to-device copy (microseconds) before replaying -- the double-buffered loader pattern, so
+the PCIe transfer of batch i+1 overlaps the compute of step i.
+
 The learning rate is read when a graph is captured: the captured kernels carry it as an argument.
 A changed `param_groups[0]["lr"]` raises at the next call unless `recapture_on_lr_change=True`,
 which captures the graphs again (a scheduler stepping every iteration would recapture every
@@ -42,6 +48,12 @@ class GraphedStep:
         self.v = int(getattr(optimizer, "inv_update_freq", 1))
         self.static_in = [t.detach().clone() for t in inputs]
         self.static_tg = [t.detach().clone() for t in targets]
+        # prefetch: two device staging slots for the next batch, filled on a copy stream
+        self._copy_stream = torch.cuda.Stream()
+        self._slots = [[torch.empty_like(t) for t in self.static_in + self.static_tg] for _ in range(2)]
+        self._slot_free = [torch.cuda.Event(), torch.cuda.Event()]
+        self._next_slot = 0
+        self._pending = None  # (slot, copy-done event)
         self.priority = priority
         self.recapture = recapture_on_lr_change
         cur = torch.cuda.current_stream()
@@ -56,6 +68,20 @@ class GraphedStep:
         if before_capture is not None:
             before_capture()
         self._capture_all()
+
+    def prefetch(self, inputs: Sequence[torch.Tensor], targets: Sequence[torch.Tensor]) -> None:
+        """Start copying the next step's batch (pinned host or device tensors) into a device staging
+        slot on the copy stream; the next call without inputs consumes it."""
+        slot = self._next_slot
+        self._next_slot ^= 1
+        cs = self._copy_stream
+        cs.wait_event(self._slot_free[slot])  # the D2D copy that last read this slot has run
+        with torch.cuda.stream(cs):
+            for d, t in zip(self._slots[slot], list(inputs) + list(targets)):
+                d.copy_(t, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        self._pending = (slot, ev)
 
     def _type(self, step: int) -> tuple:
         return (step % self.f == 0, step % self.v == 0)
@@ -104,6 +130,14 @@ class GraphedStep:
         if targets is not None:
             for s, t in zip(self.static_tg, targets):
                 s.copy_(t, non_blocking=True)
+        if inputs is None and targets is None and self._pending is not None:  # the prefetched batch
+            slot, ev = self._pending
+            cur = torch.cuda.current_stream()
+            cur.wait_event(ev)
+            for s, t in zip(self.static_in + self.static_tg, self._slots[slot]):
+                s.copy_(t, non_blocking=True)
+            self._slot_free[slot].record(cur)
+            self._pending = None
         step = getattr(self.opt, "steps", 0)
         t = self._type(step)
         self.graphs[t].replay()

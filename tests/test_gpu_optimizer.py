@@ -110,6 +110,42 @@ def test_graphed_step_matches_eager():
     o2.remove_hooks()
 
 
+def test_graphed_prefetch_matches_direct_inputs():
+    """GraphedStep.prefetch (the next batch copied from pinned host memory on a copy stream while
+    the current replay runs, then moved device-to-device into the graph inputs) gives the same
+    weights as passing each batch to the call."""
+    import torch.nn as nn
+    from paper_2107_06533_b200.graph import GraphedStep
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    from tests.smoke_impl import SmallNet
+    torch.backends.cudnn.deterministic = True
+    torch.backends.cudnn.benchmark = False
+    torch.manual_seed(11)
+    m1, m2 = SmallNet().cuda(), SmallNet().cuda()
+    m2.load_state_dict(m1.state_dict())
+    crit = nn.CrossEntropyLoss()
+    xs = [torch.randn(16, 3, 8, 8) for _ in range(6)]
+    ys = [torch.randint(0, 10, (16,)) for _ in range(6)]
+    xh, yh = [x.pin_memory() for x in xs], [y.pin_memory() for y in ys]
+    o1, o2 = SPDKFAC(m1, lr=0.05, damping=0.1), SPDKFAC(m2, lr=0.05, damping=0.1)
+    g1 = GraphedStep(m1, crit, o1, [xs[0].cuda()], [ys[0].cuda()], warmup=1)
+    g2 = GraphedStep(m2, crit, o2, [xs[0].cuda()], [ys[0].cuda()], warmup=1)
+    l1 = [float(g1([xh[i]], [yh[i]]).item()) for i in range(1, 6)]
+    l2 = []
+    g2.prefetch([xh[1]], [yh[1]])
+    for i in range(1, 6):
+        loss = g2()
+        if i + 1 < 6:
+            g2.prefetch([xh[i + 1]], [yh[i + 1]])
+        l2.append(float(loss.item()))
+    torch.cuda.synchronize()
+    assert l1 == l2
+    for p1, p2 in zip(m1.parameters(), m2.parameters()):
+        assert torch.equal(p1, p2)
+    o1.remove_hooks()
+    o2.remove_hooks()
+
+
 @pytest.mark.parametrize("graphed", [False, True])
 def test_update_in_backward_matches_step(graphed):
     """update_in_backward: early G groups precondition + update during the backward pass (on
