@@ -696,7 +696,9 @@ def run_ours(a):
         out = {"metric": METRIC, "value": round(ms_max, 3), "unit": "ms", "n_gpus": world, "steps": a.steps,
                "warmup": a.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": False, "scaling": "weak",
                "vs_baseline": None, "dtype": "f32",
-               "dtype_note": "fp32-class: 3xbf16 / 3xtf32 split-precision tcgen05 contractions, fp32 accumulate; "
+               "dtype_note": "fp32-class: split-precision tcgen05 contractions with fp32 accumulate -- factors 3xbf16, "
+                             "inverse panels / updates 3xfp16 on power-of-two-scaled planes (3xtf32 for gamma < 1e-4), "
+                             "preconditioning 3xtf32; "
                              "forward/backward fp32 with TF32 convolutions (cuDNN default)",
                "data": "synthetic (random N(0,1) images, uniform labels; random-init torchvision weights)",
                "config": workload_config(a, world), "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
