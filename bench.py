@@ -333,7 +333,7 @@ _ROOF_SPEC = {"factor_syrk": ("tensor", "bf16_tflops_sustained"),
               "inv_panel": ("tensor", _INV_PEAK), "inv_update": ("tensor", _INV_PEAK),
               "precond_gemm": ("tensor", _PREC_PEAK), "factor_stage": ("hbm", "hbm_gbs")}
 _KERNEL_NAMES = {"factor_syrk": "tc3_gemm_kernel<BF16> + tc3_pair_kernel (factor SYRK, 3 x bf16, tcgen05)",
-                 "inv_pivot": ("pivot_kernel (128-pivot block: 16 rank-8 fp32 FFMA sweeps)"
+                 "inv_pivot": ("pivot_kernel (128-pivot block: 16 pipelined 8-pivot sweeps, rank-8 updates on FFMA2)"
                                if os.environ.get("SPDKFAC_PIVOT") != "tc" else
                                "pivot_tc_kernel<false> (128-pivot block: warp sweeps + rank-32 tcgen05 updates)"),
                  "inv_panel": f"stage_panel_kernel + tc3_gemm_kernel<{_INV_KIND}> (inverse panel C = W[:,K] P^-1)",
