@@ -42,6 +42,25 @@ __device__ __forceinline__ void store_split4(__nv_bfloat16* xs, int64_t plane, i
   *reinterpret_cast<uint2*>(xs + plane + o) = lv;
 }
 
+__device__ __forceinline__ void store_split8(__nv_bfloat16* xs, int64_t plane, int64_t o, float4 a, float4 b) {
+  __nv_bfloat16 h[8], l[8];
+  split_bf16(a.x, h[0], l[0]);
+  split_bf16(a.y, h[1], l[1]);
+  split_bf16(a.z, h[2], l[2]);
+  split_bf16(a.w, h[3], l[3]);
+  split_bf16(b.x, h[4], l[4]);
+  split_bf16(b.y, h[5], l[5]);
+  split_bf16(b.z, h[6], l[6]);
+  split_bf16(b.w, h[7], l[7]);
+  uint4 hv, lv;
+  hv.x = pack_bf16x2(h[0], h[1]), hv.y = pack_bf16x2(h[2], h[3]), hv.z = pack_bf16x2(h[4], h[5]);
+  hv.w = pack_bf16x2(h[6], h[7]);
+  lv.x = pack_bf16x2(l[0], l[1]), lv.y = pack_bf16x2(l[2], l[3]), lv.z = pack_bf16x2(l[4], l[5]);
+  lv.w = pack_bf16x2(l[6], l[7]);
+  *reinterpret_cast<uint4*>(xs + o) = hv;
+  *reinterpret_cast<uint4*>(xs + plane + o) = lv;
+}
+
 __device__ __forceinline__ void store_split2(__nv_bfloat16* xs, int64_t plane, int64_t o, float v0, float v1) {
   __nv_bfloat16 h0, l0, h1, l1;
   split_bf16(v0, h0, l0);
@@ -133,7 +152,7 @@ inline RowShape row_shape(int64_t M, int64_t ncol, int rows) {
 // pairs (bf16x2).
 constexpr int kIm2colRows = 32;
 
-template <bool kNhwc, bool kVec>
+template <bool kNhwc, bool kVec, bool kW8 = false>  // kW8: 8 channels per slot (C % 8 == 0), 16-B stores
 __global__ void __launch_bounds__(256) stage_im2col_kernel(const float* __restrict__ x, ConvGeom g, int64_t M,
                                                            int64_t d, __nv_bfloat16* __restrict__ xs, int64_t ld,
                                                            int tpr, int cps, Probe* probe) {
@@ -154,7 +173,7 @@ __global__ void __launch_bounds__(256) stage_im2col_kernel(const float* __restri
   }
   __syncthreads();
   const int64_t plane = M * ld;
-  constexpr int kW = kVec ? 4 : 2;
+  constexpr int kW = kW8 ? 8 : (kVec ? 4 : 2);
   const int kk_n = g.kh * g.kw;
   const int ncol = int(ld / kW), rpar = int(blockDim.x) / tpr;
   const int cs0 = int(threadIdx.x) % tpr, r0 = int(threadIdx.x) / tpr;
@@ -181,17 +200,21 @@ __global__ void __launch_bounds__(256) stage_im2col_kernel(const float* __restri
       c[u] = cc;
     }
     for (int rb = r0; rb < rows; rb += 4 * rpar) {  // 4 rows per pass: loads first, then stores
-      float4 val[4];
+      float4 val[4], val2[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int r = rb + u * rpar;
         val[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        val2[u] = val[u];
         if (r >= rows) continue;
         const int b = s_b[r];
         if constexpr (kVec) {
           const int hi = s_h[r] + ki[0] * g.dh, wi = s_w[r] + kj[0] * g.dw;
-          if (valid[0] && hi >= 0 && hi < g.H && wi >= 0 && wi < g.W)
-            val[u] = __ldg(reinterpret_cast<const float4*>(x + ((int64_t(b) * g.H + hi) * g.W + wi) * g.C + c[0]));
+          if (valid[0] && hi >= 0 && hi < g.H && wi >= 0 && wi < g.W) {
+            const float4* p = reinterpret_cast<const float4*>(x + ((int64_t(b) * g.H + hi) * g.W + wi) * g.C + c[0]);
+            val[u] = __ldg(p);
+            if constexpr (kW8) val2[u] = __ldg(p + 1);
+          }
         } else {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
@@ -209,7 +232,9 @@ __global__ void __launch_bounds__(256) stage_im2col_kernel(const float* __restri
         const int r = rb + u * rpar;
         if (r >= rows) continue;
         const int64_t o = (m0 + r) * ld + j;
-        if constexpr (kVec)
+        if constexpr (kW8)
+          store_split8(xs, plane, o, val[u], val2[u]);
+        else if constexpr (kVec)
           store_split4(xs, plane, o, val[u]);
         else
           store_split2(xs, plane, o, val[u].x, val[u].y);
@@ -685,10 +710,14 @@ int member_stage(Member& mb, const float* x, cudaStream_t s) {
     ConvGeom cg{int(g.n), int(g.c), int(g.h), int(g.w), mb.Ho, mb.Wo, g.kh, g.kw, g.stride_h, g.stride_w,
                 g.pad_h, g.pad_w, g.dil_h, g.dil_w};
     const bool vec = g.layout == SPDKFAC_CONV_A_NHWC && g.c % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
-    const int64_t ncol = mb.ld / (vec ? 4 : 2);
+    const bool vec8 = vec && g.c % 8 == 0;  // 8 channels of one tap per slot, 16-B stores
+    const int64_t ncol = mb.ld / (vec8 ? 8 : vec ? 4 : 2);
     const RowShape rs = row_shape(mb.M, ncol, kIm2colRows);
     if (g.layout == SPDKFAC_CONV_A_NHWC) {
-      if (vec)
+      if (vec8)
+        stage_im2col_kernel<true, true, true><<<rs.grid, rs.threads, 0, s>>>(x, cg, mb.M, mb.d, mb.xt, mb.ld, rs.tpr,
+                                                                            rs.cps, pr);
+      else if (vec)
         stage_im2col_kernel<true, true><<<rs.grid, rs.threads, 0, s>>>(x, cg, mb.M, mb.d, mb.xt, mb.ld, rs.tpr, rs.cps, pr);
       else
         stage_im2col_kernel<true, false><<<rs.grid, rs.threads, 0, s>>>(x, cg, mb.M, mb.d, mb.xt, mb.ld, rs.tpr,
