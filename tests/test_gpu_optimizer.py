@@ -77,6 +77,28 @@ def test_nonpd_raises_on_next_step():
     opt.remove_hooks()
 
 
+def test_nonpd_detected_after_next_inversion():
+    """A failed inversion of step N is still reported when step N+1's forward pass has already
+    launched (and finished) its own, successful A inversion: each eager step's info goes to its own
+    pinned slot, so the next one cannot overwrite it before step() checks it."""
+    import torch.nn as nn
+    from paper_2107_06533_b200.linalg import NotPositiveDefiniteError
+    from paper_2107_06533_b200.optimizer import SPDKFAC
+    lin = nn.Linear(4, 3, bias=False).cuda()
+    opt = SPDKFAC(lin, lr=0.1, damping=0.0)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    # step 0: A = 0 (singular at gamma = 0), G full rank (random output weights)
+    (lin(torch.zeros(64, 4, device="cuda")) * torch.randn(64, 3, device="cuda", generator=g)).sum().backward()
+    opt.step()
+    opt.zero_grad(set_to_none=False)
+    # step 1: both factors full rank; its A inversion runs (and succeeds) in the forward hooks
+    (lin(torch.randn(64, 4, device="cuda", generator=g)) * torch.randn(64, 3, device="cuda", generator=g)).sum().backward()
+    torch.cuda.synchronize()
+    with pytest.raises(NotPositiveDefiniteError):
+        opt.step()
+    opt.remove_hooks()
+
+
 def test_graphed_step_matches_eager():
     """One CUDA-graph replay per iteration gives the same weights as the eager step."""
     import torch.nn as nn
