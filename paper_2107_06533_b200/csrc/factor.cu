@@ -74,13 +74,13 @@ __device__ __forceinline__ void store_split2(__nv_bfloat16* xs, int64_t plane, i
 // d % 4 == 0, x 16-B aligned -> float4 loads, 2 x 8-B stores.
 constexpr int kStageRows = 32;
 
-template <bool kVec>
+template <bool kVec, bool kW8 = false>  // kW8: 8 columns per slot (d % 8 == 0), 16-B stores
 __global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict__ x, int64_t M, int64_t d,
                                                          int64_t ldx, __nv_bfloat16* __restrict__ xs, int64_t ld,
                                                          int tpr, int cps, Probe* probe) {
   probe_start(probe);
   const int64_t plane = M * ld;
-  constexpr int kW = kVec ? 4 : 2;
+  constexpr int kW = kW8 ? 8 : (kVec ? 4 : 2);
   const int64_t m0 = int64_t(blockIdx.x) * kStageRows;
   const int ncol = int(ld / kW), rpar = int(blockDim.x) / tpr;
   const int cs0 = int(threadIdx.x) % tpr, r0 = int(threadIdx.x) / tpr;
@@ -89,15 +89,19 @@ __global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict
   for (int cs = int(blockIdx.y) * cps + cs0; cs < cs_end; cs += tpr) {
     const int j = cs * kW;
     for (int rb = r0; rb < rows; rb += 4 * rpar) {  // 4 rows per pass: loads first, then stores
-      float4 val[4];
+      float4 val[4], val2[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int r = rb + u * rpar;
         const float* src = x + (m0 + r) * ldx + j;
         val[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        val2[u] = val[u];
         if (r < rows) {
           if constexpr (kVec) {
-            if (j < d) val[u] = __ldg(reinterpret_cast<const float4*>(src));
+            if (j < d) {
+              val[u] = __ldg(reinterpret_cast<const float4*>(src));
+              if constexpr (kW8) val2[u] = __ldg(reinterpret_cast<const float4*>(src) + 1);
+            }
           } else {
             if (j < d) val[u].x = __ldg(src);
             if (j + 1 < d) val[u].y = __ldg(src + 1);
@@ -108,7 +112,9 @@ __global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict
       for (int u = 0; u < 4; ++u) {
         const int r = rb + u * rpar;
         if (r < rows) {
-          if constexpr (kVec)
+          if constexpr (kW8)
+            store_split8(xs, plane, (m0 + r) * ld + j, val[u], val2[u]);
+          else if constexpr (kVec)
             store_split4(xs, plane, (m0 + r) * ld + j, val[u]);
           else
             store_split2(xs, plane, (m0 + r) * ld + j, val[u].x, val[u].y);
@@ -701,8 +707,12 @@ int member_stage(Member& mb, const float* x, cudaStream_t s) {
     // inputs of channels-last 1x1 stride-1 convs: rows [b*h*w][C]
     const int64_t ldx = g.layout == SPDKFAC_ROWS ? g.w : g.c;
     const bool vec = ldx % 4 == 0 && mb.d % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
-    const RowShape rs = row_shape(mb.M, mb.ld / (vec ? 4 : 2), kStageRows);
-    if (vec)
+    const bool vec8 = vec && mb.d % 8 == 0;
+    const RowShape rs = row_shape(mb.M, mb.ld / (vec8 ? 8 : vec ? 4 : 2), kStageRows);
+    if (vec8)
+      stage_rows_kernel<true, true><<<rs.grid, rs.threads, 0, s>>>(x, mb.M, mb.d, ldx, mb.xt, mb.ld, rs.tpr, rs.cps,
+                                                                   pr);
+    else if (vec)
       stage_rows_kernel<true><<<rs.grid, rs.threads, 0, s>>>(x, mb.M, mb.d, ldx, mb.xt, mb.ld, rs.tpr, rs.cps, pr);
     else
       stage_rows_kernel<false><<<rs.grid, rs.threads, 0, s>>>(x, mb.M, mb.d, ldx, mb.xt, mb.ld, rs.tpr, rs.cps, pr);
