@@ -71,7 +71,9 @@ class GraphedStep:
 
     def prefetch(self, inputs: Sequence[torch.Tensor], targets: Sequence[torch.Tensor]) -> None:
         """Start copying the next step's batch (pinned host or device tensors) into a device staging
-        slot on the copy stream; the next call without inputs consumes it."""
+        slot on the copy stream; the next call without inputs consumes it.  One batch is pending at a
+        time (a second prefetch before the call replaces the first); the source tensors must stay
+        alive until that call."""
         slot = self._next_slot
         self._next_slot ^= 1
         cs = self._copy_stream
