@@ -1145,6 +1145,9 @@ struct spdkfac_inverse_plan {
   int n_blocked;
   int steps;
   std::vector<int> act_off, act_cnt, pan_off, pan_cnt, upd_off, upd_cnt, pj_off, u1_cnt;
+  std::vector<int> u1d_cnt;     // per step: U1 items of the diagonal tile (k+1, k+1), first in U1
+  bool diag_first = true;       // pivot(k+1) starts after U1's diagonal tiles (SPDKFAC_DIAG_FIRST=0: after all of U1)
+  cudaEvent_t ev_diag = nullptr;
   std::vector<double> upd_flops, u2_flops;  // per step: U1 / U2 tensor work (algorithmic, per launch)
   cudaStream_t side = nullptr;  // look-ahead stream: pivot/stage/panel of step k+1
   bool lookahead = true;        // SPDKFAC_NO_LOOKAHEAD=1 serialises (diagnostics)
@@ -1503,6 +1506,13 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     } else {
       std::stable_sort(u2v.begin(), u2v.end(), [](const TcItem& a, const TcItem& b) { return a.nk > b.nk; });
     }
+    // the diagonal tiles (k+1, k+1) first: the look-ahead pivot only needs them
+    std::stable_partition(u1v.begin(), u1v.end(), [&](const TcItem& it) {
+      return it.out_r == (k + 1) * kB && it.out_c == (k + 1) * kB;
+    });
+    p->u1d_cnt.push_back(int(std::count_if(u1v.begin(), u1v.end(), [&](const TcItem& it) {
+      return it.out_r == (k + 1) * kB && it.out_c == (k + 1) * kB;
+    })));
     u1 = int(u1v.size());
     items.insert(items.end(), u1v.begin(), u1v.end());
     items.insert(items.end(), u2v.begin(), u2v.end());
@@ -1549,6 +1559,8 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     if (const char* pc = getenv("SPDKFAC_PANEL_CTAS")) p->panel_ctas = atoi(pc);
     const char* e = getenv("SPDKFAC_NO_LOOKAHEAD");
     p->lookahead = !(e && e[0] == '1');
+    const char* df = getenv("SPDKFAC_DIAG_FIRST");
+    p->diag_first = !(df && df[0] == '0');
     // the fp32 FFMA pivot sweep is the default: the tcgen05 pivot kernel (SPDKFAC_PIVOT=tc) is 1.6x
     // faster per block but its 32-wide blocked sweep loses accuracy on rank-deficient factors
     // (ResNet-50 fc A, kappa 2e4: inverse error 2.6e-2 vs 5e-3), see DESIGN.md
@@ -1559,6 +1571,7 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   if (p->n_blocked > 0) {
     SPD_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
     SPD_CUDA(cudaEventCreateWithFlags(&p->ev_u1, cudaEventDisableTiming));
+    SPD_CUDA(cudaEventCreateWithFlags(&p->ev_diag, cudaEventDisableTiming));
     SPD_CUDA(cudaEventCreateWithFlags(&p->ev_panel, cudaEventDisableTiming));
   }
   static bool attrs = false;
@@ -1605,10 +1618,8 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
     }
     stat_end(kCatInvUnpackFinal, s, 0, 0);
     // step k's pivot -> stage -> panel GEMM on stream q (the critical chain)
-    auto front = [&](int k, cudaStream_t q) -> int {
+    auto front_pivot = [&](int k, cudaStream_t q) -> int {
       const int na = p->act_cnt[k];
-      void* pa = f16 ? static_cast<void*>(reinterpret_cast<__half*>(p->panA) + (k % kPanSlots) * kB)
-                     : static_cast<void*>(p->panA + (k % kPanSlots) * kB);
       Probe* pr = stat_begin(kCatInvPivot, q);
       if (p->legacy_pivot && p->pivot_v3)
         pivot_kernel<true><<<na, 512, 0, q>>>(p->mats, p->act_ids + p->act_off[k], k, p->pinvS,
@@ -1621,6 +1632,11 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
                                                                      int64_t(p->n_blocked) * kB * kB, int(f16), 0.f, pr);
       SPD_CHECK_LAUNCH();
       stat_end(kCatInvPivot, q, 2.0 * kB * kB * kB * na, 0);
+      return SPDKFAC_OK;
+    };
+    auto front_panel = [&](int k, cudaStream_t q) -> int {
+      void* pa = f16 ? static_cast<void*>(reinterpret_cast<__half*>(p->panA) + (k % kPanSlots) * kB)
+                     : static_cast<void*>(p->panA + (k % kPanSlots) * kB);
       TcRun prun{};
       prun.probe = stat_begin(kCatInvPanel, q);  // the probe times the panel GEMM launch
       if (f16)
@@ -1639,6 +1655,10 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       stat_end(kCatInvPanel, q, 2.0 * kB * kB * kB * p->pan_cnt[k], 0);
       return SPDKFAC_OK;
     };
+    auto front = [&](int k, cudaStream_t q) -> int {
+      const int rc = front_pivot(k, q);
+      return rc ? rc : front_panel(k, q);
+    };
     const Kind ukind = f16 ? Kind::F16 : Kind::TF32;
     int rc = front(0, s);
     if (rc) return rc;
@@ -1646,14 +1666,26 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       // U1(k): the tiles step k+1 reads; then step k+1's front runs on the side stream
       // while U2(k) (the rest of the trailing update) runs here (look-ahead)
       const int u1 = p->u1_cnt[k], u2 = p->upd_cnt[k] - u1;
+      const bool ahead = k + 1 < p->steps;
+      // U1's diagonal tiles first, so step k+1's pivot (which reads only them) runs beside the rest of U1
+      const bool split = ahead && p->lookahead && p->diag_first && p->u1d_cnt[k] > 0 && p->u1d_cnt[k] < u1;
+      const int u1a = split ? p->u1d_cnt[k] : u1;
       Probe* pu = nullptr;
-      if (u1 > 0) {
+      if (u1a > 0) {
         pu = stat_begin(kCatInvUpdate, s);
-        rc = launch_tc3_ctile(maps, items + p->upd_off[k], epis, u1, s, pu, ukind);
+        rc = launch_tc3_ctile(maps, items + p->upd_off[k], epis, u1a, s, pu, ukind);
+        if (rc) return rc;
+        stat_end(kCatInvUpdate, s, split ? 0.0 : p->upd_flops[k], 0);
+      }
+      if (split) {
+        SPD_CUDA(cudaEventRecord(p->ev_diag, s));
+        SPD_CUDA(cudaStreamWaitEvent(p->side, p->ev_diag, 0));
+        if ((rc = front_pivot(k + 1, p->side))) return rc;
+        pu = stat_begin(kCatInvUpdate, s);
+        rc = launch_tc3_ctile(maps, items + p->upd_off[k] + u1a, epis, u1 - u1a, s, pu, ukind);
         if (rc) return rc;
         stat_end(kCatInvUpdate, s, p->upd_flops[k], 0);
       }
-      const bool ahead = k + 1 < p->steps;
       if (ahead && !p->lookahead) {  // serial order: rest of the update, then the next front
         if (p->pu_cnt[k]) {
           Probe* pp = stat_begin(kCatInvUpdate, s);
@@ -1672,7 +1704,7 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       if (ahead) {
         SPD_CUDA(cudaEventRecord(p->ev_u1, s));
         SPD_CUDA(cudaStreamWaitEvent(p->side, p->ev_u1, 0));
-        if ((rc = front(k + 1, p->side))) return rc;
+        if ((rc = split ? front_panel(k + 1, p->side) : front(k + 1, p->side))) return rc;
         SPD_CUDA(cudaEventRecord(p->ev_panel, p->side));
       }
       if (p->pu_cnt[k]) {
@@ -1699,6 +1731,7 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
 void spdkfac_inverse_plan_destroy(spdkfac_inverse_plan* p) {
   if (!p) return;
   if (p->ev_u1) cudaEventDestroy(p->ev_u1);
+  if (p->ev_diag) cudaEventDestroy(p->ev_diag);
   if (p->ev_panel) cudaEventDestroy(p->ev_panel);
   if (p->side) cudaStreamDestroy(p->side);
   delete p;
