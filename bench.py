@@ -230,7 +230,14 @@ def cpu_reference(model, batch, steps=1, warmup=0):
     for _ in range(warmup):
         cpu_step.time_layer(*small)
     cache = {}
-    per_step = [cpu_step.full_step(shapes, cache=cache) for _ in range(max(1, steps))]
+    # full steps until `steps` are done or the wall budget is spent (at least one): every reported step is a
+    # whole step actually timed, and the arm still ends within a few minutes at the driver's K
+    budget = float(os.environ.get("SPDKFAC_REF_BUDGET_S", "240"))
+    t_start, per_step = time.perf_counter(), []
+    while len(per_step) < max(1, steps):
+        per_step.append(cpu_step.full_step(shapes, cache=cache))
+        if time.perf_counter() - t_start > budget:
+            break
     kind = cpu_step.implementation()[4]
     sample = (f"full step per timed step: all {len(shapes)} {model} K-FAC layers (bs{batch}; {len(keys)} distinct "
               f"shapes), each layer's factor A+G, 2 damped inverses, precondition and update timed (float64 "
@@ -749,6 +756,9 @@ def run_reference(a):
            "cpu_baseline": {"value": round(ms, 1), "unit": "ms", "cores": cores, "kind": kind, "sample": sample},
            "e2e": {"value": round(ms, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "per_step_ms": [round(x * 1e3, 1) for x in per_step], "wall_s": round(wall, 1),
+           "steps_timed": len(per_step),
+           "steps_note": ("every timed step is a full step; steps beyond the wall budget (SPDKFAC_REF_BUDGET_S, "
+                          "default 240 s) are not run, so steps_timed may be < steps"),
            "note": "reference kfacsched is CPU-only numpy/scipy (no GPU path): its own functions from "
                    "baseline/_ref (kind=reference) or the oracle port (kind=port); every timed step is a full "
                    "step (every layer of the model) on this rank's host cores"}
