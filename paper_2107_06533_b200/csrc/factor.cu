@@ -126,6 +126,59 @@ __global__ void __launch_bounds__(256) stage_rows_kernel(const float* __restrict
   probe_stop(probe);
 }
 
+// Deferred row staging of several members in ONE launch (the group's compute): block b stages
+// kStageRows rows of member t (rows [32 (b - blk0[t]), + 32)), every column, 8 columns per slot with
+// two float4 loads and two 16-B stores; 4 slots per thread in flight.  Members qualify with d % 8 == 0,
+// a row stride ldx % 4 == 0 and a 16-B aligned input (the rest stage at stage() time as before).
+constexpr int kBatchStageMax = 64;
+struct StageBatch {
+  const float* x[kBatchStageMax];
+  __nv_bfloat16* xs[kBatchStageMax];
+  int64_t M[kBatchStageMax], ldx[kBatchStageMax], ld[kBatchStageMax];
+  int32_t d[kBatchStageMax];
+  int32_t blk0[kBatchStageMax + 1];
+  int n;
+};
+__global__ void __launch_bounds__(256) stage_rows_batched_kernel(const __grid_constant__ StageBatch a, Probe* probe) {
+  probe_start(probe);
+  const int b = blockIdx.x;
+  int lo = 0, hi = a.n - 1;
+  while (lo < hi) {  // last t with blk0[t] <= b
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.blk0[mid] <= b) lo = mid;
+    else hi = mid - 1;
+  }
+  const int t = lo;
+  const int64_t M = a.M[t], ldx = a.ldx[t], ld = a.ld[t], m0 = int64_t(b - a.blk0[t]) * kStageRows;
+  const int nslot = a.d[t] >> 3;
+  const int rows = int(M - m0 < kStageRows ? M - m0 : int64_t(kStageRows));
+  const int total = rows * nslot;
+  const float* __restrict__ x = a.x[t];
+  __nv_bfloat16* __restrict__ xs = a.xs[t];
+  const int64_t plane = M * ld;
+  for (int base = int(threadIdx.x); base < total; base += 4 * int(blockDim.x)) {
+    float4 v0[4], v1[4];
+    int64_t o[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = base + u * int(blockDim.x);
+      o[u] = -1;
+      if (idx < total) {
+        const int r = idx / nslot, j = (idx - r * nslot) * 8;
+        const float4* src = reinterpret_cast<const float4*>(x + (m0 + r) * ldx + j);
+        v0[u] = __ldg(src);
+        v1[u] = __ldg(src + 1);
+        o[u] = (m0 + r) * ld + j;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (o[u] >= 0) store_split8(xs, plane, o[u], v0[u], v1[u]);
+  }
+  __syncthreads();
+  probe_stop(probe);
+}
+
 // launch shape for M rows of ncol column slots, `rows` rows per block: enough blocks for the
 // 148 SMs (column ranges of cps slots split over blockIdx.y when M is small), tpr threads
 // per row (a multiple of 32 balancing the passes over the range), as many row lanes as fit
@@ -394,6 +447,8 @@ struct Member {
   bool i2c = false;
   int64_t Mst = 0;
   Im2colGeom ig{};
+  // row-layout members staged by the group's compute launch in one batched kernel (stage() records x)
+  bool deferred = false;
 };
 
 namespace {
@@ -412,6 +467,14 @@ int f32_rows_max_blocks() {
 // 3x3 convs) staging -0.23 ms but SYRK +0.37 ms per step (16.74 vs 16.60 ms).
 bool im2col_enabled() {
   const char* e = getenv("SPDKFAC_IM2COL");
+  return e && e[0] == '1';
+}
+// SPDKFAC_BATCH_STAGE=1: row-layout members (d % 8 == 0) are staged by the group's compute in one batched
+// launch instead of at stage() time.  Off by default: measured correct but slower in the step (16.38 /
+// 16.46 vs 16.17 / 16.23 ms): per-member staging on the stage stream overlaps the forward / backward
+// kernels, the batched launch sits in front of the group's SYRK.
+bool batch_stage_enabled() {
+  const char* e = getenv("SPDKFAC_BATCH_STAGE");
   return e && e[0] == '1';
 }
 bool is_rows_layout(const spdkfac_factor_geom& g) {
@@ -511,6 +574,7 @@ int member_init(Member* mb, const spdkfac_factor_geom* g) {
   // k x k channels-last convs on the single-CTA engine: TMA im2col loads instead of an im2col staging pass
   const bool pointwise = g->kh == 1 && g->kw == 1 && g->stride_h == 1 && g->stride_w == 1 && g->pad_h == 0 &&
                          g->pad_w == 0;
+  mb->deferred = batch_stage_enabled() && !mb->f32 && is_rows_layout(*g) && mb->d % 8 == 0 && mb->ldx % 4 == 0;
   mb->i2c = false;
   if (im2col_enabled() && !mb->S && g->layout == SPDKFAC_CONV_A_NHWC && !pointwise && g->c % 64 == 0 &&
       g->pad_h <= 127 && g->pad_w <= 127 && g->stride_h <= 8 && g->stride_w <= 8 &&
@@ -687,6 +751,11 @@ int group_build(spdkfac_factor_group* G, float* const* packed, const float* scal
 
 int member_stage(Member& mb, const float* x, cudaStream_t s) {
   const spdkfac_factor_geom& g = mb.g;
+  if (mb.deferred && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {  // staged by the group's compute
+    mb.x = x;
+    return SPDKFAC_OK;
+  }
+  mb.x = nullptr;  // (an unaligned input of a deferred member is staged right here)
   if (mb.f32) {  // the SYRK reads x itself: bind it (x must stay valid until compute() has run)
     SPD_ARG((reinterpret_cast<uintptr_t>(x) & 15) == 0, SPDKFAC_ERR_ARG, "factor input must be 16-byte aligned");
     mb.x = x;
@@ -754,6 +823,31 @@ int group_compute(spdkfac_factor_group* G, float scale, float decay, float world
   double bytes_single = 0, bytes_pair = 0;
   for (const Member& mb : G->m) (mb.S ? bytes_pair : bytes_single) += 4.0 * (mb.f32 ? mb.d : mb.ld) * mb.M;
   int rc;
+  {  // deferred row staging: every such member of the group in one launch per kBatchStageMax members
+    StageBatch sb{};
+    double sbytes = 0;
+    auto flush = [&]() {
+      if (sb.n == 0) return;
+      sb.blk0[sb.n] = sb.blk0[sb.n - 1] + int(cdiv(sb.M[sb.n - 1], kStageRows));
+      Probe* pr = stat_begin(kCatFactorStage, s);
+      stage_rows_batched_kernel<<<sb.blk0[sb.n], 256, 0, s>>>(sb, pr);
+      stat_end(kCatFactorStage, s, 0, sbytes);
+      sb.n = 0, sbytes = 0;
+    };
+    for (Member& mb : G->m) {
+      if (!mb.deferred || !mb.x) continue;
+      if (sb.n == kBatchStageMax) flush();
+      const int t = sb.n;
+      sb.x[t] = mb.x, sb.xs[t] = mb.xt, sb.M[t] = mb.M, sb.ldx[t] = mb.ldx, sb.ld[t] = mb.ld;
+      sb.d[t] = int32_t(mb.d);
+      sb.blk0[t] = t == 0 ? 0 : sb.blk0[t - 1] + int(cdiv(sb.M[t - 1], kStageRows));
+      sbytes += 8.0 * double(mb.M) * mb.d;
+      ++sb.n;
+      mb.x = nullptr;  // consumed: the next compute needs a new stage()
+    }
+    flush();
+    SPD_CHECK_LAUNCH();
+  }
   if (G->n_items) {
     bool any_f32 = false;
     for (const Member& mb : G->m) any_f32 |= mb.f32;
