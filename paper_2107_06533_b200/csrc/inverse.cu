@@ -1569,7 +1569,10 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     p->pivot_v3 = !(pv && std::string(pv) == "b8");
   }
   if (p->n_blocked > 0) {
-    SPD_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+    {
+      const char* pe = getenv("SPDKFAC_INV_PRIORITY");
+      SPD_CUDA(cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, pe ? atoi(pe) : 0));
+    }
     SPD_CUDA(cudaEventCreateWithFlags(&p->ev_u1, cudaEventDisableTiming));
     SPD_CUDA(cudaEventCreateWithFlags(&p->ev_diag, cudaEventDisableTiming));
     SPD_CUDA(cudaEventCreateWithFlags(&p->ev_panel, cudaEventDisableTiming));

@@ -260,8 +260,11 @@ class SPDKFAC(torch.optim.Optimizer):
         # tensor-core convolutions instead of on the forward/backward stream
         self.stage_stream = torch.cuda.Stream(self.device)
         self._stage_refs = []  # inputs staged on stage_stream, kept alive until step() joins it
-        self.inv_stream = torch.cuda.Stream(self.device)
-        self._g_streams = {side: torch.cuda.Stream(self.device) for side in self._early}
+        # the inversion chains (latency-bound) may run at a higher stream priority than the throughput work
+        # (SPDKFAC_INV_PRIORITY, e.g. -1; default 0); the inverse plan's look-ahead stream follows the env too
+        inv_prio = int(os.environ.get("SPDKFAC_INV_PRIORITY", "0"))
+        self.inv_stream = torch.cuda.Stream(self.device, priority=inv_prio)
+        self._g_streams = {side: torch.cuda.Stream(self.device, priority=inv_prio) for side in self._early}
         # index of the early G group whose launch issues the A-inverse broadcast (default: the last)
         self._a_bcast_after = int(os.environ.get("SPDKFAC_A_BCAST_AFTER", len(self._early) - 1))
         self._g_count = 0
