@@ -352,6 +352,14 @@ _KERNEL_NAMES = {"factor_syrk": "tc3_gemm_kernel<BF16> + tc3_pair_kernel (factor
                  "factor_stage": "stage_rows / stage_im2col / stage_spatial (fp32 -> bf16 hi/lo planes)"}
 
 
+def torch_sm_count():
+    try:
+        import torch
+        return torch.cuda.get_device_properties(0).multi_processor_count
+    except Exception:
+        return None
+
+
 def kernel_roofline(cat, rec, per, peaks, world, model):
     """Roofline of one kernel category from its live CUDA-event time and the algorithmic work the
     library declares per launch (flops: SURVEY 8(d) per-unit figures x units; bytes: staging)."""
@@ -370,6 +378,13 @@ def kernel_roofline(cat, rec, per, peaks, world, model):
                      "last step (graph mode) or all timed steps (eager)",
            ("algorithmic_bytes_per_step" if bound == "hbm" else "algorithmic_flops_per_step"): work,
            "traffic": None}
+    if cat == "inv_pivot" and peak and ms > 0 and launches > 0:
+        # one CTA (one SM) per active 128-block: the kernel is a latency chain that occupies few SMs, so also
+        # report the fraction of the FFMA rate of the SMs it actually holds (2*128^3 flop per CTA)
+        ctas = (work / launches) / (2.0 * 128 ** 3)
+        sms = torch_sm_count()
+        out["ctas_per_launch"] = round(ctas, 1)
+        out["frac_of_occupied_sms"] = round(ach / (peak * min(1.0, ctas / sms)), 4) if sms else None
     try:  # DRAM bytes per launch from a committed `ncu --set full` capture of the same launches
         t = json.load(open(os.path.join(ROOT, "profiles", f"traffic_{model}_n{world}.json")))[cat]
         out["traffic"] = round(t["dram_bytes_per_step"] / max(launches, 1e-9))
