@@ -1168,6 +1168,7 @@ struct spdkfac_inverse_plan {
   TcItem* items16;              // the same with K blocks of 64 (fp16)
   TcEpi* epis16;
   TcPairCItem* pitems;          // per step: CTA-pair super tiles of the bulk update (U2)
+  TcPairCItem* pitems16;        // the same with K blocks of 64 (fp16)
   std::vector<int> pu_off, pu_cnt;
   std::vector<double> pu_flops;
   TcEpi* epis;                  // [0, n): update, [n + q n, n + (q + 1) n): panel writing panC slot q
@@ -1253,12 +1254,13 @@ size_t inverse_carve(int n, const int32_t* dims, Carve& c, spdkfac_inverse_plan*
   auto* it16 = c.take<TcItem>(size_t(std::max<int64_t>(items, 1)));
   auto* ep16 = c.take<TcEpi>(size_t(1 + kPanSlots) * n);
   auto* pit = c.take<TcPairCItem>(size_t(std::max<int64_t>(items / 4, 1)));
+  auto* pit16 = c.take<TcPairCItem>(size_t(std::max<int64_t>(items / 4, 1)));
   auto* ep = c.take<TcEpi>(size_t(1 + kPanSlots) * n);
   if (p) {
     p->panA = panA, p->panC = panC, p->pinvS = pinvS, p->mats = dm, p->small_ids = sid, p->blocked_ids = bid;
     p->act_ids = aid, p->tiles = tj, p->pan_jobs = pj, p->maps = mp, p->items = it, p->epis = ep;
     p->maps16 = mp16, p->items16 = it16, p->epis16 = ep16;
-    p->pitems = pit;
+    p->pitems = pit, p->pitems16 = pit16;
     p->plane_rows = rows, p->steps = steps, p->n_tiles = int(tiles);
   }
   return c.used;
@@ -1284,7 +1286,7 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   p->dims.assign(dims, dims + n);
   {
     const char* e = getenv("SPDKFAC_INV_TF32");
-    p->f16 = !(e && e[0] == '1') && !update_pairs();
+    p->f16 = !(e && e[0] == '1');
   }
   const int bk = 32;  // K elements per 128-byte tf32 operand row (the fp16 item copies hold half as many blocks)
   Carve c(ws, ws_bytes);
@@ -1437,7 +1439,7 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
     // rest stay single-CTA items
     p->pu_off.push_back(int(pitems.size()));
     p->pu_flops.push_back(0.0);
-    if (update_pairs()) {  // (tf32 only: the plan then never runs on fp16 planes)
+    if (update_pairs()) {
       std::map<std::tuple<int, int, int>, size_t> at;  // (matrix, I, J) -> index in u2v
       for (size_t x = 0; x < u2v.size(); ++x)
         at[{u2v[x].epi, u2v[x].out_c / kB, u2v[x].out_r / kB}] = x;
@@ -1474,6 +1476,7 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
             pi.k0 = q0.k0, pi.nk = q0.nk, pi.epi = t;
             pi.out_r[0] = J0 * kB, pi.out_r[1] = (J0 + 1) * kB;
             pi.out_c[0] = I0 * kB, pi.out_c[1] = (I0 + 1) * kB;
+            pi.flags = q0.flags & ((3 << kScaleShiftA) | (3 << kScaleShiftB));  // uniform over the super tile
             pitems.push_back(pi);
             p->pu_flops.back() += n_up * 2.0 * kB * kB * 32 * q0.nk;
             for (size_t e : ix)
@@ -1546,12 +1549,15 @@ int spdkfac_inverse_plan_create(spdkfac_inverse_plan** out, int n, const int32_t
   }
   std::vector<TcItem> items16(items);
   for (TcItem& it : items16) it.nk /= 2;  // K blocks of 64 fp16 elements (tf32: 32)
+  std::vector<TcPairCItem> pitems16(pitems);
+  for (TcPairCItem& it : pitems16) it.nk /= 2;
   if ((rc = upload(p->mats, mats, s)) || (rc = upload(p->small_ids, small, s)) ||
       (rc = upload(p->blocked_ids, blocked, s)) || (rc = upload(p->act_ids, act, s)) ||
       (rc = upload(p->tiles, tiles, s)) || (rc = upload(p->pan_jobs, pan, s)) || (p->n_blocked > 0 && (rc = upload(p->maps, maps, s))) ||
       (p->n_blocked > 0 && (rc = upload(p->maps16, maps16, s))) || (rc = upload(p->items16, items16, s)) ||
       (rc = upload(p->epis16, epis16, s)) ||
-      (rc = upload(p->items, items, s)) || (rc = upload(p->pitems, pitems, s)) || (rc = upload(p->epis, epis, s))) {
+      (rc = upload(p->items, items, s)) || (rc = upload(p->pitems, pitems, s)) ||
+      (rc = upload(p->pitems16, pitems16, s)) || (rc = upload(p->epis, epis, s))) {
     delete p;
     return rc;
   }
@@ -1692,7 +1698,9 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       if (ahead && !p->lookahead) {  // serial order: rest of the update, then the next front
         if (p->pu_cnt[k]) {
           Probe* pp = stat_begin(kCatInvUpdate, s);
-          if ((rc = launch_tc3_pair_ctile(p->maps, p->pitems + p->pu_off[k], p->epis, p->pu_cnt[k], s, pp))) return rc;
+          if ((rc = launch_tc3_pair_ctile(maps, (f16 ? p->pitems16 : p->pitems) + p->pu_off[k], epis, p->pu_cnt[k], s, pp,
+                                          ukind)))
+            return rc;
           stat_end(kCatInvUpdate, s, p->pu_flops[k], 0);
         }
         if (u2 > 0) {  // (non-last steps of a fused group have no U2)
@@ -1712,7 +1720,9 @@ int spdkfac_inverse_plan_run(spdkfac_inverse_plan* p, float gamma, void* stream)
       }
       if (p->pu_cnt[k]) {
         Probe* pp = stat_begin(kCatInvUpdate, s);
-        if ((rc = launch_tc3_pair_ctile(p->maps, p->pitems + p->pu_off[k], p->epis, p->pu_cnt[k], s, pp))) return rc;
+        if ((rc = launch_tc3_pair_ctile(maps, (f16 ? p->pitems16 : p->pitems) + p->pu_off[k], epis, p->pu_cnt[k], s, pp,
+                                          ukind)))
+            return rc;
         stat_end(kCatInvUpdate, s, p->pu_flops[k], 0);
       }
       if (u2 > 0) {

@@ -308,12 +308,14 @@ int launch_tc3_pair(const CUtensorMap* maps, const TcPairItem* items, const TcEp
 }
 
 int launch_tc3_pair_ctile(const CUtensorMap* maps, const TcPairCItem* items, const TcEpi* epis, int n, cudaStream_t s,
-                          Probe* probe) {
+                          Probe* probe, Kind kind) {
   if (n <= 0) return SPDKFAC_OK;
   static bool attr_set = false;
   if (!attr_set) {
-    SPD_CUDA(cudaFuncSetAttribute(tc3_pair_ctile_kernel<kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(kPairCSmemBytes)));
+    SPD_CUDA(cudaFuncSetAttribute(tc3_pair_ctile_kernel<kStages, Kind::TF32>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPairCSmemBytes)));
+    SPD_CUDA(cudaFuncSetAttribute(tc3_pair_ctile_kernel<kStages, Kind::F16>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPairCSmemBytes)));
     attr_set = true;
   }
   static int pairs = 0;
@@ -330,7 +332,10 @@ int launch_tc3_pair_ctile(const CUtensorMap* maps, const TcPairCItem* items, con
   TcRun run{};
   run.probe = probe;
   const int grid = 2 * (n < pairs ? n : pairs);
-  tc3_pair_ctile_kernel<kStages><<<grid, 192, kPairCSmemBytes, s>>>(maps, items, epis, run, n);
+  if (kind == Kind::F16)
+    tc3_pair_ctile_kernel<kStages, Kind::F16><<<grid, 192, kPairCSmemBytes, s>>>(maps, items, epis, run, n);
+  else
+    tc3_pair_ctile_kernel<kStages, Kind::TF32><<<grid, 192, kPairCSmemBytes, s>>>(maps, items, epis, run, n);
   SPD_CHECK_LAUNCH();
   return SPDKFAC_OK;
 }

@@ -100,7 +100,7 @@ int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* 
                      Probe* probe = nullptr, Kind kind = Kind::TF32);
 // CTA-pair TF32 engine with the C-slice ring (256 x 256 super tiles of the inverse trailing update)
 int launch_tc3_pair_ctile(const CUtensorMap* maps, const TcPairCItem* items, const TcEpi* epis, int n_items,
-                          cudaStream_t s, Probe* probe = nullptr);
+                          cudaStream_t s, Probe* probe = nullptr, Kind kind = Kind::TF32);
 // TF32 engine with chunked accumulation (kAccChunk K blocks of 32 per TMEM chunk, chunks summed in
 // fp32 registers): the preconditioning GEMMs (see tc3_gemm_kernel's kAcc)
 constexpr int kAccChunk = 2;  // 64 K elements = 24 accumulating MMAs per TMEM chunk

@@ -884,15 +884,16 @@ struct TcPairCItem {
   int32_t epi;           // epilogue table entry (kAxpby on a C-tile target: alpha, beta, c_map)
   int32_t out_r[2];      // per CTA rank: target column offset (the M block)
   int32_t out_c[2];      // per tile h: target row offset (the N block)
-  int32_t pad_;
+  int32_t flags;         // fp16 operand classes (kScaleShiftA / B; TcEpi::dscale)
 };
 
 constexpr size_t kPairCSmemBytes = size_t(kStages) * kStageBytes + kCRing * kCSliceBytes + 1024 + 256;
 
-template <int kSt>
+template <int kSt, Kind K = Kind::TF32>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     tc3_pair_ctile_kernel(const CUtensorMap* __restrict__ maps, const TcPairCItem* __restrict__ items,
                           const TcEpi* __restrict__ epis, const TcRun run, int n_items) {
+  constexpr int BKp = is_16bit(K) ? 64 : 32;  // K elements per 128-byte operand row
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_align1024(smem_raw);
   float* ctile = reinterpret_cast<float*>(smem + kSt * kStageBytes);  // kCRing x [32][128]
@@ -943,7 +944,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           if (rank == 0) mbar_expect_tx(&full[st], 2u * 4u * kTileBytes);  // both CTAs' A, B hi / lo
           const uint32_t fb = mapa_shared(&full[st], 0);
           uint8_t* sp = smem + st * kStageBytes;
-          const int kc = it.k0 + kb * 32;
+          const int kc = it.k0 + kb * BKp;
           tma_load_3d_pair(sp, am, fb, kc, ar, 0);
           tma_load_3d_pair(sp + kTileBytes, am, fb, kc, ar, 1);
           tma_load_3d_pair(sp + 2 * kTileBytes, bm, fb, kc, br, 0);
@@ -954,7 +955,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {  // ---- MMA issuer (leader only)
-      constexpr uint32_t idesc = make_idesc<Kind::TF32>(256, 256);
+      constexpr uint32_t idesc = make_idesc<K>(256, 256);
       uint32_t g = 0, t = 0;
       for (int item = int(pair); item < n_items; item += int(npairs), ++t) {
         const TcPairCItem it = items[item];
@@ -972,9 +973,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 B of K per 128-B swizzle row
             const uint64_t off = uint64_t(kk * 2);
-            umma_pair_tf32(acc, ahi + off, bhi + off, idesc, (kb | kk) != 0);
-            umma_pair_tf32(acc, ahi + off, blo + off, idesc, 1u);
-            umma_pair_tf32(acc, alo + off, bhi + off, idesc, 1u);
+            if constexpr (is_16bit(K)) {
+              umma_pair_bf16(acc, ahi + off, bhi + off, idesc, (kb | kk) != 0);  // (kind::f16; fp16 via idesc)
+              umma_pair_bf16(acc, ahi + off, blo + off, idesc, 1u);
+              umma_pair_bf16(acc, alo + off, bhi + off, idesc, 1u);
+            } else {
+              umma_pair_tf32(acc, ahi + off, bhi + off, idesc, (kb | kk) != 0);
+              umma_pair_tf32(acc, ahi + off, blo + off, idesc, 1u);
+              umma_pair_tf32(acc, alo + off, bhi + off, idesc, 1u);
+            }
           }
           tc_commit_pair(&empty[st], 3);  // both CTAs' stage free once these retire
         }
@@ -1007,6 +1014,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     for (int item = int(pair); item < n_items; item += int(npairs), ++t) {
       const TcPairCItem it = items[item];
       const TcEpi ep = epis[it.epi];
+      const float calpha = ep.dscale ? ep.alpha / (scale_of(ep.dscale, it.flags, kScaleShiftA) *
+                                                   scale_of(ep.dscale, it.flags, kScaleShiftB))
+                                     : ep.alpha;
       const uint32_t buf = t & 1, use = t >> 1;
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
@@ -1018,7 +1028,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         mbar_wait(&cfull[q], (u2 / kCRing) & 1);
         float* col = ctile + q * (kCSliceBytes / 4) + i;  // slot[j][i] = beta slot[j][i] + alpha D[i][j]
 #pragma unroll
-        for (int uu = 0; uu < 32; ++uu) col[uu * 128] = ep.beta * col[uu * 128] + ep.alpha * v[uu];
+        for (int uu = 0; uu < 32; ++uu) col[uu * 128] = ep.beta * col[uu * 128] + calpha * v[uu];
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
         if (cio) {  // slice complete: store it, then reuse the slot
