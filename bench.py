@@ -97,6 +97,10 @@ def parse(argv=None):
     p.add_argument("--stats-off", action="store_true", help="no per-launch CUDA events in the timed region (diagnostic)")
     p.add_argument("--perf-params", default=None,
                    help="planner cost-model file (perfmodel.read_params); default data/b200_p{N}.params")
+    p.add_argument("--factor-comm", choices=("auto", "reduce", "allreduce", "peer"), default="auto",
+                   help="P > 1 factor aggregation: 'peer' (each group's SYRK output pushed into the owner's inbox over "
+                        "NVLink peer memory, owner-side sum), NCCL 'reduce' onto the owner, or 'allreduce'; auto follows "
+                        "SPDKFAC_FACTOR_COMM, else peer (factor_decay 0, P <= 8) / allreduce")
     p.add_argument("--optimizer", choices=("spdkfac", "sgd"), default="spdkfac",
                    help="sgd = diagnostic floor (forward/backward + SGD, no K-FAC); never the headline")
     return p.parse_args(argv)
@@ -115,7 +119,7 @@ def make_optimizer(a, model, world):
         from paper_2107_06533_b200.perfmodel import read_params
         perf = read_params(a.perf_params)
     return SPDKFAC(model, lr=a.lr, damping=a.damping, factor_update_freq=a.factor_freq, perf=perf,
-                   factor_decay=getattr(a, "factor_decay", 0.0),
+                   factor_decay=getattr(a, "factor_decay", 0.0), factor_comm=getattr(a, "factor_comm", "auto"),
                    inv_update_freq=a.inv_freq, placement=placement, balance=a.balance,
                    fusion=FusionPolicy(fusion),
                    early_g_fraction=tuple(float(f) for f in a.g_fractions.split(",")), launch_groups=a.launch_groups,
@@ -141,6 +145,10 @@ def workload_config(a, world):
                           if a.mode == "graph" else "eager"),
             "memory_format": a.memory_format,
             "main_stream_priority": a.main_priority,
+            "factor_comm": (None if world == 1 else
+                            (a.factor_comm if a.factor_comm != "auto" else
+                             os.environ.get("SPDKFAC_FACTOR_COMM", ("peer" if world <= 8 else "reduce")
+                                            if a.factor_decay == 0 else "allreduce"))),
             "l2": "per-iteration working set (activations, 0.3 GB packed factors, im2col staging) >> 126 MB L2; no flush"}
 
 

@@ -217,6 +217,32 @@ SPDKFAC_API int spdkfac_comm_group_start(void);
 SPDKFAC_API int spdkfac_comm_group_end(void);
 SPDKFAC_API void spdkfac_comm_destroy(spdkfac_comm* c);
 
+/* ------------------------------------------------------------------ peer-memory factor aggregation
+ * factor_comm = "peer" (csrc/peer.cu): the reference's factor sum (_mean_sym, emulator.py:199-200,
+ * 236-241) restricted to the owner of each CT inverse (emulator.py:247-262), done by the SYRK
+ * epilogue itself: every rank's factor-group launch stores its 1/P-scaled packed tiles into the
+ * owner's inbox (CUDA-IPC mapping, one slot per source rank) over NVLink, then signals; the owner
+ * waits for the P-1 signals of the group and adds the slots into its packed factor.
+ *   alloc / free        a device allocation of its own (an IPC handle maps exactly it), zeroed
+ *   handle / open/close cudaIpcGetMemHandle / OpenMemHandle (64-byte handle) / CloseMemHandle
+ *   copy                stream-ordered copy-engine push of a contiguous range into a peer's inbox
+ *   epoch_advance       epoch[0] += 1 on the stream (once per step, on every rank)
+ *   signal              flags[q][slot * world + rank] = *epoch for every peer q != rank (release, sys scope)
+ *   wait_sum            poll flags[slot * world + q] == *epoch for q != rank (timeout_s: *err = slot + 1
+ *                       instead of hanging), then packed[s + i] += sum_{q != rank} inbox[q * stride + s + i]
+ *                       for the n_segs (start, count) int64 pairs at segs_dev (device memory) */
+SPDKFAC_API int spdkfac_peer_alloc(size_t bytes, void** out);
+SPDKFAC_API int spdkfac_peer_free(void* p);
+SPDKFAC_API int spdkfac_peer_handle(void* p, void* handle_out /* 64 bytes */);
+SPDKFAC_API int spdkfac_peer_open(const void* handle /* 64 bytes */, void** out);
+SPDKFAC_API int spdkfac_peer_close(void* p);
+SPDKFAC_API int spdkfac_peer_copy(void* dst, const void* src, size_t bytes, void* stream);
+SPDKFAC_API int spdkfac_peer_epoch_advance(int* epoch, void* stream);
+SPDKFAC_API int spdkfac_peer_signal(int* const* flags, int world, int rank, int slot, const int* epoch, void* stream);
+SPDKFAC_API int spdkfac_peer_wait_sum(const int* flags, int world, int rank, int slot, const int* epoch, int* err,
+                                      double timeout_s, float* packed, const float* inbox, int64_t stride,
+                                      int n_segs, const int64_t* segs_dev, int64_t max_count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

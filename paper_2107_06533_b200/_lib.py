@@ -74,6 +74,16 @@ SIGNATURES = {
     "spdkfac_comm_group_start": (C.c_int, []),
     "spdkfac_comm_group_end": (C.c_int, []),
     "spdkfac_comm_destroy": (None, [_vp]),
+    "spdkfac_peer_alloc": (C.c_int, [_sz, C.POINTER(_vp)]),
+    "spdkfac_peer_free": (C.c_int, [_vp]),
+    "spdkfac_peer_handle": (C.c_int, [_vp, _vp]),
+    "spdkfac_peer_open": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "spdkfac_peer_close": (C.c_int, [_vp]),
+    "spdkfac_peer_copy": (C.c_int, [_vp, _vp, _sz, _vp]),
+    "spdkfac_peer_epoch_advance": (C.c_int, [_vp, _vp]),
+    "spdkfac_peer_signal": (C.c_int, [_pp, C.c_int, C.c_int, C.c_int, _vp, _vp]),
+    "spdkfac_peer_wait_sum": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_double, _vp, _vp, _i64,
+                                        C.c_int, _vp, _i64, _vp]),
 }
 
 _lib = None

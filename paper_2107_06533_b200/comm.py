@@ -78,3 +78,98 @@ class NcclComm:
 
     def __del__(self):
         self.close()
+
+
+class PeerExchange:
+    """Factor aggregation over NVLink peer memory (factor_comm = "peer", csrc/peer.cu).
+
+    Each rank owns one device allocation, mapped into every other rank through CUDA IPC:
+      flags  [n_slots][world] int32  flags[slot][q]: the epoch at which rank q's group `slot` landed
+      inbox  per kind ("A", "G"): [world][size] fp32, row q = rank q's 1/P-scaled packed factors
+    The packed factors of a CT inverse another rank owns reach `remote_ptr(owner, kind, offset)`
+    by a copy-engine push right after the group's SYRK (`push`, default) or straight from the SYRK
+    epilogue (FactorGroup member target = the remote address; SPDKFAC_PEER_PUSH=epilogue: the
+    epilogue's per-row stores cross NVLink as 4-byte writes, measured slower); `signal` then raises
+    this rank's flag in every peer, and the owner's `wait_sum` polls the group's flags and adds the
+    P - 1 inbox rows into its own packed factors (the same sum an NCCL reduce onto the owner forms).
+    `epoch` advances once per step on every rank (inside CUDA graphs too)."""
+
+    def __init__(self, rank: int, world: int, sizes: dict, n_slots: int, device, timeout_s: float | None = None):
+        import os
+        import torch.distributed as dist
+        lib = L.load(require_device=True)
+        if world > 8:
+            raise ValueError("peer-memory aggregation spans one NVSwitch node (world <= 8)")
+        up = lambda x: (x + 255) // 256 * 256  # noqa: E731
+        self._off, off = {}, up(max(1, n_slots * world) * 4)
+        for kind in ("A", "G"):
+            self._off[kind] = off
+            off = up(off + world * int(sizes[kind]) * 4)
+        self.sizes, self.rank, self.world, self.n_slots = dict(sizes), rank, world, n_slots
+        own = C.c_void_p()
+        L.check(lib.spdkfac_peer_alloc(off, C.byref(own)), "peer alloc")
+        h = (C.c_char * 64)()
+        L.check(lib.spdkfac_peer_handle(own, h), "peer handle")
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(h))
+        self.bases = []
+        for q in range(world):
+            if q == rank:
+                self.bases.append(own.value)
+                continue
+            p = C.c_void_p()
+            L.check(lib.spdkfac_peer_open((C.c_char * 64).from_buffer_copy(handles[q]), C.byref(p)), "peer open")
+            self.bases.append(p.value)
+        self._own, self._lib = own.value, lib
+        self._flag_ptrs = (C.c_void_p * world)(*self.bases)
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        self.timeout_s = float(timeout_s if timeout_s is not None else os.environ.get("SPDKFAC_PEER_TIMEOUT_S", "20"))
+
+    def remote_ptr(self, owner: int, kind: str, offset: int) -> int:
+        """Address (in this process) of this rank's inbox row at `offset` elements inside `owner`'s buffer."""
+        return self.bases[owner] + self._off[kind] + (self.rank * self.sizes[kind] + int(offset)) * 4
+
+    def push(self, owner: int, kind: str, offset: int, src: torch.Tensor, stream) -> None:
+        """Copy-engine push of this rank's packed range `src` (at `offset` of its fusion buffer) into
+        its inbox row in `owner`'s buffer, ordered on `stream`."""
+        L.check(self._lib.spdkfac_peer_copy(self.remote_ptr(owner, kind, offset), src.data_ptr(), src.numel() * 4,
+                                            stream.cuda_stream), "peer copy")
+
+    def advance(self, stream) -> None:
+        L.check(self._lib.spdkfac_peer_epoch_advance(self.epoch.data_ptr(), stream.cuda_stream), "peer epoch")
+
+    def signal(self, slot: int, stream) -> None:
+        L.check(self._lib.spdkfac_peer_signal(self._flag_ptrs, self.world, self.rank, int(slot), self.epoch.data_ptr(),
+                                              stream.cuda_stream), "peer signal")
+
+    def wait_sum(self, slot: int, kind: str, packed: torch.Tensor, segs: torch.Tensor | None, max_count: int,
+                 stream) -> None:
+        """Wait for group `slot` from every peer, then packed[s:s+n] += the peers' inbox rows for each
+        (s, n) row of `segs` (int64 [k, 2] on the device; None: wait only)."""
+        n = 0 if segs is None else int(segs.shape[0])
+        L.check(self._lib.spdkfac_peer_wait_sum(
+            self._own, self.world, self.rank, int(slot), self.epoch.data_ptr(), self.err.data_ptr(), self.timeout_s,
+            packed.data_ptr(), self._own + self._off[kind], self.sizes[kind], n,
+            segs.data_ptr() if n else None, int(max_count), stream.cuda_stream), "peer wait/sum")
+
+    def error(self) -> int:
+        """0, or 1 + the slot whose peer signals timed out (synchronises)."""
+        return int(self.err.item())
+
+    def close(self) -> None:
+        if getattr(self, "_lib", None) is None:
+            return
+        torch.cuda.synchronize()
+        for q, b in enumerate(self.bases):
+            if q != self.rank:
+                self._lib.spdkfac_peer_close(b)
+        self._lib.spdkfac_peer_free(self._own)
+        self._lib = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+

@@ -83,6 +83,7 @@ int upload(T* dst, const std::vector<T>& v, cudaStream_t s) {
 
 // Pointer table passed by value (kernel parameter space).
 constexpr int kMaxPtrs = 128;
+constexpr int kMaxPeers = 8;  // ranks of one NVSwitch node (peer-memory factor aggregation)
 struct PtrTable {
   const void* p[kMaxPtrs];
 };

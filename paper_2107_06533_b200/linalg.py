@@ -109,7 +109,10 @@ class FactorGroup:
     """Several factor sides staged one by one and computed by ONE tensor-core launch
     (include/spdkfac.h factor group).  `members`: list of (layout, shape, kernel, stride,
     padding, dilation); `packed`: per member, the fusion-buffer slice it writes; `scales`:
-    per member, the factor normalisation (1/M, or b^2/M for output gradients)."""
+    per member, the factor normalisation (1/M, or b^2/M for output gradients).  A `packed` entry
+    may also be a raw device address (int): a peer rank's inbox mapped through CUDA IPC
+    (comm.PeerExchange), which the SYRK epilogue then writes over NVLink; `device` is then taken
+    from the first tensor entry (or the current device)."""
 
     def __init__(self, members, packed, scales, stream=None):
         lib = L.load(require_device=True)
@@ -127,12 +130,14 @@ class FactorGroup:
             g.pad_h, g.pad_w = (int(v) for v in padding)
             g.dil_h, g.dil_w = (int(v) for v in dilation)
         self.n = n
-        self.device = packed[0].device
-        self._keep = list(packed)
+        tensors = [p for p in packed if isinstance(p, torch.Tensor)]
+        self.device = tensors[0].device if tensors else torch.device("cuda", torch.cuda.current_device())
+        self._keep = tensors
+        addrs = [int(p) if not isinstance(p, torch.Tensor) else p.data_ptr() for p in packed]
         self._ws = _workspace(lib.spdkfac_factor_group_workspace_size(n, geoms), self.device)
         sc = (C.c_float * n)(*[float(x) for x in scales])
         h = C.c_void_p()
-        L.check(lib.spdkfac_factor_group_create(C.byref(h), n, geoms, L.ptr_array([p.data_ptr() for p in packed]),
+        L.check(lib.spdkfac_factor_group_create(C.byref(h), n, geoms, L.ptr_array(addrs),
                                                 sc, self._ws.data_ptr(), self._ws.numel(), _stream(stream)),
                 "factor group")
         self._h, self._lib = h, lib

@@ -93,10 +93,12 @@ class SPDKFAC(torch.optim.Optimizer):
             raise ValueError(f"factor_decay must be in [0, 1), got {factor_decay}")
         if factor_update_freq < 1 or inv_update_freq < 1 or inv_update_freq % factor_update_freq:
             raise ValueError("update frequencies must be >= 1 and inv_update_freq a multiple of factor_update_freq")
-        if factor_comm not in ("auto", "allreduce", "reduce"):
-            raise ValueError(f"factor_comm must be 'auto', 'allreduce' or 'reduce', got {factor_comm!r}")
-        if factor_comm == "reduce" and factor_decay != 0.0:
-            raise ValueError("factor_comm='reduce' needs factor_decay == 0 (the running average needs the aggregate "
+        if factor_comm == "auto":  # deployment override of the automatic choice
+            factor_comm = os.environ.get("SPDKFAC_FACTOR_COMM", "auto")
+        if factor_comm not in ("auto", "allreduce", "reduce", "peer"):
+            raise ValueError(f"factor_comm must be 'auto', 'allreduce', 'reduce' or 'peer', got {factor_comm!r}")
+        if factor_comm in ("reduce", "peer") and factor_decay != 0.0:
+            raise ValueError(f"factor_comm={factor_comm!r} needs factor_decay == 0 (the running average needs the aggregate "
                              "on every rank)")
         if placement not in ("lbp", "seq", "local"):
             raise ValueError(f"placement must be 'lbp', 'seq' or 'local', got {placement!r}")
@@ -192,11 +194,34 @@ class SPDKFAC(torch.optim.Optimizer):
         self._gseen = {"A": [0] * len(self.fwd_plan.groups), "G": [0] * len(self.bwd_plan.groups)}
         # factor aggregation: all-reduce (every rank holds every aggregate, needed for a running
         # average) or, with factor_decay == 0, a sum onto the owner of each CT inverse only
-        # (half the traffic; NCT factors are still all-reduced)
-        self.factor_comm = ("reduce" if factor_decay == 0.0 else "allreduce") if factor_comm == "auto" else factor_comm
+        # (half the traffic; NCT factors are still all-reduced): over NVLink peer memory ("peer",
+        # comm.PeerExchange) or an NCCL reduce ("reduce")
+        # auto: peer-memory aggregation inside one NVSwitch node (P <= 8), the NCCL reduce beyond
+        auto = ("peer" if 1 < self.world <= 8 else "reduce") if factor_decay == 0.0 else "allreduce"
+        self.factor_comm = auto if factor_comm == "auto" else factor_comm
         self._gsegs = {"A": S.reduce_segments(self.fwd_plan, a_off, a_dims, self.placement, 0),
                        "G": S.reduce_segments(self.bwd_plan, g_off, g_dims, self.placement, 1)}
         self._fgroups = None  # per fusion group FactorGroup objects, built after the first iteration
+        # factor_comm = "peer": the grouped SYRK writes CT factors owned elsewhere straight into the
+        # owner's inbox over NVLink (comm.PeerExchange); the owner adds its inbox rows per fusion group
+        self._peer = None
+        if self.world > 1 and self.factor_comm == "peer":
+            from .comm import PeerExchange
+            n_a = len(self.fwd_plan.groups)
+            self._peer_base = {"A": 0, "G": n_a}
+            self._peer = PeerExchange(self.rank, self.world, {"A": size_a, "G": size_g},
+                                      n_a + len(self.bwd_plan.groups), self.device)
+            self._peer_epilogue = os.environ.get("SPDKFAC_PEER_PUSH", "copy") == "epilogue"
+            self._peer_segs, self._peer_out = {}, {}
+            for kind in ("A", "G"):
+                self._peer_out[kind] = [[(s, e, root) for s, e, root in segs if root is not None and root != self.rank]
+                                        for segs in self._gsegs[kind]]
+                lst = []
+                for segs in self._gsegs[kind]:
+                    mine = [(s, e - s) for s, e, root in segs if root == self.rank]
+                    t = torch.tensor(mine, dtype=torch.int64, device=self.device).reshape(-1, 2) if mine else None
+                    lst.append((t, max((n for _, n in mine), default=0)))
+                self._peer_segs[kind] = lst
         self._rec = {"A": [None] * len(self.layers), "G": [None] * len(self.layers)}
 
         # ---- inverses (every rank holds all of them for preconditioning)
@@ -449,6 +474,8 @@ class SPDKFAC(torch.optim.Optimizer):
         nb = x.shape[0] if l.is_conv else x.numel() // x.shape[-1]
         if kind == "A" and self._a_count == 0:
             self._tl("fwd_start", main)
+            if self._peer is not None:  # this step's signals carry the new epoch
+                self._peer.advance(main)
         layout, x = self._prepare(l, x.detach(), kind)
         key = (layout,) + tuple(x.shape)
         capturing = torch.cuda.is_current_stream_capturing()
@@ -511,17 +538,33 @@ class SPDKFAC(torch.optim.Optimizer):
         fs = self.factor_stream
         buf = self.bufA if kind == "A" else self.bufG
         fg = self._fgroups[kind][gid] if self._fgroups is not None else None
-        if fg is not None and fg["seen"] == self._gsize[kind][gid]:
+        grouped = fg is not None and fg["seen"] == self._gsize[kind][gid]
+        peer = grouped and self._peer is not None
+        if grouped:
             fg["staged"].record(self.stage_stream)
             fs.wait_event(fg["staged"])
             fg["obj"].compute(decay, 1.0 / self.world, fs)
+            if peer:  # push this group's factors owned elsewhere into their owners' inboxes, raise the flags
+                if not self._peer_epilogue:
+                    for s, e, root in self._peer_out[kind][gid]:
+                        self._peer.push(root, kind, s, buf[s:e], fs)
+                self._peer.signal(self._peer_base[kind] + gid, fs)
             fg["done"].record(fs)
             fg["pending"] = not capturing
             fg["seen"] = 0
         if self.world > 1:
             cs = self.comm_stream
             cs.wait_stream(fs)
-            if self.factor_comm == "reduce":
+            if peer:
+                nct = [(s, e) for s, e, root in self._gsegs[kind][gid] if root is None]
+                if nct:  # replicated (NCT) inverses: every rank needs the aggregate
+                    with self.comm.group():
+                        for s, e in nct:
+                            self.comm.allreduce_sum(buf[s:e], cs)
+                segs, mx = self._peer_segs[kind][gid]
+                if segs is not None:
+                    self._peer.wait_sum(self._peer_base[kind] + gid, kind, buf, segs, mx, cs)
+            elif self.factor_comm in ("reduce", "peer"):
                 with self.comm.group():
                     for s, e, root in self._gsegs[kind][gid]:
                         if root is None:
@@ -554,7 +597,13 @@ class SPDKFAC(torch.optim.Optimizer):
                     l = self.layers[li]
                     off, d = (l.a_off, l.spec.a_dim) if kind == "A" else (l.g_off, l.spec.g_dim)
                     members.append(geo)
-                    packed.append(buf[off:off + d * (d + 1) // 2])
+                    tgt = buf[off:off + d * (d + 1) // 2]
+                    if self._peer is not None and self._peer_epilogue:  # CT factor owned elsewhere: its inbox row there
+                        t = 2 * li + (0 if kind == "A" else 1)
+                        root = None if t in self.placement.nct else self.placement.owner(t)
+                        if root is not None and root != self.rank:
+                            tgt = self._peer.remote_ptr(root, kind, off)
+                    packed.append(tgt)
                     scales.append(scale)
                     keys[li] = key
                     member[li] = k
@@ -665,6 +714,9 @@ class SPDKFAC(torch.optim.Optimizer):
             self._info_events = [e for e in self._info_events if e[2] >= self.steps]
         else:
             events, self._info_events = self._info_events, []
+        if not previous_steps_only and self._peer is not None and self._peer.error():
+            raise RuntimeError(f"SPDKFAC: peer factor signals of group slot {self._peer.error() - 1} timed out "
+                               f"after {self._peer.timeout_s} s (SPDKFAC_PEER_TIMEOUT_S)")
         for ev, side, _, slot in events:
             ev.synchronize()
             info = self._info_host[side][slot]
@@ -909,8 +961,9 @@ class SPDKFAC(torch.optim.Optimizer):
     # ------------------------------------------------------------------ introspection / checkpoint
     def factor(self, layer: int, kind: str) -> torch.Tensor:
         """Current aggregated (running-average) factor of a layer as a full matrix.  With
-        factor_comm == "reduce" and P > 1 only the owner of the factor's inverse holds the
-        aggregate (placement.owner(2 layer + side)); other ranks hold their own contribution."""
+        factor_comm "reduce" / "peer" and P > 1 only the owner of the factor's inverse holds the
+        aggregate (placement.owner(2 layer + side)); other ranks hold their own contribution
+        ("reduce") or a stale buffer ("peer": their contribution went to the owner's inbox)."""
         from .linalg import unpack_upper
         t = 2 * layer + (0 if kind == "A" else 1)
         return unpack_upper(self._packed(t), self.inv[t].shape[0])
