@@ -226,6 +226,8 @@ SPDKFAC_API void spdkfac_comm_destroy(spdkfac_comm* c);
  *   alloc / free        a device allocation of its own (an IPC handle maps exactly it), zeroed
  *   handle / open/close cudaIpcGetMemHandle / OpenMemHandle (64-byte handle) / CloseMemHandle
  *   copy                stream-ordered copy-engine push of a contiguous range into a peer's inbox
+ *   scatter_f32         the same range pushed to n_dst peers by SM stores over NVLink (16-byte vectors when
+ *                       every dst shares src's address mod 16, else 4-byte)
  *   epoch_advance       epoch[0] += 1 on the stream (once per step, on every rank)
  *   signal              flags[q][slot * world + rank] = *epoch for every peer q != rank (release, sys scope)
  *   wait_sum            poll flags[slot * world + q] == *epoch for q != rank (timeout_s: *err = slot + 1
@@ -237,6 +239,7 @@ SPDKFAC_API int spdkfac_peer_handle(void* p, void* handle_out /* 64 bytes */);
 SPDKFAC_API int spdkfac_peer_open(const void* handle /* 64 bytes */, void** out);
 SPDKFAC_API int spdkfac_peer_close(void* p);
 SPDKFAC_API int spdkfac_peer_copy(void* dst, const void* src, size_t bytes, void* stream);
+SPDKFAC_API int spdkfac_peer_scatter_f32(float* const* dsts, int n_dst, const float* src, int64_t count, void* stream);
 SPDKFAC_API int spdkfac_peer_epoch_advance(int* epoch, void* stream);
 SPDKFAC_API int spdkfac_peer_signal(int* const* flags, int world, int rank, int slot, const int* epoch, void* stream);
 SPDKFAC_API int spdkfac_peer_wait_sum(const int* flags, int world, int rank, int slot, const int* epoch, int* err,

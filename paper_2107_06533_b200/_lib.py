@@ -80,6 +80,7 @@ SIGNATURES = {
     "spdkfac_peer_open": (C.c_int, [_vp, C.POINTER(_vp)]),
     "spdkfac_peer_close": (C.c_int, [_vp]),
     "spdkfac_peer_copy": (C.c_int, [_vp, _vp, _sz, _vp]),
+    "spdkfac_peer_scatter_f32": (C.c_int, [_pp, C.c_int, _vp, _i64, _vp]),
     "spdkfac_peer_epoch_advance": (C.c_int, [_vp, _vp]),
     "spdkfac_peer_signal": (C.c_int, [_pp, C.c_int, C.c_int, C.c_int, _vp, _vp]),
     "spdkfac_peer_wait_sum": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_double, _vp, _vp, _i64,

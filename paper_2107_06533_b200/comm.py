@@ -80,6 +80,14 @@ class NcclComm:
         self.close()
 
 
+class _DeviceArray:
+    """fp32 device memory not owned by torch (the peer allocation), seen through __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
 class PeerExchange:
     """Factor aggregation over NVLink peer memory (factor_comm = "peer", csrc/peer.cu).
 
@@ -87,25 +95,32 @@ class PeerExchange:
       flags  [n_slots][world] int32  flags[slot][q]: the epoch at which rank q's group `slot` landed
       inbox  per kind ("A", "G"): [world][size] fp32, row q = rank q's 1/P-scaled packed factors
     The packed factors of a CT inverse another rank owns reach `remote_ptr(owner, kind, offset)`
-    by a copy-engine push right after the group's SYRK (`push`, default) or straight from the SYRK
+    by a push right after the group's SYRK (`push`: the copy engine, or SM stores with SPDKFAC_PEER_ENGINE=sm) or straight from the SYRK
     epilogue (FactorGroup member target = the remote address; SPDKFAC_PEER_PUSH=epilogue: the
     epilogue's per-row stores cross NVLink as 4-byte writes, measured slower); `signal` then raises
     this rank's flag in every peer, and the owner's `wait_sum` polls the group's flags and adds the
     P - 1 inbox rows into its own packed factors (the same sum an NCCL reduce onto the owner forms).
+    `extra` elements after the inboxes hold the owners' CT inverses: each owner packs its inverses into its
+    own region and pushes them into every peer's region (`push_extra`), then signals a per-side slot.
     `epoch` advances once per step on every rank (inside CUDA graphs too)."""
 
-    def __init__(self, rank: int, world: int, sizes: dict, n_slots: int, device, timeout_s: float | None = None):
+    def __init__(self, rank: int, world: int, sizes: dict, n_slots: int, device, timeout_s: float | None = None,
+                 extra: int = 0):
         import os
         import torch.distributed as dist
         lib = L.load(require_device=True)
         if world > 8:
             raise ValueError("peer-memory aggregation spans one NVSwitch node (world <= 8)")
         up = lambda x: (x + 255) // 256 * 256  # noqa: E731
+        self.sizes, self.rank, self.world, self.n_slots = dict(sizes), rank, world, n_slots
+        # inbox row stride: a multiple of 64 elements, so row q at offset s shares the fusion buffer's alignment
+        self.stride = {k: (int(v) + 63) // 64 * 64 for k, v in sizes.items()}
         self._off, off = {}, up(max(1, n_slots * world) * 4)
         for kind in ("A", "G"):
             self._off[kind] = off
-            off = up(off + world * int(sizes[kind]) * 4)
-        self.sizes, self.rank, self.world, self.n_slots = dict(sizes), rank, world, n_slots
+            off = up(off + world * self.stride[kind] * 4)
+        self._off["X"] = off  # `extra` fp32 elements: the inverse receive regions (same layout on every rank)
+        off = up(off + max(1, int(extra)) * 4)
         own = C.c_void_p()
         L.check(lib.spdkfac_peer_alloc(off, C.byref(own)), "peer alloc")
         h = (C.c_char * 64)()
@@ -122,19 +137,37 @@ class PeerExchange:
             self.bases.append(p.value)
         self._own, self._lib = own.value, lib
         self._flag_ptrs = (C.c_void_p * world)(*self.bases)
+        self.extra = torch.as_tensor(_DeviceArray(own.value + self._off["X"], max(1, int(extra))), device=device)
         self.epoch = torch.zeros(1, dtype=torch.int32, device=device)
         self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        # factor pushes: "ce" (copy engine, overlapping the backward pass without SM time; measured best) or "sm"
+        self.engine = os.environ.get("SPDKFAC_PEER_ENGINE", "ce")
         self.timeout_s = float(timeout_s if timeout_s is not None else os.environ.get("SPDKFAC_PEER_TIMEOUT_S", "20"))
 
     def remote_ptr(self, owner: int, kind: str, offset: int) -> int:
         """Address (in this process) of this rank's inbox row at `offset` elements inside `owner`'s buffer."""
-        return self.bases[owner] + self._off[kind] + (self.rank * self.sizes[kind] + int(offset)) * 4
+        return self.bases[owner] + self._off[kind] + (self.rank * self.stride[kind] + int(offset)) * 4
+
+    def _send(self, dsts, src: torch.Tensor, stream, engine: str) -> None:
+        if engine == "ce":  # copy engine: no SM time, one engine's bandwidth per copy
+            for dst in dsts:
+                L.check(self._lib.spdkfac_peer_copy(dst, src.data_ptr(), src.numel() * 4, stream.cuda_stream),
+                        "peer copy")
+        else:  # SM stores over NVLink, every destination in one launch
+            L.check(self._lib.spdkfac_peer_scatter_f32(L.ptr_array(dsts), len(dsts), src.data_ptr(), src.numel(),
+                                                       stream.cuda_stream), "peer scatter")
+
+    def push_extra_all(self, offset: int, src: torch.Tensor, stream) -> None:
+        """Push `src` (this rank's extra region at `offset` elements) into the same place of every peer."""
+        # SM stores: the inverses are pushed at the end of the critical path, where one copy engine per
+        # destination was measured ~5 ms slower per step (N = 2)
+        self._send([self.bases[q] + self._off["X"] + int(offset) * 4 for q in range(self.world) if q != self.rank],
+                   src, stream, "sm")
 
     def push(self, owner: int, kind: str, offset: int, src: torch.Tensor, stream) -> None:
-        """Copy-engine push of this rank's packed range `src` (at `offset` of its fusion buffer) into
-        its inbox row in `owner`'s buffer, ordered on `stream`."""
-        L.check(self._lib.spdkfac_peer_copy(self.remote_ptr(owner, kind, offset), src.data_ptr(), src.numel() * 4,
-                                            stream.cuda_stream), "peer copy")
+        """Push this rank's packed range `src` (at `offset` of its fusion buffer) into its inbox row in
+        `owner`'s buffer, ordered on `stream`."""
+        self._send([self.remote_ptr(owner, kind, offset)], src, stream, self.engine)
 
     def advance(self, stream) -> None:
         L.check(self._lib.spdkfac_peer_epoch_advance(self.epoch.data_ptr(), stream.cuda_stream), "peer epoch")
@@ -150,8 +183,14 @@ class PeerExchange:
         n = 0 if segs is None else int(segs.shape[0])
         L.check(self._lib.spdkfac_peer_wait_sum(
             self._own, self.world, self.rank, int(slot), self.epoch.data_ptr(), self.err.data_ptr(), self.timeout_s,
-            packed.data_ptr(), self._own + self._off[kind], self.sizes[kind], n,
+            packed.data_ptr(), self._own + self._off[kind], self.stride[kind], n,
             segs.data_ptr() if n else None, int(max_count), stream.cuda_stream), "peer wait/sum")
+
+    def wait(self, slot: int, stream) -> None:
+        """Wait (on `stream`) until every peer raised its flag of `slot` for this step."""
+        L.check(self._lib.spdkfac_peer_wait_sum(
+            self._own, self.world, self.rank, int(slot), self.epoch.data_ptr(), self.err.data_ptr(), self.timeout_s,
+            None, None, 1, 0, None, 0, stream.cuda_stream), "peer wait")
 
     def error(self) -> int:
         """0, or 1 + the slot whose peer signals timed out (synchronises)."""

@@ -60,6 +60,41 @@ __global__ void peer_wait_kernel(const int* flags, int world, int me, int slot, 
   }
 }
 
+struct PeerDsts {
+  float* p[kMaxPeers];
+};
+
+// src[0, n) -> every dst: SM-driven NVLink stores, 16-byte vectors when src and every dst share their
+// address mod 16 (the callers' regions sit at equal offsets of 256-aligned rows), else scalar
+__global__ void __launch_bounds__(512) peer_scatter_kernel(PeerDsts d, int n_dst, const float* __restrict__ src,
+                                                           int64_t n, int vec) {
+  if (!vec) {  // some destination not co-aligned with the source: scalar stores
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+      const float v = src[i];
+      for (int k = 0; k < n_dst; ++k) d.p[k][i] = v;
+    }
+    return;
+  }
+  const int64_t mis = int64_t((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15) / 4;
+  const int64_t head = n < mis ? n : mis;
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x, nth = int64_t(gridDim.x) * blockDim.x;
+  if (tid < head) {
+    const float v = src[tid];
+    for (int k = 0; k < n_dst; ++k) d.p[k][tid] = v;
+  }
+  const int64_t nv = (n - head) / 4;
+  const float4* s4 = reinterpret_cast<const float4*>(src + head);
+  for (int64_t i = tid; i < nv; i += nth) {
+    const float4 v = __ldcs(s4 + i);
+    for (int k = 0; k < n_dst; ++k) reinterpret_cast<float4*>(d.p[k] + head)[i] = v;
+  }
+  const int64_t t0 = head + nv * 4;
+  if (tid < n - t0) {
+    const float v = src[t0 + tid];
+    for (int k = 0; k < n_dst; ++k) d.p[k][t0 + tid] = v;
+  }
+}
+
 struct PeerSeg {
   int64_t start, count;
 };
@@ -129,6 +164,26 @@ int spdkfac_peer_copy(void* dst, const void* src, size_t bytes, void* stream) {
   // copy engine over NVLink: no SM time, contiguous packets (the SYRK epilogue's per-row stores
   // would reach the peer as 4-byte writes)
   SPD_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  return SPDKFAC_OK;
+}
+
+int spdkfac_peer_scatter_f32(float* const* dsts, int n_dst, const float* src, int64_t count, void* stream) {
+  SPD_ARG(dsts && n_dst >= 0 && n_dst <= kMaxPeers && (src || count == 0) && count >= 0, SPDKFAC_ERR_ARG,
+          "bad peer scatter arguments");
+  if (count == 0 || n_dst == 0) return SPDKFAC_OK;
+  PeerDsts d{};
+  int vec = 1;
+  for (int k = 0; k < n_dst; ++k) {
+    SPD_ARG(dsts[k], SPDKFAC_ERR_ARG, "peer scatter: null destination %d", k);
+    if ((reinterpret_cast<uintptr_t>(dsts[k]) ^ reinterpret_cast<uintptr_t>(src)) & 15) vec = 0;
+    d.p[k] = dsts[k];
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(cdiv(count / 4 + 1, 512 * 4), 64)));
+  stat_begin(kCatFactorReduce, s);
+  peer_scatter_kernel<<<grid, 512, 0, s>>>(d, n_dst, src, count, vec);
+  SPD_CHECK_LAUNCH();
+  stat_end(kCatFactorReduce, s, 0, double(count) * 4 * (1 + n_dst));
   return SPDKFAC_OK;
 }
 

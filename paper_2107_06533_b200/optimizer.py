@@ -202,26 +202,7 @@ class SPDKFAC(torch.optim.Optimizer):
         self._gsegs = {"A": S.reduce_segments(self.fwd_plan, a_off, a_dims, self.placement, 0),
                        "G": S.reduce_segments(self.bwd_plan, g_off, g_dims, self.placement, 1)}
         self._fgroups = None  # per fusion group FactorGroup objects, built after the first iteration
-        # factor_comm = "peer": the grouped SYRK writes CT factors owned elsewhere straight into the
-        # owner's inbox over NVLink (comm.PeerExchange); the owner adds its inbox rows per fusion group
-        self._peer = None
-        if self.world > 1 and self.factor_comm == "peer":
-            from .comm import PeerExchange
-            n_a = len(self.fwd_plan.groups)
-            self._peer_base = {"A": 0, "G": n_a}
-            self._peer = PeerExchange(self.rank, self.world, {"A": size_a, "G": size_g},
-                                      n_a + len(self.bwd_plan.groups), self.device)
-            self._peer_epilogue = os.environ.get("SPDKFAC_PEER_PUSH", "copy") == "epilogue"
-            self._peer_segs, self._peer_out = {}, {}
-            for kind in ("A", "G"):
-                self._peer_out[kind] = [[(s, e, root) for s, e, root in segs if root is not None and root != self.rank]
-                                        for segs in self._gsegs[kind]]
-                lst = []
-                for segs in self._gsegs[kind]:
-                    mine = [(s, e - s) for s, e, root in segs if root == self.rank]
-                    t = torch.tensor(mine, dtype=torch.int64, device=self.device).reshape(-1, 2) if mine else None
-                    lst.append((t, max((n for _, n in mine), default=0)))
-                self._peer_segs[kind] = lst
+        self._peer = None  # comm.PeerExchange (factor_comm "peer"), created below
         self._rec = {"A": [None] * len(self.layers), "G": [None] * len(self.layers)}
 
         # ---- inverses (every rank holds all of them for preconditioning)
@@ -254,6 +235,49 @@ class SPDKFAC(torch.optim.Optimizer):
             self._info_host[side] = ([torch.zeros(len(ts), dtype=torch.int32, pin_memory=True) for _ in range(2)]
                                      if ts else None)
             self._bcast[side] = self._bcast_layout(grp[side])
+        # factor_comm = "peer": each fusion group's CT factors owned elsewhere are pushed into the owner's
+        # inbox over NVLink (comm.PeerExchange) and the owner adds its inbox rows; the owners' CT inverses
+        # can travel the same way (SPDKFAC_PEER_BCAST=1: pushed into every peer's receive region of the
+        # allocation right after each inversion; default: the NCCL broadcasts)
+        self._peer_bcast = False
+        if self.world > 1 and self.factor_comm == "peer":
+            from .comm import PeerExchange
+            n_a = len(self.fwd_plan.groups)
+            self._peer_base = {"A": 0, "G": n_a}
+            n_groups = n_a + len(self.bwd_plan.groups)
+            self._peer_bcast = os.environ.get("SPDKFAC_PEER_BCAST", "0") == "1"  # measured no gain: opt-in
+            # receive regions: per inversion side and owner, that owner's packed CT inverses (same layout
+            # on every rank); slot n_groups + k carries side k's "inverses pushed" flags
+            self._bc_off, extra = {}, 0
+            if self._peer_bcast:
+                for side in self._sides:
+                    self._bc_off[side] = []
+                    for ct, dims, buf, views, n in self._bcast[side]:
+                        self._bc_off[side].append(extra)
+                        extra += max(n, 1)
+                self._peer_slot_bc = {side: n_groups + k for k, side in enumerate(self._sides)}
+            self._peer = PeerExchange(self.rank, self.world, {"A": size_a, "G": size_g},
+                                      n_groups + len(self._sides), self.device, extra=extra)
+            if self._peer_bcast:
+                for side in self._sides:
+                    lay = []
+                    for (ct, dims, _, _, n), off in zip(self._bcast[side], self._bc_off[side]):
+                        buf = self._peer.extra[off:off + max(n, 1)]
+                        offs = [sum(S.packed_size(e) for e in dims[:k]) for k in range(len(dims))]
+                        lay.append((ct, dims, buf, [buf[o:o + S.packed_size(d)] for o, d in zip(offs, dims)], n))
+                    self._bcast[side] = lay
+        if self._peer is not None:
+            self._peer_epilogue = os.environ.get("SPDKFAC_PEER_PUSH", "copy") == "epilogue"
+            self._peer_segs, self._peer_out = {}, {}
+            for kind in ("A", "G"):
+                self._peer_out[kind] = [[(s, e, root) for s, e, root in segs if root is not None and root != self.rank]
+                                        for segs in self._gsegs[kind]]
+                lst = []
+                for segs in self._gsegs[kind]:
+                    mine = [(s, e - s) for s, e, root in segs if root == self.rank]
+                    t = torch.tensor(mine, dtype=torch.int64, device=self.device).reshape(-1, 2) if mine else None
+                    lst.append((t, max((n for _, n in mine), default=0)))
+                self._peer_segs[kind] = lst
         # preconditioning + update in groups that follow the G inversion groups (layer sets in
         # backward order): with update_in_backward, an early group's layers are preconditioned
         # and updated on that group's stream as soon as their gradients are accumulated and
@@ -646,7 +670,9 @@ class SPDKFAC(torch.optim.Optimizer):
         if self.world > 1:
             s.wait_stream(self.comm_stream)
         self._tl("a_factors_done", s)
-        self._run_inverse("A", s, exchange=False)  # broadcast in step(), after the all-reduces
+        self._run_inverse("A", s, exchange=False)  # NCCL: broadcast in step(), after the all-reduces
+        if self._peer_bcast:  # peer pushes share no FIFO with the reductions: send right away
+            self._exchange_send("A", s)
         self._tl("a_inverse_done", s)
         self._a_inverted = True
 
@@ -669,6 +695,8 @@ class SPDKFAC(torch.optim.Optimizer):
             if self._a_inverted and side == self._early[min(self._a_bcast_after, len(self._early) - 1)]:
                 self._exchange_send("A", self.inv_stream)
         self._run_inverse(side, s, exchange=False)
+        if self._peer_bcast:
+            self._exchange_send(side, s)
         self._tl(f"{side.lower()}_inverse_done", s)
         self._g_inverted[side] = True
 
@@ -882,6 +910,12 @@ class SPDKFAC(torch.optim.Optimizer):
                                                        L.ptr_array([self.inv[t].data_ptr() for t in ct]),
                                                        L.ptr_array([v.data_ptr() for v in views]),
                                                        src.cuda_stream), "pack inverses")
+        if self._peer_bcast:  # push into every peer's receive region, then raise this rank's flag
+            if ct:
+                self._peer.push_extra_all(self._bc_off[side][self.rank], buf[:n], src)
+            self._peer.signal(self._peer_slot_bc[side], src)
+            self._sent[side] = True
+            return
         cs = self.comm_stream
         cs.wait_stream(src)
         with self.comm.group():
@@ -893,6 +927,8 @@ class SPDKFAC(torch.optim.Optimizer):
     def _exchange_recv(self, side, main) -> None:
         """Unpack the inverses received from the other owners (after main joined the comm stream):
         one pass per preconditioner group writes the full inverses and their operand planes."""
+        if self._peer_bcast:  # every owner's pushes of this side have landed
+            self._peer.wait(self._peer_slot_bc[side], main)
         for root, (ct_r, dims_r, _, views_r, n_r) in enumerate(self._bcast[side]):
             if root == self.rank or not ct_r:
                 continue

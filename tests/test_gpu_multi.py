@@ -42,10 +42,10 @@ def test_four_rank_step_matches_centralized():
     assert r["bucketed"] and r["bucket_err"] <= 1e-5, r
 
 
-def _run_peer(world):
+def _run_peer(world, bcast="0"):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
-    env = dict(os.environ, SPDKFAC_PEER_TIMEOUT_S="3")  # a missed signal fails the step instead of stalling it
+    env = dict(os.environ, SPDKFAC_PEER_TIMEOUT_S="3", SPDKFAC_PEER_BCAST=bcast)  # a missed signal fails the step instead of stalling it
     try:
         out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
                               "--master-addr=127.0.0.1", "--master-port=29519",
@@ -58,11 +58,12 @@ def _run_peer(world):
     return json.loads(lines[-1])["ranks"]
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_peer_factor_aggregation_matches_nccl_reduce(world):
+@pytest.mark.parametrize("world,bcast", [(2, "0"), (2, "1"), (4, "0"), (4, "1")])
+def test_peer_factor_aggregation_matches_nccl_reduce(world, bcast):
     """factor_comm='peer' (group SYRK -> copy-engine push into the owner's inbox over NVLink, flag wait,
-    owner-side sum) reproduces the NCCL reduce onto the owner: eager steps and CUDA-graph replays."""
-    ranks = _run_peer(world)
+    owner-side sum) reproduces the NCCL reduce onto the owner: eager steps and CUDA-graph replays.
+    bcast "1": the owners' CT inverses pushed into every peer's receive region too (SPDKFAC_PEER_BCAST)."""
+    ranks = _run_peer(world, bcast)
     for r in ranks:
         assert r["active"], r  # the peer path ran (grouped SYRK launches with peer targets)
         assert r["owned"] > 0, r
