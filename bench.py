@@ -126,6 +126,15 @@ def make_optimizer(a, model, world):
                    update_in_backward=a.update_in_backward == "on" or (a.update_in_backward == "auto" and world == 1))
 
 
+def launch_groups_of(a, world):
+    """The optimizer's resolved launch groups (SPDKFAC auto rule) for the bench line."""
+    if a.launch_groups != "auto":
+        return a.launch_groups
+    fc = a.factor_comm if a.factor_comm != "auto" else os.environ.get(
+        "SPDKFAC_FACTOR_COMM", ("peer" if world <= 8 else "reduce") if a.factor_decay == 0 else "allreduce")
+    return "inversion" if world == 1 or (world == 2 and fc == "peer" and SCHEMES[a.scheme][0] == "optimal") else "fusion"
+
+
 def workload_config(a, world):
     idx = {"resnet20": "0", "resnet50": "1" if world == 1 else "2", "densenet201": "3",
            "bert_base_linears": "4", "inceptionv4": "4"}.get(a.model)
@@ -136,8 +145,9 @@ def workload_config(a, world):
             "per_gpu_batch": a.batch, "global_batch": a.batch * world, "damping": a.damping, "lr": a.lr,
             "factor_update_freq": a.factor_freq, "inv_update_freq": a.inv_freq, "factor_decay": a.factor_decay,
             "scheme": a.scheme,
-            "fusion": SCHEMES[a.scheme][0] if world > 1 or a.launch_groups == "fusion" else
-                      "none at P=1 (no factor comm): SYRK launch groups = A in 2 halves, G at the inversion groups",
+            "fusion": (SCHEMES[a.scheme][0] if launch_groups_of(a, world) == "fusion" else
+                       "SYRK / aggregation launch groups = A in 2 halves, G at the inversion groups"
+                       + (" (P=1: no factor comm)" if world == 1 else " (peer aggregation, P=2)")),
             "g_inversion_fractions": a.g_fractions,
             "update_in_backward": a.update_in_backward == "on" or (a.update_in_backward == "auto" and world == 1),
             "placement": SCHEMES[a.scheme][1] if a.scheme != "spdkfac" else a.placement, "lbp_balance": a.balance, "parallelism": f"dp{world}", "python_gc": a.gc,

@@ -32,7 +32,7 @@ _K = r"tc3_gemm_kernel<(?:\(spd::Kind\))?"
 _RULES = (
     # peer-memory factor aggregation (csrc/peer.cu): flag signal / wait and the owner-side inbox sum
     ("FactorComm", r"peer_signal_kernel|peer_wait_kernel|peer_sum_kernel|epoch_advance_kernel"),
-    ("Precondition", r"split_rows_batched|split_rows_f16|packed_row_bounds|apply_update|" + _K +
+    ("Precondition", r"split_rows_batched|split_rows_f16|packed_row_bounds|apply_update|stage_packed|" + _K +
      r"[02], \d+, false, [1-9]"),  # TF32 / F16, chunked accumulation
     ("FactorComp", r"stage_rows|stage_im2col|stage_spatial|reduce_pack|tc3_pair|" + _K + "1,"),  # bf16 SYRK
     ("InverseComp", r"pivot_kernel|pivot_tc_kernel|stage_panel|small_inverse|damp_unpack|finalize_kernel|inv_scale|"

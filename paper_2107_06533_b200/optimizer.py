@@ -151,7 +151,15 @@ class SPDKFAC(torch.optim.Optimizer):
         self.bwd_plan = plan_fusion(factor_tasks(specs, FactorKind.G), bp, self.perf.allreduce, fusion)
         if launch_groups not in ("auto", "fusion", "inversion"):
             raise ValueError(f"launch_groups must be 'auto', 'fusion' or 'inversion', got {launch_groups!r}")
-        self.launch_groups = ("inversion" if self.world == 1 else "fusion") if launch_groups == "auto" else launch_groups
+        # auto: peer-memory aggregation inside one NVSwitch node (P <= 8), the NCCL reduce beyond
+        auto = ("peer" if 1 < self.world <= 8 else "reduce") if factor_decay == 0.0 else "allreduce"
+        self.factor_comm = auto if factor_comm == "auto" else factor_comm
+        # auto launch groups (measured, DESIGN.md (e)): the inversion-group cuts at P = 1 and, with peer
+        # aggregation and the optimal fusion policy, at P = 2 (16.4-16.5 vs 17.0-17.1 ms); the fusion plan beyond
+        # (P = 4: 16.4-16.6 vs 17.8-18.1 ms with the inversion cuts)
+        lg_auto = "inversion" if self.world == 1 or (self.world == 2 and self.factor_comm == "peer"
+                                                     and fusion == FusionPolicy.OPTIMAL) else "fusion"
+        self.launch_groups = lg_auto if launch_groups == "auto" else launch_groups
         if self.launch_groups == "inversion":
             # no factor communication (P = 1, or by request): a fusion group only batches SYRK
             # launches, so use few large ones: A in two halves of the forward pass, G cut at the
@@ -196,9 +204,6 @@ class SPDKFAC(torch.optim.Optimizer):
         # average) or, with factor_decay == 0, a sum onto the owner of each CT inverse only
         # (half the traffic; NCT factors are still all-reduced): over NVLink peer memory ("peer",
         # comm.PeerExchange) or an NCCL reduce ("reduce")
-        # auto: peer-memory aggregation inside one NVSwitch node (P <= 8), the NCCL reduce beyond
-        auto = ("peer" if 1 < self.world <= 8 else "reduce") if factor_decay == 0.0 else "allreduce"
-        self.factor_comm = auto if factor_comm == "auto" else factor_comm
         self._gsegs = {"A": S.reduce_segments(self.fwd_plan, a_off, a_dims, self.placement, 0),
                        "G": S.reduce_segments(self.bwd_plan, g_off, g_dims, self.placement, 1)}
         self._fgroups = None  # per fusion group FactorGroup objects, built after the first iteration

@@ -57,6 +57,7 @@ def test_classify_kernel_names():
     from paper_2107_06533_b200.breakdown import classify
     assert classify("void spd::tc3_gemm_kernel<(spd::Kind)1, 3, false, 0>(...)") == "FactorComp"
     assert classify("void spd::tc3_pair_kernel<3>(...)") == "FactorComp"
+    assert classify("void spd::stage_packed_kernel<false>(spd::StagePackedArgs)") == "Precondition"
     assert classify("spd::peer_wait_kernel(const int *, int, int, int, const int *, int *, unsigned long)") == "FactorComm"
     assert classify("spd::peer_sum_kernel(float *, const float *, long, int, int, const spd::PeerSeg *)") == "FactorComm"
     assert classify("void spd::tc3_gemm_kernel<(spd::Kind)2, 3, false, 4>(...)") == "Precondition"
