@@ -80,6 +80,18 @@ def main():
         out[mode]["graph"] = torch.cat([p.detach().flatten() for p in m.parameters()])
         o.remove_hooks()
         keep.append((gs, o))  # a communicator captured into a live CUDA graph is not destroyed (ncclCommDestroy stalls)
+        # inverses every second step: two captured step types, aggregation on both, inversion on one
+        m = convnet(dev)
+        o = SPDKFAC(m, lr=0.05, damping=0.1, factor_comm=mode, perf=perf, inv_update_freq=2)
+        gs = GraphedStep(m, crit, o, [data[0][0]], [data[0][1]], warmup=3)
+        for x, y in data[1:6]:
+            gs([x], [y])
+        torch.cuda.synchronize()
+        o.check_inverses()
+        log(mode, "freq-2 replayed")
+        out[mode]["freq2"] = torch.cat([p.detach().flatten() for p in m.parameters()])
+        o.remove_hooks()
+        keep.append((gs, o))
 
     def rel(a, b):
         return float((a - b).abs().max() / (b.abs().max() + 1e-30))
@@ -88,6 +100,7 @@ def main():
     res = {"eager_err": rel(p["eager"], r["eager"]), "graph_err": rel(p["graph"], r["graph"]),
            "eager_exact": bool(torch.equal(p["eager"], r["eager"])),
            "graph_exact": bool(torch.equal(p["graph"], r["graph"])),
+           "freq2_err": rel(p["freq2"], r["freq2"]), "freq2_exact": bool(torch.equal(p["freq2"], r["freq2"])),
            "factor_err": max([rel(p["factors"][t], r["factors"][t]) for t in r["factors"]] or [0.0]),
            "owned": len(r["factors"]), "active": p["active"] and not r["active"], "nct": p["nct"], "world": world}
     allres = [None] * world
