@@ -532,9 +532,11 @@ int spdkfac_precond_plan_run(spdkfac_precond_plan* p, const float* const* g_inv,
     f1 += 2.0 * p->d_out[l] * p->d_in[l] * p->d_in[l];
     f2 += 2.0 * p->d_out[l] * p->d_out[l] * p->d_in[l];
   }
+  // persistent-grid cap (SPDKFAC_PRECOND_CTAS): SMs left to a concurrent latency-bound inversion chain
+  static const int prec_ctas = getenv("SPDKFAC_PRECOND_CTAS") ? atoi(getenv("SPDKFAC_PRECOND_CTAS")) : 0;
   TcRun run1{};
   run1.probe = stat_begin(kCatPrecGemm, s);
-  if ((rc = launch_tc3_acc(p->maps, p->items1, p->epis, p->n1, s, run1, kind))) return rc;
+  if ((rc = launch_tc3_acc(p->maps, p->items1, p->epis, p->n1, s, run1, kind, prec_ctas))) return rc;
   stat_end(kCatPrecGemm, s, f1, 0);
   // weight update fused into GEMM2's epilogue (W += (-alpha) P, no P round trip) once the weight
   // pointers are bound: bound on the first run outside stream capture (weights do not move)
@@ -557,7 +559,7 @@ int spdkfac_precond_plan_run(spdkfac_precond_plan* p, const float* const* g_inv,
   }
   Probe* pr2 = stat_begin(kCatPrecGemm, s);
   if ((rc = launch_tc3_acc(p->maps, fused ? p->items2u : p->items2, p->epis, p->n2, s,
-                           TcRun{nullptr, 0, -alpha, 0.f, 1.f, 0, pr2}, kind)))
+                           TcRun{nullptr, 0, -alpha, 0.f, 1.f, 0, pr2}, kind, prec_ctas)))
     return rc;
   stat_end(kCatPrecGemm, s, f2, 0);
   if (fused || (!weight && !precond_out)) return SPDKFAC_OK;

@@ -264,13 +264,13 @@ int launch_tc3_f32(const CUtensorMap* maps, const TcItem* items, const TcEpi* ep
 }
 
 int launch_tc3_acc(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,
-                   const TcRun& run, Kind kind) {
+                   const TcRun& run, Kind kind, int max_ctas) {
   if (n <= 0) return SPDKFAC_OK;
   // fp16: chunks of one 64-element K block, the same partial-sum length as tf32's two blocks of 32 (the
   // TMEM accumulation truncates ~2^-24 of the running sum per MMA: longer chunks measured 1.6e-4 vs 9e-5
   // on Inception-v4's rank-4 fc update)
-  if (kind == Kind::F16) return launch_kind<Kind::F16, kStages, false, 1>(maps, items, epis, n, s, run);
-  return launch_kind<Kind::TF32, kStages, false, kAccChunk>(maps, items, epis, n, s, run);
+  if (kind == Kind::F16) return launch_kind<Kind::F16, kStages, false, 1>(maps, items, epis, n, s, run, max_ctas);
+  return launch_kind<Kind::TF32, kStages, false, kAccChunk>(maps, items, epis, n, s, run, max_ctas);
 }
 
 int launch_tc3_ctile(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n, cudaStream_t s,

@@ -106,7 +106,7 @@ int launch_tc3_pair_ctile(const CUtensorMap* maps, const TcPairCItem* items, con
 // fp32 registers): the preconditioning GEMMs (see tc3_gemm_kernel's kAcc)
 constexpr int kAccChunk = 2;  // 64 K elements = 24 accumulating MMAs per TMEM chunk
 int launch_tc3_acc(const CUtensorMap* maps, const TcItem* items, const TcEpi* epis, int n_items, cudaStream_t s,
-                   const TcRun& run = TcRun{}, Kind kind = Kind::TF32);
+                   const TcRun& run = TcRun{}, Kind kind = Kind::TF32, int max_ctas = 0);
 // 2-D tensor map over a row-major fp32 matrix [rows][ld], box 128 x 128, no swizzle
 int make_ctile_map(CUtensorMap* out, const float* base, int64_t rows, int64_t cols, int64_t ld);
 
