@@ -142,7 +142,7 @@ class PeerExchange:
         self.err = torch.zeros(1, dtype=torch.int32, device=device)
         # factor pushes: "ce" (copy engine, overlapping the backward pass without SM time; measured best) or "sm"
         self.engine = os.environ.get("SPDKFAC_PEER_ENGINE", "ce")
-        self.timeout_s = float(timeout_s if timeout_s is not None else os.environ.get("SPDKFAC_PEER_TIMEOUT_S", "20"))
+        self.timeout_s = float(timeout_s if timeout_s is not None else os.environ.get("SPDKFAC_PEER_TIMEOUT_S", "60"))
 
     def remote_ptr(self, owner: int, kind: str, offset: int) -> int:
         """Address (in this process) of this rank's inbox row at `offset` elements inside `owner`'s buffer."""
