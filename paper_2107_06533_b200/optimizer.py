@@ -292,8 +292,13 @@ class SPDKFAC(torch.optim.Optimizer):
             raise ValueError("update_in_backward needs P == 1 (the gradient mean is formed in step())")
         self.update_in_backward = bool(update_in_backward)
         # without it, one plan over every layer runs in step() (fewest launches)
-        self._pc_sides = self._early + [self._tail] if self.update_in_backward else ["ALL"]
-        if self.update_in_backward:
+        # P > 1 (SPDKFAC_EARLY_PRECOND): the early groups' layers are preconditioned in step() on their streams as
+        # soon as the first gradient bucket, the A inverses and their G inverses are in, beside the tail inversion
+        # (measured no gain at N = 2 / 4: opt-in)
+        self._p_early = self.world > 1 and os.environ.get("SPDKFAC_EARLY_PRECOND", "0") == "1" and bool(self._early)
+        per_side = self.update_in_backward or self._p_early
+        self._pc_sides = self._early + [self._tail] if per_side else ["ALL"]
+        if per_side:
             self._pc_side = {t // 2: side for side in self._pc_sides for t in grp[side]}
         else:
             self._pc_side = {li: "ALL" for li in range(len(self.layers))}
@@ -324,6 +329,7 @@ class SPDKFAC(torch.optim.Optimizer):
         self._g_count = 0
         self._g_inverted = {side: False for side in self._early}
         self._sent = {side: False for side in self._sides}
+        self._recvd = set()  # sides whose received inverses are unpacked this step
         self._grad_src = {}
         self.comm_stream = torch.cuda.Stream(self.device) if self.world > 1 else None
         self._info_events = []
@@ -792,6 +798,8 @@ class SPDKFAC(torch.optim.Optimizer):
                 self._exchange_send("A", self.inv_stream)
                 for side in self._early:
                     self._exchange_send(side, self._g_streams[side])
+            if self._p_early and self._b1_sent:
+                self._early_precond(invert_now, lr)
             cs.wait_stream(main)
             params = [p for p in self.param_groups[0]["params"] if p.grad is not None]
             if self._bucket1 is None and not capturing:
@@ -831,7 +839,8 @@ class SPDKFAC(torch.optim.Optimizer):
                 self._exchange_send(self._tail, main)
                 main.wait_stream(self.comm_stream)
                 for side in self._sides:
-                    self._exchange_recv(side, main)
+                    if side not in self._recvd:
+                        self._exchange_recv(side, main)
             self._tl("inverses_joined", main)
         # precondition + update for every K-FAC layer not yet done during backward (mean gradient
         # = sum / P); P > 1: the all-reduced gradient lives in the flat buffer (same shapes and strides)
@@ -853,6 +862,7 @@ class SPDKFAC(torch.optim.Optimizer):
         self._g_count = 0
         self._g_inverted = {side: False for side in self._early}
         self._sent = {side: False for side in self._sides}
+        self._recvd = set()
         self._early_left = {side: len(g) for side, g in self._early_groups.items()}
         self._pc_done = {side: False for side in self._precond}
         self._grad_left = {side: len(self._pc_layers[side]) for side in self._precond}
@@ -866,6 +876,37 @@ class SPDKFAC(torch.optim.Optimizer):
             self.steps += 1
             self._capture = self.steps % self.factor_update_freq == 0
         return loss
+
+    def _early_precond(self, invert_now: bool, lr: float) -> None:
+        """P > 1: precondition + update the early groups' layers while the tail G group is inverted.
+        Their mean gradients are in the first bucket's all-reduce and their inverses are local (owned
+        or NCT) or in the A / early-group broadcasts, all queued on the comm stream before this point:
+        one stream unpacks the received inverses once, then each early group runs on its own stream."""
+        b1 = self._b1_ids
+        sides = [sd for sd in self._early if sd in self._precond and not self._pc_done[sd]
+                 and all(id(self.layers[li].module.weight) in b1 for li in self._pc_layers[sd])]
+        if not sides:
+            return
+        _, views = self._flat_grad_buffer(self._bucket_params)
+        self._grad_src = {id(p): v for p, v in zip(self._bucket_params, views)}
+        ev = torch.cuda.Event()
+        ev.record(self.comm_stream)  # bucket-1 all-reduce and the A / early broadcasts
+        u = self._g_streams[sides[0]]
+        u.wait_event(ev)
+        if invert_now:
+            u.wait_stream(self.inv_stream)  # this rank's A inverses (and their staged planes)
+            for sd in self._early:
+                u.wait_stream(self._g_streams[sd])  # this rank's early G inverses
+            for sd in ["A"] + self._early:
+                self._exchange_recv(sd, u)
+                self._recvd.add(sd)
+        unpacked = torch.cuda.Event()
+        unpacked.record(u)
+        for sd in sides:
+            s = self._g_streams[sd]
+            s.wait_event(unpacked)
+            self._run_precond(sd, s, lr)
+            self._pc_done[sd] = True
 
     def _flat_grad_buffer(self, params):
         """One fp32 buffer holding every gradient (views with each parameter's shape and
