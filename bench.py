@@ -537,6 +537,35 @@ def run_ours(a):
         opt.placement = None
     else:
         opt = make_optimizer(a, model, world)
+        peer = getattr(opt, "_peer", None)
+        if peer is not None and measured_peaks is not None:
+            # NVLink evidence for the peer-memory factor aggregation: every rank pushes one fusion-buffer-sized
+            # range into the next rank's inbox row (copy engine, all ranks at once), before any step writes
+            # or reads those rows; plus the bytes the step pushes (CT factors owned by another rank)
+            import torch.distributed as dist
+            src = opt.bufA
+            dst = peer.remote_ptr((rank + 1) % world, "A", 0)
+            cs_ = torch.cuda.Stream()
+            best = float("inf")
+            for it in range(4):
+                dist.barrier()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(cs_)
+                _lib.check(_lib.load().spdkfac_peer_copy(dst, src.data_ptr(), src.numel() * 4, cs_.cuda_stream),
+                           "peer copy")
+                e1.record(cs_)
+                torch.cuda.synchronize()
+                t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                if it:
+                    best = min(best, float(t.item()))
+            pushed = sum(e - s_ for k in ("A", "G") for segs in opt._peer_out[k] for s_, e, _ in segs) * 4
+            measured_peaks["peer_push_gbs_per_gpu"] = round(src.numel() * 4 / (best * 1e-3) / 1e9, 1)
+            measured_peaks["peer_push_test_bytes"] = src.numel() * 4
+            measured_peaks["peer_push_bytes_per_step_per_gpu"] = pushed
+            measured_peaks["peer_push_how"] = ("cudaMemcpyAsync into the next rank's CUDA-IPC inbox (copy engine), all "
+                                               "ranks concurrently, max over ranks, best of 3")
     crit = nn.CrossEntropyLoss()
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)
