@@ -80,6 +80,22 @@ class NcclComm:
         self.close()
 
 
+def peer_layout(world: int, sizes: dict, n_slots: int, extra: int = 0) -> tuple:
+    """Byte layout of one rank's peer allocation (identical on every rank): (offsets, strides, total).
+    offsets["A"/"G"]: inbox [world][stride] fp32 after the flags [n_slots][world] int32; offsets["X"]: the
+    `extra` fp32 receive region.  Regions start 256-byte aligned and the inbox row stride is a multiple of
+    64 elements, so element s of any row shares the address mod 16 of element s of a 256-aligned buffer."""
+    up = lambda x: (x + 255) // 256 * 256  # noqa: E731
+    stride = {k: (int(v) + 63) // 64 * 64 for k, v in sizes.items()}
+    off, pos = {}, up(max(1, n_slots * world) * 4)
+    for kind in ("A", "G"):
+        off[kind] = pos
+        pos = up(pos + world * stride[kind] * 4)
+    off["X"] = pos
+    pos = up(pos + max(1, int(extra)) * 4)
+    return off, stride, pos
+
+
 class _DeviceArray:
     """fp32 device memory not owned by torch (the peer allocation), seen through __cuda_array_interface__."""
 
@@ -111,16 +127,10 @@ class PeerExchange:
         lib = L.load(require_device=True)
         if world > 8:
             raise ValueError("peer-memory aggregation spans one NVSwitch node (world <= 8)")
-        up = lambda x: (x + 255) // 256 * 256  # noqa: E731
         self.sizes, self.rank, self.world, self.n_slots = dict(sizes), rank, world, n_slots
-        # inbox row stride: a multiple of 64 elements, so row q at offset s shares the fusion buffer's alignment
-        self.stride = {k: (int(v) + 63) // 64 * 64 for k, v in sizes.items()}
-        self._off, off = {}, up(max(1, n_slots * world) * 4)
-        for kind in ("A", "G"):
-            self._off[kind] = off
-            off = up(off + world * self.stride[kind] * 4)
-        self._off["X"] = off  # `extra` fp32 elements: the inverse receive regions (same layout on every rank)
-        off = up(off + max(1, int(extra)) * 4)
+        # inbox row stride: a multiple of 64 elements, so row q at offset s shares the fusion buffer's alignment;
+        # `extra` fp32 elements after the inboxes: the inverse receive regions (same layout on every rank)
+        self._off, self.stride, off = peer_layout(world, sizes, n_slots, extra)
         own = C.c_void_p()
         L.check(lib.spdkfac_peer_alloc(off, C.byref(own)), "peer alloc")
         h = (C.c_char * 64)()
